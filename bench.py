@@ -1,0 +1,397 @@
+"""Benchmark: dirty-image throughput of the B200 w-stacking hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one pass of the hot path over one batch of synthetic input:
+prepare -> bucket -> grid -> per-plane inverse FFT -> w correction + stack ->
+dirty image (pipeline.py:95-152). At N=1 the workload is BASELINE config 2
+(10M records, 2048x2048x32, Gaussian support 7, FP64, 1 GPU). Inputs
+(360 MB) and grid (2 GiB) are larger than L2, so no explicit flush is needed.
+
+value  : records imaged per second over the whole step (Mvis/s), inputs
+         resident in HBM, CUDA events on the launching stream, max over ranks.
+e2e    : the same through the public host-buffer API (wsb_image): pinned host
+         arrays in, host image out, copies inside the timed region.
+roofline: algorithmic bytes / measured time of the dominant kernel against
+         the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+cpu_baseline / --impl reference: the CPU oracle (a NumPy restatement of the
+         reference algorithm, oracle/) timed on this host on a bounded sample
+         and scaled to the full workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CFG2 = dict(n_vis=10_000_000, n_u=2048, n_v=2048, n_w=32, cell=2e-4, w_max=1000.0,
+            kind="gaussian", S=3, shape=1.0, seed=1)
+SOURCES = ((0.02, -0.015, 2.0), (0.0, 0.0, 1.0), (-0.05, 0.03, 0.5))
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def synthetic(cfg, n=None, seed=None):
+    """generate_synthetic (visdata.py:384-434) restated: PCG64 uniform uvw,
+    exact point-source visibilities, unit weights, time-sorted."""
+    n = cfg["n_vis"] if n is None else n
+    rng = np.random.default_rng(cfg["seed"] if seed is None else seed)
+    u = rng.random(n)
+    v = rng.random(n)
+    w = rng.random(n)
+    t = (np.arange(n, dtype=np.uint64) * 8 // max(n, 1)).astype(np.uint32)
+    cell = cfg["cell"]
+    un, vn, wn = u / cell, v / cell, w * cfg["w_max"]
+    val = np.zeros(n, np.complex128)
+    for l, m, f in SOURCES:
+        nn = np.sqrt(1.0 - l * l - m * m)
+        val += (f / nn) * np.exp(-2j * np.pi * (un * l + vn * m + wn * (nn - 1.0)))
+    vis = val.astype(np.complex64)[:, None]
+    wt = np.ones((n, 1), np.float32)
+    return u, v, w, t, vis, wt
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def kernel_table(cfg, ms):
+    """Algorithmic bytes per launch group against the
+    measured per-kernel times ms = [prepare, bucket, grid, fft_rows, fft_cols, finish]."""
+    N = cfg["n_vis"]
+    cells = cfg["n_u"] * cfg["n_v"] * cfg["n_w"]
+    pix = cfg["n_u"] * cfg["n_v"]
+    groups = {
+        # K1+K2: vis read once (36 B) + grid written once (16 B/cell)
+        "gridder(K1+K2)": (N * 36 + cells * 16, ms[0] + ms[1] + ms[2]),
+        "grid(K2)": (cells * 16, ms[2]),
+        "fft_rows(K3a)": (cells * 32, ms[3]),
+        # column FFT + w correction + stacking: planes read once, image written once
+        "fft_cols_stack(K3b+K4)": (cells * 16 + pix * 8, ms[4]),
+    }
+    return groups
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_00959_b200 as W
+    from paper_2504_00959_b200 import distributed as WD
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    cfg = dict(CFG2)
+    spec = W.GridSpec(cfg["n_u"], cfg["n_v"], cfg["n_w"], cfg["cell"], w_max_native=cfg["w_max"])
+    kern = W.KernelSpec(cfg["kind"], cfg["S"], cfg["shape"])
+
+    # weak scaling: every rank holds its own 10M-record time partition
+    t0 = time.perf_counter()
+    u, v, w, t, vis, wt = synthetic(cfg, seed=cfg["seed"] + rank)
+    log(f"[rank {rank}] synthetic {cfg['n_vis']} records in {time.perf_counter() - t0:.1f}s")
+    du, dv, dw = (torch.from_numpy(a).to(dev) for a in (u, v, w))
+    dvis = torch.from_numpy(vis).to(dev)
+    dwt = torch.from_numpy(wt).to(dev)
+    img = torch.empty((cfg["n_v"], cfg["n_u"]), dtype=torch.float64, device=dev)
+
+    def step():
+        if ws > 1:
+            return WD.image_distributed(du, dv, dw, dvis, dwt, spec, kern)
+        return W.image_device(du, dv, dw, dvis, dwt, spec, kern, image_out=img)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    per_kernel = np.zeros(6)
+    launches = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+            ms, nl = W.last_timings(dev)
+            per_kernel += np.array(ms)
+            launches += nl
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    if ws > 1:
+        tt = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(tt.item())
+    ms_step = elapsed_ms / args.steps
+    total_vis = cfg["n_vis"] * ws
+    value = total_vis / (ms_step / 1e3) / 1e6
+
+    # end-to-end through the host-buffer C ABI (pinned inputs, host image out)
+    e2e = None
+    if ws == 1:
+        pin = [torch.from_numpy(a).pin_memory() for a in (u, v, w, vis, wt)]
+        pu, pv, pw, pvis, pwt = (p.numpy() for p in pin)
+        W.image(pu, pv, pw, None, pvis, pwt, spec, kern, device=dev.index)
+        torch.cuda.synchronize()
+        n_e2e = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            res, _ = W.image(pu, pv, pw, None, pvis, pwt, spec, kern, device=dev.index)
+        e2e_s = (time.perf_counter() - t0) / n_e2e
+        h2d = sum(a.nbytes for a in (u, v, w, vis, wt))
+        e2e = {"value": round(cfg["n_vis"] / e2e_s / 1e6, 2), "unit": "Mvis/s",
+               "ms_per_step": round(e2e_s * 1e3, 3), "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(res.pixels.nbytes),
+               "api": "paper_2504_00959_b200.image -> wsb_image (include/wsb.h)"}
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    per_kernel /= args.steps
+    peak, peak_kind = measured_peaks()
+    groups = kernel_table(cfg, per_kernel)
+    kernels = {}
+    for name, (bytes_, t_ms) in groups.items():
+        ach = bytes_ / (t_ms / 1e3) / 1e9 if t_ms > 0 else 0.0
+        kernels[name] = {"ms": round(t_ms, 4), "algorithmic_bytes": int(bytes_),
+                         "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 3)}
+    dom = max(("grid(K2)", "fft_rows(K3a)", "fft_cols_stack(K3b+K4)"),
+              key=lambda k: kernels[k]["ms"])
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(dom)
+    roof = {"kernel": dom, "bound": "hbm", "achieved": kernels[dom]["achieved_gbs"],
+            "peak": peak, "peak_source": peak_kind, "unit": "GB/s", "frac": kernels[dom]["frac"],
+            "traffic": traffic,
+            "bytes_per_launch": kernels[dom]["algorithmic_bytes"],
+            "note": "achieved = algorithmic bytes / CUDA-event time of the kernel on its stream"}
+    gridder = kernels["gridder(K1+K2)"]
+    out = {
+        "metric": "Mvis/s imaged (bucket+grid+FFT+w-stack, dirty image out)",
+        "value": round(value, 2), "unit": "Mvis/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: synthetic 10M visibilities per GPU, 2048x2048 grid, "
+                               "32 w-planes, Gaussian support 7 (S=3, sigma=1), single channel, FP64",
+                   "records_per_gpu": cfg["n_vis"], "n_u": cfg["n_u"], "n_v": cfg["n_v"],
+                   "n_w": cfg["n_w"], "cell_size_lm": cfg["cell"], "w_max_native": cfg["w_max"],
+                   "parallelism": f"v-slab x{ws}" if ws > 1 else "single GPU",
+                   "l2": "inputs 360 MB and grid 2 GiB exceed the 126 MB L2; no flush"},
+        "gridding_mvis_s": round(cfg["n_vis"] / (gridder["ms"] / 1e3) / 1e6, 1) if gridder["ms"] else None,
+        "roofline": roof,
+        "kernels": kernels,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg)
+    if ws > 1:
+        dist.destroy_process_group()
+    print(json.dumps(out), flush=True)
+
+
+def oracle_step(cfg, n_sample, n_planes, threads):
+    """CPU oracle on a bounded sample: gridding of n_sample records (full
+    grid geometry) and FFT + w-correction + stacking of n_planes planes;
+    both scaled to the full workload. Returns (seconds_full, detail)."""
+    from oracle import wstack_oracle as O
+    u, v, w, t, vis, wt = synthetic(cfg, n=n_sample, seed=cfg["seed"] + 1000)
+    kind = O.KIND_GAUSSIAN if cfg["kind"] == "gaussian" else O.KIND_KAISER_BESSEL
+    t0 = time.perf_counter()
+    prep = O.prepare(u, v, w, t, vis, wt, cfg["n_u"], cfg["n_v"], cfg["n_w"])
+    batch = O.exchange([prep], cfg["n_v"], 1, cfg["S"])[0]
+    import concurrent.futures as cf
+    blocks = [O.partition_1d(cfg["n_v"], threads, i) for i in range(threads)]
+
+    def work(blk):
+        b0, bc = blk
+        return O.grid_slab(batch, cfg["n_u"], cfg["n_w"], kind, cfg["S"], cfg["shape"], b0, b0 + bc)
+
+    with cf.ThreadPoolExecutor(threads) as ex:
+        grids = list(ex.map(work, blocks))
+    t_grid = time.perf_counter() - t0
+    grid = grids[0][0]
+    for g, _ in grids[1:]:
+        grid += g
+    t0 = time.perf_counter()
+    sign = O.checker_sign(cfg["n_u"], 0, cfg["n_v"])
+    planes = []
+    for k in range(n_planes):
+        p = O.ifft2(grid[k] * sign)
+        planes.append(O.w_correct(p, k, cfg["n_u"], cfg["n_v"], cfg["n_w"], cfg["cell"], 0.0,
+                                  cfg["w_max"], 0, cfg["n_v"]))
+    O.stack(planes, cfg["n_u"], cfg["n_v"], n_planes, cfg["cell"], 0, cfg["n_v"])
+    t_fft = time.perf_counter() - t0
+    full = t_grid * cfg["n_vis"] / n_sample + t_fft * cfg["n_w"] / n_planes
+    return full, {"grid_s": t_grid, "fft_wstack_s": t_fft}
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg, n_sample=500_000, n_planes=4):
+    threads = cpu_cores()
+    full_s, det = oracle_step(cfg, n_sample, n_planes, threads)
+    return {"value": round(cfg["n_vis"] / full_s / 1e6, 4), "unit": "Mvis/s", "cores": threads,
+            "kind": "port",
+            "sample": (f"oracle (NumPy restatement of the reference) on {n_sample} of "
+                       f"{cfg['n_vis']} records gridded on the full 2048x2048x32 mesh "
+                       f"({det['grid_s']:.2f}s, {threads} row-block threads) + FFT/w-stack of "
+                       f"{n_planes} of {cfg['n_w']} planes ({det['fft_wstack_s']:.2f}s); "
+                       f"scaled to the full workload: {full_s:.1f}s per image"),
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = dict(CFG2)
+    threads = cpu_cores()
+    for _ in range(args.warmup):
+        oracle_step(cfg, 100_000, 1, threads)
+    times = []
+    for _ in range(args.steps):
+        full, det = oracle_step(cfg, 100_000, 1, threads)
+        times.append(full)
+    s = float(np.mean(times))
+    value = cfg["n_vis"] / s / 1e6
+    out = {"impl": "reference", "metric": "Mvis/s imaged (bucket+grid+FFT+w-stack, dirty image out)",
+           "value": round(value, 4), "unit": "Mvis/s", "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(s * 1e3, 1), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "cfg2: synthetic 10M visibilities, 2048x2048 grid, 32 w-planes, "
+                                  "Gaussian support 7, single channel, FP64"},
+           "cpu_baseline": {"value": round(value, 4), "unit": "Mvis/s", "cores": threads,
+                            "kind": "port",
+                            "sample": "per step: 100000 records gridded on the full mesh + 1 of 32 "
+                                      "planes transformed/stacked, scaled to the full workload",
+                            "cpu": _cpu_model()},
+           "e2e": {"value": round(value, 4), "unit": "Mvis/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        log("note: warmup < 3 does not meet the timing rules")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

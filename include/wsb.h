@@ -1,0 +1,188 @@
+/*
+ * wsb.h — C ABI of the B200 w-stacking imager (libwsb.so, sm_100a).
+ *
+ * The reference (`wstack`, pure Python/NumPy) has no FFI; its drop-in
+ * boundary is the Python call `pipeline.run_pipeline` phases 2-5
+ * (/root/reference/pkg/src/wstack/pipeline.py:95-152) plus the finer hooks
+ * `gridder.grid_sector` (gridder.py:186-259) and `gridder.grid_all`
+ * (gridder.py:262-294). Each entry point below names the reference function
+ * it replaces. The Python host package `paper_2504_00959_b200` binds this
+ * ABI with ctypes and mirrors the reference API on top.
+ *
+ * Conventions
+ *   - Plain C types only. Inputs are caller-owned and read-only; nothing is
+ *     retained after a call returns. Device pointers are CUDA global-memory
+ *     pointers on the context's device; host pointers are ordinary memory
+ *     (pinned memory is faster but not required).
+ *   - Every function returns 0 or a negative WSB_E* code. The Python layer
+ *     maps WSB_EINVAL -> ValueError (mesh.py:79-95, gridder.py:56-62,
+ *     visdata.py:178-184), WSB_ECUDA/WSB_ENCCL -> RuntimeError,
+ *     WSB_ENOMEM -> MemoryError, WSB_EUNSUPPORTED -> NotImplementedError.
+ *     wsb_last_error() returns a thread-local detail string.
+ *   - Stage functions enqueue on the context's stream and return without
+ *     synchronising unless they must read a device value back
+ *     (validation flags, counts); they say so.
+ *   - No CPU fallback: every compute entry point runs CUDA kernels.
+ */
+#ifndef WSB_H
+#define WSB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WSB_VERSION 100
+
+#define WSB_OK            0
+#define WSB_EINVAL       -1
+#define WSB_ECUDA        -2
+#define WSB_ENCCL        -3
+#define WSB_ENOMEM       -4
+#define WSB_EUNSUPPORTED -5
+
+#define WSB_KERNEL_GAUSSIAN       0
+#define WSB_KERNEL_KAISER_BESSEL  1
+
+/* Column-group width of the internal "P layout" grid:
+ *   P[plane][col / WSB_P_GROUP][row][col % WSB_P_GROUP]  (complex128)
+ * The sign (-1)^(i+j) of transform.py:180-185 is already applied. */
+#define WSB_P_GROUP 2
+
+/* Largest transform length handled on chip in this build. */
+#define WSB_MAX_FFT_N 4096
+
+/* GridSpec (mesh.py:59-112). w_min/w_max normalised are fixed to [0, 1]. */
+typedef struct {
+    int32_t n_u, n_v, n_w, reserved;
+    double cell_size_lm, w_min_native, w_max_native;
+} wsb_grid;
+
+/* KernelSpec (gridder.py:47-72). shape_param = Gaussian sigma or KB beta. */
+typedef struct {
+    int32_t kind, half_support;
+    double shape_param;
+} wsb_kernel;
+
+typedef struct {
+    int32_t device;        /* CUDA ordinal */
+    int32_t precision;     /* 64 (FP64 path); 32 reserved */
+    int32_t deterministic; /* accepted for API parity; results are always deterministic */
+    int32_t reserved;
+} wsb_exec;
+
+/* Diagnostics: FinalImage norms (transform.py:72-83, 233-241) and the ops /
+ * phase-time surrogates of run_pipeline (pipeline.py:178-186). */
+typedef struct {
+    double imag_residual_norm, real_norm;
+    int64_t grid_updates;     /* == ops["grid_updates"] */
+    int64_t records;          /* == ops["records"] */
+    int64_t tile_entries;     /* (record, 64x64 tile) pairs bucketed */
+    double phase_ms[7];       /* read, gridding, reduce, fft, wcorrect, write, total (exclusive) */
+} wsb_diag;
+
+typedef struct wsb_ctx wsb_ctx;
+
+const char *wsb_strerror(int code);
+const char *wsb_last_error(void);
+int wsb_version(void);
+
+int wsb_ctx_create(int32_t device, wsb_ctx **out);
+int wsb_ctx_destroy(wsb_ctx *ctx);
+/* Use `stream` (a cudaStream_t; NULL = legacy default) for later calls. */
+int wsb_ctx_set_stream(wsb_ctx *ctx, void *stream);
+/* Release cached device workspace. */
+int wsb_ctx_trim(wsb_ctx *ctx);
+
+/* ---- whole hot path ---------------------------------------------------- */
+
+/* Replaces run_pipeline phases 2-5 (pipeline.py:95-152) for one GPU, HOST
+ * buffers in and out: uvw f64[n], time_index u32[n] (nullable; records are
+ * processed in array order, the (time_index, gindex) order the reference's
+ * exchange produces for time-sorted input), vis = interleaved (re, im) f32
+ * [n][n_chan][2], weight f32[n][n_chan]; image_out f64[n_v][n_u].
+ * Copies in and out are part of the call. Synchronous. */
+int wsb_image(const wsb_grid *grid, const wsb_kernel *kern, const wsb_exec *exec,
+              const double *u, const double *v, const double *w,
+              const uint32_t *time_index, const float *vis, const float *weight,
+              int64_t n, int32_t n_chan, double *image_out, wsb_diag *diag);
+
+/* Same on DEVICE buffers, enqueued on the context stream. image_out is a
+ * device f64[n_v][n_u]. Synchronises once (validation flag) and at the end
+ * (diagnostics) when diag != NULL. */
+int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
+                     const double *u, const double *v, const double *w,
+                     const float *vis, const float *weight, int64_t n, int32_t n_chan,
+                     double *image_out, wsb_diag *diag);
+
+/* ---- stages (device pointers; used by the multi-GPU host driver) ------- */
+
+/* prepare_chunk (comms.py:477-492) + VisChunk.validate (visdata.py:178-184):
+ * rec[i] = {gu, gv, Re value, Im value} f64x4, plane[i] u32.
+ * Synchronises to read the validation flag; WSB_EINVAL on bad input. */
+int wsb_prepare(wsb_ctx *ctx, const wsb_grid *grid,
+                const double *u, const double *v, const double *w,
+                const float *vis, const float *weight, int64_t n, int32_t n_chan,
+                double *rec, uint32_t *plane);
+
+/* Destination slabs of the time->space exchange (comms.py:516-523): counts
+ * of records per destination slab of partition_1d(n_v, n_ranks) with the
+ * +-half_support halo predicate. counts_host: int64[n_ranks]. Synchronous. */
+int wsb_route_count(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int32_t n_ranks,
+                    const double *rec, int64_t n, int64_t *counts_host);
+
+/* Pack the exchange send buffers: records for slab d land at
+ * [displ_d, displ_d + count_d) in array (gindex) order; optional src_index
+ * receives the local index of each packed record (nullable). */
+int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int32_t n_ranks,
+                   const double *rec, const uint32_t *plane, int64_t n,
+                   double *send_rec, uint32_t *send_plane, int64_t *src_index);
+
+/* grid_sector (gridder.py:186-259) for the slab rows [v_start, v_start+v_count):
+ * buckets the m records into (plane, 64x64 tile) lists (stable counting sort),
+ * grids them with the convolution kernel and writes the slab in P layout
+ * (grid_p: complex128[n_w][n_u/G][v_count][G], sign applied). grid_updates
+ * (host, nullable) receives the number of cell updates; synchronises if given. */
+int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
+                  int32_t v_start, int32_t v_count,
+                  const double *rec, const uint32_t *plane, int64_t m,
+                  double *grid_p, int64_t *grid_updates);
+
+/* Row pass of the inverse 2D FFT (transform.py:151 / fft1d inverse) on planes
+ * [plane_lo, plane_hi) of a P-layout slab, in place. Unnormalised. */
+int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count,
+                 double *grid_p, int32_t plane_lo, int32_t plane_hi);
+
+/* Column pass + w correction + stacking (transform.py:162-175, 192-230):
+ * input tgrid holds, per plane, this rank's column groups [g0, g0+ng) for all
+ * n_v rows, concatenated by source slab s (rows src_rows[s]) as
+ *   [plane][s][g - g0][row - row_start_s][G]   (the all-to-all output).
+ * Writes image_strip f64[n_v][ng*G] (row-major) and norm_partials
+ * f64[ng][2] = (sum Im^2, sum Re^2) per group; the caller sums partials in
+ * group order. */
+int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
+                       const int32_t *src_rows_host, int32_t g0, int32_t ng,
+                       const double *tgrid, double *image_strip, double *norm_partials);
+
+/* Debug / parity: P-layout slab -> natural (plane, row, col) complex128 with
+ * the checkerboard sign removed (the grid_all output layout, mesh.py:131-146). */
+int wsb_grid_unpack(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t v_count,
+                    const double *grid_p, double *grid_out);
+
+/* Debug / parity: the (tile key, record index) pairs of the last
+ * wsb_grid_slab call in sorted order, and the tile offsets.
+ * Sizes via wsb_tiles_debug(ctx, NULL, NULL, NULL, &n_entries, &n_tiles). */
+int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *keys_host, uint32_t *idx_host,
+                    uint32_t *tile_off_host, int64_t *n_entries, int64_t *n_tiles);
+
+/* Timing of the kernels launched by the last wsb_image_device call, in ms,
+ * measured with CUDA events on the context stream:
+ * [0] prepare, [1] bucket+sort, [2] grid, [3] fft rows, [4] fft cols+stack,
+ * [5] finish.  Returns the number of kernel launches in *launches. */
+int wsb_last_timings(wsb_ctx *ctx, double *ms6, int32_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WSB_H */

@@ -1,0 +1,455 @@
+// C ABI of libwsb.so (include/wsb.h): contexts, workspace, validation and
+// the whole-hot-path entry points that replace run_pipeline phases 2-5
+// (pipeline.py:95-152).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "wsb_internal.cuh"
+
+namespace wsb {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int ensure(wsb_ctx *ctx, int slot, size_t bytes, void **out) {
+    if ((int)ctx->bufs.size() <= slot) ctx->bufs.resize(kSlotCount > slot + 1 ? kSlotCount : slot + 1);
+    Buf &b = ctx->bufs[slot];
+    if (b.bytes < bytes) {
+        if (b.ptr) {
+            // a pending kernel may still read the old buffer
+            WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            WSB_CUDA_TRY(cudaFree(b.ptr));
+            b.ptr = nullptr;
+            b.bytes = 0;
+        }
+        size_t want = std::max<size_t>(bytes, 256);
+        cudaError_t e = cudaMalloc(&b.ptr, want);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(WSB_ENOMEM, "device allocation of " + std::to_string(want) + " bytes failed");
+        }
+        b.bytes = want;
+    }
+    *out = b.ptr;
+    return WSB_OK;
+}
+
+// GridSpec (mesh.py:79-95) + KernelSpec (gridder.py:56-62) rules.
+static int validate_grid(const wsb_grid *g) {
+    if (!g) return fail(WSB_EINVAL, "grid is NULL");
+    auto pow2 = [](int n) { return n >= 1 && (n & (n - 1)) == 0; };
+    if (g->n_u < 2 || !pow2(g->n_u)) return fail(WSB_EINVAL, "n_u must be a power of two >= 2");
+    if (g->n_v < 2 || !pow2(g->n_v)) return fail(WSB_EINVAL, "n_v must be a power of two >= 2");
+    if (g->n_w < 1) return fail(WSB_EINVAL, "n_w must be >= 1");
+    if (!(g->cell_size_lm > 0.0)) return fail(WSB_EINVAL, "cell_size_lm must be positive");
+    const double hl = g->n_u * g->cell_size_lm / 2.0, hm = g->n_v * g->cell_size_lm / 2.0;
+    if (hl >= 1.0 || hm >= 1.0 || hl * hl + hm * hm >= 1.0)
+        return fail(WSB_EINVAL, "field of view too wide: corner pixels leave the unit disc");
+    if (g->w_min_native > g->w_max_native) return fail(WSB_EINVAL, "w_min_native must be <= w_max_native");
+    if (g->n_u > WSB_MAX_FFT_N || g->n_v > WSB_MAX_FFT_N)
+        return fail(WSB_EUNSUPPORTED, "grids above 4096 per axis need the out-of-core FFT (not in this build)");
+    return WSB_OK;
+}
+
+static int validate_kernel(const wsb_kernel *k) {
+    if (!k) return fail(WSB_EINVAL, "kernel is NULL");
+    if (k->kind != WSB_KERNEL_GAUSSIAN && k->kind != WSB_KERNEL_KAISER_BESSEL)
+        return fail(WSB_EINVAL, "kernel kind must be gaussian or kaiser_bessel");
+    if (k->half_support < 1) return fail(WSB_EINVAL, "half_support must be >= 1");
+    if (!(k->shape_param > 0.0)) return fail(WSB_EINVAL, "shape_param must be positive");
+    if (k->half_support > kMaxS) return fail(WSB_EUNSUPPORTED, "half_support > 7 not compiled in this build");
+    return WSB_OK;
+}
+
+static int set_device(wsb_ctx *ctx) {
+    WSB_CUDA_TRY(cudaSetDevice(ctx->device));
+    return WSB_OK;
+}
+
+// Device-side final sum of the per-column-block norm partials, in block order.
+__global__ void k_sum_partials(const double *p, int nb, double *out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double si = 0.0, sr = 0.0;
+    for (int b = 0; b < nb; ++b) {
+        si += p[2 * b];
+        sr += p[2 * b + 1];
+    }
+    out[0] = si;
+    out[1] = sr;
+}
+
+// P layout -> (plane, row, col) complex128 with the checkerboard sign removed.
+__global__ void k_unpack(const double2 *p, double2 *out, int n_w, int n_u, int v_start, int v_count) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)n_w * v_count * n_u;
+    if (e >= total) return;
+    const int i = e % n_u;
+    const int64_t t = e / n_u;
+    const int j = t % v_count;
+    const int k = t / v_count;
+    double2 z = p[(((int64_t)k * (n_u / kG) + i / kG) * v_count + j) * kG + i % kG];
+    const double s = ((i + v_start + j) & 1) ? -1.0 : 1.0;
+    out[e] = make_double2(z.x * s, z.y * s);
+}
+
+}  // namespace wsb
+
+using namespace wsb;
+
+extern "C" {
+
+const char *wsb_strerror(int code) {
+    switch (code) {
+        case WSB_OK: return "ok";
+        case WSB_EINVAL: return "invalid argument";
+        case WSB_ECUDA: return "CUDA error";
+        case WSB_ENCCL: return "NCCL error";
+        case WSB_ENOMEM: return "out of device memory";
+        case WSB_EUNSUPPORTED: return "unsupported configuration";
+        default: return "unknown error";
+    }
+}
+
+const char *wsb_last_error(void) { return g_last_error.c_str(); }
+
+int wsb_version(void) { return WSB_VERSION; }
+
+int wsb_ctx_create(int32_t device, wsb_ctx **out) {
+    if (!out) return fail(WSB_EINVAL, "out is NULL");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(WSB_ECUDA, "no CUDA device available");
+    }
+    if (device < 0 || device >= n) return fail(WSB_EINVAL, "device ordinal out of range");
+    wsb_ctx *c = new wsb_ctx();
+    c->device = device;
+    c->bufs.resize(kSlotCount);
+    int rc = set_device(c);
+    if (rc == WSB_OK) {
+        cudaError_t a = cudaMallocHost(&c->flag_host, 64);
+        if (a != cudaSuccess) rc = fail(WSB_ENOMEM, "pinned allocation failed");
+    }
+    if (rc == WSB_OK) {
+        for (int i = 0; i < 8; ++i) cudaEventCreate(&c->timing.ev[i]);
+        c->timing.created = true;
+    }
+    if (rc != WSB_OK) {
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return WSB_OK;
+}
+
+int wsb_ctx_trim(wsb_ctx *ctx) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    WSB_TRY(set_device(ctx));
+    WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    for (auto &b : ctx->bufs) {
+        if (b.ptr) cudaFree(b.ptr);
+        b.ptr = nullptr;
+        b.bytes = 0;
+    }
+    return WSB_OK;
+}
+
+int wsb_ctx_destroy(wsb_ctx *ctx) {
+    if (!ctx) return WSB_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto &b : ctx->bufs)
+        if (b.ptr) cudaFree(b.ptr);
+    for (int i = 0; i < 16; ++i)
+        if (ctx->twiddle[i]) cudaFree(ctx->twiddle[i]);
+    if (ctx->timing.created)
+        for (int i = 0; i < 8; ++i) cudaEventDestroy(ctx->timing.ev[i]);
+    if (ctx->flag_host) cudaFreeHost(ctx->flag_host);
+    delete ctx;
+    return WSB_OK;
+}
+
+int wsb_ctx_set_stream(wsb_ctx *ctx, void *stream) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    ctx->stream = (cudaStream_t)stream;
+    return WSB_OK;
+}
+
+int wsb_prepare(wsb_ctx *ctx, const wsb_grid *grid, const double *u, const double *v,
+                const double *w, const float *vis, const float *weight, int64_t n, int32_t n_chan,
+                double *rec, uint32_t *plane) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    WSB_TRY(validate_grid(grid));
+    if (n < 0 || n_chan < 1) return fail(WSB_EINVAL, "n must be >= 0 and n_chan >= 1");
+    if (n > 0xFFFFFFFFll) return fail(WSB_EUNSUPPORTED, "more than 2^32 records per GPU");
+    WSB_TRY(set_device(ctx));
+    return prepare(ctx, grid, u, v, w, vis, weight, n, n_chan, rec, plane);
+}
+
+int wsb_route_count(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int32_t n_ranks,
+                    const double *rec, int64_t n, int64_t *counts_host) {
+    if (!ctx || !counts_host) return fail(WSB_EINVAL, "NULL argument");
+    WSB_TRY(validate_grid(grid));
+    if (half_support < 0) return fail(WSB_EINVAL, "halo_rows must be >= 0");
+    WSB_TRY(set_device(ctx));
+    return wsb::route_count(ctx, grid, half_support, n_ranks, rec, n, counts_host, nullptr, nullptr);
+}
+
+int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int32_t n_ranks,
+                   const double *rec, const uint32_t *plane, int64_t n, double *send_rec,
+                   uint32_t *send_plane, int64_t *src_index) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    WSB_TRY(validate_grid(grid));
+    if (half_support < 0) return fail(WSB_EINVAL, "halo_rows must be >= 0");
+    WSB_TRY(set_device(ctx));
+    return wsb::route_pack(ctx, grid, half_support, n_ranks, rec, plane, n, send_rec, send_plane,
+                           src_index);
+}
+
+static int grid_slab_impl(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
+                          int32_t v_start, int32_t v_count, const double *rec,
+                          const uint32_t *plane, int64_t m, double *grid_p,
+                          unsigned long long *updates_dev, int64_t *n_entries_out) {
+    uint32_t *sidx, *toff;
+    int64_t n_entries, n_tiles;
+    WSB_TRY(bucket_tiles(ctx, grid, kern->half_support, v_start, v_count, rec, plane, m, &sidx,
+                         &toff, &n_entries, &n_tiles));
+    if (n_entries_out) *n_entries_out = n_entries;
+    return grid_tiles(ctx, grid, kern, v_start, v_count, rec, sidx, toff, n_tiles, grid_p,
+                      updates_dev);
+}
+
+int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern, int32_t v_start,
+                  int32_t v_count, const double *rec, const uint32_t *plane, int64_t m,
+                  double *grid_p, int64_t *grid_updates) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    WSB_TRY(validate_grid(grid));
+    WSB_TRY(validate_kernel(kern));
+    if (v_start < 0 || v_count < 1 || v_start + v_count > grid->n_v)
+        return fail(WSB_EINVAL, "slab rows outside the mesh");
+    if (m < 0 || m > 0xFFFFFFFFll) return fail(WSB_EINVAL, "record count out of range");
+    WSB_TRY(set_device(ctx));
+    unsigned long long *upd;
+    WSB_TRY(ensure(ctx, kSlotU64, 64, (void **)&upd));
+    WSB_CUDA_TRY(cudaMemsetAsync(upd, 0, sizeof(unsigned long long), ctx->stream));
+    WSB_TRY(grid_slab_impl(ctx, grid, kern, v_start, v_count, rec, plane, m, grid_p, upd, nullptr));
+    if (grid_updates) {
+        unsigned long long h;
+        WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host, upd, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        std::memcpy(&h, ctx->flag_host, sizeof(h));
+        *grid_updates = (int64_t)h;
+    }
+    return WSB_OK;
+}
+
+int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count, double *grid_p,
+                 int32_t plane_lo, int32_t plane_hi) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    WSB_TRY(validate_grid(grid));
+    if (plane_lo < 0 || plane_hi > grid->n_w || plane_lo > plane_hi)
+        return fail(WSB_EINVAL, "plane range outside [0, n_w]");
+    WSB_TRY(set_device(ctx));
+    return fft_rows(ctx, grid, v_count, grid_p, plane_lo, plane_hi);
+}
+
+int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
+                       const int32_t *src_rows_host, int32_t g0, int32_t ng, const double *tgrid,
+                       double *image_strip, double *norm_partials) {
+    if (!ctx || !src_rows_host) return fail(WSB_EINVAL, "NULL argument");
+    WSB_TRY(validate_grid(grid));
+    if (g0 < 0 || ng < 1 || (g0 + ng) * kG > grid->n_u) return fail(WSB_EINVAL, "column groups outside the mesh");
+    WSB_TRY(set_device(ctx));
+    return fft_cols_stack(ctx, grid, n_sources, src_rows_host, g0, ng, tgrid, image_strip,
+                          norm_partials);
+}
+
+int wsb_grid_unpack(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t v_count,
+                    const double *grid_p, double *grid_out) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    WSB_TRY(validate_grid(grid));
+    WSB_TRY(set_device(ctx));
+    const int64_t total = (int64_t)grid->n_w * v_count * grid->n_u;
+    if (total == 0) return WSB_OK;
+    k_unpack<<<ceil_div(total, 256), 256, 0, ctx->stream>>>((const double2 *)grid_p,
+                                                            (double2 *)grid_out, grid->n_w,
+                                                            grid->n_u, v_start, v_count);
+    WSB_CUDA_TRY(cudaGetLastError());
+    return WSB_OK;
+}
+
+int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *keys_host, uint32_t *idx_host, uint32_t *tile_off_host,
+                    int64_t *n_entries, int64_t *n_tiles) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    WSB_TRY(set_device(ctx));
+    if (n_entries) *n_entries = ctx->last_entries;
+    if (n_tiles) *n_tiles = ctx->last_tiles;
+    WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (keys_host && ctx->last_entries)
+        WSB_CUDA_TRY(cudaMemcpy(keys_host, ctx->last_keys, 4 * ctx->last_entries, cudaMemcpyDeviceToHost));
+    if (idx_host && ctx->last_entries)
+        WSB_CUDA_TRY(cudaMemcpy(idx_host, ctx->last_idx, 4 * ctx->last_entries, cudaMemcpyDeviceToHost));
+    if (tile_off_host && ctx->last_tiles)
+        WSB_CUDA_TRY(cudaMemcpy(tile_off_host, ctx->last_off, 4 * (ctx->last_tiles + 1), cudaMemcpyDeviceToHost));
+    return WSB_OK;
+}
+
+int wsb_last_timings(wsb_ctx *ctx, double *ms6, int32_t *launches) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    if (ms6)
+        for (int i = 0; i < 6; ++i) ms6[i] = ctx->last_ms[i];
+    if (launches) *launches = ctx->launches;
+    return WSB_OK;
+}
+
+int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern, const double *u,
+                     const double *v, const double *w, const float *vis, const float *weight,
+                     int64_t n, int32_t n_chan, double *image_out, wsb_diag *diag) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    WSB_TRY(validate_grid(grid));
+    WSB_TRY(validate_kernel(kern));
+    if (n < 0 || n_chan < 1) return fail(WSB_EINVAL, "n must be >= 0 and n_chan >= 1");
+    if (n > 0xFFFFFFFFll) return fail(WSB_EUNSUPPORTED, "more than 2^32 records per GPU");
+    WSB_TRY(set_device(ctx));
+    ctx->launches = 0;
+    cudaEvent_t *ev = ctx->timing.ev;
+    const int n_u = grid->n_u, n_v = grid->n_v, n_w = grid->n_w;
+    double *rec, *gp, *partials;
+    uint32_t *plane;
+    unsigned long long *upd;
+    const int64_t nn = std::max<int64_t>(n, 1);
+    WSB_TRY(ensure(ctx, kSlotRec, 32 * (size_t)nn, (void **)&rec));
+    WSB_TRY(ensure(ctx, kSlotPlane, 4 * (size_t)nn, (void **)&plane));
+    WSB_TRY(ensure(ctx, kSlotGrid, (size_t)16 * n_w * n_u * n_v, (void **)&gp));
+    WSB_TRY(ensure(ctx, kSlotStrip, sizeof(double) * (2 * (size_t)n_u + 4), (void **)&partials));
+    WSB_TRY(ensure(ctx, kSlotU64, 64, (void **)&upd));
+    const double *tw;
+    WSB_TRY(twiddles(ctx, n_u, &tw));
+    WSB_TRY(twiddles(ctx, n_v, &tw));
+
+    WSB_CUDA_TRY(cudaEventRecord(ev[0], ctx->stream));
+    WSB_CUDA_TRY(cudaMemsetAsync(upd, 0, sizeof(unsigned long long), ctx->stream));
+    WSB_TRY(prepare(ctx, grid, u, v, w, vis, weight, n, n_chan, rec, plane));
+    WSB_CUDA_TRY(cudaEventRecord(ev[1], ctx->stream));
+    uint32_t *sidx, *toff;
+    int64_t n_entries = 0, n_tiles = 0;
+    WSB_TRY(bucket_tiles(ctx, grid, kern->half_support, 0, n_v, rec, plane, n, &sidx, &toff,
+                         &n_entries, &n_tiles));
+    WSB_CUDA_TRY(cudaEventRecord(ev[2], ctx->stream));
+    WSB_TRY(grid_tiles(ctx, grid, kern, 0, n_v, rec, sidx, toff, n_tiles, gp, upd));
+    WSB_CUDA_TRY(cudaEventRecord(ev[3], ctx->stream));
+    WSB_TRY(fft_rows(ctx, grid, n_v, gp, 0, n_w));
+    WSB_CUDA_TRY(cudaEventRecord(ev[4], ctx->stream));
+    const int32_t rows[1] = {n_v};
+    WSB_TRY(fft_cols_stack(ctx, grid, 1, rows, 0, n_u / kG, gp, image_out, partials));
+    WSB_CUDA_TRY(cudaEventRecord(ev[5], ctx->stream));
+    const int nb = ceil_div(n_u, std::max(1, 4096 / n_v));
+    k_sum_partials<<<1, 32, 0, ctx->stream>>>(partials, nb, partials + 2 * (size_t)n_u);
+    ctx->launches += 1;
+    WSB_CUDA_TRY(cudaGetLastError());
+    WSB_CUDA_TRY(cudaEventRecord(ev[6], ctx->stream));
+    if (diag) {
+        double norms[2];
+        unsigned long long h;
+        WSB_CUDA_TRY(cudaMemcpyAsync(norms, partials + 2 * (size_t)n_u, sizeof(norms),
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+        WSB_CUDA_TRY(cudaMemcpyAsync(&h, upd, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        diag->imag_residual_norm = std::sqrt(norms[0]);
+        diag->real_norm = std::sqrt(norms[1]);
+        diag->grid_updates = (int64_t)h;
+        diag->records = n;
+        diag->tile_entries = n_entries;
+        float ms[6];
+        for (int i = 0; i < 6; ++i) {
+            cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
+            ctx->last_ms[i] = ms[i];
+        }
+        for (int i = 0; i < 7; ++i) diag->phase_ms[i] = 0.0;
+        diag->phase_ms[1] = ms[0] + ms[1] + ms[2];      // gridding: prepare + bucket + grid
+        diag->phase_ms[3] = ms[3] + ms[4];              // fft (column pass carries w correction)
+        diag->phase_ms[4] = ms[5];                      // wcorrect: final reduction
+        diag->phase_ms[6] = ms[0] + ms[1] + ms[2] + ms[3] + ms[4] + ms[5];
+    }
+    return WSB_OK;
+}
+
+static std::mutex g_host_mu;
+static wsb_ctx *g_host_ctx[64] = {nullptr};
+
+int wsb_image(const wsb_grid *grid, const wsb_kernel *kern, const wsb_exec *exec, const double *u,
+              const double *v, const double *w, const uint32_t *time_index, const float *vis,
+              const float *weight, int64_t n, int32_t n_chan, double *image_out, wsb_diag *diag) {
+    (void)time_index;
+    WSB_TRY(validate_grid(grid));
+    WSB_TRY(validate_kernel(kern));
+    if (n < 0 || n_chan < 1) return fail(WSB_EINVAL, "n must be >= 0 and n_chan >= 1");
+    if ((n > 0 && (!u || !v || !w || !vis || !weight)) || !image_out)
+        return fail(WSB_EINVAL, "NULL buffer");
+    const int dev = exec ? exec->device : 0;
+    if (exec && exec->precision != 64) return fail(WSB_EUNSUPPORTED, "only the FP64 path is built");
+    if (dev < 0 || dev >= 64) return fail(WSB_EINVAL, "device ordinal out of range");
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    if (!g_host_ctx[dev]) WSB_TRY(wsb_ctx_create(dev, &g_host_ctx[dev]));
+    wsb_ctx *ctx = g_host_ctx[dev];
+    WSB_TRY(set_device(ctx));
+    const int64_t nn = std::max<int64_t>(n, 1);
+    auto rnd = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t b_uvw = rnd(8 * (size_t)nn), b_vis = rnd(8 * (size_t)nn * n_chan),
+                 b_wt = rnd(4 * (size_t)nn * n_chan);
+    const size_t b_img = 8 * (size_t)grid->n_u * grid->n_v;
+    unsigned char *in;
+    WSB_TRY(ensure(ctx, kSlotHostIn, 3 * b_uvw + b_vis + b_wt + b_img, (void **)&in));
+    double *du = (double *)in, *dv = (double *)(in + b_uvw), *dw = (double *)(in + 2 * b_uvw);
+    float *dvis = (float *)(in + 3 * b_uvw), *dwt = (float *)(in + 3 * b_uvw + b_vis);
+    double *dimg = (double *)(in + 3 * b_uvw + b_vis + b_wt);
+    cudaEvent_t a0, a1, a2, a3;
+    cudaEventCreate(&a0);
+    cudaEventCreate(&a1);
+    cudaEventCreate(&a2);
+    cudaEventCreate(&a3);
+    cudaEventRecord(a0, ctx->stream);
+    if (n > 0) {
+        WSB_CUDA_TRY(cudaMemcpyAsync(du, u, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+        WSB_CUDA_TRY(cudaMemcpyAsync(dv, v, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+        WSB_CUDA_TRY(cudaMemcpyAsync(dw, w, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+        WSB_CUDA_TRY(cudaMemcpyAsync(dvis, vis, 8 * (size_t)n * n_chan, cudaMemcpyHostToDevice, ctx->stream));
+        WSB_CUDA_TRY(cudaMemcpyAsync(dwt, weight, 4 * (size_t)n * n_chan, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    cudaEventRecord(a1, ctx->stream);
+    wsb_diag local;
+    int rc = wsb_image_device(ctx, grid, kern, du, dv, dw, dvis, dwt, n, n_chan, dimg, &local);
+    if (rc == WSB_OK) {
+        cudaEventRecord(a2, ctx->stream);
+        cudaError_t e = cudaMemcpyAsync(image_out, dimg, b_img, cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaEventRecord(a3, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) rc = fail(WSB_ECUDA, std::string("copy-out: ") + cudaGetErrorString(e));
+    }
+    if (rc == WSB_OK && diag) {
+        float r, wr, tot;
+        cudaEventElapsedTime(&r, a0, a1);
+        cudaEventElapsedTime(&wr, a2, a3);
+        cudaEventElapsedTime(&tot, a0, a3);
+        *diag = local;
+        diag->phase_ms[0] = r;
+        diag->phase_ms[5] = wr;
+        diag->phase_ms[6] = tot;
+    }
+    cudaEventDestroy(a0);
+    cudaEventDestroy(a1);
+    cudaEventDestroy(a2);
+    cudaEventDestroy(a3);
+    return rc;
+}
+
+}  // extern "C"

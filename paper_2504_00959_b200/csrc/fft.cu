@@ -1,0 +1,490 @@
+// K3 + K4: per-plane inverse 2-D FFT, w correction and plane stacking.
+//
+// The reference transforms each plane with an iterative radix-2 loop
+// (transform.py:99-127), distributed as row FFT -> block transpose -> row
+// FFT -> transpose back (transform.py:130-177), then applies the w phase
+// screen (transform.py:192-202) and stacks the planes (transform.py:205-230).
+//
+// Here a plane makes two passes over HBM:
+//   k_fft_rows  : CTA = 8192/N rows of one plane, loaded from the P layout in
+//                 128-byte runs, radix-16 Stockham autosort in shared memory
+//                 (FP64, twiddles from a sincospi table), written back in place.
+//   k_fft_cols  : CTA = 4096/N columns for ALL planes: per plane, column FFT
+//                 (radix-8 Stockham; the last pass stays in registers), the
+//                 phase screen exp(2 pi i w_k (n-1)) and the running sum over
+//                 planes live in registers; after the last plane the
+//                 1/(n_u n_v), 1/n_w and n factors, the real part and the
+//                 residual norms are produced. The transpose-back of the
+//                 reference is never materialised.
+#include "wsb_internal.cuh"
+
+namespace wsb {
+namespace {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -(a.y * b.y)), fma(a.x, b.y, a.y * b.x));
+}
+
+// cos/sin(2 pi u / 16), u = 0..7
+__device__ __forceinline__ double2 root16(int u) {
+    switch (u) {
+        case 0: return make_double2(1.0, 0.0);
+        case 1: return make_double2(0.92387953251128673848, 0.38268343236508977173);
+        case 2: return make_double2(0.70710678118654752440, 0.70710678118654752440);
+        case 3: return make_double2(0.38268343236508977173, 0.92387953251128673848);
+        case 4: return make_double2(0.0, 1.0);
+        case 5: return make_double2(-0.38268343236508977173, 0.92387953251128673848);
+        case 6: return make_double2(-0.70710678118654752440, 0.70710678118654752440);
+        default: return make_double2(-0.92387953251128673848, 0.38268343236508977173);
+    }
+}
+
+// a * exp(+2 pi i u/16)
+__device__ __forceinline__ double2 rot16(double2 a, int u) {
+    if (u == 0) return a;
+    if (u == 4) return make_double2(-a.y, a.x);
+    return cmul(a, root16(u));
+}
+
+constexpr int brev(int i, int R) {
+    int r = 0;
+    for (int b = 1; b < R; b <<= 1) {
+        r <<= 1;
+        if (i & b) r |= 1;
+    }
+    return r;
+}
+
+// Everything below is resolved at compile time so the values stay in
+// registers (a runtime index would push the array to local memory).
+template <int R, int I>
+__device__ __forceinline__ void brev_swap(double2 *y) {
+    if constexpr (I < R) {
+        constexpr int J = brev(I, R);
+        if constexpr (J > I) {
+            const double2 t = y[I];
+            y[I] = y[J];
+            y[J] = t;
+        }
+        brev_swap<R, I + 1>(y);
+    }
+}
+
+template <int R, int LEN, int I, int K>
+__device__ __forceinline__ void dit_butterflies(double2 *y) {
+    if constexpr (I < R) {
+        if constexpr (K < LEN / 2) {
+            const double2 t = rot16(y[I + K + LEN / 2], K * (16 / LEN));
+            const double2 a = y[I + K];
+            y[I + K] = cadd(a, t);
+            y[I + K + LEN / 2] = csub(a, t);
+            dit_butterflies<R, LEN, I, K + 1>(y);
+        } else {
+            dit_butterflies<R, LEN, I + LEN, 0>(y);
+        }
+    }
+}
+
+template <int R, int LEN>
+__device__ __forceinline__ void dit_stages(double2 *y) {
+    if constexpr (LEN <= R) {
+        dit_butterflies<R, LEN, 0, 0>(y);
+        dit_stages<R, LEN * 2>(y);
+    }
+}
+
+// In-register inverse DFT of size R (<= 16), e^{+2 pi i}, natural order out.
+template <int R>
+__device__ __forceinline__ void dft_inv(double2 *y) {
+    brev_swap<R, 0>(y);
+    dit_stages<R, 2>(y);
+}
+
+// padded shared-memory index of element idx of a sequence
+__device__ __forceinline__ int pidx(int idx) { return idx + (idx >> 4); }
+
+template <int LOGN>
+struct Seq {
+    static constexpr int N = 1 << LOGN;
+    static constexpr int STRIDE = N + (N >> 4) + (N >= 16 ? 2 : 0);  // padded sequence stride
+};
+
+// One Stockham pass of radix R = 2^RL over NSEQ sequences of length N held in
+// padded shared memory. E values per thread (E/R butterflies), T threads.
+// TO_REGS: the pass is the last one and its outputs stay in v (no store).
+template <int LOGN, int RL, int E, int T, bool TO_REGS>
+__device__ __forceinline__ void stockham_pass(double2 *s, const double2 *__restrict__ tw, int ns,
+                                              double2 (&v)[E]) {
+    constexpr int N = 1 << LOGN;
+    constexpr int R = 1 << RL;
+    constexpr int NB = E / R;
+    constexpr int M = N / R;  // butterflies per sequence
+    constexpr int STRIDE = Seq<LOGN>::STRIDE;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const int b = threadIdx.x + k * T;
+        const int seq = b / M, j = b % M;
+        const double2 *src = s + seq * STRIDE;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[k * R + r] = src[pidx(j + r * M)];
+    }
+    if (!TO_REGS) __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const int b = threadIdx.x + k * T;
+        const int seq = b / M, j = b % M;
+        const int kk = j % ns;
+        double2 y[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) y[r] = v[k * R + r];
+        if (ns > 1) {
+            const int step = kk * (N / (ns * R));
+#pragma unroll
+            for (int r = 1; r < R; ++r) y[r] = cmul(y[r], __ldg(&tw[r * step]));
+        }
+        dft_inv<R>(y);
+        if (TO_REGS) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[k * R + r] = y[r];
+        } else {
+            double2 *dst = s + seq * STRIDE;
+            const int idxd = (j / ns) * ns * R + kk;
+#pragma unroll
+            for (int r = 0; r < R; ++r) dst[pidx(idxd + r * ns)] = y[r];
+        }
+    }
+    if (!TO_REGS) __syncthreads();
+}
+
+// Radix plan: the first pass takes LOGN % RLMAX (if non-zero), then RLMAX.
+template <int LOGN, int RLMAX, int DONE>
+struct Plan {
+    static constexpr int FIRST = LOGN % RLMAX;
+    static constexpr int RL = (DONE == 0 && FIRST != 0) ? FIRST : RLMAX;
+    static constexpr bool LAST = DONE + RL == LOGN;
+};
+
+template <int LOGN, int RLMAX, int E, int T, bool LAST_TO_REGS, int DONE = 0>
+struct Passes {
+    static __device__ __forceinline__ void run(double2 *s, const double2 *tw, double2 (&v)[E]) {
+        using P = Plan<LOGN, RLMAX, DONE>;
+        stockham_pass<LOGN, P::RL, E, T, P::LAST && LAST_TO_REGS>(s, tw, 1 << DONE, v);
+        if constexpr (!P::LAST) Passes<LOGN, RLMAX, E, T, LAST_TO_REGS, DONE + P::RL>::run(s, tw, v);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// row pass
+// ---------------------------------------------------------------------------
+constexpr int kRowThreads = 512;
+constexpr int kRowE = 16;
+
+template <int LOGN>
+__global__ void __launch_bounds__(kRowThreads, 1)
+    k_fft_rows(double2 *__restrict__ grid, int n_groups, int v_count, int plane_lo,
+               const double2 *__restrict__ tw) {
+    constexpr int N = 1 << LOGN;
+    constexpr int NSEQ = kRowThreads * kRowE / N;  // rows per CTA
+    constexpr int STRIDE = Seq<LOGN>::STRIDE;
+    constexpr int TOTAL = NSEQ * N;
+    extern __shared__ __align__(16) double2 s[];
+    const int j0 = blockIdx.x * NSEQ;
+    const int64_t plane = plane_lo + blockIdx.y;
+    // P[plane][g][row][x]: a group's NSEQ rows are one contiguous run of NSEQ*G
+    for (int e = threadIdx.x; e < TOTAL; e += kRowThreads) {
+        const int g = e / (NSEQ * kG), w = e % (NSEQ * kG);
+        const int rr = w / kG, x = w % kG;
+        double2 z = make_double2(0.0, 0.0);
+        if (j0 + rr < v_count)
+            z = grid[((plane * n_groups + g) * v_count + j0 + rr) * kG + x];
+        s[rr * STRIDE + pidx(g * kG + x)] = z;
+    }
+    __syncthreads();
+    double2 v[kRowE];
+    Passes<LOGN, 4, kRowE, kRowThreads, false>::run(s, tw, v);
+    for (int e = threadIdx.x; e < TOTAL; e += kRowThreads) {
+        const int g = e / (NSEQ * kG), w = e % (NSEQ * kG);
+        const int rr = w / kG, x = w % kG;
+        if (j0 + rr < v_count)
+            grid[((plane * n_groups + g) * v_count + j0 + rr) * kG + x] = s[rr * STRIDE + pidx(g * kG + x)];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// column pass + w correction + stacking
+// ---------------------------------------------------------------------------
+constexpr int kColThreads = 512;
+constexpr int kColE = 8;
+
+struct ColArgs {
+    const double2 *tgrid;
+    double *strip;          // [n_v][ncols]
+    double *partials;       // [n_blocks][2]
+    const double *w_k;      // [n_w] native w per plane
+    int n_w, n_u, n_v, ncols, g0;
+    int n_src;
+    int src_start[9];       // row start of each source slab (+ sentinel)
+    double cell, inv_nuv, inv_nw;
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const double2 *__restrict__ tw) {
+    constexpr int N = 1 << LOGN;  // n_v
+    constexpr int C = kColThreads * kColE / N;  // columns per CTA
+    constexpr int STRIDE = Seq<LOGN>::STRIDE;
+    constexpr int RL = LOGN < 3 ? LOGN : 3;
+    constexpr int R = 1 << RL;  // radix of the last pass (the first one takes any remainder)
+    constexpr int M = N / R;
+    constexpr int NB = kColE / R;
+    extern __shared__ __align__(16) double2 s[];
+    double *nbuf = reinterpret_cast<double *>(s + C * STRIDE);  // n = sqrt(1-l^2-m^2), [C][N]
+
+    const int c0 = blockIdx.x * C;                 // first local column
+    const int64_t plane_elems = (int64_t)(a.ncols / kG) * N * kG;
+
+    // direction-cosine factor per pixel (mesh.py:202-208, transform.py:200)
+    for (int e = threadIdx.x; e < C * N; e += kColThreads) {
+        const int cc = e / N, j = e % N;
+        const int gi = a.g0 * kG + c0 + cc;
+        const double l = (double)(gi - a.n_u / 2) * a.cell;
+        const double m = (double)(j - a.n_v / 2) * a.cell;
+        nbuf[e] = __dsqrt_rn(__dsub_rn(__dsub_rn(1.0, __dmul_rn(l, l)), __dmul_rn(m, m)));
+    }
+
+    double2 acc[kColE];
+#pragma unroll
+    for (int i = 0; i < kColE; ++i) acc[i] = make_double2(0.0, 0.0);
+
+    for (int k = 0; k < a.n_w; ++k) {
+        const double2 *src = a.tgrid + (int64_t)k * plane_elems;
+        __syncthreads();  // previous plane's last pass has finished reading s
+        for (int e = threadIdx.x; e < C * N; e += kColThreads) {
+            // element (row j, local column c0+cc); runs of G along x are contiguous
+            const int cc = e % C, j = e / C;
+            const int lc = c0 + cc;
+            double2 z = make_double2(0.0, 0.0);
+            if (lc < a.ncols) {
+                // source slab of row j (constant indices keep ColArgs in the param bank)
+                int r0 = 0, r1 = a.src_start[1];
+#pragma unroll
+                for (int sidx = 1; sidx < 8; ++sidx)
+                    if (j >= a.src_start[sidx]) {
+                        r0 = a.src_start[sidx];
+                        r1 = a.src_start[sidx + 1];
+                    }
+                const int rows = r1 - r0;
+                const int64_t base = (int64_t)r0 * a.ncols;   // elements before this source
+                z = src[base + ((int64_t)(lc / kG) * rows + (j - r0)) * kG + (lc % kG)];
+            }
+            s[cc * STRIDE + pidx(j)] = z;
+        }
+        __syncthreads();
+        double2 v[kColE];
+        Passes<LOGN, RL, kColE, kColThreads, true>::run(s, tw, v);
+        // v[kb*R + r] is output row j + r*M of sequence (column) seq
+        const double wk = a.w_k[k];
+#pragma unroll
+        for (int kb = 0; kb < NB; ++kb) {
+            const int b = threadIdx.x + kb * kColThreads;
+            const int seq = b / M, j = b % M;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                double2 z = v[kb * R + r];
+                if (wk != 0.0) {  // transform.py:196-198
+                    const double n = nbuf[seq * N + j + r * M];
+                    double sn, cs;
+                    sincospi(2.0 * wk * (n - 1.0), &sn, &cs);
+                    z = cmul(z, make_double2(cs, sn));
+                }
+                acc[kb * R + r] = cadd(acc[kb * R + r], z);
+            }
+        }
+    }
+
+    // finish: /(n_u n_v) (exact power of two), /n_w (numpy multiplies by the
+    // reciprocal), * n (complex * real), real part and residual norms
+    double re_sq = 0.0, im_sq = 0.0;
+#pragma unroll
+    for (int kb = 0; kb < NB; ++kb) {
+        const int b = threadIdx.x + kb * kColThreads;
+        const int seq = b / M, j = b % M;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int lc = c0 + seq, row = j + r * M;
+            if (lc >= a.ncols) continue;
+            double2 z = acc[kb * R + r];
+            z.x *= a.inv_nuv;
+            z.y *= a.inv_nuv;
+            z.x = __dmul_rn(z.x, a.inv_nw);
+            z.y = __dmul_rn(z.y, a.inv_nw);
+            const double n = nbuf[seq * N + row];
+            const double re = __dsub_rn(__dmul_rn(z.x, n), __dmul_rn(z.y, 0.0));
+            const double im = __dadd_rn(__dmul_rn(z.x, 0.0), __dmul_rn(z.y, n));
+            a.strip[(int64_t)row * a.ncols + lc] = re;
+            re_sq = fma(re, re, re_sq);
+            im_sq = fma(im, im, im_sq);
+        }
+    }
+    // deterministic block reduction
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        re_sq += __shfl_xor_sync(0xffffffffu, re_sq, o);
+        im_sq += __shfl_xor_sync(0xffffffffu, im_sq, o);
+    }
+    __shared__ double red[2][kColThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[0][warp] = im_sq;
+        red[1][warp] = re_sq;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double si = 0.0, sr = 0.0;
+        for (int w = 0; w < kColThreads / 32; ++w) {
+            si += red[0][w];
+            sr += red[1][w];
+        }
+        a.partials[2 * blockIdx.x + 0] = si;
+        a.partials[2 * blockIdx.x + 1] = sr;
+    }
+}
+
+__global__ void k_twiddles(double2 *tw, int n) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= n) return;
+    double sn, cs;
+    sincospi(2.0 * (double)m / (double)n, &sn, &cs);
+    tw[m] = make_double2(cs, sn);
+}
+
+template <int LOGN>
+int launch_rows(wsb_ctx *ctx, double2 *grid, int n_groups, int v_count, int plo, int phi,
+                const double2 *tw) {
+    constexpr int N = 1 << LOGN;
+    constexpr int NSEQ = kRowThreads * kRowE / N;
+    const size_t smem = sizeof(double2) * NSEQ * Seq<LOGN>::STRIDE;
+    WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    dim3 grd(ceil_div(v_count, NSEQ), phi - plo);
+    k_fft_rows<LOGN><<<grd, kRowThreads, smem, ctx->stream>>>(grid, n_groups, v_count, plo, tw);
+    ctx->launches += 1;
+    WSB_CUDA_TRY(cudaGetLastError());
+    return WSB_OK;
+}
+
+template <int LOGN>
+int launch_cols(wsb_ctx *ctx, const ColArgs &a, const double2 *tw, int *nblocks) {
+    constexpr int N = 1 << LOGN;
+    constexpr int C = kColThreads * kColE / N;
+    const size_t smem = sizeof(double2) * C * Seq<LOGN>::STRIDE + sizeof(double) * C * N;
+    WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    *nblocks = ceil_div(a.ncols, C);
+    k_fft_cols<LOGN><<<*nblocks, kColThreads, smem, ctx->stream>>>(a, tw);
+    ctx->launches += 1;
+    WSB_CUDA_TRY(cudaGetLastError());
+    return WSB_OK;
+}
+
+}  // namespace
+
+int twiddles(wsb_ctx *ctx, int n, const double **out) {
+    const int l = ilog2(n);
+    if (!ctx->twiddle[l]) {
+        WSB_CUDA_TRY(cudaMalloc(&ctx->twiddle[l], sizeof(double2) * n));
+        k_twiddles<<<ceil_div(n, 256), 256, 0, ctx->stream>>>((double2 *)ctx->twiddle[l], n);
+        ctx->launches += 1;
+        WSB_CUDA_TRY(cudaGetLastError());
+    }
+    *out = ctx->twiddle[l];
+    return WSB_OK;
+}
+
+int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, double *grid_p, int plo, int phi) {
+    if (phi <= plo || v_count <= 0) return WSB_OK;
+    const double *tw;
+    WSB_TRY(twiddles(ctx, g->n_u, &tw));
+    const int ng = g->n_u / kG;
+    double2 *gp = (double2 *)grid_p;
+    const double2 *t2 = (const double2 *)tw;
+    switch (ilog2(g->n_u)) {
+        case 1: return launch_rows<1>(ctx, gp, ng, v_count, plo, phi, t2);
+        case 2: return launch_rows<2>(ctx, gp, ng, v_count, plo, phi, t2);
+        case 3: return launch_rows<3>(ctx, gp, ng, v_count, plo, phi, t2);
+        case 4: return launch_rows<4>(ctx, gp, ng, v_count, plo, phi, t2);
+        case 5: return launch_rows<5>(ctx, gp, ng, v_count, plo, phi, t2);
+        case 6: return launch_rows<6>(ctx, gp, ng, v_count, plo, phi, t2);
+        case 7: return launch_rows<7>(ctx, gp, ng, v_count, plo, phi, t2);
+        case 8: return launch_rows<8>(ctx, gp, ng, v_count, plo, phi, t2);
+        case 9: return launch_rows<9>(ctx, gp, ng, v_count, plo, phi, t2);
+        case 10: return launch_rows<10>(ctx, gp, ng, v_count, plo, phi, t2);
+        case 11: return launch_rows<11>(ctx, gp, ng, v_count, plo, phi, t2);
+        case 12: return launch_rows<12>(ctx, gp, ng, v_count, plo, phi, t2);
+        default: return fail(WSB_EUNSUPPORTED, "n_u above 4096 needs the out-of-core FFT (not in this build)");
+    }
+}
+
+int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t *src_rows,
+                   int g0, int ng, const double *tgrid, double *image_strip,
+                   double *norm_partials) {
+    if (n_sources < 1 || n_sources > 8) return fail(WSB_EINVAL, "n_sources must be in [1, 8]");
+    ColArgs a;
+    a.tgrid = (const double2 *)tgrid;
+    a.strip = image_strip;
+    a.partials = norm_partials;
+    a.n_w = g->n_w;
+    a.n_u = g->n_u;
+    a.n_v = g->n_v;
+    a.ncols = ng * kG;
+    a.g0 = g0;
+    a.n_src = n_sources;
+    a.src_start[0] = 0;
+    for (int s = 0; s < n_sources; ++s) a.src_start[s + 1] = a.src_start[s] + src_rows[s];
+    for (int s = n_sources + 1; s < 9; ++s) a.src_start[s] = 1 << 30;
+    if (a.src_start[n_sources] != g->n_v) return fail(WSB_EINVAL, "source rows must sum to n_v");
+    a.src_start[n_sources] = g->n_v;
+    a.cell = g->cell_size_lm;
+    a.inv_nuv = 1.0 / ((double)g->n_u * (double)g->n_v);
+    a.inv_nw = 1.0 / (double)g->n_w;
+    // native w per plane (mesh.py:101-112)
+    double *wk;
+    WSB_TRY(ensure(ctx, kSlotNorms, sizeof(double) * g->n_w, (void **)&wk));
+    {
+        std::vector<double> h(g->n_w);
+        for (int k = 0; k < g->n_w; ++k) {
+            if (g->n_w == 1) {
+                h[k] = 0.5 * (g->w_min_native + g->w_max_native);
+            } else {
+                const double frac = (double)k / (double)(g->n_w - 1);
+                h[k] = g->w_min_native + frac * (g->w_max_native - g->w_min_native);
+            }
+        }
+        WSB_CUDA_TRY(cudaMemcpyAsync(wk, h.data(), sizeof(double) * g->n_w, cudaMemcpyHostToDevice,
+                                     ctx->stream));
+        WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // h is a stack buffer
+    }
+    a.w_k = wk;
+    const double *tw;
+    WSB_TRY(twiddles(ctx, g->n_v, &tw));
+    const double2 *t2 = (const double2 *)tw;
+    int nb = 0;
+    switch (ilog2(g->n_v)) {
+        case 1: return launch_cols<1>(ctx, a, t2, &nb);
+        case 2: return launch_cols<2>(ctx, a, t2, &nb);
+        case 3: return launch_cols<3>(ctx, a, t2, &nb);
+        case 4: return launch_cols<4>(ctx, a, t2, &nb);
+        case 5: return launch_cols<5>(ctx, a, t2, &nb);
+        case 6: return launch_cols<6>(ctx, a, t2, &nb);
+        case 7: return launch_cols<7>(ctx, a, t2, &nb);
+        case 8: return launch_cols<8>(ctx, a, t2, &nb);
+        case 9: return launch_cols<9>(ctx, a, t2, &nb);
+        case 10: return launch_cols<10>(ctx, a, t2, &nb);
+        case 11: return launch_cols<11>(ctx, a, t2, &nb);
+        case 12: return launch_cols<12>(ctx, a, t2, &nb);
+        default: return fail(WSB_EUNSUPPORTED, "n_v above 4096 needs the out-of-core FFT (not in this build)");
+    }
+}
+
+}  // namespace wsb

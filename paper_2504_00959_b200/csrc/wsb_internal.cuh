@@ -1,0 +1,137 @@
+// Internal declarations shared by the libwsb.so translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/wsb.h"
+
+namespace wsb {
+
+constexpr int kTile = 64;          // gridding tile edge (cells)
+constexpr int kG = WSB_P_GROUP;    // P-layout column group
+constexpr int kMaxS = 7;           // largest half support compiled (window 15)
+
+// thread-local error detail
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+
+#define WSB_CUDA_TRY(expr)                                                        \
+    do {                                                                          \
+        cudaError_t _e = (expr);                                                  \
+        if (_e != cudaSuccess)                                                    \
+            return ::wsb::fail(_e == cudaErrorMemoryAllocation ? WSB_ENOMEM       \
+                                                               : WSB_ECUDA,       \
+                               std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define WSB_TRY(expr)               \
+    do {                            \
+        int _rc = (expr);           \
+        if (_rc != WSB_OK) return _rc; \
+    } while (0)
+
+// Grow-only device workspace slot.
+struct Buf {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+};
+
+struct Timing {
+    cudaEvent_t ev[8];
+    bool created = false;
+};
+
+}  // namespace wsb
+
+struct wsb_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::vector<wsb::Buf> bufs;       // indexed by slot id
+    int *flag_host = nullptr;         // pinned scratch for small readbacks
+    unsigned long long *u64_host = nullptr;
+    wsb::Timing timing;
+    // twiddle tables keyed by log2(n)
+    double *twiddle[16] = {nullptr};
+    // last bucketing (for wsb_tiles_debug)
+    int64_t last_entries = 0, last_tiles = 0;
+    uint32_t *last_keys = nullptr, *last_idx = nullptr, *last_off = nullptr;
+    int launches = 0;
+    double last_ms[6] = {0, 0, 0, 0, 0, 0};
+};
+
+namespace wsb {
+
+enum Slot {
+    kSlotFlag = 0,
+    kSlotBlockCounts,
+    kSlotBlockOffsets,
+    kSlotScanTmp,
+    kSlotKeysA,
+    kSlotKeysB,
+    kSlotIdxA,
+    kSlotIdxB,
+    kSlotTileCount,
+    kSlotTileOff,
+    kSlotRadixHist,
+    kSlotU64,
+    kSlotRec,
+    kSlotPlane,
+    kSlotGrid,
+    kSlotStrip,
+    kSlotNorms,
+    kSlotHostIn,
+    kSlotCount
+};
+
+int ensure(wsb_ctx *ctx, int slot, size_t bytes, void **out);
+int twiddles(wsb_ctx *ctx, int n, const double **out);
+
+// scan.cu
+int exclusive_scan_u32(wsb_ctx *ctx, const uint32_t *in, uint32_t *out, int64_t n,
+                       uint32_t *total_host);
+
+// sort.cu: stable LSD radix sort of (key, val) pairs by the low `bits` of key.
+// Returns the buffers holding the result in *keys_out/*vals_out.
+int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
+                     uint32_t *vals_alt, int64_t n, int bits, uint32_t **keys_out,
+                     uint32_t **vals_out);
+
+// prepare.cu
+int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v,
+            const double *w, const float *vis, const float *weight, int64_t n,
+            int32_t n_chan, double *rec, uint32_t *plane);
+int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const double *rec, int64_t n,
+                int64_t *counts_host, uint32_t **offs_out, int *nb_out);
+int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const double *rec,
+               const uint32_t *plane, int64_t n, double *send_rec, uint32_t *send_plane,
+               int64_t *src_index);
+int bucket_tiles(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_count,
+                 const double *rec, const uint32_t *plane, int64_t m, uint32_t **sorted_idx,
+                 uint32_t **tile_off, int64_t *n_entries, int64_t *n_tiles);
+
+// grid.cu
+int grid_tiles(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start,
+               int v_count, const double *rec, const uint32_t *sorted_idx,
+               const uint32_t *tile_off, int64_t n_tiles, double *grid_p,
+               unsigned long long *updates_dev);
+
+// fft.cu
+int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, double *grid_p, int plane_lo,
+             int plane_hi);
+int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t *src_rows,
+                   int g0, int ng, const double *tgrid, double *image_strip,
+                   double *norm_partials);
+int strip_to_image(wsb_ctx *ctx, const wsb_grid *g, const double *strip, double *image);
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+inline int ilog2(int64_t n) {
+    int l = 0;
+    while ((int64_t(1) << l) < n) ++l;
+    return l;
+}
+
+}  // namespace wsb

@@ -1,0 +1,188 @@
+"""GPU parity: libwsb.so (through the C ABI) against the pinned oracle and the
+reference-generated golden fixtures. Needs a B200."""
+
+import numpy as np
+import pytest
+
+from conftest import chunk_from, rel_l2
+from oracle import wstack_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def W():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_00959_b200 as W
+    return W
+
+
+def _bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64) if a.dtype == np.float64 else a
+
+
+@pytest.mark.parametrize("name", ["syn", "edge"])
+def test_prepare_bitexact(W, golden_bucket, name):
+    g = golden_bucket
+    n_u, n_v, n_w, S = (int(x) for x in g[f"{name}_spec"])
+    u, v, w, t, vis, wt = chunk_from(g, f"{name}_in_")
+    spec = W.GridSpec(n_u, n_v, n_w, 1e-3)
+    rec, plane = W.prepare_device(u, v, w, vis, wt, spec)
+    rec = rec.cpu().numpy()
+    assert np.array_equal(_bits(rec[:, 0]), _bits(g[f"{name}_prep_gu"]))
+    assert np.array_equal(_bits(rec[:, 1]), _bits(g[f"{name}_prep_gv"]))
+    assert np.array_equal(plane.cpu().numpy().astype(np.uint32), g[f"{name}_prep_plane"])
+    val = g[f"{name}_prep_value"]
+    assert np.array_equal(_bits(rec[:, 2]), _bits(val.real.copy()))
+    assert np.array_equal(_bits(rec[:, 3]), _bits(val.imag.copy()))
+
+
+@pytest.mark.parametrize("name", ["syn", "edge"])
+@pytest.mark.parametrize("R", [2, 4, 8])
+def test_route_bitexact(W, golden_bucket, name, R):
+    """Destination slabs (comms.py:516-523) and arrival order vs the
+    reference's SectorBatch columns."""
+    import ctypes as C
+    from paper_2504_00959_b200 import _lib as L
+    from paper_2504_00959_b200.imager import context, _ptr
+    g = golden_bucket
+    n_u, n_v, n_w, S = (int(x) for x in g[f"{name}_spec"])
+    u, v, w, t, vis, wt = chunk_from(g, f"{name}_in_")
+    spec = W.GridSpec(n_u, n_v, n_w, 1e-3)
+    rec, plane = W.prepare_device(u, v, w, vis, wt, spec)
+    ctx = context(rec.device)
+    counts = (C.c_int64 * R)()
+    gs = spec.c_struct()
+    L.check(L.lib().wsb_route_count(ctx.handle, C.byref(gs), S, R, _ptr(rec), rec.shape[0], counts))
+    tot = sum(counts)
+    srec = torch.empty((tot, 4), dtype=torch.float64, device=rec.device)
+    spl = torch.empty(tot, dtype=torch.int32, device=rec.device)
+    sidx = torch.empty(tot, dtype=torch.int64, device=rec.device)
+    L.check(L.lib().wsb_route_pack(ctx.handle, C.byref(gs), S, R, _ptr(rec), _ptr(plane),
+                                   rec.shape[0], _ptr(srec), _ptr(spl), _ptr(sidx)))
+    srec, spl, sidx = srec.cpu().numpy(), spl.cpu().numpy(), sidx.cpu().numpy()
+    off = 0
+    for d in range(R):
+        key = f"{name}_R{R}_d{d}_"
+        n_d = int(counts[d])
+        assert n_d == len(g[key + "gu"])
+        sl = slice(off, off + n_d)
+        assert np.array_equal(sidx[sl].astype(np.uint64), g[key + "gindex"])
+        assert np.array_equal(_bits(srec[sl, 0]), _bits(g[key + "gu"]))
+        assert np.array_equal(_bits(srec[sl, 1]), _bits(g[key + "gv"]))
+        assert np.array_equal(spl[sl].astype(np.uint32), g[key + "plane"])
+        assert np.array_equal(_bits(srec[sl, 2]), _bits(g[key + "value"].real.copy()))
+        off += n_d
+
+
+@pytest.mark.parametrize("kname", ["gauss3", "gauss1", "kb1", "kb3", "kb5"])
+def test_grid_matches_reference(W, golden_grid, kname):
+    g = golden_grid
+    S = int(g[f"{kname}_S"][0])
+    shape = float(g[f"{kname}_shape"][0])
+    kind = "gaussian" if kname.startswith("gauss") else "kaiser_bessel"
+    spec = W.GridSpec(64, 64, 4, 1e-3, w_max_native=12.0)
+    kern = W.KernelSpec(kind, S, shape)
+    u, v, w, t, vis, wt = chunk_from(g, "in_")
+    rec, plane = W.prepare_device(u, v, w, vis, wt, spec)
+    gp, upd = W.grid_slab_device(rec, plane, spec, kern, 0, 64)
+    grid = W.unpack_grid_device(gp, spec, 0, 64).cpu().numpy()
+    assert upd == int(g[f"{kname}_updates"][0])
+    assert np.max(np.abs(grid - g[f"{kname}_grid"])) <= 1e-12
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_grid_slabs_bitwise_across_slab_counts(W, golden_grid, R):
+    """Per-slab gridding after the exchange reproduces the 1-slab grid
+    bit for bit (gridder.py:267-268)."""
+    g = golden_grid
+    spec = W.GridSpec(64, 64, 4, 1e-3, w_max_native=12.0)
+    kern = W.KernelSpec("gaussian", 3, 1.0)
+    u, v, w, t, vis, wt = chunk_from(g, "in_")
+    rec, plane = W.prepare_device(u, v, w, vis, wt, spec)
+    full, upd_full = W.grid_slab_device(rec, plane, spec, kern, 0, 64)
+    full = W.unpack_grid_device(full, spec, 0, 64).cpu().numpy()
+    parts, upd_sum = [], 0
+    gv = rec[:, 1].cpu().numpy()
+    for d in range(R):
+        v0, vc = W.partition_1d(64, R, d)
+        m = (gv + 3 >= v0) & (gv - 3 <= v0 + vc - 1)
+        idx = torch.from_numpy(np.nonzero(m)[0]).to(rec.device)
+        gp, upd = W.grid_slab_device(rec[idx].contiguous(), plane[idx].contiguous(), spec, kern, v0, vc)
+        parts.append(W.unpack_grid_device(gp, spec, v0, vc).cpu().numpy())
+        upd_sum += upd
+    assert upd_sum == upd_full
+    assert np.concatenate(parts, axis=1).tobytes() == full.tobytes()
+
+
+@pytest.mark.parametrize("name", ["small", "kb5", "kb1", "nw1", "wide", "multichan"])
+def test_image_matches_reference(W, golden_image, name):
+    g = golden_image
+    n_u, n_v, n_w, S, _ = (int(x) for x in g[f"{name}_cfg"])
+    cell, wmin, wmax, shape = (float(x) for x in g[f"{name}_fcfg"])
+    kind = "gaussian" if int(g[f"{name}_kind"][0]) == 0 else "kaiser_bessel"
+    spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
+    kern = W.KernelSpec(kind, S, shape)
+    img, diag = W.image(*chunk_from(g, f"{name}_in_"), spec, kern)
+    assert diag["grid_updates"] == int(g[f"{name}_grid_updates"][0])
+    err = rel_l2(img.pixels, g[f"{name}_pixels"])
+    assert err <= 1e-10, err
+    np.testing.assert_allclose([img.imag_residual_norm, img.real_norm], g[f"{name}_norms"],
+                               rtol=1e-9, atol=1e-300)
+
+
+def test_image_medium_vs_oracle(W):
+    """256x256x8, 200k records, KB S=3, w up to 400: GPU vs oracle."""
+    src = ((0.02, -0.015, 2.0), (0.0, 0.0, 1.0), (-0.03, 0.01, 0.5))
+    u, v, w, t, vis, wt = O.generate_synthetic(src, 200_000, 1, seed=21, cell_size_lm=5e-4,
+                                               w_max_native=400.0)
+    spec = W.GridSpec(256, 256, 8, 5e-4, w_max_native=400.0)
+    kern = W.KernelSpec.kaiser_bessel(3)
+    ref = O.image(u, v, w, t, vis, wt, 256, 256, 8, 5e-4, 0.0, 400.0, O.KIND_KAISER_BESSEL, 3,
+                  kern.shape_param)
+    img, diag = W.image(u, v, w, t, vis, wt, spec, kern)
+    assert diag["grid_updates"] == ref["grid_updates"]
+    assert rel_l2(img.pixels, ref["pixels"]) <= 1e-10
+
+
+def test_image_deterministic_and_device_path(W, golden_image):
+    g = golden_image
+    n_u, n_v, n_w, S, _ = (int(x) for x in g["wide_cfg"])
+    cell, wmin, wmax, shape = (float(x) for x in g["wide_fcfg"])
+    spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
+    kern = W.KernelSpec("gaussian", S, shape)
+    u, v, w, t, vis, wt = chunk_from(g, "wide_in_")
+    a, _ = W.image(u, v, w, t, vis, wt, spec, kern)
+    b, _ = W.image(u, v, w, t, vis, wt, spec, kern)
+    dev = torch.device("cuda", 0)
+    c, _ = W.image_device(torch.from_numpy(u).to(dev), torch.from_numpy(v).to(dev),
+                          torch.from_numpy(w).to(dev), torch.from_numpy(vis).to(dev),
+                          torch.from_numpy(wt).to(dev), spec, kern)
+    assert a.pixels.tobytes() == b.pixels.tobytes()
+    assert a.pixels.tobytes() == c.cpu().numpy().tobytes()
+
+
+def test_invalid_inputs_raise_value_error(W):
+    spec = W.GridSpec(32, 32, 2, 1e-3)
+    kern = W.KernelSpec()
+    one = np.ones((1, 1), np.complex64)
+    with pytest.raises(ValueError):
+        W.image([1.0], [0.5], [0.5], None, one, np.ones((1, 1), np.float32), spec, kern)
+    with pytest.raises(ValueError):
+        W.image([0.5], [0.5], [1.5], None, one, np.ones((1, 1), np.float32), spec, kern)
+    with pytest.raises(ValueError):
+        W.image([0.5], [0.5], [0.5], None, one, -np.ones((1, 1), np.float32), spec, kern)
+    with pytest.raises(ValueError):
+        W.image([np.nan], [0.5], [0.5], None, one, np.ones((1, 1), np.float32), spec, kern)
+
+
+def test_empty_input_gives_zero_image(W):
+    spec = W.GridSpec(32, 32, 2, 1e-3)
+    img, diag = W.image(np.zeros(0), np.zeros(0), np.zeros(0), None, np.zeros((0, 1), np.complex64),
+                        np.zeros((0, 1), np.float32), spec, W.KernelSpec())
+    assert diag["grid_updates"] == 0
+    assert not np.any(img.pixels)
