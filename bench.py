@@ -158,10 +158,10 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2504_00959_b200 as W
-    from paper_2504_00959_b200 import distributed as WD
 
     ws, rank, local = dist_env()
     if ws > 1:
+        from paper_2504_00959_b200 import distributed as WD
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if ws > 1 else 0)

@@ -78,7 +78,7 @@ typedef struct {
     double imag_residual_norm, real_norm;
     int64_t grid_updates;     /* == ops["grid_updates"] */
     int64_t records;          /* == ops["records"] */
-    int64_t tile_entries;     /* (record, 64x64 tile) pairs bucketed */
+    int64_t tile_entries;     /* (record, 32-column strip) pairs bucketed */
     double phase_ms[7];       /* read, gridding, reduce, fft, wcorrect, write, total (exclusive) */
 } wsb_diag;
 
@@ -140,8 +140,9 @@ int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int
                    double *send_rec, uint32_t *send_plane, int64_t *src_index);
 
 /* grid_sector (gridder.py:186-259) for the slab rows [v_start, v_start+v_count):
- * buckets the m records into (plane, 64x64 tile) lists (stable counting sort),
- * grids them with the convolution kernel and writes the slab in P layout
+ * buckets the m records by (plane, 32-column strip, anchor row) (counting
+ * sort, record order inside a bucket), grids them with the convolution kernel
+ * in a register-window sweep and writes the slab in P layout
  * (grid_p: complex128[n_w][n_u/G][v_count][G], sign applied). grid_updates
  * (host, nullable) receives the number of cell updates; synchronises if given. */
 int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
@@ -159,8 +160,9 @@ int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count,
  * n_v rows, concatenated by source slab s (rows src_rows[s]) as
  *   [plane][s][g - g0][row - row_start_s][G]   (the all-to-all output).
  * Writes image_strip f64[n_v][ng*G] (row-major) and norm_partials
- * f64[ng][2] = (sum Im^2, sum Re^2) per group; the caller sums partials in
- * group order. */
+ * f64[ng*G][2] = (sum Im^2, sum Re^2) per image column (fixed pairwise tree
+ * over the rows); the caller sums the columns in order, which makes the
+ * norms independent of the GPU count. */
 int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
                        const int32_t *src_rows_host, int32_t g0, int32_t ng,
                        const double *tgrid, double *image_strip, double *norm_partials);
@@ -170,11 +172,12 @@ int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
 int wsb_grid_unpack(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t v_count,
                     const double *grid_p, double *grid_out);
 
-/* Debug / parity: the (tile key, record index) pairs of the last
- * wsb_grid_slab call in sorted order, and the tile offsets.
- * Sizes via wsb_tiles_debug(ctx, NULL, NULL, NULL, &n_entries, &n_tiles). */
-int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *keys_host, uint32_t *idx_host,
-                    uint32_t *tile_off_host, int64_t *n_entries, int64_t *n_tiles);
+/* Debug / parity: the bucketing of the last wsb_grid_slab / wsb_image_device
+ * call: record indices in bucket order and the n_buckets+1 bucket offsets,
+ * bucket = (plane * n_strips + strip) * (v_count + 2S) + floor(gv) - v_start + S
+ * with 32-column strips. Sizes via wsb_tiles_debug(ctx, NULL, NULL, &n, &nb). */
+int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *idx_host, uint32_t *off_host,
+                    int64_t *n_entries, int64_t *n_buckets);
 
 /* Timing of the kernels launched by the last wsb_image_device call, in ms,
  * measured with CUDA events on the context stream:

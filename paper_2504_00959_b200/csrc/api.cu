@@ -136,6 +136,9 @@ int wsb_ctx_create(int32_t device, wsb_ctx **out) {
     c->bufs.resize(kSlotCount);
     int rc = set_device(c);
     if (rc == WSB_OK) {
+        // The gridder gathers 32-byte records at random; larger L2 fetches
+        // only waste HBM bandwidth (streaming kernels read whole lines anyway).
+        if (cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32) != cudaSuccess) cudaGetLastError();
         cudaError_t a = cudaMallocHost(&c->flag_host, 64);
         if (a != cudaSuccess) rc = fail(WSB_ENOMEM, "pinned allocation failed");
     }
@@ -219,13 +222,10 @@ static int grid_slab_impl(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *
                           int32_t v_start, int32_t v_count, const double *rec,
                           const uint32_t *plane, int64_t m, double *grid_p,
                           unsigned long long *updates_dev, int64_t *n_entries_out) {
-    uint32_t *sidx, *toff;
-    int64_t n_entries, n_tiles;
-    WSB_TRY(bucket_tiles(ctx, grid, kern->half_support, v_start, v_count, rec, plane, m, &sidx,
-                         &toff, &n_entries, &n_tiles));
-    if (n_entries_out) *n_entries_out = n_entries;
-    return grid_tiles(ctx, grid, kern, v_start, v_count, rec, sidx, toff, n_tiles, grid_p,
-                      updates_dev);
+    RowBuckets bk;
+    WSB_TRY(bucket_rows(ctx, grid, kern->half_support, v_start, v_count, rec, plane, m, &bk));
+    if (n_entries_out) *n_entries_out = bk.n_entries;
+    return grid_sweep(ctx, grid, kern, v_start, v_count, rec, bk, grid_p, updates_dev);
 }
 
 int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern, int32_t v_start,
@@ -287,19 +287,17 @@ int wsb_grid_unpack(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t
     return WSB_OK;
 }
 
-int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *keys_host, uint32_t *idx_host, uint32_t *tile_off_host,
-                    int64_t *n_entries, int64_t *n_tiles) {
+int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *idx_host, uint32_t *off_host, int64_t *n_entries,
+                    int64_t *n_buckets) {
     if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
     WSB_TRY(set_device(ctx));
     if (n_entries) *n_entries = ctx->last_entries;
-    if (n_tiles) *n_tiles = ctx->last_tiles;
+    if (n_buckets) *n_buckets = ctx->last_tiles;
     WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (keys_host && ctx->last_entries)
-        WSB_CUDA_TRY(cudaMemcpy(keys_host, ctx->last_keys, 4 * ctx->last_entries, cudaMemcpyDeviceToHost));
     if (idx_host && ctx->last_entries)
         WSB_CUDA_TRY(cudaMemcpy(idx_host, ctx->last_idx, 4 * ctx->last_entries, cudaMemcpyDeviceToHost));
-    if (tile_off_host && ctx->last_tiles)
-        WSB_CUDA_TRY(cudaMemcpy(tile_off_host, ctx->last_off, 4 * (ctx->last_tiles + 1), cudaMemcpyDeviceToHost));
+    if (off_host && ctx->last_tiles)
+        WSB_CUDA_TRY(cudaMemcpy(off_host, ctx->last_off, 4 * (ctx->last_tiles + 1), cudaMemcpyDeviceToHost));
     return WSB_OK;
 }
 
@@ -340,19 +338,18 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
     WSB_CUDA_TRY(cudaMemsetAsync(upd, 0, sizeof(unsigned long long), ctx->stream));
     WSB_TRY(prepare(ctx, grid, u, v, w, vis, weight, n, n_chan, rec, plane));
     WSB_CUDA_TRY(cudaEventRecord(ev[1], ctx->stream));
-    uint32_t *sidx, *toff;
-    int64_t n_entries = 0, n_tiles = 0;
-    WSB_TRY(bucket_tiles(ctx, grid, kern->half_support, 0, n_v, rec, plane, n, &sidx, &toff,
-                         &n_entries, &n_tiles));
+    RowBuckets bk;
+    WSB_TRY(bucket_rows(ctx, grid, kern->half_support, 0, n_v, rec, plane, n, &bk));
+    const int64_t n_entries = bk.n_entries;
     WSB_CUDA_TRY(cudaEventRecord(ev[2], ctx->stream));
-    WSB_TRY(grid_tiles(ctx, grid, kern, 0, n_v, rec, sidx, toff, n_tiles, gp, upd));
+    WSB_TRY(grid_sweep(ctx, grid, kern, 0, n_v, rec, bk, gp, upd));
     WSB_CUDA_TRY(cudaEventRecord(ev[3], ctx->stream));
     WSB_TRY(fft_rows(ctx, grid, n_v, gp, 0, n_w));
     WSB_CUDA_TRY(cudaEventRecord(ev[4], ctx->stream));
     const int32_t rows[1] = {n_v};
     WSB_TRY(fft_cols_stack(ctx, grid, 1, rows, 0, n_u / kG, gp, image_out, partials));
     WSB_CUDA_TRY(cudaEventRecord(ev[5], ctx->stream));
-    const int nb = ceil_div(n_u, std::max(1, 4096 / n_v));
+    const int nb = n_u;  // one norm partial per image column
     k_sum_partials<<<1, 32, 0, ctx->stream>>>(partials, nb, partials + 2 * (size_t)n_u);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());

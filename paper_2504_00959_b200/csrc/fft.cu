@@ -178,33 +178,57 @@ struct Passes {
 // ---------------------------------------------------------------------------
 // row pass
 // ---------------------------------------------------------------------------
-constexpr int kRowThreads = 512;
+constexpr int kRowThreads = 256;
 constexpr int kRowE = 16;
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// 4096/N rows per CTA (70 KB of shared memory), two CTAs per SM so one
+// CTA's loads overlap the other's transform; all loads of a thread are in
+// flight at once (16 x 16 B).
 template <int LOGN>
-__global__ void __launch_bounds__(kRowThreads, 1)
+__global__ void __launch_bounds__(kRowThreads, 2)
     k_fft_rows(double2 *__restrict__ grid, int n_groups, int v_count, int plane_lo,
                const double2 *__restrict__ tw) {
     constexpr int N = 1 << LOGN;
     constexpr int NSEQ = kRowThreads * kRowE / N;  // rows per CTA
     constexpr int STRIDE = Seq<LOGN>::STRIDE;
     constexpr int TOTAL = NSEQ * N;
+    constexpr int PER_T = TOTAL / kRowThreads;
     extern __shared__ __align__(16) double2 s[];
     const int j0 = blockIdx.x * NSEQ;
     const int64_t plane = plane_lo + blockIdx.y;
     // P[plane][g][row][x]: a group's NSEQ rows are one contiguous run of NSEQ*G
-    for (int e = threadIdx.x; e < TOTAL; e += kRowThreads) {
+    double2 z[PER_T];
+#pragma unroll
+    for (int t = 0; t < PER_T; ++t) {
+        const int e = threadIdx.x + t * kRowThreads;
         const int g = e / (NSEQ * kG), w = e % (NSEQ * kG);
         const int rr = w / kG, x = w % kG;
-        double2 z = make_double2(0.0, 0.0);
-        if (j0 + rr < v_count)
-            z = grid[((plane * n_groups + g) * v_count + j0 + rr) * kG + x];
-        s[rr * STRIDE + pidx(g * kG + x)] = z;
+        z[t] = make_double2(0.0, 0.0);
+        if (j0 + rr < v_count) z[t] = grid[((plane * n_groups + g) * v_count + j0 + rr) * kG + x];
+    }
+#pragma unroll
+    for (int t = 0; t < PER_T; ++t) {
+        const int e = threadIdx.x + t * kRowThreads;
+        const int g = e / (NSEQ * kG), w = e % (NSEQ * kG);
+        const int rr = w / kG, x = w % kG;
+        s[rr * STRIDE + pidx(g * kG + x)] = z[t];
     }
     __syncthreads();
     double2 v[kRowE];
     Passes<LOGN, 4, kRowE, kRowThreads, false>::run(s, tw, v);
-    for (int e = threadIdx.x; e < TOTAL; e += kRowThreads) {
+#pragma unroll
+    for (int t = 0; t < PER_T; ++t) {
+        const int e = threadIdx.x + t * kRowThreads;
         const int g = e / (NSEQ * kG), w = e % (NSEQ * kG);
         const int rr = w / kG, x = w % kG;
         if (j0 + rr < v_count)
@@ -238,11 +262,40 @@ __global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const do
     constexpr int R = 1 << RL;  // radix of the last pass (the first one takes any remainder)
     constexpr int M = N / R;
     constexpr int NB = kColE / R;
-    extern __shared__ __align__(16) double2 s[];
-    double *nbuf = reinterpret_cast<double *>(s + C * STRIDE);  // n = sqrt(1-l^2-m^2), [C][N]
+    extern __shared__ __align__(16) double2 sbuf[];
+    // two plane buffers: plane k+1 streams in (cp.async) while plane k is transformed
+    double *nbuf = reinterpret_cast<double *>(sbuf + 2 * C * STRIDE);  // n = sqrt(1-l^2-m^2), [C][N]
 
     const int c0 = blockIdx.x * C;                 // first local column
     const int64_t plane_elems = (int64_t)(a.ncols / kG) * N * kG;
+
+    // element (row j, local column c0+cc) of plane k -> buffer; runs of G
+    // along x are contiguous in the (transposed) slab layout
+    auto load_plane = [&](int k, double2 *buf) {
+        const double2 *src = a.tgrid + (int64_t)k * plane_elems;
+        for (int e = threadIdx.x; e < C * N; e += kColThreads) {
+            const int cc = e % C, j = e / C;
+            const int lc = c0 + cc;
+            double2 *dst = &buf[cc * STRIDE + pidx(j)];
+            if (lc < a.ncols) {
+                // source slab of row j (constant indices keep ColArgs in the param bank)
+                int r0 = 0, r1 = a.src_start[1];
+#pragma unroll
+                for (int sidx = 1; sidx < 8; ++sidx)
+                    if (j >= a.src_start[sidx]) {
+                        r0 = a.src_start[sidx];
+                        r1 = a.src_start[sidx + 1];
+                    }
+                const int rows = r1 - r0;
+                const int64_t base = (int64_t)r0 * a.ncols;   // elements before this source
+                cp_async16(dst, &src[base + ((int64_t)(lc / kG) * rows + (j - r0)) * kG + (lc % kG)]);
+            } else {
+                *dst = make_double2(0.0, 0.0);
+            }
+        }
+        cp_async_commit();
+    };
+    load_plane(0, sbuf);
 
     // direction-cosine factor per pixel (mesh.py:202-208, transform.py:200)
     for (int e = threadIdx.x; e < C * N; e += kColThreads) {
@@ -258,29 +311,15 @@ __global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const do
     for (int i = 0; i < kColE; ++i) acc[i] = make_double2(0.0, 0.0);
 
     for (int k = 0; k < a.n_w; ++k) {
-        const double2 *src = a.tgrid + (int64_t)k * plane_elems;
-        __syncthreads();  // previous plane's last pass has finished reading s
-        for (int e = threadIdx.x; e < C * N; e += kColThreads) {
-            // element (row j, local column c0+cc); runs of G along x are contiguous
-            const int cc = e % C, j = e / C;
-            const int lc = c0 + cc;
-            double2 z = make_double2(0.0, 0.0);
-            if (lc < a.ncols) {
-                // source slab of row j (constant indices keep ColArgs in the param bank)
-                int r0 = 0, r1 = a.src_start[1];
-#pragma unroll
-                for (int sidx = 1; sidx < 8; ++sidx)
-                    if (j >= a.src_start[sidx]) {
-                        r0 = a.src_start[sidx];
-                        r1 = a.src_start[sidx + 1];
-                    }
-                const int rows = r1 - r0;
-                const int64_t base = (int64_t)r0 * a.ncols;   // elements before this source
-                z = src[base + ((int64_t)(lc / kG) * rows + (j - r0)) * kG + (lc % kG)];
-            }
-            s[cc * STRIDE + pidx(j)] = z;
+        double2 *s = sbuf + (k & 1) * C * STRIDE;
+        __syncthreads();  // plane k-1 is done with the other buffer
+        if (k + 1 < a.n_w) {
+            load_plane(k + 1, sbuf + ((k + 1) & 1) * C * STRIDE);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
-        __syncthreads();
+        __syncthreads();  // plane k is in shared memory for every thread
         double2 v[kColE];
         Passes<LOGN, RL, kColE, kColThreads, true>::run(s, tw, v);
         // v[kb*R + r] is output row j + r*M of sequence (column) seq
@@ -304,16 +343,19 @@ __global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const do
     }
 
     // finish: /(n_u n_v) (exact power of two), /n_w (numpy multiplies by the
-    // reciprocal), * n (complex * real), real part and residual norms
-    double re_sq = 0.0, im_sq = 0.0;
+    // reciprocal), * n (complex * real). Pixels go through shared memory so
+    // the image strip is written row by row and the residual norms are
+    // reduced per column in a fixed tree order (identical for any GPU count).
+    __syncthreads();  // both plane buffers are free now
+    double2 *pix = sbuf;                        // (re, im) per pixel, [C][STRIDE]
+    double2 *sq = sbuf + C * STRIDE;            // (im^2, re^2) per pixel
 #pragma unroll
     for (int kb = 0; kb < NB; ++kb) {
         const int b = threadIdx.x + kb * kColThreads;
         const int seq = b / M, j = b % M;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int lc = c0 + seq, row = j + r * M;
-            if (lc >= a.ncols) continue;
+            const int row = j + r * M;
             double2 z = acc[kb * R + r];
             z.x *= a.inv_nuv;
             z.y *= a.inv_nuv;
@@ -322,33 +364,30 @@ __global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const do
             const double n = nbuf[seq * N + row];
             const double re = __dsub_rn(__dmul_rn(z.x, n), __dmul_rn(z.y, 0.0));
             const double im = __dadd_rn(__dmul_rn(z.x, 0.0), __dmul_rn(z.y, n));
-            a.strip[(int64_t)row * a.ncols + lc] = re;
-            re_sq = fma(re, re, re_sq);
-            im_sq = fma(im, im, im_sq);
+            pix[seq * STRIDE + pidx(row)] = make_double2(re, im);
+            sq[seq * STRIDE + row] = make_double2(__dmul_rn(im, im), __dmul_rn(re, re));
         }
-    }
-    // deterministic block reduction
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        re_sq += __shfl_xor_sync(0xffffffffu, re_sq, o);
-        im_sq += __shfl_xor_sync(0xffffffffu, im_sq, o);
-    }
-    __shared__ double red[2][kColThreads / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) {
-        red[0][warp] = im_sq;
-        red[1][warp] = re_sq;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double si = 0.0, sr = 0.0;
-        for (int w = 0; w < kColThreads / 32; ++w) {
-            si += red[0][w];
-            sr += red[1][w];
-        }
-        a.partials[2 * blockIdx.x + 0] = si;
-        a.partials[2 * blockIdx.x + 1] = sr;
+    // image rows: the C columns of a row are contiguous in the strip
+    for (int e = threadIdx.x; e < C * N; e += kColThreads) {
+        const int cc = e % C, row = e / C;
+        if (c0 + cc < a.ncols) a.strip[(int64_t)row * a.ncols + c0 + cc] = pix[cc * STRIDE + pidx(row)].x;
     }
+    // per-column pairwise tree over the N rows
+    for (int half = N / 2; half > 0; half >>= 1) {
+        for (int e = threadIdx.x; e < C * half; e += kColThreads) {
+            const int cc = e / half, i = e % half;
+            double2 *p = sq + cc * STRIDE;
+            p[i] = make_double2(p[i].x + p[i + half].x, p[i].y + p[i + half].y);
+        }
+        __syncthreads();
+    }
+    for (int cc = threadIdx.x; cc < C; cc += kColThreads)
+        if (c0 + cc < a.ncols) {
+            a.partials[2 * (c0 + cc) + 0] = sq[cc * STRIDE].x;
+            a.partials[2 * (c0 + cc) + 1] = sq[cc * STRIDE].y;
+        }
 }
 
 __global__ void k_twiddles(double2 *tw, int n) {
@@ -378,7 +417,7 @@ template <int LOGN>
 int launch_cols(wsb_ctx *ctx, const ColArgs &a, const double2 *tw, int *nblocks) {
     constexpr int N = 1 << LOGN;
     constexpr int C = kColThreads * kColE / N;
-    const size_t smem = sizeof(double2) * C * Seq<LOGN>::STRIDE + sizeof(double) * C * N;
+    const size_t smem = sizeof(double2) * 2 * C * Seq<LOGN>::STRIDE + sizeof(double) * C * N;
     WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     *nblocks = ceil_div(a.ncols, C);

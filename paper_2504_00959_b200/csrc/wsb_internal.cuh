@@ -84,6 +84,9 @@ enum Slot {
     kSlotStrip,
     kSlotNorms,
     kSlotHostIn,
+    kSlotRadixTmpA,
+    kSlotRadixTmpB,
+    kSlotRadixTmpC,
     kSlotCount
 };
 
@@ -109,14 +112,20 @@ int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const double *rec
 int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const double *rec,
                const uint32_t *plane, int64_t n, double *send_rec, uint32_t *send_plane,
                int64_t *src_index);
-int bucket_tiles(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_count,
-                 const double *rec, const uint32_t *plane, int64_t m, uint32_t **sorted_idx,
-                 uint32_t **tile_off, int64_t *n_entries, int64_t *n_tiles);
+
+// bucket.cu: records of a slab bucketed by (plane, 32-column strip, anchor row)
+struct RowBuckets {
+    uint32_t *idx = nullptr;   // record indices, bucket-major, ascending inside a bucket
+    uint32_t *off = nullptr;   // [n_keys + 1] exclusive offsets
+    int64_t n_entries = 0, n_keys = 0;
+    int n_tc = 0, rs = 0;      // strips, anchor rows per strip (v_count + 2S)
+};
+int bucket_rows(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_count,
+                const double *rec, const uint32_t *plane, int64_t m, RowBuckets *out);
 
 // grid.cu
-int grid_tiles(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start,
-               int v_count, const double *rec, const uint32_t *sorted_idx,
-               const uint32_t *tile_off, int64_t n_tiles, double *grid_p,
+int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start, int v_count,
+               const double *rec, const RowBuckets &bk, double *grid_p,
                unsigned long long *updates_dev);
 
 // fft.cu
