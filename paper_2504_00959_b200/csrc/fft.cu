@@ -6,17 +6,21 @@
 // screen (transform.py:192-202) and stacks the planes (transform.py:205-230).
 //
 // Here a plane makes two passes over HBM:
-//   k_fft_rows  : CTA = 8192/N rows of one plane, loaded from the P layout in
-//                 128-byte runs, radix-16 Stockham autosort in shared memory
-//                 (FP64, twiddles from a sincospi table), written back in place.
+//   k_fft_rows  : CTA = 4096/N rows of one plane. Radix-16 Stockham autosort
+//                 (FP64, twiddles from a sincospi table): the first pass
+//                 reads the P layout straight from HBM into registers, the
+//                 inner exchanges go through shared memory, the last pass
+//                 writes straight back. In place.
 //   k_fft_cols  : CTA = 4096/N columns for ALL planes: per plane, column FFT
-//                 (radix-8 Stockham; the last pass stays in registers), the
-//                 phase screen exp(2 pi i w_k (n-1)) and the running sum over
-//                 planes live in registers; after the last plane the
-//                 1/(n_u n_v), 1/n_w and n factors, the real part and the
-//                 residual norms are produced. The transpose-back of the
-//                 reference is never materialised.
+//                 (radix-8; plane k+1's inputs are loaded into registers
+//                 while plane k is transformed; the last pass stays in
+//                 registers), the phase screen exp(2 pi i w_k (n-1)) and the
+//                 running sum over planes in registers; after the last plane
+//                 the 1/(n_u n_v), 1/n_w and n factors, the real part, the
+//                 image strip and per-column residual norms. The transpose-back
+//                 of the reference is never materialised.
 #include "wsb_internal.cuh"
+
 
 namespace wsb {
 namespace {
@@ -111,51 +115,57 @@ struct Seq {
     static constexpr int STRIDE = N + (N >> 4) + (N >= 16 ? 2 : 0);  // padded sequence stride
 };
 
-// One Stockham pass of radix R = 2^RL over NSEQ sequences of length N held in
-// padded shared memory. E values per thread (E/R butterflies), T threads.
-// TO_REGS: the pass is the last one and its outputs stay in v (no store).
-template <int LOGN, int RL, int E, int T, bool TO_REGS>
-__device__ __forceinline__ void stockham_pass(double2 *s, const double2 *__restrict__ tw, int ns,
-                                              double2 (&v)[E]) {
-    constexpr int N = 1 << LOGN;
-    constexpr int R = 1 << RL;
-    constexpr int NB = E / R;
-    constexpr int M = N / R;  // butterflies per sequence
-    constexpr int STRIDE = Seq<LOGN>::STRIDE;
+
+// ---------------------------------------------------------------------------
+// Stockham pass pieces (radix R = 2^RL, N = 2^LOGN, E values per thread, T
+// threads; butterfly b of a pass = (sequence b / (N/R), index j = b % (N/R))).
+// A pass reads x[j + r N/R], multiplies by the twiddles of its stage,
+// applies the radix-R DFT and writes y[(j/ns) ns R + j%ns + r ns].
+// ---------------------------------------------------------------------------
+template <int LOGN, int RL, int E, int T, class LD>
+__device__ __forceinline__ void pass_load(double2 (&v)[E], LD ld) {
+    constexpr int R = 1 << RL, NB = E / R, M = (1 << LOGN) / R;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
         const int b = threadIdx.x + k * T;
         const int seq = b / M, j = b % M;
-        const double2 *src = s + seq * STRIDE;
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[k * R + r] = src[pidx(j + r * M)];
+        for (int r = 0; r < R; ++r) v[k * R + r] = ld(seq, j + r * M);
     }
-    if (!TO_REGS) __syncthreads();
+}
+
+template <int LOGN, int RL, int E, int T>
+__device__ __forceinline__ void pass_compute(int ns, const double2 *__restrict__ tw,
+                                             double2 (&v)[E]) {
+    constexpr int N = 1 << LOGN, R = 1 << RL, NB = E / R, M = N / R;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
-        const int b = threadIdx.x + k * T;
-        const int seq = b / M, j = b % M;
-        const int kk = j % ns;
+        const int j = (threadIdx.x + k * T) % M;
         double2 y[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) y[r] = v[k * R + r];
         if (ns > 1) {
-            const int step = kk * (N / (ns * R));
+            const int step = (j % ns) * (N / (ns * R));
 #pragma unroll
             for (int r = 1; r < R; ++r) y[r] = cmul(y[r], __ldg(&tw[r * step]));
         }
         dft_inv<R>(y);
-        if (TO_REGS) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[k * R + r] = y[r];
-        } else {
-            double2 *dst = s + seq * STRIDE;
-            const int idxd = (j / ns) * ns * R + kk;
-#pragma unroll
-            for (int r = 0; r < R; ++r) dst[pidx(idxd + r * ns)] = y[r];
-        }
+        for (int r = 0; r < R; ++r) v[k * R + r] = y[r];
     }
-    if (!TO_REGS) __syncthreads();
+}
+
+template <int LOGN, int RL, int E, int T, class ST>
+__device__ __forceinline__ void pass_store(int ns, const double2 (&v)[E], ST st) {
+    constexpr int R = 1 << RL, NB = E / R, M = (1 << LOGN) / R;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+        const int b = threadIdx.x + k * T;
+        const int seq = b / M, j = b % M;
+        const int idxd = (j / ns) * ns * R + j % ns;
+#pragma unroll
+        for (int r = 0; r < R; ++r) st(seq, idxd + r * ns, v[k * R + r]);
+    }
 }
 
 // Radix plan: the first pass takes LOGN % RLMAX (if non-zero), then RLMAX.
@@ -166,34 +176,34 @@ struct Plan {
     static constexpr bool LAST = DONE + RL == LOGN;
 };
 
-template <int LOGN, int RLMAX, int E, int T, bool LAST_TO_REGS, int DONE = 0>
-struct Passes {
-    static __device__ __forceinline__ void run(double2 *s, const double2 *tw, double2 (&v)[E]) {
-        using P = Plan<LOGN, RLMAX, DONE>;
-        stockham_pass<LOGN, P::RL, E, T, P::LAST && LAST_TO_REGS>(s, tw, 1 << DONE, v);
-        if constexpr (!P::LAST) Passes<LOGN, RLMAX, E, T, LAST_TO_REGS, DONE + P::RL>::run(s, tw, v);
+// Passes 1..last-1 in shared memory (in place), then the last pass's loads
+// and compute: its results stay in v, at (seq, j + r*N/R) of butterfly b.
+template <int LOGN, int RLMAX, int E, int T, int DONE>
+__device__ __forceinline__ void smem_passes(double2 *s, const double2 *tw, double2 (&v)[E]) {
+    using P = Plan<LOGN, RLMAX, DONE>;
+    constexpr int STRIDE = Seq<LOGN>::STRIDE;
+    auto ld = [&](int seq, int idx) { return s[seq * STRIDE + pidx(idx)]; };
+    pass_load<LOGN, P::RL, E, T>(v, ld);
+    if constexpr (!P::LAST) __syncthreads();
+    pass_compute<LOGN, P::RL, E, T>(1 << DONE, tw, v);
+    if constexpr (!P::LAST) {
+        auto st = [&](int seq, int idx, double2 z) { s[seq * STRIDE + pidx(idx)] = z; };
+        pass_store<LOGN, P::RL, E, T>(1 << DONE, v, st);
+        __syncthreads();
+        smem_passes<LOGN, RLMAX, E, T, DONE + P::RL>(s, tw, v);
     }
-};
+}
 
 // ---------------------------------------------------------------------------
-// row pass
+// row pass: global -> registers -> (shared memory passes) -> global
 // ---------------------------------------------------------------------------
 constexpr int kRowThreads = 256;
 constexpr int kRowE = 16;
+constexpr int kRowRL = 4;
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-// 4096/N rows per CTA (70 KB of shared memory), two CTAs per SM so one
-// CTA's loads overlap the other's transform; all loads of a thread are in
-// flight at once (16 x 16 B).
+// 4096/N rows per CTA. The first pass reads its inputs straight from HBM
+// (32-byte sectors, 16 loads in flight per thread) and the last pass writes
+// its outputs straight back: shared memory only carries the inner exchanges.
 template <int LOGN>
 __global__ void __launch_bounds__(kRowThreads, 2)
     k_fft_rows(double2 *__restrict__ grid, int n_groups, int v_count, int plane_lo,
@@ -201,38 +211,32 @@ __global__ void __launch_bounds__(kRowThreads, 2)
     constexpr int N = 1 << LOGN;
     constexpr int NSEQ = kRowThreads * kRowE / N;  // rows per CTA
     constexpr int STRIDE = Seq<LOGN>::STRIDE;
-    constexpr int TOTAL = NSEQ * N;
-    constexpr int PER_T = TOTAL / kRowThreads;
+    using P0 = Plan<LOGN, kRowRL, 0>;
     extern __shared__ __align__(16) double2 s[];
     const int j0 = blockIdx.x * NSEQ;
     const int64_t plane = plane_lo + blockIdx.y;
-    // P[plane][g][row][x]: a group's NSEQ rows are one contiguous run of NSEQ*G
-    double2 z[PER_T];
-#pragma unroll
-    for (int t = 0; t < PER_T; ++t) {
-        const int e = threadIdx.x + t * kRowThreads;
-        const int g = e / (NSEQ * kG), w = e % (NSEQ * kG);
-        const int rr = w / kG, x = w % kG;
-        z[t] = make_double2(0.0, 0.0);
-        if (j0 + rr < v_count) z[t] = grid[((plane * n_groups + g) * v_count + j0 + rr) * kG + x];
-    }
-#pragma unroll
-    for (int t = 0; t < PER_T; ++t) {
-        const int e = threadIdx.x + t * kRowThreads;
-        const int g = e / (NSEQ * kG), w = e % (NSEQ * kG);
-        const int rr = w / kG, x = w % kG;
-        s[rr * STRIDE + pidx(g * kG + x)] = z[t];
-    }
-    __syncthreads();
+    // P[plane][col/G][row][col%G]
+    auto gaddr = [&](int seq, int col) -> int64_t {
+        return ((plane * n_groups + col / kG) * v_count + j0 + seq) * kG + (col % kG);
+    };
+    auto gld = [&](int seq, int col) {
+        return j0 + seq < v_count ? grid[gaddr(seq, col)] : make_double2(0.0, 0.0);
+    };
+    auto gst = [&](int seq, int col, double2 z) {
+        if (j0 + seq < v_count) grid[gaddr(seq, col)] = z;
+    };
     double2 v[kRowE];
-    Passes<LOGN, 4, kRowE, kRowThreads, false>::run(s, tw, v);
-#pragma unroll
-    for (int t = 0; t < PER_T; ++t) {
-        const int e = threadIdx.x + t * kRowThreads;
-        const int g = e / (NSEQ * kG), w = e % (NSEQ * kG);
-        const int rr = w / kG, x = w % kG;
-        if (j0 + rr < v_count)
-            grid[((plane * n_groups + g) * v_count + j0 + rr) * kG + x] = s[rr * STRIDE + pidx(g * kG + x)];
+    pass_load<LOGN, P0::RL, kRowE, kRowThreads>(v, gld);
+    pass_compute<LOGN, P0::RL, kRowE, kRowThreads>(1, tw, v);
+    if constexpr (P0::LAST) {
+        pass_store<LOGN, P0::RL, kRowE, kRowThreads>(1, v, gst);
+    } else {
+        auto sst = [&](int seq, int idx, double2 z) { s[seq * STRIDE + pidx(idx)] = z; };
+        pass_store<LOGN, P0::RL, kRowE, kRowThreads>(1, v, sst);
+        __syncthreads();
+        smem_passes<LOGN, kRowRL, kRowE, kRowThreads, P0::RL>(s, tw, v);
+        constexpr int RLL = kRowRL;  // the last pass is always a full-radix pass here
+        pass_store<LOGN, RLL, kRowE, kRowThreads>(N >> RLL, v, gst);
     }
 }
 
@@ -241,11 +245,12 @@ __global__ void __launch_bounds__(kRowThreads, 2)
 // ---------------------------------------------------------------------------
 constexpr int kColThreads = 512;
 constexpr int kColE = 8;
+constexpr int kColRL = 3;
 
 struct ColArgs {
     const double2 *tgrid;
     double *strip;          // [n_v][ncols]
-    double *partials;       // [n_blocks][2]
+    double *partials;       // [ncols][2]
     const double *w_k;      // [n_w] native w per plane
     int n_w, n_u, n_v, ncols, g0;
     int n_src;
@@ -253,49 +258,44 @@ struct ColArgs {
     double cell, inv_nuv, inv_nw;
 };
 
+// CTA = 4096/N columns for all planes. Plane k+1's first-pass inputs are
+// loaded into registers while plane k is transformed; the last pass leaves
+// its outputs in registers where the phase screen is applied and the planes
+// are summed.
 template <int LOGN>
 __global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const double2 *__restrict__ tw) {
-    constexpr int N = 1 << LOGN;  // n_v
-    constexpr int C = kColThreads * kColE / N;  // columns per CTA
+    constexpr int N = 1 << LOGN;                 // n_v
+    constexpr int C = kColThreads * kColE / N;   // columns per CTA
     constexpr int STRIDE = Seq<LOGN>::STRIDE;
-    constexpr int RL = LOGN < 3 ? LOGN : 3;
-    constexpr int R = 1 << RL;  // radix of the last pass (the first one takes any remainder)
+    constexpr int RLM = LOGN < kColRL ? LOGN : kColRL;
+    using P0 = Plan<LOGN, RLM, 0>;
+    constexpr int R = 1 << RLM;                  // radix of the last pass
     constexpr int M = N / R;
     constexpr int NB = kColE / R;
     extern __shared__ __align__(16) double2 sbuf[];
-    // two plane buffers: plane k+1 streams in (cp.async) while plane k is transformed
     double *nbuf = reinterpret_cast<double *>(sbuf + 2 * C * STRIDE);  // n = sqrt(1-l^2-m^2), [C][N]
 
     const int c0 = blockIdx.x * C;                 // first local column
     const int64_t plane_elems = (int64_t)(a.ncols / kG) * N * kG;
 
-    // element (row j, local column c0+cc) of plane k -> buffer; runs of G
-    // along x are contiguous in the (transposed) slab layout
-    auto load_plane = [&](int k, double2 *buf) {
+    // element (row j, local column c0+seq) of plane k in the transposed slab
+    // layout [s][g][row - row_start_s][x]
+    auto gld_plane = [&](int k) {
         const double2 *src = a.tgrid + (int64_t)k * plane_elems;
-        for (int e = threadIdx.x; e < C * N; e += kColThreads) {
-            const int cc = e % C, j = e / C;
-            const int lc = c0 + cc;
-            double2 *dst = &buf[cc * STRIDE + pidx(j)];
-            if (lc < a.ncols) {
-                // source slab of row j (constant indices keep ColArgs in the param bank)
-                int r0 = 0, r1 = a.src_start[1];
+        return [=](int seq, int j) {
+            const int lc = c0 + seq;
+            if (lc >= a.ncols) return make_double2(0.0, 0.0);
+            int r0 = 0, r1 = a.src_start[1];
 #pragma unroll
-                for (int sidx = 1; sidx < 8; ++sidx)
-                    if (j >= a.src_start[sidx]) {
-                        r0 = a.src_start[sidx];
-                        r1 = a.src_start[sidx + 1];
-                    }
-                const int rows = r1 - r0;
-                const int64_t base = (int64_t)r0 * a.ncols;   // elements before this source
-                cp_async16(dst, &src[base + ((int64_t)(lc / kG) * rows + (j - r0)) * kG + (lc % kG)]);
-            } else {
-                *dst = make_double2(0.0, 0.0);
-            }
-        }
-        cp_async_commit();
+            for (int sidx = 1; sidx < 8; ++sidx)
+                if (j >= a.src_start[sidx]) {
+                    r0 = a.src_start[sidx];
+                    r1 = a.src_start[sidx + 1];
+                }
+            const int64_t base = (int64_t)r0 * a.ncols;   // elements before this source
+            return src[base + ((int64_t)(lc / kG) * (r1 - r0) + (j - r0)) * kG + (lc % kG)];
+        };
     };
-    load_plane(0, sbuf);
 
     // direction-cosine factor per pixel (mesh.py:202-208, transform.py:200)
     for (int e = threadIdx.x; e < C * N; e += kColThreads) {
@@ -309,19 +309,22 @@ __global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const do
     double2 acc[kColE];
 #pragma unroll
     for (int i = 0; i < kColE; ++i) acc[i] = make_double2(0.0, 0.0);
+    double2 pf[kColE];
+    pass_load<LOGN, P0::RL, kColE, kColThreads>(pf, gld_plane(0));
 
     for (int k = 0; k < a.n_w; ++k) {
-        double2 *s = sbuf + (k & 1) * C * STRIDE;
-        __syncthreads();  // plane k-1 is done with the other buffer
-        if (k + 1 < a.n_w) {
-            load_plane(k + 1, sbuf + ((k + 1) & 1) * C * STRIDE);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();  // plane k is in shared memory for every thread
         double2 v[kColE];
-        Passes<LOGN, RL, kColE, kColThreads, true>::run(s, tw, v);
+#pragma unroll
+        for (int i = 0; i < kColE; ++i) v[i] = pf[i];
+        if (k + 1 < a.n_w) pass_load<LOGN, P0::RL, kColE, kColThreads>(pf, gld_plane(k + 1));
+        pass_compute<LOGN, P0::RL, kColE, kColThreads>(1, tw, v);
+        if constexpr (!P0::LAST) {
+            __syncthreads();  // the previous plane's last pass has read sbuf
+            auto sst = [&](int seq, int idx, double2 z) { sbuf[seq * STRIDE + pidx(idx)] = z; };
+            pass_store<LOGN, P0::RL, kColE, kColThreads>(1, v, sst);
+            __syncthreads();
+            smem_passes<LOGN, RLM, kColE, kColThreads, P0::RL>(sbuf, tw, v);
+        }
         // v[kb*R + r] is output row j + r*M of sequence (column) seq
         const double wk = a.w_k[k];
 #pragma unroll

@@ -104,6 +104,29 @@ __device__ __forceinline__ uint32_t axis_weights(double g, int i0, const KParams
     return mask;
 }
 
+// acc[off + b] += (tr, ti) * wv[b], b < W, for the uniform offset off in
+// [0, NW - W]: one static branch per offset keeps acc in registers.
+template <int W, int NW, int O>
+__device__ __forceinline__ void window_fma(double2 (&acc)[NW], int off, double tr, double ti,
+                                           const double *wv) {
+    if constexpr (O + W <= NW) {
+        if (off == O) {
+#pragma unroll
+            for (int b = 0; b < W; b += 2) {
+                const double2 wv2 = *reinterpret_cast<const double2 *>(wv + b);
+                acc[O + b].x = fma(tr, wv2.x, acc[O + b].x);
+                acc[O + b].y = fma(ti, wv2.x, acc[O + b].y);
+                if (b + 1 < W) {
+                    acc[O + b + 1].x = fma(tr, wv2.y, acc[O + b + 1].x);
+                    acc[O + b + 1].y = fma(ti, wv2.y, acc[O + b + 1].y);
+                }
+            }
+        } else {
+            window_fma<W, NW, O + 1>(acc, off, tr, ti, wv);
+        }
+    }
+}
+
 struct SweepArgs {
     const double4 *rec;
     const uint32_t *idx;
@@ -128,7 +151,7 @@ struct WarpStage {
 };
 
 template <int KIND, int S>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 5) k_grid_sweep(SweepArgs a, KParams<S> kp) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 4) k_grid_sweep(SweepArgs a, KParams<S> kp) {
     constexpr int W = 2 * S + 1;
     using St = WarpStage<S>;
     __shared__ __align__(16) St stage_all[kWarpsPerCta];
@@ -154,23 +177,31 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 5) k_grid_sweep(SweepArgs a
     const int64_t colbase = ((int64_t)plane * a.n_groups + (col >> 1)) * a.v_count;
     st.wu[lane][W] = 0.0;
 
-    double2 acc[W];
+    // window: rows base_row .. base_row+NW-1; a record lands at a static
+    // offset 0..D (uniform branch), rows leave D at a time
+    constexpr int D = S <= 3 ? 4 : 2;
+    constexpr int NW = W + D;
+    double2 acc[NW];
 #pragma unroll
-    for (int b = 0; b < W; ++b) acc[b] = make_double2(0.0, 0.0);
+    for (int b = 0; b < NW; ++b) acc[b] = make_double2(0.0, 0.0);
     int base_row = R0 - 2 * S;  // absolute row held in acc[0]
     unsigned cnt = 0;           // cell updates of the records this lane staged
 
-    auto emit_one = [&]() {
-        const int row = base_row;
-        if (row >= R0 && row < R1 && col_ok) {
-            const double s = ((col + row) & 1) ? -1.0 : 1.0;
-            a.out[(colbase + (row - a.v_start)) * kG + (col & 1)] =
-                make_double2(acc[0].x * s, acc[0].y * s);
+    auto emit_block = [&]() {
+        const double s0 = ((col + base_row) & 1) ? -1.0 : 1.0;
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+            const int row = base_row + b;
+            const double s = (b & 1) ? -s0 : s0;
+            if (row >= R0 && row < R1 && col_ok)
+                a.out[(colbase + (row - a.v_start)) * kG + (col & 1)] =
+                    make_double2(acc[b].x * s, acc[b].y * s);
         }
 #pragma unroll
-        for (int b = 0; b < W - 1; ++b) acc[b] = acc[b + 1];
-        acc[W - 1] = make_double2(0.0, 0.0);
-        ++base_row;
+        for (int b = 0; b < NW - D; ++b) acc[b] = acc[b + D];
+#pragma unroll
+        for (int b = NW - D; b < NW; ++b) acc[b] = make_double2(0.0, 0.0);
+        base_row += D;
     };
 
     for (uint32_t cb = beg; cb < end; cb += 32) {
@@ -203,26 +234,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 5) k_grid_sweep(SweepArgs a
         const int nrec = min(32u, end - cb);
         for (int r = 0; r < nrec; ++r) {
             const int2 ij = st.ij[r];
-            while (base_row < ij.y) emit_one();
+            while (ij.y - base_row > D) emit_block();
             int k = col - ij.x;
             k = (unsigned)k < (unsigned)W ? k : W;   // slot W holds weight 0
             const double2 v = st.val[r];
             const double wu = st.wu[r][k];
             const double tr = __dmul_rn(v.x, wu), ti = __dmul_rn(v.y, wu);
-#pragma unroll
-            for (int b = 0; b < W; b += 2) {
-                const double2 wv2 = *reinterpret_cast<const double2 *>(&st.wv[r][b]);
-                acc[b].x = fma(tr, wv2.x, acc[b].x);
-                acc[b].y = fma(ti, wv2.x, acc[b].y);
-                if (b + 1 < W) {
-                    acc[b + 1].x = fma(tr, wv2.y, acc[b + 1].x);
-                    acc[b + 1].y = fma(ti, wv2.y, acc[b + 1].y);
-                }
-            }
+            window_fma<W, NW, 0>(acc, ij.y - base_row, tr, ti, &st.wv[r][0]);
         }
         __syncwarp();
     }
-    while (base_row < R1) emit_one();
+    while (base_row < R1) emit_block();
 
 #pragma unroll
     for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
