@@ -1,0 +1,159 @@
+"""Multi-GPU w-stacking: v-slab decomposition over one process per GPU.
+
+Mirrors the reference's distributed structure:
+  1. time->space exchange of the prepared records to the slab owners, with
+     the +-S halo duplicates (exchange_to_space_order, comms.py:495-547),
+     as one NCCL all-to-all-v;
+  2. per-slab gridding (grid_sector, gridder.py:186-259);
+  3. distributed inverse FFT: row pass on the slab, one all-to-all block
+     transpose per plane (fft2d_slab, transform.py:130-177), column pass on
+     full columns; the reference's transpose back is not needed because the
+     column pass also applies the w screen and stacks the planes
+     (transform.py:192-230);
+  4. gather of the image strips and of the per-column residual norms to the
+     root (assemble_image, transform.py:233-241).
+The reference's reduce phase (comms.py:420-454) is the identity after the
+exchange (pipeline.py:117-122) and has no counterpart here.
+
+Every numeric stage runs through a backend; the product backend is
+``CudaBackend`` (libwsb.so). The collectives are torch.distributed calls,
+NCCL over NVLink on the GPU box. The result is bit-identical to the
+single-GPU image for any number of ranks: records reach each slab in gindex
+order, tiles never straddle slabs, and the norms are summed per column in
+global column order.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from .imager import (FinalImage, _ptr, as_grid_spec, as_kernel_spec, context, grid_slab_device,
+                     partition_1d, prepare_device)
+
+G = L.P_GROUP
+
+
+class CudaBackend:
+    """Stage implementations on the local GPU (libwsb.so)."""
+
+    def __init__(self, device=None):
+        self.ctx = context(device)
+        self.device = torch.device("cuda", self.ctx.device)
+
+    def prepare(self, u, v, w, vis, weight, spec):
+        return prepare_device(u, v, w, vis, weight, spec, device=self.device)
+
+    def route(self, rec, plane, spec, S, R):
+        g = spec.c_struct()
+        n = rec.shape[0]
+        counts = (C.c_int64 * R)()
+        L.check(L.lib().wsb_route_count(self.ctx.handle, C.byref(g), S, R, _ptr(rec), n, counts))
+        counts = [int(c) for c in counts]
+        tot = sum(counts)
+        srec = torch.empty((max(tot, 1), 4), dtype=torch.float64, device=self.device)
+        spl = torch.empty(max(tot, 1), dtype=torch.int32, device=self.device)
+        L.check(L.lib().wsb_route_pack(self.ctx.handle, C.byref(g), S, R, _ptr(rec), _ptr(plane), n,
+                                       _ptr(srec), _ptr(spl), None))
+        return srec[:tot], spl[:tot], counts
+
+    def grid_slab(self, rec, plane, spec, kern, v0, vc):
+        return grid_slab_device(rec, plane, spec, kern, v0, vc)
+
+    def fft_rows(self, grid_p, spec, vc):
+        g = spec.c_struct()
+        L.check(L.lib().wsb_fft_rows(self.ctx.handle, C.byref(g), int(vc), _ptr(grid_p), 0, spec.n_w))
+
+    def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng):
+        g = spec.c_struct()
+        strip = torch.empty((spec.n_v, ng * G), dtype=torch.float64, device=self.device)
+        partials = torch.empty((ng * G, 2), dtype=torch.float64, device=self.device)
+        rows = (C.c_int32 * len(src_rows))(*src_rows)
+        L.check(L.lib().wsb_fft_cols_stack(self.ctx.handle, C.byref(g), len(src_rows), rows, int(g0),
+                                           int(ng), _ptr(tgrid), _ptr(strip), _ptr(partials)))
+        return strip, partials
+
+
+def _a2a(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group):
+    dist.all_to_all_single(out, inp, output_split_sizes=list(out_splits),
+                           input_split_sizes=list(in_splits), group=group)
+
+
+def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None, root: int = 0):
+    """Dirty image of the union of every rank's records. Each rank passes its
+    own time partition (records in gindex order, rank r holding the r-th
+    contiguous block, as visdata.partition_time_ordered produces).
+
+    Returns (FinalImage on ``root``, None elsewhere; diag dict on every rank)."""
+    spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
+    be = backend or CudaBackend()
+    R = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    dev = be.device
+    S = kern.half_support
+    n_groups = spec.n_u // G
+    if R > spec.n_v or R > n_groups:
+        raise ValueError(f"{R} ranks exceed the mesh ({spec.n_v} rows, {n_groups} column groups)")
+
+    # 1. prepare + time->space exchange ------------------------------------
+    rec, plane = be.prepare(u, v, w, vis, weight, spec)
+    srec, spl, counts = be.route(rec, plane, spec, S, R)
+    c_send = torch.tensor(counts, dtype=torch.int64, device=dev)
+    c_recv = torch.empty(R, dtype=torch.int64, device=dev)
+    dist.all_to_all_single(c_recv, c_send, group=group)
+    recv_counts = [int(x) for x in c_recv.tolist()]
+    m = sum(recv_counts)
+    rrec = torch.empty((m, 4), dtype=torch.float64, device=dev)
+    rpl = torch.empty(m, dtype=torch.int32, device=dev)
+    _a2a(rrec, srec.contiguous(), recv_counts, counts, group)
+    _a2a(rpl, spl.contiguous(), recv_counts, counts, group)
+
+    # 2. grid this rank's slab ----------------------------------------------
+    slabs = [partition_1d(spec.n_v, R, d) for d in range(R)]
+    v0, vc = slabs[r]
+    grid_p, updates = be.grid_slab(rrec, rpl, spec, kern, v0, vc)
+
+    # 3. row FFT, per-plane block transpose, column FFT + w stack ------------
+    be.fft_rows(grid_p, spec, vc)
+    cols = [partition_1d(n_groups, R, d) for d in range(R)]
+    g0, ng = cols[r]
+    gp = grid_p.reshape(spec.n_w, -1)                       # float64 view, P layout per plane
+    in_splits = [ng_d * vc * G * 2 for _, ng_d in cols]     # float64 elements to each rank
+    out_splits = [ng * vc_s * G * 2 for _, vc_s in slabs]   # from each source slab
+    tgrid = torch.empty((spec.n_w, ng * spec.n_v * G * 2), dtype=torch.float64, device=dev)
+    for k in range(spec.n_w):
+        _a2a(tgrid[k], gp[k], out_splits, in_splits, group)
+    strip, partials = be.fft_cols_stack(tgrid, spec, [vc_s for _, vc_s in slabs], g0, ng)
+
+    # 4. gather to the root ----------------------------------------------------
+    upd = torch.tensor([updates], dtype=torch.int64, device=dev)
+    dist.all_reduce(upd, group=group)
+    maxc = max(ng_d for _, ng_d in cols) * G
+    pad = torch.zeros((spec.n_v, maxc), dtype=torch.float64, device=dev)
+    pad[:, : ng * G] = strip
+    ppad = torch.zeros((maxc, 2), dtype=torch.float64, device=dev)
+    ppad[: ng * G] = partials
+    strips = [torch.empty_like(pad) for _ in range(R)]
+    parts = [torch.empty_like(ppad) for _ in range(R)]
+    dist.all_gather(strips, pad, group=group)
+    dist.all_gather(parts, ppad, group=group)
+    diag = {"grid_updates": int(upd.item()), "records_local": int(rec.shape[0]),
+            "records_slab": m, "exchange_bytes": int(sum(counts) - counts[r]) * 36}
+    if r != root:
+        return None, diag
+    pix = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, device=dev)
+    col_parts = []
+    for d, (g0_d, ng_d) in enumerate(cols):
+        pix[:, g0_d * G:(g0_d + ng_d) * G] = strips[d][:, : ng_d * G]
+        col_parts.append(parts[d][: ng_d * G])
+    p = torch.cat(col_parts).cpu().numpy()
+    # sequential sum in global column order (cumsum is left to right): the
+    # same association as the single-GPU path, for any R
+    im_sq = float(p[:, 0].cumsum()[-1])
+    re_sq = float(p[:, 1].cumsum()[-1])
+    img = FinalImage(spec, pix.cpu().numpy(), im_sq ** 0.5, re_sq ** 0.5)
+    diag.update({"imag_residual_norm": img.imag_residual_norm, "real_norm": img.real_norm})
+    return img, diag

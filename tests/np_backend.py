@@ -1,0 +1,80 @@
+"""NumPy stand-in for distributed.CudaBackend, built on the oracle, so the
+multi-rank host logic (exchange splits, transposes, gathers) can be tested
+with gloo on CPU. Test infrastructure only: it follows the same stage
+contracts as include/wsb.h (P layout, transposed slab layout, per-column
+norm partials)."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import wstack_oracle as O
+
+G = 2
+
+
+class NumpyBackend:
+    device = torch.device("cpu")
+
+    def prepare(self, u, v, w, vis, weight, spec):
+        p = O.prepare(np.asarray(u), np.asarray(v), np.asarray(w), np.zeros(len(u), np.uint32),
+                      np.asarray(vis), np.asarray(weight), spec.n_u, spec.n_v, spec.n_w)
+        rec = np.stack([p["gu"], p["gv"], p["value"].real, p["value"].imag], axis=1)
+        return torch.from_numpy(rec), torch.from_numpy(p["plane"].astype(np.int32))
+
+    def route(self, rec, plane, spec, S, R):
+        r, pl = rec.numpy(), plane.numpy()
+        outs, outp, counts = [], [], []
+        for v0, vc in O.slabs(spec.n_v, R):
+            m = O.halo_mask(r[:, 1], S, v0, vc)
+            outs.append(r[m])
+            outp.append(pl[m])
+            counts.append(int(m.sum()))
+        return (torch.from_numpy(np.concatenate(outs)), torch.from_numpy(np.concatenate(outp)),
+                counts)
+
+    def grid_slab(self, rec, plane, spec, kern, v0, vc):
+        r = rec.numpy()
+        batch = {"gu": r[:, 0], "gv": r[:, 1], "value": r[:, 2] + 1j * r[:, 3],
+                 "plane": plane.numpy().astype(np.uint32), "v_start": v0, "v_count": vc}
+        kind = O.KIND_GAUSSIAN if kern.kind == "gaussian" else O.KIND_KAISER_BESSEL
+        grid, upd = O.grid_slab(batch, spec.n_u, spec.n_w, kind, kern.half_support, kern.shape_param)
+        grid = grid * O.checker_sign(spec.n_u, v0, vc)[None]
+        # (plane, row, col) -> P layout (plane, col/G, row, col%G)
+        p = grid.reshape(spec.n_w, vc, spec.n_u // G, G).transpose(0, 2, 1, 3)
+        p = np.ascontiguousarray(p)
+        return torch.from_numpy(p.view(np.float64).reshape(spec.n_w, spec.n_u // G, vc, G, 2)), upd
+
+    def fft_rows(self, grid_p, spec, vc):
+        a = grid_p.numpy().view(np.complex128).reshape(spec.n_w, spec.n_u // G, vc, G)
+        nat = a.transpose(0, 2, 1, 3).reshape(spec.n_w, vc, spec.n_u)
+        f = np.fft.ifft(nat, axis=-1) * spec.n_u               # unnormalised inverse
+        a[...] = f.reshape(spec.n_w, vc, spec.n_u // G, G).transpose(0, 2, 1, 3)
+
+    def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng):
+        t = tgrid.numpy().view(np.complex128).reshape(spec.n_w, -1)
+        ncols = ng * G
+        full = np.empty((spec.n_w, spec.n_v, ncols), np.complex128)
+        off, r0 = 0, 0
+        for rows in src_rows:
+            blk = t[:, off:off + ng * rows * G].reshape(spec.n_w, ng, rows, G)
+            full[:, r0:r0 + rows] = blk.transpose(0, 2, 1, 3).reshape(spec.n_w, rows, ncols)
+            off += ng * rows * G
+            r0 += rows
+        planes = np.fft.ifft(full, axis=1) * spec.n_v / (spec.n_u * spec.n_v)
+        c0 = g0 * G
+        cols = np.arange(c0, c0 + ncols, dtype=np.float64) - spec.n_u // 2
+        rowsv = np.arange(spec.n_v, dtype=np.float64) - spec.n_v // 2
+        l = np.broadcast_to(cols * spec.cell_size_lm, (spec.n_v, ncols))
+        m = np.broadcast_to((rowsv * spec.cell_size_lm)[:, None], (spec.n_v, ncols))
+        n = np.sqrt(1.0 - l * l - m * m)
+        acc = np.zeros((spec.n_v, ncols), np.complex128)
+        for k in range(spec.n_w):
+            wk = O.plane_w_native(k, spec.n_w, spec.w_min_native, spec.w_max_native)
+            p = planes[k] if wk == 0.0 else planes[k] * np.exp(2j * np.pi * wk * (n - 1.0))
+            acc = acc + p
+        acc = acc / spec.n_w * n
+        strip = np.ascontiguousarray(acc.real)
+        partials = np.stack([(acc.imag ** 2).sum(axis=0), (acc.real ** 2).sum(axis=0)], axis=1)
+        return torch.from_numpy(strip), torch.from_numpy(np.ascontiguousarray(partials))

@@ -1,0 +1,140 @@
+"""Multi-slab CUDA stages. (1) R virtual ranks on one GPU, the collectives
+replaced by tensor slicing: the slab pipeline must reproduce the single-GPU
+image bit for bit. (2) With >= 2 GPUs, the real NCCL driver under
+torch.multiprocessing."""
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import chunk_from, rel_l2
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+ROOT = Path(__file__).resolve().parents[1]
+TESTS = Path(__file__).resolve().parent
+
+
+@pytest.fixture(scope="module")
+def W():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2504_00959_b200 as W
+    return W
+
+
+def _parts(t, R):
+    from oracle import wstack_oracle as O
+    sl = np.unique(t)
+    out = []
+    for r in range(R):
+        s0, sc = O.partition_1d(len(sl), R, r)
+        out.append((np.searchsorted(t, sl[s0], "left"), np.searchsorted(t, sl[s0 + sc - 1], "right")))
+    return out
+
+
+def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R):
+    from paper_2504_00959_b200.distributed import CudaBackend
+    be = CudaBackend(0)
+    G = 2
+    S = kern.half_support
+    slabs = [W.partition_1d(spec.n_v, R, d) for d in range(R)]
+    cols = [W.partition_1d(spec.n_u // G, R, d) for d in range(R)]
+    sends = []
+    for lo, hi in _parts(t, R):
+        rec, pl = be.prepare(u[lo:hi], v[lo:hi], w[lo:hi], vis[lo:hi], wt[lo:hi], spec)
+        sends.append(be.route(rec, pl, spec, S, R))
+    grids, upd = [], 0
+    for d, (v0, vc) in enumerate(slabs):
+        recs, pls = [], []
+        for srec, spl, counts in sends:            # sources in rank (= gindex) order
+            off = sum(counts[:d])
+            recs.append(srec[off:off + counts[d]])
+            pls.append(spl[off:off + counts[d]])
+        gp, up = be.grid_slab(torch.cat(recs).contiguous(), torch.cat(pls).contiguous(), spec, kern,
+                              v0, vc)
+        be.fft_rows(gp, spec, vc)
+        grids.append(gp)
+        upd += up
+    pix = np.empty((spec.n_v, spec.n_u))
+    parts = []
+    for d, (g0, ng) in enumerate(cols):
+        chunks = [gp.reshape(spec.n_w, spec.n_u // G, -1)[:, g0:g0 + ng].reshape(spec.n_w, -1)
+                  for gp in grids]
+        tgrid = torch.cat(chunks, dim=1).contiguous()
+        strip, partials = be.fft_cols_stack(tgrid, spec, [vc for _, vc in slabs], g0, ng)
+        pix[:, g0 * G:(g0 + ng) * G] = strip.cpu().numpy()
+        parts.append(partials.cpu().numpy())
+    p = np.concatenate(parts)
+    return pix, np.sqrt([p[:, 0].cumsum()[-1], p[:, 1].cumsum()[-1]]), upd
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
+def test_virtual_ranks_bit_identical(W, golden_image, R):
+    g = golden_image
+    n_u, n_v, n_w, S, _ = (int(x) for x in g["wide_cfg"])
+    cell, wmin, wmax, shape = (float(x) for x in g["wide_fcfg"])
+    spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
+    kern = W.KernelSpec("gaussian", S, shape)
+    u, v, w, t, vis, wt = chunk_from(g, "wide_in_")
+    ref, diag = W.image(u, v, w, t, vis, wt, spec, kern)
+    pix, norms, upd = _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R)
+    assert upd == diag["grid_updates"]
+    assert pix.tobytes() == ref.pixels.tobytes()
+    assert norms[0] == ref.imag_residual_norm and norms[1] == ref.real_norm
+    assert rel_l2(pix, g["wide_pixels"]) <= 1e-10
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _nccl_worker(rank, world, port, outdir):
+    sys.path[:0] = [str(ROOT), str(TESTS)]
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        import paper_2504_00959_b200 as W
+        from paper_2504_00959_b200.distributed import image_distributed
+        g = np.load(TESTS / "golden" / "image.npz")
+        n_u, n_v, n_w, S, _ = (int(x) for x in g["wide_cfg"])
+        cell, wmin, wmax, shape = (float(x) for x in g["wide_fcfg"])
+        spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
+        kern = W.KernelSpec("gaussian", S, shape)
+        u, v, w, t, vis, wt = (g[f"wide_in_{k}"] for k in ("u", "v", "w", "time_index", "vis", "weight"))
+        lo, hi = _parts(t, world)[rank]
+        dev = torch.device("cuda", rank)
+        img, diag = image_distributed(*(torch.from_numpy(np.ascontiguousarray(a[lo:hi])).to(dev)
+                                        for a in (u, v, w, vis, wt)), spec, kern)
+        if rank == 0:
+            np.savez(Path(outdir) / "out.npz", pixels=img.pixels, updates=np.array([diag["grid_updates"]]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_multi_gpu_matches_single(W, golden_image, tmp_path):
+    world = min(torch.cuda.device_count(), 4)
+    if world < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch.multiprocessing as mp
+    mp.spawn(_nccl_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    out = np.load(tmp_path / "out.npz")
+    g = golden_image
+    n_u, n_v, n_w, S, _ = (int(x) for x in g["wide_cfg"])
+    cell, wmin, wmax, shape = (float(x) for x in g["wide_fcfg"])
+    spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
+    ref, diag = W.image(*chunk_from(g, "wide_in_"), spec, W.KernelSpec("gaussian", S, shape))
+    assert int(out["updates"][0]) == diag["grid_updates"]
+    assert out["pixels"].tobytes() == ref.pixels.tobytes()
