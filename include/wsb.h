@@ -142,18 +142,21 @@ int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int
 /* grid_sector (gridder.py:186-259) for the slab rows [v_start, v_start+v_count):
  * buckets the m records by (plane, 32-column strip, anchor row) (counting
  * sort, record order inside a bucket), grids them with the convolution kernel
- * in a register-window sweep and writes the slab in P layout
- * (grid_p: complex128[n_w][n_u/G][v_count][G], sign applied). grid_updates
- * (host, nullable) receives the number of cell updates; synchronises if given. */
+ * in a register-window sweep and writes the slab in the strip layout
+ * (grid_s: complex128[n_w][ceil(n_u/32)][v_count][32], sign applied; every
+ * row of a 32-column strip is one 512-byte run). grid_updates (host,
+ * nullable) receives the number of cell updates; synchronises if given. */
 int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
                   int32_t v_start, int32_t v_count,
                   const double *rec, const uint32_t *plane, int64_t m,
-                  double *grid_p, int64_t *grid_updates);
+                  double *grid_s, int64_t *grid_updates);
 
 /* Row pass of the inverse 2D FFT (transform.py:151 / fft1d inverse) on planes
- * [plane_lo, plane_hi) of a P-layout slab, in place. Unnormalised. */
+ * [plane_lo, plane_hi): strip-layout slab in, P-layout slab out (out of
+ * place; P groups column pairs so one destination's columns are contiguous
+ * for the transpose). Unnormalised. */
 int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count,
-                 double *grid_p, int32_t plane_lo, int32_t plane_hi);
+                 const double *grid_s, double *grid_p, int32_t plane_lo, int32_t plane_hi);
 
 /* Column pass + w correction + stacking (transform.py:162-175, 192-230):
  * input tgrid holds, per plane, this rank's column groups [g0, g0+ng) for all
@@ -167,10 +170,11 @@ int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
                        const int32_t *src_rows_host, int32_t g0, int32_t ng,
                        const double *tgrid, double *image_strip, double *norm_partials);
 
-/* Debug / parity: P-layout slab -> natural (plane, row, col) complex128 with
- * the checkerboard sign removed (the grid_all output layout, mesh.py:131-146). */
+/* Debug / parity: strip-layout slab -> natural (plane, row, col) complex128
+ * with the checkerboard sign removed (the grid_all output layout,
+ * mesh.py:131-146). */
 int wsb_grid_unpack(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t v_count,
-                    const double *grid_p, double *grid_out);
+                    const double *grid_s, double *grid_out);
 
 /* Debug / parity: the bucketing of the last wsb_grid_slab / wsb_image_device
  * call: record indices in bucket order and the n_buckets+1 bucket offsets,

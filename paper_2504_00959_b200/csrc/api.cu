@@ -95,7 +95,8 @@ __global__ void k_unpack(const double2 *p, double2 *out, int n_w, int n_u, int v
     const int64_t t = e / n_u;
     const int j = t % v_count;
     const int k = t / v_count;
-    double2 z = p[(((int64_t)k * (n_u / kG) + i / kG) * v_count + j) * kG + i % kG];
+    // strip layout [plane][col/32][row][col%32]
+    double2 z = p[(((int64_t)k * ((n_u + 31) / 32) + i / 32) * v_count + j) * 32 + i % 32];
     const double s = ((i + v_start + j) & 1) ? -1.0 : 1.0;
     out[e] = make_double2(z.x * s, z.y * s);
 }
@@ -252,14 +253,15 @@ int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern, in
     return WSB_OK;
 }
 
-int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count, double *grid_p,
-                 int32_t plane_lo, int32_t plane_hi) {
+int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count, const double *grid_s,
+                 double *grid_p, int32_t plane_lo, int32_t plane_hi) {
     if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
     WSB_TRY(validate_grid(grid));
     if (plane_lo < 0 || plane_hi > grid->n_w || plane_lo > plane_hi)
         return fail(WSB_EINVAL, "plane range outside [0, n_w]");
+    if (grid_s == grid_p) return fail(WSB_EINVAL, "the row pass is out of place");
     WSB_TRY(set_device(ctx));
-    return fft_rows(ctx, grid, v_count, grid_p, plane_lo, plane_hi);
+    return fft_rows(ctx, grid, v_count, grid_s, grid_p, plane_lo, plane_hi);
 }
 
 int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
@@ -321,13 +323,15 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
     ctx->launches = 0;
     cudaEvent_t *ev = ctx->timing.ev;
     const int n_u = grid->n_u, n_v = grid->n_v, n_w = grid->n_w;
-    double *rec, *gp, *partials;
+    double *rec, *gs, *gp, *partials;
     uint32_t *plane;
     unsigned long long *upd;
     const int64_t nn = std::max<int64_t>(n, 1);
     WSB_TRY(ensure(ctx, kSlotRec, 32 * (size_t)nn, (void **)&rec));
     WSB_TRY(ensure(ctx, kSlotPlane, 4 * (size_t)nn, (void **)&plane));
-    WSB_TRY(ensure(ctx, kSlotGrid, (size_t)16 * n_w * n_u * n_v, (void **)&gp));
+    // strip layout (gridder output) and P layout (row-pass output)
+    WSB_TRY(ensure(ctx, kSlotGrid, (size_t)16 * n_w * ceil_div(n_u, 32) * 32 * n_v, (void **)&gs));
+    WSB_TRY(ensure(ctx, kSlotGridP, (size_t)16 * n_w * n_u * n_v, (void **)&gp));
     WSB_TRY(ensure(ctx, kSlotStrip, sizeof(double) * (2 * (size_t)n_u + 4), (void **)&partials));
     WSB_TRY(ensure(ctx, kSlotU64, 64, (void **)&upd));
     const double *tw;
@@ -342,9 +346,9 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
     WSB_TRY(bucket_rows(ctx, grid, kern->half_support, 0, n_v, rec, plane, n, &bk));
     const int64_t n_entries = bk.n_entries;
     WSB_CUDA_TRY(cudaEventRecord(ev[2], ctx->stream));
-    WSB_TRY(grid_sweep(ctx, grid, kern, 0, n_v, rec, bk, gp, upd));
+    WSB_TRY(grid_sweep(ctx, grid, kern, 0, n_v, rec, bk, gs, upd));
     WSB_CUDA_TRY(cudaEventRecord(ev[3], ctx->stream));
-    WSB_TRY(fft_rows(ctx, grid, n_v, gp, 0, n_w));
+    WSB_TRY(fft_rows(ctx, grid, n_v, gs, gp, 0, n_w));
     WSB_CUDA_TRY(cudaEventRecord(ev[4], ctx->stream));
     const int32_t rows[1] = {n_v};
     WSB_TRY(fft_cols_stack(ctx, grid, 1, rows, 0, n_u / kG, gp, image_out, partials));

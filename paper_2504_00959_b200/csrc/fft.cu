@@ -31,6 +31,40 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -(a.y * b.y)), fma(a.x, b.y, a.y * b.x));
 }
 
+// (cos(pi x), sin(pi x)) for |x| < 2^30: x = t/2 + r with t = rint(2x),
+// |r| <= 1/4, then Taylor polynomials of sin(pi r)/r (degree 16) and
+// cos(pi r) (degree 16) in r^2, truncation < 1e-18; about a third of the
+// instructions of the library sincospi, a few ulp from it.
+__device__ __forceinline__ double2 cis_pi(double x) {
+    const double t = rint(2.0 * x);
+    const double r = fma(-0.5, t, x);
+    const double r2 = r * r;
+    double s = -2.2948428997269873e-08;
+    s = fma(s, r2, 7.952054001475513e-07);
+    s = fma(s, r2, -2.1915353447830217e-05);
+    s = fma(s, r2, 0.00046630280576761255);
+    s = fma(s, r2, -0.0073704309457143504);
+    s = fma(s, r2, 0.08214588661112823);
+    s = fma(s, r2, -0.5992645293207921);
+    s = fma(s, r2, 2.5501640398773455);
+    s = fma(s, r2, -5.16771278004997);
+    s = fma(s, r2, 3.141592653589793);
+    s *= r;
+    double c = 4.303069587032947e-06;
+    c = fma(c, r2, -0.0001046381049248457);
+    c = fma(c, r2, 0.0019295743094039231);
+    c = fma(c, r2, -0.02580689139001406);
+    c = fma(c, r2, 0.2353306303588932);
+    c = fma(c, r2, -1.3352627688545895);
+    c = fma(c, r2, 4.0587121264167685);
+    c = fma(c, r2, -4.934802200544679);
+    c = fma(c, r2, 1.0);
+    const int q = (int)(long long)t & 3;
+    const double cs = (q & 1) ? s : c;
+    const double sn = (q & 1) ? c : s;
+    return make_double2((q == 1 || q == 2) ? -cs : cs, (q >= 2) ? -sn : sn);
+}
+
 // cos/sin(2 pi u / 16), u = 0..7
 __device__ __forceinline__ double2 root16(int u) {
     switch (u) {
@@ -197,7 +231,14 @@ __device__ __forceinline__ void smem_passes(double2 *s, const double2 *tw, doubl
 // ---------------------------------------------------------------------------
 // row pass: global -> registers -> (shared memory passes) -> global
 // ---------------------------------------------------------------------------
-constexpr int kRowThreads = 256;
+// one row per CTA at N >= 2048 (4 CTAs per SM of 128 threads at N = 2048):
+// small independent CTAs keep the per-pass barriers of different rows out
+// of phase, so one CTA's HBM latency overlaps another's transform
+template <int LOGN>
+struct RowCfg {
+    static constexpr int T = ((1 << LOGN) / 16 > 128) ? (1 << LOGN) / 16 : 128;
+    static constexpr int MINB = T <= 128 ? 4 : 2;
+};
 constexpr int kRowE = 16;
 constexpr int kRowRL = 4;
 
@@ -205,45 +246,52 @@ constexpr int kRowRL = 4;
 // (32-byte sectors, 16 loads in flight per thread) and the last pass writes
 // its outputs straight back: shared memory only carries the inner exchanges.
 template <int LOGN>
-__global__ void __launch_bounds__(kRowThreads, 2)
-    k_fft_rows(double2 *__restrict__ grid, int n_groups, int v_count, int plane_lo,
-               const double2 *__restrict__ tw) {
+__global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
+    k_fft_rows(const double2 *__restrict__ in, double2 *__restrict__ out, int n_strips,
+               int n_groups, int v_count, int plane_lo, const double2 *__restrict__ tw) {
     constexpr int N = 1 << LOGN;
-    constexpr int NSEQ = kRowThreads * kRowE / N;  // rows per CTA
+    constexpr int RT = RowCfg<LOGN>::T;
+    constexpr int NSEQ = RT * kRowE / N;  // rows per CTA
     constexpr int STRIDE = Seq<LOGN>::STRIDE;
     using P0 = Plan<LOGN, kRowRL, 0>;
     extern __shared__ __align__(16) double2 s[];
     const int j0 = blockIdx.x * NSEQ;
     const int64_t plane = plane_lo + blockIdx.y;
-    // P[plane][col/G][row][col%G]
-    auto gaddr = [&](int seq, int col) -> int64_t {
-        return ((plane * n_groups + col / kG) * v_count + j0 + seq) * kG + (col % kG);
-    };
+    // in: strip layout [plane][col/32][row][col%32] (512-byte row runs)
     auto gld = [&](int seq, int col) {
-        return j0 + seq < v_count ? grid[gaddr(seq, col)] : make_double2(0.0, 0.0);
+        return j0 + seq < v_count
+                   ? in[((plane * n_strips + col / 32) * v_count + j0 + seq) * 32 + (col % 32)]
+                   : make_double2(0.0, 0.0);
     };
+    // out: P[plane][col/G][row][col%G] (the column pass and the transpose read it)
     auto gst = [&](int seq, int col, double2 z) {
-        if (j0 + seq < v_count) grid[gaddr(seq, col)] = z;
+        if (j0 + seq < v_count)
+            out[((plane * n_groups + col / kG) * v_count + j0 + seq) * kG + (col % kG)] = z;
     };
     double2 v[kRowE];
-    pass_load<LOGN, P0::RL, kRowE, kRowThreads>(v, gld);
-    pass_compute<LOGN, P0::RL, kRowE, kRowThreads>(1, tw, v);
+    pass_load<LOGN, P0::RL, kRowE, RT>(v, gld);
+    pass_compute<LOGN, P0::RL, kRowE, RT>(1, tw, v);
     if constexpr (P0::LAST) {
-        pass_store<LOGN, P0::RL, kRowE, kRowThreads>(1, v, gst);
+        pass_store<LOGN, P0::RL, kRowE, RT>(1, v, gst);
     } else {
         auto sst = [&](int seq, int idx, double2 z) { s[seq * STRIDE + pidx(idx)] = z; };
-        pass_store<LOGN, P0::RL, kRowE, kRowThreads>(1, v, sst);
+        pass_store<LOGN, P0::RL, kRowE, RT>(1, v, sst);
         __syncthreads();
-        smem_passes<LOGN, kRowRL, kRowE, kRowThreads, P0::RL>(s, tw, v);
+        smem_passes<LOGN, kRowRL, kRowE, RT, P0::RL>(s, tw, v);
         constexpr int RLL = kRowRL;  // the last pass is always a full-radix pass here
-        pass_store<LOGN, RLL, kRowE, kRowThreads>(N >> RLL, v, gst);
+        pass_store<LOGN, RLL, kRowE, RT>(N >> RLL, v, gst);
     }
 }
 
 // ---------------------------------------------------------------------------
 // column pass + w correction + stacking
 // ---------------------------------------------------------------------------
-constexpr int kColThreads = 512;
+// one column per CTA at N >= 2048: two 256-thread CTAs per SM at N = 2048
+template <int LOGN>
+struct ColCfg {
+    static constexpr int T = ((1 << LOGN) / 8 > 256) ? (1 << LOGN) / 8 : 256;
+    static constexpr int MINB = T <= 256 ? 2 : 1;
+};
 constexpr int kColE = 8;
 constexpr int kColRL = 3;
 
@@ -263,9 +311,11 @@ struct ColArgs {
 // its outputs in registers where the phase screen is applied and the planes
 // are summed.
 template <int LOGN>
-__global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const double2 *__restrict__ tw) {
+__global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
+    k_fft_cols(ColArgs a, const double2 *__restrict__ tw) {
+    constexpr int CT = ColCfg<LOGN>::T;
     constexpr int N = 1 << LOGN;                 // n_v
-    constexpr int C = kColThreads * kColE / N;   // columns per CTA
+    constexpr int C = CT * kColE / N;   // columns per CTA
     constexpr int STRIDE = Seq<LOGN>::STRIDE;
     constexpr int RLM = LOGN < kColRL ? LOGN : kColRL;
     using P0 = Plan<LOGN, RLM, 0>;
@@ -278,13 +328,14 @@ __global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const do
     const int c0 = blockIdx.x * C;                 // first local column
     const int64_t plane_elems = (int64_t)(a.ncols / kG) * N * kG;
 
-    // element (row j, local column c0+seq) of plane k in the transposed slab
-    // layout [s][g][row - row_start_s][x]
-    auto gld_plane = [&](int k) {
-        const double2 *src = a.tgrid + (int64_t)k * plane_elems;
-        return [=](int seq, int j) {
+    // In-plane offset of each first-pass input of this thread (the same for
+    // every plane): element (row j, local column c0+seq) in the transposed
+    // slab layout [s][g][row - row_start_s][x]; -1 past the last column.
+    int off[kColE];
+    {
+        auto offset = [&](int seq, int j) -> double2 {
             const int lc = c0 + seq;
-            if (lc >= a.ncols) return make_double2(0.0, 0.0);
+            if (lc >= a.ncols) return make_double2(__hiloint2double(-1, 0), 0.0);
             int r0 = 0, r1 = a.src_start[1];
 #pragma unroll
             for (int sidx = 1; sidx < 8; ++sidx)
@@ -292,13 +343,22 @@ __global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const do
                     r0 = a.src_start[sidx];
                     r1 = a.src_start[sidx + 1];
                 }
-            const int64_t base = (int64_t)r0 * a.ncols;   // elements before this source
-            return src[base + ((int64_t)(lc / kG) * (r1 - r0) + (j - r0)) * kG + (lc % kG)];
+            const int o = r0 * a.ncols + ((lc / kG) * (r1 - r0) + (j - r0)) * kG + (lc % kG);
+            return make_double2(__hiloint2double(o, 0), 0.0);
         };
+        double2 t[kColE];
+        pass_load<LOGN, P0::RL, kColE, CT>(t, offset);
+#pragma unroll
+        for (int i = 0; i < kColE; ++i) off[i] = __double2hiint(t[i].x);
+    }
+    auto gld_plane = [&](int k, double2 (&dst)[kColE]) {
+        const double2 *src = a.tgrid + (int64_t)k * plane_elems;
+#pragma unroll
+        for (int i = 0; i < kColE; ++i) dst[i] = off[i] >= 0 ? src[off[i]] : make_double2(0.0, 0.0);
     };
 
     // direction-cosine factor per pixel (mesh.py:202-208, transform.py:200)
-    for (int e = threadIdx.x; e < C * N; e += kColThreads) {
+    for (int e = threadIdx.x; e < C * N; e += CT) {
         const int cc = e / N, j = e % N;
         const int gi = a.g0 * kG + c0 + cc;
         const double l = (double)(gi - a.n_u / 2) * a.cell;
@@ -310,35 +370,33 @@ __global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const do
 #pragma unroll
     for (int i = 0; i < kColE; ++i) acc[i] = make_double2(0.0, 0.0);
     double2 pf[kColE];
-    pass_load<LOGN, P0::RL, kColE, kColThreads>(pf, gld_plane(0));
+    gld_plane(0, pf);
 
     for (int k = 0; k < a.n_w; ++k) {
         double2 v[kColE];
 #pragma unroll
         for (int i = 0; i < kColE; ++i) v[i] = pf[i];
-        if (k + 1 < a.n_w) pass_load<LOGN, P0::RL, kColE, kColThreads>(pf, gld_plane(k + 1));
-        pass_compute<LOGN, P0::RL, kColE, kColThreads>(1, tw, v);
+        if (k + 1 < a.n_w) gld_plane(k + 1, pf);
+        pass_compute<LOGN, P0::RL, kColE, CT>(1, tw, v);
         if constexpr (!P0::LAST) {
             __syncthreads();  // the previous plane's last pass has read sbuf
             auto sst = [&](int seq, int idx, double2 z) { sbuf[seq * STRIDE + pidx(idx)] = z; };
-            pass_store<LOGN, P0::RL, kColE, kColThreads>(1, v, sst);
+            pass_store<LOGN, P0::RL, kColE, CT>(1, v, sst);
             __syncthreads();
-            smem_passes<LOGN, RLM, kColE, kColThreads, P0::RL>(sbuf, tw, v);
+            smem_passes<LOGN, RLM, kColE, CT, P0::RL>(sbuf, tw, v);
         }
         // v[kb*R + r] is output row j + r*M of sequence (column) seq
         const double wk = a.w_k[k];
 #pragma unroll
         for (int kb = 0; kb < NB; ++kb) {
-            const int b = threadIdx.x + kb * kColThreads;
+            const int b = threadIdx.x + kb * CT;
             const int seq = b / M, j = b % M;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 double2 z = v[kb * R + r];
                 if (wk != 0.0) {  // transform.py:196-198
                     const double n = nbuf[seq * N + j + r * M];
-                    double sn, cs;
-                    sincospi(2.0 * wk * (n - 1.0), &sn, &cs);
-                    z = cmul(z, make_double2(cs, sn));
+                    z = cmul(z, cis_pi(2.0 * wk * (n - 1.0)));
                 }
                 acc[kb * R + r] = cadd(acc[kb * R + r], z);
             }
@@ -354,7 +412,7 @@ __global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const do
     double2 *sq = sbuf + C * STRIDE;            // (im^2, re^2) per pixel
 #pragma unroll
     for (int kb = 0; kb < NB; ++kb) {
-        const int b = threadIdx.x + kb * kColThreads;
+        const int b = threadIdx.x + kb * CT;
         const int seq = b / M, j = b % M;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -373,20 +431,20 @@ __global__ void __launch_bounds__(kColThreads, 1) k_fft_cols(ColArgs a, const do
     }
     __syncthreads();
     // image rows: the C columns of a row are contiguous in the strip
-    for (int e = threadIdx.x; e < C * N; e += kColThreads) {
+    for (int e = threadIdx.x; e < C * N; e += CT) {
         const int cc = e % C, row = e / C;
         if (c0 + cc < a.ncols) a.strip[(int64_t)row * a.ncols + c0 + cc] = pix[cc * STRIDE + pidx(row)].x;
     }
     // per-column pairwise tree over the N rows
     for (int half = N / 2; half > 0; half >>= 1) {
-        for (int e = threadIdx.x; e < C * half; e += kColThreads) {
+        for (int e = threadIdx.x; e < C * half; e += CT) {
             const int cc = e / half, i = e % half;
             double2 *p = sq + cc * STRIDE;
             p[i] = make_double2(p[i].x + p[i + half].x, p[i].y + p[i + half].y);
         }
         __syncthreads();
     }
-    for (int cc = threadIdx.x; cc < C; cc += kColThreads)
+    for (int cc = threadIdx.x; cc < C; cc += CT)
         if (c0 + cc < a.ncols) {
             a.partials[2 * (c0 + cc) + 0] = sq[cc * STRIDE].x;
             a.partials[2 * (c0 + cc) + 1] = sq[cc * STRIDE].y;
@@ -402,15 +460,16 @@ __global__ void k_twiddles(double2 *tw, int n) {
 }
 
 template <int LOGN>
-int launch_rows(wsb_ctx *ctx, double2 *grid, int n_groups, int v_count, int plo, int phi,
-                const double2 *tw) {
+int launch_rows(wsb_ctx *ctx, const double2 *in, double2 *out, int n_strips, int n_groups,
+                int v_count, int plo, int phi, const double2 *tw) {
     constexpr int N = 1 << LOGN;
-    constexpr int NSEQ = kRowThreads * kRowE / N;
+    constexpr int RT = RowCfg<LOGN>::T;
+    constexpr int NSEQ = RT * kRowE / N;
     const size_t smem = sizeof(double2) * NSEQ * Seq<LOGN>::STRIDE;
     WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     dim3 grd(ceil_div(v_count, NSEQ), phi - plo);
-    k_fft_rows<LOGN><<<grd, kRowThreads, smem, ctx->stream>>>(grid, n_groups, v_count, plo, tw);
+    k_fft_rows<LOGN><<<grd, RT, smem, ctx->stream>>>(in, out, n_strips, n_groups, v_count, plo, tw);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
@@ -419,12 +478,13 @@ int launch_rows(wsb_ctx *ctx, double2 *grid, int n_groups, int v_count, int plo,
 template <int LOGN>
 int launch_cols(wsb_ctx *ctx, const ColArgs &a, const double2 *tw, int *nblocks) {
     constexpr int N = 1 << LOGN;
-    constexpr int C = kColThreads * kColE / N;
+    constexpr int CT = ColCfg<LOGN>::T;
+    constexpr int C = CT * kColE / N;
     const size_t smem = sizeof(double2) * 2 * C * Seq<LOGN>::STRIDE + sizeof(double) * C * N;
     WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     *nblocks = ceil_div(a.ncols, C);
-    k_fft_cols<LOGN><<<*nblocks, kColThreads, smem, ctx->stream>>>(a, tw);
+    k_fft_cols<LOGN><<<*nblocks, CT, smem, ctx->stream>>>(a, tw);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
@@ -444,26 +504,21 @@ int twiddles(wsb_ctx *ctx, int n, const double **out) {
     return WSB_OK;
 }
 
-int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, double *grid_p, int plo, int phi) {
+int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a, double *grid_p,
+             int plo, int phi) {
     if (phi <= plo || v_count <= 0) return WSB_OK;
     const double *tw;
     WSB_TRY(twiddles(ctx, g->n_u, &tw));
-    const int ng = g->n_u / kG;
+    const int ng = g->n_u / kG, ns = ceil_div(g->n_u, 32);
+    const double2 *ga = (const double2 *)grid_a;
     double2 *gp = (double2 *)grid_p;
     const double2 *t2 = (const double2 *)tw;
     switch (ilog2(g->n_u)) {
-        case 1: return launch_rows<1>(ctx, gp, ng, v_count, plo, phi, t2);
-        case 2: return launch_rows<2>(ctx, gp, ng, v_count, plo, phi, t2);
-        case 3: return launch_rows<3>(ctx, gp, ng, v_count, plo, phi, t2);
-        case 4: return launch_rows<4>(ctx, gp, ng, v_count, plo, phi, t2);
-        case 5: return launch_rows<5>(ctx, gp, ng, v_count, plo, phi, t2);
-        case 6: return launch_rows<6>(ctx, gp, ng, v_count, plo, phi, t2);
-        case 7: return launch_rows<7>(ctx, gp, ng, v_count, plo, phi, t2);
-        case 8: return launch_rows<8>(ctx, gp, ng, v_count, plo, phi, t2);
-        case 9: return launch_rows<9>(ctx, gp, ng, v_count, plo, phi, t2);
-        case 10: return launch_rows<10>(ctx, gp, ng, v_count, plo, phi, t2);
-        case 11: return launch_rows<11>(ctx, gp, ng, v_count, plo, phi, t2);
-        case 12: return launch_rows<12>(ctx, gp, ng, v_count, plo, phi, t2);
+#define WSB_ROWS(L) \
+    case L: return launch_rows<L>(ctx, ga, gp, ns, ng, v_count, plo, phi, t2);
+        WSB_ROWS(1) WSB_ROWS(2) WSB_ROWS(3) WSB_ROWS(4) WSB_ROWS(5) WSB_ROWS(6)
+        WSB_ROWS(7) WSB_ROWS(8) WSB_ROWS(9) WSB_ROWS(10) WSB_ROWS(11) WSB_ROWS(12)
+#undef WSB_ROWS
         default: return fail(WSB_EUNSUPPORTED, "n_u above 4096 needs the out-of-core FFT (not in this build)");
     }
 }

@@ -5,7 +5,7 @@
 // sorted by anchor row floor(gv); the warp keeps the 2S+1 rows a record can
 // touch as complex128 accumulators in registers and slides that window down
 // the block: before a record is applied, every row above its footprint is
-// final and is written straight to HBM (P layout, checkerboard sign of
+// final and is written straight to HBM (strip layout, checkerboard sign of
 // transform.py:180-185 applied). Each cell is therefore accumulated by one
 // lane in (anchor row, gindex) order -- deterministic and independent of
 // the number of GPUs -- and written exactly once: no shared-memory tile, no
@@ -131,7 +131,7 @@ struct SweepArgs {
     const double4 *rec;
     const uint32_t *idx;
     const uint32_t *off;
-    double2 *out;                 // P layout [n_w][n_u/G][v_count][G]
+    double2 *out;                 // strip layout [n_w][ceil(n_u/32)][v_count][32]
     unsigned long long *updates;
     const double *i0beta;         // device scalar, np.i0(beta) (Kaiser-Bessel)
     int n_u, v_start, v_count, n_tc, rs, n_rb, n_groups;
@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 4) k_grid_sweep(SweepArgs a
     const uint32_t beg = a.off[kbase + (R0 - a.v_start)];
     const uint32_t end = a.off[kbase + (R1 - 1 - a.v_start + 2 * S) + 1];
     const double i0b = KIND == WSB_KERNEL_KAISER_BESSEL ? *a.i0beta : 0.0;
-    const int64_t colbase = ((int64_t)plane * a.n_groups + (col >> 1)) * a.v_count;
+    // strip layout [plane][strip][row][32]: an emitted row is one 512-byte run
+    const int64_t colbase = ((int64_t)plane * a.n_tc + tc) * a.v_count;
     st.wu[lane][W] = 0.0;
 
     // window: rows base_row .. base_row+NW-1; a record lands at a static
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 4) k_grid_sweep(SweepArgs a
             const int row = base_row + b;
             const double s = (b & 1) ? -s0 : s0;
             if (row >= R0 && row < R1 && col_ok)
-                a.out[(colbase + (row - a.v_start)) * kG + (col & 1)] =
+                a.out[(colbase + (row - a.v_start)) * 32 + lane] =
                     make_double2(acc[b].x * s, acc[b].y * s);
         }
 #pragma unroll

@@ -81,6 +81,7 @@ enum Slot {
     kSlotRec,
     kSlotPlane,
     kSlotGrid,
+    kSlotGridP,
     kSlotStrip,
     kSlotNorms,
     kSlotHostIn,
@@ -129,8 +130,8 @@ int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
                unsigned long long *updates_dev);
 
 // fft.cu
-int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, double *grid_p, int plane_lo,
-             int plane_hi);
+int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a, double *grid_p,
+             int plane_lo, int plane_hi);
 int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t *src_rows,
                    int g0, int ng, const double *tgrid, double *image_strip,
                    double *norm_partials);

@@ -63,9 +63,14 @@ class CudaBackend:
     def grid_slab(self, rec, plane, spec, kern, v0, vc):
         return grid_slab_device(rec, plane, spec, kern, v0, vc)
 
-    def fft_rows(self, grid_p, spec, vc):
+    def fft_rows(self, grid_s, spec, vc):
+        """Row pass: strip-layout slab in, new P-layout slab out."""
         g = spec.c_struct()
-        L.check(L.lib().wsb_fft_rows(self.ctx.handle, C.byref(g), int(vc), _ptr(grid_p), 0, spec.n_w))
+        grid_p = torch.empty((spec.n_w, spec.n_u // G, vc, G, 2), dtype=torch.float64,
+                             device=self.device)
+        L.check(L.lib().wsb_fft_rows(self.ctx.handle, C.byref(g), int(vc), _ptr(grid_s),
+                                     _ptr(grid_p), 0, spec.n_w))
+        return grid_p
 
     def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng):
         g = spec.c_struct()
@@ -114,10 +119,11 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     # 2. grid this rank's slab ----------------------------------------------
     slabs = [partition_1d(spec.n_v, R, d) for d in range(R)]
     v0, vc = slabs[r]
-    grid_p, updates = be.grid_slab(rrec, rpl, spec, kern, v0, vc)
+    grid_s, updates = be.grid_slab(rrec, rpl, spec, kern, v0, vc)
 
     # 3. row FFT, per-plane block transpose, column FFT + w stack ------------
-    be.fft_rows(grid_p, spec, vc)
+    grid_p = be.fft_rows(grid_s, spec, vc)
+    del grid_s
     cols = [partition_1d(n_groups, R, d) for d in range(R)]
     g0, ng = cols[r]
     gp = grid_p.reshape(spec.n_w, -1)                       # float64 view, P layout per plane

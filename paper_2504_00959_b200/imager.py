@@ -260,13 +260,13 @@ def prepare_device(u, v, w, vis, weight, spec: GridSpec, device=None):
 def grid_slab_device(rec: torch.Tensor, plane: torch.Tensor, spec: GridSpec, kern: KernelSpec,
                      v_start: int, v_count: int, out: torch.Tensor | None = None):
     """grid_sector (gridder.py:186-259) for one slab on the GPU. Returns
-    (P-layout grid complex128 view [n_w, n_u/G, v_count, G] as float64 [...,2],
-    grid_updates)."""
+    (strip-layout grid, complex128 [n_w, ceil(n_u/32), v_count, 32] as float64
+    [..., 2], grid_updates)."""
     spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
     ctx = context(rec.device)
     m = rec.shape[0]
     if out is None:
-        out = torch.empty((spec.n_w, spec.n_u // L.P_GROUP, v_count, L.P_GROUP, 2),
+        out = torch.empty((spec.n_w, (spec.n_u + 31) // 32, v_count, 32, 2),
                           dtype=torch.float64, device=rec.device)
     upd = C.c_int64()
     g, k = spec.c_struct(), kern.c_struct()
@@ -277,7 +277,7 @@ def grid_slab_device(rec: torch.Tensor, plane: torch.Tensor, spec: GridSpec, ker
 
 
 def unpack_grid_device(grid_p: torch.Tensor, spec: GridSpec, v_start: int, v_count: int):
-    """P layout -> (n_w, v_count, n_u) complex128 without the checkerboard sign."""
+    """Strip layout -> (n_w, v_count, n_u) complex128 without the checkerboard sign."""
     spec = as_grid_spec(spec)
     ctx = context(grid_p.device)
     out = torch.empty((spec.n_w, v_count, spec.n_u, 2), dtype=torch.float64, device=grid_p.device)

@@ -41,16 +41,21 @@ class NumpyBackend:
         kind = O.KIND_GAUSSIAN if kern.kind == "gaussian" else O.KIND_KAISER_BESSEL
         grid, upd = O.grid_slab(batch, spec.n_u, spec.n_w, kind, kern.half_support, kern.shape_param)
         grid = grid * O.checker_sign(spec.n_u, v0, vc)[None]
-        # (plane, row, col) -> P layout (plane, col/G, row, col%G)
-        p = grid.reshape(spec.n_w, vc, spec.n_u // G, G).transpose(0, 2, 1, 3)
-        p = np.ascontiguousarray(p)
-        return torch.from_numpy(p.view(np.float64).reshape(spec.n_w, spec.n_u // G, vc, G, 2)), upd
+        # (plane, row, col) -> strip layout (plane, col/32, row, col%32)
+        ns = (spec.n_u + 31) // 32
+        pad = np.zeros((spec.n_w, vc, ns * 32), np.complex128)
+        pad[:, :, : spec.n_u] = grid
+        s = np.ascontiguousarray(pad.reshape(spec.n_w, vc, ns, 32).transpose(0, 2, 1, 3))
+        return torch.from_numpy(s.view(np.float64).reshape(spec.n_w, ns, vc, 32, 2)), upd
 
-    def fft_rows(self, grid_p, spec, vc):
-        a = grid_p.numpy().view(np.complex128).reshape(spec.n_w, spec.n_u // G, vc, G)
-        nat = a.transpose(0, 2, 1, 3).reshape(spec.n_w, vc, spec.n_u)
+    def fft_rows(self, grid_s, spec, vc):
+        ns = (spec.n_u + 31) // 32
+        a = grid_s.numpy().view(np.complex128).reshape(spec.n_w, ns, vc, 32)
+        nat = a.transpose(0, 2, 1, 3).reshape(spec.n_w, vc, ns * 32)[:, :, : spec.n_u]
         f = np.fft.ifft(nat, axis=-1) * spec.n_u               # unnormalised inverse
-        a[...] = f.reshape(spec.n_w, vc, spec.n_u // G, G).transpose(0, 2, 1, 3)
+        # -> P layout (plane, col/G, row, col%G)
+        p = np.ascontiguousarray(f.reshape(spec.n_w, vc, spec.n_u // G, G).transpose(0, 2, 1, 3))
+        return torch.from_numpy(p.view(np.float64).reshape(spec.n_w, spec.n_u // G, vc, G, 2))
 
     def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng):
         t = tgrid.numpy().view(np.complex128).reshape(spec.n_w, -1)

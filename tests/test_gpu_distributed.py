@@ -55,10 +55,9 @@ def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R):
             off = sum(counts[:d])
             recs.append(srec[off:off + counts[d]])
             pls.append(spl[off:off + counts[d]])
-        gp, up = be.grid_slab(torch.cat(recs).contiguous(), torch.cat(pls).contiguous(), spec, kern,
+        gs, up = be.grid_slab(torch.cat(recs).contiguous(), torch.cat(pls).contiguous(), spec, kern,
                               v0, vc)
-        be.fft_rows(gp, spec, vc)
-        grids.append(gp)
+        grids.append(be.fft_rows(gs, spec, vc))
         upd += up
     pix = np.empty((spec.n_v, spec.n_u))
     parts = []
