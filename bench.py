@@ -105,7 +105,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark(self, which: str):
+        setattr(self, "t_" + which, time.perf_counter())
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -118,7 +121,11 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t_start", -1e18), getattr(self, "t_end", 1e18)
+        inside = [ln for t, ln in self.lines if t0 <= t <= t1 + 0.1]
+        if not inside and self.lines:  # timed region shorter than the sampling period
+            inside = [min(self.lines, key=lambda x: abs(x[0] - t1))[1]]
+        for ln in inside:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -184,6 +191,7 @@ def run_ours(args):
             return WD.image_distributed(du, dv, dw, dvis, dwt, spec, kern)
         return W.image_device(du, dv, dw, dvis, dwt, spec, kern, image_out=img)
 
+    clk = ClockSampler(dev.index).__enter__()   # sampling runs through warm-up and timing
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -194,15 +202,21 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(dev.index) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
+    clk.mark("start")
+    launches0 = W.last_timings(dev)[1]   # cumulative counter of the multi-stage path
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+        if ws == 1:
             ms, nl = W.last_timings(dev)
             per_kernel += np.array(ms)
             launches += nl
-        ev1.record(stream)
-        torch.cuda.synchronize()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        launches = W.last_timings(dev)[1] - launches0
+    clk.mark("end")
+    clk.__exit__(None, None, None)
     if ws > 1:
         dist.barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
@@ -380,7 +394,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
