@@ -11,7 +11,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libwsb.so"
+LIB_PATH = Path(os.environ.get("WSB_LIB", Path(__file__).resolve().parent / "libwsb.so"))
 
 WSB_OK = 0
 WSB_EINVAL = -1

@@ -16,14 +16,28 @@
 // (FP64; excluded taps get weight 0, so the per-record update below is
 // branch-free). The tap set is the reference's: |g - i| <= S with g - i
 // rounded as in gridder.py:170-177.
+#include <type_traits>
+
 #include "i0_coeffs.h"
 #include "wsb_internal.cuh"
 
 namespace wsb {
 namespace {
 
-constexpr int kWarpsPerCta = 4;
-constexpr int kRowBlock = 64;
+#ifndef WSB_GRID_WARPS
+#define WSB_GRID_WARPS 4
+#endif
+#ifndef WSB_GRID_ROWS
+#define WSB_GRID_ROWS 64
+#endif
+#ifndef WSB_GRID_MINB
+#define WSB_GRID_MINB 4
+#endif
+#ifndef WSB_GRID_D
+#define WSB_GRID_D 4
+#endif
+constexpr int kWarpsPerCta = WSB_GRID_WARPS;  // independent warps per CTA
+constexpr int kRowBlock = WSB_GRID_ROWS;      // slab rows per work item
 
 __device__ __forceinline__ double chbevl(double x, const double *vals, int n) {
     // numpy _chbevl: b0 = x*b1 - b2 + vals[i] with separate roundings
@@ -44,6 +58,31 @@ __device__ __forceinline__ double bessel_i0(double x) {
         return __dmul_rn(exp(x), chbevl(__dsub_rn(__ddiv_rn(x, 2.0), 2.0), kI0A, kI0A_N));
     return __ddiv_rn(__dmul_rn(exp(x), chbevl(__dsub_rn(__ddiv_rn(32.0, x), 2.0), kI0B, kI0B_N)),
                      __dsqrt_rn(x));
+}
+
+// exp(x) for -700 < x < 700: x = k ln2 + r, |r| <= ln2/2 (two-constant
+// Cody-Waite), Taylor to r^14 (truncation < 1e-17), 2^k added to the
+// exponent field. A few ulp; no special-case paths.
+__device__ __forceinline__ double fast_exp(double x) {
+    const double k = rint(x * 1.4426950408889634);
+    double r = fma(-k, 0.6931471805599453, x);
+    r = fma(-k, 2.3190468138462996e-17, r);
+    double p = 1.1470745597729725e-11;
+    p = fma(p, r, 1.6059043836821613e-10);
+    p = fma(p, r, 2.08767569878681e-09);
+    p = fma(p, r, 2.505210838544172e-08);
+    p = fma(p, r, 2.755731922398589e-07);
+    p = fma(p, r, 2.7557319223985893e-06);
+    p = fma(p, r, 2.48015873015873e-05);
+    p = fma(p, r, 0.0001984126984126984);
+    p = fma(p, r, 0.001388888888888889);
+    p = fma(p, r, 0.008333333333333333);
+    p = fma(p, r, 0.041666666666666664);
+    p = fma(p, r, 0.16666666666666666);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    return __hiloint2double(__double2hiint(p) + ((int)k << 20), __double2loint(p));
 }
 
 template <int S>
@@ -73,9 +112,9 @@ __device__ __forceinline__ uint32_t axis_weights(double g, int i0, const KParams
     }
     if (KIND == WSB_KERNEL_GAUSSIAN && kp.factorised) {
         const double f = __dsub_rn(g, (double)(i0 + S));
-        const double a = exp(__ddiv_rn(-__dmul_rn(f, f), kp.p0));
-        const double b = exp(__ddiv_rn(-2.0 * f, kp.p0));    // m > 0 side
-        const double bi = exp(__ddiv_rn(2.0 * f, kp.p0));    // m < 0 side
+        const double a = fast_exp(__ddiv_rn(-__dmul_rn(f, f), kp.p0));
+        const double b = fast_exp(__ddiv_rn(-2.0 * f, kp.p0));  // m > 0 side
+        const double bi = __drcp_rn(b);                         // m < 0 side
         w[S] = a;
         double pb = a, pbi = a;
 #pragma unroll
@@ -127,6 +166,17 @@ __device__ __forceinline__ void window_fma(double2 (&acc)[NW], int off, double t
     }
 }
 
+// Calls f(std::integral_constant<int, phase>) for a runtime phase in [0, W).
+template <int I, int W, class F>
+__device__ __forceinline__ void dispatch_phase(int phase, F &f) {
+    if constexpr (I < W) {
+        if (phase == I)
+            f(std::integral_constant<int, I>{});
+        else
+            dispatch_phase<I + 1, W>(phase, f);
+    }
+}
+
 struct SweepArgs {
     const double4 *rec;
     const uint32_t *idx;
@@ -151,7 +201,7 @@ struct WarpStage {
 };
 
 template <int KIND, int S>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 4) k_grid_sweep(SweepArgs a, KParams<S> kp) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta, WSB_GRID_MINB) k_grid_sweep(SweepArgs a, KParams<S> kp) {
     constexpr int W = 2 * S + 1;
     using St = WarpStage<S>;
     __shared__ __align__(16) St stage_all[kWarpsPerCta];
@@ -178,40 +228,82 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 4) k_grid_sweep(SweepArgs a
     const int64_t colbase = ((int64_t)plane * a.n_tc + tc) * a.v_count;
     st.wu[lane][W] = 0.0;
 
-    // window: rows base_row .. base_row+NW-1; a record lands at a static
-    // offset 0..D (uniform branch), rows leave D at a time
-    constexpr int D = S <= 3 ? 4 : 2;
-    constexpr int NW = W + D;
-    double2 acc[NW];
+    // Window of W rows kept as a ring of W register slots: row `base` is in
+    // slot `phase`, row base+b in slot (phase+b) % W. Records with anchor
+    // row == base are applied with the slot mapping fixed at compile time
+    // (one code copy per phase, no register moves); when the next record
+    // starts lower, row `base` is final: it is written out, its slot
+    // zeroed, and the ring turns by one.
+    double2 acc[W];
 #pragma unroll
-    for (int b = 0; b < NW; ++b) acc[b] = make_double2(0.0, 0.0);
-    int base_row = R0 - 2 * S;  // absolute row held in acc[0]
+    for (int b = 0; b < W; ++b) acc[b] = make_double2(0.0, 0.0);
+    int base = R0 - 2 * S;
+    int phase = 0;
     unsigned cnt = 0;           // cell updates of the records this lane staged
+    uint32_t cs = beg, ce = beg, r = beg;
 
-    auto emit_block = [&]() {
-        const double s0 = ((col + base_row) & 1) ? -1.0 : 1.0;
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-            const int row = base_row + b;
-            const double s = (b & 1) ? -s0 : s0;
-            if (row >= R0 && row < R1 && col_ok)
-                a.out[(colbase + (row - a.v_start)) * 32 + lane] =
-                    make_double2(acc[b].x * s, acc[b].y * s);
+    auto emit_slot = [&](auto P) {
+        constexpr int p = decltype(P)::value;
+        if (base >= R0 && base < R1 && col_ok) {
+            const double s = ((col + base) & 1) ? -1.0 : 1.0;
+            a.out[(colbase + (base - a.v_start)) * 32 + lane] =
+                make_double2(acc[p].x * s, acc[p].y * s);
         }
+        acc[p] = make_double2(0.0, 0.0);
+        ++base;
+        phase = (p + 1 == W) ? 0 : p + 1;
+    };
+    auto run = [&](auto P) {
+        constexpr int p = decltype(P)::value;
+        while (r < ce) {
+            const int rr = (int)(r - cs);
+            const int2 ij = st.ij[rr];
+            if (ij.y != base) {  // records are sorted by anchor row: base < ij.y
+                emit_slot(P);
+                return;
+            }
+            int k = col - ij.x;
+            k = (unsigned)k < (unsigned)W ? k : W;   // slot W holds weight 0
+            const double2 v = st.val[rr];
+            const double wu = st.wu[rr][k];
+            const double tr = __dmul_rn(v.x, wu), ti = __dmul_rn(v.y, wu);
 #pragma unroll
-        for (int b = 0; b < NW - D; ++b) acc[b] = acc[b + D];
-#pragma unroll
-        for (int b = NW - D; b < NW; ++b) acc[b] = make_double2(0.0, 0.0);
-        base_row += D;
+            for (int b = 0; b < W; b += 2) {
+                const double2 wv2 = *reinterpret_cast<const double2 *>(&st.wv[rr][b]);
+                acc[(p + b) % W].x = fma(tr, wv2.x, acc[(p + b) % W].x);
+                acc[(p + b) % W].y = fma(ti, wv2.x, acc[(p + b) % W].y);
+                if (b + 1 < W) {
+                    acc[(p + b + 1) % W].x = fma(tr, wv2.y, acc[(p + b + 1) % W].x);
+                    acc[(p + b + 1) % W].y = fma(ti, wv2.y, acc[(p + b + 1) % W].y);
+                }
+            }
+            ++r;
+        }
     };
 
-    for (uint32_t cb = beg; cb < end; cb += 32) {
-        // ---- stage 32 records: one per lane --------------------------------
-        {
-            const uint32_t e = cb + lane;
-            if (e < end) {
-                const double2 *p = reinterpret_cast<const double2 *>(a.rec + __ldg(&a.idx[e]));
-                const double2 lo = __ldg(p), hi = __ldg(p + 1);
+    // the record a lane stages next is gathered one chunk ahead, so the
+    // random 32-byte loads overlap the previous chunk's updates
+    double2 nlo = make_double2(0.0, 0.0), nhi = nlo;
+    auto fetch = [&](uint32_t e) {
+        if (e < end) {
+            const double2 *p = reinterpret_cast<const double2 *>(a.rec + __ldg(&a.idx[e]));
+            nlo = __ldg(p);
+            nhi = __ldg(p + 1);
+        }
+    };
+    fetch(beg + lane);
+
+    while (true) {
+        if (r == ce) {
+            if (ce >= end) break;
+            // ---- stage the next 32 records: one per lane -------------------
+            __syncwarp();
+            cs = ce;
+            ce = min(cs + 32u, end);
+            const uint32_t e = cs + lane;
+            const double2 lo = nlo, hi = nhi;
+            fetch(e + 32);
+            if (e < ce) {
                 const double gu = lo.x, gv = lo.y;
                 const int ib = (int)floor(gu) - S, jb = (int)floor(gv) - S;
                 double w[W];
@@ -230,22 +322,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 4) k_grid_sweep(SweepArgs a
                 const uint32_t rm = r_hi > r_lo ? ((1u << (r_hi - r_lo)) - 1u) << r_lo : 0u;
                 cnt += __popc(um & cm) * __popc(vm & rm);
             }
+            __syncwarp();
         }
-        __syncwarp();
-        const int nrec = min(32u, end - cb);
-        for (int r = 0; r < nrec; ++r) {
-            const int2 ij = st.ij[r];
-            while (ij.y - base_row > D) emit_block();
-            int k = col - ij.x;
-            k = (unsigned)k < (unsigned)W ? k : W;   // slot W holds weight 0
-            const double2 v = st.val[r];
-            const double wu = st.wu[r][k];
-            const double tr = __dmul_rn(v.x, wu), ti = __dmul_rn(v.y, wu);
-            window_fma<W, NW, 0>(acc, ij.y - base_row, tr, ti, &st.wv[r][0]);
-        }
-        __syncwarp();
+        dispatch_phase<0, W>(phase, run);
     }
-    while (base_row < R1) emit_block();
+    while (base < R1) dispatch_phase<0, W>(phase, emit_slot);
 
 #pragma unroll
     for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
