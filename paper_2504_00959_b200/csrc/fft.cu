@@ -231,13 +231,17 @@ __device__ __forceinline__ void smem_passes(double2 *s, const double2 *tw, doubl
 // ---------------------------------------------------------------------------
 // row pass: global -> registers -> (shared memory passes) -> global
 // ---------------------------------------------------------------------------
-// one row per CTA at N >= 2048 (4 CTAs per SM of 128 threads at N = 2048):
-// small independent CTAs keep the per-pass barriers of different rows out
-// of phase, so one CTA's HBM latency overlaps another's transform
+// 4096/N rows per CTA (2 at N = 2048, 2 CTAs per SM): independent CTAs keep
+// the per-pass barriers of different rows out of phase, so one CTA's HBM
+// latency overlaps another's transform (measured: 1 row/128 threads and
+// 4 rows/512 threads are both slower at N = 2048)
 template <int LOGN>
 struct RowCfg {
-    static constexpr int T = ((1 << LOGN) / 16 > 128) ? (1 << LOGN) / 16 : 128;
-    static constexpr int MINB = T <= 128 ? 4 : 2;
+#ifndef WSB_ROW_MIN_T
+#define WSB_ROW_MIN_T 256
+#endif
+    static constexpr int T = ((1 << LOGN) / 16 > WSB_ROW_MIN_T) ? (1 << LOGN) / 16 : WSB_ROW_MIN_T;
+    static constexpr int MINB = T <= 128 ? 4 : (T <= 256 ? 2 : 1);
 };
 constexpr int kRowE = 16;
 constexpr int kRowRL = 4;
@@ -282,6 +286,7 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
         pass_store<LOGN, RLL, kRowE, RT>(N >> RLL, v, gst);
     }
 }
+
 
 // ---------------------------------------------------------------------------
 // column pass + w correction + stacking

@@ -1,6 +1,6 @@
 // K2: register-window sweep gridder (gridder.py:160-259, Eq. 3).
 //
-// Work item = one warp = (w plane, 32-column strip, block of 64 slab rows).
+// Work item = one warp = (w plane, 32-column strip, block of 128 slab rows).
 // Lane l owns column 32*strip + l. The item's records (bucket.cu) arrive
 // sorted by anchor row floor(gv); the warp keeps the 2S+1 rows a record can
 // touch as complex128 accumulators in registers and slides that window down
@@ -28,7 +28,7 @@ namespace {
 #define WSB_GRID_WARPS 4
 #endif
 #ifndef WSB_GRID_ROWS
-#define WSB_GRID_ROWS 64
+#define WSB_GRID_ROWS 128
 #endif
 #ifndef WSB_GRID_MINB
 #define WSB_GRID_MINB 4
