@@ -188,7 +188,7 @@ def run_ours(args):
 
     def step():
         if ws > 1:
-            return WD.image_distributed(du, dv, dw, dvis, dwt, spec, kern)
+            return WD.image_distributed(du, dv, dw, dvis, dwt, spec, kern, to_host=False)
         return W.image_device(du, dv, dw, dvis, dwt, spec, kern, image_out=img)
 
     clk = ClockSampler(dev.index).__enter__()   # sampling runs through warm-up and timing

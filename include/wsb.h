@@ -153,15 +153,20 @@ int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
 
 /* Row pass of the inverse 2D FFT (transform.py:151 / fft1d inverse) on planes
  * [plane_lo, plane_hi): strip-layout slab in, P-layout slab out (out of
- * place; P groups column pairs so one destination's columns are contiguous
- * for the transpose). Unnormalised. */
+ * place). With n_dest > 1 the column pairs are split over destination ranks
+ * (dest_pairs_host[d] pairs each, in order) and the output is destination
+ * major, [d][plane][pair - first_pair_d][row][G], so ONE all-to-all moves the
+ * whole slab transpose (fft2d_slab's send loop, transform.py:152-161).
+ * dest_pairs_host NULL = one destination = plain P layout. Unnormalised. */
 int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count,
-                 const double *grid_s, double *grid_p, int32_t plane_lo, int32_t plane_hi);
+                 const double *grid_s, double *grid_p, int32_t plane_lo, int32_t plane_hi,
+                 int32_t n_dest, const int32_t *dest_pairs_host);
 
 /* Column pass + w correction + stacking (transform.py:162-175, 192-230):
- * input tgrid holds, per plane, this rank's column groups [g0, g0+ng) for all
- * n_v rows, concatenated by source slab s (rows src_rows[s]) as
- *   [plane][s][g - g0][row - row_start_s][G]   (the all-to-all output).
+ * input tgrid holds this rank's column pairs [g0, g0+ng) for all n_v rows,
+ * concatenated by source slab s (src_rows[s] rows each, all equal) as
+ *   [s][plane][g - g0][row - row_start_s][G]   (the all-to-all output of
+ * wsb_fft_rows with destinations; with one source it is the P layout).
  * Writes image_strip f64[n_v][ng*G] (row-major) and norm_partials
  * f64[ng*G][2] = (sum Im^2, sum Re^2) per image column (fixed pairwise tree
  * over the rows); the caller sums the columns in order, which makes the

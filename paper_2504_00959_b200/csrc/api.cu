@@ -254,14 +254,16 @@ int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern, in
 }
 
 int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count, const double *grid_s,
-                 double *grid_p, int32_t plane_lo, int32_t plane_hi) {
+                 double *grid_p, int32_t plane_lo, int32_t plane_hi, int32_t n_dest,
+                 const int32_t *dest_pairs_host) {
     if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
     WSB_TRY(validate_grid(grid));
     if (plane_lo < 0 || plane_hi > grid->n_w || plane_lo > plane_hi)
         return fail(WSB_EINVAL, "plane range outside [0, n_w]");
     if (grid_s == grid_p) return fail(WSB_EINVAL, "the row pass is out of place");
     WSB_TRY(set_device(ctx));
-    return fft_rows(ctx, grid, v_count, grid_s, grid_p, plane_lo, plane_hi);
+    return fft_rows(ctx, grid, v_count, grid_s, grid_p, plane_lo, plane_hi,
+                    dest_pairs_host ? n_dest : 1, dest_pairs_host);
 }
 
 int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
@@ -348,7 +350,7 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
     WSB_CUDA_TRY(cudaEventRecord(ev[2], ctx->stream));
     WSB_TRY(grid_sweep(ctx, grid, kern, 0, n_v, rec, bk, gs, upd));
     WSB_CUDA_TRY(cudaEventRecord(ev[3], ctx->stream));
-    WSB_TRY(fft_rows(ctx, grid, n_v, gs, gp, 0, n_w));
+    WSB_TRY(fft_rows(ctx, grid, n_v, gs, gp, 0, n_w, 1, nullptr));
     WSB_CUDA_TRY(cudaEventRecord(ev[4], ctx->stream));
     const int32_t rows[1] = {n_v};
     WSB_TRY(fft_cols_stack(ctx, grid, 1, rows, 0, n_u / kG, gp, image_out, partials));

@@ -246,13 +246,20 @@ struct RowCfg {
 constexpr int kRowE = 16;
 constexpr int kRowRL = 4;
 
+// column-pair partition of the row pass output over the destination ranks
+struct RowDest {
+    int n_w;
+    int g0[9];   // first pair of each destination, g0[n_dest] = n_u/G, unused = INT_MAX
+};
+
 // 4096/N rows per CTA. The first pass reads its inputs straight from HBM
 // (32-byte sectors, 16 loads in flight per thread) and the last pass writes
 // its outputs straight back: shared memory only carries the inner exchanges.
 template <int LOGN>
 __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
     k_fft_rows(const double2 *__restrict__ in, double2 *__restrict__ out, int n_strips,
-               int n_groups, int v_count, int plane_lo, const double2 *__restrict__ tw) {
+               int n_groups, int v_count, int plane_lo, const double2 *__restrict__ tw,
+               RowDest dst) {
     constexpr int N = 1 << LOGN;
     constexpr int RT = RowCfg<LOGN>::T;
     constexpr int NSEQ = RT * kRowE / N;  // rows per CTA
@@ -268,9 +275,22 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
                    : make_double2(0.0, 0.0);
     };
     // out: P[plane][col/G][row][col%G] (the column pass and the transpose read it)
+    // column pair g goes to destination d (g in [g0_d, g0_{d+1})), laid out
+    // [d][plane][g - g0_d][row][x] so one all-to-all moves every plane; with a
+    // single destination this is the plain P layout
     auto gst = [&](int seq, int col, double2 z) {
-        if (j0 + seq < v_count)
-            out[((plane * n_groups + col / kG) * v_count + j0 + seq) * kG + (col % kG)] = z;
+        if (j0 + seq < v_count) {
+            const int g = col / kG;
+            int lo = 0, hi = dst.g0[1];
+#pragma unroll
+            for (int d = 1; d < 8; ++d)
+                if (g >= dst.g0[d]) {
+                    lo = dst.g0[d];
+                    hi = dst.g0[d + 1];
+                }
+            const int64_t base = (int64_t)dst.n_w * v_count * kG * lo;
+            out[base + ((plane * (hi - lo) + (g - lo)) * v_count + j0 + seq) * kG + (col % kG)] = z;
+        }
     };
     double2 v[kRowE];
     pass_load<LOGN, P0::RL, kRowE, RT>(v, gld);
@@ -331,11 +351,14 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     double *nbuf = reinterpret_cast<double *>(sbuf + 2 * C * STRIDE);  // n = sqrt(1-l^2-m^2), [C][N]
 
     const int c0 = blockIdx.x * C;                 // first local column
-    const int64_t plane_elems = (int64_t)(a.ncols / kG) * N * kG;
+    // input [s][plane][g][row - row_start_s][x]: every source holds the same
+    // number of rows, so a plane advances every source block by ncols*rows
+    const int64_t plane_elems = (int64_t)a.ncols * (N / a.n_src);
 
     // In-plane offset of each first-pass input of this thread (the same for
-    // every plane): element (row j, local column c0+seq) in the transposed
-    // slab layout [s][g][row - row_start_s][x]; -1 past the last column.
+    // every plane): element (row j, local column c0+seq) of plane 0 in the
+    // transposed layout [s][plane][g][row - row_start_s][x]; -1 past the
+    // last column.
     int off[kColE];
     {
         auto offset = [&](int seq, int j) -> double2 {
@@ -348,7 +371,7 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
                     r0 = a.src_start[sidx];
                     r1 = a.src_start[sidx + 1];
                 }
-            const int o = r0 * a.ncols + ((lc / kG) * (r1 - r0) + (j - r0)) * kG + (lc % kG);
+            const int o = a.n_w * a.ncols * r0 + ((lc / kG) * (r1 - r0) + (j - r0)) * kG + (lc % kG);
             return make_double2(__hiloint2double(o, 0), 0.0);
         };
         double2 t[kColE];
@@ -466,7 +489,7 @@ __global__ void k_twiddles(double2 *tw, int n) {
 
 template <int LOGN>
 int launch_rows(wsb_ctx *ctx, const double2 *in, double2 *out, int n_strips, int n_groups,
-                int v_count, int plo, int phi, const double2 *tw) {
+                int v_count, int plo, int phi, const double2 *tw, const RowDest &dst) {
     constexpr int N = 1 << LOGN;
     constexpr int RT = RowCfg<LOGN>::T;
     constexpr int NSEQ = RT * kRowE / N;
@@ -474,7 +497,8 @@ int launch_rows(wsb_ctx *ctx, const double2 *in, double2 *out, int n_strips, int
     WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     dim3 grd(ceil_div(v_count, NSEQ), phi - plo);
-    k_fft_rows<LOGN><<<grd, RT, smem, ctx->stream>>>(in, out, n_strips, n_groups, v_count, plo, tw);
+    k_fft_rows<LOGN><<<grd, RT, smem, ctx->stream>>>(in, out, n_strips, n_groups, v_count, plo, tw,
+                                                     dst);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
@@ -510,17 +534,24 @@ int twiddles(wsb_ctx *ctx, int n, const double **out) {
 }
 
 int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a, double *grid_p,
-             int plo, int phi) {
+             int plo, int phi, int n_dest, const int32_t *dest_groups) {
     if (phi <= plo || v_count <= 0) return WSB_OK;
     const double *tw;
     WSB_TRY(twiddles(ctx, g->n_u, &tw));
     const int ng = g->n_u / kG, ns = ceil_div(g->n_u, 32);
+    RowDest dst;
+    dst.n_w = g->n_w;
+    if (n_dest < 1 || n_dest > 8) return fail(WSB_EINVAL, "n_dest must be in [1, 8]");
+    dst.g0[0] = 0;
+    for (int d = 0; d < n_dest; ++d) dst.g0[d + 1] = dst.g0[d] + (dest_groups ? dest_groups[d] : ng);
+    if (dst.g0[n_dest] != ng) return fail(WSB_EINVAL, "destination column pairs must sum to n_u/2");
+    for (int d = n_dest + 1; d < 9; ++d) dst.g0[d] = 0x7fffffff;
     const double2 *ga = (const double2 *)grid_a;
     double2 *gp = (double2 *)grid_p;
     const double2 *t2 = (const double2 *)tw;
     switch (ilog2(g->n_u)) {
 #define WSB_ROWS(L) \
-    case L: return launch_rows<L>(ctx, ga, gp, ns, ng, v_count, plo, phi, t2);
+    case L: return launch_rows<L>(ctx, ga, gp, ns, ng, v_count, plo, phi, t2, dst);
         WSB_ROWS(1) WSB_ROWS(2) WSB_ROWS(3) WSB_ROWS(4) WSB_ROWS(5) WSB_ROWS(6)
         WSB_ROWS(7) WSB_ROWS(8) WSB_ROWS(9) WSB_ROWS(10) WSB_ROWS(11) WSB_ROWS(12)
 #undef WSB_ROWS
@@ -546,6 +577,9 @@ int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t
     for (int s = 0; s < n_sources; ++s) a.src_start[s + 1] = a.src_start[s] + src_rows[s];
     for (int s = n_sources + 1; s < 9; ++s) a.src_start[s] = 1 << 30;
     if (a.src_start[n_sources] != g->n_v) return fail(WSB_EINVAL, "source rows must sum to n_v");
+    for (int s = 1; s < n_sources; ++s)
+        if (src_rows[s] != src_rows[0])
+            return fail(WSB_EUNSUPPORTED, "slabs of unequal height (n_v not a multiple of the rank count)");
     a.src_start[n_sources] = g->n_v;
     a.cell = g->cell_size_lm;
     a.inv_nuv = 1.0 / ((double)g->n_u * (double)g->n_v);

@@ -63,13 +63,14 @@ class CudaBackend:
     def grid_slab(self, rec, plane, spec, kern, v0, vc):
         return grid_slab_device(rec, plane, spec, kern, v0, vc)
 
-    def fft_rows(self, grid_s, spec, vc):
-        """Row pass: strip-layout slab in, new P-layout slab out."""
+    def fft_rows(self, grid_s, spec, vc, dest_pairs):
+        """Row pass: strip-layout slab in; out: float64 buffer laid out
+        [dest][plane][pair][row][G][2] (the all-to-all send buffer)."""
         g = spec.c_struct()
-        grid_p = torch.empty((spec.n_w, spec.n_u // G, vc, G, 2), dtype=torch.float64,
-                             device=self.device)
+        grid_p = torch.empty(spec.n_w * spec.n_u * vc * 2, dtype=torch.float64, device=self.device)
+        pairs = (C.c_int32 * len(dest_pairs))(*dest_pairs)
         L.check(L.lib().wsb_fft_rows(self.ctx.handle, C.byref(g), int(vc), _ptr(grid_s),
-                                     _ptr(grid_p), 0, spec.n_w))
+                                     _ptr(grid_p), 0, spec.n_w, len(dest_pairs), pairs))
         return grid_p
 
     def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng):
@@ -87,7 +88,8 @@ def _a2a(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group):
                            input_split_sizes=list(in_splits), group=group)
 
 
-def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None, root: int = 0):
+def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None, root: int = 0,
+                      to_host: bool = True):
     """Dirty image of the union of every rank's records. Each rank passes its
     own time partition (records in gindex order, rank r holding the r-th
     contiguous block, as visdata.partition_time_ordered produces).
@@ -102,6 +104,8 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     n_groups = spec.n_u // G
     if R > spec.n_v or R > n_groups:
         raise ValueError(f"{R} ranks exceed the mesh ({spec.n_v} rows, {n_groups} column groups)")
+    if spec.n_v % R:
+        raise NotImplementedError("the GPU slab transpose needs n_v to be a multiple of the rank count")
 
     # 1. prepare + time->space exchange ------------------------------------
     rec, plane = be.prepare(u, v, w, vis, weight, spec)
@@ -121,17 +125,16 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     v0, vc = slabs[r]
     grid_s, updates = be.grid_slab(rrec, rpl, spec, kern, v0, vc)
 
-    # 3. row FFT, per-plane block transpose, column FFT + w stack ------------
-    grid_p = be.fft_rows(grid_s, spec, vc)
-    del grid_s
+    # 3. row FFT, one all-to-all block transpose, column FFT + w stack --------
     cols = [partition_1d(n_groups, R, d) for d in range(R)]
     g0, ng = cols[r]
-    gp = grid_p.reshape(spec.n_w, -1)                       # float64 view, P layout per plane
-    in_splits = [ng_d * vc * G * 2 for _, ng_d in cols]     # float64 elements to each rank
-    out_splits = [ng * vc_s * G * 2 for _, vc_s in slabs]   # from each source slab
-    tgrid = torch.empty((spec.n_w, ng * spec.n_v * G * 2), dtype=torch.float64, device=dev)
-    for k in range(spec.n_w):
-        _a2a(tgrid[k], gp[k], out_splits, in_splits, group)
+    grid_p = be.fft_rows(grid_s, spec, vc, [ng_d for _, ng_d in cols])   # [dest][plane][pair][row][G]
+    del grid_s
+    in_splits = [spec.n_w * ng_d * vc * G * 2 for _, ng_d in cols]     # float64 elements to each rank
+    out_splits = [spec.n_w * ng * vc_s * G * 2 for _, vc_s in slabs]   # from each source slab
+    tgrid = torch.empty(sum(out_splits), dtype=torch.float64, device=dev)
+    _a2a(tgrid, grid_p, out_splits, in_splits, group)
+    del grid_p
     strip, partials = be.fft_cols_stack(tgrid, spec, [vc_s for _, vc_s in slabs], g0, ng)
 
     # 4. gather to the root ----------------------------------------------------
@@ -160,6 +163,6 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     # same association as the single-GPU path, for any R
     im_sq = float(p[:, 0].cumsum()[-1])
     re_sq = float(p[:, 1].cumsum()[-1])
-    img = FinalImage(spec, pix.cpu().numpy(), im_sq ** 0.5, re_sq ** 0.5)
+    img = FinalImage(spec, pix.cpu().numpy() if to_host else pix, im_sq ** 0.5, re_sq ** 0.5)
     diag.update({"imag_residual_norm": img.imag_residual_norm, "real_norm": img.real_norm})
     return img, diag

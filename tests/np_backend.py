@@ -48,24 +48,29 @@ class NumpyBackend:
         s = np.ascontiguousarray(pad.reshape(spec.n_w, vc, ns, 32).transpose(0, 2, 1, 3))
         return torch.from_numpy(s.view(np.float64).reshape(spec.n_w, ns, vc, 32, 2)), upd
 
-    def fft_rows(self, grid_s, spec, vc):
+    def fft_rows(self, grid_s, spec, vc, dest_pairs):
         ns = (spec.n_u + 31) // 32
         a = grid_s.numpy().view(np.complex128).reshape(spec.n_w, ns, vc, 32)
         nat = a.transpose(0, 2, 1, 3).reshape(spec.n_w, vc, ns * 32)[:, :, : spec.n_u]
         f = np.fft.ifft(nat, axis=-1) * spec.n_u               # unnormalised inverse
-        # -> P layout (plane, col/G, row, col%G)
-        p = np.ascontiguousarray(f.reshape(spec.n_w, vc, spec.n_u // G, G).transpose(0, 2, 1, 3))
-        return torch.from_numpy(p.view(np.float64).reshape(spec.n_w, spec.n_u // G, vc, G, 2))
+        # -> P layout (plane, col/G, row, col%G), then destination major
+        p = f.reshape(spec.n_w, vc, spec.n_u // G, G).transpose(0, 2, 1, 3)
+        out, g0 = [], 0
+        for ng in dest_pairs:
+            out.append(np.ascontiguousarray(p[:, g0:g0 + ng]).ravel())
+            g0 += ng
+        return torch.from_numpy(np.concatenate(out).view(np.float64))
 
     def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng):
-        t = tgrid.numpy().view(np.complex128).reshape(spec.n_w, -1)
+        t = tgrid.numpy().view(np.complex128)
         ncols = ng * G
         full = np.empty((spec.n_w, spec.n_v, ncols), np.complex128)
         off, r0 = 0, 0
-        for rows in src_rows:
-            blk = t[:, off:off + ng * rows * G].reshape(spec.n_w, ng, rows, G)
+        for rows in src_rows:                    # [s][plane][pair][row][G]
+            n = spec.n_w * ng * rows * G
+            blk = t[off:off + n].reshape(spec.n_w, ng, rows, G)
             full[:, r0:r0 + rows] = blk.transpose(0, 2, 1, 3).reshape(spec.n_w, rows, ncols)
-            off += ng * rows * G
+            off += n
             r0 += rows
         planes = np.fft.ifft(full, axis=1) * spec.n_v / (spec.n_u * spec.n_v)
         c0 = g0 * G

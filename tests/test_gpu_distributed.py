@@ -57,14 +57,18 @@ def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R):
             pls.append(spl[off:off + counts[d]])
         gs, up = be.grid_slab(torch.cat(recs).contiguous(), torch.cat(pls).contiguous(), spec, kern,
                               v0, vc)
-        grids.append(be.fft_rows(gs, spec, vc))
+        grids.append(be.fft_rows(gs, spec, vc, [ng for _, ng in cols]))
         upd += up
     pix = np.empty((spec.n_v, spec.n_u))
     parts = []
     for d, (g0, ng) in enumerate(cols):
-        chunks = [gp.reshape(spec.n_w, spec.n_u // G, -1)[:, g0:g0 + ng].reshape(spec.n_w, -1)
-                  for gp in grids]
-        tgrid = torch.cat(chunks, dim=1).contiguous()
+        # the all-to-all: destination d's block of every source, in source order
+        chunks = []
+        for (v0, vc), gp in zip(slabs, grids):
+            n = spec.n_w * vc * G * 2
+            start = sum(n * ng_d for _, ng_d in cols[:d])
+            chunks.append(gp[start:start + n * ng])
+        tgrid = torch.cat(chunks).contiguous()
         strip, partials = be.fft_cols_stack(tgrid, spec, [vc for _, vc in slabs], g0, ng)
         pix[:, g0 * G:(g0 + ng) * G] = strip.cpu().numpy()
         parts.append(partials.cpu().numpy())
