@@ -228,6 +228,35 @@ def run_ours(args):
     total_vis = cfg["n_vis"] * ws
     value = total_vis / (ms_step / 1e3) / 1e6
 
+    # energy to solution: NVML (+ RAPL) over a >= 1 s window of the same step
+    energy = None
+    try:
+        from paper_2504_00959_b200.energy import NvmlRaplMeter
+        meter = NvmlRaplMeter(devices=[dev.index], host=(rank == 0))
+        n_en = max(args.steps, int(1.0 / max(ms_step / 1e3, 1e-4)) + 1)
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        meter.start()
+        t0 = time.perf_counter()
+        for _ in range(n_en):
+            step()
+        torch.cuda.synchronize()
+        win = time.perf_counter() - t0
+        j = meter.joules()
+        gj = torch.tensor([j["gpu"]], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(gj)
+        energy = {"gpu_joules_per_step": round(float(gj.item()) / n_en, 4),
+                  "host_joules_per_step": (round(j["host"] / n_en, 4) if j["host"] is not None
+                                           else None),
+                  "window_s": round(win, 3), "steps": n_en,
+                  "source": "NVML total energy (all GPUs) + RAPL package (rank 0 host)"
+                            if j["host"] is not None else
+                            "NVML total energy (all GPUs); RAPL unreadable on this host"}
+    except Exception as exc:  # NVML missing or not permitted: report, do not fail the bench
+        energy = {"unavailable": f"{type(exc).__name__}: {exc}"}
+
     # end-to-end through the host-buffer C ABI (pinned inputs, host image out)
     e2e = None
     if ws == 1:
@@ -287,9 +316,18 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "e2e": e2e,
+        "energy": energy,
     }
     if ws == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(cfg)
+        cb = out["cpu_baseline"] = cpu_baseline(cfg)
+        # green productivity, Eq. 4 (metrics.py:200-207): needs both energies
+        if cb.get("host_joules_per_image") and energy and energy.get("host_joules_per_step") is not None:
+            from paper_2504_00959_b200.energy import green_productivity
+            e_gpu = energy["gpu_joules_per_step"] + energy["host_joules_per_step"]
+            out["green_productivity"] = round(green_productivity(
+                cb["seconds_per_image"], cb["host_joules_per_image"], ms_step / 1e3, e_gpu), 1)
+        else:
+            out["green_productivity"] = None
     if ws > 1:
         dist.destroy_process_group()
     print(json.dumps(out), flush=True)
@@ -340,8 +378,24 @@ def cpu_cores():
 
 def cpu_baseline(cfg, n_sample=500_000, n_planes=4):
     threads = cpu_cores()
+    meter = None
+    try:
+        from paper_2504_00959_b200.energy import NvmlRaplMeter
+        meter = NvmlRaplMeter(devices=[], host=True)
+        meter = meter if meter.host_available else None
+    except Exception:
+        meter = None
+    t0 = time.perf_counter()
+    if meter:
+        meter.start()
     full_s, det = oracle_step(cfg, n_sample, n_planes, threads)
+    sample_s = time.perf_counter() - t0
+    host_j = None
+    if meter:
+        # same average package power over the scaled-up run
+        host_j = round(meter.joules()["host"] * full_s / sample_s, 1)
     return {"value": round(cfg["n_vis"] / full_s / 1e6, 4), "unit": "Mvis/s", "cores": threads,
+            "seconds_per_image": round(full_s, 2), "host_joules_per_image": host_j,
             "kind": "port",
             "sample": (f"oracle (NumPy restatement of the reference) on {n_sample} of "
                        f"{cfg['n_vis']} records gridded on the full 2048x2048x32 mesh "

@@ -1,0 +1,81 @@
+"""Energy-to-solution meter: NVML on the GPUs + RAPL on the host.
+
+Same duck type as the reference's PlatformCounterMeter (metrics.py:147-180):
+``start()`` latches the counters, ``joules(durations, freq_level)`` returns
+``{"total": J, ...}`` for the window since ``start()``. GPU energy comes from
+``nvmlDeviceGetTotalEnergyConsumption`` (mJ, per device); host energy from
+``/sys/class/powercap/intel-rapl:*/energy_uj`` package counters when they
+are readable (they are absent in some containers: the host part is then
+reported as None and ``total`` is the GPU energy alone, flagged by
+``host_available``). ``green_productivity`` is the paper's Eq. 4 exactly as
+metrics.py:200-207 computes it.
+"""
+
+from __future__ import annotations
+
+import glob
+from pathlib import Path
+
+
+def _rapl_domains():
+    doms = []
+    for d in sorted(glob.glob("/sys/class/powercap/intel-rapl:*")):
+        if ":" in Path(d).name[len("intel-rapl:"):]:
+            continue                      # sub-domains (core, uncore, dram) are inside the package
+        e = Path(d) / "energy_uj"
+        m = Path(d) / "max_energy_range_uj"
+        try:
+            int(e.read_text())
+            doms.append((e, int(m.read_text()) if m.exists() else 2 ** 32))
+        except (OSError, ValueError):
+            pass
+    return doms
+
+
+class NvmlRaplMeter:
+    def __init__(self, devices=None, host: bool = True):
+        import pynvml
+        self._nv = pynvml
+        pynvml.nvmlInit()
+        n = pynvml.nvmlDeviceGetCount()
+        idx = range(n) if devices is None else devices
+        self.handles = [pynvml.nvmlDeviceGetHandleByIndex(int(i)) for i in idx]
+        self.rapl = _rapl_domains() if host else []
+        self._g0 = self._h0 = None
+
+    @property
+    def host_available(self) -> bool:
+        return bool(self.rapl)
+
+    def _gpu_mj(self):
+        return [self._nv.nvmlDeviceGetTotalEnergyConsumption(h) for h in self.handles]
+
+    def _host_uj(self):
+        return [int(e.read_text()) for e, _ in self.rapl]
+
+    def start(self):
+        self._g0 = self._gpu_mj()
+        self._h0 = self._host_uj()
+
+    def joules(self, durations=None, freq_level: str = "default") -> dict:
+        if self._g0 is None:
+            self.start()
+        g1, h1 = self._gpu_mj(), self._host_uj()
+        gpu = sum(b - a for a, b in zip(self._g0, g1)) / 1e3
+        host = None
+        if self.rapl:
+            host = 0.0
+            for (e, wrap), a, b in zip(self.rapl, self._h0, h1):
+                host += ((b - a) % wrap) / 1e6
+        self._g0 = self._h0 = None
+        return {"total": gpu + (host or 0.0), "gpu": gpu, "host": host}
+
+
+def green_productivity(t_ref: float, e_ref: float, t_test: float, e_test: float,
+                       alpha: float = 1.0) -> float:
+    """GP = (t_ref / t_test) / (alpha * e_test / e_ref) (metrics.py:200-207)."""
+    if alpha <= 0:
+        raise ValueError("alpha must be positive")
+    if min(t_ref, e_ref, t_test, e_test) <= 0:
+        raise ValueError("times and energies must be positive")
+    return (t_ref / t_test) / (alpha * e_test / e_ref)
