@@ -75,15 +75,27 @@ static int set_device(wsb_ctx *ctx) {
 }
 
 // Device-side final sum of the per-column-block norm partials, in block order.
-__global__ void k_sum_partials(const double *p, int nb, double *out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// Chunks are staged in shared memory by the whole block (coalesced); one
+// thread adds them left to right, the association the multi-GPU root uses.
+__global__ void __launch_bounds__(256) k_sum_partials(const double *p, int nb, double *out) {
+    __shared__ double2 buf[1024];
     double si = 0.0, sr = 0.0;
-    for (int b = 0; b < nb; ++b) {
-        si += p[2 * b];
-        sr += p[2 * b + 1];
+    for (int base = 0; base < nb; base += 1024) {
+        const int n = min(1024, nb - base);
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            buf[i] = make_double2(p[2 * (base + i)], p[2 * (base + i) + 1]);
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int i = 0; i < n; ++i) {
+                si += buf[i].x;
+                sr += buf[i].y;
+            }
+        __syncthreads();
     }
-    out[0] = si;
-    out[1] = sr;
+    if (threadIdx.x == 0) {
+        out[0] = si;
+        out[1] = sr;
+    }
 }
 
 // P layout -> (plane, row, col) complex128 with the checkerboard sign removed.
@@ -356,7 +368,7 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
     WSB_TRY(fft_cols_stack(ctx, grid, 1, rows, 0, n_u / kG, gp, image_out, partials));
     WSB_CUDA_TRY(cudaEventRecord(ev[5], ctx->stream));
     const int nb = n_u;  // one norm partial per image column
-    k_sum_partials<<<1, 32, 0, ctx->stream>>>(partials, nb, partials + 2 * (size_t)n_u);
+    k_sum_partials<<<1, 256, 0, ctx->stream>>>(partials, nb, partials + 2 * (size_t)n_u);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     WSB_CUDA_TRY(cudaEventRecord(ev[6], ctx->stream));

@@ -1,25 +1,26 @@
-// K1b: bucketing of a slab's records by (w plane, 32-column tile, anchor row).
+// K1b: bucketing of a slab's records by (w plane, 32-column strip, anchor row).
 //
 // The reference gives every slab the records of exchange_to_space_order in
 // (time_index, gindex) order (comms.py:534-545) and grids them tap-major
 // (gridder.py:160-183). The sweep gridder (grid.cu) instead walks each
 // 32-column strip of a plane down its rows, so it needs the strip's records
-// sorted by anchor row floor(gv). This file builds that order with a
-// counting sort over the dense key
+// sorted by anchor row floor(gv). Every (record, strip) pair becomes one
+// entry with the dense key
 //     key = (plane * n_tc + tc) * RS + (floor(gv) - v_start + S),
 //     RS  = v_count + 2S (anchor rows that can touch the slab),
-// a record being listed once per tile column its footprint reaches.
-// Slots are claimed with atomics, then every bucket is sorted by record
-// index, so the final order is (key, record index): deterministic and, since
-// the record index follows gindex, independent of the GPU count.
+// written in record order (block-stable compaction), then sorted by a
+// stable LSD radix sort (sort.cu). The final order is (key, record index):
+// deterministic, independent of how skewed the buckets are (LOFAR-like
+// tracks put millions of records into a few buckets), and -- the record
+// index following gindex -- independent of the GPU count. Bucket offsets
+// come from a key histogram.
 #include "wsb_internal.cuh"
 
 namespace wsb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kSmallBucket = 32;     // insertion-sorted by one thread
-constexpr int kMidBucket = 8192;     // bitonic-sorted in shared memory by one CTA
+constexpr int kBlockItems = 2048;  // records per block
 
 struct KeyGeom {
     int n_u, v_start, v_count, S, n_tc, rs;
@@ -38,7 +39,7 @@ __device__ __forceinline__ bool tap_range(double g, int S, int lo, int hi, int *
     return *a <= *b;
 }
 
-// Returns the number of tile columns (0, 1 or 2) and the first key.
+// Number of strips (0, 1 or 2) a record reaches and its first key.
 __device__ __forceinline__ int record_keys(const double4 &r, uint32_t plane, const KeyGeom &k,
                                            uint32_t *key0) {
     int i0, i1, j0, j1;
@@ -51,89 +52,78 @@ __device__ __forceinline__ int record_keys(const double4 &r, uint32_t plane, con
     return tc1 - tc0 + 1;
 }
 
-__global__ void __launch_bounds__(kThreads) k_bkt_count(const double4 *__restrict__ rec,
-                                                        const uint32_t *__restrict__ plane,
-                                                        int64_t m, KeyGeom k,
-                                                        uint32_t *__restrict__ cnt) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t key;
-        const int n = record_keys(rec[i], plane[i], k, &key);
-        for (int t = 0; t < n; ++t) atomicAdd(&cnt[key + t * k.rs], 1u);
+__device__ __forceinline__ uint32_t block_excl_sum(uint32_t x, uint32_t *total, uint32_t *smem) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
     }
-}
-
-__global__ void __launch_bounds__(kThreads) k_bkt_scatter(const double4 *__restrict__ rec,
-                                                          const uint32_t *__restrict__ plane,
-                                                          int64_t m, KeyGeom k,
-                                                          const uint32_t *__restrict__ off,
-                                                          uint32_t *__restrict__ fill,
-                                                          uint32_t *__restrict__ idx) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t key;
-        const int n = record_keys(rec[i], plane[i], k, &key);
-        for (int t = 0; t < n; ++t) {
-            const uint32_t kk = key + t * k.rs;
-            idx[off[kk] + atomicAdd(&fill[kk], 1u)] = (uint32_t)i;
-        }
-    }
-}
-
-// Small buckets: insertion sort by one thread. Larger ones are listed.
-__global__ void __launch_bounds__(kThreads) k_bkt_fix(const uint32_t *__restrict__ off,
-                                                      int64_t n_keys, uint32_t *__restrict__ idx,
-                                                      uint32_t *__restrict__ big,
-                                                      uint32_t *__restrict__ n_big) {
-    const int64_t key = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (key >= n_keys) return;
-    const uint32_t b = off[key], e = off[key + 1], n = e - b;
-    if (n < 2) return;
-    if (n > kSmallBucket) {
-        big[atomicAdd(n_big, 1u)] = (uint32_t)key;
-        return;
-    }
-    uint32_t *p = idx + b;
-    for (uint32_t i = 1; i < n; ++i) {
-        const uint32_t x = p[i];
-        uint32_t j = i;
-        while (j > 0 && p[j - 1] > x) {
-            p[j] = p[j - 1];
-            --j;
-        }
-        p[j] = x;
-    }
-}
-
-// Mid buckets (<= kMidBucket): bitonic sort in shared memory, one CTA each.
-__global__ void __launch_bounds__(1024) k_bkt_fix_mid(const uint32_t *__restrict__ off,
-                                                      const uint32_t *__restrict__ big,
-                                                      uint32_t *__restrict__ idx) {
-    __shared__ uint32_t s[kMidBucket];
-    const uint32_t key = big[blockIdx.x];
-    const uint32_t b = off[key], n = off[key + 1] - b;
-    if (n > kMidBucket) return;  // handled on the host path
-    uint32_t p2 = 1;
-    while (p2 < n) p2 <<= 1;
-    for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) s[i] = i < n ? idx[b + i] : 0xFFFFFFFFu;
+    if (lane == 31) smem[warp] = incl;
     __syncthreads();
-    for (uint32_t size = 2; size <= p2; size <<= 1) {
-        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) {
-                const uint32_t j = i ^ stride;
-                if (j > i) {
-                    const bool up = (i & size) == 0;
-                    const uint32_t a = s[i], c = s[j];
-                    if ((a > c) == up) {
-                        s[i] = c;
-                        s[j] = a;
-                    }
-                }
-            }
-            __syncthreads();
+    uint32_t base = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < kThreads / 32; ++k) {
+        const uint32_t s = smem[k];
+        if (k < warp) base += s;
+        tot += s;
+    }
+    __syncthreads();
+    *total = tot;
+    return base + incl - x;
+}
+
+// entries per block (for the compaction) and the key histogram
+__global__ void __launch_bounds__(kThreads) k_keys_count(const double4 *__restrict__ rec,
+                                                         const uint32_t *__restrict__ plane,
+                                                         int64_t m, KeyGeom k,
+                                                         uint32_t *__restrict__ block_cnt,
+                                                         uint32_t *__restrict__ key_cnt) {
+    __shared__ uint32_t c;
+    if (threadIdx.x == 0) c = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kBlockItems;
+    uint32_t local = 0;
+    for (int it = 0; it < kBlockItems / kThreads; ++it) {
+        const int64_t i = base + it * kThreads + threadIdx.x;
+        if (i < m) {
+            uint32_t key;
+            const int n = record_keys(rec[i], plane[i], k, &key);
+            for (int t = 0; t < n; ++t) atomicAdd(&key_cnt[key + t * k.rs], 1u);
+            local += n;
         }
     }
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) idx[b + i] = s[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&c, local);
+    __syncthreads();
+    if (threadIdx.x == 0) block_cnt[blockIdx.x] = c;
+}
+
+// (key, record) entries in record order
+__global__ void __launch_bounds__(kThreads) k_keys_write(const double4 *__restrict__ rec,
+                                                         const uint32_t *__restrict__ plane,
+                                                         int64_t m, KeyGeom k,
+                                                         const uint32_t *__restrict__ block_off,
+                                                         uint32_t *__restrict__ keys,
+                                                         uint32_t *__restrict__ idx) {
+    __shared__ uint32_t wsum[kThreads / 32];
+    uint32_t run = block_off[blockIdx.x];
+    const int64_t base = (int64_t)blockIdx.x * kBlockItems;
+    for (int it = 0; it < kBlockItems / kThreads; ++it) {
+        const int64_t i = base + it * kThreads + threadIdx.x;
+        uint32_t key = 0;
+        int n = 0;
+        if (i < m) n = record_keys(rec[i], plane[i], k, &key);
+        uint32_t tot;
+        uint32_t pos = run + block_excl_sum((uint32_t)n, &tot, wsum);
+        for (int t = 0; t < n; ++t) {
+            keys[pos + t] = key + t * k.rs;
+            idx[pos + t] = (uint32_t)i;
+        }
+        run += tot;
+    }
 }
 
 }  // namespace
@@ -149,70 +139,42 @@ int bucket_rows(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_count
     k.rs = v_count + 2 * S;
     const int64_t n_keys = (int64_t)g->n_w * k.n_tc * k.rs;
     if (n_keys >= 0xFFFFFFFFll) return fail(WSB_EUNSUPPORTED, "bucket key space exceeds 32 bits");
-    uint32_t *cnt, *off, *fill, *idx, *big;
+    uint32_t *cnt, *off;
     WSB_TRY(ensure(ctx, kSlotTileCount, sizeof(uint32_t) * (n_keys + 1), (void **)&cnt));
     WSB_TRY(ensure(ctx, kSlotTileOff, sizeof(uint32_t) * (n_keys + 1), (void **)&off));
-    WSB_TRY(ensure(ctx, kSlotKeysA, sizeof(uint32_t) * (n_keys + 1), (void **)&fill));
     WSB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (n_keys + 1), ctx->stream));
-    WSB_CUDA_TRY(cudaMemsetAsync(fill, 0, sizeof(uint32_t) * (n_keys + 1), ctx->stream));
-    const int grid = (int)std::min<int64_t>(std::max<int64_t>(1, ceil_div(m, kThreads)), 148 * 16);
+    const int nb = std::max(1, ceil_div(m, kBlockItems));
+    uint32_t *bcnt, *boff;
+    WSB_TRY(ensure(ctx, kSlotBlockCounts, sizeof(uint32_t) * (nb + 1), (void **)&bcnt));
+    WSB_TRY(ensure(ctx, kSlotBlockOffsets, sizeof(uint32_t) * (nb + 1), (void **)&boff));
+    uint32_t total = 0;
     if (m > 0) {
-        k_bkt_count<<<grid, kThreads, 0, ctx->stream>>>((const double4 *)rec, plane, m, k, cnt);
+        k_keys_count<<<nb, kThreads, 0, ctx->stream>>>((const double4 *)rec, plane, m, k, bcnt, cnt);
+        ctx->launches += 1;
+        WSB_CUDA_TRY(cudaGetLastError());
+        WSB_TRY(exclusive_scan_u32(ctx, bcnt, boff, nb, &total));
+    }
+    WSB_TRY(exclusive_scan_u32(ctx, cnt, off, n_keys + 1, nullptr));
+    const size_t eb = sizeof(uint32_t) * std::max<int64_t>(1, total);
+    uint32_t *ka, *kb, *ia, *ib;
+    WSB_TRY(ensure(ctx, kSlotKeysA, eb, (void **)&ka));
+    WSB_TRY(ensure(ctx, kSlotKeysB, eb, (void **)&kb));
+    WSB_TRY(ensure(ctx, kSlotIdxA, eb, (void **)&ia));
+    WSB_TRY(ensure(ctx, kSlotIdxB, eb, (void **)&ib));
+    if (total > 0) {
+        k_keys_write<<<nb, kThreads, 0, ctx->stream>>>((const double4 *)rec, plane, m, k, boff, ka, ia);
         ctx->launches += 1;
         WSB_CUDA_TRY(cudaGetLastError());
     }
-    uint32_t total = 0;
-    WSB_TRY(exclusive_scan_u32(ctx, cnt, off, n_keys + 1, &total));
-    const int64_t ne = std::max<uint32_t>(total, 1);
-    WSB_TRY(ensure(ctx, kSlotIdxA, sizeof(uint32_t) * ne, (void **)&idx));
-    WSB_TRY(ensure(ctx, kSlotIdxB, sizeof(uint32_t) * (ne / (kSmallBucket + 1) + 2), (void **)&big));
-    uint32_t *n_big;
-    WSB_TRY(ensure(ctx, kSlotU64, 64, (void **)&n_big));
-    n_big += 2;  // bytes 8..11 of the u64 slot (0..7 hold the update counter)
-    WSB_CUDA_TRY(cudaMemsetAsync(n_big, 0, sizeof(uint32_t), ctx->stream));
-    if (total > 0) {
-        k_bkt_scatter<<<grid, kThreads, 0, ctx->stream>>>((const double4 *)rec, plane, m, k, off,
-                                                          fill, idx);
-        k_bkt_fix<<<ceil_div(n_keys, kThreads), kThreads, 0, ctx->stream>>>(off, n_keys, idx, big,
-                                                                           n_big);
-        ctx->launches += 2;
-        WSB_CUDA_TRY(cudaGetLastError());
-        uint32_t nb = 0;
-        WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host, n_big, 4, cudaMemcpyDeviceToHost, ctx->stream));
-        WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-        nb = (uint32_t)ctx->flag_host[0];
-        if (nb > 0) {
-            k_bkt_fix_mid<<<nb, 1024, 0, ctx->stream>>>(off, big, idx);
-            ctx->launches += 1;
-            WSB_CUDA_TRY(cudaGetLastError());
-            // buckets beyond kMidBucket: stable radix sort of the segment by record index
-            std::vector<uint32_t> keys(nb);
-            WSB_CUDA_TRY(cudaMemcpyAsync(keys.data(), big, 4 * nb, cudaMemcpyDeviceToHost, ctx->stream));
-            WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-            for (uint32_t kk : keys) {
-                uint32_t be[2];
-                WSB_CUDA_TRY(cudaMemcpy(be, off + kk, 8, cudaMemcpyDeviceToHost));
-                const uint32_t n = be[1] - be[0];
-                if (n <= (uint32_t)kMidBucket) continue;
-                uint32_t *ka, *kb, *va, *vb, *ko, *vo;
-                WSB_TRY(ensure(ctx, kSlotKeysB, 4 * (size_t)n, (void **)&ka));
-                WSB_TRY(ensure(ctx, kSlotRadixTmpA, 4 * (size_t)n, (void **)&kb));
-                WSB_TRY(ensure(ctx, kSlotRadixTmpB, 4 * (size_t)n, (void **)&va));
-                WSB_TRY(ensure(ctx, kSlotRadixTmpC, 4 * (size_t)n, (void **)&vb));
-                WSB_CUDA_TRY(cudaMemcpyAsync(ka, idx + be[0], 4 * (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
-                WSB_CUDA_TRY(cudaMemcpyAsync(va, idx + be[0], 4 * (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
-                WSB_TRY(radix_sort_pairs(ctx, ka, kb, va, vb, n, 32, &ko, &vo));
-                WSB_CUDA_TRY(cudaMemcpyAsync(idx + be[0], ko, 4 * (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
-            }
-        }
-    }
-    out->idx = idx;
+    uint32_t *ks, *is;
+    WSB_TRY(radix_sort_pairs(ctx, ka, kb, ia, ib, total, ilog2(n_keys), &ks, &is));
+    out->idx = is;
     out->off = off;
     out->n_entries = total;
     out->n_keys = n_keys;
     out->n_tc = k.n_tc;
     out->rs = k.rs;
-    ctx->last_idx = idx;
+    ctx->last_idx = is;
     ctx->last_off = off;
     ctx->last_entries = total;
     ctx->last_tiles = n_keys;

@@ -139,17 +139,34 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_scatter(
         __syncwarp();
     }
     __syncthreads();
+    // block-local start of each digit run (exclusive scan over the 256
+    // digits of the block totals) and the start of each warp inside it
+    __shared__ uint32_t bstart[256], goff[256], wsum[kRsWarps];
     {
         const int d = threadIdx.x;  // 256 threads == 256 digits
-        uint32_t run = offs[(int64_t)d * nb + blockIdx.x];
+        uint32_t tot = 0;
 #pragma unroll
         for (int w = 0; w < kRsWarps; ++w) {
-            uint32_t c = wc[w][d];
-            wc[w][d] = run;
-            run += c;
+            const uint32_t c = wc[w][d];
+            wc[w][d] = tot;
+            tot += c;
         }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        uint32_t wbase = 0;
+        for (int w = 0; w < warp; ++w) wbase += wsum[w];
+        bstart[d] = wbase + incl - tot;
+        goff[d] = offs[(int64_t)d * nb + blockIdx.x];
     }
     __syncthreads();
+    // stable rank inside the block -> shared-memory staging in digit order
+    __shared__ uint32_t ks[kRsItems], vs[kRsItems];
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int r = 0; r < kRsIpt; ++r) {
@@ -158,14 +175,24 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_scatter(
         uint32_t d = ok ? (k[r] >> shift) & 255u : 256u;
         uint32_t peers = __match_any_sync(0xffffffffu, d);
         uint32_t pos = 0;
-        if (ok) pos = wc[warp][d] + __popc(peers & lt);
+        if (ok) pos = bstart[d] + wc[warp][d] + __popc(peers & lt);
         __syncwarp();
         if (ok && lane == __ffs(peers) - 1) wc[warp][d] += __popc(peers);
         __syncwarp();
         if (ok) {
-            kout[pos] = k[r];
-            vout[pos] = v[r];
+            ks[pos] = k[r];
+            vs[pos] = v[r];
         }
+    }
+    __syncthreads();
+    // consecutive threads write consecutive positions of each digit run
+    const int64_t nblk = min((int64_t)kRsItems, n - (int64_t)blockIdx.x * kRsItems);
+    for (int p = threadIdx.x; p < nblk; p += kRsThreads) {
+        const uint32_t key = ks[p];
+        const uint32_t d = (key >> shift) & 255u;
+        const uint32_t gpos = goff[d] + (p - bstart[d]);
+        kout[gpos] = key;
+        vout[gpos] = vs[p];
     }
 }
 

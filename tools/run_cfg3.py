@@ -1,0 +1,97 @@
+"""BASELINE config 3 (north star): 100M LOFAR-like track records,
+4096x4096x64, Gaussian support 7, FP64. Single process (1 GPU) or torchrun
+(v-slab over N GPUs). Prints kernel/step timings and a linearity check
+(image(a + b) == image(a) + image(b) within FP64 roundoff), a property that
+holds at any size."""
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path[:0] = [str(ROOT), str(ROOT / "tools")]
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2504_00959_b200 as W  # noqa: E402
+from lofar import tracks  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=100_000_000)
+    ap.add_argument("--nu", type=int, default=4096)
+    ap.add_argument("--nw", type=int, default=64)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--check", action="store_true")
+    a = ap.parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        from paper_2504_00959_b200.distributed import image_distributed
+    cell = 1e-4
+    spec = W.GridSpec(a.nu, a.nu, a.nw, cell, w_max_native=1000.0)
+    kern = W.KernelSpec.gaussian(3, 1.0)
+    per = a.n // ws
+    t0 = time.perf_counter()
+    u, v, w, t, vis, wt = tracks(a.n, cell, first=rank * per, count=per, device=dev)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+
+    def run(vv=vis):
+        if ws > 1:
+            img, d = image_distributed(u, v, w, vv, wt, spec, kern, to_host=False)
+            return (img.pixels if img is not None else None), d
+        return W.image_device(u, v, w, vv, wt, spec, kern)
+
+    run()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        pix, d = run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    if ws > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    out = {"config": "cfg3 LOFAR-like tracks", "records": a.n, "grid": [a.nu, a.nu, a.nw],
+           "n_gpus": ws, "ms_per_step": round(ms, 3), "mvis_s": round(a.n / ms / 1e3, 1),
+           "grid_updates": d["grid_updates"], "generate_s": round(gen_s, 2)}
+    if ws == 1:
+        kms, _ = W.last_timings(dev)
+        out["kernel_ms"] = [round(x, 3) for x in kms]
+    if a.check:
+        # linearity: image(vis_a + vis_b) = image(vis_a) + image(vis_b)
+        g = torch.Generator(device=dev).manual_seed(7)
+        va = (torch.randn(vis.shape, generator=g, device=dev, dtype=torch.float32)
+              + 1j * torch.randn(vis.shape, generator=g, device=dev, dtype=torch.float32)).to(torch.complex64)
+        vb = (vis - va).to(torch.complex64)
+        pa, _ = run(va)
+        pa = None if pa is None else pa.clone()
+        pb, _ = run(vb)
+        pb = None if pb is None else pb.clone()
+        pab, _ = run((va + vb).to(torch.complex64))
+        if pab is not None:
+            err = float((pab - pa - pb).norm() / pab.norm())
+            out["linearity_rel_l2"] = err
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
