@@ -184,8 +184,10 @@ struct SweepArgs {
     double2 *out;                 // strip layout [n_w][ceil(n_u/32)][v_count][32]
     unsigned long long *updates;
     const double *i0beta;         // device scalar, np.i0(beta) (Kaiser-Bessel)
+    const uint4 *parts;           // (item, first entry, end entry, slot | ~0 = direct)
+    double2 *partial;             // [slot][kRowBlock][32] partial tiles of split items
     int n_u, v_start, v_count, n_tc, rs, n_rb, n_groups;
-    int64_t n_items;
+    int64_t n_items, n_parts;
 };
 
 template <int S>
@@ -207,8 +209,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, WSB_GRID_MINB) k_grid_sweep
     __shared__ __align__(16) St stage_all[kWarpsPerCta];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     St &st = stage_all[warp];
-    const int64_t item = (int64_t)blockIdx.x * kWarpsPerCta + warp;
-    if (item >= a.n_items) return;
+    const int64_t part = (int64_t)blockIdx.x * kWarpsPerCta + warp;
+    if (part >= a.n_parts) return;
+    // work part = (item, record sub-range, partial-tile slot or direct)
+    const uint4 pd = a.parts[part];
+    const int64_t item = pd.x;
     // item -> (plane, strip, row block); row block fastest
     const int rb = (int)(item % a.n_rb);
     const int64_t pt = item / a.n_rb;
@@ -220,12 +225,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, WSB_GRID_MINB) k_grid_sweep
     const int ncols = min(32, a.n_u - col0);
     const int R0 = a.v_start + rb * kRowBlock;
     const int R1 = min(R0 + kRowBlock, a.v_start + a.v_count);
-    const uint32_t kbase = ((uint32_t)plane * a.n_tc + tc) * (uint32_t)a.rs;
-    const uint32_t beg = a.off[kbase + (R0 - a.v_start)];
-    const uint32_t end = a.off[kbase + (R1 - 1 - a.v_start + 2 * S) + 1];
+    const uint32_t beg = pd.y, end = pd.z;
+    const bool direct = pd.w == 0xFFFFFFFFu;
     const double i0b = KIND == WSB_KERNEL_KAISER_BESSEL ? *a.i0beta : 0.0;
-    // strip layout [plane][strip][row][32]: an emitted row is one 512-byte run
-    const int64_t colbase = ((int64_t)plane * a.n_tc + tc) * a.v_count;
+    // strip layout [plane][strip][row][32]: an emitted row is one 512-byte run;
+    // a split item writes its unsigned partial tile [slot][row - R0][32]
+    const int64_t colbase = direct ? ((int64_t)plane * a.n_tc + tc) * a.v_count + (R0 - a.v_start)
+                                   : (int64_t)pd.w * kRowBlock;
+    double2 *const out = direct ? a.out : a.partial;
     st.wu[lane][W] = 0.0;
 
     // Window of W rows kept as a ring of W register slots: row `base` is in
@@ -245,9 +252,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, WSB_GRID_MINB) k_grid_sweep
     auto emit_slot = [&](auto P) {
         constexpr int p = decltype(P)::value;
         if (base >= R0 && base < R1 && col_ok) {
-            const double s = ((col + base) & 1) ? -1.0 : 1.0;
-            a.out[(colbase + (base - a.v_start)) * 32 + lane] =
-                make_double2(acc[p].x * s, acc[p].y * s);
+            const double s = (direct && ((col + base) & 1)) ? -1.0 : 1.0;
+            out[(colbase + (base - R0)) * 32 + lane] = make_double2(acc[p].x * s, acc[p].y * s);
         }
         acc[p] = make_double2(0.0, 0.0);
         ++base;
@@ -350,7 +356,7 @@ int launch_s(wsb_ctx *ctx, const SweepArgs &a, double p0) {
             kp.cm[k] = std::exp(-(m * m) / p0);
         }
     }
-    const int64_t blocks = (a.n_items + kWarpsPerCta - 1) / kWarpsPerCta;
+    const int64_t blocks = (a.n_parts + kWarpsPerCta - 1) / kWarpsPerCta;
     k_grid_sweep<KIND, S><<<(unsigned)blocks, 32 * kWarpsPerCta, 0, ctx->stream>>>(a, kp);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
@@ -368,6 +374,90 @@ int launch_kind(wsb_ctx *ctx, int S, const SweepArgs &a, double p0) {
         case 6: return launch_s<KIND, 6>(ctx, a, p0);
         case 7: return launch_s<KIND, 7>(ctx, a, p0);
         default: return fail(WSB_EUNSUPPORTED, "half_support > 7 not compiled in this build");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Load balancing. Earth-rotation tracks pile millions of records into a few
+// (plane, strip, row block) items. An item with more than kPartRecords
+// records is split into equal consecutive sub-ranges of its (sorted) list;
+// each part sweeps the item into its own partial tile, and k_combine adds
+// the parts in part order (fixed association: deterministic, and the same
+// split for any GPU count since items never straddle slabs).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kPartRecords = 4096;
+
+__device__ __forceinline__ void item_range(const SweepArgs &a, int S, int64_t item, uint32_t *b,
+                                           uint32_t *e) {
+    const int rb = (int)(item % a.n_rb);
+    const int64_t pt = item / a.n_rb;
+    const int tc = (int)(pt % a.n_tc), plane = (int)(pt / a.n_tc);
+    const int R0 = a.v_start + rb * kRowBlock;
+    const int R1 = min(R0 + kRowBlock, a.v_start + a.v_count);
+    const uint32_t kbase = ((uint32_t)plane * a.n_tc + tc) * (uint32_t)a.rs;
+    *b = a.off[kbase + (R0 - a.v_start)];
+    *e = a.off[kbase + (R1 - 1 - a.v_start + 2 * S) + 1];
+}
+
+__global__ void k_item_parts(SweepArgs a, int S, uint32_t *nparts, uint32_t *nslots,
+                             uint32_t *split) {
+    const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= a.n_items) return;
+    uint32_t b, e;
+    item_range(a, S, item, &b, &e);
+    const uint32_t np = e - b > kPartRecords ? (e - b + kPartRecords - 1) / kPartRecords : 1;
+    nparts[item] = np;
+    nslots[item] = np > 1 ? np : 0;
+    split[item] = np > 1 ? 1 : 0;
+}
+
+__global__ void k_build_parts(SweepArgs a, int S, const uint32_t *part_off, const uint32_t *slot_off,
+                              const uint32_t *split_off, uint4 *parts, uint2 *split_items) {
+    const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= a.n_items) return;
+    uint32_t b, e;
+    item_range(a, S, item, &b, &e);
+    const uint32_t np = part_off[item + 1] - part_off[item];
+    if (np == 1) {
+        parts[part_off[item]] = make_uint4((uint32_t)item, b, e, 0xFFFFFFFFu);
+        return;
+    }
+    const uint32_t chunk = (e - b + np - 1) / np;
+    for (uint32_t p = 0; p < np; ++p) {
+        const uint32_t pb = min(e, b + p * chunk), pe = min(e, pb + chunk);
+        parts[part_off[item] + p] = make_uint4((uint32_t)item, pb, pe, slot_off[item] + p);
+    }
+    split_items[split_off[item]] = make_uint2((uint32_t)item, slot_off[item]);
+}
+
+// one warp per row of a split item: sum its parts' partial rows in part order
+__global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split_items,
+                                                  const uint32_t *part_off) {
+    const uint2 si = split_items[blockIdx.x];
+    const int64_t item = si.x;
+    const int np = (int)(part_off[item + 1] - part_off[item]);
+    const int rb = (int)(item % a.n_rb);
+    const int64_t pt = item / a.n_rb;
+    const int tc = (int)(pt % a.n_tc), plane = (int)(pt / a.n_tc);
+    const int R0 = a.v_start + rb * kRowBlock;
+    const int R1 = min(R0 + kRowBlock, a.v_start + a.v_count);
+    const int lane = threadIdx.x & 31;
+    const int col = tc * 32 + lane;
+    for (int r = blockIdx.y * 4 + (threadIdx.x >> 5); r < kRowBlock; r += gridDim.y * 4) {
+        const int row = R0 + r;
+        if (row >= R1) break;
+        double2 acc = make_double2(0.0, 0.0);
+        const double2 *src = a.partial + ((int64_t)si.y * kRowBlock + r) * 32 + lane;
+        for (int p = 0; p < np; ++p) {
+            const double2 z = src[(int64_t)p * kRowBlock * 32];
+            acc.x += z.x;
+            acc.y += z.y;
+        }
+        if (col < a.n_u) {
+            const double s = ((col + row) & 1) ? -1.0 : 1.0;
+            a.out[(((int64_t)plane * a.n_tc + tc) * a.v_count + (row - a.v_start)) * 32 + lane] =
+                make_double2(acc.x * s, acc.y * s);
+        }
     }
 }
 
@@ -392,15 +482,57 @@ int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
     a.n_groups = g->n_u / kG;
     a.n_items = (int64_t)g->n_w * a.n_tc * a.n_rb;
     if (a.n_items <= 0) return WSB_OK;
-    if (k->kind == WSB_KERNEL_GAUSSIAN)  // s2 = 2 sigma^2 (gridder.py:85)
-        return launch_kind<WSB_KERNEL_GAUSSIAN>(ctx, k->half_support, a,
-                                                2.0 * k->shape_param * k->shape_param);
-    double *i0b;
-    WSB_TRY(ensure(ctx, kSlotFlag, 64, (void **)&i0b));
-    k_i0<<<1, 1, 0, ctx->stream>>>(k->shape_param, i0b + 4);  // slot bytes 32..39
+    const int S = k->half_support;
+    // ---- work parts (split heavy items) ------------------------------------
+    const int64_t ni = a.n_items;
+    uint32_t *np, *ns, *sp, *np_off, *ns_off, *sp_off;
+    WSB_TRY(ensure(ctx, kSlotPartCnt, sizeof(uint32_t) * 3 * (ni + 1), (void **)&np));
+    WSB_TRY(ensure(ctx, kSlotPartOff, sizeof(uint32_t) * 3 * (ni + 1), (void **)&np_off));
+    ns = np + (ni + 1);
+    sp = ns + (ni + 1);
+    ns_off = np_off + (ni + 1);
+    sp_off = ns_off + (ni + 1);
+    WSB_CUDA_TRY(cudaMemsetAsync(np, 0, sizeof(uint32_t) * 3 * (ni + 1), ctx->stream));
+    k_item_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(a, S, np, ns, sp);
     ctx->launches += 1;
-    a.i0beta = i0b + 4;
-    return launch_kind<WSB_KERNEL_KAISER_BESSEL>(ctx, k->half_support, a, k->shape_param);
+    WSB_CUDA_TRY(cudaGetLastError());
+    uint32_t n_parts = 0, n_slots = 0, n_split = 0;
+    WSB_TRY(exclusive_scan_u32(ctx, np, np_off, ni + 1, &n_parts));
+    WSB_TRY(exclusive_scan_u32(ctx, ns, ns_off, ni + 1, &n_slots));
+    WSB_TRY(exclusive_scan_u32(ctx, sp, sp_off, ni + 1, &n_split));
+    uint4 *parts;
+    uint2 *split_items;
+    double2 *partial = nullptr;
+    WSB_TRY(ensure(ctx, kSlotParts, sizeof(uint4) * n_parts + sizeof(uint2) * (n_split + 1),
+                   (void **)&parts));
+    split_items = reinterpret_cast<uint2 *>(parts + n_parts);
+    if (n_slots)
+        WSB_TRY(ensure(ctx, kSlotPartial, sizeof(double2) * (size_t)n_slots * kRowBlock * 32,
+                       (void **)&partial));
+    k_build_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(a, S, np_off, ns_off, sp_off, parts,
+                                                              split_items);
+    ctx->launches += 1;
+    WSB_CUDA_TRY(cudaGetLastError());
+    a.parts = parts;
+    a.partial = partial;
+    a.n_parts = n_parts;
+    // ---- sweep ---------------------------------------------------------------
+    int rc;
+    if (k->kind == WSB_KERNEL_GAUSSIAN) {  // s2 = 2 sigma^2 (gridder.py:85)
+        rc = launch_kind<WSB_KERNEL_GAUSSIAN>(ctx, S, a, 2.0 * k->shape_param * k->shape_param);
+    } else {
+        double *i0b;
+        WSB_TRY(ensure(ctx, kSlotFlag, 64, (void **)&i0b));
+        k_i0<<<1, 1, 0, ctx->stream>>>(k->shape_param, i0b + 4);  // slot bytes 32..39
+        ctx->launches += 1;
+        a.i0beta = i0b + 4;
+        rc = launch_kind<WSB_KERNEL_KAISER_BESSEL>(ctx, S, a, k->shape_param);
+    }
+    if (rc != WSB_OK || n_split == 0) return rc;
+    k_combine<<<dim3(n_split, kRowBlock / 4 / 4), 128, 0, ctx->stream>>>(a, split_items, np_off);
+    ctx->launches += 1;
+    WSB_CUDA_TRY(cudaGetLastError());
+    return WSB_OK;
 }
 
 }  // namespace wsb

@@ -85,6 +85,10 @@ enum Slot {
     kSlotStrip,
     kSlotNorms,
     kSlotHostIn,
+    kSlotPartCnt,
+    kSlotPartOff,
+    kSlotParts,
+    kSlotPartial,
     kSlotRadixTmpA,
     kSlotRadixTmpB,
     kSlotRadixTmpC,
