@@ -102,19 +102,28 @@ constexpr int kRsPerWarp = 32 * kRsIpt;         // 512
 __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const uint32_t *__restrict__ keys,
                                                            int64_t n, int shift,
                                                            uint32_t *hist, int nb) {
-    __shared__ uint32_t h[256];
-    h[threadIdx.x] = 0;
+    // one sub-histogram per warp (shared-memory atomics, little contention),
+    // all loads of a thread issued up front
+    __shared__ uint32_t h[kRsWarps][256];
+    const int warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int w = 0; w < kRsWarps; ++w) h[w][threadIdx.x] = 0;
     __syncthreads();
     const int64_t base = (int64_t)blockIdx.x * kRsItems;
-    const int lane = threadIdx.x & 31;
+    uint32_t d[kRsIpt];
+#pragma unroll
     for (int r = 0; r < kRsIpt; ++r) {
-        int64_t i = base + (int64_t)r * kRsThreads + threadIdx.x;
-        uint32_t d = i < n ? (keys[i] >> shift) & 255u : 256u;
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
-        if (d < 256u && lane == __ffs(peers) - 1) atomicAdd(&h[d], (uint32_t)__popc(peers));
+        const int64_t i = base + (int64_t)r * kRsThreads + threadIdx.x;
+        d[r] = i < n ? (__ldg(&keys[i]) >> shift) & 255u : 256u;
     }
+#pragma unroll
+    for (int r = 0; r < kRsIpt; ++r)
+        if (d[r] < 256u) atomicAdd(&h[warp][d[r]], 1u);
     __syncthreads();
-    hist[(int64_t)threadIdx.x * nb + blockIdx.x] = h[threadIdx.x];
+    uint32_t s = 0;
+#pragma unroll
+    for (int w = 0; w < kRsWarps; ++w) s += h[w][threadIdx.x];
+    hist[(int64_t)threadIdx.x * nb + blockIdx.x] = s;
 }
 
 __global__ void __launch_bounds__(kRsThreads) k_radix_scatter(
@@ -126,16 +135,20 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_scatter(
     for (int i = 0; i < 8; ++i) wc[warp][lane + 32 * i] = 0;
     __syncwarp();
     const int64_t base = (int64_t)blockIdx.x * kRsItems + warp * kRsPerWarp;
-    uint32_t k[kRsIpt], v[kRsIpt];
+    uint32_t k[kRsIpt], v[kRsIpt], pm[kRsIpt];
 #pragma unroll
     for (int r = 0; r < kRsIpt; ++r) {
         int64_t i = base + r * 32 + lane;
         bool ok = i < n;
         k[r] = ok ? kin[i] : 0u;
         v[r] = ok ? vin[i] : 0u;
-        uint32_t d = ok ? (k[r] >> shift) & 255u : 256u;
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
-        if (d < 256u && lane == __ffs(peers) - 1) wc[warp][d] += __popc(peers);
+    }
+#pragma unroll
+    for (int r = 0; r < kRsIpt; ++r) {
+        const bool ok = base + r * 32 + lane < n;
+        const uint32_t d = ok ? (k[r] >> shift) & 255u : 256u;
+        pm[r] = __match_any_sync(0xffffffffu, d);
+        if (d < 256u && lane == __ffs(pm[r]) - 1) wc[warp][d] += __popc(pm[r]);
         __syncwarp();
     }
     __syncthreads();
@@ -173,7 +186,7 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_scatter(
         int64_t i = base + r * 32 + lane;
         bool ok = i < n;
         uint32_t d = ok ? (k[r] >> shift) & 255u : 256u;
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t peers = pm[r];
         uint32_t pos = 0;
         if (ok) pos = bstart[d] + wc[warp][d] + __popc(peers & lt);
         __syncwarp();
