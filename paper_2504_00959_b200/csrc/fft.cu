@@ -35,30 +35,29 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 // |r| <= 1/4, then Taylor polynomials of sin(pi r)/r (degree 16) and
 // cos(pi r) (degree 16) in r^2, truncation < 1e-18; about a third of the
 // instructions of the library sincospi, a few ulp from it.
+// FP64 constants live in the constant bank: DFMA takes c[][] operands
+// directly, whereas literals are rebuilt with two UMOVs each per use.
+__constant__ double kSinPiC[10] = {3.141592653589793, -5.16771278004997, 2.5501640398773455,
+                                   -0.5992645293207921, 0.08214588661112823,
+                                   -0.0073704309457143504, 0.00046630280576761255,
+                                   -2.1915353447830217e-05, 7.952054001475513e-07,
+                                   -2.2948428997269873e-08};
+__constant__ double kCosPiC[9] = {1.0, -4.934802200544679, 4.0587121264167685,
+                                  -1.3352627688545895, 0.2353306303588932, -0.02580689139001406,
+                                  0.0019295743094039231, -0.0001046381049248457,
+                                  4.303069587032947e-06};
+
 __device__ __forceinline__ double2 cis_pi(double x) {
     const double t = rint(2.0 * x);
     const double r = fma(-0.5, t, x);
     const double r2 = r * r;
-    double s = -2.2948428997269873e-08;
-    s = fma(s, r2, 7.952054001475513e-07);
-    s = fma(s, r2, -2.1915353447830217e-05);
-    s = fma(s, r2, 0.00046630280576761255);
-    s = fma(s, r2, -0.0073704309457143504);
-    s = fma(s, r2, 0.08214588661112823);
-    s = fma(s, r2, -0.5992645293207921);
-    s = fma(s, r2, 2.5501640398773455);
-    s = fma(s, r2, -5.16771278004997);
-    s = fma(s, r2, 3.141592653589793);
+    double s = kSinPiC[9];
+#pragma unroll
+    for (int i = 8; i >= 0; --i) s = fma(s, r2, kSinPiC[i]);
     s *= r;
-    double c = 4.303069587032947e-06;
-    c = fma(c, r2, -0.0001046381049248457);
-    c = fma(c, r2, 0.0019295743094039231);
-    c = fma(c, r2, -0.02580689139001406);
-    c = fma(c, r2, 0.2353306303588932);
-    c = fma(c, r2, -1.3352627688545895);
-    c = fma(c, r2, 4.0587121264167685);
-    c = fma(c, r2, -4.934802200544679);
-    c = fma(c, r2, 1.0);
+    double c = kCosPiC[8];
+#pragma unroll
+    for (int i = 7; i >= 0; --i) c = fma(c, r2, kCosPiC[i]);
     const int q = (int)(long long)t & 3;
     const double cs = (q & 1) ? s : c;
     const double sn = (q & 1) ? c : s;
@@ -66,18 +65,16 @@ __device__ __forceinline__ double2 cis_pi(double x) {
 }
 
 // cos/sin(2 pi u / 16), u = 0..7
-__device__ __forceinline__ double2 root16(int u) {
-    switch (u) {
-        case 0: return make_double2(1.0, 0.0);
-        case 1: return make_double2(0.92387953251128673848, 0.38268343236508977173);
-        case 2: return make_double2(0.70710678118654752440, 0.70710678118654752440);
-        case 3: return make_double2(0.38268343236508977173, 0.92387953251128673848);
-        case 4: return make_double2(0.0, 1.0);
-        case 5: return make_double2(-0.38268343236508977173, 0.92387953251128673848);
-        case 6: return make_double2(-0.70710678118654752440, 0.70710678118654752440);
-        default: return make_double2(-0.92387953251128673848, 0.38268343236508977173);
-    }
-}
+__constant__ double kRoot16[8][2] = {{1.0, 0.0},
+                                     {0.92387953251128673848, 0.38268343236508977173},
+                                     {0.70710678118654752440, 0.70710678118654752440},
+                                     {0.38268343236508977173, 0.92387953251128673848},
+                                     {0.0, 1.0},
+                                     {-0.38268343236508977173, 0.92387953251128673848},
+                                     {-0.70710678118654752440, 0.70710678118654752440},
+                                     {-0.92387953251128673848, 0.38268343236508977173}};
+
+__device__ __forceinline__ double2 root16(int u) { return make_double2(kRoot16[u][0], kRoot16[u][1]); }
 
 // a * exp(+2 pi i u/16)
 __device__ __forceinline__ double2 rot16(double2 a, int u) {

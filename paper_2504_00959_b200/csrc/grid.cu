@@ -63,25 +63,22 @@ __device__ __forceinline__ double bessel_i0(double x) {
 // exp(x) for -700 < x < 700: x = k ln2 + r, |r| <= ln2/2 (two-constant
 // Cody-Waite), Taylor to r^14 (truncation < 1e-17), 2^k added to the
 // exponent field. A few ulp; no special-case paths.
+// Constants in the constant bank (DFMA c[][] operands instead of UMOV pairs).
+__constant__ double kExpC[18] = {1.4426950408889634, 0.6931471805599453, 2.3190468138462996e-17,
+                                 1.1470745597729725e-11, 1.6059043836821613e-10,
+                                 2.08767569878681e-09, 2.505210838544172e-08,
+                                 2.755731922398589e-07, 2.7557319223985893e-06,
+                                 2.48015873015873e-05, 0.0001984126984126984,
+                                 0.001388888888888889, 0.008333333333333333,
+                                 0.041666666666666664, 0.16666666666666666, 0.5, 1.0, 1.0};
+
 __device__ __forceinline__ double fast_exp(double x) {
-    const double k = rint(x * 1.4426950408889634);
-    double r = fma(-k, 0.6931471805599453, x);
-    r = fma(-k, 2.3190468138462996e-17, r);
-    double p = 1.1470745597729725e-11;
-    p = fma(p, r, 1.6059043836821613e-10);
-    p = fma(p, r, 2.08767569878681e-09);
-    p = fma(p, r, 2.505210838544172e-08);
-    p = fma(p, r, 2.755731922398589e-07);
-    p = fma(p, r, 2.7557319223985893e-06);
-    p = fma(p, r, 2.48015873015873e-05);
-    p = fma(p, r, 0.0001984126984126984);
-    p = fma(p, r, 0.001388888888888889);
-    p = fma(p, r, 0.008333333333333333);
-    p = fma(p, r, 0.041666666666666664);
-    p = fma(p, r, 0.16666666666666666);
-    p = fma(p, r, 0.5);
-    p = fma(p, r, 1.0);
-    p = fma(p, r, 1.0);
+    const double k = rint(x * kExpC[0]);
+    double r = fma(-k, kExpC[1], x);
+    r = fma(-k, kExpC[2], r);
+    double p = kExpC[3];
+#pragma unroll
+    for (int i = 4; i < 18; ++i) p = fma(p, r, kExpC[i]);
     return __hiloint2double(__double2hiint(p) + ((int)k << 20), __double2loint(p));
 }
 
