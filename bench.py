@@ -143,12 +143,13 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def kernel_table(cfg, ms):
+def kernel_table(cfg, ms, ws=1):
     """Algorithmic bytes per launch group against the
-    measured per-kernel times ms = [prepare, bucket, grid, fft_rows, fft_cols, finish]."""
+    measured per-kernel times ms = [prepare, bucket, grid, fft_rows, fft_cols, finish]
+    of one rank (which holds 1/ws of the mesh)."""
     N = cfg["n_vis"]
-    cells = cfg["n_u"] * cfg["n_v"] * cfg["n_w"]
-    pix = cfg["n_u"] * cfg["n_v"]
+    cells = cfg["n_u"] * cfg["n_v"] * cfg["n_w"] // ws
+    pix = cfg["n_u"] * cfg["n_v"] // ws
     groups = {
         # K1+K2: vis read once (36 B) + grid written once (16 B/cell)
         "gridder(K1+K2)": (N * 36 + cells * 16, ms[0] + ms[1] + ms[2]),
@@ -228,6 +229,22 @@ def run_ours(args):
     total_vis = cfg["n_vis"] * ws
     value = total_vis / (ms_step / 1e3) / 1e6
 
+    # multi-GPU: per-stage times of the compute stream from a few extra
+    # (untimed) steps with stage events; the bucket / sweep split comes from
+    # the library's own events around the gridder
+    stages = None
+    if ws > 1:
+        acc = {}
+        n_st = 3
+        for _ in range(n_st):
+            tm = {}
+            WD.image_distributed(du, dv, dw, dvis, dwt, spec, kern, to_host=False, timings=tm)
+            for k_, v_ in tm.items():
+                acc[k_] = acc.get(k_, 0.0) + v_ / n_st
+        stages = {k_: round(v_, 4) for k_, v_ in acc.items()}
+        per_kernel = np.array([acc.get("prepare", 0.0), acc.get("bucket", 0.0), acc.get("sweep", 0.0),
+                               acc.get("rows", 0.0), acc.get("cols", 0.0), 0.0]) * args.steps
+
     # energy to solution: NVML (+ RAPL) over a >= 1 s window of the same step
     energy = None
     try:
@@ -259,6 +276,32 @@ def run_ours(args):
 
     # end-to-end through the host-buffer C ABI (pinned inputs, host image out)
     e2e = None
+    if ws > 1:
+        # every rank: its pinned host records -> device -> distributed image ->
+        # host image on the root; wall time per step, max over ranks
+        pin = [torch.from_numpy(a).pin_memory() for a in (u, v, w, vis, wt)]
+
+        def e2e_step():
+            d = [p_.to(dev, non_blocking=True) for p_ in pin]
+            return WD.image_distributed(*d, spec, kern, to_host=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        n_e2e = max(1, min(args.steps, 5))
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            res, _ = e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = torch.tensor([(time.perf_counter() - t0) / n_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e_s = float(e2e_s.item())
+        h2d = sum(a.nbytes for a in (u, v, w, vis, wt)) * ws
+        e2e = {"value": round(total_vis / e2e_s / 1e6, 2), "unit": "Mvis/s",
+               "ms_per_step": round(e2e_s * 1e3, 3), "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(cfg["n_u"] * cfg["n_v"] * 8),
+               "api": "paper_2504_00959_b200.distributed.image_distributed(to_host=True), "
+                      "pinned host inputs on every rank"}
     if ws == 1:
         pin = [torch.from_numpy(a).pin_memory() for a in (u, v, w, vis, wt)]
         pu, pv, pw, pvis, pwt = (p.numpy() for p in pin)
@@ -281,7 +324,7 @@ def run_ours(args):
         return
     per_kernel /= args.steps
     peak, peak_kind = measured_peaks()
-    groups = kernel_table(cfg, per_kernel)
+    groups = kernel_table(cfg, per_kernel, ws)
     kernels = {}
     for name, (bytes_, t_ms) in groups.items():
         ach = bytes_ / (t_ms / 1e3) / 1e9 if t_ms > 0 else 0.0
@@ -313,6 +356,7 @@ def run_ours(args):
         "gridding_mvis_s": round(cfg["n_vis"] / (gridder["ms"] / 1e3) / 1e6, 1) if gridder["ms"] else None,
         "roofline": roof,
         "kernels": kernels,
+        "stages_ms": stages,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "e2e": e2e,

@@ -155,25 +155,33 @@ int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
  * [plane_lo, plane_hi): strip-layout slab in, P-layout slab out (out of
  * place). With n_dest > 1 the column pairs are split over destination ranks
  * (dest_pairs_host[d] pairs each, in order) and the output is destination
- * major, [d][plane][pair - first_pair_d][row][G], so ONE all-to-all moves the
- * whole slab transpose (fft2d_slab's send loop, transform.py:152-161).
+ * major, [d][plane - plane_lo][pair - first_pair_d][row][G], so ONE
+ * all-to-all moves the slab transpose of the range (fft2d_slab's send loop,
+ * transform.py:152-161). grid_p holds planes [plane_lo, plane_hi) only, so a
+ * plane range can be sent while the next one is transformed.
  * dest_pairs_host NULL = one destination = plain P layout. Unnormalised. */
 int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count,
                  const double *grid_s, double *grid_p, int32_t plane_lo, int32_t plane_hi,
                  int32_t n_dest, const int32_t *dest_pairs_host);
 
-/* Column pass + w correction + stacking (transform.py:162-175, 192-230):
- * input tgrid holds this rank's column pairs [g0, g0+ng) for all n_v rows,
- * concatenated by source slab s (src_rows[s] rows each, all equal) as
- *   [s][plane][g - g0][row - row_start_s][G]   (the all-to-all output of
- * wsb_fft_rows with destinations; with one source it is the P layout).
- * Writes image_strip f64[n_v][ng*G] (row-major) and norm_partials
- * f64[ng*G][2] = (sum Im^2, sum Re^2) per image column (fixed pairwise tree
- * over the rows); the caller sums the columns in order, which makes the
- * norms independent of the GPU count. */
+/* Column pass + w correction + stacking (transform.py:162-175, 192-230) of
+ * planes [plane_lo, plane_hi): input tgrid holds this rank's column pairs
+ * [g0, g0+ng) of those planes for all n_v rows, concatenated by source slab s
+ * (src_rows[s] rows each, all equal) as
+ *   [s][plane - plane_lo][g - g0][row - row_start_s][G]   (the all-to-all
+ * output of wsb_fft_rows with destinations; one source = the P layout).
+ * Plane ranges are stacked in call order: the context carries the running
+ * sum from a call ending at plane k to the next call, which must start at
+ * plane k with the same (grid, g0, ng) -- the sum is the one a single call
+ * over [0, n_w) forms. The call whose range ends at n_w writes image_strip
+ * f64[n_v][ng*G] (row-major) and norm_partials f64[ng*G][2] = (sum Im^2,
+ * sum Re^2) per image column (fixed pairwise tree over the rows); the
+ * caller sums the columns in order, which makes the norms independent of
+ * the GPU count. Earlier calls leave both untouched. */
 int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
                        const int32_t *src_rows_host, int32_t g0, int32_t ng,
-                       const double *tgrid, double *image_strip, double *norm_partials);
+                       int32_t plane_lo, int32_t plane_hi, const double *tgrid,
+                       double *image_strip, double *norm_partials);
 
 /* Debug / parity: strip-layout slab -> natural (plane, row, col) complex128
  * with the checkerboard sign removed (the grid_all output layout,

@@ -89,7 +89,7 @@ def lib() -> C.CDLL:
         "wsb_route_pack": (C.c_int, [p, G, i32, i32, p, p, i64, p, p, p]),
         "wsb_grid_slab": (C.c_int, [p, G, K, i32, i32, p, p, i64, p, p]),
         "wsb_fft_rows": (C.c_int, [p, G, i32, p, p, i32, i32, i32, p]),
-        "wsb_fft_cols_stack": (C.c_int, [p, G, i32, p, i32, i32, p, p, p]),
+        "wsb_fft_cols_stack": (C.c_int, [p, G, i32, p, i32, i32, i32, i32, p, p, p]),
         "wsb_grid_unpack": (C.c_int, [p, G, i32, i32, p, p]),
         "wsb_tiles_debug": (C.c_int, [p, p, p, p, p]),
         "wsb_last_timings": (C.c_int, [p, p, p]),

@@ -234,10 +234,12 @@ int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int
 static int grid_slab_impl(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
                           int32_t v_start, int32_t v_count, const double *rec,
                           const uint32_t *plane, int64_t m, double *grid_p,
-                          unsigned long long *updates_dev, int64_t *n_entries_out) {
+                          unsigned long long *updates_dev, int64_t *n_entries_out,
+                          const cudaEvent_t *mid = nullptr) {
     RowBuckets bk;
     WSB_TRY(bucket_rows(ctx, grid, kern->half_support, v_start, v_count, rec, plane, m, &bk));
     if (n_entries_out) *n_entries_out = bk.n_entries;
+    if (mid) WSB_CUDA_TRY(cudaEventRecord(*mid, ctx->stream));
     return grid_sweep(ctx, grid, kern, v_start, v_count, rec, bk, grid_p, updates_dev);
 }
 
@@ -254,13 +256,25 @@ int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern, in
     unsigned long long *upd;
     WSB_TRY(ensure(ctx, kSlotU64, 64, (void **)&upd));
     WSB_CUDA_TRY(cudaMemsetAsync(upd, 0, sizeof(unsigned long long), ctx->stream));
-    WSB_TRY(grid_slab_impl(ctx, grid, kern, v_start, v_count, rec, plane, m, grid_p, upd, nullptr));
+    // bucket / sweep times of this call go to wsb_last_timings slots 1 and 2
+    // (read when the call synchronises anyway, i.e. grid_updates requested)
+    cudaEvent_t *ev = ctx->timing.ev;
+    WSB_CUDA_TRY(cudaEventRecord(ev[0], ctx->stream));
+    WSB_TRY(grid_slab_impl(ctx, grid, kern, v_start, v_count, rec, plane, m, grid_p, upd, nullptr,
+                           &ev[1]));
+    WSB_CUDA_TRY(cudaEventRecord(ev[2], ctx->stream));
     if (grid_updates) {
         unsigned long long h;
         WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host, upd, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         std::memcpy(&h, ctx->flag_host, sizeof(h));
         *grid_updates = (int64_t)h;
+        float a = 0.f, b = 0.f;
+        WSB_CUDA_TRY(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        WSB_CUDA_TRY(cudaEventElapsedTime(&b, ev[1], ev[2]));
+        for (int i = 0; i < 6; ++i) ctx->last_ms[i] = 0.0;
+        ctx->last_ms[1] = a;
+        ctx->last_ms[2] = b;
     }
     return WSB_OK;
 }
@@ -279,14 +293,17 @@ int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count, const doub
 }
 
 int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
-                       const int32_t *src_rows_host, int32_t g0, int32_t ng, const double *tgrid,
-                       double *image_strip, double *norm_partials) {
+                       const int32_t *src_rows_host, int32_t g0, int32_t ng, int32_t plane_lo,
+                       int32_t plane_hi, const double *tgrid, double *image_strip,
+                       double *norm_partials) {
     if (!ctx || !src_rows_host) return fail(WSB_EINVAL, "NULL argument");
     WSB_TRY(validate_grid(grid));
+    if (plane_lo < 0 || plane_hi > grid->n_w || plane_lo > plane_hi)
+        return fail(WSB_EINVAL, "plane range outside [0, n_w]");
     if (g0 < 0 || ng < 1 || (g0 + ng) * kG > grid->n_u) return fail(WSB_EINVAL, "column groups outside the mesh");
     WSB_TRY(set_device(ctx));
-    return fft_cols_stack(ctx, grid, n_sources, src_rows_host, g0, ng, tgrid, image_strip,
-                          norm_partials);
+    return fft_cols_stack(ctx, grid, n_sources, src_rows_host, g0, ng, plane_lo, plane_hi, tgrid,
+                          image_strip, norm_partials);
 }
 
 int wsb_grid_unpack(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t v_count,
@@ -365,7 +382,7 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
     WSB_TRY(fft_rows(ctx, grid, n_v, gs, gp, 0, n_w, 1, nullptr));
     WSB_CUDA_TRY(cudaEventRecord(ev[4], ctx->stream));
     const int32_t rows[1] = {n_v};
-    WSB_TRY(fft_cols_stack(ctx, grid, 1, rows, 0, n_u / kG, gp, image_out, partials));
+    WSB_TRY(fft_cols_stack(ctx, grid, 1, rows, 0, n_u / kG, 0, n_w, gp, image_out, partials));
     WSB_CUDA_TRY(cudaEventRecord(ev[5], ctx->stream));
     const int nb = n_u;  // one norm partial per image column
     k_sum_partials<<<1, 256, 0, ctx->stream>>>(partials, nb, partials + 2 * (size_t)n_u);

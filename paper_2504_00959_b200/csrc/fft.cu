@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
                     hi = dst.g0[d + 1];
                 }
             const int64_t base = (int64_t)dst.n_w * v_count * kG * lo;
-            out[base + ((plane * (hi - lo) + (g - lo)) * v_count + j0 + seq) * kG + (col % kG)] = z;
+            out[base + (((plane - plane_lo) * (hi - lo) + (g - lo)) * v_count + j0 + seq) * kG +
+                (col % kG)] = z;
         }
     };
     double2 v[kRowE];
@@ -318,15 +319,23 @@ constexpr int kColE = 8;
 constexpr int kColRL = 3;
 
 struct ColArgs {
-    const double2 *tgrid;
+    const double2 *tgrid;   // planes [k0, k1) only
     double *strip;          // [n_v][ncols]
     double *partials;       // [ncols][2]
-    const double *w_k;      // [n_w] native w per plane
+    double2 *run;           // running stack between plane ranges, per thread element
     int n_w, n_u, n_v, ncols, g0;
+    int k0, k1;             // plane range of this call
     int n_src;
     int src_start[9];       // row start of each source slab (+ sentinel)
-    double cell, inv_nuv, inv_nw;
+    double cell, inv_nuv, inv_nw, w_min, w_max;
 };
+
+// native w of plane k (mesh.py:101-112), the same IEEE operations as the host
+__device__ __forceinline__ double plane_w(const ColArgs &a, int k) {
+    if (a.n_w == 1) return __dmul_rn(0.5, __dadd_rn(a.w_min, a.w_max));
+    const double frac = __ddiv_rn((double)k, (double)(a.n_w - 1));
+    return __dadd_rn(a.w_min, __dmul_rn(frac, __dsub_rn(a.w_max, a.w_min)));
+}
 
 // CTA = 4096/N columns for all planes. Plane k+1's first-pass inputs are
 // loaded into registers while plane k is transformed; the last pass leaves
@@ -348,8 +357,9 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     double *nbuf = reinterpret_cast<double *>(sbuf + 2 * C * STRIDE);  // n = sqrt(1-l^2-m^2), [C][N]
 
     const int c0 = blockIdx.x * C;                 // first local column
-    // input [s][plane][g][row - row_start_s][x]: every source holds the same
-    // number of rows, so a plane advances every source block by ncols*rows
+    const int nk = a.k1 - a.k0;                    // planes in this call
+    // input [s][plane - k0][g][row - row_start_s][x]: every source holds the
+    // same number of rows, so a plane advances every source block by ncols*rows
     const int64_t plane_elems = (int64_t)a.ncols * (N / a.n_src);
 
     // In-plane offset of each first-pass input of this thread (the same for
@@ -368,7 +378,7 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
                     r0 = a.src_start[sidx];
                     r1 = a.src_start[sidx + 1];
                 }
-            const int o = a.n_w * a.ncols * r0 + ((lc / kG) * (r1 - r0) + (j - r0)) * kG + (lc % kG);
+            const int o = nk * a.ncols * r0 + ((lc / kG) * (r1 - r0) + (j - r0)) * kG + (lc % kG);
             return make_double2(__hiloint2double(o, 0), 0.0);
         };
         double2 t[kColE];
@@ -391,17 +401,20 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
         nbuf[e] = __dsqrt_rn(__dsub_rn(__dsub_rn(1.0, __dmul_rn(l, l)), __dmul_rn(m, m)));
     }
 
+    // the running stack of earlier plane ranges continues in the same order
+    double2 *run = a.run + (int64_t)blockIdx.x * kColE * CT + threadIdx.x;
     double2 acc[kColE];
 #pragma unroll
-    for (int i = 0; i < kColE; ++i) acc[i] = make_double2(0.0, 0.0);
+    for (int i = 0; i < kColE; ++i) acc[i] = a.k0 > 0 ? run[i * CT] : make_double2(0.0, 0.0);
     double2 pf[kColE];
     gld_plane(0, pf);
 
-    for (int k = 0; k < a.n_w; ++k) {
+    for (int kl = 0; kl < nk; ++kl) {
+        const int k = a.k0 + kl;
         double2 v[kColE];
 #pragma unroll
         for (int i = 0; i < kColE; ++i) v[i] = pf[i];
-        if (k + 1 < a.n_w) gld_plane(k + 1, pf);
+        if (kl + 1 < nk) gld_plane(kl + 1, pf);
         pass_compute<LOGN, P0::RL, kColE, CT>(1, tw, v);
         if constexpr (!P0::LAST) {
             __syncthreads();  // the previous plane's last pass has read sbuf
@@ -411,7 +424,7 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
             smem_passes<LOGN, RLM, kColE, CT, P0::RL>(sbuf, tw, v);
         }
         // v[kb*R + r] is output row j + r*M of sequence (column) seq
-        const double wk = a.w_k[k];
+        const double wk = plane_w(a, k);
 #pragma unroll
         for (int kb = 0; kb < NB; ++kb) {
             const int b = threadIdx.x + kb * CT;
@@ -426,6 +439,12 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
                 acc[kb * R + r] = cadd(acc[kb * R + r], z);
             }
         }
+    }
+
+    if (a.k1 < a.n_w) {  // more planes to come: park the running stack
+#pragma unroll
+        for (int i = 0; i < kColE; ++i) run[i * CT] = acc[i];
+        return;
     }
 
     // finish: /(n_u n_v) (exact power of two), /n_w (numpy multiplies by the
@@ -537,7 +556,7 @@ int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a,
     WSB_TRY(twiddles(ctx, g->n_u, &tw));
     const int ng = g->n_u / kG, ns = ceil_div(g->n_u, 32);
     RowDest dst;
-    dst.n_w = g->n_w;
+    dst.n_w = phi - plo;  // the output holds planes [plo, phi) only
     if (n_dest < 1 || n_dest > 8) return fail(WSB_EINVAL, "n_dest must be in [1, 8]");
     dst.g0[0] = 0;
     for (int d = 0; d < n_dest; ++d) dst.g0[d + 1] = dst.g0[d] + (dest_groups ? dest_groups[d] : ng);
@@ -557,8 +576,9 @@ int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a,
 }
 
 int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t *src_rows,
-                   int g0, int ng, const double *tgrid, double *image_strip,
+                   int g0, int ng, int plo, int phi, const double *tgrid, double *image_strip,
                    double *norm_partials) {
+    if (phi <= plo) return WSB_OK;
     if (n_sources < 1 || n_sources > 8) return fail(WSB_EINVAL, "n_sources must be in [1, 8]");
     ColArgs a;
     a.tgrid = (const double2 *)tgrid;
@@ -581,24 +601,17 @@ int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t
     a.cell = g->cell_size_lm;
     a.inv_nuv = 1.0 / ((double)g->n_u * (double)g->n_v);
     a.inv_nw = 1.0 / (double)g->n_w;
-    // native w per plane (mesh.py:101-112)
-    double *wk;
-    WSB_TRY(ensure(ctx, kSlotNorms, sizeof(double) * g->n_w, (void **)&wk));
+    a.w_min = g->w_min_native;
+    a.w_max = g->w_max_native;
+    a.k0 = plo;
+    a.k1 = phi;
+    // the running stack: one complex per thread element of the launch
     {
-        std::vector<double> h(g->n_w);
-        for (int k = 0; k < g->n_w; ++k) {
-            if (g->n_w == 1) {
-                h[k] = 0.5 * (g->w_min_native + g->w_max_native);
-            } else {
-                const double frac = (double)k / (double)(g->n_w - 1);
-                h[k] = g->w_min_native + frac * (g->w_max_native - g->w_min_native);
-            }
-        }
-        WSB_CUDA_TRY(cudaMemcpyAsync(wk, h.data(), sizeof(double) * g->n_w, cudaMemcpyHostToDevice,
-                                     ctx->stream));
-        WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // h is a stack buffer
+        const int lg = ilog2(g->n_v);
+        const int ct = std::max((1 << lg) / 8, 256), cpb = std::max(1, ct * 8 / (1 << lg));
+        const size_t bytes = sizeof(double2) * (size_t)ceil_div(a.ncols, cpb) * ct * 8;
+        WSB_TRY(ensure(ctx, kSlotColRun, bytes, (void **)&a.run));
     }
-    a.w_k = wk;
     const double *tw;
     WSB_TRY(twiddles(ctx, g->n_v, &tw));
     const double2 *t2 = (const double2 *)tw;

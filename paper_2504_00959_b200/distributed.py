@@ -32,7 +32,7 @@ import torch.distributed as dist
 
 from . import _lib as L
 from .imager import (FinalImage, _ptr, as_grid_spec, as_kernel_spec, context, grid_slab_device,
-                     partition_1d, prepare_device)
+                     last_timings, partition_1d, prepare_device)
 
 G = L.P_GROUP
 
@@ -63,36 +63,81 @@ class CudaBackend:
     def grid_slab(self, rec, plane, spec, kern, v0, vc):
         return grid_slab_device(rec, plane, spec, kern, v0, vc)
 
-    def fft_rows(self, grid_s, spec, vc, dest_pairs):
-        """Row pass: strip-layout slab in; out: float64 buffer laid out
-        [dest][plane][pair][row][G][2] (the all-to-all send buffer)."""
+    def fft_rows(self, grid_s, spec, vc, dest_pairs, plane_lo=0, plane_hi=None):
+        """Row pass of planes [plane_lo, plane_hi): strip-layout slab in; out:
+        float64 buffer laid out [dest][plane - plane_lo][pair][row][G][2] (the
+        all-to-all send buffer)."""
+        plane_hi = spec.n_w if plane_hi is None else plane_hi
         g = spec.c_struct()
-        grid_p = torch.empty(spec.n_w * spec.n_u * vc * 2, dtype=torch.float64, device=self.device)
+        grid_p = torch.empty((plane_hi - plane_lo) * spec.n_u * vc * 2, dtype=torch.float64,
+                             device=self.device)
         pairs = (C.c_int32 * len(dest_pairs))(*dest_pairs)
         L.check(L.lib().wsb_fft_rows(self.ctx.handle, C.byref(g), int(vc), _ptr(grid_s),
-                                     _ptr(grid_p), 0, spec.n_w, len(dest_pairs), pairs))
+                                     _ptr(grid_p), int(plane_lo), int(plane_hi), len(dest_pairs),
+                                     pairs))
         return grid_p
 
-    def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng):
+    def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng, plane_lo=0, plane_hi=None):
+        """Column pass + stack of planes [plane_lo, plane_hi) (ranges in order;
+        the context carries the running stack). Returns (strip, partials)
+        after the range ending at n_w, (None, None) before."""
+        plane_hi = spec.n_w if plane_hi is None else plane_hi
         g = spec.c_struct()
-        strip = torch.empty((spec.n_v, ng * G), dtype=torch.float64, device=self.device)
-        partials = torch.empty((ng * G, 2), dtype=torch.float64, device=self.device)
+        final = plane_hi == spec.n_w
+        strip = torch.empty((spec.n_v, ng * G) if final else (1,), dtype=torch.float64,
+                            device=self.device)
+        partials = torch.empty((ng * G, 2) if final else (1,), dtype=torch.float64,
+                               device=self.device)
         rows = (C.c_int32 * len(src_rows))(*src_rows)
         L.check(L.lib().wsb_fft_cols_stack(self.ctx.handle, C.byref(g), len(src_rows), rows, int(g0),
-                                           int(ng), _ptr(tgrid), _ptr(strip), _ptr(partials)))
-        return strip, partials
+                                           int(ng), int(plane_lo), int(plane_hi), _ptr(tgrid),
+                                           _ptr(strip), _ptr(partials)))
+        return (strip, partials) if final else (None, None)
 
 
-def _a2a(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group):
-    dist.all_to_all_single(out, inp, output_split_sizes=list(out_splits),
-                           input_split_sizes=list(in_splits), group=group)
+def _a2a(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group, async_op=False):
+    return dist.all_to_all_single(out, inp, output_split_sizes=list(out_splits),
+                                  input_split_sizes=list(in_splits), group=group,
+                                  async_op=async_op)
+
+
+def plane_ranges(n_w: int, n_ranges: int):
+    """Contiguous plane ranges of the pipelined transpose (partition_1d)."""
+    n_ranges = max(1, min(n_ranges, n_w))
+    return [(a, a + c) for a, c in (partition_1d(n_w, n_ranges, i) for i in range(n_ranges))]
+
+
+class _Stages:
+    """CUDA events on the compute stream between pipeline stages (optional)."""
+
+    def __init__(self, on: bool, device):
+        self.on, self.device, self.marks = on, device, []
+
+    def mark(self, name):
+        if self.on:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(torch.cuda.current_stream(self.device))
+            self.marks.append((name, ev))
+
+    def ms(self):
+        if not self.on or len(self.marks) < 2:
+            return {}
+        torch.cuda.current_stream(self.device).synchronize()
+        return {b[0]: a[1].elapsed_time(b[1]) for a, b in zip(self.marks, self.marks[1:])}
 
 
 def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None, root: int = 0,
-                      to_host: bool = True):
+                      to_host: bool = True, n_ranges: int = 4, timings: dict | None = None):
     """Dirty image of the union of every rank's records. Each rank passes its
     own time partition (records in gindex order, rank r holding the r-th
     contiguous block, as visdata.partition_time_ordered produces).
+
+    The slab transpose is pipelined over ``n_ranges`` plane ranges: the
+    all-to-all of range i runs on NCCL's stream while the row pass of range
+    i+1 and the column pass of range i-1 run on the compute stream. The
+    result does not depend on n_ranges (the planes are stacked in order).
+    ``timings``, if a dict, receives per-stage milliseconds of the compute
+    stream (and the bucket / sweep split of the gridder).
 
     Returns (FinalImage on ``root``, None elsewhere; diag dict on every rank)."""
     spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
@@ -107,9 +152,14 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     if spec.n_v % R:
         raise NotImplementedError("the GPU slab transpose needs n_v to be a multiple of the rank count")
 
+    st = _Stages(timings is not None and dev.type == "cuda", dev)
+    st.mark("start")
+
     # 1. prepare + time->space exchange ------------------------------------
     rec, plane = be.prepare(u, v, w, vis, weight, spec)
+    st.mark("prepare")
     srec, spl, counts = be.route(rec, plane, spec, S, R)
+    st.mark("route")
     c_send = torch.tensor(counts, dtype=torch.int64, device=dev)
     c_recv = torch.empty(R, dtype=torch.int64, device=dev)
     dist.all_to_all_single(c_recv, c_send, group=group)
@@ -119,28 +169,43 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     rpl = torch.empty(m, dtype=torch.int32, device=dev)
     _a2a(rrec, srec.contiguous(), recv_counts, counts, group)
     _a2a(rpl, spl.contiguous(), recv_counts, counts, group)
+    st.mark("exchange")
 
     # 2. grid this rank's slab ----------------------------------------------
     slabs = [partition_1d(spec.n_v, R, d) for d in range(R)]
     v0, vc = slabs[r]
     grid_s, updates = be.grid_slab(rrec, rpl, spec, kern, v0, vc)
+    st.mark("grid")
+    split = last_timings(dev)[0][1:3] if st.on else None
+    del rrec, rpl
 
-    # 3. row FFT, one all-to-all block transpose, column FFT + w stack --------
+    # 3. row FFT, all-to-all block transpose, column FFT + w stack, pipelined
+    #    over plane ranges ----------------------------------------------------
     cols = [partition_1d(n_groups, R, d) for d in range(R)]
     g0, ng = cols[r]
-    grid_p = be.fft_rows(grid_s, spec, vc, [ng_d for _, ng_d in cols])   # [dest][plane][pair][row][G]
+    dest_pairs = [ng_d for _, ng_d in cols]
+    src_rows = [vc_s for _, vc_s in slabs]
+    inflight = []
+    for k0, k1 in plane_ranges(spec.n_w, n_ranges):
+        nk = k1 - k0
+        grid_p = be.fft_rows(grid_s, spec, vc, dest_pairs, k0, k1)   # [dest][plane][pair][row][G]
+        in_splits = [nk * ng_d * vc * G * 2 for ng_d in dest_pairs]   # float64 elements per rank
+        out_splits = [nk * ng * vc_s * G * 2 for vc_s in src_rows]    # from each source slab
+        tgrid = torch.empty(sum(out_splits), dtype=torch.float64, device=dev)
+        work = _a2a(tgrid, grid_p, out_splits, in_splits, group, async_op=True)
+        inflight.append((k0, k1, work, tgrid, grid_p))
+    st.mark("rows")
     del grid_s
-    in_splits = [spec.n_w * ng_d * vc * G * 2 for _, ng_d in cols]     # float64 elements to each rank
-    out_splits = [spec.n_w * ng * vc_s * G * 2 for _, vc_s in slabs]   # from each source slab
-    tgrid = torch.empty(sum(out_splits), dtype=torch.float64, device=dev)
-    _a2a(tgrid, grid_p, out_splits, in_splits, group)
-    del grid_p
-    strip, partials = be.fft_cols_stack(tgrid, spec, [vc_s for _, vc_s in slabs], g0, ng)
+    for k0, k1, work, tgrid, grid_p in inflight:
+        work.wait()
+        strip, partials = be.fft_cols_stack(tgrid, spec, src_rows, g0, ng, k0, k1)
+    inflight.clear()
+    st.mark("cols")
 
     # 4. gather to the root ----------------------------------------------------
     upd = torch.tensor([updates], dtype=torch.int64, device=dev)
     dist.all_reduce(upd, group=group)
-    maxc = max(ng_d for _, ng_d in cols) * G
+    maxc = max(dest_pairs) * G
     pad = torch.zeros((spec.n_v, maxc), dtype=torch.float64, device=dev)
     pad[:, : ng * G] = strip
     ppad = torch.zeros((maxc, 2), dtype=torch.float64, device=dev)
@@ -149,8 +214,13 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     parts = [torch.empty_like(ppad) for _ in range(R)]
     dist.all_gather(strips, pad, group=group)
     dist.all_gather(parts, ppad, group=group)
+    st.mark("gather")
     diag = {"grid_updates": int(upd.item()), "records_local": int(rec.shape[0]),
             "records_slab": m, "exchange_bytes": int(sum(counts) - counts[r]) * 36}
+    if timings is not None:
+        timings.update(st.ms())
+        if split is not None:
+            timings["bucket"], timings["sweep"] = split
     if r != root:
         return None, diag
     pix = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, device=dev)

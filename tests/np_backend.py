@@ -48,28 +48,34 @@ class NumpyBackend:
         s = np.ascontiguousarray(pad.reshape(spec.n_w, vc, ns, 32).transpose(0, 2, 1, 3))
         return torch.from_numpy(s.view(np.float64).reshape(spec.n_w, ns, vc, 32, 2)), upd
 
-    def fft_rows(self, grid_s, spec, vc, dest_pairs):
+    def fft_rows(self, grid_s, spec, vc, dest_pairs, plane_lo=0, plane_hi=None):
+        plane_hi = spec.n_w if plane_hi is None else plane_hi
+        nk = plane_hi - plane_lo
         ns = (spec.n_u + 31) // 32
-        a = grid_s.numpy().view(np.complex128).reshape(spec.n_w, ns, vc, 32)
-        nat = a.transpose(0, 2, 1, 3).reshape(spec.n_w, vc, ns * 32)[:, :, : spec.n_u]
+        a = grid_s.numpy().view(np.complex128).reshape(spec.n_w, ns, vc, 32)[plane_lo:plane_hi]
+        nat = a.transpose(0, 2, 1, 3).reshape(nk, vc, ns * 32)[:, :, : spec.n_u]
         f = np.fft.ifft(nat, axis=-1) * spec.n_u               # unnormalised inverse
         # -> P layout (plane, col/G, row, col%G), then destination major
-        p = f.reshape(spec.n_w, vc, spec.n_u // G, G).transpose(0, 2, 1, 3)
+        p = f.reshape(nk, vc, spec.n_u // G, G).transpose(0, 2, 1, 3)
         out, g0 = [], 0
         for ng in dest_pairs:
             out.append(np.ascontiguousarray(p[:, g0:g0 + ng]).ravel())
             g0 += ng
         return torch.from_numpy(np.concatenate(out).view(np.float64))
 
-    def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng):
+    def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng, plane_lo=0, plane_hi=None):
+        """Plane ranges accumulate in self._run between calls (the context's
+        running stack in the CUDA backend)."""
+        plane_hi = spec.n_w if plane_hi is None else plane_hi
+        nk = plane_hi - plane_lo
         t = tgrid.numpy().view(np.complex128)
         ncols = ng * G
-        full = np.empty((spec.n_w, spec.n_v, ncols), np.complex128)
+        full = np.empty((nk, spec.n_v, ncols), np.complex128)
         off, r0 = 0, 0
         for rows in src_rows:                    # [s][plane][pair][row][G]
-            n = spec.n_w * ng * rows * G
-            blk = t[off:off + n].reshape(spec.n_w, ng, rows, G)
-            full[:, r0:r0 + rows] = blk.transpose(0, 2, 1, 3).reshape(spec.n_w, rows, ncols)
+            n = nk * ng * rows * G
+            blk = t[off:off + n].reshape(nk, ng, rows, G)
+            full[:, r0:r0 + rows] = blk.transpose(0, 2, 1, 3).reshape(nk, rows, ncols)
             off += n
             r0 += rows
         planes = np.fft.ifft(full, axis=1) * spec.n_v / (spec.n_u * spec.n_v)
@@ -79,11 +85,15 @@ class NumpyBackend:
         l = np.broadcast_to(cols * spec.cell_size_lm, (spec.n_v, ncols))
         m = np.broadcast_to((rowsv * spec.cell_size_lm)[:, None], (spec.n_v, ncols))
         n = np.sqrt(1.0 - l * l - m * m)
-        acc = np.zeros((spec.n_v, ncols), np.complex128)
-        for k in range(spec.n_w):
+        acc = np.zeros((spec.n_v, ncols), np.complex128) if plane_lo == 0 else self._run
+        for k in range(plane_lo, plane_hi):
             wk = O.plane_w_native(k, spec.n_w, spec.w_min_native, spec.w_max_native)
-            p = planes[k] if wk == 0.0 else planes[k] * np.exp(2j * np.pi * wk * (n - 1.0))
+            pk = planes[k - plane_lo]
+            p = pk if wk == 0.0 else pk * np.exp(2j * np.pi * wk * (n - 1.0))
             acc = acc + p
+        if plane_hi < spec.n_w:
+            self._run = acc
+            return None, None
         acc = acc / spec.n_w * n
         strip = np.ascontiguousarray(acc.real)
         partials = np.stack([(acc.imag ** 2).sum(axis=0), (acc.real ** 2).sum(axis=0)], axis=1)

@@ -37,8 +37,8 @@ def _parts(t, R):
     return out
 
 
-def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R):
-    from paper_2504_00959_b200.distributed import CudaBackend
+def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges=1):
+    from paper_2504_00959_b200.distributed import CudaBackend, plane_ranges
     be = CudaBackend(0)
     G = 2
     S = kern.half_support
@@ -57,27 +57,29 @@ def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R):
             pls.append(spl[off:off + counts[d]])
         gs, up = be.grid_slab(torch.cat(recs).contiguous(), torch.cat(pls).contiguous(), spec, kern,
                               v0, vc)
-        grids.append(be.fft_rows(gs, spec, vc, [ng for _, ng in cols]))
+        grids.append([be.fft_rows(gs, spec, vc, [ng for _, ng in cols], k0, k1)
+                      for k0, k1 in plane_ranges(spec.n_w, n_ranges)])
         upd += up
     pix = np.empty((spec.n_v, spec.n_u))
     parts = []
     for d, (g0, ng) in enumerate(cols):
-        # the all-to-all: destination d's block of every source, in source order
-        chunks = []
-        for (v0, vc), gp in zip(slabs, grids):
-            n = spec.n_w * vc * G * 2
-            start = sum(n * ng_d for _, ng_d in cols[:d])
-            chunks.append(gp[start:start + n * ng])
-        tgrid = torch.cat(chunks).contiguous()
-        strip, partials = be.fft_cols_stack(tgrid, spec, [vc for _, vc in slabs], g0, ng)
+        for i, (k0, k1) in enumerate(plane_ranges(spec.n_w, n_ranges)):
+            # the all-to-all: destination d's block of every source, in source order
+            chunks = []
+            for (v0, vc), gps in zip(slabs, grids):
+                n = (k1 - k0) * vc * G * 2
+                start = sum(n * ng_d for _, ng_d in cols[:d])
+                chunks.append(gps[i][start:start + n * ng])
+            tgrid = torch.cat(chunks).contiguous()
+            strip, partials = be.fft_cols_stack(tgrid, spec, [vc for _, vc in slabs], g0, ng, k0, k1)
         pix[:, g0 * G:(g0 + ng) * G] = strip.cpu().numpy()
         parts.append(partials.cpu().numpy())
     p = np.concatenate(parts)
     return pix, np.sqrt([p[:, 0].cumsum()[-1], p[:, 1].cumsum()[-1]]), upd
 
 
-@pytest.mark.parametrize("R", [2, 4, 8])
-def test_virtual_ranks_bit_identical(W, golden_image, R):
+@pytest.mark.parametrize("R,n_ranges", [(2, 1), (4, 1), (8, 1), (2, 3), (4, 4)])
+def test_virtual_ranks_bit_identical(W, golden_image, R, n_ranges):
     g = golden_image
     n_u, n_v, n_w, S, _ = (int(x) for x in g["wide_cfg"])
     cell, wmin, wmax, shape = (float(x) for x in g["wide_fcfg"])
@@ -85,7 +87,7 @@ def test_virtual_ranks_bit_identical(W, golden_image, R):
     kern = W.KernelSpec("gaussian", S, shape)
     u, v, w, t, vis, wt = chunk_from(g, "wide_in_")
     ref, diag = W.image(u, v, w, t, vis, wt, spec, kern)
-    pix, norms, upd = _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R)
+    pix, norms, upd = _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges)
     assert upd == diag["grid_updates"]
     assert pix.tobytes() == ref.pixels.tobytes()
     assert norms[0] == ref.imag_residual_norm and norms[1] == ref.real_norm
