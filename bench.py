@@ -460,30 +460,44 @@ def _cpu_model():
 
 
 def run_reference(args):
+    """The reference arm: the reference's algorithm (oracle port) on the host
+    cores, rank 0 only. Each step grids a bounded record sample on the full
+    mesh and transforms / stacks one plane, scaled to the job's workload
+    (ws x 10M records, one 2048^2 x 32 mesh). The sample shrinks so that the
+    whole --steps/--warmup run stays within about three minutes."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     cfg = dict(CFG2)
     threads = cpu_cores()
-    for _ in range(args.warmup):
-        oracle_step(cfg, 100_000, 1, threads)
+    n_sample = 100_000
+    budget_s = 180.0
+    t0 = time.perf_counter()
+    oracle_step(cfg, n_sample, 1, threads)     # first warm-up step sizes the sample
+    first = time.perf_counter() - t0
+    n_steps = args.steps + max(args.warmup - 1, 0)
+    if n_steps * first > budget_s:
+        n_sample = max(10_000, int(n_sample * budget_s / (n_steps * first)))
+    for _ in range(max(args.warmup - 1, 0)):
+        oracle_step(cfg, n_sample, 1, threads)
     times = []
     for _ in range(args.steps):
-        full, det = oracle_step(cfg, 100_000, 1, threads)
-        times.append(full)
+        full, det = oracle_step(cfg, n_sample, 1, threads)
+        # the job grids ws x n_vis records on one mesh: scale the gridding part
+        times.append(full + det["grid_s"] * cfg["n_vis"] * (ws - 1) / n_sample)
     s = float(np.mean(times))
-    value = cfg["n_vis"] / s / 1e6
+    value = cfg["n_vis"] * ws / s / 1e6
+    sample = (f"per step: {n_sample} records gridded on the full mesh + 1 of 32 planes "
+              f"transformed/stacked, scaled to {ws} x {cfg['n_vis']} records")
     out = {"impl": "reference", "metric": "Mvis/s imaged (bucket+grid+FFT+w-stack, dirty image out)",
            "value": round(value, 4), "unit": "Mvis/s", "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(s * 1e3, 1), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "cfg2: synthetic 10M visibilities, 2048x2048 grid, 32 w-planes, "
-                                  "Gaussian support 7, single channel, FP64"},
+           "config": {"workload": "cfg2: synthetic 10M visibilities per GPU, 2048x2048 grid, "
+                                  "32 w-planes, Gaussian support 7 (S=3, sigma=1), single channel, "
+                                  "FP64", "records_total": cfg["n_vis"] * ws},
            "cpu_baseline": {"value": round(value, 4), "unit": "Mvis/s", "cores": threads,
-                            "kind": "port",
-                            "sample": "per step: 100000 records gridded on the full mesh + 1 of 32 "
-                                      "planes transformed/stacked, scaled to the full workload",
-                            "cpu": _cpu_model()},
+                            "kind": "port", "sample": sample, "cpu": _cpu_model()},
            "e2e": {"value": round(value, 4), "unit": "Mvis/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
