@@ -170,10 +170,12 @@ int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count,
  * (src_rows[s] rows each, all equal) as
  *   [s][plane - plane_lo][g - g0][row - row_start_s][G]   (the all-to-all
  * output of wsb_fft_rows with destinations; one source = the P layout).
- * Plane ranges are stacked in call order: the context carries the running
- * sum from a call ending at plane k to the next call, which must start at
- * plane k with the same (grid, g0, ng) -- the sum is the one a single call
- * over [0, n_w) forms. The call whose range ends at n_w writes image_strip
+ * The planes are stacked from the top plane down (Horner's rule in the w
+ * phase step), so plane ranges are passed in DESCENDING order: the first call
+ * ends at n_w, each next call ends where the previous one began, with the
+ * same (grid, g0, ng); the context carries the running sum between calls and
+ * the result equals that of a single call over [0, n_w). The call whose range
+ * starts at plane 0 writes image_strip
  * f64[n_v][ng*G] (row-major) and norm_partials f64[ng*G][2] = (sum Im^2,
  * sum Re^2) per image column (fixed pairwise tree over the rows); the
  * caller sums the columns in order, which makes the norms independent of

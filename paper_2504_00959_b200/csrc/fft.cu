@@ -337,10 +337,15 @@ __device__ __forceinline__ double plane_w(const ColArgs &a, int k) {
     return __dadd_rn(a.w_min, __dmul_rn(frac, __dsub_rn(a.w_max, a.w_min)));
 }
 
-// CTA = 4096/N columns for all planes. Plane k+1's first-pass inputs are
-// loaded into registers while plane k is transformed; the last pass leaves
-// its outputs in registers where the phase screen is applied and the planes
-// are summed.
+// CTA = 4096/N columns for all planes. The planes are stacked by Horner's
+// rule from the top plane down: with w_k = w_0 + k dw (mesh.py:101-112),
+//   sum_k P_k exp(2 pi i w_k (n-1)) = c * sum_k P_k z^k
+//       = c * (((P_{K-1} z + P_{K-2}) z + ...) z + P_0),
+//   z = exp(2 pi i dw (n-1)),  c = exp(2 pi i w_0 (n-1)),
+// so a plane costs one complex multiply-add per pixel instead of a phase
+// evaluation (|z| = 1: the rounding grows by about one ulp per plane).
+// Plane k-1's first-pass inputs are loaded into registers while plane k is
+// transformed; the last pass leaves its outputs in registers.
 template <int LOGN>
 __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     k_fft_cols(ColArgs a, const double2 *__restrict__ tw) {
@@ -354,7 +359,7 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     constexpr int M = N / R;
     constexpr int NB = kColE / R;
     extern __shared__ __align__(16) double2 sbuf[];
-    double *nbuf = reinterpret_cast<double *>(sbuf + 2 * C * STRIDE);  // n = sqrt(1-l^2-m^2), [C][N]
+    double2 *zbuf = sbuf + 2 * C * STRIDE;       // z per pixel, [C][N]
 
     const int c0 = blockIdx.x * C;                 // first local column
     const int nk = a.k1 - a.k0;                    // planes in this call
@@ -391,30 +396,31 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
 #pragma unroll
         for (int i = 0; i < kColE; ++i) dst[i] = off[i] >= 0 ? src[off[i]] : make_double2(0.0, 0.0);
     };
-
-    // direction-cosine factor per pixel (mesh.py:202-208, transform.py:200)
-    for (int e = threadIdx.x; e < C * N; e += CT) {
-        const int cc = e / N, j = e % N;
+    // direction-cosine factor of a pixel (mesh.py:202-208, transform.py:200)
+    auto n_of = [&](int cc, int j) {
         const int gi = a.g0 * kG + c0 + cc;
         const double l = (double)(gi - a.n_u / 2) * a.cell;
         const double m = (double)(j - a.n_v / 2) * a.cell;
-        nbuf[e] = __dsqrt_rn(__dsub_rn(__dsub_rn(1.0, __dmul_rn(l, l)), __dmul_rn(m, m)));
-    }
+        return __dsqrt_rn(__dsub_rn(__dsub_rn(1.0, __dmul_rn(l, l)), __dmul_rn(m, m)));
+    };
 
-    // the running stack of earlier plane ranges continues in the same order
+    const double dw = a.n_w > 1 ? (a.w_max - a.w_min) / (double)(a.n_w - 1) : 0.0;
+    for (int e = threadIdx.x; e < C * N; e += CT)
+        zbuf[e] = cis_pi(2.0 * dw * (n_of(e / N, e % N) - 1.0));
+
+    // the running stack of the planes above this range continues
     double2 *run = a.run + (int64_t)blockIdx.x * kColE * CT + threadIdx.x;
     double2 acc[kColE];
 #pragma unroll
-    for (int i = 0; i < kColE; ++i) acc[i] = a.k0 > 0 ? run[i * CT] : make_double2(0.0, 0.0);
+    for (int i = 0; i < kColE; ++i) acc[i] = a.k1 < a.n_w ? run[i * CT] : make_double2(0.0, 0.0);
     double2 pf[kColE];
-    gld_plane(0, pf);
+    gld_plane(nk - 1, pf);
 
-    for (int kl = 0; kl < nk; ++kl) {
-        const int k = a.k0 + kl;
+    for (int kl = nk - 1; kl >= 0; --kl) {
         double2 v[kColE];
 #pragma unroll
         for (int i = 0; i < kColE; ++i) v[i] = pf[i];
-        if (kl + 1 < nk) gld_plane(kl + 1, pf);
+        if (kl > 0) gld_plane(kl - 1, pf);
         pass_compute<LOGN, P0::RL, kColE, CT>(1, tw, v);
         if constexpr (!P0::LAST) {
             __syncthreads();  // the previous plane's last pass has read sbuf
@@ -424,24 +430,23 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
             smem_passes<LOGN, RLM, kColE, CT, P0::RL>(sbuf, tw, v);
         }
         // v[kb*R + r] is output row j + r*M of sequence (column) seq
-        const double wk = plane_w(a, k);
 #pragma unroll
         for (int kb = 0; kb < NB; ++kb) {
             const int b = threadIdx.x + kb * CT;
             const int seq = b / M, j = b % M;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                double2 z = v[kb * R + r];
-                if (wk != 0.0) {  // transform.py:196-198
-                    const double n = nbuf[seq * N + j + r * M];
-                    z = cmul(z, cis_pi(2.0 * wk * (n - 1.0)));
-                }
-                acc[kb * R + r] = cadd(acc[kb * R + r], z);
+                const double2 z = zbuf[seq * N + j + r * M];
+                const double2 p = v[kb * R + r];
+                double2 &q = acc[kb * R + r];
+                const double qx = fma(q.x, z.x, fma(-q.y, z.y, p.x));
+                q.y = fma(q.x, z.y, fma(q.y, z.x, p.y));
+                q.x = qx;
             }
         }
     }
 
-    if (a.k1 < a.n_w) {  // more planes to come: park the running stack
+    if (a.k0 > 0) {  // planes below this range to come: park the running stack
 #pragma unroll
         for (int i = 0; i < kColE; ++i) run[i * CT] = acc[i];
         return;
@@ -452,6 +457,7 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     // the image strip is written row by row and the residual norms are
     // reduced per column in a fixed tree order (identical for any GPU count).
     __syncthreads();  // both plane buffers are free now
+    const double w0 = plane_w(a, 0);
     double2 *pix = sbuf;                        // (re, im) per pixel, [C][STRIDE]
     double2 *sq = sbuf + C * STRIDE;            // (im^2, re^2) per pixel
 #pragma unroll
@@ -461,12 +467,12 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int row = j + r * M;
-            double2 z = acc[kb * R + r];
+            const double n = n_of(seq, row);
+            double2 z = cmul(acc[kb * R + r], cis_pi(2.0 * w0 * (n - 1.0)));
             z.x *= a.inv_nuv;
             z.y *= a.inv_nuv;
             z.x = __dmul_rn(z.x, a.inv_nw);
             z.y = __dmul_rn(z.y, a.inv_nw);
-            const double n = nbuf[seq * N + row];
             const double re = __dsub_rn(__dmul_rn(z.x, n), __dmul_rn(z.y, 0.0));
             const double im = __dadd_rn(__dmul_rn(z.x, 0.0), __dmul_rn(z.y, n));
             pix[seq * STRIDE + pidx(row)] = make_double2(re, im);
@@ -525,7 +531,7 @@ int launch_cols(wsb_ctx *ctx, const ColArgs &a, const double2 *tw, int *nblocks)
     constexpr int N = 1 << LOGN;
     constexpr int CT = ColCfg<LOGN>::T;
     constexpr int C = CT * kColE / N;
-    const size_t smem = sizeof(double2) * 2 * C * Seq<LOGN>::STRIDE + sizeof(double) * C * N;
+    const size_t smem = sizeof(double2) * (2 * C * Seq<LOGN>::STRIDE + C * N);
     WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     *nblocks = ceil_div(a.ncols, C);

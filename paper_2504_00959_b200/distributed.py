@@ -78,12 +78,13 @@ class CudaBackend:
         return grid_p
 
     def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng, plane_lo=0, plane_hi=None):
-        """Column pass + stack of planes [plane_lo, plane_hi) (ranges in order;
-        the context carries the running stack). Returns (strip, partials)
-        after the range ending at n_w, (None, None) before."""
+        """Column pass + stack of planes [plane_lo, plane_hi) (ranges in
+        descending order; the context carries the running stack). Returns
+        (strip, partials) after the range starting at plane 0, (None, None)
+        before."""
         plane_hi = spec.n_w if plane_hi is None else plane_hi
         g = spec.c_struct()
-        final = plane_hi == spec.n_w
+        final = plane_lo == 0
         strip = torch.empty((spec.n_v, ng * G) if final else (1,), dtype=torch.float64,
                             device=self.device)
         partials = torch.empty((ng * G, 2) if final else (1,), dtype=torch.float64,
@@ -132,10 +133,11 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     own time partition (records in gindex order, rank r holding the r-th
     contiguous block, as visdata.partition_time_ordered produces).
 
-    The slab transpose is pipelined over ``n_ranges`` plane ranges: the
-    all-to-all of range i runs on NCCL's stream while the row pass of range
-    i+1 and the column pass of range i-1 run on the compute stream. The
-    result does not depend on n_ranges (the planes are stacked in order).
+    The slab transpose is pipelined over ``n_ranges`` plane ranges (from the
+    top plane down, the stacking order of the column pass): the all-to-all
+    of one range runs on NCCL's stream while the row pass of the next range
+    and the column pass of the previous one run on the compute stream. The
+    result does not depend on n_ranges.
     ``timings``, if a dict, receives per-stage milliseconds of the compute
     stream (and the bucket / sweep split of the gridder).
 
@@ -186,7 +188,7 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     dest_pairs = [ng_d for _, ng_d in cols]
     src_rows = [vc_s for _, vc_s in slabs]
     inflight = []
-    for k0, k1 in plane_ranges(spec.n_w, n_ranges):
+    for k0, k1 in reversed(plane_ranges(spec.n_w, n_ranges)):   # top planes first
         nk = k1 - k0
         grid_p = be.fft_rows(grid_s, spec, vc, dest_pairs, k0, k1)   # [dest][plane][pair][row][G]
         in_splits = [nk * ng_d * vc * G * 2 for ng_d in dest_pairs]   # float64 elements per rank

@@ -64,8 +64,8 @@ class NumpyBackend:
         return torch.from_numpy(np.concatenate(out).view(np.float64))
 
     def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng, plane_lo=0, plane_hi=None):
-        """Plane ranges accumulate in self._run between calls (the context's
-        running stack in the CUDA backend)."""
+        """Plane ranges come in descending order (the CUDA backend's
+        contract); their planes are kept until the range starting at 0."""
         plane_hi = spec.n_w if plane_hi is None else plane_hi
         nk = plane_hi - plane_lo
         t = tgrid.numpy().view(np.complex128)
@@ -85,15 +85,18 @@ class NumpyBackend:
         l = np.broadcast_to(cols * spec.cell_size_lm, (spec.n_v, ncols))
         m = np.broadcast_to((rowsv * spec.cell_size_lm)[:, None], (spec.n_v, ncols))
         n = np.sqrt(1.0 - l * l - m * m)
-        acc = np.zeros((spec.n_v, ncols), np.complex128) if plane_lo == 0 else self._run
+        # ranges arrive top-down; the oracle's order (k ascending) at the end
+        if plane_hi == spec.n_w:
+            self._planes = {}
         for k in range(plane_lo, plane_hi):
             wk = O.plane_w_native(k, spec.n_w, spec.w_min_native, spec.w_max_native)
             pk = planes[k - plane_lo]
-            p = pk if wk == 0.0 else pk * np.exp(2j * np.pi * wk * (n - 1.0))
-            acc = acc + p
-        if plane_hi < spec.n_w:
-            self._run = acc
+            self._planes[k] = pk if wk == 0.0 else pk * np.exp(2j * np.pi * wk * (n - 1.0))
+        if plane_lo > 0:
             return None, None
+        acc = np.zeros((spec.n_v, ncols), np.complex128)
+        for k in range(spec.n_w):
+            acc = acc + self._planes[k]
         acc = acc / spec.n_w * n
         strip = np.ascontiguousarray(acc.real)
         partials = np.stack([(acc.imag ** 2).sum(axis=0), (acc.real ** 2).sum(axis=0)], axis=1)

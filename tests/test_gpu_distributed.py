@@ -63,7 +63,7 @@ def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges=1):
     pix = np.empty((spec.n_v, spec.n_u))
     parts = []
     for d, (g0, ng) in enumerate(cols):
-        for i, (k0, k1) in enumerate(plane_ranges(spec.n_w, n_ranges)):
+        for i, (k0, k1) in reversed(list(enumerate(plane_ranges(spec.n_w, n_ranges)))):
             # the all-to-all: destination d's block of every source, in source order
             chunks = []
             for (v0, vc), gps in zip(slabs, grids):
