@@ -185,7 +185,7 @@ int wsb_ctx_destroy(wsb_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto &b : ctx->bufs)
         if (b.ptr) cudaFree(b.ptr);
-    for (int i = 0; i < 16; ++i)
+    for (int i = 0; i < 32; ++i)
         if (ctx->twiddle[i]) cudaFree(ctx->twiddle[i]);
     if (ctx->timing.created)
         for (int i = 0; i < 8; ++i) cudaEventDestroy(ctx->timing.ev[i]);
@@ -366,8 +366,8 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
     WSB_TRY(ensure(ctx, kSlotStrip, sizeof(double) * (2 * (size_t)n_u + 4), (void **)&partials));
     WSB_TRY(ensure(ctx, kSlotU64, 64, (void **)&upd));
     const double *tw;
-    WSB_TRY(twiddles(ctx, n_u, &tw));
-    WSB_TRY(twiddles(ctx, n_v, &tw));
+    WSB_TRY(twiddles(ctx, n_u, 4, &tw));   // row plan (radix 16)
+    WSB_TRY(twiddles(ctx, n_v, 3, &tw));   // column plan (radix 8)
 
     WSB_CUDA_TRY(cudaEventRecord(ev[0], ctx->stream));
     WSB_CUDA_TRY(cudaMemsetAsync(upd, 0, sizeof(unsigned long long), ctx->stream));

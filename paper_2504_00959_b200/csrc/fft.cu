@@ -165,6 +165,21 @@ __device__ __forceinline__ void pass_load(double2 (&v)[E], LD ld) {
     }
 }
 
+// Twiddles of a pass (span ns, radix R) are stored pass by pass as
+// [r - 1][j % ns] = exp(2 pi i (j % ns) r / (ns R)), so the lanes of a warp
+// (consecutive j) read consecutive entries: a few sectors per load instead
+// of one sector per lane from a strided N-entry table.
+constexpr int tw_offset(int logn, int rlmax, int done) {
+    int off = 0, d = 0;
+    while (d < done) {
+        const int first = logn % rlmax;
+        const int rl = (d == 0 && first != 0) ? first : rlmax;
+        if (d > 0) off += ((1 << rl) - 1) << d;
+        d += rl;
+    }
+    return off;
+}
+
 template <int LOGN, int RL, int E, int T>
 __device__ __forceinline__ void pass_compute(int ns, const double2 *__restrict__ tw,
                                              double2 (&v)[E]) {
@@ -176,9 +191,9 @@ __device__ __forceinline__ void pass_compute(int ns, const double2 *__restrict__
 #pragma unroll
         for (int r = 0; r < R; ++r) y[r] = v[k * R + r];
         if (ns > 1) {
-            const int step = (j % ns) * (N / (ns * R));
+            const double2 *t = tw + (j % ns);
 #pragma unroll
-            for (int r = 1; r < R; ++r) y[r] = cmul(y[r], __ldg(&tw[r * step]));
+            for (int r = 1; r < R; ++r) y[r] = cmul(y[r], __ldg(&t[(r - 1) * ns]));
         }
         dft_inv<R>(y);
 #pragma unroll
@@ -216,7 +231,7 @@ __device__ __forceinline__ void smem_passes(double2 *s, const double2 *tw, doubl
     auto ld = [&](int seq, int idx) { return s[seq * STRIDE + pidx(idx)]; };
     pass_load<LOGN, P::RL, E, T>(v, ld);
     if constexpr (!P::LAST) __syncthreads();
-    pass_compute<LOGN, P::RL, E, T>(1 << DONE, tw, v);
+    pass_compute<LOGN, P::RL, E, T>(1 << DONE, tw + tw_offset(LOGN, RLMAX, DONE), v);
     if constexpr (!P::LAST) {
         auto st = [&](int seq, int idx, double2 z) { s[seq * STRIDE + pidx(idx)] = z; };
         pass_store<LOGN, P::RL, E, T>(1 << DONE, v, st);
@@ -501,12 +516,31 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
         }
 }
 
-__global__ void k_twiddles(double2 *tw, int n) {
-    const int m = blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= n) return;
+// pass-ordered twiddle table of an N-point plan (see tw_offset): entry
+// [r - 1][t] of the pass with span ns and radix R is exp(2 pi i m / N),
+// m = t r N / (ns R) -- the same sincospi values as an N-entry table
+__global__ void k_twiddles(double2 *tw, int logn, int rlmax, int size) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= size) return;
+    const int n = 1 << logn;
+    int off = 0, d = 0, m = 0;
+    while (d < logn) {
+        const int first = logn % rlmax;
+        const int rl = (d == 0 && first != 0) ? first : rlmax;
+        if (d > 0) {
+            const int ns = 1 << d, sz = ((1 << rl) - 1) << d;
+            if (e < off + sz) {
+                const int r = (e - off) / ns + 1, t = (e - off) % ns;
+                m = t * r * (n >> (d + rl));
+                break;
+            }
+            off += sz;
+        }
+        d += rl;
+    }
     double sn, cs;
     sincospi(2.0 * (double)m / (double)n, &sn, &cs);
-    tw[m] = make_double2(cs, sn);
+    tw[e] = make_double2(cs, sn);
 }
 
 template <int LOGN>
@@ -543,15 +577,19 @@ int launch_cols(wsb_ctx *ctx, const ColArgs &a, const double2 *tw, int *nblocks)
 
 }  // namespace
 
-int twiddles(wsb_ctx *ctx, int n, const double **out) {
+int twiddles(wsb_ctx *ctx, int n, int rlmax, const double **out) {
     const int l = ilog2(n);
-    if (!ctx->twiddle[l]) {
-        WSB_CUDA_TRY(cudaMalloc(&ctx->twiddle[l], sizeof(double2) * n));
-        k_twiddles<<<ceil_div(n, 256), 256, 0, ctx->stream>>>((double2 *)ctx->twiddle[l], n);
+    const int key = l + 16 * (rlmax - 3);
+    if (rlmax < 3 || rlmax > 4) return fail(WSB_EINVAL, "twiddle plan radix");
+    if (!ctx->twiddle[key]) {
+        const int size = std::max(1, tw_offset(l, rlmax, l));
+        WSB_CUDA_TRY(cudaMalloc(&ctx->twiddle[key], sizeof(double2) * size));
+        k_twiddles<<<ceil_div(size, 256), 256, 0, ctx->stream>>>((double2 *)ctx->twiddle[key], l,
+                                                                 rlmax, size);
         ctx->launches += 1;
         WSB_CUDA_TRY(cudaGetLastError());
     }
-    *out = ctx->twiddle[l];
+    *out = ctx->twiddle[key];
     return WSB_OK;
 }
 
@@ -559,7 +597,7 @@ int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a,
              int plo, int phi, int n_dest, const int32_t *dest_groups) {
     if (phi <= plo || v_count <= 0) return WSB_OK;
     const double *tw;
-    WSB_TRY(twiddles(ctx, g->n_u, &tw));
+    WSB_TRY(twiddles(ctx, g->n_u, kRowRL, &tw));
     const int ng = g->n_u / kG, ns = ceil_div(g->n_u, 32);
     RowDest dst;
     dst.n_w = phi - plo;  // the output holds planes [plo, phi) only
@@ -619,7 +657,7 @@ int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t
         WSB_TRY(ensure(ctx, kSlotColRun, bytes, (void **)&a.run));
     }
     const double *tw;
-    WSB_TRY(twiddles(ctx, g->n_v, &tw));
+    WSB_TRY(twiddles(ctx, g->n_v, kColRL, &tw));
     const double2 *t2 = (const double2 *)tw;
     int nb = 0;
     switch (ilog2(g->n_v)) {

@@ -54,8 +54,8 @@ struct wsb_ctx {
     int *flag_host = nullptr;         // pinned scratch for small readbacks
     unsigned long long *u64_host = nullptr;
     wsb::Timing timing;
-    // twiddle tables keyed by log2(n)
-    double *twiddle[16] = {nullptr};
+    // pass-ordered twiddle tables keyed by log2(n) + 16 * (plan radix bits - 3)
+    double *twiddle[32] = {nullptr};
     // last bucketing (for wsb_tiles_debug)
     int64_t last_entries = 0, last_tiles = 0;
     uint32_t *last_keys = nullptr, *last_idx = nullptr, *last_off = nullptr;
@@ -96,7 +96,7 @@ enum Slot {
 };
 
 int ensure(wsb_ctx *ctx, int slot, size_t bytes, void **out);
-int twiddles(wsb_ctx *ctx, int n, const double **out);
+int twiddles(wsb_ctx *ctx, int n, int rlmax, const double **out);
 
 // scan.cu
 int exclusive_scan_u32(wsb_ctx *ctx, const uint32_t *in, uint32_t *out, int64_t n,
