@@ -102,7 +102,9 @@ int wsb_ctx_trim(wsb_ctx *ctx);
  * processed in array order, the (time_index, gindex) order the reference's
  * exchange produces for time-sorted input), vis = interleaved (re, im) f32
  * [n][n_chan][2], weight f32[n][n_chan]; image_out f64[n_v][n_u].
- * Copies in and out are part of the call. Synchronous. */
+ * Copies in and out are part of the call. Synchronous. Page-locked buffers
+ * (cudaHostAlloc / cudaHostRegister) move at DMA speed; pageable ones work
+ * but the driver stages them (~10x slower for the image copy-out). */
 int wsb_image(const wsb_grid *grid, const wsb_kernel *kern, const wsb_exec *exec,
               const double *u, const double *v, const double *w,
               const uint32_t *time_index, const float *vis, const float *weight,

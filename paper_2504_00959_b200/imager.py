@@ -341,7 +341,9 @@ def image(u, v, w, time_index, vis, weight, spec, kern, device: int = 0) -> tupl
     weight = np.ascontiguousarray(_cols2d(np.asarray(weight, np.float32), n))
     if not (len(v) == len(w) == n and vis.shape == weight.shape):
         raise ValueError("inconsistent column lengths")
-    out = np.empty((spec.n_v, spec.n_u), np.float64)
+    # page-locked result buffer: the device->host copy runs at DMA speed
+    # (a pageable destination costs ~10x on the 32 MB cfg2 image)
+    out = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, pin_memory=True).numpy()
     d = L.WsbDiag()
     g, k = spec.c_struct(), kern.c_struct()
     ex = L.WsbExec(int(device), 64, 1, 0)
