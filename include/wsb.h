@@ -45,10 +45,13 @@ extern "C" {
 #define WSB_KERNEL_GAUSSIAN       0
 #define WSB_KERNEL_KAISER_BESSEL  1
 
-/* Column-group width of the internal "P layout" grid:
+/* Column-group width of the internal "P layout" grid (row-pass output,
+ * column-pass input):
  *   P[plane][col / WSB_P_GROUP][row][col % WSB_P_GROUP]  (complex128)
- * The sign (-1)^(i+j) of transform.py:180-185 is already applied. */
-#define WSB_P_GROUP 2
+ * i.e. column-major: every column of a plane is one contiguous run, read
+ * by the column pass with full 32-byte sectors. The sign (-1)^(i+j) of
+ * transform.py:180-185 is already applied. */
+#define WSB_P_GROUP 1
 
 /* Largest transform length handled on chip in this build. */
 #define WSB_MAX_FFT_N 4096

@@ -19,7 +19,7 @@ WSB_ECUDA = -2
 WSB_ENCCL = -3
 WSB_ENOMEM = -4
 WSB_EUNSUPPORTED = -5
-P_GROUP = 2
+P_GROUP = 1
 KERNEL_GAUSSIAN = 0
 KERNEL_KAISER_BESSEL = 1
 

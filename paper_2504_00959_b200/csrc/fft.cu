@@ -140,11 +140,29 @@ __device__ __forceinline__ void dft_inv(double2 *y) {
 // padded shared-memory index of element idx of a sequence
 __device__ __forceinline__ int pidx(int idx) { return idx + (idx >> 4); }
 
+// padded sequence stride: = 4 (mod 8) in 16-byte units for N >= 64, so the
+// two sequences of an interleaved pass (IL = 2) fall on disjoint bank halves
 template <int LOGN>
 struct Seq {
     static constexpr int N = 1 << LOGN;
-    static constexpr int STRIDE = N + (N >> 4) + (N >= 16 ? 2 : 0);  // padded sequence stride
+    static constexpr int STRIDE = N + (N >> 4) + (N >= 16 ? 4 : 0);
 };
+
+// Butterfly b -> (sequence, index j). IL = 1: b / M, b % M. IL = 2: two
+// sequences interleaved lane by lane, so a warp touches element j of both
+// sequences side by side (the row pass's last stores: rows j0, j0+1 of a
+// column are one 32-byte sector of the column-major P layout).
+template <int IL, int M>
+__device__ __forceinline__ void seq_of(int b, int &seq, int &j) {
+    if constexpr (IL == 1) {
+        seq = b / M;
+        j = b % M;
+    } else {
+        const int q = b % (M * IL);
+        seq = (b / (M * IL)) * IL + q % IL;
+        j = q / IL;
+    }
+}
 
 
 // ---------------------------------------------------------------------------
@@ -153,13 +171,13 @@ struct Seq {
 // A pass reads x[j + r N/R], multiplies by the twiddles of its stage,
 // applies the radix-R DFT and writes y[(j/ns) ns R + j%ns + r ns].
 // ---------------------------------------------------------------------------
-template <int LOGN, int RL, int E, int T, class LD>
+template <int LOGN, int RL, int E, int T, int IL = 1, class LD>
 __device__ __forceinline__ void pass_load(double2 (&v)[E], LD ld) {
     constexpr int R = 1 << RL, NB = E / R, M = (1 << LOGN) / R;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
-        const int b = threadIdx.x + k * T;
-        const int seq = b / M, j = b % M;
+        int seq, j;
+        seq_of<IL, M>(threadIdx.x + k * T, seq, j);
 #pragma unroll
         for (int r = 0; r < R; ++r) v[k * R + r] = ld(seq, j + r * M);
     }
@@ -180,13 +198,14 @@ constexpr int tw_offset(int logn, int rlmax, int done) {
     return off;
 }
 
-template <int LOGN, int RL, int E, int T>
+template <int LOGN, int RL, int E, int T, int IL = 1>
 __device__ __forceinline__ void pass_compute(int ns, const double2 *__restrict__ tw,
                                              double2 (&v)[E]) {
     constexpr int N = 1 << LOGN, R = 1 << RL, NB = E / R, M = N / R;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
-        const int j = (threadIdx.x + k * T) % M;
+        int seq, j;
+        seq_of<IL, M>(threadIdx.x + k * T, seq, j);
         double2 y[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) y[r] = v[k * R + r];
@@ -201,13 +220,13 @@ __device__ __forceinline__ void pass_compute(int ns, const double2 *__restrict__
     }
 }
 
-template <int LOGN, int RL, int E, int T, class ST>
+template <int LOGN, int RL, int E, int T, int IL = 1, class ST>
 __device__ __forceinline__ void pass_store(int ns, const double2 (&v)[E], ST st) {
     constexpr int R = 1 << RL, NB = E / R, M = (1 << LOGN) / R;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
-        const int b = threadIdx.x + k * T;
-        const int seq = b / M, j = b % M;
+        int seq, j;
+        seq_of<IL, M>(threadIdx.x + k * T, seq, j);
         const int idxd = (j / ns) * ns * R + j % ns;
 #pragma unroll
         for (int r = 0; r < R; ++r) st(seq, idxd + r * ns, v[k * R + r]);
@@ -223,20 +242,22 @@ struct Plan {
 };
 
 // Passes 1..last-1 in shared memory (in place), then the last pass's loads
-// and compute: its results stay in v, at (seq, j + r*N/R) of butterfly b.
-template <int LOGN, int RLMAX, int E, int T, int DONE>
+// and compute: its results stay in v, at (seq, j + r*N/R) of butterfly b
+// (mapped with ILL, the interleave of the last pass).
+template <int LOGN, int RLMAX, int E, int T, int DONE, int ILL = 1>
 __device__ __forceinline__ void smem_passes(double2 *s, const double2 *tw, double2 (&v)[E]) {
     using P = Plan<LOGN, RLMAX, DONE>;
     constexpr int STRIDE = Seq<LOGN>::STRIDE;
+    constexpr int IL = P::LAST ? ILL : 1;
     auto ld = [&](int seq, int idx) { return s[seq * STRIDE + pidx(idx)]; };
-    pass_load<LOGN, P::RL, E, T>(v, ld);
+    pass_load<LOGN, P::RL, E, T, IL>(v, ld);
     if constexpr (!P::LAST) __syncthreads();
-    pass_compute<LOGN, P::RL, E, T>(1 << DONE, tw + tw_offset(LOGN, RLMAX, DONE), v);
+    pass_compute<LOGN, P::RL, E, T, IL>(1 << DONE, tw + tw_offset(LOGN, RLMAX, DONE), v);
     if constexpr (!P::LAST) {
         auto st = [&](int seq, int idx, double2 z) { s[seq * STRIDE + pidx(idx)] = z; };
         pass_store<LOGN, P::RL, E, T>(1 << DONE, v, st);
         __syncthreads();
-        smem_passes<LOGN, RLMAX, E, T, DONE + P::RL>(s, tw, v);
+        smem_passes<LOGN, RLMAX, E, T, DONE + P::RL, ILL>(s, tw, v);
     }
 }
 
@@ -314,9 +335,12 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
         auto sst = [&](int seq, int idx, double2 z) { s[seq * STRIDE + pidx(idx)] = z; };
         pass_store<LOGN, P0::RL, kRowE, RT>(1, v, sst);
         __syncthreads();
-        smem_passes<LOGN, kRowRL, kRowE, RT, P0::RL>(s, tw, v);
+        // last pass with the two rows of a CTA interleaved lane by lane: the
+        // column-major P layout then receives full 32-byte sectors
+        constexpr int ILL = NSEQ >= 2 ? 2 : 1;
+        smem_passes<LOGN, kRowRL, kRowE, RT, P0::RL, ILL>(s, tw, v);
         constexpr int RLL = kRowRL;  // the last pass is always a full-radix pass here
-        pass_store<LOGN, RLL, kRowE, RT>(N >> RLL, v, gst);
+        pass_store<LOGN, RLL, kRowE, RT, ILL>(N >> RLL, v, gst);
     }
 }
 

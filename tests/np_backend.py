@@ -11,7 +11,7 @@ import torch
 
 from oracle import wstack_oracle as O
 
-G = 2
+G = 1
 
 
 class NumpyBackend:

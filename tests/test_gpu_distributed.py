@@ -40,7 +40,7 @@ def _parts(t, R):
 def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges=1):
     from paper_2504_00959_b200.distributed import CudaBackend, plane_ranges
     be = CudaBackend(0)
-    G = 2
+    G = 1
     S = kern.half_support
     slabs = [W.partition_1d(spec.n_v, R, d) for d in range(R)]
     cols = [W.partition_1d(spec.n_u // G, R, d) for d in range(R)]
