@@ -137,15 +137,18 @@ __device__ __forceinline__ void dft_inv(double2 *y) {
     dit_stages<R, 2>(y);
 }
 
-// padded shared-memory index of element idx of a sequence
-__device__ __forceinline__ int pidx(int idx) { return idx + (idx >> 4); }
+// padded shared-memory index of element idx of a sequence: one pad slot per
+// 8 elements keeps the 8 lanes of a 128-byte wavefront on distinct bank
+// groups for contiguous runs and for the stride-4/8 and (ns = 4) stores of
+// the radix-4/8 passes
+__device__ __forceinline__ int pidx(int idx) { return idx + (idx >> 3); }
 
 // padded sequence stride: = 4 (mod 8) in 16-byte units for N >= 64, so the
 // two sequences of an interleaved pass (IL = 2) fall on disjoint bank halves
 template <int LOGN>
 struct Seq {
     static constexpr int N = 1 << LOGN;
-    static constexpr int STRIDE = N + (N >> 4) + (N >= 16 ? 4 : 0);
+    static constexpr int STRIDE = N + (N >> 3) + (N >= 16 ? 4 : 0);
 };
 
 // Butterfly b -> (sequence, index j). IL = 1: b / M, b % M. IL = 2: two
