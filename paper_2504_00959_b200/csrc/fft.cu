@@ -186,8 +186,8 @@ __device__ __forceinline__ void pass_load(double2 (&v)[E], LD ld) {
     }
 }
 
-// Twiddles of a pass (span ns, radix R) are stored pass by pass as
-// [r - 1][j % ns] = exp(2 pi i (j % ns) r / (ns R)), so the lanes of a warp
+// The base twiddle of a pass (span ns, radix R) is stored pass by pass as
+// [j % ns] = exp(2 pi i (j % ns) / (ns R)), so the lanes of a warp
 // (consecutive j) read consecutive entries: a few sectors per load instead
 // of one sector per lane from a strided N-entry table.
 constexpr int tw_offset(int logn, int rlmax, int done) {
@@ -195,7 +195,7 @@ constexpr int tw_offset(int logn, int rlmax, int done) {
     while (d < done) {
         const int first = logn % rlmax;
         const int rl = (d == 0 && first != 0) ? first : rlmax;
-        if (d > 0) off += ((1 << rl) - 1) << d;
+        if (d > 0) off += 1 << d;
         d += rl;
     }
     return off;
@@ -213,9 +213,15 @@ __device__ __forceinline__ void pass_compute(int ns, const double2 *__restrict__
 #pragma unroll
         for (int r = 0; r < R; ++r) y[r] = v[k * R + r];
         if (ns > 1) {
-            const double2 *t = tw + (j % ns);
+            // one table load per butterfly; the other powers by a product
+            // tree w^r = w^(r/2) w^(r - r/2) (depth log2 R, a few ulp): the
+            // loads, not the FP64 pipe, are what the passes queue on
+            double2 wp[R];
+            wp[1] = __ldg(&tw[j % ns]);
 #pragma unroll
-            for (int r = 1; r < R; ++r) y[r] = cmul(y[r], __ldg(&t[(r - 1) * ns]));
+            for (int r = 2; r < R; ++r) wp[r] = cmul(wp[r / 2], wp[r - r / 2]);
+#pragma unroll
+            for (int r = 1; r < R; ++r) y[r] = cmul(y[r], wp[r]);
         }
         dft_inv<R>(y);
 #pragma unroll
@@ -543,9 +549,8 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
         }
 }
 
-// pass-ordered twiddle table of an N-point plan (see tw_offset): entry
-// [r - 1][t] of the pass with span ns and radix R is exp(2 pi i m / N),
-// m = t r N / (ns R) -- the same sincospi values as an N-entry table
+// pass-ordered twiddle table of an N-point plan (see tw_offset): entry [t]
+// of the pass with span ns and radix R is exp(2 pi i m / N), m = t N / (ns R)
 __global__ void k_twiddles(double2 *tw, int logn, int rlmax, int size) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= size) return;
@@ -555,13 +560,12 @@ __global__ void k_twiddles(double2 *tw, int logn, int rlmax, int size) {
         const int first = logn % rlmax;
         const int rl = (d == 0 && first != 0) ? first : rlmax;
         if (d > 0) {
-            const int ns = 1 << d, sz = ((1 << rl) - 1) << d;
-            if (e < off + sz) {
-                const int r = (e - off) / ns + 1, t = (e - off) % ns;
-                m = t * r * (n >> (d + rl));
+            const int ns = 1 << d;
+            if (e < off + ns) {
+                m = (e - off) * (n >> (d + rl));
                 break;
             }
-            off += sz;
+            off += ns;
         }
         d += rl;
     }
