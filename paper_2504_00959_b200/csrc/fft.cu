@@ -282,7 +282,10 @@ struct RowCfg {
 #ifndef WSB_ROW_MIN_T
 #define WSB_ROW_MIN_T 256
 #endif
-    static constexpr int T = ((1 << LOGN) / 16 > WSB_ROW_MIN_T) ? (1 << LOGN) / 16 : WSB_ROW_MIN_T;
+    // N = 4096 takes 2 rows (512 threads) so the interleaved last pass can
+    // write whole 32-byte sectors of the column-major P layout
+    static constexpr int T = LOGN >= 12 ? (1 << LOGN) / 8
+                             : ((1 << LOGN) / 16 > WSB_ROW_MIN_T) ? (1 << LOGN) / 16 : WSB_ROW_MIN_T;
     static constexpr int MINB = T <= 128 ? 4 : (T <= 256 ? 2 : 1);
 };
 constexpr int kRowE = 16;
