@@ -21,6 +21,9 @@ import paper_2504_00959_b200 as W  # noqa: E402
 from lofar import tracks  # noqa: E402
 
 
+STAGES = ("prepare", "route", "exchange", "grid", "bucket", "sweep", "rows", "cols", "gather")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=100_000_000)
@@ -73,6 +76,12 @@ def main():
     if ws == 1:
         kms, _ = W.last_timings(dev)
         out["kernel_ms"] = [round(x, 3) for x in kms]
+    else:
+        tm = {}
+        image_distributed(u, v, w, vis, wt, spec, kern, to_host=False, timings=tm)
+        st = torch.tensor([tm.get(k, 0.0) for k in STAGES], device=dev, dtype=torch.float64)
+        dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        out["stage_ms_max_over_ranks"] = {k: round(float(x), 3) for k, x in zip(STAGES, st.tolist())}
     if a.check:
         # linearity: image(vis_a + vis_b) = image(vis_a) + image(vis_b)
         g = torch.Generator(device=dev).manual_seed(7)
