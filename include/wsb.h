@@ -132,17 +132,29 @@ int wsb_prepare(wsb_ctx *ctx, const wsb_grid *grid,
                 double *rec, uint32_t *plane);
 
 /* Destination slabs of the time->space exchange (comms.py:516-523): counts
- * of records per destination slab of partition_1d(n_v, n_ranks) with the
- * +-half_support halo predicate. counts_host: int64[n_ranks]. Synchronous. */
+ * of records per destination slab with the +-half_support halo predicate.
+ * Slabs are partition_1d(n_v, n_ranks) (mesh.py:34-45) when
+ * slab_starts_host is NULL, else rows [starts[d], starts[d+1]) with
+ * starts[0] = 0 < ... < starts[n_ranks] = n_v (load-balanced slabs; the
+ * image does not depend on the slab rows). counts_host: int64[n_ranks].
+ * Synchronous. */
 int wsb_route_count(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int32_t n_ranks,
-                    const double *rec, int64_t n, int64_t *counts_host);
+                    const int32_t *slab_starts_host, const double *rec, int64_t n,
+                    int64_t *counts_host);
 
 /* Pack the exchange send buffers: records for slab d land at
  * [displ_d, displ_d + count_d) in array (gindex) order; optional src_index
  * receives the local index of each packed record (nullable). */
 int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int32_t n_ranks,
-                   const double *rec, const uint32_t *plane, int64_t n,
-                   double *send_rec, uint32_t *send_plane, int64_t *src_index);
+                   const int32_t *slab_starts_host, const double *rec, const uint32_t *plane,
+                   int64_t n, double *send_rec, uint32_t *send_plane, int64_t *src_index);
+
+/* Records per anchor row floor(gv) of prepared records: hist u32[n_v]
+ * (device). Feeds the load balancing of the slab rows (the
+ * v-slabs of partition_1d are unbalanced for centrally concentrated uv
+ * coverage). Enqueued, no synchronisation. */
+int wsb_row_histogram(wsb_ctx *ctx, const wsb_grid *grid, const double *rec, int64_t n,
+                      uint32_t *hist);
 
 /* grid_sector (gridder.py:186-259) for the slab rows [v_start, v_start+v_count):
  * buckets the m records by (plane, 32-column strip, anchor row) (counting
@@ -172,7 +184,7 @@ int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count,
 /* Column pass + w correction + stacking (transform.py:162-175, 192-230) of
  * planes [plane_lo, plane_hi): input tgrid holds this rank's column pairs
  * [g0, g0+ng) of those planes for all n_v rows, concatenated by source slab s
- * (src_rows[s] rows each, all equal) as
+ * (src_rows[s] >= 1 rows each; slabs may differ in height) as
  *   [s][plane - plane_lo][g - g0][row - row_start_s][G]   (the all-to-all
  * output of wsb_fft_rows with destinations; one source = the P layout).
  * The planes are stacked from the top plane down (Horner's rule in the w

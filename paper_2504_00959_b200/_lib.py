@@ -28,7 +28,7 @@ EXPORTS = (
     "wsb_strerror", "wsb_last_error", "wsb_version", "wsb_ctx_create", "wsb_ctx_destroy",
     "wsb_ctx_set_stream", "wsb_ctx_trim", "wsb_image", "wsb_image_device", "wsb_prepare",
     "wsb_route_count", "wsb_route_pack", "wsb_grid_slab", "wsb_fft_rows", "wsb_fft_cols_stack",
-    "wsb_grid_unpack", "wsb_tiles_debug", "wsb_last_timings",
+    "wsb_grid_unpack", "wsb_tiles_debug", "wsb_last_timings", "wsb_row_histogram",
 )
 
 
@@ -85,8 +85,9 @@ def lib() -> C.CDLL:
         "wsb_image": (C.c_int, [G, K, E, p, p, p, p, p, p, i64, i32, p, D]),
         "wsb_image_device": (C.c_int, [p, G, K, p, p, p, p, p, i64, i32, p, D]),
         "wsb_prepare": (C.c_int, [p, G, p, p, p, p, p, i64, i32, p, p]),
-        "wsb_route_count": (C.c_int, [p, G, i32, i32, p, i64, p]),
-        "wsb_route_pack": (C.c_int, [p, G, i32, i32, p, p, i64, p, p, p]),
+        "wsb_route_count": (C.c_int, [p, G, i32, i32, p, p, i64, p]),
+        "wsb_route_pack": (C.c_int, [p, G, i32, i32, p, p, p, i64, p, p, p]),
+        "wsb_row_histogram": (C.c_int, [p, G, p, i64, p]),
         "wsb_grid_slab": (C.c_int, [p, G, K, i32, i32, p, p, i64, p, p]),
         "wsb_fft_rows": (C.c_int, [p, G, i32, p, p, i32, i32, i32, p]),
         "wsb_fft_cols_stack": (C.c_int, [p, G, i32, p, i32, i32, i32, i32, p, p, p]),

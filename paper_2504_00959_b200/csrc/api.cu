@@ -212,23 +212,33 @@ int wsb_prepare(wsb_ctx *ctx, const wsb_grid *grid, const double *u, const doubl
 }
 
 int wsb_route_count(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int32_t n_ranks,
-                    const double *rec, int64_t n, int64_t *counts_host) {
+                    const int32_t *slab_starts_host, const double *rec, int64_t n,
+                    int64_t *counts_host) {
     if (!ctx || !counts_host) return fail(WSB_EINVAL, "NULL argument");
     WSB_TRY(validate_grid(grid));
     if (half_support < 0) return fail(WSB_EINVAL, "halo_rows must be >= 0");
     WSB_TRY(set_device(ctx));
-    return wsb::route_count(ctx, grid, half_support, n_ranks, rec, n, counts_host, nullptr, nullptr);
+    return wsb::route_count(ctx, grid, half_support, n_ranks, slab_starts_host, rec, n, counts_host,
+                            nullptr, nullptr);
 }
 
 int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int32_t n_ranks,
-                   const double *rec, const uint32_t *plane, int64_t n, double *send_rec,
-                   uint32_t *send_plane, int64_t *src_index) {
+                   const int32_t *slab_starts_host, const double *rec, const uint32_t *plane,
+                   int64_t n, double *send_rec, uint32_t *send_plane, int64_t *src_index) {
     if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
     WSB_TRY(validate_grid(grid));
     if (half_support < 0) return fail(WSB_EINVAL, "halo_rows must be >= 0");
     WSB_TRY(set_device(ctx));
-    return wsb::route_pack(ctx, grid, half_support, n_ranks, rec, plane, n, send_rec, send_plane,
-                           src_index);
+    return wsb::route_pack(ctx, grid, half_support, n_ranks, slab_starts_host, rec, plane, n,
+                           send_rec, send_plane, src_index);
+}
+
+int wsb_row_histogram(wsb_ctx *ctx, const wsb_grid *grid, const double *rec, int64_t n,
+                      uint32_t *hist) {
+    if (!ctx || !hist) return fail(WSB_EINVAL, "NULL argument");
+    WSB_TRY(validate_grid(grid));
+    WSB_TRY(set_device(ctx));
+    return wsb::row_histogram(ctx, grid, rec, n, hist);
 }
 
 static int grid_slab_impl(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,

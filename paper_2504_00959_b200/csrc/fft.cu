@@ -414,15 +414,14 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
 
     const int c0 = blockIdx.x * C;                 // first local column
     const int nk = a.k1 - a.k0;                    // planes in this call
-    // input [s][plane - k0][g][row - row_start_s][x]: every source holds the
-    // same number of rows, so a plane advances every source block by ncols*rows
-    const int64_t plane_elems = (int64_t)a.ncols * (N / a.n_src);
-
-    // In-plane offset of each first-pass input of this thread (the same for
-    // every plane): element (row j, local column c0+seq) of plane 0 in the
-    // transposed layout [s][plane][g][row - row_start_s][x]; -1 past the
-    // last column.
-    int off[kColE];
+    // Offset of each first-pass input of this thread in plane 0 and its
+    // per-plane stride (both the same for every plane): element (row j,
+    // local column c0+seq) in the transposed layout
+    // [s][plane - k0][g][row - row_start_s][x], where source s holds rows
+    // [row_start_s, row_start_{s+1}) -- load-balanced slabs differ in height,
+    // so a plane advances each source block by its own ncols * rows_s.
+    // off = -1 past the last column.
+    int off[kColE], pst[kColE];
     {
         auto offset = [&](int seq, int j) -> double2 {
             const int lc = c0 + seq;
@@ -435,17 +434,20 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
                     r1 = a.src_start[sidx + 1];
                 }
             const int o = nk * a.ncols * r0 + ((lc / kG) * (r1 - r0) + (j - r0)) * kG + (lc % kG);
-            return make_double2(__hiloint2double(o, 0), 0.0);
+            return make_double2(__hiloint2double(o, a.ncols * (r1 - r0)), 0.0);
         };
         double2 t[kColE];
         pass_load<LOGN, P0::RL, kColE, CT>(t, offset);
 #pragma unroll
-        for (int i = 0; i < kColE; ++i) off[i] = __double2hiint(t[i].x);
+        for (int i = 0; i < kColE; ++i) {
+            off[i] = __double2hiint(t[i].x);
+            pst[i] = __double2loint(t[i].x);
+        }
     }
     auto gld_plane = [&](int k, double2 (&dst)[kColE]) {
-        const double2 *src = a.tgrid + (int64_t)k * plane_elems;
 #pragma unroll
-        for (int i = 0; i < kColE; ++i) dst[i] = off[i] >= 0 ? src[off[i]] : make_double2(0.0, 0.0);
+        for (int i = 0; i < kColE; ++i)
+            dst[i] = off[i] >= 0 ? a.tgrid[off[i] + k * pst[i]] : make_double2(0.0, 0.0);
     };
     // direction-cosine factor of a pixel (mesh.py:202-208, transform.py:200)
     auto n_of = [&](int cc, int j) {
@@ -672,10 +674,8 @@ int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t
     for (int s = 0; s < n_sources; ++s) a.src_start[s + 1] = a.src_start[s] + src_rows[s];
     for (int s = n_sources + 1; s < 9; ++s) a.src_start[s] = 1 << 30;
     if (a.src_start[n_sources] != g->n_v) return fail(WSB_EINVAL, "source rows must sum to n_v");
-    for (int s = 1; s < n_sources; ++s)
-        if (src_rows[s] != src_rows[0])
-            return fail(WSB_EUNSUPPORTED, "slabs of unequal height (n_v not a multiple of the rank count)");
-    a.src_start[n_sources] = g->n_v;
+    for (int s = 0; s < n_sources; ++s)
+        if (src_rows[s] < 1) return fail(WSB_EINVAL, "every source slab needs at least one row");
     a.cell = g->cell_size_lm;
     a.inv_nuv = 1.0 / ((double)g->n_u * (double)g->n_v);
     a.inv_nw = 1.0 / (double)g->n_w;

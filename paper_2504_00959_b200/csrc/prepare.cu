@@ -216,7 +216,41 @@ __global__ void __launch_bounds__(kThreads) k_route_pack(
     }
 }
 
+// Records per anchor row floor(gv) (load balancing of the slabs): a block
+// histogram in shared memory, flushed with one global atomic per non-zero bin.
+__global__ void __launch_bounds__(kThreads) k_row_hist(const double4 *__restrict__ rec, int64_t n,
+                                                       int n_v, uint32_t *__restrict__ hist) {
+    extern __shared__ uint32_t h[];
+    for (int i = threadIdx.x; i < n_v; i += kThreads) h[i] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kBlockItems;
+    for (int it = 0; it < kBlockItems / kThreads; ++it) {
+        const int64_t i = base + it * kThreads + threadIdx.x;
+        if (i < n) {
+            const int row = min(max((int)floor(rec[i].y), 0), n_v - 1);
+            atomicAdd(&h[row], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_v; i += kThreads)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
 }  // namespace
+
+int row_histogram(wsb_ctx *ctx, const wsb_grid *g, const double *rec, int64_t n, uint32_t *hist) {
+    WSB_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * g->n_v, ctx->stream));
+    if (n <= 0) return WSB_OK;
+    const size_t smem = sizeof(uint32_t) * g->n_v;
+    if (smem > 200 * 1024) return fail(WSB_EUNSUPPORTED, "row histogram above 51200 rows");
+    WSB_CUDA_TRY(cudaFuncSetAttribute(k_row_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    k_row_hist<<<ceil_div(n, kBlockItems), kThreads, smem, ctx->stream>>>((const double4 *)rec, n,
+                                                                          g->n_v, hist);
+    ctx->launches += 1;
+    WSB_CUDA_TRY(cudaGetLastError());
+    return WSB_OK;
+}
 
 int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v, const double *w,
             const float *vis, const float *weight, int64_t n, int32_t n_chan, double *rec,
@@ -245,10 +279,21 @@ int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v, c
     return WSB_OK;
 }
 
-static int make_slabs(int n_v, int R, Slabs *sl) {
+// Slab rows: partition_1d (mesh.py:34-45) or explicit starts (load-balanced
+// slabs: starts[0] = 0 < starts[1] < ... < starts[R] = n_v).
+static int make_slabs(int n_v, int R, const int32_t *starts, Slabs *sl) {
     if (R < 1 || R > 8) return fail(WSB_EINVAL, "n_ranks must be in [1, 8]");
     if (R > n_v) return fail(WSB_EINVAL, "n_ranks exceeds n_v");
-    const int q = n_v / R, r = n_v % R;  // partition_1d (mesh.py:34-45)
+    if (starts) {
+        if (starts[0] != 0 || starts[R] != n_v) return fail(WSB_EINVAL, "slab starts must span [0, n_v]");
+        for (int d = 0; d < R; ++d) {
+            if (starts[d + 1] <= starts[d]) return fail(WSB_EINVAL, "slab starts must increase");
+            sl->start[d] = starts[d];
+            sl->count[d] = starts[d + 1] - starts[d];
+        }
+        return WSB_OK;
+    }
+    const int q = n_v / R, r = n_v % R;
     for (int d = 0; d < R; ++d) {
         sl->start[d] = d < r ? d * (q + 1) : r * (q + 1) + (d - r) * q;
         sl->count[d] = d < r ? q + 1 : q;
@@ -256,10 +301,11 @@ static int make_slabs(int n_v, int R, Slabs *sl) {
     return WSB_OK;
 }
 
-int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const double *rec, int64_t n,
-                int64_t *counts_host, uint32_t **offs_out, int *nb_out) {
+int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *starts,
+                const double *rec, int64_t n, int64_t *counts_host, uint32_t **offs_out,
+                int *nb_out) {
     Slabs sl;
-    WSB_TRY(make_slabs(g->n_v, R, &sl));
+    WSB_TRY(make_slabs(g->n_v, R, starts, &sl));
     const int nb = std::max(1, ceil_div(n, kBlockItems));
     uint32_t *cnt, *off;
     WSB_TRY(ensure(ctx, kSlotBlockCounts, sizeof(uint32_t) * R * (size_t)nb, (void **)&cnt));
@@ -288,15 +334,15 @@ int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const double *rec
     return WSB_OK;
 }
 
-int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const double *rec,
-               const uint32_t *plane, int64_t n, double *send_rec, uint32_t *send_plane,
-               int64_t *src_index) {
+int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *starts,
+               const double *rec, const uint32_t *plane, int64_t n, double *send_rec,
+               uint32_t *send_plane, int64_t *src_index) {
     uint32_t *off;
     int nb;
-    WSB_TRY(route_count(ctx, g, S, R, rec, n, nullptr, &off, &nb));
+    WSB_TRY(route_count(ctx, g, S, R, starts, rec, n, nullptr, &off, &nb));
     if (n <= 0) return WSB_OK;
     Slabs sl;
-    WSB_TRY(make_slabs(g->n_v, R, &sl));
+    WSB_TRY(make_slabs(g->n_v, R, starts, &sl));
     k_route_pack<<<nb, kThreads, 0, ctx->stream>>>((const double4 *)rec, plane, n, (double)S, sl,
                                                    R, off, nb, (double4 *)send_rec, send_plane,
                                                    src_index);

@@ -112,11 +112,13 @@ int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t 
 int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v,
             const double *w, const float *vis, const float *weight, int64_t n,
             int32_t n_chan, double *rec, uint32_t *plane);
-int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const double *rec, int64_t n,
-                int64_t *counts_host, uint32_t **offs_out, int *nb_out);
-int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const double *rec,
-               const uint32_t *plane, int64_t n, double *send_rec, uint32_t *send_plane,
-               int64_t *src_index);
+int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *starts,
+                const double *rec, int64_t n, int64_t *counts_host, uint32_t **offs_out,
+                int *nb_out);
+int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *starts,
+               const double *rec, const uint32_t *plane, int64_t n, double *send_rec,
+               uint32_t *send_plane, int64_t *src_index);
+int row_histogram(wsb_ctx *ctx, const wsb_grid *g, const double *rec, int64_t n, uint32_t *hist);
 
 // bucket.cu: records of a slab bucketed by (plane, 32-column strip, anchor row)
 struct RowBuckets {

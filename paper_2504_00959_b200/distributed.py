@@ -47,17 +47,26 @@ class CudaBackend:
     def prepare(self, u, v, w, vis, weight, spec):
         return prepare_device(u, v, w, vis, weight, spec, device=self.device)
 
-    def route(self, rec, plane, spec, S, R):
+    def row_histogram(self, rec, spec):
+        """Records per anchor row floor(gv), int64 [n_v] on the device."""
+        g = spec.c_struct()
+        h = torch.empty(spec.n_v, dtype=torch.int32, device=self.device)
+        L.check(L.lib().wsb_row_histogram(self.ctx.handle, C.byref(g), _ptr(rec), rec.shape[0],
+                                          _ptr(h)))
+        return h.to(torch.int64)
+
+    def route(self, rec, plane, spec, S, R, starts=None):
         g = spec.c_struct()
         n = rec.shape[0]
         counts = (C.c_int64 * R)()
-        L.check(L.lib().wsb_route_count(self.ctx.handle, C.byref(g), S, R, _ptr(rec), n, counts))
+        st = None if starts is None else (C.c_int32 * (R + 1))(*starts)
+        L.check(L.lib().wsb_route_count(self.ctx.handle, C.byref(g), S, R, st, _ptr(rec), n, counts))
         counts = [int(c) for c in counts]
         tot = sum(counts)
         srec = torch.empty((max(tot, 1), 4), dtype=torch.float64, device=self.device)
         spl = torch.empty(max(tot, 1), dtype=torch.int32, device=self.device)
-        L.check(L.lib().wsb_route_pack(self.ctx.handle, C.byref(g), S, R, _ptr(rec), _ptr(plane), n,
-                                       _ptr(srec), _ptr(spl), None))
+        L.check(L.lib().wsb_route_pack(self.ctx.handle, C.byref(g), S, R, st, _ptr(rec), _ptr(plane),
+                                       n, _ptr(srec), _ptr(spl), None))
         return srec[:tot], spl[:tot], counts
 
     def grid_slab(self, rec, plane, spec, kern, v0, vc):
@@ -127,8 +136,34 @@ class _Stages:
         return {b[0]: a[1].elapsed_time(b[1]) for a, b in zip(self.marks, self.marks[1:])}
 
 
+def balanced_slab_starts(row_counts, n_ranks: int, row_weight: float = 10_000.0):
+    """Slab rows with equal estimated work instead of partition_1d's equal
+    rows. A slab's cost is modelled as records + row_weight * rows (the
+    gridder scales with the records, the row pass and the sweep's row
+    emission with the rows; row_weight ~ records-equivalent of one row,
+    measured on cfg3). Returns starts[0..R] with starts[R] = n_v and every
+    slab at least one row. The image does not depend on the slab rows."""
+    import numpy as np
+    h = np.asarray(row_counts, dtype=np.float64)
+    n_v = h.shape[0]
+    cost = np.cumsum(h + row_weight)
+    total = cost[-1]
+    starts = [0]
+    for d in range(1, n_ranks):
+        # boundary whose prefix cost (rows above it) is closest to d/R of the total
+        target = total * d / n_ranks
+        i = int(np.searchsorted(cost, target, side="left"))
+        r = i if i > 0 and target - cost[i - 1] <= cost[min(i, n_v - 1)] - target else i + 1
+        r = max(r, starts[-1] + 1)
+        r = min(r, n_v - (n_ranks - d))
+        starts.append(r)
+    starts.append(n_v)
+    return starts
+
+
 def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None, root: int = 0,
-                      to_host: bool = True, n_ranges: int = 4, timings: dict | None = None):
+                      to_host: bool = True, n_ranges: int = 4, timings: dict | None = None,
+                      balance: bool = True, row_weight: float = 10_000.0):
     """Dirty image of the union of every rank's records. Each rank passes its
     own time partition (records in gindex order, rank r holding the r-th
     contiguous block, as visdata.partition_time_ordered produces).
@@ -140,6 +175,9 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     result does not depend on n_ranges.
     ``timings``, if a dict, receives per-stage milliseconds of the compute
     stream (and the bucket / sweep split of the gridder).
+    ``balance`` sizes the v-slabs for equal work from a global histogram of
+    the anchor rows (one all-reduce of n_v counts) instead of partition_1d's
+    equal rows: Earth-rotation tracks put most records in the central rows.
 
     Returns (FinalImage on ``root``, None elsewhere; diag dict on every rank)."""
     spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
@@ -151,8 +189,6 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     n_groups = spec.n_u // G
     if R > spec.n_v or R > n_groups:
         raise ValueError(f"{R} ranks exceed the mesh ({spec.n_v} rows, {n_groups} column groups)")
-    if spec.n_v % R:
-        raise NotImplementedError("the GPU slab transpose needs n_v to be a multiple of the rank count")
 
     st = _Stages(timings is not None and dev.type == "cuda", dev)
     st.mark("start")
@@ -160,7 +196,14 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     # 1. prepare + time->space exchange ------------------------------------
     rec, plane = be.prepare(u, v, w, vis, weight, spec)
     st.mark("prepare")
-    srec, spl, counts = be.route(rec, plane, spec, S, R)
+    if balance and R > 1:
+        hist = be.row_histogram(rec, spec)
+        dist.all_reduce(hist, group=group)
+        starts = balanced_slab_starts(hist.cpu().numpy(), R, row_weight)
+    else:
+        starts = [partition_1d(spec.n_v, R, d)[0] for d in range(R)] + [spec.n_v]
+    slabs = [(starts[d], starts[d + 1] - starts[d]) for d in range(R)]
+    srec, spl, counts = be.route(rec, plane, spec, S, R, starts)
     st.mark("route")
     c_send = torch.tensor(counts, dtype=torch.int64, device=dev)
     c_recv = torch.empty(R, dtype=torch.int64, device=dev)
@@ -174,7 +217,6 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     st.mark("exchange")
 
     # 2. grid this rank's slab ----------------------------------------------
-    slabs = [partition_1d(spec.n_v, R, d) for d in range(R)]
     v0, vc = slabs[r]
     grid_s, updates = be.grid_slab(rrec, rpl, spec, kern, v0, vc)
     st.mark("grid")
@@ -218,7 +260,8 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     dist.all_gather(parts, ppad, group=group)
     st.mark("gather")
     diag = {"grid_updates": int(upd.item()), "records_local": int(rec.shape[0]),
-            "records_slab": m, "exchange_bytes": int(sum(counts) - counts[r]) * 36}
+            "records_slab": m, "exchange_bytes": int(sum(counts) - counts[r]) * 36,
+            "slab_starts": starts}
     if timings is not None:
         timings.update(st.ms())
         if split is not None:

@@ -23,10 +23,16 @@ class NumpyBackend:
         rec = np.stack([p["gu"], p["gv"], p["value"].real, p["value"].imag], axis=1)
         return torch.from_numpy(rec), torch.from_numpy(p["plane"].astype(np.int32))
 
-    def route(self, rec, plane, spec, S, R):
+    def row_histogram(self, rec, spec):
+        rows = np.clip(np.floor(rec.numpy()[:, 1]).astype(np.int64), 0, spec.n_v - 1)
+        return torch.from_numpy(np.bincount(rows, minlength=spec.n_v).astype(np.int64))
+
+    def route(self, rec, plane, spec, S, R, starts=None):
         r, pl = rec.numpy(), plane.numpy()
         outs, outp, counts = [], [], []
-        for v0, vc in O.slabs(spec.n_v, R):
+        bounds = (O.slabs(spec.n_v, R) if starts is None
+                  else [(starts[d], starts[d + 1] - starts[d]) for d in range(R)])
+        for v0, vc in bounds:
             m = O.halo_mask(r[:, 1], S, v0, vc)
             outs.append(r[m])
             outp.append(pl[m])

@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, outdir):
+def _worker(rank, world, port, case, outdir, row_weight):
     sys.path[:0] = [str(ROOT), str(TESTS)]
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -51,23 +51,45 @@ def _worker(rank, world, port, case, outdir):
         spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
         kern = W.KernelSpec(kind, S, shape)
         img, diag = image_distributed(u[lo:hi], v[lo:hi], w[lo:hi], vis[lo:hi], wt[lo:hi], spec,
-                                      kern, backend=NumpyBackend())
+                                      kern, backend=NumpyBackend(), row_weight=row_weight)
         if rank == 0:
-            np.savez(Path(outdir) / "out.npz", pixels=img.pixels,
+            np.savez(Path(outdir) / "out.npz", pixels=img.pixels, starts=np.array(diag["slab_starts"]),
                      norms=np.array([img.imag_residual_norm, img.real_norm]),
                      updates=np.array([diag["grid_updates"]]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,case", [(2, "wide"), (4, "wide"), (2, "kb1")])
-def test_image_distributed_gloo(tmp_path, golden_image, world, case):
+# row_weight 1.0: slabs sized by the records alone (uneven rows); 1e9: the
+# equal-row partition
+@pytest.mark.parametrize("world,case,row_weight", [(2, "wide", 1e9), (4, "wide", 1e9),
+                                                   (2, "kb1", 1e9), (2, "wide", 1.0),
+                                                   (4, "wide", 1.0)])
+def test_image_distributed_gloo(tmp_path, golden_image, world, case, row_weight):
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, case, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, case, str(tmp_path), row_weight), nprocs=world, join=True)
     out = np.load(tmp_path / "out.npz")
+    starts = out["starts"]
+    assert starts[0] == 0 and starts[-1] == golden_image[f"{case}_cfg"][1] and np.all(np.diff(starts) > 0)
     g = golden_image
     ref = g[f"{case}_pixels"]
     err = float(np.linalg.norm(out["pixels"] - ref) / np.linalg.norm(ref))
     assert err <= 1e-12, err
     assert int(out["updates"][0]) == int(g[f"{case}_grid_updates"][0])
     np.testing.assert_allclose(out["norms"], g[f"{case}_norms"], rtol=1e-10)
+
+
+def test_balanced_slab_starts():
+    from paper_2504_00959_b200.distributed import balanced_slab_starts
+    h = np.zeros(64, np.int64)
+    h[28:36] = 1000                       # records piled in the central rows
+    st = balanced_slab_starts(h, 4, row_weight=0.0)
+    assert st[0] == 0 and st[-1] == 64 and all(b > a for a, b in zip(st, st[1:]))
+    # the central block is cut into four (nearly) equal parts
+    per = [h[a:b].sum() for a, b in zip(st, st[1:])]
+    assert max(per) - min(per) <= 1000
+    # huge row weight -> equal rows
+    assert balanced_slab_starts(h, 4, row_weight=1e12) == [0, 16, 32, 48, 64]
+    # more ranks than loaded rows still gives non-empty slabs
+    st = balanced_slab_starts(np.eye(1, 8, 7, dtype=np.int64)[0] * 10, 8, row_weight=0.0)
+    assert st == list(range(9))

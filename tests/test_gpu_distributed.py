@@ -37,17 +37,20 @@ def _parts(t, R):
     return out
 
 
-def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges=1):
+def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges=1, starts=None):
     from paper_2504_00959_b200.distributed import CudaBackend, plane_ranges
     be = CudaBackend(0)
     G = 1
     S = kern.half_support
-    slabs = [W.partition_1d(spec.n_v, R, d) for d in range(R)]
+    if starts is None:
+        slabs = [W.partition_1d(spec.n_v, R, d) for d in range(R)]
+    else:
+        slabs = [(starts[d], starts[d + 1] - starts[d]) for d in range(R)]
     cols = [W.partition_1d(spec.n_u // G, R, d) for d in range(R)]
     sends = []
     for lo, hi in _parts(t, R):
         rec, pl = be.prepare(u[lo:hi], v[lo:hi], w[lo:hi], vis[lo:hi], wt[lo:hi], spec)
-        sends.append(be.route(rec, pl, spec, S, R))
+        sends.append(be.route(rec, pl, spec, S, R, starts))
     grids, upd = [], 0
     for d, (v0, vc) in enumerate(slabs):
         recs, pls = [], []
@@ -78,8 +81,10 @@ def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges=1):
     return pix, np.sqrt([p[:, 0].cumsum()[-1], p[:, 1].cumsum()[-1]]), upd
 
 
-@pytest.mark.parametrize("R,n_ranges", [(2, 1), (4, 1), (8, 1), (2, 3), (4, 4)])
-def test_virtual_ranks_bit_identical(W, golden_image, R, n_ranges):
+@pytest.mark.parametrize("R,n_ranges,uneven", [(2, 1, False), (4, 1, False), (8, 1, False),
+                                               (2, 3, False), (4, 4, False), (3, 2, True),
+                                               (4, 1, True)])
+def test_virtual_ranks_bit_identical(W, golden_image, R, n_ranges, uneven):
     g = golden_image
     n_u, n_v, n_w, S, _ = (int(x) for x in g["wide_cfg"])
     cell, wmin, wmax, shape = (float(x) for x in g["wide_fcfg"])
@@ -87,7 +92,15 @@ def test_virtual_ranks_bit_identical(W, golden_image, R, n_ranges):
     kern = W.KernelSpec("gaussian", S, shape)
     u, v, w, t, vis, wt = chunk_from(g, "wide_in_")
     ref, diag = W.image(u, v, w, t, vis, wt, spec, kern)
-    pix, norms, upd = _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges)
+    starts = None
+    if uneven:
+        # load-balanced slab rows from the record histogram (distinct heights)
+        from paper_2504_00959_b200.distributed import CudaBackend, balanced_slab_starts
+        be = CudaBackend(0)
+        rec, _ = be.prepare(u, v, w, vis, wt, spec)
+        starts = balanced_slab_starts(be.row_histogram(rec, spec).cpu().numpy(), R, row_weight=1.0)
+        assert len({b - a for a, b in zip(starts, starts[1:])}) > 1, starts
+    pix, norms, upd = _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges, starts)
     assert upd == diag["grid_updates"]
     assert pix.tobytes() == ref.pixels.tobytes()
     assert norms[0] == ref.imag_residual_norm and norms[1] == ref.real_norm

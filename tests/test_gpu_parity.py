@@ -57,12 +57,13 @@ def test_route_bitexact(W, golden_bucket, name, R):
     ctx = context(rec.device)
     counts = (C.c_int64 * R)()
     gs = spec.c_struct()
-    L.check(L.lib().wsb_route_count(ctx.handle, C.byref(gs), S, R, _ptr(rec), rec.shape[0], counts))
+    L.check(L.lib().wsb_route_count(ctx.handle, C.byref(gs), S, R, None, _ptr(rec), rec.shape[0],
+                                    counts))
     tot = sum(counts)
     srec = torch.empty((tot, 4), dtype=torch.float64, device=rec.device)
     spl = torch.empty(tot, dtype=torch.int32, device=rec.device)
     sidx = torch.empty(tot, dtype=torch.int64, device=rec.device)
-    L.check(L.lib().wsb_route_pack(ctx.handle, C.byref(gs), S, R, _ptr(rec), _ptr(plane),
+    L.check(L.lib().wsb_route_pack(ctx.handle, C.byref(gs), S, R, None, _ptr(rec), _ptr(plane),
                                    rec.shape[0], _ptr(srec), _ptr(spl), _ptr(sidx)))
     srec, spl, sidx = srec.cpu().numpy(), spl.cpu().numpy(), sidx.cpu().numpy()
     off = 0
@@ -186,3 +187,40 @@ def test_empty_input_gives_zero_image(W):
                         np.zeros((0, 1), np.float32), spec, W.KernelSpec())
     assert diag["grid_updates"] == 0
     assert not np.any(img.pixels)
+
+
+@pytest.mark.gpu
+def test_route_uneven_slabs_and_row_histogram(W, golden_bucket):
+    """Explicit (load-balanced) slab starts: the packed records of each slab
+    are exactly the oracle's halo selection (comms.py:521-523) in gindex
+    order; the row histogram is the bincount of floor(gv)."""
+    import ctypes as C
+    from oracle import wstack_oracle as O
+    from paper_2504_00959_b200 import _lib as L
+    from paper_2504_00959_b200.distributed import CudaBackend
+    g = golden_bucket
+    n_u, n_v, n_w, S = (int(x) for x in g["syn_spec"])
+    u, v, w, t, vis, wt = chunk_from(g, "syn_in_")
+    spec = W.GridSpec(n_u, n_v, n_w, 1e-3)
+    be = CudaBackend(0)
+    rec, plane = be.prepare(u, v, w, vis, wt, spec)
+    gv = rec[:, 1].cpu().numpy()
+    hist = be.row_histogram(rec, spec).cpu().numpy()
+    assert np.array_equal(hist, np.bincount(np.floor(gv).astype(np.int64), minlength=n_v))
+    R = 3
+    starts = [0, n_v // 5, n_v // 5 + 3, n_v]
+    srec, spl, counts = be.route(rec, plane, spec, S, R, starts)
+    srec = srec.cpu().numpy()
+    off = 0
+    for d in range(R):
+        m = O.halo_mask(gv, S, starts[d], starts[d + 1] - starts[d])
+        assert counts[d] == int(m.sum())
+        assert _bits(srec[off:off + counts[d], 1]).tobytes() == _bits(gv[m]).tobytes()
+        off += counts[d]
+    # invalid starts are rejected
+    gs = spec.c_struct()
+    bad = (C.c_int32 * 4)(0, 10, 10, n_v)
+    cnt = (C.c_int64 * 3)()
+    with pytest.raises(ValueError):
+        L.check(L.lib().wsb_route_count(be.ctx.handle, C.byref(gs), S, 3, bad,
+                                        C.c_void_p(rec.data_ptr()), rec.shape[0], cnt))
