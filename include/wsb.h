@@ -181,6 +181,20 @@ int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count,
                  const double *grid_s, double *grid_p, int32_t plane_lo, int32_t plane_hi,
                  int32_t n_dest, const int32_t *dest_pairs_host);
 
+/* Row pass fused with the slab transpose (fft2d_slab's send loop,
+ * transform.py:152-161, without a separate all-to-all): the results for
+ * destination rank d (dest_cols_host[d] column groups, in order) are stored
+ * straight into d's column-pass input through dest_ptrs_host[d], a device
+ * pointer valid on this GPU (peer memory over NVLink, e.g. a symmetric
+ * allocation; or local memory for d = this rank), pointing at this source
+ * slab's block: element (plane k, column group g, row j) of this slab goes
+ * to dest_ptrs_host[d][(k * dest_cols_host[d] + g - first_d) * v_count + j]
+ * (x G), k absolute in [0, n_w). The caller orders the writes of all ranks
+ * before the column pass reads them (a barrier after this call). */
+int wsb_fft_rows_peer(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count,
+                      const double *grid_s, int32_t plane_lo, int32_t plane_hi, int32_t n_dest,
+                      const int32_t *dest_cols_host, void *const *dest_ptrs_host);
+
 /* Column pass + w correction + stacking (transform.py:162-175, 192-230) of
  * planes [plane_lo, plane_hi): input tgrid holds this rank's column pairs
  * [g0, g0+ng) of those planes for all n_v rows, concatenated by source slab s

@@ -302,6 +302,18 @@ int wsb_fft_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count, const doub
                     dest_pairs_host ? n_dest : 1, dest_pairs_host);
 }
 
+int wsb_fft_rows_peer(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count, const double *grid_s,
+                      int32_t plane_lo, int32_t plane_hi, int32_t n_dest,
+                      const int32_t *dest_cols_host, void *const *dest_ptrs_host) {
+    if (!ctx || !dest_cols_host || !dest_ptrs_host) return fail(WSB_EINVAL, "NULL argument");
+    WSB_TRY(validate_grid(grid));
+    if (plane_lo < 0 || plane_hi > grid->n_w || plane_lo > plane_hi)
+        return fail(WSB_EINVAL, "plane range outside [0, n_w]");
+    WSB_TRY(set_device(ctx));
+    return fft_rows(ctx, grid, v_count, grid_s, nullptr, plane_lo, plane_hi, n_dest,
+                    dest_cols_host, dest_ptrs_host);
+}
+
 int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
                        const int32_t *src_rows_host, int32_t g0, int32_t ng, int32_t plane_lo,
                        int32_t plane_hi, const double *tgrid, double *image_strip,

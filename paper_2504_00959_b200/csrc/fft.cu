@@ -291,10 +291,15 @@ struct RowCfg {
 constexpr int kRowE = 16;
 constexpr int kRowRL = 4;
 
-// column-pair partition of the row pass output over the destination ranks
+// Column-group partition of the row pass output over the destination ranks.
+// Destination d receives column groups [g0[d], g0[d+1]) of every row, laid
+// out from ptr[d] as [plane - plane0][g - g0[d]][row][G]. ptr[d] is either a
+// block of a local send buffer or -- the fused transpose -- this source's
+// block of rank d's column-pass input in peer memory (NVLink stores).
 struct RowDest {
-    int n_w;
-    int g0[9];   // first pair of each destination, g0[n_dest] = n_u/G, unused = INT_MAX
+    double2 *ptr[8];
+    int plane0;
+    int g0[9];   // first group of each destination, g0[n_dest] = n_u/G, unused = INT_MAX
 };
 
 // 4096/N rows per CTA. The first pass reads its inputs straight from HBM
@@ -302,9 +307,8 @@ struct RowDest {
 // its outputs straight back: shared memory only carries the inner exchanges.
 template <int LOGN>
 __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
-    k_fft_rows(const double2 *__restrict__ in, double2 *__restrict__ out, int n_strips,
-               int n_groups, int v_count, int plane_lo, const double2 *__restrict__ tw,
-               RowDest dst) {
+    k_fft_rows(const double2 *__restrict__ in, int n_strips, int n_groups, int v_count,
+               int plane_lo, const double2 *__restrict__ tw, RowDest dst) {
     constexpr int N = 1 << LOGN;
     constexpr int RT = RowCfg<LOGN>::T;
     constexpr int NSEQ = RT * kRowE / N;  // rows per CTA
@@ -319,23 +323,22 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
                    ? in[((plane * n_strips + col / 32) * v_count + j0 + seq) * 32 + (col % 32)]
                    : make_double2(0.0, 0.0);
     };
-    // out: P[plane][col/G][row][col%G] (the column pass and the transpose read it)
-    // column pair g goes to destination d (g in [g0_d, g0_{d+1})), laid out
-    // [d][plane][g - g0_d][row][x] so one all-to-all moves every plane; with a
+    // out: P[plane][col/G][row][col%G] per destination (RowDest); with a
     // single destination this is the plain P layout
     auto gst = [&](int seq, int col, double2 z) {
         if (j0 + seq < v_count) {
             const int g = col / kG;
             int lo = 0, hi = dst.g0[1];
+            double2 *base = dst.ptr[0];
 #pragma unroll
             for (int d = 1; d < 8; ++d)
                 if (g >= dst.g0[d]) {
                     lo = dst.g0[d];
                     hi = dst.g0[d + 1];
+                    base = dst.ptr[d];
                 }
-            const int64_t base = (int64_t)dst.n_w * v_count * kG * lo;
-            out[base + (((plane - plane_lo) * (hi - lo) + (g - lo)) * v_count + j0 + seq) * kG +
-                (col % kG)] = z;
+            base[(((plane - dst.plane0) * (hi - lo) + (g - lo)) * v_count + j0 + seq) * kG +
+                 (col % kG)] = z;
         }
     };
     double2 v[kRowE];
@@ -580,8 +583,8 @@ __global__ void k_twiddles(double2 *tw, int logn, int rlmax, int size) {
 }
 
 template <int LOGN>
-int launch_rows(wsb_ctx *ctx, const double2 *in, double2 *out, int n_strips, int n_groups,
-                int v_count, int plo, int phi, const double2 *tw, const RowDest &dst) {
+int launch_rows(wsb_ctx *ctx, const double2 *in, int n_strips, int n_groups, int v_count, int plo,
+                int phi, const double2 *tw, const RowDest &dst) {
     constexpr int N = 1 << LOGN;
     constexpr int RT = RowCfg<LOGN>::T;
     constexpr int NSEQ = RT * kRowE / N;
@@ -589,8 +592,7 @@ int launch_rows(wsb_ctx *ctx, const double2 *in, double2 *out, int n_strips, int
     WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     dim3 grd(ceil_div(v_count, NSEQ), phi - plo);
-    k_fft_rows<LOGN><<<grd, RT, smem, ctx->stream>>>(in, out, n_strips, n_groups, v_count, plo, tw,
-                                                     dst);
+    k_fft_rows<LOGN><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo, tw, dst);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
@@ -630,24 +632,36 @@ int twiddles(wsb_ctx *ctx, int n, int rlmax, const double **out) {
 }
 
 int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a, double *grid_p,
-             int plo, int phi, int n_dest, const int32_t *dest_groups) {
+             int plo, int phi, int n_dest, const int32_t *dest_groups, void *const *dest_ptrs) {
     if (phi <= plo || v_count <= 0) return WSB_OK;
     const double *tw;
     WSB_TRY(twiddles(ctx, g->n_u, kRowRL, &tw));
     const int ng = g->n_u / kG, ns = ceil_div(g->n_u, 32);
     RowDest dst;
-    dst.n_w = phi - plo;  // the output holds planes [plo, phi) only
     if (n_dest < 1 || n_dest > 8) return fail(WSB_EINVAL, "n_dest must be in [1, 8]");
     dst.g0[0] = 0;
     for (int d = 0; d < n_dest; ++d) dst.g0[d + 1] = dst.g0[d] + (dest_groups ? dest_groups[d] : ng);
-    if (dst.g0[n_dest] != ng) return fail(WSB_EINVAL, "destination column pairs must sum to n_u/2");
+    if (dst.g0[n_dest] != ng) return fail(WSB_EINVAL, "destination column groups must sum to n_u/G");
     for (int d = n_dest + 1; d < 9; ++d) dst.g0[d] = 0x7fffffff;
+    for (int d = 0; d < 8; ++d) dst.ptr[d] = nullptr;
+    if (dest_ptrs) {
+        // fused transpose: every destination's block holds all n_w planes
+        dst.plane0 = 0;
+        for (int d = 0; d < n_dest; ++d) {
+            if (!dest_ptrs[d]) return fail(WSB_EINVAL, "NULL destination pointer");
+            dst.ptr[d] = (double2 *)dest_ptrs[d];
+        }
+    } else {
+        // local destination-major buffer holding planes [plo, phi) only
+        dst.plane0 = plo;
+        for (int d = 0; d < n_dest; ++d)
+            dst.ptr[d] = (double2 *)grid_p + (int64_t)(phi - plo) * v_count * kG * dst.g0[d];
+    }
     const double2 *ga = (const double2 *)grid_a;
-    double2 *gp = (double2 *)grid_p;
     const double2 *t2 = (const double2 *)tw;
     switch (ilog2(g->n_u)) {
 #define WSB_ROWS(L) \
-    case L: return launch_rows<L>(ctx, ga, gp, ns, ng, v_count, plo, phi, t2, dst);
+    case L: return launch_rows<L>(ctx, ga, ns, ng, v_count, plo, phi, t2, dst);
         WSB_ROWS(1) WSB_ROWS(2) WSB_ROWS(3) WSB_ROWS(4) WSB_ROWS(5) WSB_ROWS(6)
         WSB_ROWS(7) WSB_ROWS(8) WSB_ROWS(9) WSB_ROWS(10) WSB_ROWS(11) WSB_ROWS(12)
 #undef WSB_ROWS

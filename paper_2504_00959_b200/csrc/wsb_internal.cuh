@@ -137,7 +137,8 @@ int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
 
 // fft.cu
 int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a, double *grid_p,
-             int plane_lo, int plane_hi, int n_dest, const int32_t *dest_groups);
+             int plane_lo, int plane_hi, int n_dest, const int32_t *dest_groups,
+             void *const *dest_ptrs = nullptr);
 int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t *src_rows,
                    int g0, int ng, int plane_lo, int plane_hi, const double *tgrid,
                    double *image_strip,

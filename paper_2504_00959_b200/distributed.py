@@ -86,6 +86,16 @@ class CudaBackend:
                                      pairs))
         return grid_p
 
+    def fft_rows_peer(self, grid_s, spec, vc, dest_cols, dest_ptrs):
+        """Row pass of all planes stored into the destinations' column-pass
+        inputs through device pointers (peer memory)."""
+        g = spec.c_struct()
+        R = len(dest_cols)
+        cols = (C.c_int32 * R)(*dest_cols)
+        ptrs = (C.c_void_p * R)(*dest_ptrs)
+        L.check(L.lib().wsb_fft_rows_peer(self.ctx.handle, C.byref(g), int(vc), _ptr(grid_s), 0,
+                                          spec.n_w, R, cols, ptrs))
+
     def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng, plane_lo=0, plane_hi=None):
         """Column pass + stack of planes [plane_lo, plane_hi) (ranges in
         descending order; the context carries the running stack). Returns
@@ -161,18 +171,48 @@ def balanced_slab_starts(row_counts, n_ranks: int, row_weight: float = 10_000.0)
     return starts
 
 
+_SYMM: dict = {}
+
+
+def _symm_available() -> bool:
+    try:
+        import torch.distributed._symmetric_memory  # noqa: F401
+        return True
+    except Exception:
+        return False
+
+
+def _symm_buffer(elems: int, dev, group):
+    """Symmetric (peer-mapped) float64 buffer of 2*elems values on every rank,
+    cached: the rendezvous is collective and costly. Keeps the largest."""
+    import torch.distributed._symmetric_memory as symm
+    key = (id(group), dev.index)
+    hit = _SYMM.get(key)
+    if hit is None or hit[0].numel() < 2 * elems:
+        _SYMM.pop(key, None)
+        buf = symm.empty(2 * elems, dtype=torch.float64, device=dev)
+        hdl = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
+        _SYMM[key] = (buf, hdl)
+    return _SYMM[key]
+
+
 def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None, root: int = 0,
                       to_host: bool = True, n_ranges: int = 4, timings: dict | None = None,
-                      balance: bool = True, row_weight: float = 10_000.0):
+                      balance: bool = True, row_weight: float = 10_000.0,
+                      transpose: str = "auto"):
     """Dirty image of the union of every rank's records. Each rank passes its
     own time partition (records in gindex order, rank r holding the r-th
     contiguous block, as visdata.partition_time_ordered produces).
 
-    The slab transpose is pipelined over ``n_ranges`` plane ranges (from the
-    top plane down, the stacking order of the column pass): the all-to-all
-    of one range runs on NCCL's stream while the row pass of the next range
-    and the column pass of the previous one run on the compute stream. The
-    result does not depend on n_ranges.
+    ``transpose``: "peer" fuses the slab transpose into the row pass -- its
+    results are stored straight into the destination ranks' column-pass
+    inputs in symmetric memory over NVLink (wsb_fft_rows_peer); "nccl"
+    pipelines an NCCL all-to-all over ``n_ranges`` plane ranges (from the top
+    plane down, the stacking order of the column pass): the all-to-all of one
+    range runs on NCCL's stream while the row pass of the next range and the
+    column pass of the previous one run on the compute stream; "auto" picks
+    "peer" when the backend and torch's symmetric memory support it. The
+    result does not depend on the choice.
     ``timings``, if a dict, receives per-stage milliseconds of the compute
     stream (and the bucket / sweep split of the gridder).
     ``balance`` sizes the v-slabs for equal work from a global histogram of
@@ -229,22 +269,43 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     g0, ng = cols[r]
     dest_pairs = [ng_d for _, ng_d in cols]
     src_rows = [vc_s for _, vc_s in slabs]
-    inflight = []
-    for k0, k1 in reversed(plane_ranges(spec.n_w, n_ranges)):   # top planes first
-        nk = k1 - k0
-        grid_p = be.fft_rows(grid_s, spec, vc, dest_pairs, k0, k1)   # [dest][plane][pair][row][G]
-        in_splits = [nk * ng_d * vc * G * 2 for ng_d in dest_pairs]   # float64 elements per rank
-        out_splits = [nk * ng * vc_s * G * 2 for vc_s in src_rows]    # from each source slab
-        tgrid = torch.empty(sum(out_splits), dtype=torch.float64, device=dev)
-        work = _a2a(tgrid, grid_p, out_splits, in_splits, group, async_op=True)
-        inflight.append((k0, k1, work, tgrid, grid_p))
-    st.mark("rows")
-    del grid_s
-    for k0, k1, work, tgrid, grid_p in inflight:
-        work.wait()
-        strip, partials = be.fft_cols_stack(tgrid, spec, src_rows, g0, ng, k0, k1)
-    inflight.clear()
-    st.mark("cols")
+    if transpose == "auto":
+        transpose = "peer" if (hasattr(be, "fft_rows_peer") and dev.type == "cuda"
+                               and _symm_available()) else "nccl"
+    if transpose == "peer":
+        # fused transpose: the row pass stores each destination's columns
+        # straight into that rank's column-pass input (symmetric memory,
+        # NVLink stores); one device-side barrier orders them before the
+        # column pass. Layout of every rank's input: [s][plane][g][row - r0_s].
+        elems = spec.n_w * max(dest_pairs) * G * spec.n_v            # complex128 per rank
+        buf, hdl = _symm_buffer(elems, dev, group)
+        ptrs = [hdl.buffer_ptrs[d] + 16 * spec.n_w * dest_pairs[d] * G * slabs[r][0]
+                for d in range(R)]
+        hdl.barrier(channel=0)          # every rank has finished reading the previous image
+        be.fft_rows_peer(grid_s, spec, vc, dest_pairs, ptrs)
+        st.mark("rows")
+        del grid_s
+        hdl.barrier(channel=0)          # all slabs' columns have landed
+        tgrid = buf[: 2 * spec.n_w * ng * G * spec.n_v]
+        strip, partials = be.fft_cols_stack(tgrid, spec, src_rows, g0, ng, 0, spec.n_w)
+        st.mark("cols")
+    else:
+        inflight = []
+        for k0, k1 in reversed(plane_ranges(spec.n_w, n_ranges)):   # top planes first
+            nk = k1 - k0
+            grid_p = be.fft_rows(grid_s, spec, vc, dest_pairs, k0, k1)  # [dest][plane][g][row][G]
+            in_splits = [nk * ng_d * vc * G * 2 for ng_d in dest_pairs]  # float64 elements per rank
+            out_splits = [nk * ng * vc_s * G * 2 for vc_s in src_rows]   # from each source slab
+            tgrid = torch.empty(sum(out_splits), dtype=torch.float64, device=dev)
+            work = _a2a(tgrid, grid_p, out_splits, in_splits, group, async_op=True)
+            inflight.append((k0, k1, work, tgrid, grid_p))
+        st.mark("rows")
+        del grid_s
+        for k0, k1, work, tgrid, grid_p in inflight:
+            work.wait()
+            strip, partials = be.fft_cols_stack(tgrid, spec, src_rows, g0, ng, k0, k1)
+        inflight.clear()
+        st.mark("cols")
 
     # 4. gather to the root ----------------------------------------------------
     upd = torch.tensor([updates], dtype=torch.int64, device=dev)

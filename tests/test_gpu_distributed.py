@@ -130,10 +130,19 @@ def _nccl_worker(rank, world, port, outdir):
         u, v, w, t, vis, wt = (g[f"wide_in_{k}"] for k in ("u", "v", "w", "time_index", "vis", "weight"))
         lo, hi = _parts(t, world)[rank]
         dev = torch.device("cuda", rank)
-        img, diag = image_distributed(*(torch.from_numpy(np.ascontiguousarray(a[lo:hi])).to(dev)
-                                        for a in (u, v, w, vis, wt)), spec, kern)
+        args = [torch.from_numpy(np.ascontiguousarray(a[lo:hi])).to(dev) for a in (u, v, w, vis, wt)]
+        outs = {}
+        # fused peer-memory transpose (twice: the symmetric buffer is reused),
+        # the pipelined NCCL all-to-all, and partition_1d slabs
+        for name, kw in (("peer", dict(transpose="peer")), ("peer2", dict(transpose="peer")),
+                         ("nccl", dict(transpose="nccl")),
+                         ("even", dict(transpose="nccl", balance=False))):
+            img, diag = image_distributed(*args, spec, kern, **kw)
+            if rank == 0:
+                outs[name] = img.pixels
+                outs[name + "_updates"] = np.array([diag["grid_updates"]])
         if rank == 0:
-            np.savez(Path(outdir) / "out.npz", pixels=img.pixels, updates=np.array([diag["grid_updates"]]))
+            np.savez(Path(outdir) / "out.npz", **outs)
     finally:
         dist.destroy_process_group()
 
@@ -150,5 +159,6 @@ def test_nccl_multi_gpu_matches_single(W, golden_image, tmp_path):
     cell, wmin, wmax, shape = (float(x) for x in g["wide_fcfg"])
     spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
     ref, diag = W.image(*chunk_from(g, "wide_in_"), spec, W.KernelSpec("gaussian", S, shape))
-    assert int(out["updates"][0]) == diag["grid_updates"]
-    assert out["pixels"].tobytes() == ref.pixels.tobytes()
+    for name in ("peer", "peer2", "nccl", "even"):
+        assert int(out[name + "_updates"][0]) == diag["grid_updates"], name
+        assert out[name].tobytes() == ref.pixels.tobytes(), name
