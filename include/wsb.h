@@ -195,6 +195,15 @@ int wsb_fft_rows_peer(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count,
                       const double *grid_s, int32_t plane_lo, int32_t plane_hi, int32_t n_dest,
                       const int32_t *dest_cols_host, void *const *dest_ptrs_host);
 
+/* Slab-transpose push: copies n_dest contiguous device blocks
+ * src_ptrs[d] -> dst_ptrs[d] (bytes_host[d] each, multiples of 16, 16-byte
+ * aligned) in ONE launch on the context stream; dst may be peer memory
+ * (NVLink stores). Used to move each plane range of the wsb_fft_rows
+ * destination-major output into the other ranks' column-pass inputs while
+ * the next range is transformed. Enqueued, no synchronisation. */
+int wsb_push_blocks(wsb_ctx *ctx, int32_t n_dest, const void *const *src_ptrs,
+                    void *const *dst_ptrs, const int64_t *bytes_host);
+
 /* Column pass + w correction + stacking (transform.py:162-175, 192-230) of
  * planes [plane_lo, plane_hi): input tgrid holds this rank's column pairs
  * [g0, g0+ng) of those planes for all n_v rows, concatenated by source slab s

@@ -20,7 +20,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build"
 LIB = PKG / "libwsb.so"
-SOURCES = ["api.cu", "prepare.cu", "bucket.cu", "sort.cu", "grid.cu", "fft.cu"]
+SOURCES = ["api.cu", "prepare.cu", "bucket.cu", "sort.cu", "grid.cu", "fft.cu", "peer.cu"]
 HEADERS = ["wsb_internal.cuh", "i0_coeffs.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -135,6 +135,11 @@ int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
                const double *rec, const RowBuckets &bk, double *grid_p,
                unsigned long long *updates_dev);
 
+// peer.cu: copy n_dest contiguous blocks src[d] -> dst[d] (bytes[d] each; dst
+// may be peer memory) with one launch on the context stream
+int push_blocks(wsb_ctx *ctx, int n_dest, const void *const *src, void *const *dst,
+                const int64_t *bytes);
+
 // fft.cu
 int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a, double *grid_p,
              int plane_lo, int plane_hi, int n_dest, const int32_t *dest_groups,

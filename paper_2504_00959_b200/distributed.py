@@ -96,6 +96,19 @@ class CudaBackend:
         L.check(L.lib().wsb_fft_rows_peer(self.ctx.handle, C.byref(g), int(vc), _ptr(grid_s), 0,
                                           spec.n_w, R, cols, ptrs))
 
+    def push_blocks(self, srcs, dsts, nbytes, stream):
+        """One launch copying block d: srcs[d] -> dsts[d] (device addresses,
+        dsts may be peer memory), enqueued on ``stream``."""
+        R = len(srcs)
+        lib, h = L.lib(), self.ctx.handle
+        L.check(lib.wsb_ctx_set_stream(h, C.c_void_p(stream.cuda_stream)))
+        try:
+            L.check(lib.wsb_push_blocks(h, R, (C.c_void_p * R)(*srcs), (C.c_void_p * R)(*dsts),
+                                        (C.c_int64 * R)(*nbytes)))
+        finally:
+            L.check(lib.wsb_ctx_set_stream(h, C.c_void_p(torch.cuda.current_stream(self.device)
+                                                         .cuda_stream)))
+
     def fft_cols_stack(self, tgrid, spec, src_rows, g0, ng, plane_lo=0, plane_hi=None):
         """Column pass + stack of planes [plane_lo, plane_hi) (ranges in
         descending order; the context carries the running stack). Returns
@@ -182,6 +195,15 @@ def _symm_available() -> bool:
         return False
 
 
+_SIDE: dict = {}
+
+
+def _side_stream(dev):
+    if dev.index not in _SIDE:
+        _SIDE[dev.index] = torch.cuda.Stream(dev)
+    return _SIDE[dev.index]
+
+
 def _symm_buffer(elems: int, dev, group):
     """Symmetric (peer-mapped) float64 buffer of 2*elems values on every rank,
     cached: the rendezvous is collective and costly. Keeps the largest."""
@@ -204,14 +226,17 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     own time partition (records in gindex order, rank r holding the r-th
     contiguous block, as visdata.partition_time_ordered produces).
 
-    ``transpose``: "peer" fuses the slab transpose into the row pass -- its
+    ``transpose``: "push" (default on GPUs) overlaps NVLink pushes of each
+    plane range (a copy kernel into the destinations' inputs in symmetric
+    memory) with the row pass of the next range; "peer" fuses the slab
+    transpose into the row pass -- its
     results are stored straight into the destination ranks' column-pass
     inputs in symmetric memory over NVLink (wsb_fft_rows_peer); "nccl"
     pipelines an NCCL all-to-all over ``n_ranges`` plane ranges (from the top
     plane down, the stacking order of the column pass): the all-to-all of one
     range runs on NCCL's stream while the row pass of the next range and the
     column pass of the previous one run on the compute stream; "auto" picks
-    "peer" when the backend and torch's symmetric memory support it. The
+    "push" when the backend and torch's symmetric memory support it. The
     result does not depend on the choice.
     ``timings``, if a dict, receives per-stage milliseconds of the compute
     stream (and the bucket / sweep split of the gridder).
@@ -270,9 +295,48 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     dest_pairs = [ng_d for _, ng_d in cols]
     src_rows = [vc_s for _, vc_s in slabs]
     if transpose == "auto":
-        transpose = "peer" if (hasattr(be, "fft_rows_peer") and dev.type == "cuda"
+        transpose = "push" if (hasattr(be, "push_blocks") and dev.type == "cuda"
                                and _symm_available()) else "nccl"
-    if transpose == "peer":
+    if transpose == "push":
+        # row pass into local destination-major plane ranges; each range is
+        # pushed by a copy kernel on a side stream straight into the other
+        # ranks' column-pass inputs (symmetric memory, NVLink stores) while
+        # the next range is transformed; one device-side barrier, then the
+        # column pass over all planes. Every rank's input:
+        # [s][plane][g][row - r0_s].
+        elems = spec.n_w * max(dest_pairs) * G * spec.n_v
+        buf, hdl = _symm_buffer(elems, dev, group)
+        cur = torch.cuda.current_stream(dev)
+        ps = _side_stream(dev)
+        hdl.barrier(channel=0)          # every rank has finished reading the previous image
+        ps.wait_stream(cur)
+        keep = []
+        for k0, k1 in reversed(plane_ranges(spec.n_w, n_ranges)):
+            nk = k1 - k0
+            grid_p = be.fft_rows(grid_s, spec, vc, dest_pairs, k0, k1)  # [dest][plane][g][row][G]
+            srcs, dsts, nbytes = [], [], []
+            lo = 0
+            for d in range(R):
+                n_el = nk * dest_pairs[d] * G * vc              # complex128 elements
+                srcs.append(grid_p.data_ptr() + 16 * nk * vc * G * lo)
+                blk = spec.n_w * dest_pairs[d] * G * slabs[r][0] + k0 * dest_pairs[d] * G * vc
+                dsts.append(hdl.buffer_ptrs[d] + 16 * blk)
+                nbytes.append(16 * n_el)
+                lo += dest_pairs[d]
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            ps.wait_event(ev)
+            be.push_blocks(srcs, dsts, nbytes, ps)
+            keep.append(grid_p)
+        st.mark("rows")
+        del grid_s
+        cur.wait_stream(ps)
+        hdl.barrier(channel=0)          # all slabs' columns have landed
+        keep.clear()
+        tgrid = buf[: 2 * spec.n_w * ng * G * spec.n_v]
+        strip, partials = be.fft_cols_stack(tgrid, spec, src_rows, g0, ng, 0, spec.n_w)
+        st.mark("cols")
+    elif transpose == "peer":
         # fused transpose: the row pass stores each destination's columns
         # straight into that rank's column-pass input (symmetric memory,
         # NVLink stores); one device-side barrier orders them before the

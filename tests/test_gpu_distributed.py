@@ -134,7 +134,8 @@ def _nccl_worker(rank, world, port, outdir):
         outs = {}
         # fused peer-memory transpose (twice: the symmetric buffer is reused),
         # the pipelined NCCL all-to-all, and partition_1d slabs
-        for name, kw in (("peer", dict(transpose="peer")), ("peer2", dict(transpose="peer")),
+        for name, kw in (("push", dict(transpose="push")), ("push2", dict(transpose="push")),
+                         ("peer", dict(transpose="peer")),
                          ("nccl", dict(transpose="nccl")),
                          ("even", dict(transpose="nccl", balance=False))):
             img, diag = image_distributed(*args, spec, kern, **kw)
@@ -159,6 +160,6 @@ def test_nccl_multi_gpu_matches_single(W, golden_image, tmp_path):
     cell, wmin, wmax, shape = (float(x) for x in g["wide_fcfg"])
     spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
     ref, diag = W.image(*chunk_from(g, "wide_in_"), spec, W.KernelSpec("gaussian", S, shape))
-    for name in ("peer", "peer2", "nccl", "even"):
+    for name in ("push", "push2", "peer", "nccl", "even"):
         assert int(out[name + "_updates"][0]) == diag["grid_updates"], name
         assert out[name].tobytes() == ref.pixels.tobytes(), name
