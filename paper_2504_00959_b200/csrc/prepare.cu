@@ -147,10 +147,11 @@ struct Slabs {
 
 __device__ __forceinline__ uint32_t dest_mask(double gv, double S, const Slabs &sl, int R) {
     uint32_t m = 0;
-    for (int d = 0; d < R; ++d) {
-        // comms.py:521-523, rounded FP64 adds
-        bool in = (__dadd_rn(gv, S) >= (double)sl.start[d]) &&
-                  (__dsub_rn(gv, S) <= (double)(sl.start[d] + sl.count[d] - 1));
+    const double hi = __dadd_rn(gv, S), lo = __dsub_rn(gv, S);  // comms.py:521-523
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+        const bool in = d < R && hi >= (double)sl.start[d] &&
+                        lo <= (double)(sl.start[d] + sl.count[d] - 1);
         m |= (uint32_t)in << d;
     }
     return m;
@@ -168,10 +169,12 @@ __global__ void __launch_bounds__(kThreads) k_route_count(const double4 *__restr
         int64_t i = base + it * kThreads + threadIdx.x;
         if (i < n) {
             uint32_t m = dest_mask(rec[i].y, S, sl, R);
-            for (int d = 0; d < R; ++d) local[d] += (m >> d) & 1u;
+#pragma unroll
+            for (int d = 0; d < 8; ++d) local[d] += (m >> d) & 1u;
         }
     }
-    for (int d = 0; d < R; ++d) {
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
         uint32_t x = local[d];
 #pragma unroll
         for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -185,13 +188,21 @@ __global__ void __launch_bounds__(kThreads) k_route_pack(
     const double4 *__restrict__ rec, const uint32_t *__restrict__ plane, int64_t n, double S,
     Slabs sl, int R, const uint32_t *__restrict__ offs /*[R][nb] exclusive*/, int nb,
     double4 *__restrict__ send_rec, uint32_t *__restrict__ send_plane, int64_t *src_index) {
-    __shared__ uint32_t wsum[8];
-    __shared__ uint32_t run[8];
-    if (threadIdx.x < 8) run[threadIdx.x] = threadIdx.x < R ? offs[(int64_t)threadIdx.x * nb + blockIdx.x] : 0;
-    __syncthreads();
+    // Per 256 records: one ballot per destination ranks each lane inside its
+    // warp; the warps' counts go through shared memory once (double-buffered)
+    // and every thread advances its own copy of the running offsets, so a
+    // round costs one barrier instead of 2R.
+    constexpr int kW = kThreads / 32;
+    __shared__ uint32_t wc[2][8][kW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t run[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) run[d] = d < R ? offs[(int64_t)d * nb + blockIdx.x] : 0u;
     const int64_t base = (int64_t)blockIdx.x * kBlockItems;
     for (int it = 0; it < kBlockItems / kThreads; ++it) {
-        int64_t i = base + it * kThreads + threadIdx.x;
+        const int buf = it & 1;
+        const int64_t i = base + it * kThreads + threadIdx.x;
         double4 r = make_double4(0, 0, 0, 0);
         uint32_t p = 0, m = 0;
         if (i < n) {
@@ -199,19 +210,34 @@ __global__ void __launch_bounds__(kThreads) k_route_pack(
             p = plane[i];
             m = dest_mask(r.y, S, sl, R);
         }
-        for (int d = 0; d < R; ++d) {
-            uint32_t tot;
-            uint32_t f = (m >> d) & 1u;
-            uint32_t ex = block_excl_sum256(f, &tot, wsum);
-            if (f) {
-                uint32_t pos = run[d] + ex;
-                send_rec[pos] = r;
-                send_plane[pos] = p;
-                if (src_index) src_index[pos] = i;
+        uint32_t in_warp[8];
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+            if (d < R) {
+                const uint32_t b = __ballot_sync(0xffffffffu, (m >> d) & 1u);
+                in_warp[d] = __popc(b & lt);
+                if (lane == 0) wc[buf][d][warp] = __popc(b);
             }
-            __syncthreads();
-            if (threadIdx.x == 0) run[d] += tot;
-            __syncthreads();
+        }
+        __syncthreads();
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+            if (d < R) {
+                uint32_t before = 0, tot = 0;
+#pragma unroll
+                for (int k = 0; k < kW; ++k) {
+                    const uint32_t c = wc[buf][d][k];
+                    before += k < warp ? c : 0u;
+                    tot += c;
+                }
+                if ((m >> d) & 1u) {
+                    const uint32_t pos = run[d] + before + in_warp[d];
+                    send_rec[pos] = r;
+                    send_plane[pos] = p;
+                    if (src_index) src_index[pos] = i;
+                }
+                run[d] += tot;
+            }
         }
     }
 }
