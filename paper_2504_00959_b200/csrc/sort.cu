@@ -1,4 +1,4 @@
-// Exclusive scan and stable LSD radix sort (8-bit digits) for the K1
+// Exclusive scan and stable LSD radix sort (8..11-bit digits) for the K1
 // bucketing stage. Stability is what makes the per-cell accumulation order
 // of the gridder the global record order (gindex), independent of the GPU
 // count -- the property gridder.py:262-269 guarantees for the reference.
@@ -91,7 +91,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t *__r
 }
 
 // ---------------------------------------------------------------------------
-// radix sort
+// radix sort: B-bit digits (B = 8..11, chosen so the key needs as few passes
+// as possible: cfg3's 26-bit keys take 3 passes of 9 bits instead of 4 of 8;
+// wider digits scatter too thinly -- 2 passes of 12 bits were measured 1.6x
+// slower than 3 of 8 at cfg2)
 // ---------------------------------------------------------------------------
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
@@ -99,40 +102,56 @@ constexpr int kRsIpt = 16;                      // rounds of 32 per warp
 constexpr int kRsItems = kRsThreads * kRsIpt;   // 4096 per block
 constexpr int kRsPerWarp = 32 * kRsIpt;         // 512
 
+template <int B>
+struct RsSmem {
+    static constexpr int D = 1 << B;
+    uint16_t wc[kRsWarps][D];     // per-warp digit counts, then per-warp starts (<= 4096)
+    uint32_t bstart[D], goff[D];  // block-local digit starts, global digit offsets
+    uint32_t ks[kRsItems], vs[kRsItems];
+    uint32_t wsum[kRsWarps];
+};
+
+template <int B>
 __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const uint32_t *__restrict__ keys,
                                                            int64_t n, int shift,
                                                            uint32_t *hist, int nb) {
     // one sub-histogram per warp (shared-memory atomics, little contention),
     // all loads of a thread issued up front
-    __shared__ uint32_t h[kRsWarps][256];
+    constexpr int D = 1 << B;
+    extern __shared__ __align__(16) unsigned char raw[];
+    uint32_t(*h)[D] = reinterpret_cast<uint32_t(*)[D]>(raw);
     const int warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int w = 0; w < kRsWarps; ++w) h[w][threadIdx.x] = 0;
+    for (int e = threadIdx.x; e < kRsWarps * D; e += kRsThreads) (&h[0][0])[e] = 0;
     __syncthreads();
     const int64_t base = (int64_t)blockIdx.x * kRsItems;
     uint32_t d[kRsIpt];
 #pragma unroll
     for (int r = 0; r < kRsIpt; ++r) {
         const int64_t i = base + (int64_t)r * kRsThreads + threadIdx.x;
-        d[r] = i < n ? (__ldg(&keys[i]) >> shift) & 255u : 256u;
+        d[r] = i < n ? (__ldg(&keys[i]) >> shift) & (D - 1) : (uint32_t)D;
     }
 #pragma unroll
     for (int r = 0; r < kRsIpt; ++r)
-        if (d[r] < 256u) atomicAdd(&h[warp][d[r]], 1u);
+        if (d[r] < (uint32_t)D) atomicAdd(&h[warp][d[r]], 1u);
     __syncthreads();
-    uint32_t s = 0;
+    for (int dg = threadIdx.x; dg < D; dg += kRsThreads) {
+        uint32_t s = 0;
 #pragma unroll
-    for (int w = 0; w < kRsWarps; ++w) s += h[w][threadIdx.x];
-    hist[(int64_t)threadIdx.x * nb + blockIdx.x] = s;
+        for (int w = 0; w < kRsWarps; ++w) s += h[w][dg];
+        hist[(int64_t)dg * nb + blockIdx.x] = s;
+    }
 }
 
+template <int B>
 __global__ void __launch_bounds__(kRsThreads) k_radix_scatter(
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
     uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ offs, int nb) {
-    __shared__ uint32_t wc[kRsWarps][256];
+    constexpr int D = 1 << B;
+    constexpr int DPT = D / kRsThreads;  // digits per thread in the block scan (1..8)
+    extern __shared__ __align__(16) unsigned char raw[];
+    RsSmem<B> &sm = *reinterpret_cast<RsSmem<B> *>(raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) wc[warp][lane + 32 * i] = 0;
+    for (int i = lane; i < D; i += 32) sm.wc[warp][i] = 0;
     __syncwarp();
     const int64_t base = (int64_t)blockIdx.x * kRsItems + warp * kRsPerWarp;
     uint32_t k[kRsIpt], v[kRsIpt], pm[kRsIpt];
@@ -146,67 +165,95 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_scatter(
 #pragma unroll
     for (int r = 0; r < kRsIpt; ++r) {
         const bool ok = base + r * 32 + lane < n;
-        const uint32_t d = ok ? (k[r] >> shift) & 255u : 256u;
+        const uint32_t d = ok ? (k[r] >> shift) & (D - 1) : (uint32_t)D;
         pm[r] = __match_any_sync(0xffffffffu, d);
-        if (d < 256u && lane == __ffs(pm[r]) - 1) wc[warp][d] += __popc(pm[r]);
+        if (d < (uint32_t)D && lane == __ffs(pm[r]) - 1) sm.wc[warp][d] += __popc(pm[r]);
         __syncwarp();
     }
     __syncthreads();
-    // block-local start of each digit run (exclusive scan over the 256
-    // digits of the block totals) and the start of each warp inside it
-    __shared__ uint32_t bstart[256], goff[256], wsum[kRsWarps];
+    // block-local start of each digit run (exclusive scan over the D digits
+    // of the block totals; thread t owns digits [t*DPT, (t+1)*DPT)) and the
+    // start of each warp inside it
     {
-        const int d = threadIdx.x;  // 256 threads == 256 digits
-        uint32_t tot = 0;
+        uint32_t tot[DPT], sum = 0;
 #pragma unroll
-        for (int w = 0; w < kRsWarps; ++w) {
-            const uint32_t c = wc[w][d];
-            wc[w][d] = tot;
-            tot += c;
+        for (int q = 0; q < DPT; ++q) {
+            const int d = threadIdx.x * DPT + q;
+            uint32_t t = 0;
+#pragma unroll
+            for (int w = 0; w < kRsWarps; ++w) {
+                const uint32_t c = sm.wc[w][d];
+                sm.wc[w][d] = (uint16_t)t;
+                t += c;
+            }
+            tot[q] = t;
+            sum += t;
         }
-        uint32_t incl = tot;
+        uint32_t incl = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        if (lane == 31) wsum[warp] = incl;
+        if (lane == 31) sm.wsum[warp] = incl;
         __syncthreads();
-        uint32_t wbase = 0;
-        for (int w = 0; w < warp; ++w) wbase += wsum[w];
-        bstart[d] = wbase + incl - tot;
-        goff[d] = offs[(int64_t)d * nb + blockIdx.x];
+        uint32_t run = incl - sum;
+        for (int w = 0; w < warp; ++w) run += sm.wsum[w];
+#pragma unroll
+        for (int q = 0; q < DPT; ++q) {
+            const int d = threadIdx.x * DPT + q;
+            sm.bstart[d] = run;
+            sm.goff[d] = offs[(int64_t)d * nb + blockIdx.x];
+            run += tot[q];
+        }
     }
     __syncthreads();
     // stable rank inside the block -> shared-memory staging in digit order
-    __shared__ uint32_t ks[kRsItems], vs[kRsItems];
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int r = 0; r < kRsIpt; ++r) {
         int64_t i = base + r * 32 + lane;
         bool ok = i < n;
-        uint32_t d = ok ? (k[r] >> shift) & 255u : 256u;
+        uint32_t d = ok ? (k[r] >> shift) & (D - 1) : (uint32_t)D;
         const uint32_t peers = pm[r];
         uint32_t pos = 0;
-        if (ok) pos = bstart[d] + wc[warp][d] + __popc(peers & lt);
+        if (ok) pos = sm.bstart[d] + sm.wc[warp][d] + __popc(peers & lt);
         __syncwarp();
-        if (ok && lane == __ffs(peers) - 1) wc[warp][d] += __popc(peers);
+        if (ok && lane == __ffs(peers) - 1) sm.wc[warp][d] += __popc(peers);
         __syncwarp();
         if (ok) {
-            ks[pos] = k[r];
-            vs[pos] = v[r];
+            sm.ks[pos] = k[r];
+            sm.vs[pos] = v[r];
         }
     }
     __syncthreads();
     // consecutive threads write consecutive positions of each digit run
     const int64_t nblk = min((int64_t)kRsItems, n - (int64_t)blockIdx.x * kRsItems);
     for (int p = threadIdx.x; p < nblk; p += kRsThreads) {
-        const uint32_t key = ks[p];
-        const uint32_t d = (key >> shift) & 255u;
-        const uint32_t gpos = goff[d] + (p - bstart[d]);
+        const uint32_t key = sm.ks[p];
+        const uint32_t d = (key >> shift) & (D - 1);
+        const uint32_t gpos = sm.goff[d] + (p - sm.bstart[d]);
         kout[gpos] = key;
-        vout[gpos] = vs[p];
+        vout[gpos] = sm.vs[p];
     }
+}
+
+template <int B>
+int radix_pass(wsb_ctx *ctx, const uint32_t *ka, const uint32_t *va, uint32_t *kb, uint32_t *vb,
+               int64_t n, int shift, uint32_t *hist, int nb) {
+    constexpr int D = 1 << B;
+    const size_t hsm = sizeof(uint32_t) * kRsWarps * D, ssm = sizeof(RsSmem<B>);
+    WSB_CUDA_TRY(cudaFuncSetAttribute(k_radix_hist<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)hsm));
+    WSB_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter<B>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    k_radix_hist<B><<<nb, kRsThreads, hsm, ctx->stream>>>(ka, n, shift, hist, nb);
+    ctx->launches += 1;
+    WSB_TRY(exclusive_scan_u32(ctx, hist, hist, (int64_t)D * nb, nullptr));
+    k_radix_scatter<B><<<nb, kRsThreads, ssm, ctx->stream>>>(ka, va, kb, vb, n, shift, hist, nb);
+    ctx->launches += 1;
+    WSB_CUDA_TRY(cudaGetLastError());
+    return WSB_OK;
 }
 
 }  // namespace
@@ -240,17 +287,21 @@ int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t 
     *keys_out = keys;
     *vals_out = vals;
     if (n <= 1 || bits <= 0) return WSB_OK;
+    const int passes = (bits + 10) / 11;
+    const int B = std::max(8, (bits + passes - 1) / passes);
     const int nb = ceil_div(n, kRsItems);
     uint32_t *hist;
-    WSB_TRY(ensure(ctx, kSlotRadixHist, sizeof(uint32_t) * 256 * (size_t)nb, (void **)&hist));
+    WSB_TRY(ensure(ctx, kSlotRadixHist, sizeof(uint32_t) * ((size_t)1 << B) * (size_t)nb,
+                   (void **)&hist));
     uint32_t *ka = keys, *kb = keys_alt, *va = vals, *vb = vals_alt;
-    for (int shift = 0; shift < bits; shift += 8) {
-        k_radix_hist<<<nb, kRsThreads, 0, ctx->stream>>>(ka, n, shift, hist, nb);
-        ctx->launches += 1;
-        WSB_TRY(exclusive_scan_u32(ctx, hist, hist, (int64_t)256 * nb, nullptr));
-        k_radix_scatter<<<nb, kRsThreads, 0, ctx->stream>>>(ka, va, kb, vb, n, shift, hist, nb);
-        ctx->launches += 1;
-        WSB_CUDA_TRY(cudaGetLastError());
+    for (int shift = 0; shift < bits; shift += B) {
+        switch (B) {
+            case 8: WSB_TRY(radix_pass<8>(ctx, ka, va, kb, vb, n, shift, hist, nb)); break;
+            case 9: WSB_TRY(radix_pass<9>(ctx, ka, va, kb, vb, n, shift, hist, nb)); break;
+            case 10: WSB_TRY(radix_pass<10>(ctx, ka, va, kb, vb, n, shift, hist, nb)); break;
+            case 11: WSB_TRY(radix_pass<11>(ctx, ka, va, kb, vb, n, shift, hist, nb)); break;
+            default: return fail(WSB_EUNSUPPORTED, "radix digit width");
+        }
         uint32_t *t = ka; ka = kb; kb = t;
         t = va; va = vb; vb = t;
     }
