@@ -19,6 +19,8 @@
 //                 the 1/(n_u n_v), 1/n_w and n factors, the real part, the
 //                 image strip and per-column residual norms. The transpose-back
 //                 of the reference is never materialised.
+#include <cuda_pipeline_primitives.h>
+
 #include "wsb_internal.cuh"
 
 
@@ -447,10 +449,17 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
             pst[i] = __double2loint(t[i].x);
         }
     }
-    auto gld_plane = [&](int k, double2 (&dst)[kColE]) {
+    // The next plane's inputs are prefetched with asynchronous global->shared
+    // copies (LDGSTS) into thread-private slots of the otherwise idle second
+    // buffer: no registers held across the plane's transform.
+    double2 *pbuf = sbuf + C * STRIDE;
+    auto prefetch = [&](int k) {
 #pragma unroll
         for (int i = 0; i < kColE; ++i)
-            dst[i] = off[i] >= 0 ? a.tgrid[off[i] + k * pst[i]] : make_double2(0.0, 0.0);
+            if (off[i] >= 0)
+                __pipeline_memcpy_async(&pbuf[i * CT + threadIdx.x], &a.tgrid[off[i] + k * pst[i]],
+                                        sizeof(double2));
+        __pipeline_commit();
     };
     // direction-cosine factor of a pixel (mesh.py:202-208, transform.py:200)
     auto n_of = [&](int cc, int j) {
@@ -469,15 +478,17 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     double2 acc[kColE];
 #pragma unroll
     for (int i = 0; i < kColE; ++i) acc[i] = a.k1 < a.n_w ? run[i * CT] : make_double2(0.0, 0.0);
-    double2 pf[kColE];
-    gld_plane(nk - 1, pf);
+    prefetch(nk - 1);
 
     for (int kl = nk - 1; kl >= 0; --kl) {
         double2 v[kColE];
+        __pipeline_wait_prior(0);
 #pragma unroll
-        for (int i = 0; i < kColE; ++i) v[i] = pf[i];
-        if (kl > 0) gld_plane(kl - 1, pf);
+        for (int i = 0; i < kColE; ++i)
+            v[i] = off[i] >= 0 ? pbuf[i * CT + threadIdx.x] : make_double2(0.0, 0.0);
         pass_compute<LOGN, P0::RL, kColE, CT>(1, tw, v);
+        // v has been consumed from the slots: refill them with the next plane
+        if (kl > 0) prefetch(kl - 1);
         if constexpr (!P0::LAST) {
             __syncthreads();  // the previous plane's last pass has read sbuf
             auto sst = [&](int seq, int idx, double2 z) { sbuf[seq * STRIDE + pidx(idx)] = z; };
