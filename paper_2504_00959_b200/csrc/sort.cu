@@ -98,7 +98,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t *__r
 // ---------------------------------------------------------------------------
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsIpt = 16;                      // rounds of 32 per warp
+#ifndef WSB_RS_IPT
+#define WSB_RS_IPT 8
+#endif
+constexpr int kRsIpt = WSB_RS_IPT;              // rounds of 32 per warp
 constexpr int kRsItems = kRsThreads * kRsIpt;   // 4096 per block
 constexpr int kRsPerWarp = 32 * kRsIpt;         // 512
 
@@ -143,7 +146,7 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const uint32_t *__res
 }
 
 template <int B>
-__global__ void __launch_bounds__(kRsThreads) k_radix_scatter(
+__global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
     uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ offs, int nb) {
     constexpr int D = 1 << B;

@@ -10,7 +10,8 @@ from collections import OrderedDict
 
 def short(name):
     name = re.sub(r"\(.*$", "", name)
-    name = name.replace("wsb::<unnamed>::", "").replace("void ", "")
+    for junk in ("wsb::<unnamed>::", "unnamed>::", "void "):
+        name = name.replace(junk, "")
     return name.strip()
 
 
@@ -26,7 +27,7 @@ def main():
         unit = r.get("Metric Unit", "ns")
         us = v / 1e3 if unit == "nsecond" or unit == "ns" else (v if unit in ("usecond", "us") else v * 1e3)
         rows.append((int(r["ID"]), short(r["Kernel Name"]), us))
-    starts = [i for i, (_, k, _) in enumerate(rows) if k.startswith("k_prepare")]
+    starts = [i for i, (_, k, _) in enumerate(rows) if k == "k_prepare"]
     if len(starts) >= 2:
         a, b = starts[-2], starts[-1]
     else:
