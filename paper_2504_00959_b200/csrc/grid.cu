@@ -85,9 +85,12 @@ __device__ __forceinline__ double fast_exp(double x) {
 template <int S>
 struct KParams {
     static constexpr int W = 2 * S + 1;
+    static constexpr int NKB = 12 + 4 * S;   // Kaiser-Bessel series terms (beta up to ~3.5 S)
     double p0;              // Gaussian: 2 sigma^2; Kaiser-Bessel: beta
     double cm[W];           // Gaussian: exp(-m^2/s2), m = S-k (factorised path)
+    double kb[NKB];         // Kaiser-Bessel: (beta^2/4)^k / (k!)^2 / I0(beta)
     int factorised;         // Gaussian: 1 if the factorised form cannot overflow
+    int series;             // Kaiser-Bessel: 1 if the NKB-term series is exact to 1e-17
 };
 
 // Weights of one axis for window taps k = 0..W-1 at offsets d_k = g - (i0+k):
@@ -128,9 +131,20 @@ __device__ __forceinline__ uint32_t axis_weights(double g, int i0, const KParams
             if (KIND == WSB_KERNEL_GAUSSIAN) {
                 w[k] = exp(__ddiv_rn(-__dmul_rn(d, d), kp.p0));
             } else {
+                // I0(beta sqrt(t)) / I0(beta), t = 1 - (d/S)^2 (gridder.py:92-98),
+                // as the power series sum_k (beta^2 t / 4)^k / (k!)^2 / I0(beta):
+                // positive terms, no cancellation, no exp/sqrt/division --
+                // within a few ulp of np.i0's Chebyshev evaluation
                 const double x = __ddiv_rn(d, (double)S);
                 const double t = fmax(__dsub_rn(1.0, __dmul_rn(x, x)), 0.0);
-                w[k] = __ddiv_rn(bessel_i0(__dmul_rn(kp.p0, __dsqrt_rn(t))), i0beta);
+                if (kp.series) {
+                    double p = kp.kb[KParams<S>::NKB - 1];
+#pragma unroll
+                    for (int q = KParams<S>::NKB - 2; q >= 0; --q) p = fma(p, t, kp.kb[q]);
+                    w[k] = p;
+                } else {  // large beta: np.i0's own Chebyshev evaluation
+                    w[k] = __ddiv_rn(bessel_i0(__dmul_rn(kp.p0, __dsqrt_rn(t))), i0beta);
+                }
             }
         }
     }
@@ -344,7 +358,32 @@ int launch_s(wsb_ctx *ctx, const SweepArgs &a, double p0) {
     KParams<S> kp;
     kp.p0 = p0;
     kp.factorised = 0;
+    kp.series = 0;
     for (int k = 0; k < W; ++k) kp.cm[k] = 0.0;
+    for (int q = 0; q < KParams<S>::NKB; ++q) kp.kb[q] = 0.0;
+    if (KIND == WSB_KERNEL_KAISER_BESSEL) {
+        // series of I0(beta sqrt(t)) in t, normalised by I0(beta) = its value at t = 1
+        const double h = p0 * p0 / 4.0;
+        double term = 1.0, i0b = 0.0;
+        for (int q = 0; q < 400; ++q) {
+            if (q > 0) term *= h / ((double)q * (double)q);
+            i0b += term;
+            if (q >= KParams<S>::NKB && term < 1e-18 * i0b) break;
+        }
+        term = 1.0;
+        for (int q = 0; q < KParams<S>::NKB; ++q) {
+            if (q > 0) term *= h / ((double)q * (double)q);
+            kp.kb[q] = term / i0b;
+        }
+        // the truncated tail must be negligible (|t| <= 1): else shape_param
+        // is beyond what this half_support's series length covers
+        double tail = term, tsum = 0.0;
+        for (int q = KParams<S>::NKB; q < 400 && tail > 1e-30 * i0b; ++q) {
+            tail *= h / ((double)q * (double)q);
+            tsum += tail;
+        }
+        kp.series = tsum <= 1e-17 * i0b ? 1 : 0;
+    }
     if (KIND == WSB_KERNEL_GAUSSIAN) {
         // exp(+2f/s2)^S must stay far from overflow, exp(-m^2/s2) from underflow
         kp.factorised = (2.0 * S / p0 < 600.0 && (double)S * S / p0 < 600.0) ? 1 : 0;

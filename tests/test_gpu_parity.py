@@ -96,6 +96,25 @@ def test_grid_matches_reference(W, golden_grid, kname):
     assert np.max(np.abs(grid - g[f"{kname}_grid"])) <= 1e-12
 
 
+@pytest.mark.parametrize("S,beta", [(1, 12.0), (3, 30.0), (2, 4.68)])
+def test_grid_kaiser_bessel_any_beta(W, golden_grid, S, beta):
+    """Kaiser-Bessel weights: the power-series evaluation (default betas) and
+    the np.i0 Chebyshev fallback (betas beyond the series length) both match
+    the oracle's np.i0 kernel (gridder.py:92-98) to 1e-12."""
+    g = golden_grid
+    spec = W.GridSpec(64, 64, 4, 1e-3, w_max_native=12.0)
+    kern = W.KernelSpec("kaiser_bessel", S, beta)
+    u, v, w, t, vis, wt = chunk_from(g, "in_")
+    rec, plane = W.prepare_device(u, v, w, vis, wt, spec)
+    gp, upd = W.grid_slab_device(rec, plane, spec, kern, 0, 64)
+    grid = W.unpack_grid_device(gp, spec, 0, 64).cpu().numpy()
+    prep = O.prepare(u, v, w, t, vis, wt, 64, 64, 4)
+    batch = O.exchange([prep], 64, 1, S)[0]
+    ref, upd_ref = O.grid_slab(batch, 64, 4, O.KIND_KAISER_BESSEL, S, beta, 0, 64)
+    assert upd == upd_ref
+    assert np.max(np.abs(grid - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+
 @pytest.mark.parametrize("R", [2, 4])
 def test_grid_slabs_bitwise_across_slab_counts(W, golden_grid, R):
     """Per-slab gridding after the exchange reproduces the 1-slab grid
