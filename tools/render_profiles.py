@@ -1,0 +1,54 @@
+"""Render profiles/ from a make_profiles.sh run (gpurun_out/): launch list
+of one step, ncu --set full summary, per-kernel DRAM traffic (traffic.json,
+read by bench.py), SASS listings of the hot kernels.
+    python tools/render_profiles.py ROUND   (e.g. r01)"""
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+OUT = ROOT / "gpurun_out"
+PROF = ROOT / "profiles"
+
+GROUPS = {  # bench.py kernel-table names
+    "k_prepare": "prepare(K1a)", "k_radix_scatter": "bucket_scatter(K1c)",
+    "k_grid_sweep": "grid(K2)", "k_fft_rows": "fft_rows(K3a)",
+    "k_fft_cols": "fft_cols_stack(K3b+K4)",
+}
+
+
+def main():
+    rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    PROF.mkdir(exist_ok=True)
+    subprocess.run([sys.executable, str(ROOT / "tools/launch_summary.py"),
+                    str(OUT / "launches_raw.csv"), str(PROF / f"launches_{rnd}.csv")], check=True,
+                   capture_output=True)
+    rep = OUT / "full.ncu-rep"
+    txt = subprocess.run([sys.executable, str(ROOT / "tools/ncu_summary.py"), str(rep)],
+                         capture_output=True, text=True).stdout
+    (PROF / f"ncu_{rnd}.txt").write_text(txt)
+    raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr = rows[0]
+    ki, rd, wr = hdr.index("Kernel Name"), hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    units = rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    traffic = {}
+    for r in rows[2:]:
+        name = r[ki]
+        for k, g in GROUPS.items():
+            if re.search(k + r"\b", name):
+                b = (float(r[rd].replace(",", "")) * scale.get(units[rd], 1) +
+                     float(r[wr].replace(",", "")) * scale.get(units[wr], 1))
+                traffic.setdefault(g, int(b))   # first launch of the kind
+    (PROF / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+    print(json.dumps(traffic, indent=1))
+
+
+if __name__ == "__main__":
+    main()
