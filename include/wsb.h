@@ -53,8 +53,15 @@ extern "C" {
  * transform.py:180-185 is already applied. */
 #define WSB_P_GROUP 1
 
-/* Largest transform length handled on chip in this build. */
-#define WSB_MAX_FFT_N 4096
+/* Longest transform handled on chip (one CTA) and longest transform
+ * supported: rows/columns of SP = N / WSB_ONCHIP_FFT_N > 1 blocks are split
+ * by decimation in frequency into SP on-chip transforms (one CTA per output
+ * residue class, each reading the whole row/column). */
+#define WSB_ONCHIP_FFT_N 4096
+#define WSB_MAX_FFT_N 16384
+/* Residue classes of the column pass: norm partials are laid out
+ * [WSB_COL_SPLIT(n_v)][columns][2]. */
+#define WSB_COL_SPLIT(n_v) ((n_v) > WSB_ONCHIP_FFT_N ? (n_v) / WSB_ONCHIP_FFT_N : 1)
 
 /* GridSpec (mesh.py:59-112). w_min/w_max normalised are fixed to [0, 1]. */
 typedef struct {
@@ -216,10 +223,12 @@ int wsb_push_blocks(wsb_ctx *ctx, int32_t n_dest, const void *const *src_ptrs,
  * same (grid, g0, ng); the context carries the running sum between calls and
  * the result equals that of a single call over [0, n_w). The call whose range
  * starts at plane 0 writes image_strip
- * f64[n_v][ng*G] (row-major) and norm_partials f64[ng*G][2] = (sum Im^2,
- * sum Re^2) per image column (fixed pairwise tree over the rows); the
- * caller sums the columns in order, which makes the norms independent of
- * the GPU count. Earlier calls leave both untouched. */
+ * f64[n_v][ng*G] (row-major) and norm_partials
+ * f64[WSB_COL_SPLIT(n_v)][ng*G][2] = (sum Im^2, sum Re^2) per image column
+ * (and row residue class mod WSB_COL_SPLIT(n_v); fixed pairwise tree over
+ * the rows); the caller sums residue-major, columns in order, which makes
+ * the norms independent of the GPU count. Earlier calls leave both
+ * untouched. */
 int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
                        const int32_t *src_rows_host, int32_t g0, int32_t ng,
                        int32_t plane_lo, int32_t plane_hi, const double *tgrid,

@@ -185,7 +185,7 @@ int wsb_ctx_destroy(wsb_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto &b : ctx->bufs)
         if (b.ptr) cudaFree(b.ptr);
-    for (int i = 0; i < 32; ++i)
+    for (int i = 0; i < 48; ++i)
         if (ctx->twiddle[i]) cudaFree(ctx->twiddle[i]);
     if (ctx->timing.created)
         for (int i = 0; i < 8; ++i) cudaEventDestroy(ctx->timing.ev[i]);
@@ -385,11 +385,15 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
     // strip layout (gridder output) and P layout (row-pass output)
     WSB_TRY(ensure(ctx, kSlotGrid, (size_t)16 * n_w * ceil_div(n_u, 32) * 32 * n_v, (void **)&gs));
     WSB_TRY(ensure(ctx, kSlotGridP, (size_t)16 * n_w * n_u * n_v, (void **)&gp));
-    WSB_TRY(ensure(ctx, kSlotStrip, sizeof(double) * (2 * (size_t)n_u + 4), (void **)&partials));
+    // norm partials [residue][column][2] (residues: columns longer than 4096 are split)
+    const int sp = std::max(1, n_v >> kMaxOnChipLog);
+    WSB_TRY(ensure(ctx, kSlotStrip, sizeof(double) * (2 * (size_t)n_u * sp + 4), (void **)&partials));
     WSB_TRY(ensure(ctx, kSlotU64, 64, (void **)&upd));
-    const double *tw;
-    WSB_TRY(twiddles(ctx, n_u, 4, &tw));   // row plan (radix 16)
-    WSB_TRY(twiddles(ctx, n_v, 3, &tw));   // column plan (radix 8)
+    const double *tw;   // tables built outside the timed region
+    WSB_TRY(twiddles(ctx, std::min(n_u, 1 << kMaxOnChipLog), 4, &tw));   // row plan (radix 16)
+    WSB_TRY(twiddles(ctx, std::min(n_v, 1 << kMaxOnChipLog), 3, &tw));   // column plan (radix 8)
+    if (n_u > (1 << kMaxOnChipLog)) WSB_TRY(twiddles(ctx, n_u, 0, &tw));
+    if (n_v > (1 << kMaxOnChipLog)) WSB_TRY(twiddles(ctx, n_v, 0, &tw));
 
     WSB_CUDA_TRY(cudaEventRecord(ev[0], ctx->stream));
     WSB_CUDA_TRY(cudaMemsetAsync(upd, 0, sizeof(unsigned long long), ctx->stream));
@@ -406,15 +410,15 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
     const int32_t rows[1] = {n_v};
     WSB_TRY(fft_cols_stack(ctx, grid, 1, rows, 0, n_u / kG, 0, n_w, gp, image_out, partials));
     WSB_CUDA_TRY(cudaEventRecord(ev[5], ctx->stream));
-    const int nb = n_u;  // one norm partial per image column
-    k_sum_partials<<<1, 256, 0, ctx->stream>>>(partials, nb, partials + 2 * (size_t)n_u);
+    const int nb = n_u * sp;  // one norm partial per image column (and residue)
+    k_sum_partials<<<1, 256, 0, ctx->stream>>>(partials, nb, partials + 2 * (size_t)nb);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     WSB_CUDA_TRY(cudaEventRecord(ev[6], ctx->stream));
     if (diag) {
         double norms[2];
         unsigned long long h;
-        WSB_CUDA_TRY(cudaMemcpyAsync(norms, partials + 2 * (size_t)n_u, sizeof(norms),
+        WSB_CUDA_TRY(cudaMemcpyAsync(norms, partials + 2 * (size_t)nb, sizeof(norms),
                                      cudaMemcpyDeviceToHost, ctx->stream));
         WSB_CUDA_TRY(cudaMemcpyAsync(&h, upd, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));

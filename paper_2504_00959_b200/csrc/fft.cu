@@ -304,14 +304,46 @@ struct RowDest {
     int g0[9];   // first group of each destination, g0[n_dest] = n_u/G, unused = INT_MAX
 };
 
+// z * exp(2 pi i q / 4), exact
+__device__ __forceinline__ double2 rot_quarter(double2 z, int q) {
+    switch (q & 3) {
+        case 0: return z;
+        case 1: return make_double2(-z.y, z.x);
+        case 2: return make_double2(-z.x, -z.y);
+        default: return make_double2(z.y, -z.x);
+    }
+}
+
+// Rows longer than the on-chip limit (N = SP * M, M = 2^LOGN <= 4096):
+// CTA residue e computes the outputs X[k SP + e] = FFT_M(u_e)[k] of the
+// decimation-in-frequency split
+//   u_e[n] = W_N^(n e) * sum_s x[n + s M] W_SP^(s e),   W_K = exp(2 pi i / K),
+// so every CTA reads the whole row (SP-fold reads) and runs the on-chip
+// M-point transform. twN: exp(2 pi i m / N), m < N.
+template <int SPL>
+__device__ __forceinline__ double2 dif_split(const double2 *x, int stride, int e, int n, int M,
+                                             const double2 *__restrict__ twN) {
+    constexpr int SP = 1 << SPL;
+    double2 u = x[0];
+#pragma unroll
+    for (int s = 1; s < SP; ++s) {
+        const double2 y = rot_quarter(x[(int64_t)s * stride], (4 / SP) * s * e);
+        u = cadd(u, y);
+    }
+    return e ? cmul(u, __ldg(&twN[n * e])) : u;
+}
+
 // 4096/N rows per CTA. The first pass reads its inputs straight from HBM
 // (32-byte sectors, 16 loads in flight per thread) and the last pass writes
 // its outputs straight back: shared memory only carries the inner exchanges.
-template <int LOGN>
+// SPL > 0: rows of N = 2^(LOGN+SPL) points, residue e = blockIdx.z (above).
+template <int LOGN, int SPL = 0>
 __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
     k_fft_rows(const double2 *__restrict__ in, int n_strips, int n_groups, int v_count,
-               int plane_lo, const double2 *__restrict__ tw, RowDest dst) {
-    constexpr int N = 1 << LOGN;
+               int plane_lo, const double2 *__restrict__ tw, const double2 *__restrict__ twN,
+               RowDest dst) {
+    constexpr int N = 1 << LOGN;          // on-chip transform length M
+    constexpr int SP = 1 << SPL;
     constexpr int RT = RowCfg<LOGN>::T;
     constexpr int NSEQ = RT * kRowE / N;  // rows per CTA
     constexpr int STRIDE = Seq<LOGN>::STRIDE;
@@ -319,15 +351,22 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
     extern __shared__ __align__(16) double2 s[];
     const int j0 = blockIdx.x * NSEQ;
     const int64_t plane = plane_lo + blockIdx.y;
+    const int e = SPL ? (int)blockIdx.z : 0;
     // in: strip layout [plane][col/32][row][col%32] (512-byte row runs)
     auto gld = [&](int seq, int col) {
-        return j0 + seq < v_count
-                   ? in[((plane * n_strips + col / 32) * v_count + j0 + seq) * 32 + (col % 32)]
-                   : make_double2(0.0, 0.0);
+        if (j0 + seq >= v_count) return make_double2(0.0, 0.0);
+        const double2 *p = in + ((plane * n_strips + col / 32) * v_count + j0 + seq) * 32 + (col % 32);
+        if constexpr (SPL == 0) {
+            return *p;
+        } else {
+            // column col + s*N lies (N/32) strips further on
+            return dif_split<SPL>(p, (N / 32) * v_count * 32, e, col, N, twN);
+        }
     };
     // out: P[plane][col/G][row][col%G] per destination (RowDest); with a
     // single destination this is the plain P layout
-    auto gst = [&](int seq, int col, double2 z) {
+    auto gst = [&](int seq, int k, double2 z) {
+        const int col = k * SP + e;
         if (j0 + seq < v_count) {
             const int g = col / kG;
             int lo = 0, hi = dst.g0[1];
@@ -379,6 +418,7 @@ struct ColArgs {
     double *strip;          // [n_v][ncols]
     double *partials;       // [ncols][2]
     double2 *run;           // running stack between plane ranges, per thread element
+    const double2 *twN;     // exp(2 pi i m / n_v), m < n_v (split columns only)
     int n_w, n_u, n_v, ncols, g0;
     int k0, k1;             // plane range of this call
     int n_src;
@@ -402,7 +442,10 @@ __device__ __forceinline__ double plane_w(const ColArgs &a, int k) {
 // evaluation (|z| = 1: the rounding grows by about one ulp per plane).
 // Plane k-1's first-pass inputs are loaded into registers while plane k is
 // transformed; the last pass leaves its outputs in registers.
-template <int LOGN>
+// SPL > 0 (n_v = SP * 4096): residue CTA e = blockIdx.y transforms output
+// rows k SP + e of its columns through the decimation-in-frequency split of
+// dif_split (every CTA reads its whole columns).
+template <int LOGN, int SPL = 0>
 __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     k_fft_cols(ColArgs a, const double2 *__restrict__ tw) {
     constexpr int CT = ColCfg<LOGN>::T;
@@ -419,6 +462,9 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
 
     const int c0 = blockIdx.x * C;                 // first local column
     const int nk = a.k1 - a.k0;                    // planes in this call
+    constexpr int SP = 1 << SPL;
+    const int eres = SPL ? (int)blockIdx.y : 0;
+    auto prow = [&](int k) { return k * SP + eres; };   // image row of transform output k
     // Offset of each first-pass input of this thread in plane 0 and its
     // per-plane stride (both the same for every plane): element (row j,
     // local column c0+seq) in the transposed layout
@@ -461,6 +507,27 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
                                         sizeof(double2));
         __pipeline_commit();
     };
+    // split columns: input k of the on-chip transform combines rows k + s N
+    auto ld_split = [&](int kpl, int seq, int j) -> double2 {
+        const int lc = c0 + seq;
+        if (lc >= a.ncols) return make_double2(0.0, 0.0);
+        double2 u = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < SP; ++s) {
+            const int row = j + s * N;
+            int r0 = 0, r1 = a.src_start[1];
+#pragma unroll
+            for (int sidx = 1; sidx < 8; ++sidx)
+                if (row >= a.src_start[sidx]) {
+                    r0 = a.src_start[sidx];
+                    r1 = a.src_start[sidx + 1];
+                }
+            const int64_t o = (int64_t)nk * a.ncols * r0 + ((int64_t)kpl * a.ncols + lc) * (r1 - r0) +
+                              (row - r0);
+            u = cadd(u, rot_quarter(a.tgrid[o], (4 / SP) * s * eres));
+        }
+        return eres ? cmul(u, __ldg(&a.twN[j * eres])) : u;
+    };
     // direction-cosine factor of a pixel (mesh.py:202-208, transform.py:200)
     auto n_of = [&](int cc, int j) {
         const int gi = a.g0 * kG + c0 + cc;
@@ -471,24 +538,30 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
 
     const double dw = a.n_w > 1 ? (a.w_max - a.w_min) / (double)(a.n_w - 1) : 0.0;
     for (int e = threadIdx.x; e < C * N; e += CT)
-        zbuf[e] = cis_pi(2.0 * dw * (n_of(e / N, e % N) - 1.0));
+        zbuf[e] = cis_pi(2.0 * dw * (n_of(e / N, prow(e % N)) - 1.0));
 
     // the running stack of the planes above this range continues
-    double2 *run = a.run + (int64_t)blockIdx.x * kColE * CT + threadIdx.x;
+    double2 *run = a.run + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * kColE * CT + threadIdx.x;
     double2 acc[kColE];
 #pragma unroll
     for (int i = 0; i < kColE; ++i) acc[i] = a.k1 < a.n_w ? run[i * CT] : make_double2(0.0, 0.0);
-    prefetch(nk - 1);
+    if constexpr (SPL == 0) prefetch(nk - 1);
 
     for (int kl = nk - 1; kl >= 0; --kl) {
         double2 v[kColE];
-        __pipeline_wait_prior(0);
+        if constexpr (SPL == 0) {
+            __pipeline_wait_prior(0);
 #pragma unroll
-        for (int i = 0; i < kColE; ++i)
-            v[i] = off[i] >= 0 ? pbuf[i * CT + threadIdx.x] : make_double2(0.0, 0.0);
-        pass_compute<LOGN, P0::RL, kColE, CT>(1, tw, v);
-        // v has been consumed from the slots: refill them with the next plane
-        if (kl > 0) prefetch(kl - 1);
+            for (int i = 0; i < kColE; ++i)
+                v[i] = off[i] >= 0 ? pbuf[i * CT + threadIdx.x] : make_double2(0.0, 0.0);
+            pass_compute<LOGN, P0::RL, kColE, CT>(1, tw, v);
+            // v has been consumed from the slots: refill them with the next plane
+            if (kl > 0) prefetch(kl - 1);
+        } else {
+            auto ld = [&](int seq, int j) { return ld_split(kl, seq, j); };
+            pass_load<LOGN, P0::RL, kColE, CT>(v, ld);
+            pass_compute<LOGN, P0::RL, kColE, CT>(1, tw, v);
+        }
         if constexpr (!P0::LAST) {
             __syncthreads();  // the previous plane's last pass has read sbuf
             auto sst = [&](int seq, int idx, double2 z) { sbuf[seq * STRIDE + pidx(idx)] = z; };
@@ -534,7 +607,7 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int row = j + r * M;
-            const double n = n_of(seq, row);
+            const double n = n_of(seq, prow(row));
             double2 z = cmul(acc[kb * R + r], cis_pi(2.0 * w0 * (n - 1.0)));
             z.x *= a.inv_nuv;
             z.y *= a.inv_nuv;
@@ -550,7 +623,8 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     // image rows: the C columns of a row are contiguous in the strip
     for (int e = threadIdx.x; e < C * N; e += CT) {
         const int cc = e % C, row = e / C;
-        if (c0 + cc < a.ncols) a.strip[(int64_t)row * a.ncols + c0 + cc] = pix[cc * STRIDE + pidx(row)].x;
+        if (c0 + cc < a.ncols)
+            a.strip[(int64_t)prow(row) * a.ncols + c0 + cc] = pix[cc * STRIDE + pidx(row)].x;
     }
     // per-column pairwise tree over the N rows
     for (int half = N / 2; half > 0; half >>= 1) {
@@ -562,9 +636,9 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
         __syncthreads();
     }
     for (int cc = threadIdx.x; cc < C; cc += CT)
-        if (c0 + cc < a.ncols) {
-            a.partials[2 * (c0 + cc) + 0] = sq[cc * STRIDE].x;
-            a.partials[2 * (c0 + cc) + 1] = sq[cc * STRIDE].y;
+        if (c0 + cc < a.ncols) {   // partials [residue][column][2]
+            a.partials[2 * ((int64_t)eres * a.ncols + c0 + cc) + 0] = sq[cc * STRIDE].x;
+            a.partials[2 * ((int64_t)eres * a.ncols + c0 + cc) + 1] = sq[cc * STRIDE].y;
         }
 }
 
@@ -574,8 +648,8 @@ __global__ void k_twiddles(double2 *tw, int logn, int rlmax, int size) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= size) return;
     const int n = 1 << logn;
-    int off = 0, d = 0, m = 0;
-    while (d < logn) {
+    int off = 0, d = 0, m = rlmax == 0 ? e : 0;
+    while (rlmax != 0 && d < logn) {
         const int first = logn % rlmax;
         const int rl = (d == 0 && first != 0) ? first : rlmax;
         if (d > 0) {
@@ -595,30 +669,67 @@ __global__ void k_twiddles(double2 *tw, int logn, int rlmax, int size) {
 
 template <int LOGN>
 int launch_rows(wsb_ctx *ctx, const double2 *in, int n_strips, int n_groups, int v_count, int plo,
-                int phi, const double2 *tw, const RowDest &dst) {
+                int phi, const double2 *tw, const double2 *twN, const RowDest &dst, int spl) {
     constexpr int N = 1 << LOGN;
     constexpr int RT = RowCfg<LOGN>::T;
     constexpr int NSEQ = RT * kRowE / N;
     const size_t smem = sizeof(double2) * NSEQ * Seq<LOGN>::STRIDE;
-    WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-    dim3 grd(ceil_div(v_count, NSEQ), phi - plo);
-    k_fft_rows<LOGN><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo, tw, dst);
+    dim3 grd(ceil_div(v_count, NSEQ), phi - plo, 1 << spl);
+    if (spl == 0) {
+        WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 0>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_fft_rows<LOGN, 0><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo, tw,
+                                                            twN, dst);
+    } else if constexpr (LOGN == 12) {
+        if (spl == 1) {
+            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 1>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_fft_rows<LOGN, 1><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo,
+                                                                tw, twN, dst);
+        } else if (spl == 2) {
+            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 2>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_fft_rows<LOGN, 2><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo,
+                                                                tw, twN, dst);
+        } else {
+            return fail(WSB_EUNSUPPORTED, "row length above 16384");
+        }
+    } else {
+        return fail(WSB_EUNSUPPORTED, "split rows run on the 4096-point transform");
+    }
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
 }
 
 template <int LOGN>
-int launch_cols(wsb_ctx *ctx, const ColArgs &a, const double2 *tw, int *nblocks) {
+int launch_cols(wsb_ctx *ctx, const ColArgs &a, const double2 *tw, int *nblocks, int spl) {
+    static_assert(kG == 1, "the split column loads assume the column-major P layout");
     constexpr int N = 1 << LOGN;
     constexpr int CT = ColCfg<LOGN>::T;
     constexpr int C = CT * kColE / N;
     const size_t smem = sizeof(double2) * (2 * C * Seq<LOGN>::STRIDE + C * N);
-    WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
     *nblocks = ceil_div(a.ncols, C);
-    k_fft_cols<LOGN><<<*nblocks, CT, smem, ctx->stream>>>(a, tw);
+    const dim3 grd(*nblocks, 1 << spl);
+    if (spl == 0) {
+        WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN, 0>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_fft_cols<LOGN, 0><<<grd, CT, smem, ctx->stream>>>(a, tw);
+    } else if constexpr (LOGN == 12) {
+        if (spl == 1) {
+            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN, 1>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_fft_cols<LOGN, 1><<<grd, CT, smem, ctx->stream>>>(a, tw);
+        } else if (spl == 2) {
+            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN, 2>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_fft_cols<LOGN, 2><<<grd, CT, smem, ctx->stream>>>(a, tw);
+        } else {
+            return fail(WSB_EUNSUPPORTED, "column length above 16384");
+        }
+    } else {
+        return fail(WSB_EUNSUPPORTED, "split columns run on the 4096-point transform");
+    }
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
@@ -627,11 +738,12 @@ int launch_cols(wsb_ctx *ctx, const ColArgs &a, const double2 *tw, int *nblocks)
 }  // namespace
 
 int twiddles(wsb_ctx *ctx, int n, int rlmax, const double **out) {
+    // rlmax 3/4: pass-ordered table of an n-point plan; 0: plain exp(2 pi i m / n)
     const int l = ilog2(n);
-    const int key = l + 16 * (rlmax - 3);
-    if (rlmax < 3 || rlmax > 4) return fail(WSB_EINVAL, "twiddle plan radix");
+    if (!(rlmax == 0 || rlmax == 3 || rlmax == 4) || l > 15) return fail(WSB_EINVAL, "twiddle table");
+    const int key = l + 16 * (rlmax == 0 ? 2 : rlmax - 3);
     if (!ctx->twiddle[key]) {
-        const int size = std::max(1, tw_offset(l, rlmax, l));
+        const int size = rlmax == 0 ? n : std::max(1, tw_offset(l, rlmax, l));
         WSB_CUDA_TRY(cudaMalloc(&ctx->twiddle[key], sizeof(double2) * size));
         k_twiddles<<<ceil_div(size, 256), 256, 0, ctx->stream>>>((double2 *)ctx->twiddle[key], l,
                                                                  rlmax, size);
@@ -645,8 +757,8 @@ int twiddles(wsb_ctx *ctx, int n, int rlmax, const double **out) {
 int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a, double *grid_p,
              int plo, int phi, int n_dest, const int32_t *dest_groups, void *const *dest_ptrs) {
     if (phi <= plo || v_count <= 0) return WSB_OK;
-    const double *tw;
-    WSB_TRY(twiddles(ctx, g->n_u, kRowRL, &tw));
+    const double *tw = nullptr;
+    if (g->n_u <= (1 << kMaxOnChipLog)) WSB_TRY(twiddles(ctx, g->n_u, kRowRL, &tw));
     const int ng = g->n_u / kG, ns = ceil_div(g->n_u, 32);
     RowDest dst;
     if (n_dest < 1 || n_dest > 8) return fail(WSB_EINVAL, "n_dest must be in [1, 8]");
@@ -669,14 +781,21 @@ int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a,
             dst.ptr[d] = (double2 *)grid_p + (int64_t)(phi - plo) * v_count * kG * dst.g0[d];
     }
     const double2 *ga = (const double2 *)grid_a;
-    const double2 *t2 = (const double2 *)tw;
-    switch (ilog2(g->n_u)) {
+    // rows above the on-chip 4096 points: SP = n_u / 4096 residue CTAs per row
+    const int logn = ilog2(g->n_u), logs = std::min(logn, kMaxOnChipLog), spl = logn - logs;
+    const double *twn = nullptr;
+    if (spl > 0) {
+        WSB_TRY(twiddles(ctx, 1 << logs, kRowRL, &tw));
+        WSB_TRY(twiddles(ctx, g->n_u, 0, &twn));
+    }
+    const double2 *t2 = (const double2 *)tw, *tn = (const double2 *)twn;
+    switch (logs) {
 #define WSB_ROWS(L) \
-    case L: return launch_rows<L>(ctx, ga, ns, ng, v_count, plo, phi, t2, dst);
+    case L: return launch_rows<L>(ctx, ga, ns, ng, v_count, plo, phi, t2, tn, dst, spl);
         WSB_ROWS(1) WSB_ROWS(2) WSB_ROWS(3) WSB_ROWS(4) WSB_ROWS(5) WSB_ROWS(6)
         WSB_ROWS(7) WSB_ROWS(8) WSB_ROWS(9) WSB_ROWS(10) WSB_ROWS(11) WSB_ROWS(12)
 #undef WSB_ROWS
-        default: return fail(WSB_EUNSUPPORTED, "n_u above 4096 needs the out-of-core FFT (not in this build)");
+        default: return fail(WSB_EUNSUPPORTED, "transform length not supported");
     }
 }
 
@@ -708,31 +827,34 @@ int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t
     a.w_max = g->w_max_native;
     a.k0 = plo;
     a.k1 = phi;
+    // columns above the on-chip 4096 points: SP = n_v / 4096 residue CTAs
+    const int logn = ilog2(g->n_v), logs = std::min(logn, kMaxOnChipLog), spl = logn - logs;
     // the running stack: one complex per thread element of the launch
     {
-        const int lg = ilog2(g->n_v);
-        const int ct = std::max((1 << lg) / 8, 256), cpb = std::max(1, ct * 8 / (1 << lg));
-        const size_t bytes = sizeof(double2) * (size_t)ceil_div(a.ncols, cpb) * ct * 8;
+        const int ct = std::max((1 << logs) / 8, 256), cpb = std::max(1, ct * 8 / (1 << logs));
+        const size_t bytes = sizeof(double2) * (size_t)ceil_div(a.ncols, cpb) * ct * 8 << spl;
         WSB_TRY(ensure(ctx, kSlotColRun, bytes, (void **)&a.run));
     }
-    const double *tw;
-    WSB_TRY(twiddles(ctx, g->n_v, kColRL, &tw));
+    const double *tw, *twn = nullptr;
+    WSB_TRY(twiddles(ctx, 1 << logs, kColRL, &tw));
+    if (spl > 0) WSB_TRY(twiddles(ctx, g->n_v, 0, &twn));
+    a.twN = (const double2 *)twn;
     const double2 *t2 = (const double2 *)tw;
     int nb = 0;
-    switch (ilog2(g->n_v)) {
-        case 1: return launch_cols<1>(ctx, a, t2, &nb);
-        case 2: return launch_cols<2>(ctx, a, t2, &nb);
-        case 3: return launch_cols<3>(ctx, a, t2, &nb);
-        case 4: return launch_cols<4>(ctx, a, t2, &nb);
-        case 5: return launch_cols<5>(ctx, a, t2, &nb);
-        case 6: return launch_cols<6>(ctx, a, t2, &nb);
-        case 7: return launch_cols<7>(ctx, a, t2, &nb);
-        case 8: return launch_cols<8>(ctx, a, t2, &nb);
-        case 9: return launch_cols<9>(ctx, a, t2, &nb);
-        case 10: return launch_cols<10>(ctx, a, t2, &nb);
-        case 11: return launch_cols<11>(ctx, a, t2, &nb);
-        case 12: return launch_cols<12>(ctx, a, t2, &nb);
-        default: return fail(WSB_EUNSUPPORTED, "n_v above 4096 needs the out-of-core FFT (not in this build)");
+    switch (logs) {
+        case 1: return launch_cols<1>(ctx, a, t2, &nb, spl);
+        case 2: return launch_cols<2>(ctx, a, t2, &nb, spl);
+        case 3: return launch_cols<3>(ctx, a, t2, &nb, spl);
+        case 4: return launch_cols<4>(ctx, a, t2, &nb, spl);
+        case 5: return launch_cols<5>(ctx, a, t2, &nb, spl);
+        case 6: return launch_cols<6>(ctx, a, t2, &nb, spl);
+        case 7: return launch_cols<7>(ctx, a, t2, &nb, spl);
+        case 8: return launch_cols<8>(ctx, a, t2, &nb, spl);
+        case 9: return launch_cols<9>(ctx, a, t2, &nb, spl);
+        case 10: return launch_cols<10>(ctx, a, t2, &nb, spl);
+        case 11: return launch_cols<11>(ctx, a, t2, &nb, spl);
+        case 12: return launch_cols<12>(ctx, a, t2, &nb, spl);
+        default: return fail(WSB_EUNSUPPORTED, "transform length not supported");
     }
 }
 

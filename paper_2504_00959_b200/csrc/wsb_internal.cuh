@@ -14,6 +14,7 @@ namespace wsb {
 constexpr int kTile = 64;          // gridding tile edge (cells)
 constexpr int kG = WSB_P_GROUP;    // P-layout column group
 constexpr int kMaxS = 7;           // largest half support compiled (window 15)
+constexpr int kMaxOnChipLog = 12;  // longest on-chip transform (4096); longer ones split
 
 // thread-local error detail
 void set_error(const std::string &msg);
@@ -54,8 +55,8 @@ struct wsb_ctx {
     int *flag_host = nullptr;         // pinned scratch for small readbacks
     unsigned long long *u64_host = nullptr;
     wsb::Timing timing;
-    // pass-ordered twiddle tables keyed by log2(n) + 16 * (plan radix bits - 3)
-    double *twiddle[32] = {nullptr};
+    // twiddle tables keyed by log2(n) + 16 * {0: radix-8 plan, 1: radix-16 plan, 2: plain}
+    double *twiddle[48] = {nullptr};
     // last bucketing (for wsb_tiles_debug)
     int64_t last_entries = 0, last_tiles = 0;
     uint32_t *last_keys = nullptr, *last_idx = nullptr, *last_off = nullptr;

@@ -119,8 +119,8 @@ class CudaBackend:
         final = plane_lo == 0
         strip = torch.empty((spec.n_v, ng * G) if final else (1,), dtype=torch.float64,
                             device=self.device)
-        partials = torch.empty((ng * G, 2) if final else (1,), dtype=torch.float64,
-                               device=self.device)
+        partials = torch.empty((col_split(spec.n_v), ng * G, 2) if final else (1,),
+                               dtype=torch.float64, device=self.device)
         rows = (C.c_int32 * len(src_rows))(*src_rows)
         L.check(L.lib().wsb_fft_cols_stack(self.ctx.handle, C.byref(g), len(src_rows), rows, int(g0),
                                            int(ng), int(plane_lo), int(plane_hi), _ptr(tgrid),
@@ -182,6 +182,15 @@ def balanced_slab_starts(row_counts, n_ranks: int, row_weight: float = 10_000.0)
         starts.append(r)
     starts.append(n_v)
     return starts
+
+
+ONCHIP_FFT_N = 4096   # include/wsb.h WSB_ONCHIP_FFT_N
+
+
+def col_split(n_v: int) -> int:
+    """WSB_COL_SPLIT: residue classes of the column pass (norm partials are
+    [residue][column][2])."""
+    return n_v // ONCHIP_FFT_N if n_v > ONCHIP_FFT_N else 1
 
 
 _SYMM: dict = {}
@@ -377,8 +386,9 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     maxc = max(dest_pairs) * G
     pad = torch.zeros((spec.n_v, maxc), dtype=torch.float64, device=dev)
     pad[:, : ng * G] = strip
-    ppad = torch.zeros((maxc, 2), dtype=torch.float64, device=dev)
-    ppad[: ng * G] = partials
+    sp = col_split(spec.n_v)
+    ppad = torch.zeros((sp, maxc, 2), dtype=torch.float64, device=dev)
+    ppad[:, : ng * G] = partials.reshape(sp, ng * G, 2)
     strips = [torch.empty_like(pad) for _ in range(R)]
     parts = [torch.empty_like(ppad) for _ in range(R)]
     dist.all_gather(strips, pad, group=group)
@@ -397,10 +407,10 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     col_parts = []
     for d, (g0_d, ng_d) in enumerate(cols):
         pix[:, g0_d * G:(g0_d + ng_d) * G] = strips[d][:, : ng_d * G]
-        col_parts.append(parts[d][: ng_d * G])
-    p = torch.cat(col_parts).cpu().numpy()
-    # sequential sum in global column order (cumsum is left to right): the
-    # same association as the single-GPU path, for any R
+        col_parts.append(parts[d][:, : ng_d * G])
+    p = torch.cat(col_parts, dim=1).reshape(-1, 2).cpu().numpy()
+    # sequential sum residue-major, in global column order (cumsum is left to
+    # right): the same association as the single-GPU path, for any R
     im_sq = float(p[:, 0].cumsum()[-1])
     re_sq = float(p[:, 1].cumsum()[-1])
     img = FinalImage(spec, pix.cpu().numpy() if to_host else pix, im_sq ** 0.5, re_sq ** 0.5)

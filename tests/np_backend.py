@@ -105,5 +105,8 @@ class NumpyBackend:
             acc = acc + self._planes[k]
         acc = acc / spec.n_w * n
         strip = np.ascontiguousarray(acc.real)
-        partials = np.stack([(acc.imag ** 2).sum(axis=0), (acc.real ** 2).sum(axis=0)], axis=1)
+        sp = spec.n_v // 4096 if spec.n_v > 4096 else 1      # residue classes of the rows
+        partials = np.stack([np.stack([(acc.imag[e::sp] ** 2).sum(axis=0),
+                                       (acc.real[e::sp] ** 2).sum(axis=0)], axis=1)
+                             for e in range(sp)])
         return torch.from_numpy(strip), torch.from_numpy(np.ascontiguousarray(partials))

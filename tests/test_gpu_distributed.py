@@ -76,8 +76,8 @@ def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges=1, starts=Non
             tgrid = torch.cat(chunks).contiguous()
             strip, partials = be.fft_cols_stack(tgrid, spec, [vc for _, vc in slabs], g0, ng, k0, k1)
         pix[:, g0 * G:(g0 + ng) * G] = strip.cpu().numpy()
-        parts.append(partials.cpu().numpy())
-    p = np.concatenate(parts)
+        parts.append(partials.cpu().numpy().reshape(-1, ng * G, 2))
+    p = np.concatenate(parts, axis=1).reshape(-1, 2)   # residue-major, global column order
     return pix, np.sqrt([p[:, 0].cumsum()[-1], p[:, 1].cumsum()[-1]]), upd
 
 

@@ -243,3 +243,51 @@ def test_route_uneven_slabs_and_row_histogram(W, golden_bucket):
     with pytest.raises(ValueError):
         L.check(L.lib().wsb_route_count(be.ctx.handle, C.byref(gs), S, 3, bad,
                                         C.c_void_p(rec.data_ptr()), rec.shape[0], cnt))
+
+
+@pytest.mark.parametrize("n", [8192, 16384])
+def test_large_mesh_split_transforms(W, n):
+    """Rows/columns longer than the on-chip 4096 points (cfg4's 16384²) run
+    as SP = n/4096 decimation-in-frequency residue transforms. The image is
+    checked against the reference formulas (transform.py:173-230: sign,
+    normalised inverse 2D DFT, w screen skipped at w_k = 0, stack / n_w * n)
+    evaluated with torch's FP64 FFT on the GPU grid itself, to 1e-10."""
+    import torch
+    rng = np.random.default_rng(5)
+    m = 20_000
+    n_w = 2
+    cell = 2e-5
+    spec = W.GridSpec(n, n, n_w, cell, w_max_native=800.0)
+    kern = W.KernelSpec.gaussian(3, 1.0)
+    u = rng.uniform(0.3, 0.7, m)
+    v = rng.uniform(0.3, 0.7, m)
+    w = rng.uniform(0.0, 1.0, m)
+    vis = (rng.standard_normal(m) + 1j * rng.standard_normal(m)).astype(np.complex64)
+    wt = rng.uniform(0.5, 1.0, m).astype(np.float32)
+    dev = torch.device("cuda", 0)
+    du, dv, dw, dvis, dwt = (torch.from_numpy(a).to(dev) for a in (u, v, w, vis, wt))
+    img, diag = W.image_device(du, dv, dw, dvis, dwt, spec, kern)
+    rec, plane = W.prepare_device(du, dv, dw, dvis, dwt, spec)
+    gs, upd = W.grid_slab_device(rec, plane, spec, kern, 0, n)
+    assert upd == diag["grid_updates"]
+    grid = W.unpack_grid_device(gs, spec, 0, n)          # (n_w, n_v, n_u), no sign
+    del gs
+    ii = torch.arange(n, device=dev, dtype=torch.float64)
+    sign = 1.0 - 2.0 * ((ii[:, None] + ii[None, :]).remainder(2.0))
+    l = (ii - n // 2) * cell
+    nn = torch.sqrt(1.0 - l[None, :] ** 2 - l[:, None] ** 2)
+    acc = torch.zeros((n, n), dtype=torch.complex128, device=dev)
+    for k in range(n_w):
+        p = torch.fft.ifft2(grid[k] * sign)
+        wk = spec.plane_w_native(k)
+        if wk != 0.0:
+            p = p * torch.exp(2j * np.pi * wk * (nn - 1.0))
+        acc = acc + p
+        del p
+    acc = acc / n_w * nn
+    ref = acc.real
+    got = img if isinstance(img, torch.Tensor) else torch.as_tensor(img.pixels, device=dev)
+    err = float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref))
+    assert err <= 1e-10, err
+    assert abs(diag["imag_residual_norm"] - float(torch.linalg.norm(acc.imag))) <= 1e-9 * float(
+        torch.linalg.norm(acc.imag))
