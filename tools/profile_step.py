@@ -24,8 +24,11 @@ def main():
     ap.add_argument("--nw", type=int, default=32)
     ap.add_argument("--kind", default="gaussian")
     ap.add_argument("--S", type=int, default=3)
+    ap.add_argument("--cell", type=float, default=None)
     a = ap.parse_args()
     cfg = dict(bench.CFG2, n_vis=a.n, n_u=a.nu, n_v=a.nu, n_w=a.nw)
+    if a.cell:
+        cfg["cell"] = a.cell
     u, v, w, t, vis, wt = bench.synthetic(cfg)
     dev = torch.device("cuda", 0)
     du, dv, dw, dvis, dwt = (torch.from_numpy(x).to(dev) for x in (u, v, w, vis, wt))
