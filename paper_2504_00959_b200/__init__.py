@@ -18,6 +18,7 @@ from .imager import (  # noqa: F401
     grid_slab_device,
     image,
     image_device,
+    image_stream,
     last_timings,
     partition_1d,
     prepare_device,

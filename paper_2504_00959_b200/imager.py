@@ -310,6 +310,88 @@ def image_device(u, v, w, vis, weight, spec, kern, image_out: torch.Tensor | Non
     return image_out, diag_dict(d)
 
 
+def image_stream(batches, spec, kern, device: int = 0):
+    """Dirty images of a stream of HOST record batches (one image per batch,
+    e.g. successive time chunks of an observation), double-buffered: the
+    host->device copy of batch i+1 and the device->host copy of image i-1
+    run on their own streams (both PCIe directions) while batch i is imaged.
+    Every batch still makes the full round trip; only the copies overlap the
+    device work. Each batch is (u, v, w, vis, weight) as in ``image``;
+    page-locked host arrays move at DMA speed. Yields (FinalImage, diag)."""
+    spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
+    _require_cuda()
+    dev = torch.device("cuda", int(device))
+    ctx = context(dev)
+    compute = torch.cuda.current_stream(dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    sets = [None, None]            # device input buffers per slot
+    imgs = [None, None]            # device images per slot
+    done = [None, None]            # compute-finished event per slot
+    read = [None, None]            # image-copied-out event per slot
+
+    def upload(i, b):
+        u, v, w, vis, wt = b
+        n = len(u)
+        vis = _cols2d(np.asarray(vis, np.complex64), n)
+        wt = _cols2d(np.asarray(wt, np.float32), n)
+        host = [torch.from_numpy(np.ascontiguousarray(x)) for x in
+                (np.asarray(u, np.float64), np.asarray(v, np.float64), np.asarray(w, np.float64),
+                 vis.view(np.float32), wt)]
+        slot = i % 2
+        with torch.cuda.stream(s_in):
+            if done[slot] is not None:
+                s_in.wait_event(done[slot])      # the slot's previous batch has been imaged
+            sets[slot] = [h.to(dev, non_blocking=True) for h in host]
+            ev = torch.cuda.Event()
+            ev.record(s_in)
+        return ev, vis.shape[1], host
+
+    it = iter(batches)
+    nxt = next(it, None)
+    if nxt is None:
+        return
+    staged = upload(0, nxt)
+    pending = None                 # (event, pinned image, diag, slot) of the previous batch
+    i = 0
+    while staged is not None:
+        ev, n_chan, _host = staged
+        slot = i % 2
+        nxt = next(it, None)
+        compute.wait_event(ev)
+        # the next upload is enqueued before this batch's (synchronising) call
+        staged_next = upload(i + 1, nxt) if nxt is not None else None
+        u, v, w, visf, wt = sets[slot]
+        n = u.numel()
+        if imgs[slot] is None:
+            imgs[slot] = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, device=dev)
+        if read[slot] is not None:
+            compute.wait_event(read[slot])       # image of batch i-2 has left the device
+        d = L.WsbDiag()
+        g, k = spec.c_struct(), kern.c_struct()
+        L.check(L.lib().wsb_image_device(ctx.handle, C.byref(g), C.byref(k), _ptr(u), _ptr(v),
+                                         _ptr(w), _ptr(visf), _ptr(wt), n, n_chan,
+                                         _ptr(imgs[slot]), C.byref(d)))
+        done[slot] = torch.cuda.Event()
+        done[slot].record(compute)
+        out = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, pin_memory=True)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(done[slot])
+            out.copy_(imgs[slot], non_blocking=True)
+            oev = torch.cuda.Event()
+            oev.record(s_out)
+        read[slot] = oev
+        if pending is not None:
+            pev, pout, pd = pending
+            pev.synchronize()
+            yield FinalImage(spec, pout.numpy(), pd.imag_residual_norm, pd.real_norm), diag_dict(pd)
+        pending = (oev, out, d)
+        staged = staged_next
+        i += 1
+    pev, pout, pd = pending
+    pev.synchronize()
+    yield FinalImage(spec, pout.numpy(), pd.imag_residual_norm, pd.real_norm), diag_dict(pd)
+
+
 def diag_dict(d: L.WsbDiag) -> dict:
     return {"imag_residual_norm": d.imag_residual_norm, "real_norm": d.real_norm,
             "grid_updates": int(d.grid_updates), "records": int(d.records),

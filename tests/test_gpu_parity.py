@@ -291,3 +291,29 @@ def test_large_mesh_split_transforms(W, n):
     assert err <= 1e-10, err
     assert abs(diag["imag_residual_norm"] - float(torch.linalg.norm(acc.imag))) <= 1e-9 * float(
         torch.linalg.norm(acc.imag))
+
+
+def test_image_stream_matches_single_calls(W, golden_image):
+    """The double-buffered stream API returns, batch by batch, exactly the
+    images of separate wsb_image calls (the copies overlap, the math does
+    not change)."""
+    import torch
+    g = golden_image
+    n_u, n_v, n_w, S, _ = (int(x) for x in g["wide_cfg"])
+    cell, wmin, wmax, shape = (float(x) for x in g["wide_fcfg"])
+    spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
+    kern = W.KernelSpec("gaussian", S, shape)
+    u, v, w, t, vis, wt = chunk_from(g, "wide_in_")
+    n = len(u)
+    cuts = [0, n // 3, n // 2, n]
+    batches = []
+    for a, b in zip(cuts, cuts[1:]):
+        batches.append(tuple(torch.from_numpy(np.ascontiguousarray(x[a:b])).pin_memory().numpy()
+                             for x in (u, v, w, vis, wt)))
+    got = list(W.image_stream(batches, spec, kern))
+    assert len(got) == 3
+    for bt, (img, d) in zip(batches, got):
+        ref, dref = W.image(bt[0], bt[1], bt[2], None, bt[3], bt[4], spec, kern)
+        assert img.pixels.tobytes() == ref.pixels.tobytes()
+        assert img.imag_residual_norm == ref.imag_residual_norm
+        assert d["grid_updates"] == dref["grid_updates"]

@@ -1,6 +1,7 @@
 """BASELINE config 3 (north star): 100M LOFAR-like track records,
 4096x4096x64, Gaussian support 7, FP64. Single process (1 GPU) or torchrun
-(v-slab over N GPUs). Prints kernel/step timings and a linearity check
+(v-slab over N GPUs). cfg4 (SKA-scale) is the same driver with
+--n 1000000000 --nu 16384 --nw 32 --cell 1e-5 on 4-8 GPUs. Prints kernel/step timings and a linearity check
 (image(a + b) == image(a) + image(b) within FP64 roundoff), a property that
 holds at any size."""
 
@@ -31,6 +32,8 @@ def main():
     ap.add_argument("--nw", type=int, default=64)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--cell", type=float, default=1e-4)
+    ap.add_argument("--label", default="cfg3 LOFAR-like tracks")
     a = ap.parse_args()
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -40,7 +43,7 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
         from paper_2504_00959_b200.distributed import image_distributed
-    cell = 1e-4
+    cell = a.cell
     spec = W.GridSpec(a.nu, a.nu, a.nw, cell, w_max_native=1000.0)
     kern = W.KernelSpec.gaussian(3, 1.0)
     per = a.n // ws
@@ -70,7 +73,7 @@ def main():
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    out = {"config": "cfg3 LOFAR-like tracks", "records": a.n, "grid": [a.nu, a.nu, a.nw],
+    out = {"config": a.label, "records": a.n, "grid": [a.nu, a.nu, a.nw],
            "n_gpus": ws, "ms_per_step": round(ms, 3), "mvis_s": round(a.n / ms / 1e3, 1),
            "grid_updates": d["grid_updates"], "generate_s": round(gen_s, 2)}
     if ws == 1:
