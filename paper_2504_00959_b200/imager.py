@@ -328,6 +328,7 @@ def image_stream(batches, spec, kern, device: int = 0):
     imgs = [None, None]            # device images per slot
     done = [None, None]            # compute-finished event per slot
     read = [None, None]            # image-copied-out event per slot
+    pinned = [None, None]          # page-locked image staging per slot
 
     def upload(i, b):
         u, v, w, vis, wt = b
@@ -338,10 +339,13 @@ def image_stream(batches, spec, kern, device: int = 0):
                 (np.asarray(u, np.float64), np.asarray(v, np.float64), np.asarray(w, np.float64),
                  vis.view(np.float32), wt)]
         slot = i % 2
+        if sets[slot] is None or any(d.shape != h.shape for d, h in zip(sets[slot], host)):
+            sets[slot] = [torch.empty(h.shape, dtype=h.dtype, device=dev) for h in host]
         with torch.cuda.stream(s_in):
             if done[slot] is not None:
                 s_in.wait_event(done[slot])      # the slot's previous batch has been imaged
-            sets[slot] = [h.to(dev, non_blocking=True) for h in host]
+            for d, h in zip(sets[slot], host):
+                d.copy_(h, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(s_in)
         return ev, vis.shape[1], host
@@ -373,7 +377,11 @@ def image_stream(batches, spec, kern, device: int = 0):
                                          _ptr(imgs[slot]), C.byref(d)))
         done[slot] = torch.cuda.Event()
         done[slot].record(compute)
-        out = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, pin_memory=True)
+        # page-locked staging ring (allocated once: pinning is slow); the
+        # yielded image is a private copy made while the device works on
+        if pinned[slot] is None:
+            pinned[slot] = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, pin_memory=True)
+        out = pinned[slot]
         with torch.cuda.stream(s_out):
             s_out.wait_event(done[slot])
             out.copy_(imgs[slot], non_blocking=True)
@@ -383,13 +391,23 @@ def image_stream(batches, spec, kern, device: int = 0):
         if pending is not None:
             pev, pout, pd = pending
             pev.synchronize()
-            yield FinalImage(spec, pout.numpy(), pd.imag_residual_norm, pd.real_norm), diag_dict(pd)
+            yield (FinalImage(spec, _host_copy(pout), pd.imag_residual_norm, pd.real_norm),
+                   diag_dict(pd))
         pending = (oev, out, d)
         staged = staged_next
         i += 1
     pev, pout, pd = pending
     pev.synchronize()
-    yield FinalImage(spec, pout.numpy(), pd.imag_residual_norm, pd.real_norm), diag_dict(pd)
+    yield FinalImage(spec, _host_copy(pout), pd.imag_residual_norm, pd.real_norm), diag_dict(pd)
+
+
+def _host_copy(t: torch.Tensor) -> np.ndarray:
+    """Private host copy of a page-locked staging tensor (torch's parallel
+    copy: the single-threaded numpy copy of a 32 MB image costs more than
+    the device pipeline it overlaps)."""
+    out = torch.empty(t.shape, dtype=t.dtype)
+    out.copy_(t)
+    return out.numpy()
 
 
 def diag_dict(d: L.WsbDiag) -> dict:
