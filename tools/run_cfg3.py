@@ -1,7 +1,7 @@
 """BASELINE config 3 (north star): 100M LOFAR-like track records,
 4096x4096x64, Gaussian support 7, FP64. Single process (1 GPU) or torchrun
 (v-slab over N GPUs). cfg4 (SKA-scale) is the same driver with
---records 1000000000 --nu 16384 --nw 32 --cell 1e-5 on 4-8 GPUs. Prints kernel/step timings and a linearity check
+--records 1000000000 --mesh 16384 --planes 32 --cell 1e-5 on 4-8 GPUs. Prints kernel/step timings and a linearity check
 (image(a + b) == image(a) + image(b) within FP64 roundoff), a property that
 holds at any size."""
 
@@ -28,8 +28,8 @@ STAGES = ("prepare", "route", "exchange", "grid", "bucket", "sweep", "rows", "co
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--records", dest="n", type=int, default=100_000_000)
-    ap.add_argument("--nu", type=int, default=4096)
-    ap.add_argument("--nw", type=int, default=64)
+    ap.add_argument("--mesh", dest="nu", type=int, default=4096)
+    ap.add_argument("--planes", dest="nw", type=int, default=64)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--cell", type=float, default=1e-4)
