@@ -278,6 +278,8 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
         starts = [partition_1d(spec.n_v, R, d)[0] for d in range(R)] + [spec.n_v]
     slabs = [(starts[d], starts[d + 1] - starts[d]) for d in range(R)]
     srec, spl, counts = be.route(rec, plane, spec, S, R, starts)
+    n_local = int(rec.shape[0])
+    del rec, plane                  # large meshes: keep the peak footprint down
     st.mark("route")
     c_send = torch.tensor(counts, dtype=torch.int64, device=dev)
     c_recv = torch.empty(R, dtype=torch.int64, device=dev)
@@ -288,6 +290,7 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     rpl = torch.empty(m, dtype=torch.int32, device=dev)
     _a2a(rrec, srec.contiguous(), recv_counts, counts, group)
     _a2a(rpl, spl.contiguous(), recv_counts, counts, group)
+    del srec, spl
     st.mark("exchange")
 
     # 2. grid this rank's slab ----------------------------------------------
@@ -303,6 +306,8 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     g0, ng = cols[r]
     dest_pairs = [ng_d for _, ng_d in cols]
     src_rows = [vc_s for _, vc_s in slabs]
+    # plane ranges of at most ~4 GiB of row-pass output each (cfg4 meshes)
+    n_ranges = max(n_ranges, -(-spec.n_w * spec.n_u * vc * 16 // (4 << 30)))
     if transpose == "auto":
         transpose = "push" if (hasattr(be, "push_blocks") and dev.type == "cuda"
                                and _symm_available()) else "nccl"
@@ -319,7 +324,6 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
         ps = _side_stream(dev)
         hdl.barrier(channel=0)          # every rank has finished reading the previous image
         ps.wait_stream(cur)
-        keep = []
         for k0, k1 in reversed(plane_ranges(spec.n_w, n_ranges)):
             nk = k1 - k0
             grid_p = be.fft_rows(grid_s, spec, vc, dest_pairs, k0, k1)  # [dest][plane][g][row][G]
@@ -336,12 +340,12 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
             ev.record(cur)
             ps.wait_event(ev)
             be.push_blocks(srcs, dsts, nbytes, ps)
-            keep.append(grid_p)
+            grid_p.record_stream(ps)    # freed for reuse once its push has run
+            del grid_p
         st.mark("rows")
         del grid_s
         cur.wait_stream(ps)
         hdl.barrier(channel=0)          # all slabs' columns have landed
-        keep.clear()
         tgrid = buf[: 2 * spec.n_w * ng * G * spec.n_v]
         strip, partials = be.fft_cols_stack(tgrid, spec, src_rows, g0, ng, 0, spec.n_w)
         st.mark("cols")
@@ -394,7 +398,7 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     dist.all_gather(strips, pad, group=group)
     dist.all_gather(parts, ppad, group=group)
     st.mark("gather")
-    diag = {"grid_updates": int(upd.item()), "records_local": int(rec.shape[0]),
+    diag = {"grid_updates": int(upd.item()), "records_local": n_local,
             "records_slab": m, "exchange_bytes": int(sum(counts) - counts[r]) * 36,
             "slab_starts": starts}
     if timings is not None:
