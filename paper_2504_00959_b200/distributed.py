@@ -159,7 +159,8 @@ class _Stages:
         return {b[0]: a[1].elapsed_time(b[1]) for a, b in zip(self.marks, self.marks[1:])}
 
 
-def balanced_slab_starts(row_counts, n_ranks: int, row_weight: float = 10_000.0):
+def balanced_slab_starts(row_counts, n_ranks: int, row_weight: float = 10_000.0,
+                         max_rows: int | None = None):
     """Slab rows with equal estimated work instead of partition_1d's equal
     rows. A slab's cost is modelled as records + row_weight * rows (the
     gridder scales with the records, the row pass and the sweep's row
@@ -181,6 +182,15 @@ def balanced_slab_starts(row_counts, n_ranks: int, row_weight: float = 10_000.0)
         r = min(r, n_v - (n_ranks - d))
         starts.append(r)
     starts.append(n_v)
+    # memory bound: no slab taller than max_rows (default 1.5x the equal share;
+    # the slab's grid and transforms scale with its rows)
+    if max_rows is None:
+        max_rows = -(-3 * n_v // (2 * n_ranks))
+    max_rows = max(max_rows, -(-n_v // n_ranks))
+    for d in range(1, n_ranks):
+        starts[d] = min(starts[d], starts[d - 1] + max_rows)
+    for d in range(n_ranks - 1, 0, -1):
+        starts[d] = max(starts[d], starts[d + 1] - max_rows)
     return starts
 
 

@@ -83,7 +83,7 @@ def test_balanced_slab_starts():
     from paper_2504_00959_b200.distributed import balanced_slab_starts
     h = np.zeros(64, np.int64)
     h[28:36] = 1000                       # records piled in the central rows
-    st = balanced_slab_starts(h, 4, row_weight=0.0)
+    st = balanced_slab_starts(h, 4, row_weight=0.0, max_rows=64)
     assert st[0] == 0 and st[-1] == 64 and all(b > a for a, b in zip(st, st[1:]))
     # the central block is cut into four (nearly) equal parts
     per = [h[a:b].sum() for a, b in zip(st, st[1:])]
@@ -93,3 +93,6 @@ def test_balanced_slab_starts():
     # more ranks than loaded rows still gives non-empty slabs
     st = balanced_slab_starts(np.eye(1, 8, 7, dtype=np.int64)[0] * 10, 8, row_weight=0.0)
     assert st == list(range(9))
+    # the memory cap: no slab above 1.5x the equal share by default
+    st = balanced_slab_starts(h, 4, row_weight=0.0)
+    assert max(b - a for a, b in zip(st, st[1:])) <= 24 and st[-1] == 64
