@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--cell", type=float, default=1e-4)
+    ap.add_argument("--transpose", default="auto", choices=["auto", "push", "peer", "nccl"])
     ap.add_argument("--label", default="cfg3 LOFAR-like tracks")
     a = ap.parse_args()
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -55,7 +56,7 @@ def main():
 
     def run(vv=vis):
         if ws > 1:
-            img, d = image_distributed(u, v, w, vv, wt, spec, kern, to_host=False)
+            img, d = image_distributed(u, v, w, vv, wt, spec, kern, to_host=False, transpose=a.transpose)
             return (img.pixels if img is not None else None), d
         return W.image_device(u, v, w, vv, wt, spec, kern)
 
@@ -82,7 +83,8 @@ def main():
         out["kernel_ms"] = [round(x, 3) for x in kms]
     else:
         tm = {}
-        image_distributed(u, v, w, vis, wt, spec, kern, to_host=False, timings=tm)
+        image_distributed(u, v, w, vis, wt, spec, kern, to_host=False, timings=tm,
+                          transpose=a.transpose)
         st = torch.tensor([tm.get(k, 0.0) for k in STAGES], device=dev, dtype=torch.float64)
         dist.all_reduce(st, op=dist.ReduceOp.MAX)
         out["stage_ms_max_over_ranks"] = {k: round(float(x), 3) for k, x in zip(STAGES, st.tolist())}
