@@ -283,7 +283,16 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     if balance and R > 1:
         hist = be.row_histogram(rec, spec)
         dist.all_reduce(hist, group=group)
-        starts = balanced_slab_starts(hist.cpu().numpy(), R, row_weight)
+        # memory bound on a slab's rows: its strip grid and row-pass output
+        # (2 x n_w x n_u complex128 per row) within ~60% of the free memory
+        # of the tightest rank
+        max_rows = None
+        if dev.type == "cuda":
+            free = torch.tensor([torch.cuda.mem_get_info(dev)[0]], dtype=torch.float64, device=dev)
+            dist.all_reduce(free, op=dist.ReduceOp.MIN, group=group)
+            max_rows = int(0.6 * float(free.item()) / (2 * spec.n_w * spec.n_u * 16))
+        starts = balanced_slab_starts(hist.cpu().numpy(), R, row_weight,
+                                      max_rows=min(spec.n_v, max_rows) if max_rows else spec.n_v)
     else:
         starts = [partition_1d(spec.n_v, R, d)[0] for d in range(R)] + [spec.n_v]
     slabs = [(starts[d], starts[d + 1] - starts[d]) for d in range(R)]
