@@ -204,6 +204,7 @@ def col_split(n_v: int) -> int:
 
 
 _SYMM: dict = {}
+_ROW_CAP: dict = {}
 
 
 def _symm_available() -> bool:
@@ -288,9 +289,13 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
         # of the tightest rank
         max_rows = None
         if dev.type == "cuda":
-            free = torch.tensor([torch.cuda.mem_get_info(dev)[0]], dtype=torch.float64, device=dev)
-            dist.all_reduce(free, op=dist.ReduceOp.MIN, group=group)
-            max_rows = int(0.6 * float(free.item()) / (2 * spec.n_w * spec.n_u * 16))
+            key = (id(group), dev.index, spec.n_u, spec.n_v, spec.n_w, R)
+            if key not in _ROW_CAP:     # once per mesh: a collective + host sync
+                free = torch.tensor([torch.cuda.mem_get_info(dev)[0]], dtype=torch.float64,
+                                    device=dev)
+                dist.all_reduce(free, op=dist.ReduceOp.MIN, group=group)
+                _ROW_CAP[key] = int(0.6 * float(free.item()) / (2 * spec.n_w * spec.n_u * 16))
+            max_rows = _ROW_CAP[key]
         starts = balanced_slab_starts(hist.cpu().numpy(), R, row_weight,
                                       max_rows=min(spec.n_v, max_rows) if max_rows else spec.n_v)
     else:
