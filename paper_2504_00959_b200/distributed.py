@@ -333,7 +333,10 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     # plane ranges of at most ~4 GiB of row-pass output each (cfg4 meshes)
     n_ranges = max(n_ranges, -(-spec.n_w * spec.n_u * vc * 16 // (4 << 30)))
     if transpose == "auto":
-        transpose = "push" if (hasattr(be, "push_blocks") and dev.type == "cuda"
+        # measured: the NVLink push beats NCCL's all-to-all on 2 GPUs (cfg2
+        # 5.98 vs 6.60 ms/step); on 4 the pushes' CTAs slow the concurrent row
+        # pass more than NCCL does (cfg3 27.7 vs 23.0 ms/step)
+        transpose = "push" if (R == 2 and hasattr(be, "push_blocks") and dev.type == "cuda"
                                and _symm_available()) else "nccl"
     if transpose == "push":
         # row pass into local destination-major plane ranges; each range is
