@@ -77,7 +77,7 @@ typedef struct {
 
 typedef struct {
     int32_t device;        /* CUDA ordinal */
-    int32_t precision;     /* 64 (FP64 path); 32 reserved */
+    int32_t precision;     /* 64 (FP64 path) or 32 (FP32 path, see wsb_ctx_set_precision) */
     int32_t deterministic; /* accepted for API parity; results are always deterministic */
     int32_t reserved;
 } wsb_exec;
@@ -102,6 +102,11 @@ int wsb_ctx_create(int32_t device, wsb_ctx **out);
 int wsb_ctx_destroy(wsb_ctx *ctx);
 /* Use `stream` (a cudaStream_t; NULL = legacy default) for later calls. */
 int wsb_ctx_set_stream(wsb_ctx *ctx, void *stream);
+/* Grid precision of wsb_image_device on this context: 64 (complex128, the
+ * default) or 32 (the FP32 path: complex64 grid and transforms; prepare,
+ * weights, accumulation, phase screen and plane stack stay FP64; within 1e-5
+ * relative L2 of the reference image). wsb_image takes it from exec. */
+int wsb_ctx_set_precision(wsb_ctx *ctx, int32_t precision);
 /* Release cached device workspace. */
 int wsb_ctx_trim(wsb_ctx *ctx);
 

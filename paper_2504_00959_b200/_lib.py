@@ -29,7 +29,7 @@ EXPORTS = (
     "wsb_ctx_set_stream", "wsb_ctx_trim", "wsb_image", "wsb_image_device", "wsb_prepare",
     "wsb_route_count", "wsb_route_pack", "wsb_grid_slab", "wsb_fft_rows", "wsb_fft_cols_stack",
     "wsb_grid_unpack", "wsb_tiles_debug", "wsb_last_timings", "wsb_row_histogram",
-    "wsb_fft_rows_peer", "wsb_push_blocks",
+    "wsb_fft_rows_peer", "wsb_push_blocks", "wsb_ctx_set_precision",
 )
 
 
@@ -93,6 +93,7 @@ def lib() -> C.CDLL:
         "wsb_fft_rows": (C.c_int, [p, G, i32, p, p, i32, i32, i32, p]),
         "wsb_fft_rows_peer": (C.c_int, [p, G, i32, p, i32, i32, i32, p, p]),
         "wsb_push_blocks": (C.c_int, [p, i32, p, p, p]),
+        "wsb_ctx_set_precision": (C.c_int, [p, i32]),
         "wsb_fft_cols_stack": (C.c_int, [p, G, i32, p, i32, i32, i32, i32, p, p, p]),
         "wsb_grid_unpack": (C.c_int, [p, G, i32, i32, p, p]),
         "wsb_tiles_debug": (C.c_int, [p, p, p, p, p]),

@@ -55,7 +55,7 @@ static int validate_grid(const wsb_grid *g) {
         return fail(WSB_EINVAL, "field of view too wide: corner pixels leave the unit disc");
     if (g->w_min_native > g->w_max_native) return fail(WSB_EINVAL, "w_min_native must be <= w_max_native");
     if (g->n_u > WSB_MAX_FFT_N || g->n_v > WSB_MAX_FFT_N)
-        return fail(WSB_EUNSUPPORTED, "grids above 4096 per axis need the out-of-core FFT (not in this build)");
+        return fail(WSB_EUNSUPPORTED, "grids above 16384 per axis are not supported in this build");
     return WSB_OK;
 }
 
@@ -185,12 +185,19 @@ int wsb_ctx_destroy(wsb_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto &b : ctx->bufs)
         if (b.ptr) cudaFree(b.ptr);
-    for (int i = 0; i < 48; ++i)
+    for (int i = 0; i < 96; ++i)
         if (ctx->twiddle[i]) cudaFree(ctx->twiddle[i]);
     if (ctx->timing.created)
         for (int i = 0; i < 8; ++i) cudaEventDestroy(ctx->timing.ev[i]);
     if (ctx->flag_host) cudaFreeHost(ctx->flag_host);
     delete ctx;
+    return WSB_OK;
+}
+
+int wsb_ctx_set_precision(wsb_ctx *ctx, int32_t precision) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    if (precision != 64 && precision != 32) return fail(WSB_EINVAL, "precision must be 64 or 32");
+    ctx->precision = precision;
     return WSB_OK;
 }
 
@@ -376,24 +383,27 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
     ctx->launches = 0;
     cudaEvent_t *ev = ctx->timing.ev;
     const int n_u = grid->n_u, n_v = grid->n_v, n_w = grid->n_w;
-    double *rec, *gs, *gp, *partials;
+    double *rec, *partials;
+    void *gs, *gp;
+    const int prec = ctx->precision;
+    const size_t esz = prec == 32 ? 8 : 16;   // complex64 / complex128 grid cells
     uint32_t *plane;
     unsigned long long *upd;
     const int64_t nn = std::max<int64_t>(n, 1);
     WSB_TRY(ensure(ctx, kSlotRec, 32 * (size_t)nn, (void **)&rec));
     WSB_TRY(ensure(ctx, kSlotPlane, 4 * (size_t)nn, (void **)&plane));
     // strip layout (gridder output) and P layout (row-pass output)
-    WSB_TRY(ensure(ctx, kSlotGrid, (size_t)16 * n_w * ceil_div(n_u, 32) * 32 * n_v, (void **)&gs));
-    WSB_TRY(ensure(ctx, kSlotGridP, (size_t)16 * n_w * n_u * n_v, (void **)&gp));
+    WSB_TRY(ensure(ctx, kSlotGrid, esz * n_w * ceil_div(n_u, 32) * 32 * n_v, &gs));
+    WSB_TRY(ensure(ctx, kSlotGridP, esz * n_w * n_u * n_v, &gp));
     // norm partials [residue][column][2] (residues: columns longer than 4096 are split)
     const int sp = std::max(1, n_v >> kMaxOnChipLog);
     WSB_TRY(ensure(ctx, kSlotStrip, sizeof(double) * (2 * (size_t)n_u * sp + 4), (void **)&partials));
     WSB_TRY(ensure(ctx, kSlotU64, 64, (void **)&upd));
-    const double *tw;   // tables built outside the timed region
-    WSB_TRY(twiddles(ctx, std::min(n_u, 1 << kMaxOnChipLog), 4, &tw));   // row plan (radix 16)
-    WSB_TRY(twiddles(ctx, std::min(n_v, 1 << kMaxOnChipLog), 3, &tw));   // column plan (radix 8)
-    if (n_u > (1 << kMaxOnChipLog)) WSB_TRY(twiddles(ctx, n_u, 0, &tw));
-    if (n_v > (1 << kMaxOnChipLog)) WSB_TRY(twiddles(ctx, n_v, 0, &tw));
+    const void *tw;   // tables built outside the timed region
+    WSB_TRY(twiddles(ctx, std::min(n_u, 1 << kMaxOnChipLog), 4, &tw, prec));   // rows (radix 16)
+    WSB_TRY(twiddles(ctx, std::min(n_v, 1 << kMaxOnChipLog), 3, &tw, prec));   // columns (radix 8)
+    if (n_u > (1 << kMaxOnChipLog)) WSB_TRY(twiddles(ctx, n_u, 0, &tw, prec));
+    if (n_v > (1 << kMaxOnChipLog)) WSB_TRY(twiddles(ctx, n_v, 0, &tw, prec));
 
     WSB_CUDA_TRY(cudaEventRecord(ev[0], ctx->stream));
     WSB_CUDA_TRY(cudaMemsetAsync(upd, 0, sizeof(unsigned long long), ctx->stream));
@@ -403,12 +413,12 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
     WSB_TRY(bucket_rows(ctx, grid, kern->half_support, 0, n_v, rec, plane, n, &bk));
     const int64_t n_entries = bk.n_entries;
     WSB_CUDA_TRY(cudaEventRecord(ev[2], ctx->stream));
-    WSB_TRY(grid_sweep(ctx, grid, kern, 0, n_v, rec, bk, gs, upd));
+    WSB_TRY(grid_sweep(ctx, grid, kern, 0, n_v, rec, bk, gs, upd, prec));
     WSB_CUDA_TRY(cudaEventRecord(ev[3], ctx->stream));
-    WSB_TRY(fft_rows(ctx, grid, n_v, gs, gp, 0, n_w, 1, nullptr));
+    WSB_TRY(fft_rows(ctx, grid, n_v, gs, gp, 0, n_w, 1, nullptr, nullptr, prec));
     WSB_CUDA_TRY(cudaEventRecord(ev[4], ctx->stream));
     const int32_t rows[1] = {n_v};
-    WSB_TRY(fft_cols_stack(ctx, grid, 1, rows, 0, n_u / kG, 0, n_w, gp, image_out, partials));
+    WSB_TRY(fft_cols_stack(ctx, grid, 1, rows, 0, n_u / kG, 0, n_w, gp, image_out, partials, prec));
     WSB_CUDA_TRY(cudaEventRecord(ev[5], ctx->stream));
     const int nb = n_u * sp;  // one norm partial per image column (and residue)
     k_sum_partials<<<1, 256, 0, ctx->stream>>>(partials, nb, partials + 2 * (size_t)nb);
@@ -454,11 +464,13 @@ int wsb_image(const wsb_grid *grid, const wsb_kernel *kern, const wsb_exec *exec
     if ((n > 0 && (!u || !v || !w || !vis || !weight)) || !image_out)
         return fail(WSB_EINVAL, "NULL buffer");
     const int dev = exec ? exec->device : 0;
-    if (exec && exec->precision != 64) return fail(WSB_EUNSUPPORTED, "only the FP64 path is built");
+    const int prec = exec ? exec->precision : 64;
+    if (prec != 64 && prec != 32) return fail(WSB_EINVAL, "precision must be 64 or 32");
     if (dev < 0 || dev >= 64) return fail(WSB_EINVAL, "device ordinal out of range");
     std::lock_guard<std::mutex> lock(g_host_mu);
     if (!g_host_ctx[dev]) WSB_TRY(wsb_ctx_create(dev, &g_host_ctx[dev]));
     wsb_ctx *ctx = g_host_ctx[dev];
+    ctx->precision = prec;
     WSB_TRY(set_device(ctx));
     const int64_t nn = std::max<int64_t>(n, 1);
     auto rnd = [](size_t b) { return (b + 255) & ~(size_t)255; };

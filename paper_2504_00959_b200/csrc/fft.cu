@@ -32,6 +32,20 @@ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -(a.y * b.y)), fma(a.x, b.y, a.y * b.x));
 }
+// FP32 path (transforms in complex64; coordinates, weights, phases and the
+// plane stack stay FP64)
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -(a.y * b.y)), fmaf(a.x, b.y, a.y * b.x));
+}
+template <class V> __device__ __forceinline__ V cx(double x, double y);
+template <> __device__ __forceinline__ double2 cx<double2>(double x, double y) { return make_double2(x, y); }
+template <> __device__ __forceinline__ float2 cx<float2>(double x, double y) {
+    return make_float2((float)x, (float)y);
+}
+__device__ __forceinline__ double2 to_d2(double2 z) { return z; }
+__device__ __forceinline__ double2 to_d2(float2 z) { return make_double2(z.x, z.y); }
 
 // (cos(pi x), sin(pi x)) for |x| < 2^30: x = t/2 + r with t = rint(2x),
 // |r| <= 1/4, then Taylor polynomials of sin(pi r)/r (degree 16) and
@@ -76,13 +90,15 @@ __constant__ double kRoot16[8][2] = {{1.0, 0.0},
                                      {-0.70710678118654752440, 0.70710678118654752440},
                                      {-0.92387953251128673848, 0.38268343236508977173}};
 
-__device__ __forceinline__ double2 root16(int u) { return make_double2(kRoot16[u][0], kRoot16[u][1]); }
+template <class V>
+__device__ __forceinline__ V root16(int u) { return cx<V>(kRoot16[u][0], kRoot16[u][1]); }
 
 // a * exp(+2 pi i u/16)
-__device__ __forceinline__ double2 rot16(double2 a, int u) {
+template <class V>
+__device__ __forceinline__ V rot16(V a, int u) {
     if (u == 0) return a;
-    if (u == 4) return make_double2(-a.y, a.x);
-    return cmul(a, root16(u));
+    if (u == 4) { V r; r.x = -a.y; r.y = a.x; return r; }
+    return cmul(a, root16<V>(u));
 }
 
 constexpr int brev(int i, int R) {
@@ -96,12 +112,12 @@ constexpr int brev(int i, int R) {
 
 // Everything below is resolved at compile time so the values stay in
 // registers (a runtime index would push the array to local memory).
-template <int R, int I>
-__device__ __forceinline__ void brev_swap(double2 *y) {
+template <int R, int I, class V>
+__device__ __forceinline__ void brev_swap(V *y) {
     if constexpr (I < R) {
         constexpr int J = brev(I, R);
         if constexpr (J > I) {
-            const double2 t = y[I];
+            const V t = y[I];
             y[I] = y[J];
             y[J] = t;
         }
@@ -109,12 +125,12 @@ __device__ __forceinline__ void brev_swap(double2 *y) {
     }
 }
 
-template <int R, int LEN, int I, int K>
-__device__ __forceinline__ void dit_butterflies(double2 *y) {
+template <int R, int LEN, int I, int K, class V>
+__device__ __forceinline__ void dit_butterflies(V *y) {
     if constexpr (I < R) {
         if constexpr (K < LEN / 2) {
-            const double2 t = rot16(y[I + K + LEN / 2], K * (16 / LEN));
-            const double2 a = y[I + K];
+            const V t = rot16(y[I + K + LEN / 2], K * (16 / LEN));
+            const V a = y[I + K];
             y[I + K] = cadd(a, t);
             y[I + K + LEN / 2] = csub(a, t);
             dit_butterflies<R, LEN, I, K + 1>(y);
@@ -124,8 +140,8 @@ __device__ __forceinline__ void dit_butterflies(double2 *y) {
     }
 }
 
-template <int R, int LEN>
-__device__ __forceinline__ void dit_stages(double2 *y) {
+template <int R, int LEN, class V>
+__device__ __forceinline__ void dit_stages(V *y) {
     if constexpr (LEN <= R) {
         dit_butterflies<R, LEN, 0, 0>(y);
         dit_stages<R, LEN * 2>(y);
@@ -133,8 +149,8 @@ __device__ __forceinline__ void dit_stages(double2 *y) {
 }
 
 // In-register inverse DFT of size R (<= 16), e^{+2 pi i}, natural order out.
-template <int R>
-__device__ __forceinline__ void dft_inv(double2 *y) {
+template <int R, class V>
+__device__ __forceinline__ void dft_inv(V *y) {
     brev_swap<R, 0>(y);
     dit_stages<R, 2>(y);
 }
@@ -176,8 +192,8 @@ __device__ __forceinline__ void seq_of(int b, int &seq, int &j) {
 // A pass reads x[j + r N/R], multiplies by the twiddles of its stage,
 // applies the radix-R DFT and writes y[(j/ns) ns R + j%ns + r ns].
 // ---------------------------------------------------------------------------
-template <int LOGN, int RL, int E, int T, int IL = 1, class LD>
-__device__ __forceinline__ void pass_load(double2 (&v)[E], LD ld) {
+template <int LOGN, int RL, int E, int T, int IL = 1, class V, class LD>
+__device__ __forceinline__ void pass_load(V (&v)[E], LD ld) {
     constexpr int R = 1 << RL, NB = E / R, M = (1 << LOGN) / R;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
@@ -203,22 +219,21 @@ constexpr int tw_offset(int logn, int rlmax, int done) {
     return off;
 }
 
-template <int LOGN, int RL, int E, int T, int IL = 1>
-__device__ __forceinline__ void pass_compute(int ns, const double2 *__restrict__ tw,
-                                             double2 (&v)[E]) {
+template <int LOGN, int RL, int E, int T, int IL = 1, class V>
+__device__ __forceinline__ void pass_compute(int ns, const V *__restrict__ tw, V (&v)[E]) {
     constexpr int N = 1 << LOGN, R = 1 << RL, NB = E / R, M = N / R;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
         int seq, j;
         seq_of<IL, M>(threadIdx.x + k * T, seq, j);
-        double2 y[R];
+        V y[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) y[r] = v[k * R + r];
         if (ns > 1) {
             // one table load per butterfly; the other powers by a product
             // tree w^r = w^(r/2) w^(r - r/2) (depth log2 R, a few ulp): the
             // loads, not the FP64 pipe, are what the passes queue on
-            double2 wp[R];
+            V wp[R];
             wp[1] = __ldg(&tw[j % ns]);
 #pragma unroll
             for (int r = 2; r < R; ++r) wp[r] = cmul(wp[r / 2], wp[r - r / 2]);
@@ -231,8 +246,8 @@ __device__ __forceinline__ void pass_compute(int ns, const double2 *__restrict__
     }
 }
 
-template <int LOGN, int RL, int E, int T, int IL = 1, class ST>
-__device__ __forceinline__ void pass_store(int ns, const double2 (&v)[E], ST st) {
+template <int LOGN, int RL, int E, int T, int IL = 1, class V, class ST>
+__device__ __forceinline__ void pass_store(int ns, const V (&v)[E], ST st) {
     constexpr int R = 1 << RL, NB = E / R, M = (1 << LOGN) / R;
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
@@ -255,8 +270,8 @@ struct Plan {
 // Passes 1..last-1 in shared memory (in place), then the last pass's loads
 // and compute: its results stay in v, at (seq, j + r*N/R) of butterfly b
 // (mapped with ILL, the interleave of the last pass).
-template <int LOGN, int RLMAX, int E, int T, int DONE, int ILL = 1>
-__device__ __forceinline__ void smem_passes(double2 *s, const double2 *tw, double2 (&v)[E]) {
+template <int LOGN, int RLMAX, int E, int T, int DONE, int ILL = 1, class V>
+__device__ __forceinline__ void smem_passes(V *s, const V *tw, V (&v)[E]) {
     using P = Plan<LOGN, RLMAX, DONE>;
     constexpr int STRIDE = Seq<LOGN>::STRIDE;
     constexpr int IL = P::LAST ? ILL : 1;
@@ -265,7 +280,7 @@ __device__ __forceinline__ void smem_passes(double2 *s, const double2 *tw, doubl
     if constexpr (!P::LAST) __syncthreads();
     pass_compute<LOGN, P::RL, E, T, IL>(1 << DONE, tw + tw_offset(LOGN, RLMAX, DONE), v);
     if constexpr (!P::LAST) {
-        auto st = [&](int seq, int idx, double2 z) { s[seq * STRIDE + pidx(idx)] = z; };
+        auto st = [&](int seq, int idx, V z) { s[seq * STRIDE + pidx(idx)] = z; };
         pass_store<LOGN, P::RL, E, T>(1 << DONE, v, st);
         __syncthreads();
         smem_passes<LOGN, RLMAX, E, T, DONE + P::RL, ILL>(s, tw, v);
@@ -299,18 +314,20 @@ constexpr int kRowRL = 4;
 // block of a local send buffer or -- the fused transpose -- this source's
 // block of rank d's column-pass input in peer memory (NVLink stores).
 struct RowDest {
-    double2 *ptr[8];
+    void *ptr[8];
     int plane0;
     int g0[9];   // first group of each destination, g0[n_dest] = n_u/G, unused = INT_MAX
 };
 
 // z * exp(2 pi i q / 4), exact
-__device__ __forceinline__ double2 rot_quarter(double2 z, int q) {
+template <class V>
+__device__ __forceinline__ V rot_quarter(V z, int q) {
+    V r;
     switch (q & 3) {
         case 0: return z;
-        case 1: return make_double2(-z.y, z.x);
-        case 2: return make_double2(-z.x, -z.y);
-        default: return make_double2(z.y, -z.x);
+        case 1: r.x = -z.y; r.y = z.x; return r;
+        case 2: r.x = -z.x; r.y = -z.y; return r;
+        default: r.x = z.y; r.y = -z.x; return r;
     }
 }
 
@@ -320,14 +337,14 @@ __device__ __forceinline__ double2 rot_quarter(double2 z, int q) {
 //   u_e[n] = W_N^(n e) * sum_s x[n + s M] W_SP^(s e),   W_K = exp(2 pi i / K),
 // so every CTA reads the whole row (SP-fold reads) and runs the on-chip
 // M-point transform. twN: exp(2 pi i m / N), m < N.
-template <int SPL>
-__device__ __forceinline__ double2 dif_split(const double2 *x, int stride, int e, int n, int M,
-                                             const double2 *__restrict__ twN) {
+template <int SPL, class V>
+__device__ __forceinline__ V dif_split(const V *x, int stride, int e, int n, int M,
+                                       const V *__restrict__ twN) {
     constexpr int SP = 1 << SPL;
-    double2 u = x[0];
+    V u = x[0];
 #pragma unroll
     for (int s = 1; s < SP; ++s) {
-        const double2 y = rot_quarter(x[(int64_t)s * stride], (4 / SP) * s * e);
+        const V y = rot_quarter(x[(int64_t)s * stride], (4 / SP) * s * e);
         u = cadd(u, y);
     }
     return e ? cmul(u, __ldg(&twN[n * e])) : u;
@@ -337,10 +354,10 @@ __device__ __forceinline__ double2 dif_split(const double2 *x, int stride, int e
 // (32-byte sectors, 16 loads in flight per thread) and the last pass writes
 // its outputs straight back: shared memory only carries the inner exchanges.
 // SPL > 0: rows of N = 2^(LOGN+SPL) points, residue e = blockIdx.z (above).
-template <int LOGN, int SPL = 0>
+template <int LOGN, int SPL, class V>
 __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
-    k_fft_rows(const double2 *__restrict__ in, int n_strips, int n_groups, int v_count,
-               int plane_lo, const double2 *__restrict__ tw, const double2 *__restrict__ twN,
+    k_fft_rows(const V *__restrict__ in, int n_strips, int n_groups, int v_count,
+               int plane_lo, const V *__restrict__ tw, const V *__restrict__ twN,
                RowDest dst) {
     constexpr int N = 1 << LOGN;          // on-chip transform length M
     constexpr int SP = 1 << SPL;
@@ -348,14 +365,15 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
     constexpr int NSEQ = RT * kRowE / N;  // rows per CTA
     constexpr int STRIDE = Seq<LOGN>::STRIDE;
     using P0 = Plan<LOGN, kRowRL, 0>;
-    extern __shared__ __align__(16) double2 s[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V *s = reinterpret_cast<V *>(smem_raw);
     const int j0 = blockIdx.x * NSEQ;
     const int64_t plane = plane_lo + blockIdx.y;
     const int e = SPL ? (int)blockIdx.z : 0;
     // in: strip layout [plane][col/32][row][col%32] (512-byte row runs)
     auto gld = [&](int seq, int col) {
-        if (j0 + seq >= v_count) return make_double2(0.0, 0.0);
-        const double2 *p = in + ((plane * n_strips + col / 32) * v_count + j0 + seq) * 32 + (col % 32);
+        if (j0 + seq >= v_count) return cx<V>(0.0, 0.0);
+        const V *p = in + ((plane * n_strips + col / 32) * v_count + j0 + seq) * 32 + (col % 32);
         if constexpr (SPL == 0) {
             return *p;
         } else {
@@ -365,30 +383,30 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
     };
     // out: P[plane][col/G][row][col%G] per destination (RowDest); with a
     // single destination this is the plain P layout
-    auto gst = [&](int seq, int k, double2 z) {
+    auto gst = [&](int seq, int k, V z) {
         const int col = k * SP + e;
         if (j0 + seq < v_count) {
             const int g = col / kG;
             int lo = 0, hi = dst.g0[1];
-            double2 *base = dst.ptr[0];
+            V *base = reinterpret_cast<V *>(dst.ptr[0]);
 #pragma unroll
             for (int d = 1; d < 8; ++d)
                 if (g >= dst.g0[d]) {
                     lo = dst.g0[d];
                     hi = dst.g0[d + 1];
-                    base = dst.ptr[d];
+                    base = reinterpret_cast<V *>(dst.ptr[d]);
                 }
             base[(((plane - dst.plane0) * (hi - lo) + (g - lo)) * v_count + j0 + seq) * kG +
                  (col % kG)] = z;
         }
     };
-    double2 v[kRowE];
+    V v[kRowE];
     pass_load<LOGN, P0::RL, kRowE, RT>(v, gld);
     pass_compute<LOGN, P0::RL, kRowE, RT>(1, tw, v);
     if constexpr (P0::LAST) {
         pass_store<LOGN, P0::RL, kRowE, RT>(1, v, gst);
     } else {
-        auto sst = [&](int seq, int idx, double2 z) { s[seq * STRIDE + pidx(idx)] = z; };
+        auto sst = [&](int seq, int idx, V z) { s[seq * STRIDE + pidx(idx)] = z; };
         pass_store<LOGN, P0::RL, kRowE, RT>(1, v, sst);
         __syncthreads();
         // last pass with the two rows of a CTA interleaved lane by lane: the
@@ -414,11 +432,11 @@ constexpr int kColE = 8;
 constexpr int kColRL = 3;
 
 struct ColArgs {
-    const double2 *tgrid;   // planes [k0, k1) only
+    const void *tgrid;      // planes [k0, k1) only (complex128, or complex64 on the FP32 path)
     double *strip;          // [n_v][ncols]
     double *partials;       // [ncols][2]
     double2 *run;           // running stack between plane ranges, per thread element
-    const double2 *twN;     // exp(2 pi i m / n_v), m < n_v (split columns only)
+    const void *twN;        // exp(2 pi i m / n_v), m < n_v (split columns only)
     int n_w, n_u, n_v, ncols, g0;
     int k0, k1;             // plane range of this call
     int n_src;
@@ -445,9 +463,9 @@ __device__ __forceinline__ double plane_w(const ColArgs &a, int k) {
 // SPL > 0 (n_v = SP * 4096): residue CTA e = blockIdx.y transforms output
 // rows k SP + e of its columns through the decimation-in-frequency split of
 // dif_split (every CTA reads its whole columns).
-template <int LOGN, int SPL = 0>
+template <int LOGN, int SPL, class V>
 __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
-    k_fft_cols(ColArgs a, const double2 *__restrict__ tw) {
+    k_fft_cols(ColArgs a, const V *__restrict__ tw) {
     constexpr int CT = ColCfg<LOGN>::T;
     constexpr int N = 1 << LOGN;                 // n_v
     constexpr int C = CT * kColE / N;   // columns per CTA
@@ -457,8 +475,12 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     constexpr int R = 1 << RLM;                  // radix of the last pass
     constexpr int M = N / R;
     constexpr int NB = kColE / R;
-    extern __shared__ __align__(16) double2 sbuf[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2 *sbuf = reinterpret_cast<double2 *>(smem_raw);  // finish: pixels + squares
+    V *sv = reinterpret_cast<V *>(smem_raw);                 // transform exchanges
     double2 *zbuf = sbuf + 2 * C * STRIDE;       // z per pixel, [C][N]
+    const V *tg = reinterpret_cast<const V *>(a.tgrid);
+    const V *twN = reinterpret_cast<const V *>(a.twN);
 
     const int c0 = blockIdx.x * C;                 // first local column
     const int nk = a.k1 - a.k0;                    // planes in this call
@@ -498,20 +520,20 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     // The next plane's inputs are prefetched with asynchronous global->shared
     // copies (LDGSTS) into thread-private slots of the otherwise idle second
     // buffer: no registers held across the plane's transform.
-    double2 *pbuf = sbuf + C * STRIDE;
+    V *pbuf = reinterpret_cast<V *>(sbuf + C * STRIDE);
     auto prefetch = [&](int k) {
 #pragma unroll
         for (int i = 0; i < kColE; ++i)
             if (off[i] >= 0)
-                __pipeline_memcpy_async(&pbuf[i * CT + threadIdx.x], &a.tgrid[off[i] + k * pst[i]],
-                                        sizeof(double2));
+                __pipeline_memcpy_async(&pbuf[i * CT + threadIdx.x], &tg[off[i] + k * pst[i]],
+                                        sizeof(V));
         __pipeline_commit();
     };
     // split columns: input k of the on-chip transform combines rows k + s N
-    auto ld_split = [&](int kpl, int seq, int j) -> double2 {
+    auto ld_split = [&](int kpl, int seq, int j) -> V {
         const int lc = c0 + seq;
-        if (lc >= a.ncols) return make_double2(0.0, 0.0);
-        double2 u = make_double2(0.0, 0.0);
+        if (lc >= a.ncols) return cx<V>(0.0, 0.0);
+        V u = cx<V>(0.0, 0.0);
 #pragma unroll
         for (int s = 0; s < SP; ++s) {
             const int row = j + s * N;
@@ -524,9 +546,9 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
                 }
             const int64_t o = (int64_t)nk * a.ncols * r0 + ((int64_t)kpl * a.ncols + lc) * (r1 - r0) +
                               (row - r0);
-            u = cadd(u, rot_quarter(a.tgrid[o], (4 / SP) * s * eres));
+            u = cadd(u, rot_quarter(tg[o], (4 / SP) * s * eres));
         }
-        return eres ? cmul(u, __ldg(&a.twN[j * eres])) : u;
+        return eres ? cmul(u, __ldg(&twN[j * eres])) : u;
     };
     // direction-cosine factor of a pixel (mesh.py:202-208, transform.py:200)
     auto n_of = [&](int cc, int j) {
@@ -548,12 +570,12 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     if constexpr (SPL == 0) prefetch(nk - 1);
 
     for (int kl = nk - 1; kl >= 0; --kl) {
-        double2 v[kColE];
+        V v[kColE];
         if constexpr (SPL == 0) {
             __pipeline_wait_prior(0);
 #pragma unroll
             for (int i = 0; i < kColE; ++i)
-                v[i] = off[i] >= 0 ? pbuf[i * CT + threadIdx.x] : make_double2(0.0, 0.0);
+                v[i] = off[i] >= 0 ? pbuf[i * CT + threadIdx.x] : cx<V>(0.0, 0.0);
             pass_compute<LOGN, P0::RL, kColE, CT>(1, tw, v);
             // v has been consumed from the slots: refill them with the next plane
             if (kl > 0) prefetch(kl - 1);
@@ -564,10 +586,10 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
         }
         if constexpr (!P0::LAST) {
             __syncthreads();  // the previous plane's last pass has read sbuf
-            auto sst = [&](int seq, int idx, double2 z) { sbuf[seq * STRIDE + pidx(idx)] = z; };
+            auto sst = [&](int seq, int idx, V z) { sv[seq * STRIDE + pidx(idx)] = z; };
             pass_store<LOGN, P0::RL, kColE, CT>(1, v, sst);
             __syncthreads();
-            smem_passes<LOGN, RLM, kColE, CT, P0::RL>(sbuf, tw, v);
+            smem_passes<LOGN, RLM, kColE, CT, P0::RL>(sv, tw, v);
         }
         // v[kb*R + r] is output row j + r*M of sequence (column) seq
 #pragma unroll
@@ -577,7 +599,7 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const double2 z = zbuf[seq * N + j + r * M];
-                const double2 p = v[kb * R + r];
+                const double2 p = to_d2(v[kb * R + r]);
                 double2 &q = acc[kb * R + r];
                 const double qx = fma(q.x, z.x, fma(-q.y, z.y, p.x));
                 q.y = fma(q.x, z.y, fma(q.y, z.x, p.y));
@@ -644,7 +666,8 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
 
 // pass-ordered twiddle table of an N-point plan (see tw_offset): entry [t]
 // of the pass with span ns and radix R is exp(2 pi i m / N), m = t N / (ns R)
-__global__ void k_twiddles(double2 *tw, int logn, int rlmax, int size) {
+template <class V>
+__global__ void k_twiddles(V *tw, int logn, int rlmax, int size) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= size) return;
     const int n = 1 << logn;
@@ -664,33 +687,33 @@ __global__ void k_twiddles(double2 *tw, int logn, int rlmax, int size) {
     }
     double sn, cs;
     sincospi(2.0 * (double)m / (double)n, &sn, &cs);
-    tw[e] = make_double2(cs, sn);
+    tw[e] = cx<V>(cs, sn);
 }
 
-template <int LOGN>
-int launch_rows(wsb_ctx *ctx, const double2 *in, int n_strips, int n_groups, int v_count, int plo,
-                int phi, const double2 *tw, const double2 *twN, const RowDest &dst, int spl) {
+template <int LOGN, class V>
+int launch_rows(wsb_ctx *ctx, const V *in, int n_strips, int n_groups, int v_count, int plo,
+                int phi, const V *tw, const V *twN, const RowDest &dst, int spl) {
     constexpr int N = 1 << LOGN;
     constexpr int RT = RowCfg<LOGN>::T;
     constexpr int NSEQ = RT * kRowE / N;
-    const size_t smem = sizeof(double2) * NSEQ * Seq<LOGN>::STRIDE;
+    const size_t smem = sizeof(V) * NSEQ * Seq<LOGN>::STRIDE;
     dim3 grd(ceil_div(v_count, NSEQ), phi - plo, 1 << spl);
     if (spl == 0) {
-        WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 0>,
+        WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 0, V>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_fft_rows<LOGN, 0><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo, tw,
-                                                            twN, dst);
+        k_fft_rows<LOGN, 0, V><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo,
+                                                               tw, twN, dst);
     } else if constexpr (LOGN == 12) {
         if (spl == 1) {
-            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 1>,
+            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 1, V>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_fft_rows<LOGN, 1><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo,
-                                                                tw, twN, dst);
+            k_fft_rows<LOGN, 1, V><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count,
+                                                                   plo, tw, twN, dst);
         } else if (spl == 2) {
-            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 2>,
+            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 2, V>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_fft_rows<LOGN, 2><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo,
-                                                                tw, twN, dst);
+            k_fft_rows<LOGN, 2, V><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count,
+                                                                   plo, tw, twN, dst);
         } else {
             return fail(WSB_EUNSUPPORTED, "row length above 16384");
         }
@@ -702,28 +725,29 @@ int launch_rows(wsb_ctx *ctx, const double2 *in, int n_strips, int n_groups, int
     return WSB_OK;
 }
 
-template <int LOGN>
-int launch_cols(wsb_ctx *ctx, const ColArgs &a, const double2 *tw, int *nblocks, int spl) {
+template <int LOGN, class V>
+int launch_cols(wsb_ctx *ctx, const ColArgs &a, const V *tw, int *nblocks, int spl) {
     static_assert(kG == 1, "the split column loads assume the column-major P layout");
     constexpr int N = 1 << LOGN;
     constexpr int CT = ColCfg<LOGN>::T;
     constexpr int C = CT * kColE / N;
+    // the finish stages complex128 pixels whatever the transform precision
     const size_t smem = sizeof(double2) * (2 * C * Seq<LOGN>::STRIDE + C * N);
     *nblocks = ceil_div(a.ncols, C);
     const dim3 grd(*nblocks, 1 << spl);
     if (spl == 0) {
-        WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN, 0>,
+        WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN, 0, V>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_fft_cols<LOGN, 0><<<grd, CT, smem, ctx->stream>>>(a, tw);
+        k_fft_cols<LOGN, 0, V><<<grd, CT, smem, ctx->stream>>>(a, tw);
     } else if constexpr (LOGN == 12) {
         if (spl == 1) {
-            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN, 1>,
+            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN, 1, V>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_fft_cols<LOGN, 1><<<grd, CT, smem, ctx->stream>>>(a, tw);
+            k_fft_cols<LOGN, 1, V><<<grd, CT, smem, ctx->stream>>>(a, tw);
         } else if (spl == 2) {
-            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN, 2>,
+            WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_cols<LOGN, 2, V>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_fft_cols<LOGN, 2><<<grd, CT, smem, ctx->stream>>>(a, tw);
+            k_fft_cols<LOGN, 2, V><<<grd, CT, smem, ctx->stream>>>(a, tw);
         } else {
             return fail(WSB_EUNSUPPORTED, "column length above 16384");
         }
@@ -735,18 +759,66 @@ int launch_cols(wsb_ctx *ctx, const ColArgs &a, const double2 *tw, int *nblocks,
     return WSB_OK;
 }
 
+template <class V>
+int rows_dispatch(wsb_ctx *ctx, const wsb_grid *g, int v_count, const void *grid_a, int plo,
+                  int phi, const RowDest &dst) {
+    const int ng = g->n_u / kG, ns = ceil_div(g->n_u, 32);
+    const int prec = sizeof(V) == 8 ? 32 : 64;
+    // rows above the on-chip 4096 points: SP = n_u / 4096 residue CTAs per row
+    const int logn = ilog2(g->n_u), logs = std::min(logn, kMaxOnChipLog), spl = logn - logs;
+    const void *tw = nullptr, *twn = nullptr;
+    WSB_TRY(twiddles(ctx, 1 << logs, kRowRL, &tw, prec));
+    if (spl > 0) WSB_TRY(twiddles(ctx, g->n_u, 0, &twn, prec));
+    const V *ga = (const V *)grid_a, *t2 = (const V *)tw, *tn = (const V *)twn;
+    switch (logs) {
+#define WSB_ROWS(L) \
+    case L: return launch_rows<L, V>(ctx, ga, ns, ng, v_count, plo, phi, t2, tn, dst, spl);
+        WSB_ROWS(1) WSB_ROWS(2) WSB_ROWS(3) WSB_ROWS(4) WSB_ROWS(5) WSB_ROWS(6)
+        WSB_ROWS(7) WSB_ROWS(8) WSB_ROWS(9) WSB_ROWS(10) WSB_ROWS(11) WSB_ROWS(12)
+#undef WSB_ROWS
+        default: return fail(WSB_EUNSUPPORTED, "transform length not supported");
+    }
+}
+
+template <class V>
+int cols_dispatch(wsb_ctx *ctx, ColArgs &a, int n_v) {
+    const int prec = sizeof(V) == 8 ? 32 : 64;
+    const int logn = ilog2(n_v), logs = std::min(logn, kMaxOnChipLog), spl = logn - logs;
+    const void *tw = nullptr, *twn = nullptr;
+    WSB_TRY(twiddles(ctx, 1 << logs, kColRL, &tw, prec));
+    if (spl > 0) WSB_TRY(twiddles(ctx, n_v, 0, &twn, prec));
+    a.twN = twn;
+    const V *t2 = (const V *)tw;
+    int nb = 0;
+    switch (logs) {
+#define WSB_COLS(L) \
+    case L: return launch_cols<L, V>(ctx, a, t2, &nb, spl);
+        WSB_COLS(1) WSB_COLS(2) WSB_COLS(3) WSB_COLS(4) WSB_COLS(5) WSB_COLS(6)
+        WSB_COLS(7) WSB_COLS(8) WSB_COLS(9) WSB_COLS(10) WSB_COLS(11) WSB_COLS(12)
+#undef WSB_COLS
+        default: return fail(WSB_EUNSUPPORTED, "transform length not supported");
+    }
+}
+
 }  // namespace
 
-int twiddles(wsb_ctx *ctx, int n, int rlmax, const double **out) {
-    // rlmax 3/4: pass-ordered table of an n-point plan; 0: plain exp(2 pi i m / n)
+int twiddles(wsb_ctx *ctx, int n, int rlmax, const void **out, int prec) {
+    // rlmax 3/4: pass-ordered table of an n-point plan; 0: plain exp(2 pi i m / n);
+    // complex128 (prec 64) or complex64 (prec 32) entries
     const int l = ilog2(n);
     if (!(rlmax == 0 || rlmax == 3 || rlmax == 4) || l > 15) return fail(WSB_EINVAL, "twiddle table");
-    const int key = l + 16 * (rlmax == 0 ? 2 : rlmax - 3);
+    const int key = l + 16 * (rlmax == 0 ? 2 : rlmax - 3) + (prec == 32 ? 48 : 0);
     if (!ctx->twiddle[key]) {
         const int size = rlmax == 0 ? n : std::max(1, tw_offset(l, rlmax, l));
-        WSB_CUDA_TRY(cudaMalloc(&ctx->twiddle[key], sizeof(double2) * size));
-        k_twiddles<<<ceil_div(size, 256), 256, 0, ctx->stream>>>((double2 *)ctx->twiddle[key], l,
-                                                                 rlmax, size);
+        if (prec == 32) {
+            WSB_CUDA_TRY(cudaMalloc(&ctx->twiddle[key], sizeof(float2) * size));
+            k_twiddles<float2><<<ceil_div(size, 256), 256, 0, ctx->stream>>>(
+                (float2 *)ctx->twiddle[key], l, rlmax, size);
+        } else {
+            WSB_CUDA_TRY(cudaMalloc(&ctx->twiddle[key], sizeof(double2) * size));
+            k_twiddles<double2><<<ceil_div(size, 256), 256, 0, ctx->stream>>>(
+                (double2 *)ctx->twiddle[key], l, rlmax, size);
+        }
         ctx->launches += 1;
         WSB_CUDA_TRY(cudaGetLastError());
     }
@@ -754,12 +826,12 @@ int twiddles(wsb_ctx *ctx, int n, int rlmax, const double **out) {
     return WSB_OK;
 }
 
-int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a, double *grid_p,
-             int plo, int phi, int n_dest, const int32_t *dest_groups, void *const *dest_ptrs) {
+int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const void *grid_a, void *grid_p,
+             int plo, int phi, int n_dest, const int32_t *dest_groups, void *const *dest_ptrs,
+             int prec) {
     if (phi <= plo || v_count <= 0) return WSB_OK;
-    const double *tw = nullptr;
-    if (g->n_u <= (1 << kMaxOnChipLog)) WSB_TRY(twiddles(ctx, g->n_u, kRowRL, &tw));
-    const int ng = g->n_u / kG, ns = ceil_div(g->n_u, 32);
+    const int ng = g->n_u / kG;
+    const size_t esz = prec == 32 ? sizeof(float2) : sizeof(double2);
     RowDest dst;
     if (n_dest < 1 || n_dest > 8) return fail(WSB_EINVAL, "n_dest must be in [1, 8]");
     dst.g0[0] = 0;
@@ -772,40 +844,25 @@ int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a,
         dst.plane0 = 0;
         for (int d = 0; d < n_dest; ++d) {
             if (!dest_ptrs[d]) return fail(WSB_EINVAL, "NULL destination pointer");
-            dst.ptr[d] = (double2 *)dest_ptrs[d];
+            dst.ptr[d] = dest_ptrs[d];
         }
     } else {
         // local destination-major buffer holding planes [plo, phi) only
         dst.plane0 = plo;
         for (int d = 0; d < n_dest; ++d)
-            dst.ptr[d] = (double2 *)grid_p + (int64_t)(phi - plo) * v_count * kG * dst.g0[d];
+            dst.ptr[d] = (char *)grid_p + esz * (int64_t)(phi - plo) * v_count * kG * dst.g0[d];
     }
-    const double2 *ga = (const double2 *)grid_a;
-    // rows above the on-chip 4096 points: SP = n_u / 4096 residue CTAs per row
-    const int logn = ilog2(g->n_u), logs = std::min(logn, kMaxOnChipLog), spl = logn - logs;
-    const double *twn = nullptr;
-    if (spl > 0) {
-        WSB_TRY(twiddles(ctx, 1 << logs, kRowRL, &tw));
-        WSB_TRY(twiddles(ctx, g->n_u, 0, &twn));
-    }
-    const double2 *t2 = (const double2 *)tw, *tn = (const double2 *)twn;
-    switch (logs) {
-#define WSB_ROWS(L) \
-    case L: return launch_rows<L>(ctx, ga, ns, ng, v_count, plo, phi, t2, tn, dst, spl);
-        WSB_ROWS(1) WSB_ROWS(2) WSB_ROWS(3) WSB_ROWS(4) WSB_ROWS(5) WSB_ROWS(6)
-        WSB_ROWS(7) WSB_ROWS(8) WSB_ROWS(9) WSB_ROWS(10) WSB_ROWS(11) WSB_ROWS(12)
-#undef WSB_ROWS
-        default: return fail(WSB_EUNSUPPORTED, "transform length not supported");
-    }
+    return prec == 32 ? rows_dispatch<float2>(ctx, g, v_count, grid_a, plo, phi, dst)
+                      : rows_dispatch<double2>(ctx, g, v_count, grid_a, plo, phi, dst);
 }
 
 int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t *src_rows,
-                   int g0, int ng, int plo, int phi, const double *tgrid, double *image_strip,
-                   double *norm_partials) {
+                   int g0, int ng, int plo, int phi, const void *tgrid, double *image_strip,
+                   double *norm_partials, int prec) {
     if (phi <= plo) return WSB_OK;
     if (n_sources < 1 || n_sources > 8) return fail(WSB_EINVAL, "n_sources must be in [1, 8]");
     ColArgs a;
-    a.tgrid = (const double2 *)tgrid;
+    a.tgrid = tgrid;
     a.strip = image_strip;
     a.partials = norm_partials;
     a.n_w = g->n_w;
@@ -829,33 +886,13 @@ int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t
     a.k1 = phi;
     // columns above the on-chip 4096 points: SP = n_v / 4096 residue CTAs
     const int logn = ilog2(g->n_v), logs = std::min(logn, kMaxOnChipLog), spl = logn - logs;
-    // the running stack: one complex per thread element of the launch
+    // the running stack (complex128): one per thread element of the launch
     {
         const int ct = std::max((1 << logs) / 8, 256), cpb = std::max(1, ct * 8 / (1 << logs));
         const size_t bytes = sizeof(double2) * (size_t)ceil_div(a.ncols, cpb) * ct * 8 << spl;
         WSB_TRY(ensure(ctx, kSlotColRun, bytes, (void **)&a.run));
     }
-    const double *tw, *twn = nullptr;
-    WSB_TRY(twiddles(ctx, 1 << logs, kColRL, &tw));
-    if (spl > 0) WSB_TRY(twiddles(ctx, g->n_v, 0, &twn));
-    a.twN = (const double2 *)twn;
-    const double2 *t2 = (const double2 *)tw;
-    int nb = 0;
-    switch (logs) {
-        case 1: return launch_cols<1>(ctx, a, t2, &nb, spl);
-        case 2: return launch_cols<2>(ctx, a, t2, &nb, spl);
-        case 3: return launch_cols<3>(ctx, a, t2, &nb, spl);
-        case 4: return launch_cols<4>(ctx, a, t2, &nb, spl);
-        case 5: return launch_cols<5>(ctx, a, t2, &nb, spl);
-        case 6: return launch_cols<6>(ctx, a, t2, &nb, spl);
-        case 7: return launch_cols<7>(ctx, a, t2, &nb, spl);
-        case 8: return launch_cols<8>(ctx, a, t2, &nb, spl);
-        case 9: return launch_cols<9>(ctx, a, t2, &nb, spl);
-        case 10: return launch_cols<10>(ctx, a, t2, &nb, spl);
-        case 11: return launch_cols<11>(ctx, a, t2, &nb, spl);
-        case 12: return launch_cols<12>(ctx, a, t2, &nb, spl);
-        default: return fail(WSB_EUNSUPPORTED, "transform length not supported");
-    }
+    return prec == 32 ? cols_dispatch<float2>(ctx, a, g->n_v) : cols_dispatch<double2>(ctx, a, g->n_v);
 }
 
 }  // namespace wsb

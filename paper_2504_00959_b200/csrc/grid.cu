@@ -192,7 +192,8 @@ struct SweepArgs {
     const double4 *rec;
     const uint32_t *idx;
     const uint32_t *off;
-    double2 *out;                 // strip layout [n_w][ceil(n_u/32)][v_count][32]
+    void *out;                    // strip layout [n_w][ceil(n_u/32)][v_count][32]
+    int out_f32;                  // 1: complex64 grid (FP32 path; accumulation stays FP64)
     unsigned long long *updates;
     const double *i0beta;         // device scalar, np.i0(beta) (Kaiser-Bessel)
     const uint4 *parts;           // (item, first entry, end entry, slot | ~0 = direct)
@@ -243,7 +244,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, WSB_GRID_MINB) k_grid_sweep
     // a split item writes its unsigned partial tile [slot][row - R0][32]
     const int64_t colbase = direct ? ((int64_t)plane * a.n_tc + tc) * a.v_count + (R0 - a.v_start)
                                    : (int64_t)pd.w * kRowBlock;
-    double2 *const out = direct ? a.out : a.partial;
+    double2 *const out = direct ? (double2 *)a.out : a.partial;
+    float2 *const out32 = (float2 *)a.out;
+    const bool f32 = direct && a.out_f32;
     st.wu[lane][W] = 0.0;
 
     // Window of W rows kept as a ring of W register slots: row `base` is in
@@ -264,7 +267,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, WSB_GRID_MINB) k_grid_sweep
         constexpr int p = decltype(P)::value;
         if (base >= R0 && base < R1 && col_ok) {
             const double s = (direct && ((col + base) & 1)) ? -1.0 : 1.0;
-            out[(colbase + (base - R0)) * 32 + lane] = make_double2(acc[p].x * s, acc[p].y * s);
+            const int64_t o = (colbase + (base - R0)) * 32 + lane;
+            if (f32)
+                out32[o] = make_float2((float)(acc[p].x * s), (float)(acc[p].y * s));
+            else
+                out[o] = make_double2(acc[p].x * s, acc[p].y * s);
         }
         acc[p] = make_double2(0.0, 0.0);
         ++base;
@@ -491,8 +498,11 @@ __global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split
         }
         if (col < a.n_u) {
             const double s = ((col + row) & 1) ? -1.0 : 1.0;
-            a.out[(((int64_t)plane * a.n_tc + tc) * a.v_count + (row - a.v_start)) * 32 + lane] =
-                make_double2(acc.x * s, acc.y * s);
+            const int64_t o = (((int64_t)plane * a.n_tc + tc) * a.v_count + (row - a.v_start)) * 32 + lane;
+            if (a.out_f32)
+                ((float2 *)a.out)[o] = make_float2((float)(acc.x * s), (float)(acc.y * s));
+            else
+                ((double2 *)a.out)[o] = make_double2(acc.x * s, acc.y * s);
         }
     }
 }
@@ -500,13 +510,14 @@ __global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split
 }  // namespace
 
 int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start, int v_count,
-               const double *rec, const RowBuckets &bk, double *grid_p,
-               unsigned long long *updates_dev) {
+               const double *rec, const RowBuckets &bk, void *grid_p,
+               unsigned long long *updates_dev, int prec) {
     SweepArgs a;
     a.rec = (const double4 *)rec;
     a.idx = bk.idx;
     a.off = bk.off;
-    a.out = (double2 *)grid_p;
+    a.out = grid_p;
+    a.out_f32 = prec == 32 ? 1 : 0;
     a.updates = updates_dev;
     a.i0beta = nullptr;
     a.n_u = g->n_u;

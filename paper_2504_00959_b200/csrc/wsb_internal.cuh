@@ -56,11 +56,12 @@ struct wsb_ctx {
     unsigned long long *u64_host = nullptr;
     wsb::Timing timing;
     // twiddle tables keyed by log2(n) + 16 * {0: radix-8 plan, 1: radix-16 plan, 2: plain}
-    double *twiddle[48] = {nullptr};
+    double *twiddle[96] = {nullptr};   // + 48: complex64 copies
     // last bucketing (for wsb_tiles_debug)
     int64_t last_entries = 0, last_tiles = 0;
     uint32_t *last_keys = nullptr, *last_idx = nullptr, *last_off = nullptr;
     int launches = 0;
+    int precision = 64;               // wsb_ctx_set_precision: 64 or 32 (complex64 grids)
     double last_ms[6] = {0, 0, 0, 0, 0, 0};
 };
 
@@ -97,7 +98,7 @@ enum Slot {
 };
 
 int ensure(wsb_ctx *ctx, int slot, size_t bytes, void **out);
-int twiddles(wsb_ctx *ctx, int n, int rlmax, const double **out);
+int twiddles(wsb_ctx *ctx, int n, int rlmax, const void **out, int prec = 64);
 
 // scan.cu
 int exclusive_scan_u32(wsb_ctx *ctx, const uint32_t *in, uint32_t *out, int64_t n,
@@ -133,8 +134,8 @@ int bucket_rows(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_count
 
 // grid.cu
 int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start, int v_count,
-               const double *rec, const RowBuckets &bk, double *grid_p,
-               unsigned long long *updates_dev);
+               const double *rec, const RowBuckets &bk, void *grid_p,
+               unsigned long long *updates_dev, int prec = 64);
 
 // peer.cu: copy n_dest contiguous blocks src[d] -> dst[d] (bytes[d] each; dst
 // may be peer memory) with one launch on the context stream
@@ -142,13 +143,13 @@ int push_blocks(wsb_ctx *ctx, int n_dest, const void *const *src, void *const *d
                 const int64_t *bytes);
 
 // fft.cu
-int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const double *grid_a, double *grid_p,
+// prec 64: complex128 grids; 32: complex64 grids (FP32 path)
+int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const void *grid_a, void *grid_p,
              int plane_lo, int plane_hi, int n_dest, const int32_t *dest_groups,
-             void *const *dest_ptrs = nullptr);
+             void *const *dest_ptrs = nullptr, int prec = 64);
 int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t *src_rows,
-                   int g0, int ng, int plane_lo, int plane_hi, const double *tgrid,
-                   double *image_strip,
-                   double *norm_partials);
+                   int g0, int ng, int plane_lo, int plane_hi, const void *tgrid,
+                   double *image_strip, double *norm_partials, int prec = 64);
 int strip_to_image(wsb_ctx *ctx, const wsb_grid *g, const double *strip, double *image);
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }

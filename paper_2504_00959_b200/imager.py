@@ -287,9 +287,11 @@ def unpack_grid_device(grid_p: torch.Tensor, spec: GridSpec, v_start: int, v_cou
     return torch.view_as_complex(out)
 
 
-def image_device(u, v, w, vis, weight, spec, kern, image_out: torch.Tensor | None = None):
+def image_device(u, v, w, vis, weight, spec, kern, image_out: torch.Tensor | None = None,
+                 precision: int = 64):
     """Whole hot path on device-resident inputs (one GPU): returns
-    (pixels f64 tensor (n_v, n_u), diag dict)."""
+    (pixels f64 tensor (n_v, n_u), diag dict). precision=32 selects the FP32
+    path (complex64 grid and transforms; within 1e-5 of the FP64 image)."""
     spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
     dev = u.device if isinstance(u, torch.Tensor) and u.is_cuda else None
     ctx = context(dev)
@@ -305,8 +307,13 @@ def image_device(u, v, w, vis, weight, spec, kern, image_out: torch.Tensor | Non
         image_out = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, device=dev)
     d = L.WsbDiag()
     g, k = spec.c_struct(), kern.c_struct()
-    L.check(L.lib().wsb_image_device(ctx.handle, C.byref(g), C.byref(k), _ptr(u), _ptr(v), _ptr(w),
+    lib = L.lib()
+    L.check(lib.wsb_ctx_set_precision(ctx.handle, int(precision)))
+    try:
+        L.check(lib.wsb_image_device(ctx.handle, C.byref(g), C.byref(k), _ptr(u), _ptr(v), _ptr(w),
                                      _ptr(visf), _ptr(wt), n, n_chan, _ptr(image_out), C.byref(d)))
+    finally:
+        lib.wsb_ctx_set_precision(ctx.handle, 64)
     return image_out, diag_dict(d)
 
 
@@ -428,7 +435,8 @@ def last_timings(device=None):
 # host-buffer entry (the C-ABI drop-in, include/wsb.h wsb_image)
 # ---------------------------------------------------------------------------
 
-def image(u, v, w, time_index, vis, weight, spec, kern, device: int = 0) -> tuple[FinalImage, dict]:
+def image(u, v, w, time_index, vis, weight, spec, kern, device: int = 0,
+          precision: int = 64) -> tuple[FinalImage, dict]:
     """Dirty image from HOST arrays through wsb_image (copies in and out are
     part of the call). Mirrors run_pipeline phases 2-5 (pipeline.py:95-152)."""
     spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
@@ -446,7 +454,7 @@ def image(u, v, w, time_index, vis, weight, spec, kern, device: int = 0) -> tupl
     out = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, pin_memory=True).numpy()
     d = L.WsbDiag()
     g, k = spec.c_struct(), kern.c_struct()
-    ex = L.WsbExec(int(device), 64, 1, 0)
+    ex = L.WsbExec(int(device), int(precision), 1, 0)
     ti = None if time_index is None else np.ascontiguousarray(time_index, np.uint32)
     vp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)  # noqa: E731
     L.check(L.lib().wsb_image(C.byref(g), C.byref(k), C.byref(ex), vp(u), vp(v), vp(w), vp(ti),

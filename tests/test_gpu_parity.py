@@ -317,3 +317,43 @@ def test_image_stream_matches_single_calls(W, golden_image):
         assert img.pixels.tobytes() == ref.pixels.tobytes()
         assert img.imag_residual_norm == ref.imag_residual_norm
         assert d["grid_updates"] == dref["grid_updates"]
+
+
+@pytest.mark.parametrize("name", ["small", "kb5", "kb1", "nw1", "wide", "multichan"])
+def test_image_fp32_path_within_1e5(W, golden_image, name):
+    """The optional FP32 path (complex64 grid and transforms, FP64
+    coordinates / weights / phases / stack) against the reference image:
+    north-star tolerance 1e-5 relative L2."""
+    g = golden_image
+    n_u, n_v, n_w, S, _ = (int(x) for x in g[f"{name}_cfg"])
+    cell, wmin, wmax, shape = (float(x) for x in g[f"{name}_fcfg"])
+    kind = "gaussian" if int(g[f"{name}_kind"][0]) == 0 else "kaiser_bessel"
+    spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
+    kern = W.KernelSpec(kind, S, shape)
+    img, diag = W.image(*chunk_from(g, f"{name}_in_"), spec, kern, precision=32)
+    assert diag["grid_updates"] == int(g[f"{name}_grid_updates"][0])
+    err = rel_l2(img.pixels, g[f"{name}_pixels"])
+    assert err <= 1e-5, err
+
+
+def test_image_fp32_medium_and_device_path(W):
+    """FP32 path on the 200k-record KB case vs the oracle, and through the
+    device entry point (same kernels, same result)."""
+    import torch
+    src = ((0.02, -0.015, 2.0), (0.0, 0.0, 1.0), (-0.03, 0.01, 0.5))
+    u, v, w, t, vis, wt = O.generate_synthetic(src, 200_000, 1, seed=21, cell_size_lm=5e-4,
+                                               w_max_native=400.0)
+    spec = W.GridSpec(256, 256, 8, 5e-4, w_max_native=400.0)
+    kern = W.KernelSpec.kaiser_bessel(3)
+    ref = O.image(u, v, w, t, vis, wt, 256, 256, 8, 5e-4, 0.0, 400.0, O.KIND_KAISER_BESSEL, 3,
+                  kern.shape_param)
+    img, _ = W.image(u, v, w, t, vis, wt, spec, kern, precision=32)
+    assert rel_l2(img.pixels, ref["pixels"]) <= 1e-5
+    dev = torch.device("cuda", 0)
+    dimg, _ = W.image_device(*(torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+                               for x in (u, v, w, vis, wt)), spec, kern, precision=32)
+    assert dimg.cpu().numpy().tobytes() == img.pixels.tobytes()
+    # the context is back on FP64 afterwards
+    d64, _ = W.image_device(*(torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+                              for x in (u, v, w, vis, wt)), spec, kern)
+    assert rel_l2(d64.cpu().numpy(), ref["pixels"]) <= 1e-10
