@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--kind", default="gaussian")
     ap.add_argument("--S", type=int, default=3)
     ap.add_argument("--cell", type=float, default=None)
+    ap.add_argument("--precision", type=int, default=64)
     a = ap.parse_args()
     cfg = dict(bench.CFG2, n_vis=a.n, n_u=a.nu, n_v=a.nu, n_w=a.nw)
     if a.cell:
@@ -35,7 +36,7 @@ def main():
     spec = W.GridSpec(cfg["n_u"], cfg["n_v"], cfg["n_w"], cfg["cell"], w_max_native=cfg["w_max"])
     kern = (W.KernelSpec.gaussian(a.S, 1.0) if a.kind == "gaussian" else W.KernelSpec.kaiser_bessel(a.S))
     for _ in range(a.steps):
-        img, diag = W.image_device(du, dv, dw, dvis, dwt, spec, kern)
+        img, diag = W.image_device(du, dv, dw, dvis, dwt, spec, kern, precision=a.precision)
     torch.cuda.synchronize()
     ms, n = W.last_timings(dev)
     print("kernel ms [prepare, bucket, grid, rows, cols, finish]:", [round(x, 3) for x in ms],
