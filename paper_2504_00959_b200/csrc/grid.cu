@@ -135,14 +135,17 @@ __device__ __forceinline__ uint32_t axis_weights(double g, int i0, const KParams
                 // as the power series sum_k (beta^2 t / 4)^k / (k!)^2 / I0(beta):
                 // positive terms, no cancellation, no exp/sqrt/division --
                 // within a few ulp of np.i0's Chebyshev evaluation
-                const double x = __ddiv_rn(d, (double)S);
-                const double t = fmax(__dsub_rn(1.0, __dmul_rn(x, x)), 0.0);
                 if (kp.series) {
+                    // t = 1 - d^2/S^2 without the FP64 division (a few ulp)
+                    constexpr double kInvS2 = 1.0 / (double)(S * S);
+                    const double t = fmax(fma(-d, d * kInvS2, 1.0), 0.0);
                     double p = kp.kb[KParams<S>::NKB - 1];
 #pragma unroll
                     for (int q = KParams<S>::NKB - 2; q >= 0; --q) p = fma(p, t, kp.kb[q]);
                     w[k] = p;
                 } else {  // large beta: np.i0's own Chebyshev evaluation
+                    const double x = __ddiv_rn(d, (double)S);
+                    const double t = fmax(__dsub_rn(1.0, __dmul_rn(x, x)), 0.0);
                     w[k] = __ddiv_rn(bessel_i0(__dmul_rn(kp.p0, __dsqrt_rn(t))), i0beta);
                 }
             }
