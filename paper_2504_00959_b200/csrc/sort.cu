@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t *__r
 }
 
 // ---------------------------------------------------------------------------
-// radix sort: B-bit digits (B = 8..11, chosen so the key needs as few passes
+// radix sort: B-bit digits (B = 8..9, chosen so the key needs as few passes
 // as possible: cfg3's 26-bit keys take 3 passes of 9 bits instead of 4 of 8;
 // wider digits scatter too thinly -- 2 passes of 12 bits were measured 1.6x
 // slower than 3 of 8 at cfg2)
@@ -290,7 +290,10 @@ int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t 
     *keys_out = keys;
     *vals_out = vals;
     if (n <= 1 || bits <= 0) return WSB_OK;
-    const int passes = (bits + 10) / 11;
+    // digits of at most 9 bits (wider digits scatter too thinly: measured
+    // slower), as few passes as that allows: 21 or 23 bits -> 3 x 8,
+    // 26 -> 3 x 9 (never below 8 bits)
+    const int passes = (bits + 8) / 9;
     const int B = std::max(8, (bits + passes - 1) / passes);
     const int nb = ceil_div(n, kRsItems);
     uint32_t *hist;
