@@ -444,7 +444,7 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     # right): the same association as the single-GPU path, for any R
     im_sq = float(p[:, 0].cumsum()[-1])
     re_sq = float(p[:, 1].cumsum()[-1])
-    if to_host:
+    if to_host and pix.is_cuda:
         # page-locked staging: the image leaves at DMA speed (a pageable
         # destination costs ~10x), then a private host copy
         stage = torch.empty(pix.shape, dtype=pix.dtype, pin_memory=True)
@@ -453,7 +453,7 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
         out.copy_(stage)
         pixels = out.numpy()
     else:
-        pixels = pix
+        pixels = pix.numpy() if to_host else pix
     img = FinalImage(spec, pixels, im_sq ** 0.5, re_sq ** 0.5)
     diag.update({"imag_residual_norm": img.imag_residual_norm, "real_norm": img.real_norm})
     return img, diag
