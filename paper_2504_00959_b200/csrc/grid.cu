@@ -87,6 +87,7 @@ struct KParams {
     static constexpr int W = 2 * S + 1;
     static constexpr int NKB = 12 + 4 * S;   // Kaiser-Bessel series terms (beta up to ~3.5 S)
     double p0;              // Gaussian: 2 sigma^2; Kaiser-Bessel: beta
+    double inv_p0;          // 1 / p0
     double cm[W];           // Gaussian: exp(-m^2/s2), m = S-k (factorised path)
     double kb[NKB];         // Kaiser-Bessel: (beta^2/4)^k / (k!)^2 / I0(beta)
     int factorised;         // Gaussian: 1 if the factorised form cannot overflow
@@ -112,8 +113,9 @@ __device__ __forceinline__ uint32_t axis_weights(double g, int i0, const KParams
     }
     if (KIND == WSB_KERNEL_GAUSSIAN && kp.factorised) {
         const double f = __dsub_rn(g, (double)(i0 + S));
-        const double a = fast_exp(__ddiv_rn(-__dmul_rn(f, f), kp.p0));
-        const double b = fast_exp(__ddiv_rn(-2.0 * f, kp.p0));  // m > 0 side
+        // (multiplying by 1/s2 instead of dividing: a few ulp, no FP64 division)
+        const double a = fast_exp(-__dmul_rn(f, f) * kp.inv_p0);
+        const double b = fast_exp(-2.0 * f * kp.inv_p0);  // m > 0 side
         const double bi = __drcp_rn(b);                         // m < 0 side
         w[S] = a;
         double pb = a, pbi = a;
@@ -369,6 +371,7 @@ int launch_s(wsb_ctx *ctx, const SweepArgs &a, double p0) {
     kp.p0 = p0;
     kp.factorised = 0;
     kp.series = 0;
+    kp.inv_p0 = 1.0 / p0;
     for (int k = 0; k < W; ++k) kp.cm[k] = 0.0;
     for (int q = 0; q < KParams<S>::NKB; ++q) kp.kb[q] = 0.0;
     if (KIND == WSB_KERNEL_KAISER_BESSEL) {
