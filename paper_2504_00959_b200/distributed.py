@@ -457,3 +457,56 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     img = FinalImage(spec, pixels, im_sq ** 0.5, re_sq ** 0.5)
     diag.update({"imag_residual_norm": img.imag_residual_norm, "real_norm": img.real_norm})
     return img, diag
+
+
+def image_distributed_stream(batches, spec, kern, group=None, root: int = 0, **kwargs):
+    """``image_distributed`` over a stream of this rank's HOST record batches
+    (one image per batch, e.g. successive time chunks), double-buffered: the
+    host->device copy of batch i+1 runs on a side stream while batch i is
+    imaged. Every batch still makes the full round trip (pinned host records
+    in, root image to host); only the copies overlap the device work. Each
+    batch is (u, v, w, vis, weight) host arrays (page-locked for DMA speed).
+    Yields (FinalImage on ``root`` / None elsewhere, diag)."""
+    import numpy as np
+    be = kwargs.pop("backend", None) or CudaBackend()
+    dev = be.device
+    compute = torch.cuda.current_stream(dev)
+    s_in = torch.cuda.Stream(dev)
+    slots, done = [None, None], [None, None]
+
+    def upload(i, b):
+        u, v, w, vis, wt = b
+        n = len(u)
+        vis = np.asarray(vis, np.complex64).reshape(n, -1)
+        wt = np.asarray(wt, np.float32).reshape(n, -1)
+        host = [torch.from_numpy(np.ascontiguousarray(x)) for x in
+                (np.asarray(u, np.float64), np.asarray(v, np.float64), np.asarray(w, np.float64),
+                 vis, wt)]
+        slot = i % 2
+        if slots[slot] is None or any(d.shape != h.shape for d, h in zip(slots[slot], host)):
+            slots[slot] = [torch.empty(h.shape, dtype=h.dtype, device=dev) for h in host]
+        with torch.cuda.stream(s_in):
+            if done[slot] is not None:
+                s_in.wait_event(done[slot])
+            for d, h in zip(slots[slot], host):
+                d.copy_(h, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(s_in)
+        return ev, host
+
+    it = iter(batches)
+    nxt = next(it, None)
+    staged = upload(0, nxt) if nxt is not None else None
+    i = 0
+    while staged is not None:
+        ev, _host = staged
+        slot = i % 2
+        nxt = next(it, None)
+        compute.wait_event(ev)
+        staged = upload(i + 1, nxt) if nxt is not None else None
+        img, diag = image_distributed(*slots[slot], spec, kern, group=group, backend=be, root=root,
+                                      to_host=True, **kwargs)
+        done[slot] = torch.cuda.Event()
+        done[slot].record(compute)
+        yield img, diag
+        i += 1

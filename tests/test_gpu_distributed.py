@@ -142,6 +142,14 @@ def _nccl_worker(rank, world, port, outdir):
             if rank == 0:
                 outs[name] = img.pixels
                 outs[name + "_updates"] = np.array([diag["grid_updates"]])
+        # the double-buffered stream API: this rank's slice in two batches
+        from paper_2504_00959_b200.distributed import image_distributed_stream
+        mid = (lo + hi) // 2
+        batches = [tuple(np.ascontiguousarray(x[a_:b_]) for x in (u, v, w, vis, wt))
+                   for a_, b_ in ((lo, mid), (mid, hi))]
+        for bi, (img, diag) in enumerate(image_distributed_stream(batches, spec, kern)):
+            if rank == 0:
+                outs[f"stream{bi}"] = img.pixels
         if rank == 0:
             np.savez(Path(outdir) / "out.npz", **outs)
     finally:
@@ -163,3 +171,12 @@ def test_nccl_multi_gpu_matches_single(W, golden_image, tmp_path):
     for name in ("push", "push2", "peer", "nccl", "even"):
         assert int(out[name + "_updates"][0]) == diag["grid_updates"], name
         assert out[name].tobytes() == ref.pixels.tobytes(), name
+    # stream batches: batch b = every rank's b-th half of its slice, in rank order
+    u, v, w, t, vis, wt = chunk_from(g, "wide_in_")
+    parts = _parts(t, world)
+    for bi in range(2):
+        sel = np.concatenate([np.arange(lo, (lo + hi) // 2) if bi == 0 else np.arange((lo + hi) // 2, hi)
+                              for lo, hi in parts])
+        ref_b, _ = W.image(*(x[sel] for x in (u, v, w)), None, vis[sel], wt[sel], spec,
+                           W.KernelSpec("gaussian", S, shape))
+        assert out[f"stream{bi}"].tobytes() == ref_b.pixels.tobytes(), bi
