@@ -207,9 +207,10 @@ int wsb_fft_rows_peer(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_count,
                       const double *grid_s, int32_t plane_lo, int32_t plane_hi, int32_t n_dest,
                       const int32_t *dest_cols_host, void *const *dest_ptrs_host);
 
-/* Slab-transpose push: copies n_dest contiguous device blocks
- * src_ptrs[d] -> dst_ptrs[d] (bytes_host[d] each, multiples of 16, 16-byte
- * aligned) in ONE launch on the context stream; dst may be peer memory
+/* Slab-transpose / record-exchange push: copies n_dest contiguous device
+ * blocks src_ptrs[d] -> dst_ptrs[d] (bytes_host[d] each, multiples of 4,
+ * 4-byte aligned; 16-byte vector stores when all are 16-byte multiples) in
+ * ONE launch on the context stream; dst may be peer memory
  * (NVLink stores). Used to move each plane range of the wsb_fft_rows
  * destination-major output into the other ranks' column-pass inputs while
  * the next range is transformed. Enqueued, no synchronisation. */

@@ -41,6 +41,23 @@ __global__ void __launch_bounds__(kPushThreads) k_push(PushArgs a) {
     }
 }
 
+// 4-byte granular variant (blocks of int32 columns at arbitrary offsets)
+struct PushArgs4 {
+    const uint32_t *src[8];
+    uint32_t *dst[8];
+    int64_t n4[8];
+};
+
+__global__ void __launch_bounds__(kPushThreads) k_push4(PushArgs4 a) {
+    const int d = blockIdx.y;
+    const uint32_t *__restrict__ s = a.src[d];
+    uint32_t *__restrict__ t = a.dst[d];
+    const int64_t n = a.n4[d];
+    for (int64_t i = (int64_t)blockIdx.x * kPushThreads + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * kPushThreads)
+        t[i] = __ldcs(&s[i]);
+}
+
 }  // namespace
 
 int push_blocks(wsb_ctx *ctx, int n_dest, const void *const *src, void *const *dst,
@@ -53,10 +70,30 @@ int push_blocks(wsb_ctx *ctx, int n_dest, const void *const *src, void *const *d
         a.dst[d] = nullptr;
         a.n16[d] = 0;
     }
+    bool wide = true;
     for (int d = 0; d < n_dest; ++d) {
-        if (bytes[d] < 0 || bytes[d] % 16) return fail(WSB_EINVAL, "block sizes must be multiples of 16 bytes");
+        if (bytes[d] < 0 || bytes[d] % 4) return fail(WSB_EINVAL, "block sizes must be multiples of 4 bytes");
         if (bytes[d] && (!src[d] || !dst[d])) return fail(WSB_EINVAL, "NULL block pointer");
-        if (((uintptr_t)src[d] | (uintptr_t)dst[d]) % 16) return fail(WSB_EINVAL, "blocks must be 16-byte aligned");
+        if (((uintptr_t)src[d] | (uintptr_t)dst[d]) % 4) return fail(WSB_EINVAL, "blocks must be 4-byte aligned");
+        if (bytes[d] % 16 || ((uintptr_t)src[d] | (uintptr_t)dst[d]) % 16) wide = false;
+    }
+    if (!wide) {
+        PushArgs4 b;
+        int64_t most4 = 0;
+        for (int d = 0; d < 8; ++d) {
+            b.src[d] = d < n_dest ? (const uint32_t *)src[d] : nullptr;
+            b.dst[d] = d < n_dest ? (uint32_t *)dst[d] : nullptr;
+            b.n4[d] = d < n_dest ? bytes[d] / 4 : 0;
+            most4 = std::max(most4, b.n4[d]);
+        }
+        if (most4 == 0) return WSB_OK;
+        const int per = (int)std::min<int64_t>(64, (most4 + kPushThreads - 1) / kPushThreads);
+        k_push4<<<dim3(per, n_dest), kPushThreads, 0, ctx->stream>>>(b);
+        ctx->launches += 1;
+        WSB_CUDA_TRY(cudaGetLastError());
+        return WSB_OK;
+    }
+    for (int d = 0; d < n_dest; ++d) {
         a.src[d] = (const uint4 *)src[d];
         a.dst[d] = (uint4 *)dst[d];
         a.n16[d] = bytes[d] / 16;

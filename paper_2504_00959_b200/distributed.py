@@ -224,11 +224,12 @@ def _side_stream(dev):
     return _SIDE[dev.index]
 
 
-def _symm_buffer(elems: int, dev, group):
+def _symm_buffer(elems: int, dev, group, tag: str = "transpose"):
     """Symmetric (peer-mapped) float64 buffer of 2*elems values on every rank,
-    cached: the rendezvous is collective and costly. Keeps the largest."""
+    cached per tag: the rendezvous is collective and costly. Keeps the
+    largest (all ranks must ask for the same size)."""
     import torch.distributed._symmetric_memory as symm
-    key = (id(group), dev.index)
+    key = (tag, id(group), dev.index)
     hit = _SYMM.get(key)
     if hit is None or hit[0].numel() < 2 * elems:
         _SYMM.pop(key, None)
@@ -241,7 +242,7 @@ def _symm_buffer(elems: int, dev, group):
 def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None, root: int = 0,
                       to_host: bool = True, n_ranges: int = 4, timings: dict | None = None,
                       balance: bool = True, row_weight: float = 10_000.0,
-                      transpose: str = "auto"):
+                      transpose: str = "auto", exchange: str = "auto"):
     """Dirty image of the union of every rank's records. Each rank passes its
     own time partition (records in gindex order, rank r holding the r-th
     contiguous block, as visdata.partition_time_ordered produces).
@@ -305,15 +306,54 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     n_local = int(rec.shape[0])
     del rec, plane                  # large meshes: keep the peak footprint down
     st.mark("route")
-    c_send = torch.tensor(counts, dtype=torch.int64, device=dev)
-    c_recv = torch.empty(R, dtype=torch.int64, device=dev)
-    dist.all_to_all_single(c_recv, c_send, group=group)
-    recv_counts = [int(x) for x in c_recv.tolist()]
-    m = sum(recv_counts)
-    rrec = torch.empty((m, 4), dtype=torch.float64, device=dev)
-    rpl = torch.empty(m, dtype=torch.int32, device=dev)
-    _a2a(rrec, srec.contiguous(), recv_counts, counts, group)
-    _a2a(rpl, spl.contiguous(), recv_counts, counts, group)
+    if exchange == "auto":
+        exchange = ("push" if (hasattr(be, "push_blocks") and dev.type == "cuda"
+                               and _symm_available()) else "nccl")
+    if exchange == "push":
+        # every rank learns the whole count matrix, then pushes its block for
+        # slab d straight into d's receive buffer (symmetric memory, NVLink
+        # stores) at the offset of its rank in gindex order
+        cm = torch.empty((R, R), dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(cm, torch.tensor(counts, dtype=torch.int64, device=dev),
+                                    group=group)
+        cmat = cm.tolist()                                  # cmat[s][d]
+        recv_counts = [cmat[s_][r] for s_ in range(R)]
+        m = sum(recv_counts)
+        need = max(sum(cmat[s_][d] for s_ in range(R)) for d in range(R))
+        cap = max(1, -(-need * 5 // 4))                    # 25% headroom against re-rendezvous
+        # records: 4 float64 each (2 * 2cap values); planes: int32, viewed in a float64 buffer
+        rbuf, rh = _symm_buffer(2 * cap, dev, group, "records")
+        pbuf, ph = _symm_buffer(-(-cap // 4) + 1, dev, group, "planes")
+        if rbuf.numel() < 4 * need or pbuf.numel() * 2 < need:
+            raise RuntimeError("symmetric exchange buffers out of sync")
+        rh.barrier(channel=0)                               # the previous slab has been gridded
+        srcs_r, dsts_r, b_r, srcs_p, dsts_p, b_p = [], [], [], [], [], []
+        sent = 0
+        for d in range(R):
+            off = sum(cmat[s_][d] for s_ in range(r))       # my place in d's buffer
+            srcs_r.append(srec.data_ptr() + 32 * sent)
+            dsts_r.append(rh.buffer_ptrs[d] + 32 * off)
+            b_r.append(32 * counts[d])
+            srcs_p.append(spl.data_ptr() + 4 * sent)
+            dsts_p.append(ph.buffer_ptrs[d] + 4 * off)
+            b_p.append(4 * counts[d])
+            sent += counts[d]
+        cur = torch.cuda.current_stream(dev)
+        be.push_blocks(srcs_r, dsts_r, b_r, cur)
+        be.push_blocks(srcs_p, dsts_p, b_p, cur)
+        rh.barrier(channel=0)                               # every block has landed
+        rrec = rbuf[: 4 * m].view(m, 4)
+        rpl = pbuf.view(torch.int32)[:m]
+    else:
+        c_send = torch.tensor(counts, dtype=torch.int64, device=dev)
+        c_recv = torch.empty(R, dtype=torch.int64, device=dev)
+        dist.all_to_all_single(c_recv, c_send, group=group)
+        recv_counts = [int(x) for x in c_recv.tolist()]
+        m = sum(recv_counts)
+        rrec = torch.empty((m, 4), dtype=torch.float64, device=dev)
+        rpl = torch.empty(m, dtype=torch.int32, device=dev)
+        _a2a(rrec, srec.contiguous(), recv_counts, counts, group)
+        _a2a(rpl, spl.contiguous(), recv_counts, counts, group)
     del srec, spl
     st.mark("exchange")
 

@@ -137,6 +137,7 @@ def _nccl_worker(rank, world, port, outdir):
         for name, kw in (("push", dict(transpose="push")), ("push2", dict(transpose="push")),
                          ("peer", dict(transpose="peer")),
                          ("nccl", dict(transpose="nccl")),
+                         ("xnccl", dict(exchange="nccl", transpose="nccl")),
                          ("even", dict(transpose="nccl", balance=False))):
             img, diag = image_distributed(*args, spec, kern, **kw)
             if rank == 0:
@@ -168,7 +169,7 @@ def test_nccl_multi_gpu_matches_single(W, golden_image, tmp_path):
     cell, wmin, wmax, shape = (float(x) for x in g["wide_fcfg"])
     spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
     ref, diag = W.image(*chunk_from(g, "wide_in_"), spec, W.KernelSpec("gaussian", S, shape))
-    for name in ("push", "push2", "peer", "nccl", "even"):
+    for name in ("push", "push2", "peer", "nccl", "xnccl", "even"):
         assert int(out[name + "_updates"][0]) == diag["grid_updates"], name
         assert out[name].tobytes() == ref.pixels.tobytes(), name
     # stream batches: batch b = every rank's b-th half of its slice, in rank order

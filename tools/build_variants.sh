@@ -8,7 +8,7 @@ FL="-O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr"
 build() {  # name, defines...
   name=$1; shift
   objs=""
-  for f in api prepare bucket sort grid fft; do
+  for f in api prepare bucket sort grid fft peer; do
     nvcc $ARCH $FL "$@" -I include -c paper_2504_00959_b200/csrc/$f.cu -o build/variants/${name}_$f.o
     objs="$objs build/variants/${name}_$f.o"
   done
