@@ -335,7 +335,6 @@ def image_stream(batches, spec, kern, device: int = 0):
     imgs = [None, None]            # device images per slot
     done = [None, None]            # compute-finished event per slot
     read = [None, None]            # image-copied-out event per slot
-    pinned = [None, None]          # page-locked image staging per slot
 
     def upload(i, b):
         u, v, w, vis, wt = b
@@ -384,11 +383,10 @@ def image_stream(batches, spec, kern, device: int = 0):
                                          _ptr(imgs[slot]), C.byref(d)))
         done[slot] = torch.cuda.Event()
         done[slot].record(compute)
-        # page-locked staging ring (allocated once: pinning is slow); the
-        # yielded image is a private copy made while the device works on
-        if pinned[slot] is None:
-            pinned[slot] = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, pin_memory=True)
-        out = pinned[slot]
+        # page-locked image from torch's caching host allocator (recycled
+        # once the caller drops an image: no re-pinning in steady state); the
+        # yielded pixels are that buffer itself, no host copy
+        out = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, pin_memory=True)
         with torch.cuda.stream(s_out):
             s_out.wait_event(done[slot])
             out.copy_(imgs[slot], non_blocking=True)
@@ -398,14 +396,14 @@ def image_stream(batches, spec, kern, device: int = 0):
         if pending is not None:
             pev, pout, pd = pending
             pev.synchronize()
-            yield (FinalImage(spec, _host_copy(pout), pd.imag_residual_norm, pd.real_norm),
+            yield (FinalImage(spec, pout.numpy(), pd.imag_residual_norm, pd.real_norm),
                    diag_dict(pd))
         pending = (oev, out, d)
         staged = staged_next
         i += 1
     pev, pout, pd = pending
     pev.synchronize()
-    yield FinalImage(spec, _host_copy(pout), pd.imag_residual_norm, pd.real_norm), diag_dict(pd)
+    yield FinalImage(spec, pout.numpy(), pd.imag_residual_norm, pd.real_norm), diag_dict(pd)
 
 
 def _host_copy(t: torch.Tensor) -> np.ndarray:
