@@ -335,6 +335,8 @@ def image_stream(batches, spec, kern, device: int = 0):
     imgs = [None, None]            # device images per slot
     done = [None, None]            # compute-finished event per slot
     read = [None, None]            # image-copied-out event per slot
+    # page-locked images, recycled (across calls) once the caller drops them
+    pool = _PINNED_POOLS.setdefault((spec.n_v, spec.n_u), [])
 
     def upload(i, b):
         u, v, w, vis, wt = b
@@ -386,7 +388,7 @@ def image_stream(batches, spec, kern, device: int = 0):
         # page-locked image from torch's caching host allocator (recycled
         # once the caller drops an image: no re-pinning in steady state); the
         # yielded pixels are that buffer itself, no host copy
-        out = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, pin_memory=True)
+        out = _pinned_image(pool, spec)
         with torch.cuda.stream(s_out):
             s_out.wait_event(done[slot])
             out.copy_(imgs[slot], non_blocking=True)
@@ -404,6 +406,24 @@ def image_stream(batches, spec, kern, device: int = 0):
     pev, pout, pd = pending
     pev.synchronize()
     yield FinalImage(spec, pout.numpy(), pd.imag_residual_norm, pd.real_norm), diag_dict(pd)
+
+
+_PINNED_POOLS: dict = {}
+
+
+def _pinned_image(pool: list, spec) -> torch.Tensor:
+    """A page-locked (n_v, n_u) float64 tensor from ``pool``: one nobody else
+    references any more (the yielded numpy view holds its tensor), else a new
+    one -- pinning is slow, so steady state allocates nothing and the image
+    is handed out without a host copy."""
+    import sys
+    for t in pool:
+        # references: the pool list, the loop variable, getrefcount's argument
+        if sys.getrefcount(t) <= 3:
+            return t
+    t = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, pin_memory=True)
+    pool.append(t)
+    return t
 
 
 def _host_copy(t: torch.Tensor) -> np.ndarray:
