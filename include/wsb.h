@@ -156,7 +156,9 @@ int wsb_route_count(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, in
 
 /* Pack the exchange send buffers: records for slab d land at
  * [displ_d, displ_d + count_d) in array (gindex) order; optional src_index
- * receives the local index of each packed record (nullable). */
+ * receives the local index of each packed record (nullable). Directly
+ * after wsb_route_count on the same records and slabs (no wsb_prepare in
+ * between) the counts of that call are reused instead of recounted. */
 int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int32_t n_ranks,
                    const int32_t *slab_starts_host, const double *rec, const uint32_t *plane,
                    int64_t n, double *send_rec, uint32_t *send_plane, int64_t *src_index);

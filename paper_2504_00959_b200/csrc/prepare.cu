@@ -281,6 +281,7 @@ int row_histogram(wsb_ctx *ctx, const wsb_grid *g, const double *rec, int64_t n,
 int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v, const double *w,
             const float *vis, const float *weight, int64_t n, int32_t n_chan, double *rec,
             uint32_t *plane) {
+    ctx->route.valid = false;   // records are (re)written
     if (n <= 0) return WSB_OK;
     int *err;
     WSB_TRY(ensure(ctx, kSlotFlag, 64, (void **)&err));
@@ -334,8 +335,9 @@ int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *st
     WSB_TRY(make_slabs(g->n_v, R, starts, &sl));
     const int nb = std::max(1, ceil_div(n, kBlockItems));
     uint32_t *cnt, *off;
-    WSB_TRY(ensure(ctx, kSlotBlockCounts, sizeof(uint32_t) * R * (size_t)nb, (void **)&cnt));
-    WSB_TRY(ensure(ctx, kSlotBlockOffsets, sizeof(uint32_t) * (R * (size_t)nb + 1), (void **)&off));
+    WSB_TRY(ensure(ctx, kSlotRouteCnt, sizeof(uint32_t) * R * (size_t)nb, (void **)&cnt));
+    WSB_TRY(ensure(ctx, kSlotRouteOff, sizeof(uint32_t) * (R * (size_t)nb + 1), (void **)&off));
+    ctx->route.valid = false;
     if (n > 0) {
         k_route_count<<<nb, kThreads, 0, ctx->stream>>>((const double4 *)rec, n, (double)S, sl, R,
                                                         cnt, nb);
@@ -357,6 +359,16 @@ int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *st
     }
     if (offs_out) *offs_out = off;
     if (nb_out) *nb_out = nb;
+    auto &c = ctx->route;
+    c.rec = rec;
+    c.n = n;
+    c.S = S;
+    c.R = R;
+    c.n_v = g->n_v;
+    c.nb = nb;
+    for (int d = 0; d < 8; ++d) c.starts[d] = sl.start[d];
+    c.starts[8] = R;
+    c.valid = true;
     return WSB_OK;
 }
 
@@ -365,10 +377,22 @@ int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *sta
                uint32_t *send_plane, int64_t *src_index) {
     uint32_t *off;
     int nb;
-    WSB_TRY(route_count(ctx, g, S, R, starts, rec, n, nullptr, &off, &nb));
-    if (n <= 0) return WSB_OK;
     Slabs sl;
     WSB_TRY(make_slabs(g->n_v, R, starts, &sl));
+    auto &c = ctx->route;
+    bool hit = c.valid && c.rec == rec && c.n == n && c.S == S && c.R == R && c.n_v == g->n_v &&
+               c.starts[8] == R;
+    for (int d = 0; hit && d < R; ++d) hit = c.starts[d] == sl.start[d];
+    if (hit) {   // the counts of the preceding route_count on these records
+        void *p;
+        WSB_TRY(ensure(ctx, kSlotRouteOff, 0, &p));
+        off = (uint32_t *)p;
+        nb = c.nb;
+    } else {
+        WSB_TRY(route_count(ctx, g, S, R, starts, rec, n, nullptr, &off, &nb));
+    }
+    c.valid = false;
+    if (n <= 0) return WSB_OK;
     k_route_pack<<<nb, kThreads, 0, ctx->stream>>>((const double4 *)rec, plane, n, (double)S, sl,
                                                    R, off, nb, (double4 *)send_rec, send_plane,
                                                    src_index);

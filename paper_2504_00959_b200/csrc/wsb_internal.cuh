@@ -61,6 +61,15 @@ struct wsb_ctx {
     int64_t last_entries = 0, last_tiles = 0;
     uint32_t *last_keys = nullptr, *last_idx = nullptr, *last_off = nullptr;
     int launches = 0;
+    // route_count -> route_pack hand-over: the pack reuses the counts of the
+    // immediately preceding count on the same records and slabs
+    struct {
+        const double *rec = nullptr;
+        int64_t n = -1;
+        int S = -1, R = -1, n_v = -1, nb = 0;
+        int starts[9] = {0};
+        bool valid = false;
+    } route;
     int precision = 64;               // wsb_ctx_set_precision: 64 or 32 (complex64 grids)
     double last_ms[6] = {0, 0, 0, 0, 0, 0};
 };
@@ -94,6 +103,8 @@ enum Slot {
     kSlotRadixTmpA,
     kSlotRadixTmpB,
     kSlotRadixTmpC,
+    kSlotRouteCnt,
+    kSlotRouteOff,
     kSlotCount
 };
 
