@@ -5,6 +5,8 @@
 // fully coalesced (512 contiguous bytes per warp instruction), several
 // independent loads in flight per thread. No protocol, no staging: one
 // launch moves the blocks of all destinations (blockIdx.y = destination).
+#include <cstdlib>
+
 #include "wsb_internal.cuh"
 
 namespace wsb {
@@ -104,7 +106,11 @@ int push_blocks(wsb_ctx *ctx, int n_dest, const void *const *src, void *const *d
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device);
     // about two SMs' worth of CTAs per destination: enough outstanding
     // stores for the link, most SMs stay with the concurrent row pass
-    const int per = (int)std::min<int64_t>(std::min(64, std::max(2, 2 * dev_sms / (n_dest + 1))),
+    // CTAs per destination: enough outstanding stores for the link; capped
+    // (WSB_PUSH_CTAS overrides) so a push overlapping compute leaves it SMs
+    int cap = 64;
+    if (const char *e = std::getenv("WSB_PUSH_CTAS")) cap = std::max(1, std::atoi(e));
+    const int per = (int)std::min<int64_t>(std::min(cap, std::max(2, 2 * dev_sms / (n_dest + 1))),
                                            (most + kPushThreads * kPushUnroll - 1) /
                                                (kPushThreads * kPushUnroll));
     k_push<<<dim3(per, n_dest), kPushThreads, 0, ctx->stream>>>(a);
