@@ -559,6 +559,7 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     };
 
     const double dw = a.n_w > 1 ? (a.w_max - a.w_min) / (double)(a.n_w - 1) : 0.0;
+    // (z in registers instead: 104 B of spills, measured 0.90 vs 0.79 ms)
     for (int e = threadIdx.x; e < C * N; e += CT)
         zbuf[e] = cis_pi(2.0 * dw * (n_of(e / N, prow(e % N)) - 1.0));
 
