@@ -19,6 +19,9 @@ from .imager import (  # noqa: F401
     image,
     image_device,
     image_stream,
+    image_time_chunks,
+    write_dataset,
+    ChunkSpec,
     last_timings,
     partition_1d,
     prepare_device,

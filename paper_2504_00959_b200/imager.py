@@ -526,35 +526,106 @@ class FormatError(Exception):
     """Malformed dataset or image file (visdata.py:60-61)."""
 
 
-def read_dataset(path):
-    """Read an RVIS file: 64-byte header + records of 28 + 12*n_chan bytes.
-    Returns (header dict, dict of column arrays)."""
-    raw = Path(path).read_bytes()
-    if len(raw) < _HEADER.size:
+def _record_dtype(n_chan: int) -> np.dtype:
+    """visdata.py:262-272: 28 + 12 * n_chan bytes per record."""
+    return np.dtype({"names": ["u", "v", "w", "time_index", "vis", "weight"],
+                     "formats": ["<f8", "<f8", "<f8", "<u4", ("<f4", (n_chan, 2)),
+                                 ("<f4", (n_chan,))],
+                     "offsets": [0, 8, 16, 24, 28, 28 + 8 * n_chan],
+                     "itemsize": 28 + 12 * n_chan})
+
+
+@dataclass(frozen=True)
+class ChunkSpec:
+    """Which piece of a dataset to load (visdata.py:217-229): a frequency
+    chunk keeps every record and a contiguous block of channels; a time chunk
+    keeps every channel and the records of a contiguous block of time slices
+    (partition_1d of the slices). The chunks of an axis cover the dataset
+    exactly once."""
+    axis: str
+    chunk_index: int
+    n_chunks: int
+
+    def __post_init__(self):
+        if self.axis not in ("frequency", "time"):
+            raise ValueError(f"axis must be one of ('frequency', 'time'), got {self.axis!r}")
+        if self.n_chunks < 1 or not (0 <= self.chunk_index < self.n_chunks):
+            raise ValueError(f"chunk_index {self.chunk_index} outside range(0, {self.n_chunks})")
+
+
+def read_dataset(path, chunk: ChunkSpec | None = None):
+    """Read an RVIS file (visdata.py:312-341): 64-byte header + records of
+    28 + 12*n_chan bytes, optionally one ChunkSpec of it. The file is memory
+    mapped, so a chunk reads only what it selects. Returns (header dict,
+    dict of column arrays)."""
+    path = Path(path)
+    with open(path, "rb") as fh:
+        head = fh.read(_HEADER.size)
+    if len(head) < _HEADER.size:
         raise FormatError("truncated header")
-    magic, version, n_rec, n_freq, n_corr, n_time, wmin, wmax, res = _HEADER.unpack(raw[:64])
+    magic, version, n_rec, n_freq, n_corr, n_time, wmin, wmax, res = _HEADER.unpack(head)
     if magic != b"RVIS":
         raise FormatError(f"bad magic {magic!r}")
     if version != 1:
         raise FormatError(f"unsupported version {version}")
     n_chan = n_freq * n_corr
-    rec_dt = np.dtype({"names": ["u", "v", "w", "time_index", "vis", "weight"],
-                       "formats": ["<f8", "<f8", "<f8", "<u4", ("<f4", (n_chan, 2)),
-                                   ("<f4", (n_chan,))],
-                       "offsets": [0, 8, 16, 24, 28, 28 + 8 * n_chan],
-                       "itemsize": 28 + 12 * n_chan})
-    body = raw[64:]
-    if len(body) != n_rec * rec_dt.itemsize:
-        raise FormatError(f"truncated file: {len(body)} payload bytes, expected {n_rec * rec_dt.itemsize}")
-    packed = np.frombuffer(body, dtype=rec_dt)
-    vis = (packed["vis"][..., 0] + 1j * packed["vis"][..., 1]).astype(np.complex64)
+    rec_dt = _record_dtype(n_chan)
+    body = path.stat().st_size - _HEADER.size
+    if body != n_rec * rec_dt.itemsize:
+        raise FormatError(f"truncated file: {body} payload bytes, expected {n_rec * rec_dt.itemsize}")
+    packed = (np.memmap(path, dtype=rec_dt, mode="r", offset=_HEADER.size, shape=(n_rec,))
+              if n_rec else np.zeros(0, dtype=rec_dt))
+    c0, c1 = 0, n_chan
+    if chunk is not None and chunk.axis == "frequency":
+        f0, fc = partition_1d(n_freq, chunk.n_chunks, chunk.chunk_index)   # visdata.py:297-300
+        c0, c1 = f0 * n_corr, (f0 + fc) * n_corr
+    elif chunk is not None:
+        s0, sc = partition_1d(n_time, chunk.n_chunks, chunk.chunk_index)   # visdata.py:303-306
+        t = np.asarray(packed["time_index"])
+        packed = packed[(t >= s0) & (t < s0 + sc)]
+    vis_ri = packed["vis"][:, c0:c1]
+    vis = (vis_ri[..., 0] + 1j * vis_ri[..., 1]).astype(np.complex64)
     header = {"n_records": n_rec, "n_freq": n_freq, "n_corr": n_corr, "n_time_slices": n_time,
-              "w_min_native": wmin, "w_max_native": wmax}
+              "w_min_native": wmin, "w_max_native": wmax, "reserved": res}
     cols = {"u": np.ascontiguousarray(packed["u"]), "v": np.ascontiguousarray(packed["v"]),
             "w": np.ascontiguousarray(packed["w"]),
             "time_index": np.ascontiguousarray(packed["time_index"]),
-            "vis": vis, "weight": np.ascontiguousarray(packed["weight"])}
+            "vis": vis, "weight": np.ascontiguousarray(packed["weight"][:, c0:c1])}
     return header, cols
+
+
+def write_dataset(cols: dict, header: dict, path) -> None:
+    """Write an RVIS file (visdata.py:275-293 layout) from column arrays and
+    a header dict as read_dataset returns them; read_dataset of the result is
+    bit-identical."""
+    n = len(cols["u"])
+    n_chan = header["n_freq"] * header["n_corr"]
+    if n != header["n_records"]:
+        raise ValueError(f"header/record count mismatch: {header['n_records']} vs {n}")
+    packed = np.zeros(n, dtype=_record_dtype(n_chan))
+    for k in ("u", "v", "w", "time_index"):
+        packed[k] = cols[k]
+    vis = np.asarray(cols["vis"], np.complex64).reshape(n, n_chan)
+    packed["vis"][..., 0] = vis.real
+    packed["vis"][..., 1] = vis.imag
+    packed["weight"] = np.asarray(cols["weight"], np.float32).reshape(n, n_chan)
+    head = _HEADER.pack(b"RVIS", 1, n, header["n_freq"], header["n_corr"], header["n_time_slices"],
+                        float(header["w_min_native"]), float(header["w_max_native"]),
+                        bytes(header.get("reserved", b"")))
+    with open(path, "wb") as fh:
+        fh.write(head)
+        fh.write(packed.tobytes())
+
+
+def image_time_chunks(path, spec, kern, n_chunks: int, device: int = 0):
+    """Dirty image of each time chunk of an RVIS dataset (ChunkSpec axis
+    "time"), streamed: the next chunk is read and copied to the device while
+    the current one is imaged (image_stream). Yields (FinalImage, diag)."""
+    def batches():
+        for i in range(n_chunks):
+            _, c = read_dataset(path, ChunkSpec("time", i, n_chunks))
+            yield c["u"], c["v"], c["w"], c["vis"], c["weight"]
+    yield from image_stream(batches(), spec, kern, device=device)
 
 
 def write_image(img: FinalImage, base_path, provenance: dict | None = None, pgm: bool = False):

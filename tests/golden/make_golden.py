@@ -190,11 +190,33 @@ def make_images(comms, gridder, mesh, pipeline, visdata):
     np.savez_compressed(HERE / "image.npz", **out)
 
 
+def make_rvis(visdata):
+    """A small multi-channel RVIS file written by the reference and the
+    reference's own reads of it: whole, time chunk 1 of 3, frequency chunk 1
+    of 3 (visdata.py:312-341)."""
+    sky = visdata.SkyModel(sources=((0.01, -0.008, 2.0), (0.0, 0.0, 1.0)))
+    header, chunk = visdata.generate_synthetic(sky, 1500, 3, seed=13, n_corr=2, n_time_slices=8,
+                                               cell_size_lm=1e-3, w_min_native=0.0,
+                                               w_max_native=40.0)
+    path = HERE / "chunks.rvis"
+    visdata.write_dataset(chunk, header, path)
+    out = {}
+    for tag, spec in (("all", None), ("t1of3", visdata.ChunkSpec("time", 1, 3)),
+                      ("f1of3", visdata.ChunkSpec("frequency", 1, 3))):
+        _, c = visdata.read_dataset(path, spec)
+        out.update(chunk_arrays(tag + "_", c))
+    np.savez_compressed(HERE / "rvis.npz", **out)
+
+
 def main():
     comms, gridder, mesh, pipeline, visdata = _ref()
+    if sys.argv[1:] == ["rvis"]:
+        make_rvis(visdata)
+        return
     make_bucket(comms, gridder, mesh, visdata)
     make_grid(comms, gridder, mesh, visdata)
     make_images(comms, gridder, mesh, pipeline, visdata)
+    make_rvis(visdata)
     for f in sorted(HERE.glob("*.npz")):
         print(f.name, f.stat().st_size)
 
