@@ -33,9 +33,6 @@ namespace {
 #ifndef WSB_GRID_MINB
 #define WSB_GRID_MINB 4
 #endif
-#ifndef WSB_GRID_D
-#define WSB_GRID_D 4
-#endif
 constexpr int kWarpsPerCta = WSB_GRID_WARPS;  // independent warps per CTA
 constexpr int kRowBlock = WSB_GRID_ROWS;      // slab rows per work item
 
@@ -157,29 +154,6 @@ __device__ __forceinline__ uint32_t axis_weights(double g, int i0, const KParams
     for (int k = 0; k < W; ++k)
         if (!((mask >> k) & 1)) w[k] = 0.0;
     return mask;
-}
-
-// acc[off + b] += (tr, ti) * wv[b], b < W, for the uniform offset off in
-// [0, NW - W]: one static branch per offset keeps acc in registers.
-template <int W, int NW, int O>
-__device__ __forceinline__ void window_fma(double2 (&acc)[NW], int off, double tr, double ti,
-                                           const double *wv) {
-    if constexpr (O + W <= NW) {
-        if (off == O) {
-#pragma unroll
-            for (int b = 0; b < W; b += 2) {
-                const double2 wv2 = *reinterpret_cast<const double2 *>(wv + b);
-                acc[O + b].x = fma(tr, wv2.x, acc[O + b].x);
-                acc[O + b].y = fma(ti, wv2.x, acc[O + b].y);
-                if (b + 1 < W) {
-                    acc[O + b + 1].x = fma(tr, wv2.y, acc[O + b + 1].x);
-                    acc[O + b + 1].y = fma(ti, wv2.y, acc[O + b + 1].y);
-                }
-            }
-        } else {
-            window_fma<W, NW, O + 1>(acc, off, tr, ti, wv);
-        }
-    }
 }
 
 // Calls f(std::integral_constant<int, phase>) for a runtime phase in [0, W).

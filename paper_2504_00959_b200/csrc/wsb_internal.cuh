@@ -11,7 +11,6 @@
 
 namespace wsb {
 
-constexpr int kTile = 64;          // gridding tile edge (cells)
 constexpr int kG = WSB_P_GROUP;    // P-layout column group
 constexpr int kMaxS = 7;           // largest half support compiled (window 15)
 constexpr int kMaxOnChipLog = 12;  // longest on-chip transform (4096); longer ones split
