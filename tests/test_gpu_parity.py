@@ -357,3 +357,30 @@ def test_image_fp32_medium_and_device_path(W):
     d64, _ = W.image_device(*(torch.from_numpy(np.ascontiguousarray(x)).to(dev)
                               for x in (u, v, w, vis, wt)), spec, kern)
     assert rel_l2(d64.cpu().numpy(), ref["pixels"]) <= 1e-10
+
+
+def test_linearity_complementary_halves(W):
+    """Size-independent parity (the property run_cfg3.py --check applies at
+    cfg3's full size): image(all) = image(A) + image(B) for complementary
+    record halves A, B (other half's weights zeroed), and the update count
+    does not depend on the weights."""
+    import torch
+    rng = np.random.default_rng(17)
+    m = 1_000_000
+    dev = torch.device("cuda", 0)
+    u = torch.from_numpy(rng.uniform(0.1, 0.9, m)).to(dev)
+    v = torch.from_numpy(rng.uniform(0.1, 0.9, m)).to(dev)
+    w = torch.from_numpy(rng.uniform(0.0, 1.0, m)).to(dev)
+    vis = torch.from_numpy((rng.standard_normal(m) + 1j * rng.standard_normal(m)).astype(np.complex64)).to(dev)
+    wt = torch.from_numpy(rng.uniform(0.2, 1.0, m).astype(np.float32)).to(dev)
+    spec = W.GridSpec(1024, 1024, 16, 2e-4, w_max_native=500.0)
+    kern = W.KernelSpec.gaussian(3, 1.0)
+    mask = torch.from_numpy(rng.random(m) < 0.5).to(dev)
+    pall, dall = W.image_device(u, v, w, vis, wt, spec, kern)
+    pall = pall.clone()
+    pa, da = W.image_device(u, v, w, vis, torch.where(mask, wt, 0 * wt), spec, kern)
+    pa = pa.clone()
+    pb, db = W.image_device(u, v, w, vis, torch.where(mask, 0 * wt, wt), spec, kern)
+    assert da["grid_updates"] == db["grid_updates"] == dall["grid_updates"]
+    err = float((pall - pa - pb).norm() / pall.norm())
+    assert err <= 1e-12, err
