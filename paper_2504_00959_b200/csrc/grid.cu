@@ -30,11 +30,15 @@ namespace {
 #ifndef WSB_GRID_ROWS
 #define WSB_GRID_ROWS 128
 #endif
+#ifndef WSB_GRID_RUNROLL
+#define WSB_GRID_RUNROLL 1
+#endif
 #ifndef WSB_GRID_MINB
-#define WSB_GRID_MINB 4
+#define WSB_GRID_MINB 0   // > 0: one occupancy target for every instantiation
 #endif
 constexpr int kWarpsPerCta = WSB_GRID_WARPS;  // independent warps per CTA
 constexpr int kRowBlock = WSB_GRID_ROWS;      // slab rows per work item
+constexpr int kRunUnroll = WSB_GRID_RUNROLL;  // records per iteration of the run loop
 
 __device__ __forceinline__ double chbevl(double x, const double *vals, int n) {
     // numpy _chbevl: b0 = x*b1 - b2 + vals[i] with separate roundings
@@ -201,8 +205,19 @@ struct WarpStage {
 #define ST_VAL(r) st.rec[r].val
 #define ST_IJ(r) st.rec[r].ij
 
+// Resident CTAs per SM the sweep is compiled for (register budget), per
+// (kernel, half_support): measured on cfg2 records (profiles/gridder_minb_r01.txt);
+// the best point moves with each instantiation's register allocation.
 template <int KIND, int S>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, WSB_GRID_MINB) k_grid_sweep(SweepArgs a, KParams<S> kp) {
+constexpr int sweep_min_blocks() {
+    if (WSB_GRID_MINB > 0) return WSB_GRID_MINB;
+    constexpr int gauss[8] = {4, 6, 6, 6, 4, 4, 3, 3};
+    constexpr int kb[8] = {4, 6, 2, 5, 5, 4, 2, 2};
+    return KIND == WSB_KERNEL_GAUSSIAN ? gauss[S] : kb[S];
+}
+
+template <int KIND, int S>
+__global__ void __launch_bounds__(32 * kWarpsPerCta, sweep_min_blocks<KIND, S>()) k_grid_sweep(SweepArgs a, KParams<S> kp) {
     constexpr int W = 2 * S + 1;
     using St = WarpStage<S>;
     __shared__ __align__(16) St stage_all[kWarpsPerCta];
@@ -264,16 +279,18 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, WSB_GRID_MINB) k_grid_sweep
         ++base;
         phase = (p + 1 == W) ? 0 : p + 1;
     };
+    // lane l holds the anchor row of staged record cs+l (INT_MAX past the
+    // chunk end); records are sorted by anchor row, so the staged records
+    // with anchor row == base are the contiguous run starting at r
+    int my_jb = INT_MAX;
     auto run = [&](auto P) {
         constexpr int p = decltype(P)::value;
-        while (r < ce) {
-            const int rr = (int)(r - cs);
-            const int2 ij = ST_IJ(rr);
-            if (ij.y != base) {  // records are sorted by anchor row: base < ij.y
-                emit_slot(P);
-                return;
-            }
-            int k = col - ij.x;
+        const int rr0 = (int)(r - cs);
+        const uint32_t m = __ballot_sync(0xffffffffu, my_jb == base) >> rr0;
+        const int n = __popc(m);
+#pragma unroll kRunUnroll
+        for (int rr = rr0; rr < rr0 + n; ++rr) {
+            int k = col - ST_IJ(rr).x;
             k = (unsigned)k < (unsigned)W ? k : W;   // slot W holds weight 0
             const double2 v = ST_VAL(rr);
             const double wu = ST_WU(rr, k);
@@ -288,8 +305,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, WSB_GRID_MINB) k_grid_sweep
                     acc[(p + b + 1) % W].y = fma(ti, wv2.y, acc[(p + b + 1) % W].y);
                 }
             }
-            ++r;
         }
+        r += n;
+        if (r < ce) emit_slot(P);   // the next record starts lower: row base is final
     };
 
     // the record a lane stages next is gathered one chunk ahead, so the
@@ -313,6 +331,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, WSB_GRID_MINB) k_grid_sweep
             ce = min(cs + 32u, end);
             const uint32_t e = cs + lane;
             const double2 lo = nlo, hi = nhi;
+            my_jb = INT_MAX;
             fetch(e + 32);
             if (e < ce) {
                 const double gu = lo.x, gv = lo.y;
@@ -326,6 +345,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, WSB_GRID_MINB) k_grid_sweep
                 for (int k = 0; k < W; ++k) ST_WV(lane, k) = w[k];
                 ST_VAL(lane) = hi;
                 ST_IJ(lane) = make_int2(ib, jb);
+                my_jb = jb;
                 // cell updates inside this strip and row block (grid_sector's count)
                 const int c_lo = max(col0 - ib, 0), c_hi = min(col0 + ncols - ib, W);
                 const int r_lo = max(R0 - jb, 0), r_hi = min(R1 - jb, W);
