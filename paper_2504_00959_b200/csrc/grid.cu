@@ -199,6 +199,7 @@ struct WarpStage {
         int2 ij;                  // (first window column, first window row)
     };
     Rec rec[32];
+    double2 raw[2][32][2];        // records in flight (cp.async), one chunk ahead
 };
 #define ST_WU(r, k) st.rec[r].wu[k]
 #define ST_WV(r, b) st.rec[r].wv[b]
@@ -211,8 +212,8 @@ struct WarpStage {
 template <int KIND, int S>
 constexpr int sweep_min_blocks() {
     if (WSB_GRID_MINB > 0) return WSB_GRID_MINB;
-    constexpr int gauss[8] = {4, 6, 6, 6, 4, 4, 3, 3};
-    constexpr int kb[8] = {4, 6, 2, 5, 5, 4, 2, 2};
+    constexpr int gauss[8] = {4, 4, 5, 5, 4, 4, 3, 3};
+    constexpr int kb[8] = {4, 6, 2, 6, 5, 2, 2, 2};
     return KIND == WSB_KERNEL_GAUSSIAN ? gauss[S] : kb[S];
 }
 
@@ -310,17 +311,24 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, sweep_min_blocks<KIND, S>()
         if (r < ce) emit_slot(P);   // the next record starts lower: row base is final
     };
 
-    // the record a lane stages next is gathered one chunk ahead, so the
-    // random 32-byte loads overlap the previous chunk's updates
-    double2 nlo = make_double2(0.0, 0.0), nhi = nlo;
-    auto fetch = [&](uint32_t e) {
+    // the record a lane stages next is gathered one chunk ahead by cp.async
+    // into the warp's raw buffer (no registers held across the run, so the
+    // random 32-byte loads overlap the previous chunk's updates), and its
+    // bucket index one chunk before that
+    int buf = 0;
+    auto fetch = [&](uint32_t e, uint32_t id, int b) {
         if (e < end) {
-            const double2 *p = reinterpret_cast<const double2 *>(a.rec + __ldg(&a.idx[e]));
-            nlo = __ldg(p);
-            nhi = __ldg(p + 1);
+            const double2 *src = reinterpret_cast<const double2 *>(a.rec + id);
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&st.raw[b][lane][0]);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16), "l"(src + 1)
+                         : "memory");
         }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    fetch(beg + lane);
+    auto index_at = [&](uint32_t e) { return e < end ? __ldg(&a.idx[e]) : 0u; };
+    fetch(beg + lane, index_at(beg + lane), 0);
+    uint32_t nid = index_at(beg + 32 + lane);
 
     while (true) {
         if (r == ce) {
@@ -330,9 +338,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, sweep_min_blocks<KIND, S>()
             cs = ce;
             ce = min(cs + 32u, end);
             const uint32_t e = cs + lane;
-            const double2 lo = nlo, hi = nhi;
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            const double2 lo = st.raw[buf][lane][0], hi = st.raw[buf][lane][1];
             my_jb = INT_MAX;
-            fetch(e + 32);
+            fetch(e + 32, nid, buf ^ 1);
+            nid = index_at(e + 64);
+            buf ^= 1;
             if (e < ce) {
                 const double gu = lo.x, gv = lo.y;
                 const int ib = (int)floor(gu) - S, jb = (int)floor(gv) - S;
