@@ -308,7 +308,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, sweep_min_blocks<KIND, S>()
             }
         }
         r += n;
-        if (r < ce) emit_slot(P);   // the next record starts lower: row base is final
+        if (r == ce) return true;   // chunk used up: stage the next one, same row
+        emit_slot(P);               // the next record starts lower: row base is final
+        return false;
     };
 
     // the record a lane stages next is gathered one chunk ahead by cp.async
@@ -366,7 +368,24 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, sweep_min_blocks<KIND, S>()
             }
             __syncwarp();
         }
-        dispatch_phase<0, W>(phase, run);
+        // consecutive rows walk the ring statically: one jump-table dispatch
+        // per W rows (and per staged chunk) instead of one per row
+        for (;;) {
+            switch (phase) {
+#define WSB_STEP(q)                                                   \
+    case q:                                                           \
+        if constexpr (q < W) {                                        \
+            if (run(std::integral_constant<int, q>{})) goto next_chunk; \
+        }                                                             \
+        [[fallthrough]];
+                WSB_STEP(0) WSB_STEP(1) WSB_STEP(2) WSB_STEP(3) WSB_STEP(4)
+                WSB_STEP(5) WSB_STEP(6) WSB_STEP(7) WSB_STEP(8) WSB_STEP(9)
+                WSB_STEP(10) WSB_STEP(11) WSB_STEP(12) WSB_STEP(13) WSB_STEP(14)
+#undef WSB_STEP
+                default: break;
+            }
+        }
+    next_chunk:;
     }
     while (base < R1) dispatch_phase<0, W>(phase, emit_slot);
 

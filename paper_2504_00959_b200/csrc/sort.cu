@@ -145,7 +145,10 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const uint32_t *__res
     }
 }
 
-template <int B>
+// LAST: the final pass -- its keys are not needed (the consumers read the
+// values and the key histogram only), so each item's global position is
+// staged in place of its key and only the values are written
+template <int B, bool LAST>
 __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
     uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ offs, int nb) {
@@ -225,13 +228,17 @@ __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
         if (ok && lane == __ffs(peers) - 1) sm.wc[warp][d] += __popc(peers);
         __syncwarp();
         if (ok) {
-            sm.ks[pos] = k[r];
+            sm.ks[pos] = LAST ? sm.goff[d] + (pos - sm.bstart[d]) : k[r];
             sm.vs[pos] = v[r];
         }
     }
     __syncthreads();
     // consecutive threads write consecutive positions of each digit run
     const int64_t nblk = min((int64_t)kRsItems, n - (int64_t)blockIdx.x * kRsItems);
+    if (LAST) {
+        for (int p = threadIdx.x; p < nblk; p += kRsThreads) vout[sm.ks[p]] = sm.vs[p];
+        return;
+    }
     for (int p = threadIdx.x; p < nblk; p += kRsThreads) {
         const uint32_t key = sm.ks[p];
         const uint32_t d = (key >> shift) & (D - 1);
@@ -243,17 +250,17 @@ __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
 
 template <int B>
 int radix_pass(wsb_ctx *ctx, const uint32_t *ka, const uint32_t *va, uint32_t *kb, uint32_t *vb,
-               int64_t n, int shift, uint32_t *hist, int nb) {
+               int64_t n, int shift, uint32_t *hist, int nb, bool last) {
     constexpr int D = 1 << B;
     const size_t hsm = sizeof(uint32_t) * kRsWarps * D, ssm = sizeof(RsSmem<B>);
+    auto scatter = last ? k_radix_scatter<B, true> : k_radix_scatter<B, false>;
     WSB_CUDA_TRY(cudaFuncSetAttribute(k_radix_hist<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)hsm));
-    WSB_CUDA_TRY(cudaFuncSetAttribute(k_radix_scatter<B>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    WSB_CUDA_TRY(cudaFuncSetAttribute(scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
     k_radix_hist<B><<<nb, kRsThreads, hsm, ctx->stream>>>(ka, n, shift, hist, nb);
     ctx->launches += 1;
     WSB_TRY(exclusive_scan_u32(ctx, hist, hist, (int64_t)D * nb, nullptr));
-    k_radix_scatter<B><<<nb, kRsThreads, ssm, ctx->stream>>>(ka, va, kb, vb, n, shift, hist, nb);
+    scatter<<<nb, kRsThreads, ssm, ctx->stream>>>(ka, va, kb, vb, n, shift, hist, nb);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
@@ -301,11 +308,12 @@ int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t 
                    (void **)&hist));
     uint32_t *ka = keys, *kb = keys_alt, *va = vals, *vb = vals_alt;
     for (int shift = 0; shift < bits; shift += B) {
+        const bool last = shift + B >= bits;
         switch (B) {
-            case 8: WSB_TRY(radix_pass<8>(ctx, ka, va, kb, vb, n, shift, hist, nb)); break;
-            case 9: WSB_TRY(radix_pass<9>(ctx, ka, va, kb, vb, n, shift, hist, nb)); break;
-            case 10: WSB_TRY(radix_pass<10>(ctx, ka, va, kb, vb, n, shift, hist, nb)); break;
-            case 11: WSB_TRY(radix_pass<11>(ctx, ka, va, kb, vb, n, shift, hist, nb)); break;
+            case 8: WSB_TRY(radix_pass<8>(ctx, ka, va, kb, vb, n, shift, hist, nb, last)); break;
+            case 9: WSB_TRY(radix_pass<9>(ctx, ka, va, kb, vb, n, shift, hist, nb, last)); break;
+            case 10: WSB_TRY(radix_pass<10>(ctx, ka, va, kb, vb, n, shift, hist, nb, last)); break;
+            case 11: WSB_TRY(radix_pass<11>(ctx, ka, va, kb, vb, n, shift, hist, nb, last)); break;
             default: return fail(WSB_EUNSUPPORTED, "radix digit width");
         }
         uint32_t *t = ka; ka = kb; kb = t;

@@ -115,7 +115,8 @@ int exclusive_scan_u32(wsb_ctx *ctx, const uint32_t *in, uint32_t *out, int64_t 
                        uint32_t *total_host);
 
 // sort.cu: stable LSD radix sort of (key, val) pairs by the low `bits` of key.
-// Returns the buffers holding the result in *keys_out/*vals_out.
+// Returns the buffers holding the result in *keys_out/*vals_out; the final
+// pass writes the values only (*keys_out then holds a previous pass's keys).
 int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
                      uint32_t *vals_alt, int64_t n, int bits, uint32_t **keys_out,
                      uint32_t **vals_out);
