@@ -524,6 +524,13 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    # stdout carries exactly the one JSON line: native libraries (NCCL prints
+    # its version banner at communicator init) write to fd 1 directly, so fd 1
+    # is pointed at stderr and Python's stdout keeps a private copy of it
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(json_fd, "w", buffering=1)
     if args.warmup < 3 and args.impl == "ours":
         log("note: warmup < 3 does not meet the timing rules")
     if args.impl == "reference":
