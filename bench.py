@@ -189,7 +189,8 @@ def run_ours(args):
 
     def step():
         if ws > 1:
-            return WD.image_distributed(du, dv, dw, dvis, dwt, spec, kern, to_host=False)
+            return WD.image_distributed(du, dv, dw, dvis, dwt, spec, kern, to_host=False,
+                                        decomposition=args.decomp)
         return W.image_device(du, dv, dw, dvis, dwt, spec, kern, image_out=img)
 
     clk = ClockSampler(dev.index).__enter__()   # sampling runs through warm-up and timing
@@ -238,7 +239,8 @@ def run_ours(args):
         n_st = 3
         for _ in range(n_st):
             tm = {}
-            WD.image_distributed(du, dv, dw, dvis, dwt, spec, kern, to_host=False, timings=tm)
+            WD.image_distributed(du, dv, dw, dvis, dwt, spec, kern, to_host=False, timings=tm,
+                                 decomposition=args.decomp)
             for k_, v_ in tm.items():
                 acc[k_] = acc.get(k_, 0.0) + v_ / n_st
         stages = {k_: round(v_, 4) for k_, v_ in acc.items()}
@@ -281,13 +283,14 @@ def run_ours(args):
         # host image on the root; wall time per step, max over ranks
         pin = [torch.from_numpy(a).pin_memory().numpy() for a in (u, v, w, vis, wt)]
         batch = tuple(pin)
-        for _r in WD.image_distributed_stream([batch] * 2, spec, kern):
+        for _r in WD.image_distributed_stream([batch] * 2, spec, kern, decomposition=args.decomp):
             pass
         torch.cuda.synchronize()
         n_e2e = max(4, min(args.steps, 12))
         dist.barrier()
         t0 = time.perf_counter()
-        for res, _ in WD.image_distributed_stream([batch] * n_e2e, spec, kern):
+        for res, _ in WD.image_distributed_stream([batch] * n_e2e, spec, kern,
+                                                  decomposition=args.decomp):
             pass
         torch.cuda.synchronize()
         e2e_s = torch.tensor([(time.perf_counter() - t0) / n_e2e], dtype=torch.float64, device=dev)
@@ -364,7 +367,8 @@ def run_ours(args):
                                "32 w-planes, Gaussian support 7 (S=3, sigma=1), single channel, FP64",
                    "records_per_gpu": cfg["n_vis"], "n_u": cfg["n_u"], "n_v": cfg["n_v"],
                    "n_w": cfg["n_w"], "cell_size_lm": cfg["cell"], "w_max_native": cfg["w_max"],
-                   "parallelism": f"v-slab x{ws}" if ws > 1 else "single GPU",
+                   "parallelism": ((f"v-slab x{ws}" if args.decomp == "slabs" else f"w-plane ranges x{ws}")
+                                   if ws > 1 else "single GPU"),
                    "l2": "inputs 360 MB and grid 2 GiB exceed the 126 MB L2; no flush"},
         "gridding_mvis_s": round(cfg["n_vis"] / (gridder["ms"] / 1e3) / 1e6, 1) if gridder["ms"] else None,
         "roofline": roof,
@@ -523,6 +527,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--decomp", choices=["slabs", "planes"], default="slabs",
+                    help="multi-GPU decomposition: v-slabs (grid transpose) or w-plane ranges "
+                         "(partial-stack reduce)")
     args = ap.parse_args()
     # stdout carries exactly the one JSON line: native libraries (NCCL prints
     # its version banner at communicator init) write to fd 1 directly, so fd 1

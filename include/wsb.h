@@ -163,6 +163,23 @@ int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int
                    const int32_t *slab_starts_host, const double *rec, const uint32_t *plane,
                    int64_t n, double *send_rec, uint32_t *send_plane, int64_t *src_index);
 
+/* w-plane decomposition (the alternative to the v-slabs above): rank d
+ * owns the planes [plane_starts[d], plane_starts[d+1]) (plane_starts[0] = 0
+ * < ... < plane_starts[n_ranks] = n_w) and grids, transforms and stacks
+ * them on its own; the ranks' partial images are summed afterwards
+ * (wsb_fft_cols_partial, wsb_image_finish). Each record goes to exactly one
+ * rank (no halo). Counts per destination, as wsb_route_count. Synchronous. */
+int wsb_route_planes_count(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_ranks,
+                           const int32_t *plane_starts_host, const double *rec,
+                           const uint32_t *plane, int64_t n, int64_t *counts_host);
+
+/* Pack for the plane decomposition, as wsb_route_pack; send_plane holds the
+ * plane index relative to the destination's first plane. */
+int wsb_route_planes_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_ranks,
+                          const int32_t *plane_starts_host, const double *rec,
+                          const uint32_t *plane, int64_t n, double *send_rec,
+                          uint32_t *send_plane, int64_t *src_index);
+
 /* Records per anchor row floor(gv) of prepared records: hist u32[n_v]
  * (device). Feeds the load balancing of the slab rows (the
  * v-slabs of partition_1d are unbalanced for centrally concentrated uv
@@ -241,6 +258,31 @@ int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
                        const int32_t *src_rows_host, int32_t g0, int32_t ng,
                        int32_t plane_lo, int32_t plane_hi, const double *tgrid,
                        double *image_strip, double *norm_partials);
+
+/* Column pass + stack for the w-plane decomposition: this rank stacks the
+ * planes [rank_plane_lo, rank_plane_hi) over all n_v rows and n_u columns;
+ * tgrid holds planes [plane_lo, plane_hi) in the P layout (the output of
+ * wsb_fft_rows of the rank's full-height grid, one destination). Ranges in
+ * DESCENDING order as for wsb_fft_cols_stack, the first ending at
+ * rank_plane_hi. The call whose range starts at rank_plane_lo writes
+ * partial_image c128[n_v][n_u] = sum_k P_k exp(2 pi i w_k (n-1)) over the
+ * rank's planes (unscaled); earlier calls leave it untouched. The sum of
+ * the ranks' partial images goes through wsb_image_finish. */
+int wsb_fft_cols_partial(wsb_ctx *ctx, const wsb_grid *grid, int32_t plane_lo, int32_t plane_hi,
+                         int32_t rank_plane_lo, int32_t rank_plane_hi, const double *tgrid,
+                         double *partial_image);
+
+/* Number of row residues of wsb_image_finish's norm partials. */
+#define WSB_FINISH_SPLIT(n_v) ((n_v) >= 4096 ? 16 : ((n_v) >= 256 ? (n_v) / 256 : 1))
+
+/* Finish of a summed partial-stack image (w-plane decomposition): image
+ * f64[n_v][n_u] = Re(sum / (n_u n_v) / n_w * n) (transform.py:192-230, the
+ * same operations as the column pass' finish) and norm_partials
+ * f64[WSB_FINISH_SPLIT(n_v)][n_u][2] = (sum Im^2, sum Re^2) per column and
+ * row block (rows in order); the caller sums them residue-major, columns in
+ * order. Enqueued. */
+int wsb_image_finish(wsb_ctx *ctx, const wsb_grid *grid, const double *image_sum, double *image,
+                     double *norm_partials);
 
 /* Debug / parity: strip-layout slab -> natural (plane, row, col) complex128
  * with the checkerboard sign removed (the grid_all output layout,

@@ -29,7 +29,8 @@ EXPORTS = (
     "wsb_ctx_set_stream", "wsb_ctx_trim", "wsb_image", "wsb_image_device", "wsb_prepare",
     "wsb_route_count", "wsb_route_pack", "wsb_grid_slab", "wsb_fft_rows", "wsb_fft_cols_stack",
     "wsb_grid_unpack", "wsb_tiles_debug", "wsb_last_timings", "wsb_row_histogram",
-    "wsb_fft_rows_peer", "wsb_push_blocks", "wsb_ctx_set_precision",
+    "wsb_fft_rows_peer", "wsb_push_blocks", "wsb_ctx_set_precision", "wsb_route_planes_count",
+    "wsb_route_planes_pack", "wsb_fft_cols_partial", "wsb_image_finish",
 )
 
 
@@ -89,6 +90,10 @@ def lib() -> C.CDLL:
         "wsb_route_count": (C.c_int, [p, G, i32, i32, p, p, i64, p]),
         "wsb_route_pack": (C.c_int, [p, G, i32, i32, p, p, p, i64, p, p, p]),
         "wsb_row_histogram": (C.c_int, [p, G, p, i64, p]),
+        "wsb_route_planes_count": (C.c_int, [p, G, i32, p, p, p, i64, p]),
+        "wsb_route_planes_pack": (C.c_int, [p, G, i32, p, p, p, i64, p, p, p]),
+        "wsb_fft_cols_partial": (C.c_int, [p, G, i32, i32, i32, i32, p, p]),
+        "wsb_image_finish": (C.c_int, [p, G, p, p, p]),
         "wsb_grid_slab": (C.c_int, [p, G, K, i32, i32, p, p, i64, p, p]),
         "wsb_fft_rows": (C.c_int, [p, G, i32, p, p, i32, i32, i32, p]),
         "wsb_fft_rows_peer": (C.c_int, [p, G, i32, p, i32, i32, i32, p, p]),

@@ -240,6 +240,27 @@ int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int
                            send_rec, send_plane, src_index);
 }
 
+int wsb_route_planes_count(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_ranks,
+                           const int32_t *plane_starts_host, const double *rec,
+                           const uint32_t *plane, int64_t n, int64_t *counts_host) {
+    if (!ctx || !counts_host) return fail(WSB_EINVAL, "NULL argument");
+    WSB_TRY(validate_grid(grid));
+    WSB_TRY(set_device(ctx));
+    return wsb::route_count(ctx, grid, 0, n_ranks, plane_starts_host, rec, n, counts_host, nullptr,
+                            nullptr, plane, 1);
+}
+
+int wsb_route_planes_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_ranks,
+                          const int32_t *plane_starts_host, const double *rec,
+                          const uint32_t *plane, int64_t n, double *send_rec,
+                          uint32_t *send_plane, int64_t *src_index) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    WSB_TRY(validate_grid(grid));
+    WSB_TRY(set_device(ctx));
+    return wsb::route_pack(ctx, grid, 0, n_ranks, plane_starts_host, rec, plane, n, send_rec,
+                           send_plane, src_index, 1);
+}
+
 int wsb_row_histogram(wsb_ctx *ctx, const wsb_grid *grid, const double *rec, int64_t n,
                       uint32_t *hist) {
     if (!ctx || !hist) return fail(WSB_EINVAL, "NULL argument");
@@ -333,6 +354,28 @@ int wsb_fft_cols_stack(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_sources,
     WSB_TRY(set_device(ctx));
     return fft_cols_stack(ctx, grid, n_sources, src_rows_host, g0, ng, plane_lo, plane_hi, tgrid,
                           image_strip, norm_partials);
+}
+
+int wsb_fft_cols_partial(wsb_ctx *ctx, const wsb_grid *grid, int32_t plane_lo, int32_t plane_hi,
+                         int32_t rank_plane_lo, int32_t rank_plane_hi, const double *tgrid,
+                         double *partial_image) {
+    if (!ctx || !tgrid || !partial_image) return fail(WSB_EINVAL, "NULL argument");
+    WSB_TRY(validate_grid(grid));
+    if (!(0 <= rank_plane_lo && rank_plane_lo <= plane_lo && plane_lo < plane_hi &&
+          plane_hi <= rank_plane_hi && rank_plane_hi <= grid->n_w))
+        return fail(WSB_EINVAL, "plane range outside the rank's planes");
+    WSB_TRY(set_device(ctx));
+    const int32_t rows[1] = {grid->n_v};
+    return fft_cols_stack(ctx, grid, 1, rows, 0, grid->n_u / kG, plane_lo, plane_hi, tgrid, nullptr,
+                          nullptr, 64, rank_plane_lo, rank_plane_hi, partial_image);
+}
+
+int wsb_image_finish(wsb_ctx *ctx, const wsb_grid *grid, const double *image_sum, double *image,
+                     double *norm_partials) {
+    if (!ctx || !image_sum || !image || !norm_partials) return fail(WSB_EINVAL, "NULL argument");
+    WSB_TRY(validate_grid(grid));
+    WSB_TRY(set_device(ctx));
+    return image_finish(ctx, grid, image_sum, image, norm_partials);
 }
 
 int wsb_grid_unpack(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t v_count,

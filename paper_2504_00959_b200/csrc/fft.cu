@@ -439,6 +439,9 @@ struct ColArgs {
     const void *twN;        // exp(2 pi i m / n_v), m < n_v (split columns only)
     int n_w, n_u, n_v, ncols, g0;
     int k0, k1;             // plane range of this call
+    int k_top, k_bottom;    // planes this process stacks: [k_bottom, k_top) (default [0, n_w))
+    double2 *pimg;          // non-null: write the partial stack of [k_bottom, k_top) as a
+                            // complex128 image [n_v][ncols] instead of finishing
     int n_src;
     int src_start[9];       // row start of each source slab (+ sentinel)
     double cell, inv_nuv, inv_nw, w_min, w_max;
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     double2 *run = a.run + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * kColE * CT + threadIdx.x;
     double2 acc[kColE];
 #pragma unroll
-    for (int i = 0; i < kColE; ++i) acc[i] = a.k1 < a.n_w ? run[i * CT] : make_double2(0.0, 0.0);
+    for (int i = 0; i < kColE; ++i) acc[i] = a.k1 < a.k_top ? run[i * CT] : make_double2(0.0, 0.0);
     if constexpr (SPL == 0) prefetch(nk - 1);
 
     for (int kl = nk - 1; kl >= 0; --kl) {
@@ -609,7 +612,7 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
         }
     }
 
-    if (a.k0 > 0) {  // planes below this range to come: park the running stack
+    if (a.k0 > a.k_bottom) {  // planes below this range to come: park the running stack
 #pragma unroll
         for (int i = 0; i < kColE; ++i) run[i * CT] = acc[i];
         return;
@@ -620,7 +623,31 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     // the image strip is written row by row and the residual norms are
     // reduced per column in a fixed tree order (identical for any GPU count).
     __syncthreads();  // both plane buffers are free now
-    const double w0 = plane_w(a, 0);
+    const double w0 = plane_w(a, a.k0);   // k0 = k_bottom: phase of the lowest stacked plane
+    if (a.pimg) {
+        // partial stack of a plane range (w-plane decomposition): sum_k P_k
+        // exp(2 pi i w_k (n-1)) over [k_bottom, k_top); summed over the ranks
+        // and finished by k_image_finish
+        double2 *pix = sbuf;
+#pragma unroll
+        for (int kb = 0; kb < NB; ++kb) {
+            const int b = threadIdx.x + kb * CT;
+            const int seq = b / M, j = b % M;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int row = j + r * M;
+                const double n = n_of(seq, prow(row));
+                pix[seq * STRIDE + pidx(row)] = cmul(acc[kb * R + r], cis_pi(2.0 * w0 * (n - 1.0)));
+            }
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < C * N; e += CT) {
+            const int cc = e % C, row = e / C;
+            if (c0 + cc < a.ncols)
+                a.pimg[(int64_t)prow(row) * a.ncols + c0 + cc] = pix[cc * STRIDE + pidx(row)];
+        }
+        return;
+    }
     double2 *pix = sbuf;                        // (re, im) per pixel, [C][STRIDE]
     double2 *sq = sbuf + C * STRIDE;            // (im^2, re^2) per pixel
 #pragma unroll
@@ -663,6 +690,47 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
             a.partials[2 * ((int64_t)eres * a.ncols + c0 + cc) + 0] = sq[cc * STRIDE].x;
             a.partials[2 * ((int64_t)eres * a.ncols + c0 + cc) + 1] = sq[cc * STRIDE].y;
         }
+}
+
+// Finish of a summed partial-stack image (w-plane decomposition): the same
+// per-pixel operations as k_fft_cols' finish -- /(n_u n_v), /n_w, * n, real
+// part -- and per-column residual norm partials [residue][column][2], row
+// residues e = blockIdx.y summed in row order (fixed association).
+__global__ void __launch_bounds__(256) k_image_finish(const double2 *__restrict__ sum, int n_u,
+                                                      int n_v, double cell, double inv_nuv,
+                                                      double inv_nw, double *__restrict__ image,
+                                                      double *__restrict__ partials) {
+    __shared__ double2 red[8][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int col = blockIdx.x * 32 + tx;
+    const int rs = gridDim.y, e = blockIdx.y;
+    const int rows = n_v / rs, r0 = e * rows;
+    double2 s = make_double2(0.0, 0.0);
+    if (col < n_u) {
+        const double l = (double)(col - n_u / 2) * cell;
+        for (int row = r0 + ty; row < r0 + rows; row += 8) {
+            const double m = (double)(row - n_v / 2) * cell;
+            const double n = __dsqrt_rn(__dsub_rn(__dsub_rn(1.0, __dmul_rn(l, l)), __dmul_rn(m, m)));
+            double2 z = sum[(int64_t)row * n_u + col];
+            z.x *= inv_nuv;
+            z.y *= inv_nuv;
+            z.x = __dmul_rn(z.x, inv_nw);
+            z.y = __dmul_rn(z.y, inv_nw);
+            const double re = __dsub_rn(__dmul_rn(z.x, n), __dmul_rn(z.y, 0.0));
+            const double im = __dadd_rn(__dmul_rn(z.x, 0.0), __dmul_rn(z.y, n));
+            image[(int64_t)row * n_u + col] = re;
+            s.x += __dmul_rn(im, im);
+            s.y += __dmul_rn(re, re);
+        }
+    }
+    red[ty][tx] = s;
+    __syncthreads();
+    if (ty == 0 && col < n_u) {
+        double2 t = red[0][tx];
+        for (int k = 1; k < 8; ++k) t = make_double2(t.x + red[k][tx].x, t.y + red[k][tx].y);
+        partials[2 * ((int64_t)e * n_u + col) + 0] = t.x;
+        partials[2 * ((int64_t)e * n_u + col) + 1] = t.y;
+    }
 }
 
 // pass-ordered twiddle table of an N-point plan (see tw_offset): entry [t]
@@ -859,8 +927,11 @@ int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const void *grid_a, v
 
 int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t *src_rows,
                    int g0, int ng, int plo, int phi, const void *tgrid, double *image_strip,
-                   double *norm_partials, int prec) {
+                   double *norm_partials, int prec, int k_bottom, int k_top, double *partial_img) {
     if (phi <= plo) return WSB_OK;
+    if (k_top < 0) k_top = g->n_w;
+    if (!(0 <= k_bottom && k_bottom <= plo && phi <= k_top && k_top <= g->n_w))
+        return fail(WSB_EINVAL, "plane range outside the stacked planes");
     if (n_sources < 1 || n_sources > 8) return fail(WSB_EINVAL, "n_sources must be in [1, 8]");
     ColArgs a;
     a.tgrid = tgrid;
@@ -885,6 +956,9 @@ int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t
     a.w_max = g->w_max_native;
     a.k0 = plo;
     a.k1 = phi;
+    a.k_top = k_top;
+    a.k_bottom = k_bottom;
+    a.pimg = (double2 *)partial_img;
     // columns above the on-chip 4096 points: SP = n_v / 4096 residue CTAs
     const int logn = ilog2(g->n_v), logs = std::min(logn, kMaxOnChipLog), spl = logn - logs;
     // the running stack (complex128): one per thread element of the launch
@@ -894,6 +968,17 @@ int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t
         WSB_TRY(ensure(ctx, kSlotColRun, bytes, (void **)&a.run));
     }
     return prec == 32 ? cols_dispatch<float2>(ctx, a, g->n_v) : cols_dispatch<double2>(ctx, a, g->n_v);
+}
+
+int image_finish(wsb_ctx *ctx, const wsb_grid *g, const double *sum, double *image,
+                 double *norm_partials) {
+    const int rs = WSB_FINISH_SPLIT(g->n_v);
+    k_image_finish<<<dim3(ceil_div(g->n_u, 32), rs), 256, 0, ctx->stream>>>(
+        (const double2 *)sum, g->n_u, g->n_v, g->cell_size_lm, 1.0 / ((double)g->n_u * (double)g->n_v),
+        1.0 / (double)g->n_w, image, norm_partials);
+    ctx->launches += 1;
+    WSB_CUDA_TRY(cudaGetLastError());
+    return WSB_OK;
 }
 
 }  // namespace wsb

@@ -143,10 +143,18 @@ __device__ __forceinline__ uint32_t block_excl_sum256(uint32_t x, uint32_t *tota
 struct Slabs {
     int start[8];
     int count[8];
+    int by_plane;   // 1: ranges of w planes (each record to the one owner of its plane)
 };
 
-__device__ __forceinline__ uint32_t dest_mask(double gv, double S, const Slabs &sl, int R) {
+__device__ __forceinline__ uint32_t dest_mask(double gv, uint32_t p, double S, const Slabs &sl,
+                                              int R) {
     uint32_t m = 0;
+    if (sl.by_plane) {
+#pragma unroll
+        for (int d = 0; d < 8; ++d)
+            m |= (uint32_t)(d < R && (int)p >= sl.start[d] && (int)p < sl.start[d] + sl.count[d]) << d;
+        return m;
+    }
     const double hi = __dadd_rn(gv, S), lo = __dsub_rn(gv, S);  // comms.py:521-523
 #pragma unroll
     for (int d = 0; d < 8; ++d) {
@@ -158,6 +166,7 @@ __device__ __forceinline__ uint32_t dest_mask(double gv, double S, const Slabs &
 }
 
 __global__ void __launch_bounds__(kThreads) k_route_count(const double4 *__restrict__ rec,
+                                                          const uint32_t *__restrict__ plane,
                                                           int64_t n, double S, Slabs sl, int R,
                                                           uint32_t *counts /*[R][nb]*/, int nb) {
     __shared__ uint32_t c[8];
@@ -168,7 +177,7 @@ __global__ void __launch_bounds__(kThreads) k_route_count(const double4 *__restr
     for (int it = 0; it < kBlockItems / kThreads; ++it) {
         int64_t i = base + it * kThreads + threadIdx.x;
         if (i < n) {
-            uint32_t m = dest_mask(rec[i].y, S, sl, R);
+            uint32_t m = dest_mask(rec[i].y, sl.by_plane ? plane[i] : 0u, S, sl, R);
 #pragma unroll
             for (int d = 0; d < 8; ++d) local[d] += (m >> d) & 1u;
         }
@@ -208,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) k_route_pack(
         if (i < n) {
             r = rec[i];
             p = plane[i];
-            m = dest_mask(r.y, S, sl, R);
+            m = dest_mask(r.y, p, S, sl, R);
         }
         uint32_t in_warp[8];
 #pragma unroll
@@ -233,7 +242,7 @@ __global__ void __launch_bounds__(kThreads) k_route_pack(
                 if ((m >> d) & 1u) {
                     const uint32_t pos = run[d] + before + in_warp[d];
                     send_rec[pos] = r;
-                    send_plane[pos] = p;
+                    send_plane[pos] = sl.by_plane ? p - (uint32_t)sl.start[d] : p;
                     if (src_index) src_index[pos] = i;
                 }
                 run[d] += tot;
@@ -309,6 +318,7 @@ int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v, c
 // Slab rows: partition_1d (mesh.py:34-45) or explicit starts (load-balanced
 // slabs: starts[0] = 0 < starts[1] < ... < starts[R] = n_v).
 static int make_slabs(int n_v, int R, const int32_t *starts, Slabs *sl) {
+    sl->by_plane = 0;
     if (R < 1 || R > 8) return fail(WSB_EINVAL, "n_ranks must be in [1, 8]");
     if (R > n_v) return fail(WSB_EINVAL, "n_ranks exceeds n_v");
     if (starts) {
@@ -328,19 +338,39 @@ static int make_slabs(int n_v, int R, const int32_t *starts, Slabs *sl) {
     return WSB_OK;
 }
 
+// Plane ranges [starts[d], starts[d+1]) over [0, n_w] (w-plane decomposition).
+static int make_plane_ranges(int n_w, int R, const int32_t *starts, Slabs *sl) {
+    if (R < 1 || R > 8) return fail(WSB_EINVAL, "n_ranks must be in [1, 8]");
+    if (R > n_w) return fail(WSB_EINVAL, "n_ranks exceeds n_w");
+    if (!starts) return fail(WSB_EINVAL, "plane_starts is NULL");
+    if (starts[0] != 0 || starts[R] != n_w) return fail(WSB_EINVAL, "plane starts must span [0, n_w]");
+    for (int d = 0; d < R; ++d) {
+        if (starts[d + 1] <= starts[d]) return fail(WSB_EINVAL, "plane starts must increase");
+        sl->start[d] = starts[d];
+        sl->count[d] = starts[d + 1] - starts[d];
+    }
+    sl->by_plane = 1;
+    return WSB_OK;
+}
+
+static int make_routing(const wsb_grid *g, int R, const int32_t *starts, int by_plane, Slabs *sl) {
+    return by_plane ? make_plane_ranges(g->n_w, R, starts, sl) : make_slabs(g->n_v, R, starts, sl);
+}
+
 int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *starts,
                 const double *rec, int64_t n, int64_t *counts_host, uint32_t **offs_out,
-                int *nb_out) {
+                int *nb_out, const uint32_t *plane, int by_plane) {
     Slabs sl;
-    WSB_TRY(make_slabs(g->n_v, R, starts, &sl));
+    WSB_TRY(make_routing(g, R, starts, by_plane, &sl));
+    if (by_plane && n > 0 && !plane) return fail(WSB_EINVAL, "plane is NULL");
     const int nb = std::max(1, ceil_div(n, kBlockItems));
     uint32_t *cnt, *off;
     WSB_TRY(ensure(ctx, kSlotRouteCnt, sizeof(uint32_t) * R * (size_t)nb, (void **)&cnt));
     WSB_TRY(ensure(ctx, kSlotRouteOff, sizeof(uint32_t) * (R * (size_t)nb + 1), (void **)&off));
     ctx->route.valid = false;
     if (n > 0) {
-        k_route_count<<<nb, kThreads, 0, ctx->stream>>>((const double4 *)rec, n, (double)S, sl, R,
-                                                        cnt, nb);
+        k_route_count<<<nb, kThreads, 0, ctx->stream>>>((const double4 *)rec, plane, n, (double)S,
+                                                        sl, R, cnt, nb);
         ctx->launches += 1;
         WSB_CUDA_TRY(cudaGetLastError());
     } else {
@@ -364,7 +394,7 @@ int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *st
     c.n = n;
     c.S = S;
     c.R = R;
-    c.n_v = g->n_v;
+    c.n_v = by_plane ? -g->n_w : g->n_v;
     c.nb = nb;
     for (int d = 0; d < 8; ++d) c.starts[d] = sl.start[d];
     c.starts[8] = R;
@@ -374,13 +404,14 @@ int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *st
 
 int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *starts,
                const double *rec, const uint32_t *plane, int64_t n, double *send_rec,
-               uint32_t *send_plane, int64_t *src_index) {
+               uint32_t *send_plane, int64_t *src_index, int by_plane) {
     uint32_t *off;
     int nb;
     Slabs sl;
-    WSB_TRY(make_slabs(g->n_v, R, starts, &sl));
+    WSB_TRY(make_routing(g, R, starts, by_plane, &sl));
     auto &c = ctx->route;
-    bool hit = c.valid && c.rec == rec && c.n == n && c.S == S && c.R == R && c.n_v == g->n_v &&
+    bool hit = c.valid && c.rec == rec && c.n == n && c.S == S && c.R == R &&
+               c.n_v == (by_plane ? -g->n_w : g->n_v) &&
                c.starts[8] == R;
     for (int d = 0; hit && d < R; ++d) hit = c.starts[d] == sl.start[d];
     if (hit) {   // the counts of the preceding route_count on these records
@@ -389,7 +420,7 @@ int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *sta
         off = (uint32_t *)p;
         nb = c.nb;
     } else {
-        WSB_TRY(route_count(ctx, g, S, R, starts, rec, n, nullptr, &off, &nb));
+        WSB_TRY(route_count(ctx, g, S, R, starts, rec, n, nullptr, &off, &nb, plane, by_plane));
     }
     c.valid = false;
     if (n <= 0) return WSB_OK;

@@ -125,12 +125,14 @@ int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t 
 int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v,
             const double *w, const float *vis, const float *weight, int64_t n,
             int32_t n_chan, double *rec, uint32_t *plane);
+// by_plane = 0: v-slabs with the +-S halo; 1: w-plane ranges (plane is read,
+// packed planes are rebased to the destination's first plane)
 int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *starts,
                 const double *rec, int64_t n, int64_t *counts_host, uint32_t **offs_out,
-                int *nb_out);
+                int *nb_out, const uint32_t *plane = nullptr, int by_plane = 0);
 int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *starts,
                const double *rec, const uint32_t *plane, int64_t n, double *send_rec,
-               uint32_t *send_plane, int64_t *src_index);
+               uint32_t *send_plane, int64_t *src_index, int by_plane = 0);
 int row_histogram(wsb_ctx *ctx, const wsb_grid *g, const double *rec, int64_t n, uint32_t *hist);
 
 // bucket.cu: records of a slab bucketed by (plane, 32-column strip, anchor row)
@@ -160,7 +162,10 @@ int fft_rows(wsb_ctx *ctx, const wsb_grid *g, int v_count, const void *grid_a, v
              void *const *dest_ptrs = nullptr, int prec = 64);
 int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t *src_rows,
                    int g0, int ng, int plane_lo, int plane_hi, const void *tgrid,
-                   double *image_strip, double *norm_partials, int prec = 64);
+                   double *image_strip, double *norm_partials, int prec = 64,
+                   int k_bottom = 0, int k_top = -1, double *partial_img = nullptr);
+int image_finish(wsb_ctx *ctx, const wsb_grid *g, const double *sum, double *image,
+                 double *norm_partials);
 int strip_to_image(wsb_ctx *ctx, const wsb_grid *g, const double *strip, double *image);
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }

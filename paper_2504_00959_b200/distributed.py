@@ -127,6 +127,47 @@ class CudaBackend:
                                            _ptr(strip), _ptr(partials)))
         return (strip, partials) if final else (None, None)
 
+    # ---- w-plane decomposition ------------------------------------------------
+    def route_planes(self, rec, plane, spec, R, starts):
+        """Records to the owners of their planes; planes rebased per owner."""
+        g = spec.c_struct()
+        n = rec.shape[0]
+        counts = (C.c_int64 * R)()
+        st = (C.c_int32 * (R + 1))(*starts)
+        lib, h = L.lib(), self.ctx.handle
+        L.check(lib.wsb_route_planes_count(h, C.byref(g), R, st, _ptr(rec), _ptr(plane), n, counts))
+        counts = [int(c) for c in counts]
+        tot = sum(counts)
+        srec = torch.empty((max(tot, 1), 4), dtype=torch.float64, device=self.device)
+        spl = torch.empty(max(tot, 1), dtype=torch.int32, device=self.device)
+        L.check(lib.wsb_route_planes_pack(h, C.byref(g), R, st, _ptr(rec), _ptr(plane), n,
+                                          _ptr(srec), _ptr(spl), None))
+        return srec[:tot], spl[:tot], counts
+
+    def fft_cols_partial(self, tgrid, spec, plane_lo, plane_hi, rank_lo, rank_hi, pimg):
+        """Column pass + stack of planes [plane_lo, plane_hi) of this rank's
+        [rank_lo, rank_hi); the call starting at rank_lo writes ``pimg``
+        (complex128 [n_v][n_u] as float64 [..., 2])."""
+        g = spec.c_struct()
+        L.check(L.lib().wsb_fft_cols_partial(self.ctx.handle, C.byref(g), int(plane_lo),
+                                             int(plane_hi), int(rank_lo), int(rank_hi),
+                                             _ptr(tgrid), _ptr(pimg)))
+
+    def image_finish(self, pimg, spec):
+        """Summed partial stacks -> (image [n_v, n_u], norm partials [RS, n_u, 2])."""
+        g = spec.c_struct()
+        img = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, device=self.device)
+        parts = torch.empty((finish_split(spec.n_v), spec.n_u, 2), dtype=torch.float64,
+                            device=self.device)
+        L.check(L.lib().wsb_image_finish(self.ctx.handle, C.byref(g), _ptr(pimg), _ptr(img),
+                                         _ptr(parts)))
+        return img, parts
+
+
+def finish_split(n_v: int) -> int:
+    """WSB_FINISH_SPLIT: row blocks of wsb_image_finish's norm partials."""
+    return 16 if n_v >= 4096 else (n_v // 256 if n_v >= 256 else 1)
+
 
 def _a2a(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group, async_op=False):
     return dist.all_to_all_single(out, inp, output_split_sizes=list(out_splits),
@@ -239,73 +280,13 @@ def _symm_buffer(elems: int, dev, group, tag: str = "transpose"):
     return _SYMM[key]
 
 
-def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None, root: int = 0,
-                      to_host: bool = True, n_ranges: int = 4, timings: dict | None = None,
-                      balance: bool = True, row_weight: float = 10_000.0,
-                      transpose: str = "auto", exchange: str = "auto"):
-    """Dirty image of the union of every rank's records. Each rank passes its
-    own time partition (records in gindex order, rank r holding the r-th
-    contiguous block, as visdata.partition_time_ordered produces).
-
-    ``transpose``: "push" (default on GPUs) overlaps NVLink pushes of each
-    plane range (a copy kernel into the destinations' inputs in symmetric
-    memory) with the row pass of the next range; "peer" fuses the slab
-    transpose into the row pass -- its
-    results are stored straight into the destination ranks' column-pass
-    inputs in symmetric memory over NVLink (wsb_fft_rows_peer); "nccl"
-    pipelines an NCCL all-to-all over ``n_ranges`` plane ranges (from the top
-    plane down, the stacking order of the column pass): the all-to-all of one
-    range runs on NCCL's stream while the row pass of the next range and the
-    column pass of the previous one run on the compute stream; "auto" picks
-    "push" when the backend and torch's symmetric memory support it. The
-    result does not depend on the choice.
-    ``timings``, if a dict, receives per-stage milliseconds of the compute
-    stream (and the bucket / sweep split of the gridder).
-    ``balance`` sizes the v-slabs for equal work from a global histogram of
-    the anchor rows (one all-reduce of n_v counts) instead of partition_1d's
-    equal rows: Earth-rotation tracks put most records in the central rows.
-
-    Returns (FinalImage on ``root``, None elsewhere; diag dict on every rank)."""
-    spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
-    be = backend or CudaBackend()
+def _exchange(be, srec, spl, counts, group, exchange: str = "auto"):
+    """Time->space exchange of packed records: block d of (srec, spl) goes to
+    rank d, blocks arrive in source-rank (gindex) order. "push": NVLink stores
+    into symmetric memory; "nccl": all-to-all-v. Returns (records, planes, m)."""
     R = dist.get_world_size(group)
     r = dist.get_rank(group)
     dev = be.device
-    S = kern.half_support
-    n_groups = spec.n_u // G
-    if R > spec.n_v or R > n_groups:
-        raise ValueError(f"{R} ranks exceed the mesh ({spec.n_v} rows, {n_groups} column groups)")
-
-    st = _Stages(timings is not None and dev.type == "cuda", dev)
-    st.mark("start")
-
-    # 1. prepare + time->space exchange ------------------------------------
-    rec, plane = be.prepare(u, v, w, vis, weight, spec)
-    st.mark("prepare")
-    if balance and R > 1:
-        hist = be.row_histogram(rec, spec)
-        dist.all_reduce(hist, group=group)
-        # memory bound on a slab's rows: its strip grid and row-pass output
-        # (2 x n_w x n_u complex128 per row) within ~60% of the free memory
-        # of the tightest rank
-        max_rows = None
-        if dev.type == "cuda":
-            key = (id(group), dev.index, spec.n_u, spec.n_v, spec.n_w, R)
-            if key not in _ROW_CAP:     # once per mesh: a collective + host sync
-                free = torch.tensor([torch.cuda.mem_get_info(dev)[0]], dtype=torch.float64,
-                                    device=dev)
-                dist.all_reduce(free, op=dist.ReduceOp.MIN, group=group)
-                _ROW_CAP[key] = int(0.6 * float(free.item()) / (2 * spec.n_w * spec.n_u * 16))
-            max_rows = _ROW_CAP[key]
-        starts = balanced_slab_starts(hist.cpu().numpy(), R, row_weight,
-                                      max_rows=min(spec.n_v, max_rows) if max_rows else spec.n_v)
-    else:
-        starts = [partition_1d(spec.n_v, R, d)[0] for d in range(R)] + [spec.n_v]
-    slabs = [(starts[d], starts[d + 1] - starts[d]) for d in range(R)]
-    srec, spl, counts = be.route(rec, plane, spec, S, R, starts)
-    n_local = int(rec.shape[0])
-    del rec, plane                  # large meshes: keep the peak footprint down
-    st.mark("route")
     if exchange == "auto":
         exchange = ("push" if (hasattr(be, "push_blocks") and dev.type == "cuda"
                                and _symm_available()) else "nccl")
@@ -354,6 +335,91 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
         rpl = torch.empty(m, dtype=torch.int32, device=dev)
         _a2a(rrec, srec.contiguous(), recv_counts, counts, group)
         _a2a(rpl, spl.contiguous(), recv_counts, counts, group)
+    return rrec, rpl, m
+
+
+def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None, root: int = 0,
+                      to_host: bool = True, n_ranges: int = 4, timings: dict | None = None,
+                      balance: bool = True, row_weight: float = 10_000.0,
+                      transpose: str = "auto", exchange: str = "auto",
+                      decomposition: str = "slabs", plane_weight: float | None = None):
+    """Dirty image of the union of every rank's records. Each rank passes its
+    own time partition (records in gindex order, rank r holding the r-th
+    contiguous block, as visdata.partition_time_ordered produces).
+
+    ``transpose``: "push" (default on GPUs) overlaps NVLink pushes of each
+    plane range (a copy kernel into the destinations' inputs in symmetric
+    memory) with the row pass of the next range; "peer" fuses the slab
+    transpose into the row pass -- its
+    results are stored straight into the destination ranks' column-pass
+    inputs in symmetric memory over NVLink (wsb_fft_rows_peer); "nccl"
+    pipelines an NCCL all-to-all over ``n_ranges`` plane ranges (from the top
+    plane down, the stacking order of the column pass): the all-to-all of one
+    range runs on NCCL's stream while the row pass of the next range and the
+    column pass of the previous one run on the compute stream; "auto" picks
+    "push" when the backend and torch's symmetric memory support it. The
+    result does not depend on the choice.
+    ``timings``, if a dict, receives per-stage milliseconds of the compute
+    stream (and the bucket / sweep split of the gridder).
+    ``balance`` sizes the v-slabs for equal work from a global histogram of
+    the anchor rows (one all-reduce of n_v counts) instead of partition_1d's
+    equal rows: Earth-rotation tracks put most records in the central rows.
+    ``decomposition``: "slabs" (the reference's v-slabs, above; the image is
+    bit-identical for any R) or "planes": rank d owns a contiguous range of w
+    planes (balanced on records per plane + ``plane_weight`` records per
+    plane's transforms), grids them over the whole mesh, transforms and
+    stacks them locally, and the ranks' complex partial stacks are summed by
+    one NCCL reduce to the root -- no grid transpose; the image agrees with
+    the single-GPU one to rounding (~1e-16 relative; the stack's association
+    over planes depends on R).
+
+    Returns (FinalImage on ``root``, None elsewhere; diag dict on every rank)."""
+    spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
+    be = backend or CudaBackend()
+    R = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    dev = be.device
+    S = kern.half_support
+    n_groups = spec.n_u // G
+    if R > spec.n_v or R > n_groups:
+        raise ValueError(f"{R} ranks exceed the mesh ({spec.n_v} rows, {n_groups} column groups)")
+
+    st = _Stages(timings is not None and dev.type == "cuda", dev)
+    st.mark("start")
+
+    # 1. prepare + time->space exchange ------------------------------------
+    rec, plane = be.prepare(u, v, w, vis, weight, spec)
+    st.mark("prepare")
+    if decomposition == "planes":
+        return _image_planes(be, rec, plane, spec, kern, group, root, to_host, timings, st,
+                             balance, plane_weight, exchange)
+    if decomposition != "slabs":
+        raise ValueError(f"unknown decomposition {decomposition!r}")
+    if balance and R > 1:
+        hist = be.row_histogram(rec, spec)
+        dist.all_reduce(hist, group=group)
+        # memory bound on a slab's rows: its strip grid and row-pass output
+        # (2 x n_w x n_u complex128 per row) within ~60% of the free memory
+        # of the tightest rank
+        max_rows = None
+        if dev.type == "cuda":
+            key = (id(group), dev.index, spec.n_u, spec.n_v, spec.n_w, R)
+            if key not in _ROW_CAP:     # once per mesh: a collective + host sync
+                free = torch.tensor([torch.cuda.mem_get_info(dev)[0]], dtype=torch.float64,
+                                    device=dev)
+                dist.all_reduce(free, op=dist.ReduceOp.MIN, group=group)
+                _ROW_CAP[key] = int(0.6 * float(free.item()) / (2 * spec.n_w * spec.n_u * 16))
+            max_rows = _ROW_CAP[key]
+        starts = balanced_slab_starts(hist.cpu().numpy(), R, row_weight,
+                                      max_rows=min(spec.n_v, max_rows) if max_rows else spec.n_v)
+    else:
+        starts = [partition_1d(spec.n_v, R, d)[0] for d in range(R)] + [spec.n_v]
+    slabs = [(starts[d], starts[d + 1] - starts[d]) for d in range(R)]
+    srec, spl, counts = be.route(rec, plane, spec, S, R, starts)
+    n_local = int(rec.shape[0])
+    del rec, plane                  # large meshes: keep the peak footprint down
+    st.mark("route")
+    rrec, rpl, m = _exchange(be, srec, spl, counts, group, exchange)
     del srec, spl
     st.mark("exchange")
 
@@ -479,7 +545,13 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     for d, (g0_d, ng_d) in enumerate(cols):
         pix[:, g0_d * G:(g0_d + ng_d) * G] = strips[d][:, : ng_d * G]
         col_parts.append(parts[d][:, : ng_d * G])
-    p = torch.cat(col_parts, dim=1).reshape(-1, 2).cpu().numpy()
+    return _final(spec, pix, torch.cat(col_parts, dim=1), to_host, diag)
+
+
+def _final(spec, pix, partials, to_host, diag):
+    """FinalImage on the root from the device image and the norm partials
+    [residue][column][2]."""
+    p = partials.reshape(-1, 2).cpu().numpy()
     # sequential sum residue-major, in global column order (cumsum is left to
     # right): the same association as the single-GPU path, for any R
     im_sq = float(p[:, 0].cumsum()[-1])
@@ -497,6 +569,87 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     img = FinalImage(spec, pixels, im_sq ** 0.5, re_sq ** 0.5)
     diag.update({"imag_residual_norm": img.imag_residual_norm, "real_norm": img.real_norm})
     return img, diag
+
+
+_PLANE_CAP: dict = {}
+
+
+def _image_planes(be, rec, plane, spec, kern, group, root, to_host, timings, st, balance,
+                  plane_weight, exchange):
+    """w-plane decomposition of image_distributed (see its docstring)."""
+    import dataclasses
+    R = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    dev = be.device
+    n_w, n_u, n_v = spec.n_w, spec.n_u, spec.n_v
+    if R > n_w:
+        raise ValueError(f"{R} ranks exceed the {n_w} w planes")
+    if plane_weight is None:
+        plane_weight = n_u * n_v / 8.0     # a plane's transforms ~ gridding n_u n_v / 8 records
+    if balance and R > 1:
+        hist = torch.bincount(plane.to(torch.int64), minlength=n_w)
+        dist.all_reduce(hist, group=group)
+        max_planes = None
+        if dev.type == "cuda":
+            key = (id(group), dev.index, n_u, n_v, n_w, R)
+            if key not in _PLANE_CAP:   # once per mesh: a collective + host sync
+                free = torch.tensor([torch.cuda.mem_get_info(dev)[0]], dtype=torch.float64,
+                                    device=dev)
+                dist.all_reduce(free, op=dist.ReduceOp.MIN, group=group)
+                # a plane's strip grid and row-pass output, complex128 each
+                _PLANE_CAP[key] = max(1, int(0.6 * float(free.item()) / (2 * n_u * n_v * 16)))
+            max_planes = _PLANE_CAP[key]
+        starts = balanced_slab_starts(hist.cpu().numpy(), R, plane_weight,
+                                      max_rows=min(n_w, max_planes) if max_planes else n_w)
+    else:
+        starts = [partition_1d(n_w, R, d)[0] for d in range(R)] + [n_w]
+    srec, spl, counts = be.route_planes(rec, plane, spec, R, starts)
+    n_local = int(rec.shape[0])
+    del rec, plane
+    st.mark("route")
+    rrec, rpl, m = _exchange(be, srec, spl, counts, group, exchange)
+    del srec, spl
+    st.mark("exchange")
+
+    # 2. grid this rank's planes over the whole mesh ---------------------------
+    p0, p1 = starts[r], starts[r + 1]
+    nloc = p1 - p0
+    spec_l = dataclasses.replace(spec, n_w=nloc)
+    grid_s, updates = be.grid_slab(rrec, rpl, spec_l, kern, 0, n_v)
+    st.mark("grid")
+    split = last_timings(dev)[0][1:3] if st.on else None
+    del rrec, rpl
+
+    # 3. row + column passes and the stack of the local planes, top range
+    #    first (ranges of at most ~4 GiB of row-pass output) ------------------
+    pimg = torch.empty((n_v, n_u, 2), dtype=torch.float64, device=dev)
+    n_groups = n_u // G
+    n_rng = max(1, -(-nloc * n_u * n_v * 16 // (4 << 30)))
+    for l0, l1 in reversed(plane_ranges(nloc, n_rng)):
+        grid_p = be.fft_rows(grid_s, spec_l, n_v, [n_groups], l0, l1)
+        be.fft_cols_partial(grid_p, spec, p0 + l0, p0 + l1, p0, p1, pimg)
+        del grid_p
+    del grid_s
+    st.mark("fft")
+
+    # 4. sum of the partial stacks on the root, finish there ---------------------
+    upd = torch.tensor([updates], dtype=torch.int64, device=dev)
+    dist.all_reduce(upd, group=group)
+    if R > 1:
+        dist.reduce(pimg, dst=dist.get_global_rank(group, root) if group is not None else root,
+                    op=dist.ReduceOp.SUM, group=group)
+    st.mark("reduce")
+    diag = {"grid_updates": int(upd.item()), "records_local": n_local, "records_slab": m,
+            "exchange_bytes": int(sum(counts) - counts[r]) * 36, "plane_starts": starts,
+            "decomposition": "planes"}
+    if timings is not None:
+        timings.update(st.ms())
+        if split is not None:
+            timings["bucket"], timings["sweep"] = split
+    if r != root:
+        return None, diag
+    pix, parts = be.image_finish(pimg, spec)
+    return _final(spec, pix, parts, to_host, diag)
 
 
 def image_distributed_stream(batches, spec, kern, group=None, root: int = 0, **kwargs):

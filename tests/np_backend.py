@@ -110,3 +110,53 @@ class NumpyBackend:
                                        (acc.real[e::sp] ** 2).sum(axis=0)], axis=1)
                              for e in range(sp)])
         return torch.from_numpy(strip), torch.from_numpy(np.ascontiguousarray(partials))
+
+    # ---- w-plane decomposition (distributed._image_planes) -------------------
+    def route_planes(self, rec, plane, spec, R, starts):
+        r, pl = rec.numpy(), plane.numpy()
+        outs, outp, counts = [], [], []
+        for d in range(R):
+            m = (pl >= starts[d]) & (pl < starts[d + 1])
+            outs.append(r[m])
+            outp.append((pl[m] - starts[d]).astype(pl.dtype))
+            counts.append(int(m.sum()))
+        return (torch.from_numpy(np.concatenate(outs)), torch.from_numpy(np.concatenate(outp)),
+                counts)
+
+    def fft_cols_partial(self, tgrid, spec, plane_lo, plane_hi, rank_lo, rank_hi, pimg):
+        """Unscaled stack sum_k P_k exp(2 pi i w_k (n-1)) of the rank's planes
+        (ranges in descending order), written at the range starting at rank_lo."""
+        nk = plane_hi - plane_lo
+        ng = spec.n_u // G
+        t = tgrid.numpy().view(np.complex128)[: nk * ng * spec.n_v * G]
+        full = t.reshape(nk, ng, spec.n_v, G).transpose(0, 2, 1, 3).reshape(nk, spec.n_v, spec.n_u)
+        planes = np.fft.ifft(full, axis=1) * spec.n_v            # unnormalised inverse
+        if plane_hi == rank_hi:
+            self._pacc = np.zeros((spec.n_v, spec.n_u), np.complex128)
+        n = self._n(spec)
+        for k in range(plane_lo, plane_hi):
+            wk = O.plane_w_native(k, spec.n_w, spec.w_min_native, spec.w_max_native)
+            pk = planes[k - plane_lo]
+            self._pacc = self._pacc + (pk if wk == 0.0 else pk * np.exp(2j * np.pi * wk * (n - 1.0)))
+        if plane_lo == rank_lo:
+            pimg.numpy().view(np.complex128).reshape(spec.n_v, spec.n_u)[:] = self._pacc
+
+    def image_finish(self, pimg, spec):
+        from paper_2504_00959_b200.distributed import finish_split
+        acc = pimg.numpy().view(np.complex128).reshape(spec.n_v, spec.n_u)
+        acc = acc / (spec.n_u * spec.n_v) / spec.n_w * self._n(spec)
+        rs = finish_split(spec.n_v)
+        blk = spec.n_v // rs
+        partials = np.stack([np.stack([(acc.imag[e * blk:(e + 1) * blk] ** 2).sum(axis=0),
+                                       (acc.real[e * blk:(e + 1) * blk] ** 2).sum(axis=0)], axis=1)
+                             for e in range(rs)])
+        return (torch.from_numpy(np.ascontiguousarray(acc.real)),
+                torch.from_numpy(np.ascontiguousarray(partials)))
+
+    @staticmethod
+    def _n(spec):
+        cols = np.arange(spec.n_u, dtype=np.float64) - spec.n_u // 2
+        rowsv = np.arange(spec.n_v, dtype=np.float64) - spec.n_v // 2
+        l = np.broadcast_to(cols * spec.cell_size_lm, (spec.n_v, spec.n_u))
+        m = np.broadcast_to((rowsv * spec.cell_size_lm)[:, None], (spec.n_v, spec.n_u))
+        return np.sqrt(1.0 - l * l - m * m)

@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, outdir, row_weight):
+def _worker(rank, world, port, case, outdir, row_weight, decomp="slabs"):
     sys.path[:0] = [str(ROOT), str(TESTS)]
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -51,9 +51,11 @@ def _worker(rank, world, port, case, outdir, row_weight):
         spec = W.GridSpec(n_u, n_v, n_w, cell, w_min_native=wmin, w_max_native=wmax)
         kern = W.KernelSpec(kind, S, shape)
         img, diag = image_distributed(u[lo:hi], v[lo:hi], w[lo:hi], vis[lo:hi], wt[lo:hi], spec,
-                                      kern, backend=NumpyBackend(), row_weight=row_weight)
+                                      kern, backend=NumpyBackend(), row_weight=row_weight,
+                                      decomposition=decomp)
         if rank == 0:
-            np.savez(Path(outdir) / "out.npz", pixels=img.pixels, starts=np.array(diag["slab_starts"]),
+            starts = diag["slab_starts"] if decomp == "slabs" else diag["plane_starts"]
+            np.savez(Path(outdir) / "out.npz", pixels=img.pixels, starts=np.array(starts),
                      norms=np.array([img.imag_residual_norm, img.real_norm]),
                      updates=np.array([diag["grid_updates"]]))
     finally:
@@ -72,6 +74,25 @@ def test_image_distributed_gloo(tmp_path, golden_image, world, case, row_weight)
     starts = out["starts"]
     assert starts[0] == 0 and starts[-1] == golden_image[f"{case}_cfg"][1] and np.all(np.diff(starts) > 0)
     g = golden_image
+    ref = g[f"{case}_pixels"]
+    err = float(np.linalg.norm(out["pixels"] - ref) / np.linalg.norm(ref))
+    assert err <= 1e-12, err
+    assert int(out["updates"][0]) == int(g[f"{case}_grid_updates"][0])
+    np.testing.assert_allclose(out["norms"], g[f"{case}_norms"], rtol=1e-10)
+
+
+# w-plane decomposition: plane ranges, partial stacks summed on the root;
+# row_weight is unused there (plane_weight default)
+@pytest.mark.parametrize("world,case", [(2, "wide"), (4, "wide"), (2, "kb1"), (4, "small")])
+def test_image_distributed_planes_gloo(tmp_path, golden_image, world, case):
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, case, str(tmp_path), 1.0, "planes"), nprocs=world,
+             join=True)
+    out = np.load(tmp_path / "out.npz")
+    starts = out["starts"]
+    g = golden_image
+    assert starts[0] == 0 and starts[-1] == g[f"{case}_cfg"][2] and np.all(np.diff(starts) > 0)
+    assert len(starts) == world + 1
     ref = g[f"{case}_pixels"]
     err = float(np.linalg.norm(out["pixels"] - ref) / np.linalg.norm(ref))
     assert err <= 1e-12, err

@@ -138,11 +138,15 @@ def _nccl_worker(rank, world, port, outdir):
                          ("peer", dict(transpose="peer")),
                          ("nccl", dict(transpose="nccl")),
                          ("xnccl", dict(exchange="nccl", transpose="nccl")),
-                         ("even", dict(transpose="nccl", balance=False))):
+                         ("even", dict(transpose="nccl", balance=False)),
+                         ("planes", dict(decomposition="planes")),
+                         ("planes_even", dict(decomposition="planes", balance=False)),
+                         ("planes_xnccl", dict(decomposition="planes", exchange="nccl"))):
             img, diag = image_distributed(*args, spec, kern, **kw)
             if rank == 0:
                 outs[name] = img.pixels
                 outs[name + "_updates"] = np.array([diag["grid_updates"]])
+                outs[name + "_norms"] = np.array([img.imag_residual_norm, img.real_norm])
         # the double-buffered stream API: this rank's slice in two batches
         from paper_2504_00959_b200.distributed import image_distributed_stream
         mid = (lo + hi) // 2
@@ -172,6 +176,16 @@ def test_nccl_multi_gpu_matches_single(W, golden_image, tmp_path):
     for name in ("push", "push2", "peer", "nccl", "xnccl", "even"):
         assert int(out[name + "_updates"][0]) == diag["grid_updates"], name
         assert out[name].tobytes() == ref.pixels.tobytes(), name
+    # w-plane decomposition: the stack's association over planes depends on
+    # the ranks -- equal to rounding, not bitwise
+    for name in ("planes", "planes_even", "planes_xnccl"):
+        assert int(out[name + "_updates"][0]) == diag["grid_updates"], name
+        err = np.linalg.norm(out[name] - ref.pixels) / np.linalg.norm(ref.pixels)
+        assert err <= 1e-13, (name, err)
+        np.testing.assert_allclose(out[name + "_norms"], [ref.imag_residual_norm, ref.real_norm],
+                                   rtol=1e-12)
+        err_g = np.linalg.norm(out[name] - g["wide_pixels"]) / np.linalg.norm(g["wide_pixels"])
+        assert err_g <= 1e-10, (name, err_g)
     # stream batches: batch b = every rank's b-th half of its slice, in rank order
     u, v, w, t, vis, wt = chunk_from(g, "wide_in_")
     parts = _parts(t, world)
