@@ -176,6 +176,8 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     cfg = dict(CFG2)
     spec = W.GridSpec(cfg["n_u"], cfg["n_v"], cfg["n_w"], cfg["cell"], w_max_native=cfg["w_max"])
+    # multi-GPU decomposition (distributed.image_distributed's "auto" rule)
+    decomp = args.decomp if args.decomp != "auto" else ("planes" if ws <= cfg["n_w"] else "slabs")
     kern = W.KernelSpec(cfg["kind"], cfg["S"], cfg["shape"])
 
     # weak scaling: every rank holds its own 10M-record time partition
@@ -190,7 +192,7 @@ def run_ours(args):
     def step():
         if ws > 1:
             return WD.image_distributed(du, dv, dw, dvis, dwt, spec, kern, to_host=False,
-                                        decomposition=args.decomp)
+                                        decomposition=decomp)
         return W.image_device(du, dv, dw, dvis, dwt, spec, kern, image_out=img)
 
     clk = ClockSampler(dev.index).__enter__()   # sampling runs through warm-up and timing
@@ -240,7 +242,7 @@ def run_ours(args):
         for _ in range(n_st):
             tm = {}
             WD.image_distributed(du, dv, dw, dvis, dwt, spec, kern, to_host=False, timings=tm,
-                                 decomposition=args.decomp)
+                                 decomposition=decomp)
             for k_, v_ in tm.items():
                 acc[k_] = acc.get(k_, 0.0) + v_ / n_st
         stages = {k_: round(v_, 4) for k_, v_ in acc.items()}
@@ -283,14 +285,14 @@ def run_ours(args):
         # host image on the root; wall time per step, max over ranks
         pin = [torch.from_numpy(a).pin_memory().numpy() for a in (u, v, w, vis, wt)]
         batch = tuple(pin)
-        for _r in WD.image_distributed_stream([batch] * 2, spec, kern, decomposition=args.decomp):
+        for _r in WD.image_distributed_stream([batch] * 2, spec, kern, decomposition=decomp):
             pass
         torch.cuda.synchronize()
         n_e2e = max(4, min(args.steps, 12))
         dist.barrier()
         t0 = time.perf_counter()
         for res, _ in WD.image_distributed_stream([batch] * n_e2e, spec, kern,
-                                                  decomposition=args.decomp):
+                                                  decomposition=decomp):
             pass
         torch.cuda.synchronize()
         e2e_s = torch.tensor([(time.perf_counter() - t0) / n_e2e], dtype=torch.float64, device=dev)
@@ -367,7 +369,7 @@ def run_ours(args):
                                "32 w-planes, Gaussian support 7 (S=3, sigma=1), single channel, FP64",
                    "records_per_gpu": cfg["n_vis"], "n_u": cfg["n_u"], "n_v": cfg["n_v"],
                    "n_w": cfg["n_w"], "cell_size_lm": cfg["cell"], "w_max_native": cfg["w_max"],
-                   "parallelism": ((f"v-slab x{ws}" if args.decomp == "slabs" else f"w-plane ranges x{ws}")
+                   "parallelism": ((f"v-slab x{ws}" if decomp == "slabs" else f"w-plane ranges x{ws}")
                                    if ws > 1 else "single GPU"),
                    "l2": "inputs 360 MB and grid 2 GiB exceed the 126 MB L2; no flush"},
         "gridding_mvis_s": round(cfg["n_vis"] / (gridder["ms"] / 1e3) / 1e6, 1) if gridder["ms"] else None,
@@ -527,7 +529,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--decomp", choices=["slabs", "planes"], default="slabs",
+    ap.add_argument("--decomp", choices=["auto", "slabs", "planes"], default="auto",
                     help="multi-GPU decomposition: v-slabs (grid transpose) or w-plane ranges "
                          "(partial-stack reduce)")
     args = ap.parse_args()

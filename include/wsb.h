@@ -169,6 +169,11 @@ int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int
  * them on its own; the ranks' partial images are summed afterwards
  * (wsb_fft_cols_partial, wsb_image_finish). Each record goes to exactly one
  * rank (no halo). Counts per destination, as wsb_route_count. Synchronous. */
+/* Records per w plane of prepared records: hist u32[n_w] (device); feeds the
+ * load balancing of the plane ranges. Enqueued, no synchronisation. */
+int wsb_plane_histogram(wsb_ctx *ctx, const wsb_grid *grid, const uint32_t *plane, int64_t n,
+                        uint32_t *hist);
+
 int wsb_route_planes_count(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_ranks,
                            const int32_t *plane_starts_host, const double *rec,
                            const uint32_t *plane, int64_t n, int64_t *counts_host);

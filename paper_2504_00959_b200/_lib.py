@@ -30,7 +30,7 @@ EXPORTS = (
     "wsb_route_count", "wsb_route_pack", "wsb_grid_slab", "wsb_fft_rows", "wsb_fft_cols_stack",
     "wsb_grid_unpack", "wsb_tiles_debug", "wsb_last_timings", "wsb_row_histogram",
     "wsb_fft_rows_peer", "wsb_push_blocks", "wsb_ctx_set_precision", "wsb_route_planes_count",
-    "wsb_route_planes_pack", "wsb_fft_cols_partial", "wsb_image_finish",
+    "wsb_route_planes_pack", "wsb_fft_cols_partial", "wsb_image_finish", "wsb_plane_histogram",
 )
 
 
@@ -90,6 +90,7 @@ def lib() -> C.CDLL:
         "wsb_route_count": (C.c_int, [p, G, i32, i32, p, p, i64, p]),
         "wsb_route_pack": (C.c_int, [p, G, i32, i32, p, p, p, i64, p, p, p]),
         "wsb_row_histogram": (C.c_int, [p, G, p, i64, p]),
+        "wsb_plane_histogram": (C.c_int, [p, G, p, i64, p]),
         "wsb_route_planes_count": (C.c_int, [p, G, i32, p, p, p, i64, p]),
         "wsb_route_planes_pack": (C.c_int, [p, G, i32, p, p, p, i64, p, p, p]),
         "wsb_fft_cols_partial": (C.c_int, [p, G, i32, i32, i32, i32, p, p]),

@@ -240,6 +240,14 @@ int wsb_route_pack(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int
                            send_rec, send_plane, src_index);
 }
 
+int wsb_plane_histogram(wsb_ctx *ctx, const wsb_grid *grid, const uint32_t *plane, int64_t n,
+                        uint32_t *hist) {
+    if (!ctx || !hist) return fail(WSB_EINVAL, "NULL argument");
+    WSB_TRY(validate_grid(grid));
+    WSB_TRY(set_device(ctx));
+    return plane_histogram(ctx, grid, plane, n, hist);
+}
+
 int wsb_route_planes_count(wsb_ctx *ctx, const wsb_grid *grid, int32_t n_ranks,
                            const int32_t *plane_starts_host, const double *rec,
                            const uint32_t *plane, int64_t n, int64_t *counts_host) {

@@ -271,7 +271,38 @@ __global__ void __launch_bounds__(kThreads) k_row_hist(const double4 *__restrict
         if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
+// Records per w plane (load balancing of the plane ranges), as k_row_hist.
+__global__ void __launch_bounds__(kThreads) k_plane_hist(const uint32_t *__restrict__ plane,
+                                                         int64_t n, int n_w,
+                                                         uint32_t *__restrict__ hist) {
+    extern __shared__ uint32_t h[];
+    for (int i = threadIdx.x; i < n_w; i += kThreads) h[i] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kBlockItems;
+    for (int it = 0; it < kBlockItems / kThreads; ++it) {
+        const int64_t i = base + it * kThreads + threadIdx.x;
+        if (i < n) atomicAdd(&h[min(plane[i], (uint32_t)(n_w - 1))], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_w; i += kThreads)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
 }  // namespace
+
+int plane_histogram(wsb_ctx *ctx, const wsb_grid *g, const uint32_t *plane, int64_t n,
+                    uint32_t *hist) {
+    WSB_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * g->n_w, ctx->stream));
+    if (n <= 0) return WSB_OK;
+    const size_t smem = sizeof(uint32_t) * g->n_w;
+    if (smem > 200 * 1024) return fail(WSB_EUNSUPPORTED, "plane histogram above 51200 planes");
+    WSB_CUDA_TRY(cudaFuncSetAttribute(k_plane_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    k_plane_hist<<<ceil_div(n, kBlockItems), kThreads, smem, ctx->stream>>>(plane, n, g->n_w, hist);
+    ctx->launches += 1;
+    WSB_CUDA_TRY(cudaGetLastError());
+    return WSB_OK;
+}
 
 int row_histogram(wsb_ctx *ctx, const wsb_grid *g, const double *rec, int64_t n, uint32_t *hist) {
     WSB_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * g->n_v, ctx->stream));

@@ -134,6 +134,8 @@ int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *sta
                const double *rec, const uint32_t *plane, int64_t n, double *send_rec,
                uint32_t *send_plane, int64_t *src_index, int by_plane = 0);
 int row_histogram(wsb_ctx *ctx, const wsb_grid *g, const double *rec, int64_t n, uint32_t *hist);
+int plane_histogram(wsb_ctx *ctx, const wsb_grid *g, const uint32_t *plane, int64_t n,
+                    uint32_t *hist);
 
 // bucket.cu: records of a slab bucketed by (plane, 32-column strip, anchor row)
 struct RowBuckets {

@@ -112,6 +112,9 @@ class NumpyBackend:
         return torch.from_numpy(strip), torch.from_numpy(np.ascontiguousarray(partials))
 
     # ---- w-plane decomposition (distributed._image_planes) -------------------
+    def plane_histogram(self, plane, spec):
+        return torch.from_numpy(np.bincount(plane.numpy().astype(np.int64), minlength=spec.n_w))
+
     def route_planes(self, rec, plane, spec, R, starts):
         r, pl = rec.numpy(), plane.numpy()
         outs, outp, counts = [], [], []

@@ -134,11 +134,12 @@ def _nccl_worker(rank, world, port, outdir):
         outs = {}
         # fused peer-memory transpose (twice: the symmetric buffer is reused),
         # the pipelined NCCL all-to-all, and partition_1d slabs
-        for name, kw in (("push", dict(transpose="push")), ("push2", dict(transpose="push")),
-                         ("peer", dict(transpose="peer")),
-                         ("nccl", dict(transpose="nccl")),
-                         ("xnccl", dict(exchange="nccl", transpose="nccl")),
-                         ("even", dict(transpose="nccl", balance=False)),
+        sl = dict(decomposition="slabs")
+        for name, kw in (("push", dict(transpose="push", **sl)), ("push2", dict(transpose="push", **sl)),
+                         ("peer", dict(transpose="peer", **sl)),
+                         ("nccl", dict(transpose="nccl", **sl)),
+                         ("xnccl", dict(exchange="nccl", transpose="nccl", **sl)),
+                         ("even", dict(transpose="nccl", balance=False, **sl)),
                          ("planes", dict(decomposition="planes")),
                          ("planes_even", dict(decomposition="planes", balance=False)),
                          ("planes_xnccl", dict(decomposition="planes", exchange="nccl"))):
@@ -152,9 +153,13 @@ def _nccl_worker(rank, world, port, outdir):
         mid = (lo + hi) // 2
         batches = [tuple(np.ascontiguousarray(x[a_:b_]) for x in (u, v, w, vis, wt))
                    for a_, b_ in ((lo, mid), (mid, hi))]
-        for bi, (img, diag) in enumerate(image_distributed_stream(batches, spec, kern)):
+        for bi, (img, diag) in enumerate(image_distributed_stream(batches, spec, kern,
+                                                                  decomposition="slabs")):
             if rank == 0:
                 outs[f"stream{bi}"] = img.pixels
+        for bi, (img, diag) in enumerate(image_distributed_stream(batches, spec, kern)):  # auto
+            if rank == 0:
+                outs[f"pstream{bi}"] = img.pixels
         if rank == 0:
             np.savez(Path(outdir) / "out.npz", **outs)
     finally:
@@ -195,3 +200,5 @@ def test_nccl_multi_gpu_matches_single(W, golden_image, tmp_path):
         ref_b, _ = W.image(*(x[sel] for x in (u, v, w)), None, vis[sel], wt[sel], spec,
                            W.KernelSpec("gaussian", S, shape))
         assert out[f"stream{bi}"].tobytes() == ref_b.pixels.tobytes(), bi
+        err = np.linalg.norm(out[f"pstream{bi}"] - ref_b.pixels) / np.linalg.norm(ref_b.pixels)
+        assert err <= 1e-13, (bi, err)

@@ -22,7 +22,8 @@ import paper_2504_00959_b200 as W  # noqa: E402
 from lofar import tracks  # noqa: E402
 
 
-STAGES = ("prepare", "route", "exchange", "grid", "bucket", "sweep", "rows", "cols", "gather")
+STAGES = ("prepare", "route", "exchange", "grid", "bucket", "sweep", "rows", "cols", "gather",
+          "fft", "reduce")
 
 
 def main():
@@ -34,6 +35,7 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--cell", type=float, default=1e-4)
     ap.add_argument("--transpose", default="auto", choices=["auto", "push", "peer", "nccl"])
+    ap.add_argument("--decomp", default="auto", choices=["auto", "slabs", "planes"])
     ap.add_argument("--label", default="cfg3 LOFAR-like tracks")
     a = ap.parse_args()
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -55,7 +57,8 @@ def main():
 
     def run(vv=vis):
         if ws > 1:
-            img, d = image_distributed(u, v, w, vv, wt, spec, kern, to_host=False, transpose=a.transpose)
+            img, d = image_distributed(u, v, w, vv, wt, spec, kern, to_host=False, transpose=a.transpose,
+                                           decomposition=a.decomp)
             return (img.pixels if img is not None else None), d
         return W.image_device(u, v, w, vv, wt, spec, kern)
 
@@ -83,10 +86,12 @@ def main():
     else:
         tm = {}
         image_distributed(u, v, w, vis, wt, spec, kern, to_host=False, timings=tm,
-                          transpose=a.transpose)
+                          transpose=a.transpose, decomposition=a.decomp)
         st = torch.tensor([tm.get(k, 0.0) for k in STAGES], device=dev, dtype=torch.float64)
         dist.all_reduce(st, op=dist.ReduceOp.MAX)
-        out["stage_ms_max_over_ranks"] = {k: round(float(x), 3) for k, x in zip(STAGES, st.tolist())}
+        out["stage_ms_max_over_ranks"] = {k: round(float(x), 3) for k, x in zip(STAGES, st.tolist())
+                                          if k in tm}
+        out["decomposition"] = a.decomp
     if a.check:
         # Size-independent parity at full size (linearity of the whole path):
         # split the records into two complementary halves by zeroing the
@@ -100,7 +105,8 @@ def main():
 
         def run_w(wts):
             if ws > 1:
-                img, d = image_distributed(u, v, w, vis, wts, spec, kern, to_host=False)
+                img, d = image_distributed(u, v, w, vis, wts, spec, kern, to_host=False,
+                                           decomposition=a.decomp)
                 return (img.pixels.clone() if img is not None else None), d
             pix, d = W.image_device(u, v, w, vis, wts, spec, kern)
             return pix.clone(), d
