@@ -48,6 +48,33 @@ def main():
                 traffic.setdefault(g, int(b))   # first launch of the kind
     (PROF / "traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
     print(json.dumps(traffic, indent=1))
+    sass_listings()
+
+
+# hot kernels whose SASS is kept: (file stem, regex on the mangled name)
+SASS = (("k_grid_sweep_0_3", r"k_grid_sweepILi0ELi3E"), ("k_fft_rows_11", r"k_fft_rowsILi11ELi0E7double2"),
+        ("k_fft_cols_11", r"k_fft_colsILi11ELi0E7double2"), ("k_fft_cols_11_fp32", r"k_fft_colsILi11ELi0E6float2"),
+        ("k_radix_scatter_8", r"k_radix_scatterILi8ELb0E"), ("k_keys_write", r"k_keys_write"),
+        ("k_prepare", r"k_prepareEPK"), ("k_push", r"k_push[^4]"), ("k_image_finish", r"k_image_finish"),
+        ("k_route_pack", r"k_route_pack"))
+
+
+def sass_listings():
+    """cuobjdump -sass of the in-tree libwsb.so, one file per hot kernel,
+    instruction encodings stripped."""
+    so = ROOT / "paper_2504_00959_b200" / "libwsb.so"
+    dump = subprocess.run(["cuobjdump", "-sass", str(so)], capture_output=True, text=True).stdout
+    funcs = re.split(r"\n\s*Function : ", dump)
+    out = PROF / "sass"
+    out.mkdir(exist_ok=True)
+    for stem, pat in SASS:
+        for f in funcs[1:]:
+            name = f.split("\n", 1)[0]
+            if re.search(pat, name):
+                body = re.sub(r"\s*/\* 0x[0-9a-f]{16} \*/", "", f)
+                body = "\n".join(l for l in body.splitlines() if l.strip())
+                (out / f"{stem}.sass").write_text("Function : " + body + "\n")
+                break
 
 
 if __name__ == "__main__":

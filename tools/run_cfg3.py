@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--cell", type=float, default=1e-4)
     ap.add_argument("--transpose", default="auto", choices=["auto", "push", "peer", "nccl"])
     ap.add_argument("--decomp", default="auto", choices=["auto", "slabs", "planes"])
+    ap.add_argument("--plane-weight-div", type=float, default=None,
+                    help="plane decomposition: plane weight = n_u n_v / this (default: library's)")
     ap.add_argument("--label", default="cfg3 LOFAR-like tracks")
     a = ap.parse_args()
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -47,6 +49,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         from paper_2504_00959_b200.distributed import image_distributed
     cell = a.cell
+    pw = None if a.plane_weight_div is None else a.nu * a.nu / a.plane_weight_div
     spec = W.GridSpec(a.nu, a.nu, a.nw, cell, w_max_native=1000.0)
     kern = W.KernelSpec.gaussian(3, 1.0)
     per = a.n // ws
@@ -58,7 +61,7 @@ def main():
     def run(vv=vis):
         if ws > 1:
             img, d = image_distributed(u, v, w, vv, wt, spec, kern, to_host=False, transpose=a.transpose,
-                                           decomposition=a.decomp)
+                                           decomposition=a.decomp, plane_weight=pw)
             return (img.pixels if img is not None else None), d
         return W.image_device(u, v, w, vv, wt, spec, kern)
 
@@ -86,12 +89,14 @@ def main():
     else:
         tm = {}
         image_distributed(u, v, w, vis, wt, spec, kern, to_host=False, timings=tm,
-                          transpose=a.transpose, decomposition=a.decomp)
+                          transpose=a.transpose, decomposition=a.decomp, plane_weight=pw)
         st = torch.tensor([tm.get(k, 0.0) for k in STAGES], device=dev, dtype=torch.float64)
         dist.all_reduce(st, op=dist.ReduceOp.MAX)
         out["stage_ms_max_over_ranks"] = {k: round(float(x), 3) for k, x in zip(STAGES, st.tolist())
                                           if k in tm}
         out["decomposition"] = a.decomp
+        if "plane_starts" in d:
+            out["plane_starts"] = d["plane_starts"]
     if a.check:
         # Size-independent parity at full size (linearity of the whole path):
         # split the records into two complementary halves by zeroing the
@@ -106,7 +111,7 @@ def main():
         def run_w(wts):
             if ws > 1:
                 img, d = image_distributed(u, v, w, vis, wts, spec, kern, to_host=False,
-                                           decomposition=a.decomp)
+                                           decomposition=a.decomp, plane_weight=pw)
                 return (img.pixels.clone() if img is not None else None), d
             pix, d = W.image_device(u, v, w, vis, wts, spec, kern)
             return pix.clone(), d
