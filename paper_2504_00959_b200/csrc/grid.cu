@@ -33,6 +33,9 @@ namespace {
 #ifndef WSB_GRID_RUNROLL
 #define WSB_GRID_RUNROLL 1
 #endif
+#ifndef WSB_GRID_PREMUL
+#define WSB_GRID_PREMUL 1   // stage value * u weight per window column (vs value and weights)
+#endif
 #ifndef WSB_GRID_MINB
 #define WSB_GRID_MINB 0   // > 0: one occupancy target for every instantiation
 #endif
@@ -185,22 +188,42 @@ struct SweepArgs {
     int64_t n_items, n_parts;
 };
 
-template <int S>
+// Value * u-weight staging on/off per (kernel, half_support): measured on
+// cfg2 records (profiles/gridder_minb_r01.txt); above S = 5 the premultiplied
+// records exceed 48 KB of static shared memory per CTA.
+template <int KIND, int S>
+constexpr bool sweep_premul() {
+    constexpr bool gauss[8] = {false, false, true, true, false, true, false, false};
+    constexpr bool kb[8] = {false, true, true, true, false, true, false, false};
+    return WSB_GRID_PREMUL && (KIND == WSB_KERNEL_GAUSSIAN ? gauss[S] : kb[S]);
+}
+
+template <int KIND, int S>
 struct WarpStage {
     static constexpr int W = 2 * S + 1;
     // one contiguous struct per staged record: the sweep addresses a record
     // with a single base pointer (vs. separate wu/wv/val/ij arrays: -2% grid
     // time at S=3, -20% at S=4 where the split arrays had bank conflicts)
     static constexpr int WVS = (W + 1) & ~1;
-    struct Rec {
+    // PRE: value * u weight staged per window column (the run loop loads one
+    // complex instead of the value and a weight, no multiplies)
+    static constexpr bool PRE = sweep_premul<KIND, S>();
+    struct RecPre {
+        double2 tu[W + 1];        // value * u weight per window column; slot W = 0 (off the footprint)
+        double wv[WVS];
+        int2 ij;                  // (first window column, first window row)
+    };
+    struct RecVal {
         double2 val;
         double wv[WVS];
         double wu[W + 1];         // slot W is the zero weight for columns off the footprint
         int2 ij;                  // (first window column, first window row)
     };
+    using Rec = std::conditional_t<PRE, RecPre, RecVal>;
     Rec rec[32];
     double2 raw[2][32][2];        // records in flight (cp.async), one chunk ahead
 };
+#define ST_TU(r, k) st.rec[r].tu[k]
 #define ST_WU(r, k) st.rec[r].wu[k]
 #define ST_WV(r, b) st.rec[r].wv[b]
 #define ST_VAL(r) st.rec[r].val
@@ -220,7 +243,7 @@ constexpr int sweep_min_blocks() {
 template <int KIND, int S>
 __global__ void __launch_bounds__(32 * kWarpsPerCta, sweep_min_blocks<KIND, S>()) k_grid_sweep(SweepArgs a, KParams<S> kp) {
     constexpr int W = 2 * S + 1;
-    using St = WarpStage<S>;
+    using St = WarpStage<KIND, S>;
     __shared__ __align__(16) St stage_all[kWarpsPerCta];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     St &st = stage_all[warp];
@@ -250,7 +273,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, sweep_min_blocks<KIND, S>()
     double2 *const out = direct ? (double2 *)a.out : a.partial;
     float2 *const out32 = (float2 *)a.out;
     const bool f32 = direct && a.out_f32;
-    ST_WU(lane, W) = 0.0;
+    if constexpr (St::PRE)
+        ST_TU(lane, W) = make_double2(0.0, 0.0);
+    else
+        ST_WU(lane, W) = 0.0;
 
     // Window of W rows kept as a ring of W register slots: row `base` is in
     // slot `phase`, row base+b in slot (phase+b) % W. Records with anchor
@@ -293,9 +319,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, sweep_min_blocks<KIND, S>()
         for (int rr = rr0; rr < rr0 + n; ++rr) {
             int k = col - ST_IJ(rr).x;
             k = (unsigned)k < (unsigned)W ? k : W;   // slot W holds weight 0
-            const double2 v = ST_VAL(rr);
-            const double wu = ST_WU(rr, k);
-            const double tr = __dmul_rn(v.x, wu), ti = __dmul_rn(v.y, wu);
+            double tr, ti;
+            if constexpr (St::PRE) {
+                const double2 t = ST_TU(rr, k);
+                tr = t.x;
+                ti = t.y;
+            } else {
+                const double2 v = ST_VAL(rr);
+                const double wu = ST_WU(rr, k);
+                tr = __dmul_rn(v.x, wu);
+                ti = __dmul_rn(v.y, wu);
+            }
 #pragma unroll
             for (int b = 0; b < W; b += 2) {
                 const double2 wv2 = *reinterpret_cast<const double2 *>(&ST_WV(rr, b));
@@ -351,12 +385,19 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, sweep_min_blocks<KIND, S>()
                 const int ib = (int)floor(gu) - S, jb = (int)floor(gv) - S;
                 double w[W];
                 const uint32_t um = axis_weights<KIND, S>(gu, ib, kp, i0b, w);
+                if constexpr (St::PRE) {
+                    // the run loop's value * u-weight products, formed once per record
 #pragma unroll
-                for (int k = 0; k < W; ++k) ST_WU(lane, k) = w[k];
+                    for (int k = 0; k < W; ++k)
+                        ST_TU(lane, k) = make_double2(__dmul_rn(hi.x, w[k]), __dmul_rn(hi.y, w[k]));
+                } else {
+#pragma unroll
+                    for (int k = 0; k < W; ++k) ST_WU(lane, k) = w[k];
+                    ST_VAL(lane) = hi;
+                }
                 const uint32_t vm = axis_weights<KIND, S>(gv, jb, kp, i0b, w);
 #pragma unroll
                 for (int k = 0; k < W; ++k) ST_WV(lane, k) = w[k];
-                ST_VAL(lane) = hi;
                 ST_IJ(lane) = make_int2(ib, jb);
                 my_jb = jb;
                 // cell updates inside this strip and row block (grid_sector's count)
