@@ -598,9 +598,11 @@ def _image_planes(be, rec, plane, spec, kern, group, root, to_host, timings, st,
     if R > n_w:
         raise ValueError(f"{R} ranks exceed the {n_w} w planes")
     if plane_weight is None:
-        # a plane's row + column passes cost about as much as bucketing and
-        # gridding n_u n_v / 12 records (cfg2 and cfg3 on B200)
-        plane_weight = n_u * n_v / 12.0
+        # a plane's row + column passes and emission cost about as much as
+        # bucketing and gridding n_u n_v / 8 records: measured per rank on cfg3
+        # (4 GPUs: grid + transforms 10.8 / 9.8 / 9.6 / 9.9 ms with /8 against
+        # 8.5 / 9.8 / 10.3 / 12.1 with /12, 12.5 / 9.8 / 9.2 / 8.2 with /5)
+        plane_weight = n_u * n_v / 8.0
     if balance and R > 1:
         hist = be.plane_histogram(plane, spec)
         dist.all_reduce(hist, group=group)

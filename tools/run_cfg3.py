@@ -91,6 +91,10 @@ def main():
         image_distributed(u, v, w, vis, wt, spec, kern, to_host=False, timings=tm,
                           transpose=a.transpose, decomposition=a.decomp, plane_weight=pw)
         st = torch.tensor([tm.get(k, 0.0) for k in STAGES], device=dev, dtype=torch.float64)
+        per = [torch.empty_like(st) for _ in range(ws)]
+        dist.all_gather(per, st)
+        out["stage_ms_per_rank"] = {k: [round(float(p_[i]), 2) for p_ in per]
+                                    for i, k in enumerate(STAGES) if k in tm}
         dist.all_reduce(st, op=dist.ReduceOp.MAX)
         out["stage_ms_max_over_ranks"] = {k: round(float(x), 3) for k, x in zip(STAGES, st.tolist())
                                           if k in tm}
