@@ -570,13 +570,13 @@ def _final(spec, pix, partials, to_host, diag):
     im_sq = float(p[:, 0].cumsum()[-1])
     re_sq = float(p[:, 1].cumsum()[-1])
     if to_host and pix.is_cuda:
-        # page-locked staging: the image leaves at DMA speed (a pageable
-        # destination costs ~10x), then a private host copy
+        # page-locked destination: the image leaves at DMA speed (a pageable
+        # destination costs ~10x). The returned pixels are that buffer itself
+        # (the array keeps the tensor alive; torch's caching host allocator
+        # recycles it once the caller drops the image): no host-side copy
         stage = torch.empty(pix.shape, dtype=pix.dtype, pin_memory=True)
         stage.copy_(pix)
-        out = torch.empty(pix.shape, dtype=pix.dtype)
-        out.copy_(stage)
-        pixels = out.numpy()
+        pixels = stage.numpy()
     else:
         pixels = pix.numpy() if to_host else pix
     img = FinalImage(spec, pixels, im_sq ** 0.5, re_sq ** 0.5)
