@@ -15,8 +15,8 @@ e2e    : the same through the public host-buffer API (wsb_image): pinned host
 roofline: algorithmic bytes / measured time of the dominant kernel against
          the measured HBM copy bandwidth (MEASURED_PEAKS.json).
 cpu_baseline / --impl reference: the CPU oracle (a NumPy restatement of the
-         reference algorithm, oracle/) timed on this host on a bounded sample
-         and scaled to the full workload.
+         reference algorithm, oracle/) imaging full cfg2 batches on all host
+         cores, measured (N > 1: gridding scaled to the job's records).
 """
 
 from __future__ import annotations
@@ -264,17 +264,21 @@ def run_ours(args):
             step()
         torch.cuda.synchronize()
         win = time.perf_counter() - t0
-        j = meter.joules()
+        j = meter.joules({"window": win}, "default")
         gj = torch.tensor([j["gpu"]], dtype=torch.float64, device=dev)
         if ws > 1:
             dist.all_reduce(gj)
+        host = j.get("host")
+        host_src = "RAPL package counters (rank 0 host)"
+        if host is None:
+            from paper_2504_00959_b200.energy import ModelledHostMeter
+            hm = ModelledHostMeter()
+            host = hm.joules({"window": win})["window"]
+            host_src = hm.source + "; RAPL unreadable on this host"
         energy = {"gpu_joules_per_step": round(float(gj.item()) / n_en, 4),
-                  "host_joules_per_step": (round(j["host"] / n_en, 4) if j["host"] is not None
-                                           else None),
+                  "host_joules_per_step": round(host / n_en, 4),
                   "window_s": round(win, 3), "steps": n_en,
-                  "source": "NVML total energy (all GPUs) + RAPL package (rank 0 host)"
-                            if j["host"] is not None else
-                            "NVML total energy (all GPUs); RAPL unreadable on this host"}
+                  "source": f"GPU: NVML total energy (all GPUs); host: {host_src}"}
     except Exception as exc:  # NVML missing or not permitted: report, do not fail the bench
         energy = {"unavailable": f"{type(exc).__name__}: {exc}"}
 
@@ -393,12 +397,21 @@ def run_ours(args):
     }
     if ws == 1 and not args.no_cpu_baseline:
         cb = out["cpu_baseline"] = cpu_baseline(cfg)
-        # green productivity, Eq. 4 (metrics.py:200-207): needs both energies
-        if cb.get("host_joules_per_image") and energy and energy.get("host_joules_per_step") is not None:
+        # green productivity, Eq. 4 (metrics.py:200-207): reference run = the
+        # CPU image (host energy), test run = the GPU step (NVML + host)
+        if energy and energy.get("host_joules_per_step") is not None:
             from paper_2504_00959_b200.energy import green_productivity
             e_gpu = energy["gpu_joules_per_step"] + energy["host_joules_per_step"]
-            out["green_productivity"] = round(green_productivity(
-                cb["seconds_per_image"], cb["host_joules_per_image"], ms_step / 1e3, e_gpu), 1)
+            out["green_productivity"] = {
+                "value": round(green_productivity(cb["seconds_per_image"],
+                                                  cb["host_joules_per_image"],
+                                                  ms_step / 1e3, e_gpu), 1),
+                "alpha": 1.0,
+                "ref": {"seconds": cb["seconds_per_image"], "joules": cb["host_joules_per_image"],
+                        "energy": cb["host_energy_source"]},
+                "test": {"seconds": round(ms_step / 1e3, 6), "joules": round(e_gpu, 4),
+                         "energy": energy["source"]},
+                "formula": "(t_ref / t_test) / (alpha * E_test / E_ref), metrics.py:200-207"}
         else:
             out["green_productivity"] = None
     if ws > 1:
@@ -406,76 +419,11 @@ def run_ours(args):
     print(json.dumps(out), flush=True)
 
 
-def oracle_step(cfg, n_sample, n_planes, threads):
-    """CPU oracle on a bounded sample: gridding of n_sample records (full
-    grid geometry) and FFT + w-correction + stacking of n_planes planes;
-    both scaled to the full workload. Returns (seconds_full, detail)."""
-    from oracle import wstack_oracle as O
-    u, v, w, t, vis, wt = synthetic(cfg, n=n_sample, seed=cfg["seed"] + 1000)
-    kind = O.KIND_GAUSSIAN if cfg["kind"] == "gaussian" else O.KIND_KAISER_BESSEL
-    t0 = time.perf_counter()
-    prep = O.prepare(u, v, w, t, vis, wt, cfg["n_u"], cfg["n_v"], cfg["n_w"])
-    batch = O.exchange([prep], cfg["n_v"], 1, cfg["S"])[0]
-    import concurrent.futures as cf
-    blocks = [O.partition_1d(cfg["n_v"], threads, i) for i in range(threads)]
-
-    def work(blk):
-        b0, bc = blk
-        return O.grid_slab(batch, cfg["n_u"], cfg["n_w"], kind, cfg["S"], cfg["shape"], b0, b0 + bc)
-
-    with cf.ThreadPoolExecutor(threads) as ex:
-        grids = list(ex.map(work, blocks))
-    t_grid = time.perf_counter() - t0
-    grid = grids[0][0]
-    for g, _ in grids[1:]:
-        grid += g
-    t0 = time.perf_counter()
-    sign = O.checker_sign(cfg["n_u"], 0, cfg["n_v"])
-    planes = []
-    for k in range(n_planes):
-        p = O.ifft2(grid[k] * sign)
-        planes.append(O.w_correct(p, k, cfg["n_u"], cfg["n_v"], cfg["n_w"], cfg["cell"], 0.0,
-                                  cfg["w_max"], 0, cfg["n_v"]))
-    O.stack(planes, cfg["n_u"], cfg["n_v"], n_planes, cfg["cell"], 0, cfg["n_v"])
-    t_fft = time.perf_counter() - t0
-    full = t_grid * cfg["n_vis"] / n_sample + t_fft * cfg["n_w"] / n_planes
-    return full, {"grid_s": t_grid, "fft_wstack_s": t_fft}
-
-
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
-
-
-def cpu_baseline(cfg, n_sample=500_000, n_planes=4):
-    threads = cpu_cores()
-    meter = None
-    try:
-        from paper_2504_00959_b200.energy import NvmlRaplMeter
-        meter = NvmlRaplMeter(devices=[], host=True)
-        meter = meter if meter.host_available else None
-    except Exception:
-        meter = None
-    t0 = time.perf_counter()
-    if meter:
-        meter.start()
-    full_s, det = oracle_step(cfg, n_sample, n_planes, threads)
-    sample_s = time.perf_counter() - t0
-    host_j = None
-    if meter:
-        # same average package power over the scaled-up run
-        host_j = round(meter.joules()["host"] * full_s / sample_s, 1)
-    return {"value": round(cfg["n_vis"] / full_s / 1e6, 4), "unit": "Mvis/s", "cores": threads,
-            "seconds_per_image": round(full_s, 2), "host_joules_per_image": host_j,
-            "kind": "port",
-            "sample": (f"oracle (NumPy restatement of the reference) on {n_sample} of "
-                       f"{cfg['n_vis']} records gridded on the full 2048x2048x32 mesh "
-                       f"({det['grid_s']:.2f}s, {threads} row-block threads) + FFT/w-stack of "
-                       f"{n_planes} of {cfg['n_w']} planes ({det['fft_wstack_s']:.2f}s); "
-                       f"scaled to the full workload: {full_s:.1f}s per image"),
-            "cpu": _cpu_model()}
 
 
 def _cpu_model():
@@ -488,39 +436,113 @@ def _cpu_model():
     return "unknown"
 
 
+def host_meter():
+    """RAPL package counters when readable, else the labelled power model
+    (energy.ModelledHostMeter). Returns (meter, source, measured?)."""
+    from paper_2504_00959_b200 import energy as E
+    try:
+        m = E.NvmlRaplMeter(devices=[], host=True)
+        if m.host_available:
+            return m, "RAPL package counters", True
+    except Exception:
+        pass
+    m = E.ModelledHostMeter()
+    return m, m.source, False
+
+
+class CpuImage:
+    """The reference algorithm (oracle port: NumPy restatement of
+    prepare_chunk / exchange / tap-major np.add.at gridding / FFT / w screen /
+    stack, oracle/wstack_oracle.py) imaging ONE full batch of records on the
+    host cores: row-block gridding threads (the reference's deterministic
+    threaded mode, gridder.py:206-221) and plane-parallel transforms.
+    Inputs are generated before the timed call."""
+
+    def __init__(self, cfg, n_records, threads, seed):
+        from oracle import wstack_oracle as O
+        self.O = O
+        self.cfg = cfg
+        self.threads = threads
+        self.n = n_records
+        self.data = synthetic(cfg, n=n_records, seed=seed)
+
+    def run(self):
+        O, c = self.O, self.cfg
+        u, v, w, t, vis, wt = self.data
+        kind = O.KIND_GAUSSIAN if c["kind"] == "gaussian" else O.KIND_KAISER_BESSEL
+        t0 = time.perf_counter()
+        r = O.image(u, v, w, t, vis, wt, c["n_u"], c["n_v"], c["n_w"], c["cell"], 0.0, c["w_max"],
+                    kind, c["S"], c["shape"], threads=self.threads)
+        return time.perf_counter() - t0, r
+
+
+def cpu_baseline(cfg):
+    """One full cfg2 image (10M records, 2048^2 x 32) by the oracle port on
+    all host cores, measured (no extrapolation), with host energy."""
+    threads = cpu_cores()
+    job = CpuImage(cfg, cfg["n_vis"], threads, cfg["seed"] + 1000)
+    meter, src, measured = host_meter()
+    meter.start()
+    secs, r = job.run()
+    host_j = meter.joules({"image": secs}, "default")
+    host_j = host_j.get("host", host_j.get("image"))
+    return {"value": round(cfg["n_vis"] / secs / 1e6, 4), "unit": "Mvis/s", "cores": threads,
+            "seconds_per_image": round(secs, 2), "host_joules_per_image": round(host_j, 1),
+            "host_energy_source": src, "host_energy_measured": measured,
+            "kind": "port",
+            "sample": (f"one full cfg2 image measured (no scaling): {cfg['n_vis']} records "
+                       f"gridded on the 2048x2048x32 mesh + 32 plane transforms / w screens / "
+                       f"stack, oracle port, {threads} threads "
+                       f"(grid_updates {r['grid_updates']})"),
+            "cpu": _cpu_model()}
+
+
 def run_reference(args):
-    """The reference arm: the reference's algorithm (oracle port) on the host
-    cores, rank 0 only. Each step grids a bounded record sample on the full
-    mesh and transforms / stacks one plane, scaled to the job's workload
-    (ws x 10M records, one 2048^2 x 32 mesh). The sample shrinks so that the
-    whole --steps/--warmup run stays within about three minutes."""
+    """The reference arm: the reference's algorithm (oracle port, oracle/) on
+    the host cores, rank 0 only, same metric and configuration as our arm.
+
+    N = 1: every timed step images the full cfg2 batch (10M records,
+    2048^2 x 32): measured, nothing scaled; one untimed warm-up image.
+    N > 1 (the job images N x 10M records on one mesh): each step grids a
+    10M-record batch and transforms/stacks the full mesh, and the gridding
+    time is scaled by N (gridding is linear in the records on a fixed mesh;
+    the transforms do not depend on them) so the run stays within minutes."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     cfg = dict(CFG2)
     threads = cpu_cores()
-    n_sample = 100_000
-    budget_s = 180.0
-    t0 = time.perf_counter()
-    oracle_step(cfg, n_sample, 1, threads)     # first warm-up step sizes the sample
-    first = time.perf_counter() - t0
-    n_steps = args.steps + max(args.warmup - 1, 0)
-    if n_steps * first > budget_s:
-        n_sample = max(10_000, int(n_sample * budget_s / (n_steps * first)))
-    for _ in range(max(args.warmup - 1, 0)):
-        oracle_step(cfg, n_sample, 1, threads)
+    job = CpuImage(cfg, cfg["n_vis"], threads, cfg["seed"])
+    n_warm = 1 if args.warmup > 0 else 0
+    for _ in range(n_warm):
+        job.run()
     times = []
+    t_fft = None
     for _ in range(args.steps):
-        full, det = oracle_step(cfg, n_sample, 1, threads)
-        # the job grids ws x n_vis records on one mesh: scale the gridding part
-        times.append(full + det["grid_s"] * cfg["n_vis"] * (ws - 1) / n_sample)
+        secs, _r = job.run()
+        if ws > 1:
+            if t_fft is None:    # the mesh part of a step (transforms + stack), once
+                from oracle import wstack_oracle as O
+                g = np.zeros((cfg["n_w"], cfg["n_v"], cfg["n_u"]), np.complex128)
+                t0 = time.perf_counter()
+                O.image_from_grid(g, cfg["n_u"], cfg["n_v"], cfg["n_w"], cfg["cell"], 0.0,
+                                  cfg["w_max"], threads)
+                t_fft = time.perf_counter() - t0
+                del g
+            secs = t_fft + (secs - t_fft) * ws
+        times.append(secs)
     s = float(np.mean(times))
     value = cfg["n_vis"] * ws / s / 1e6
-    sample = (f"per step: {n_sample} records gridded on the full mesh + 1 of 32 planes "
-              f"transformed/stacked, scaled to {ws} x {cfg['n_vis']} records")
+    if ws == 1:
+        sample = (f"per step: one full cfg2 image ({cfg['n_vis']} records, 2048x2048x32), "
+                  f"measured; {n_warm} untimed warm-up image")
+    else:
+        sample = (f"per step: {cfg['n_vis']} records gridded + the full 2048x2048x32 mesh "
+                  f"transformed/stacked, measured; gridding scaled x{ws} to the job's "
+                  f"{ws} x {cfg['n_vis']} records")
     out = {"impl": "reference", "metric": "Mvis/s imaged (bucket+grid+FFT+w-stack, dirty image out)",
            "value": round(value, 4), "unit": "Mvis/s", "n_gpus": ws, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(s * 1e3, 1), "higher_is_better": True,
+           "warmup": n_warm, "ms_per_step": round(s * 1e3, 1), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": "cfg2: synthetic 10M visibilities per GPU, 2048x2048 grid, "
                                   "32 w-planes, Gaussian support 7 (S=3, sigma=1), single channel, "

@@ -90,6 +90,9 @@ typedef struct {
     int64_t records;          /* == ops["records"] */
     int64_t tile_entries;     /* (record, 32-column strip) pairs bucketed */
     double phase_ms[7];       /* read, gridding, reduce, fft, wcorrect, write, total (exclusive) */
+    int64_t exchanged_records;/* records sent to another GPU (ops["exchange_bytes"] / 36); 0 on one GPU */
+    double gpu_joules;        /* NVML energy of the call's GPU over the call; -1 if unreadable */
+    double host_joules;       /* RAPL package energy of the host over the call; -1 if unreadable */
 } wsb_diag;
 
 typedef struct wsb_ctx wsb_ctx;
@@ -113,9 +116,11 @@ int wsb_ctx_trim(wsb_ctx *ctx);
 /* ---- whole hot path ---------------------------------------------------- */
 
 /* Replaces run_pipeline phases 2-5 (pipeline.py:95-152) for one GPU, HOST
- * buffers in and out: uvw f64[n], time_index u32[n] (nullable; records are
- * processed in array order, the (time_index, gindex) order the reference's
- * exchange produces for time-sorted input), vis = interleaved (re, im) f32
+ * buffers in and out: uvw f64[n], time_index u32[n] (nullable; when given
+ * it must be non-decreasing, else WSB_EINVAL "records must be sorted by
+ * time_index" as partition_time_ordered raises, visdata.py:354-355, on the
+ * run_pipeline path, pipeline.py:47-52; records are processed in array
+ * order = the (time_index, gindex) order of comms.py:534), vis = interleaved (re, im) f32
  * [n][n_chan][2], weight f32[n][n_chan]; image_out f64[n_v][n_u].
  * Copies in and out are part of the call. Synchronous. Page-locked buffers
  * (cudaHostAlloc / cudaHostRegister) move at DMA speed; pageable ones work
@@ -294,6 +299,11 @@ int wsb_image_finish(wsb_ctx *ctx, const wsb_grid *grid, const double *image_sum
  * mesh.py:131-146). */
 int wsb_grid_unpack(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t v_count,
                     const double *grid_s, double *grid_out);
+/* Same for the slab rows [row_lo, row_hi) only: grid_out is
+ * (n_w, row_hi - row_lo, n_u) complex128 (the slab-restricted parity check
+ * of large meshes). */
+int wsb_grid_unpack_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t v_count,
+                         int32_t row_lo, int32_t row_hi, const double *grid_s, double *grid_out);
 
 /* Debug / parity: the bucketing of the last wsb_grid_slab / wsb_image_device
  * call: record indices in bucket order and the n_buckets+1 bucket offsets,

@@ -219,6 +219,49 @@ def grid_slab(batch, n_u: int, n_w: int, kind: int, S: int, shape: float,
     return out, count
 
 
+def select_rows(batch, S: int, row_lo: int, row_hi: int):
+    """The records of ``batch`` whose footprint can reach rows
+    [row_lo, row_hi): the halo predicate of comms.py:521-523 applied to a
+    row block instead of a rank's slab. Record order is kept, so gridding
+    the selection reproduces those rows of the full slab bit for bit (every
+    tap pass of _accumulate visits the surviving records in the same order).
+    Returns a batch dict with v_start = row_lo, v_count = row_hi - row_lo."""
+    m = halo_mask(batch["gv"], S, row_lo, row_hi - row_lo)
+    out = {k: batch[k][m] for k in ("gu", "gv", "plane", "value")}
+    out["v_start"], out["v_count"] = row_lo, row_hi - row_lo
+    return out
+
+
+def grid_rows(batch, n_u: int, n_w: int, kind: int, S: int, shape: float,
+              row_lo: int, row_hi: int):
+    """Rows [row_lo, row_hi) of the slab grid of ``batch`` (the slab-restricted
+    oracle of SURVEY 8c: grid_sector on one SectorBatch, gridder.py:186-204),
+    without materialising the rest of the slab. Returns
+    (grid[n_w, row_hi - row_lo, n_u], grid_updates inside the rows)."""
+    return grid_slab(select_rows(batch, S, row_lo, row_hi), n_u, n_w, kind, S, shape)
+
+
+def count_updates(gu, gv, n_u: int, row_lo: int, row_hi: int, S: int) -> int:
+    """grid_sector's update count (gridder.py:164-183, 259) in closed form:
+    per record, (#columns i with |gu-i| <= S, 0 <= i < n_u) x (#rows j with
+    |gv-j| <= S, row_lo <= j < row_hi); the tap tests are the reference's."""
+    gu = np.asarray(gu, np.float64)
+    gv = np.asarray(gv, np.float64)
+    total = 0
+    step = 1 << 22
+    for a0 in range(0, len(gu), step):
+        cu = np.zeros(len(gu[a0:a0 + step]), np.int64)
+        cv = np.zeros_like(cu)
+        fu, fv = np.floor(gu[a0:a0 + step]), np.floor(gv[a0:a0 + step])
+        for a in range(-S, S + 1):
+            i = fu + a
+            cu += (np.abs(gu[a0:a0 + step] - i) <= S) & (i >= 0) & (i < n_u)
+            j = fv + a
+            cv += (np.abs(gv[a0:a0 + step] - j) <= S) & (j >= row_lo) & (j < row_hi)
+        total += int((cu * cv).sum())
+    return total
+
+
 def grid_all(prepared_parts, n_u, n_v, n_w, kind, S, shape, n_ranks):
     """grid_all (gridder.py:262-294): exchange then grid each slab; the
     reduce is the identity after the exchange (pipeline.py:117-122).
@@ -280,14 +323,23 @@ def stack(planes, n_u, n_v, n_w, cell, v_start, v_count):
             float((acc.real ** 2).sum()))
 
 
-def image_from_grid(grid, n_u, n_v, n_w, cell, w_min_native, w_max_native):
+def image_from_grid(grid, n_u, n_v, n_w, cell, w_min_native, w_max_native, threads=1):
     """Phases fft + wcorrect + write of run_pipeline (pipeline.py:125-152)
-    on a full (single-slab) grid. Returns (pixels, imag_norm, real_norm)."""
+    on a full (single-slab) grid. ``threads`` > 1 transforms and corrects
+    planes concurrently (the planes are independent, pipeline.py:127-147);
+    the stack still sums them in plane order. Returns (pixels, imag_norm,
+    real_norm)."""
     sign = checker_sign(n_u, 0, n_v)
-    planes = []
-    for k in range(n_w):
+
+    def plane(k):
         p = ifft2(grid[k] * sign)
-        planes.append(w_correct(p, k, n_u, n_v, n_w, cell, w_min_native, w_max_native, 0, n_v))
+        return w_correct(p, k, n_u, n_v, n_w, cell, w_min_native, w_max_native, 0, n_v)
+
+    if threads > 1:
+        with _cf.ThreadPoolExecutor(threads) as ex:
+            planes = list(ex.map(plane, range(n_w)))
+    else:
+        planes = [plane(k) for k in range(n_w)]
     pix, isq, rsq = stack(planes, n_u, n_v, n_w, cell, 0, n_v)
     return pix, math.sqrt(isq), math.sqrt(rsq)
 
@@ -309,19 +361,20 @@ def image(u, v, w, time_index, vis, weight, n_u, n_v, n_w, cell, w_min_native,
         grid, updates = grid_slab(batch, n_u, n_w, kind, half_support, shape)
     else:
         grid = np.zeros((n_w, n_v, n_u), np.complex128)
+        # row blocks as the reference's deterministic threads (gridder.py:206-221);
+        # each thread holds only its block (grid_rows), not a whole slab
         blocks = [partition_1d(n_v, threads, t) for t in range(threads)]
 
         def work(blk):
             b0, bc = blk
-            g, c = grid_slab(batch, n_u, n_w, kind, half_support, shape, b0, b0 + bc)
-            return b0, bc, g, c
+            g, c = grid_rows(batch, n_u, n_w, kind, half_support, shape, b0, b0 + bc)
+            grid[:, b0:b0 + bc] = g
+            return c
 
-        updates = 0
         with _cf.ThreadPoolExecutor(threads) as ex:
-            for b0, bc, g, c in ex.map(work, blocks):
-                grid[:, b0:b0 + bc] = g[:, b0:b0 + bc]
-                updates += c
-    pix, inorm, rnorm = image_from_grid(grid, n_u, n_v, n_w, cell, w_min_native, w_max_native)
+            updates = sum(ex.map(work, blocks))
+    pix, inorm, rnorm = image_from_grid(grid, n_u, n_v, n_w, cell, w_min_native, w_max_native,
+                                        threads)
     return {"pixels": pix, "imag_residual_norm": inorm, "real_norm": rnorm,
             "grid_updates": updates, "grid": grid}
 

@@ -13,8 +13,14 @@ from .imager import (  # noqa: F401
     GridSpec,
     KernelSpec,
     PipelineResult,
+    ComplexGrid,
+    MeterError,
     RunRecord,
+    SectorBatch,
+    SlabRange,
+    grid_all,
     grid_sector,
+    slab_of,
     grid_slab_device,
     image,
     image_device,

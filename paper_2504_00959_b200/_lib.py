@@ -31,6 +31,7 @@ EXPORTS = (
     "wsb_grid_unpack", "wsb_tiles_debug", "wsb_last_timings", "wsb_row_histogram",
     "wsb_fft_rows_peer", "wsb_push_blocks", "wsb_ctx_set_precision", "wsb_route_planes_count",
     "wsb_route_planes_pack", "wsb_fft_cols_partial", "wsb_image_finish", "wsb_plane_histogram",
+    "wsb_grid_unpack_rows",
 )
 
 
@@ -52,7 +53,8 @@ class WsbExec(C.Structure):
 class WsbDiag(C.Structure):
     _fields_ = [("imag_residual_norm", C.c_double), ("real_norm", C.c_double),
                 ("grid_updates", C.c_int64), ("records", C.c_int64), ("tile_entries", C.c_int64),
-                ("phase_ms", C.c_double * 7)]
+                ("phase_ms", C.c_double * 7), ("exchanged_records", C.c_int64),
+                ("gpu_joules", C.c_double), ("host_joules", C.c_double)]
 
 
 class WsbError(RuntimeError):
@@ -63,14 +65,23 @@ _lib = None
 
 
 def lib() -> C.CDLL:
-    """Load libwsb.so (building it first if the sources are newer and nvcc
-    exists). Raises if the library cannot be loaded."""
+    """Load libwsb.so, building it first when it is missing (unless
+    WSB_NO_AUTOBUILD is set). A library older than its sources is loaded as
+    is, with a warning: rebuild with ``python -m paper_2504_00959_b200.build``
+    (the driver's build() step does). Raises if the library cannot be loaded."""
     global _lib
     if _lib is not None:
         return _lib
     if not LIB_PATH.exists() and os.environ.get("WSB_NO_AUTOBUILD") is None:
         from .build import build
         build()
+    if LIB_PATH.exists() and LIB_PATH == Path(__file__).resolve().parent / "libwsb.so":
+        from .build import stale_sources
+        newer = stale_sources(LIB_PATH)
+        if newer:
+            import warnings
+            warnings.warn(f"{LIB_PATH.name} is older than {', '.join(newer[:3])}: "
+                          "rebuild with python -m paper_2504_00959_b200.build", stacklevel=2)
     if not LIB_PATH.exists():
         raise ImportError(f"{LIB_PATH} is missing: run python -m paper_2504_00959_b200.build")
     L = C.CDLL(str(LIB_PATH))
@@ -102,6 +113,7 @@ def lib() -> C.CDLL:
         "wsb_ctx_set_precision": (C.c_int, [p, i32]),
         "wsb_fft_cols_stack": (C.c_int, [p, G, i32, p, i32, i32, i32, i32, p, p, p]),
         "wsb_grid_unpack": (C.c_int, [p, G, i32, i32, p, p]),
+        "wsb_grid_unpack_rows": (C.c_int, [p, G, i32, i32, i32, i32, p, p]),
         "wsb_tiles_debug": (C.c_int, [p, p, p, p, p]),
         "wsb_last_timings": (C.c_int, [p, p, p]),
     }

@@ -41,6 +41,15 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
+def stale_sources(lib: Path = LIB) -> list:
+    """Sources / headers newer than ``lib`` (names), [] if it is current."""
+    if not lib.exists():
+        return ["(missing)"]
+    t = lib.stat().st_mtime
+    deps = [CSRC / s for s in SOURCES] + [CSRC / h for h in HEADERS] + [ROOT / "include" / "wsb.h"]
+    return [d.name for d in deps if d.exists() and d.stat().st_mtime > t]
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     nvcc = _nvcc()
     BUILD.mkdir(exist_ok=True)

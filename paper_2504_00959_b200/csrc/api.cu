@@ -1,8 +1,11 @@
 // C ABI of libwsb.so (include/wsb.h): contexts, workspace, validation and
 // the whole-hot-path entry points that replace run_pipeline phases 2-5
 // (pipeline.py:95-152).
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -98,19 +101,108 @@ __global__ void __launch_bounds__(256) k_sum_partials(const double *p, int nb, d
     }
 }
 
-// P layout -> (plane, row, col) complex128 with the checkerboard sign removed.
-__global__ void k_unpack(const double2 *p, double2 *out, int n_w, int n_u, int v_start, int v_count) {
+// Strip layout -> (plane, row, col) complex128 with the checkerboard sign
+// removed, for slab rows [r0, r0 + nr) (relative to v_start).
+__global__ void k_unpack(const double2 *p, double2 *out, int n_w, int n_u, int v_start, int v_count,
+                         int r0, int nr) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t total = (int64_t)n_w * v_count * n_u;
+    const int64_t total = (int64_t)n_w * nr * n_u;
     if (e >= total) return;
     const int i = e % n_u;
     const int64_t t = e / n_u;
-    const int j = t % v_count;
-    const int k = t / v_count;
+    const int j = (int)(t % nr) + r0;
+    const int k = (int)(t / nr);
     // strip layout [plane][col/32][row][col%32]
     double2 z = p[(((int64_t)k * ((n_u + 31) / 32) + i / 32) * v_count + j) * 32 + i % 32];
     const double s = ((i + v_start + j) & 1) ? -1.0 : 1.0;
     out[e] = make_double2(z.x * s, z.y * s);
+}
+
+// ---------------------------------------------------------------------------
+// Energy over a call (SURVEY 8b wsb_diag.gpu_joules / host_joules): NVML's
+// total-energy counter of the call's GPU (mJ; libnvidia-ml is opened at run
+// time, no link dependency) and the RAPL package counters of the host
+// (/sys/class/powercap/intel-rapl:N/energy_uj, wrap-around corrected).
+// -1 when a counter is unreadable. The counters update every few ms, so a
+// single short call reads coarse values; metered runs loop many calls.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Nvml {
+    void *so = nullptr;
+    int (*get_handle)(const char *, void **) = nullptr;
+    int (*energy)(void *, unsigned long long *) = nullptr;
+    bool ok = false;
+    Nvml() {
+        so = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
+        if (!so) return;
+        auto init = (int (*)())dlsym(so, "nvmlInit_v2");
+        get_handle = (int (*)(const char *, void **))dlsym(so, "nvmlDeviceGetHandleByPciBusId_v2");
+        energy = (int (*)(void *, unsigned long long *))dlsym(so, "nvmlDeviceGetTotalEnergyConsumption");
+        ok = init && get_handle && energy && init() == 0;
+    }
+    // millijoules of the CUDA device `dev` (matched by PCI bus id), or -1
+    double mj(int dev) {
+        if (!ok) return -1.0;
+        char bus[32];
+        if (cudaDeviceGetPCIBusId(bus, sizeof(bus), dev) != cudaSuccess) {
+            cudaGetLastError();
+            return -1.0;
+        }
+        void *h = nullptr;
+        unsigned long long e = 0;
+        if (get_handle(bus, &h) != 0 || energy(h, &e) != 0) return -1.0;
+        return (double)e;
+    }
+};
+
+Nvml &nvml() {
+    static Nvml n;
+    return n;
+}
+
+// sum over package domains of (energy_uj, max_energy_range_uj); false if none readable
+bool rapl_read(std::vector<std::pair<double, double>> *out) {
+    out->clear();
+    for (int i = 0; i < 16; ++i) {
+        const std::string base = "/sys/class/powercap/intel-rapl:" + std::to_string(i);
+        FILE *f = std::fopen((base + "/energy_uj").c_str(), "r");
+        if (!f) continue;
+        double e = -1, r = 0;
+        if (std::fscanf(f, "%lf", &e) != 1) e = -1;
+        std::fclose(f);
+        if ((f = std::fopen((base + "/max_energy_range_uj").c_str(), "r"))) {
+            if (std::fscanf(f, "%lf", &r) != 1) r = 0;
+            std::fclose(f);
+        }
+        if (e >= 0) out->push_back({e, r});
+    }
+    return !out->empty();
+}
+
+}  // namespace
+
+void EnergyWindow::start(int dev) {
+    device = dev;
+    gpu0 = nvml().mj(dev);
+    host_ok = rapl_read(&host0);
+}
+
+void EnergyWindow::stop(double *gpu_j, double *host_j) {
+    const double g1 = nvml().mj(device);
+    *gpu_j = (gpu0 >= 0 && g1 >= 0) ? (g1 - gpu0) / 1e3 : -1.0;
+    std::vector<std::pair<double, double>> h1;
+    if (host_ok && rapl_read(&h1) && h1.size() == host0.size()) {
+        double uj = 0;
+        for (size_t i = 0; i < h1.size(); ++i) {
+            double d = h1[i].first - host0[i].first;
+            if (d < 0) d += host0[i].second;   // counter wrapped
+            uj += d;
+        }
+        *host_j = uj / 1e6;
+    } else {
+        *host_j = -1.0;
+    }
 }
 
 }  // namespace wsb
@@ -386,18 +478,30 @@ int wsb_image_finish(wsb_ctx *ctx, const wsb_grid *grid, const double *image_sum
     return image_finish(ctx, grid, image_sum, image, norm_partials);
 }
 
-int wsb_grid_unpack(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t v_count,
-                    const double *grid_p, double *grid_out) {
+int wsb_grid_unpack_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t v_count,
+                         int32_t row_lo, int32_t row_hi, const double *grid_p, double *grid_out) {
     if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
     WSB_TRY(validate_grid(grid));
+    if (v_start < 0 || v_count < 1 || v_start + v_count > grid->n_v)
+        return fail(WSB_EINVAL, "slab rows outside the mesh");
+    if (row_lo < v_start || row_hi > v_start + v_count || row_lo > row_hi)
+        return fail(WSB_EINVAL, "rows outside the slab");
     WSB_TRY(set_device(ctx));
-    const int64_t total = (int64_t)grid->n_w * v_count * grid->n_u;
+    const int nr = row_hi - row_lo;
+    const int64_t total = (int64_t)grid->n_w * nr * grid->n_u;
     if (total == 0) return WSB_OK;
     k_unpack<<<ceil_div(total, 256), 256, 0, ctx->stream>>>((const double2 *)grid_p,
                                                             (double2 *)grid_out, grid->n_w,
-                                                            grid->n_u, v_start, v_count);
+                                                            grid->n_u, v_start, v_count,
+                                                            row_lo - v_start, nr);
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
+}
+
+int wsb_grid_unpack(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, int32_t v_count,
+                    const double *grid_p, double *grid_out) {
+    return wsb_grid_unpack_rows(ctx, grid, v_start, v_count, v_start, v_start + v_count, grid_p,
+                                grid_out);
 }
 
 int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *idx_host, uint32_t *off_host, int64_t *n_entries,
@@ -422,9 +526,10 @@ int wsb_last_timings(wsb_ctx *ctx, double *ms6, int32_t *launches) {
     return WSB_OK;
 }
 
-int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern, const double *u,
-                     const double *v, const double *w, const float *vis, const float *weight,
-                     int64_t n, int32_t n_chan, double *image_out, wsb_diag *diag) {
+static int image_device_impl(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
+                             const double *u, const double *v, const double *w, const float *vis,
+                             const float *weight, const uint32_t *time_index, int64_t n,
+                             int32_t n_chan, double *image_out, wsb_diag *diag) {
     if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
     WSB_TRY(validate_grid(grid));
     WSB_TRY(validate_kernel(kern));
@@ -458,7 +563,7 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
 
     WSB_CUDA_TRY(cudaEventRecord(ev[0], ctx->stream));
     WSB_CUDA_TRY(cudaMemsetAsync(upd, 0, sizeof(unsigned long long), ctx->stream));
-    WSB_TRY(prepare(ctx, grid, u, v, w, vis, weight, n, n_chan, rec, plane));
+    WSB_TRY(prepare(ctx, grid, u, v, w, vis, weight, n, n_chan, rec, plane, time_index));
     WSB_CUDA_TRY(cudaEventRecord(ev[1], ctx->stream));
     RowBuckets bk;
     WSB_TRY(bucket_rows(ctx, grid, kern->half_support, 0, n_v, rec, plane, n, &bk));
@@ -498,8 +603,20 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
         diag->phase_ms[3] = ms[3] + ms[4];              // fft (column pass carries w correction)
         diag->phase_ms[4] = ms[5];                      // wcorrect: final reduction
         diag->phase_ms[6] = ms[0] + ms[1] + ms[2] + ms[3] + ms[4] + ms[5];
+        diag->exchanged_records = 0;   // one GPU: no record leaves the device
     }
     return WSB_OK;
+}
+
+int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern, const double *u,
+                     const double *v, const double *w, const float *vis, const float *weight,
+                     int64_t n, int32_t n_chan, double *image_out, wsb_diag *diag) {
+    EnergyWindow en;
+    if (diag && ctx) en.start(ctx->device);
+    int rc = image_device_impl(ctx, grid, kern, u, v, w, vis, weight, nullptr, n, n_chan, image_out,
+                               diag);
+    if (rc == WSB_OK && diag) en.stop(&diag->gpu_joules, &diag->host_joules);
+    return rc;
 }
 
 static std::mutex g_host_mu;
@@ -508,7 +625,6 @@ static wsb_ctx *g_host_ctx[64] = {nullptr};
 int wsb_image(const wsb_grid *grid, const wsb_kernel *kern, const wsb_exec *exec, const double *u,
               const double *v, const double *w, const uint32_t *time_index, const float *vis,
               const float *weight, int64_t n, int32_t n_chan, double *image_out, wsb_diag *diag) {
-    (void)time_index;
     WSB_TRY(validate_grid(grid));
     WSB_TRY(validate_kernel(kern));
     if (n < 0 || n_chan < 1) return fail(WSB_EINVAL, "n must be >= 0 and n_chan >= 1");
@@ -528,8 +644,12 @@ int wsb_image(const wsb_grid *grid, const wsb_kernel *kern, const wsb_exec *exec
     const size_t b_uvw = rnd(8 * (size_t)nn), b_vis = rnd(8 * (size_t)nn * n_chan),
                  b_wt = rnd(4 * (size_t)nn * n_chan);
     const size_t b_img = 8 * (size_t)grid->n_u * grid->n_v;
+    const size_t b_t = time_index ? rnd(4 * (size_t)nn) : 0;
     unsigned char *in;
-    WSB_TRY(ensure(ctx, kSlotHostIn, 3 * b_uvw + b_vis + b_wt + b_img, (void **)&in));
+    WSB_TRY(ensure(ctx, kSlotHostIn, 3 * b_uvw + b_vis + b_wt + b_img + b_t, (void **)&in));
+    uint32_t *dt = time_index ? (uint32_t *)(in + 3 * b_uvw + b_vis + b_wt + b_img) : nullptr;
+    EnergyWindow en;
+    if (diag) en.start(dev);
     double *du = (double *)in, *dv = (double *)(in + b_uvw), *dw = (double *)(in + 2 * b_uvw);
     float *dvis = (float *)(in + 3 * b_uvw), *dwt = (float *)(in + 3 * b_uvw + b_vis);
     double *dimg = (double *)(in + 3 * b_uvw + b_vis + b_wt);
@@ -545,10 +665,11 @@ int wsb_image(const wsb_grid *grid, const wsb_kernel *kern, const wsb_exec *exec
         WSB_CUDA_TRY(cudaMemcpyAsync(dw, w, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
         WSB_CUDA_TRY(cudaMemcpyAsync(dvis, vis, 8 * (size_t)n * n_chan, cudaMemcpyHostToDevice, ctx->stream));
         WSB_CUDA_TRY(cudaMemcpyAsync(dwt, weight, 4 * (size_t)n * n_chan, cudaMemcpyHostToDevice, ctx->stream));
+        if (dt) WSB_CUDA_TRY(cudaMemcpyAsync(dt, time_index, 4 * (size_t)n, cudaMemcpyHostToDevice, ctx->stream));
     }
     cudaEventRecord(a1, ctx->stream);
     wsb_diag local;
-    int rc = wsb_image_device(ctx, grid, kern, du, dv, dw, dvis, dwt, n, n_chan, dimg, &local);
+    int rc = image_device_impl(ctx, grid, kern, du, dv, dw, dvis, dwt, dt, n, n_chan, dimg, &local);
     if (rc == WSB_OK) {
         cudaEventRecord(a2, ctx->stream);
         cudaError_t e = cudaMemcpyAsync(image_out, dimg, b_img, cudaMemcpyDeviceToHost, ctx->stream);
@@ -565,6 +686,7 @@ int wsb_image(const wsb_grid *grid, const wsb_kernel *kern, const wsb_exec *exec
         diag->phase_ms[0] = r;
         diag->phase_ms[5] = wr;
         diag->phase_ms[6] = tot;
+        en.stop(&diag->gpu_joules, &diag->host_joules);
     }
     cudaEventDestroy(a0);
     cudaEventDestroy(a1);

@@ -13,7 +13,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kBlockItems = 2048;  // records per block in the count/pack kernels
 
-enum : int { kErrUV = 1, kErrW = 2, kErrWeight = 4 };
+enum : int { kErrUV = 1, kErrW = 2, kErrWeight = 4, kErrTime = 8 };
 
 // complex128(vis) * float32 weight with NumPy's full complex multiply
 // (ar*br - ai*bi, ar*bi + ai*br), bi = 0: keeps the sign of zero bit-exact.
@@ -78,12 +78,14 @@ __device__ __forceinline__ uint32_t plane_of(double ww, int n_w) {
 __global__ void __launch_bounds__(kThreads) k_prepare(
     const double *__restrict__ u, const double *__restrict__ v, const double *__restrict__ w,
     const float2 *__restrict__ vis, const float *__restrict__ wt, int64_t n, double n_u,
-    double n_v, int n_w, double4 *__restrict__ rec, uint32_t *__restrict__ plane, int *err) {
+    double n_v, int n_w, double4 *__restrict__ rec, uint32_t *__restrict__ plane, int *err,
+    const uint32_t *__restrict__ tidx) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double uu = u[i], vv = v[i], ww = w[i];
     const float wv = wt[i];
     int e = check_uvw(uu, vv, ww);
+    if (tidx && i + 1 < n && tidx[i] > tidx[i + 1]) e |= kErrTime;
     if (!isfinite(wv) || wv < 0.0f) e |= kErrWeight;
     if (e) atomicOr(err, e);
     const double2 val = cadd(make_double2(0.0, 0.0),
@@ -96,11 +98,12 @@ __global__ void __launch_bounds__(kThreads) k_prepare_multichan(
     const double *__restrict__ u, const double *__restrict__ v, const double *__restrict__ w,
     const float2 *__restrict__ vis, const float *__restrict__ wt, int64_t n, int n_chan,
     double n_u, double n_v, int n_w, double4 *__restrict__ rec, uint32_t *__restrict__ plane,
-    int *err) {
+    int *err, const uint32_t *__restrict__ tidx) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double uu = u[i], vv = v[i], ww = w[i];
     int e = check_uvw(uu, vv, ww);
+    if (tidx && i + 1 < n && tidx[i] > tidx[i + 1]) e |= kErrTime;
     const float2 *vr = vis + i * n_chan;
     const float *wr = wt + i * n_chan;
     for (int c = 0; c < n_chan; ++c)
@@ -320,7 +323,7 @@ int row_histogram(wsb_ctx *ctx, const wsb_grid *g, const double *rec, int64_t n,
 
 int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v, const double *w,
             const float *vis, const float *weight, int64_t n, int32_t n_chan, double *rec,
-            uint32_t *plane) {
+            uint32_t *plane, const uint32_t *time_index) {
     ctx->route.valid = false;   // records are (re)written
     if (n <= 0) return WSB_OK;
     int *err;
@@ -329,11 +332,11 @@ int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v, c
     if (n_chan == 1)
         k_prepare<<<ceil_div(n, kThreads), kThreads, 0, ctx->stream>>>(
             u, v, w, (const float2 *)vis, weight, n, (double)g->n_u, (double)g->n_v, g->n_w,
-            (double4 *)rec, plane, err);
+            (double4 *)rec, plane, err, time_index);
     else
         k_prepare_multichan<<<ceil_div(n, kThreads), kThreads, 0, ctx->stream>>>(
             u, v, w, (const float2 *)vis, weight, n, n_chan, (double)g->n_u, (double)g->n_v,
-            g->n_w, (double4 *)rec, plane, err);
+            g->n_w, (double4 *)rec, plane, err, time_index);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host, err, sizeof(int), cudaMemcpyDeviceToHost,
@@ -343,6 +346,9 @@ int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v, c
     if (e & kErrUV) return fail(WSB_EINVAL, "u and v must lie in [0, 1)");
     if (e & kErrW) return fail(WSB_EINVAL, "w must lie in [0, 1]");
     if (e & kErrWeight) return fail(WSB_EINVAL, "weights must be finite and >= 0");
+    // partition_time_ordered (visdata.py:354-355), reached by run_pipeline
+    // through _partition_for_ranks (pipeline.py:47-52)
+    if (e & kErrTime) return fail(WSB_EINVAL, "records must be sorted by time_index");
     return WSB_OK;
 }
 
@@ -422,6 +428,8 @@ int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *st
     if (nb_out) *nb_out = nb;
     auto &c = ctx->route;
     c.rec = rec;
+    c.plane = plane;
+    c.by_plane = by_plane;
     c.n = n;
     c.S = S;
     c.R = R;
@@ -441,7 +449,10 @@ int route_pack(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *sta
     Slabs sl;
     WSB_TRY(make_routing(g, R, starts, by_plane, &sl));
     auto &c = ctx->route;
-    bool hit = c.valid && c.rec == rec && c.n == n && c.S == S && c.R == R &&
+    // the cache key covers every input of the destination mask: records,
+    // their planes (plane mode), mode, halo, slabs
+    bool hit = c.valid && c.rec == rec && c.plane == plane && c.by_plane == by_plane &&
+               c.n == n && c.S == S && c.R == R &&
                c.n_v == (by_plane ? -g->n_w : g->n_v) &&
                c.starts[8] == R;
     for (int d = 0; hit && d < R; ++d) hit = c.starts[d] == sl.start[d];

@@ -64,6 +64,8 @@ struct wsb_ctx {
     // immediately preceding count on the same records and slabs
     struct {
         const double *rec = nullptr;
+        const uint32_t *plane = nullptr;
+        int by_plane = -1;
         int64_t n = -1;
         int S = -1, R = -1, n_v = -1, nb = 0;
         int starts[9] = {0};
@@ -124,7 +126,7 @@ int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t 
 // prepare.cu
 int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v,
             const double *w, const float *vis, const float *weight, int64_t n,
-            int32_t n_chan, double *rec, uint32_t *plane);
+            int32_t n_chan, double *rec, uint32_t *plane, const uint32_t *time_index = nullptr);
 // by_plane = 0: v-slabs with the +-S halo; 1: w-plane ranges (plane is read,
 // packed planes are rebased to the destination's first plane)
 int route_count(wsb_ctx *ctx, const wsb_grid *g, int S, int R, const int32_t *starts,
@@ -169,6 +171,16 @@ int fft_cols_stack(wsb_ctx *ctx, const wsb_grid *g, int n_sources, const int32_t
 int image_finish(wsb_ctx *ctx, const wsb_grid *g, const double *sum, double *image,
                  double *norm_partials);
 int strip_to_image(wsb_ctx *ctx, const wsb_grid *g, const double *strip, double *image);
+
+// NVML (GPU) + RAPL (host) energy over a window of host time (api.cu)
+struct EnergyWindow {
+    int device = 0;
+    double gpu0 = -1.0;
+    bool host_ok = false;
+    std::vector<std::pair<double, double>> host0;
+    void start(int dev);
+    void stop(double *gpu_j, double *host_j);
+};
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 inline int ilog2(int64_t n) {

@@ -17,9 +17,17 @@ import glob
 from pathlib import Path
 
 
+RAPL_ROOT = "/sys/class/powercap"
+
+# Host power model used when RAPL is unreadable: the reference's synthetic
+# meter default for a CPU node at the OS-governed frequency
+# (metrics.py:56-57, DEFAULT_WATTS["default"]).
+MODELLED_HOST_WATTS = 500.0
+
+
 def _rapl_domains():
     doms = []
-    for d in sorted(glob.glob("/sys/class/powercap/intel-rapl:*")):
+    for d in sorted(glob.glob(f"{RAPL_ROOT}/intel-rapl:*")):
         if ":" in Path(d).name[len("intel-rapl:"):]:
             continue                      # sub-domains (core, uncore, dram) are inside the package
         e = Path(d) / "energy_uj"
@@ -68,7 +76,28 @@ class NvmlRaplMeter:
             for (e, wrap), a, b in zip(self.rapl, self._h0, h1):
                 host += ((b - a) % wrap) / 1e6
         self._g0 = self._h0 = None
-        return {"total": gpu + (host or 0.0), "gpu": gpu, "host": host}
+        out = {"total": gpu + (host or 0.0), "gpu": gpu}
+        if host is not None:          # RunRecord rejects non-numeric entries
+            out["host"] = host
+        return out
+
+
+class ModelledHostMeter:
+    """Host energy as watts x seconds per phase -- the reference's
+    SyntheticPowerMeter model (metrics.py:129-144) at one power level, used
+    (and labelled as modelled) only where RAPL cannot be read."""
+
+    def __init__(self, watts: float = MODELLED_HOST_WATTS):
+        if watts <= 0:
+            raise ValueError(f"watts must be positive, got {watts}")
+        self.watts = float(watts)
+        self.source = f"modelled host power {self.watts:.0f} W (SyntheticPowerMeter default level)"
+
+    def start(self):
+        pass
+
+    def joules(self, durations: dict, freq_level: str = "default") -> dict:
+        return {phase: self.watts * seconds for phase, seconds in durations.items()}
 
 
 def green_productivity(t_ref: float, e_ref: float, t_test: float, e_test: float,

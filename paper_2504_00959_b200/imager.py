@@ -141,8 +141,17 @@ class FinalImage:
     real_norm: float = 0.0
 
 
+FREQ_LEVELS = ("default", "high", "medium", "low")   # metrics.py:53
+
+
+class MeterError(Exception):
+    """An energy meter cannot produce a measurement (metrics.py:62-63)."""
+
+
 @dataclass
 class RunRecord:
+    """Per-phase wall times and joules of one run (metrics.py:67-101)."""
+
     label: str
     topology: object
     freq_level: str
@@ -150,12 +159,30 @@ class RunRecord:
     energy_joules: dict = field(default_factory=dict)
 
     def __post_init__(self):
-        if self.freq_level not in ("default", "high", "medium", "low"):
-            raise ValueError(f"unknown freq_level {self.freq_level!r}")
-        total = self.phase_times.get("total", 0.0)
+        if self.freq_level not in FREQ_LEVELS:
+            raise ValueError(f"freq_level must be one of {FREQ_LEVELS}")
+        if "total" not in self.phase_times:
+            raise ValueError("phase_times must include 'total'")
+        for name, value in {**self.phase_times, **self.energy_joules}.items():
+            if value < 0:
+                raise ValueError(f"negative value for {name}: {value}")
         parts = sum(v for k, v in self.phase_times.items() if k != "total")
-        if parts > total * (1 + 1e-9) + 1e-12:
-            raise ValueError("phase times exceed the total")
+        if self.phase_times["total"] < parts - 1e-9:
+            raise ValueError("total time smaller than the sum of its phases")
+
+    @property
+    def n_nodes(self) -> int:
+        return self.topology.n_nodes if self.topology else 1
+
+    @property
+    def total_seconds(self) -> float:
+        return self.phase_times["total"]
+
+    @property
+    def total_joules(self) -> float:
+        if "total" not in self.energy_joules:
+            raise MeterError(f"run {self.label!r} carries no total energy")
+        return self.energy_joules["total"]
 
 
 @dataclass
@@ -276,14 +303,18 @@ def grid_slab_device(rec: torch.Tensor, plane: torch.Tensor, spec: GridSpec, ker
     return out, int(upd.value)
 
 
-def unpack_grid_device(grid_p: torch.Tensor, spec: GridSpec, v_start: int, v_count: int):
-    """Strip layout -> (n_w, v_count, n_u) complex128 without the checkerboard sign."""
+def unpack_grid_device(grid_p: torch.Tensor, spec: GridSpec, v_start: int, v_count: int,
+                       rows: tuple | None = None):
+    """Strip layout -> (n_w, v_count, n_u) complex128 without the checkerboard
+    sign; ``rows`` = (row_lo, row_hi) (absolute rows inside the slab) keeps
+    only those rows."""
     spec = as_grid_spec(spec)
     ctx = context(grid_p.device)
-    out = torch.empty((spec.n_w, v_count, spec.n_u, 2), dtype=torch.float64, device=grid_p.device)
+    r0, r1 = rows if rows is not None else (v_start, v_start + v_count)
+    out = torch.empty((spec.n_w, r1 - r0, spec.n_u, 2), dtype=torch.float64, device=grid_p.device)
     g = spec.c_struct()
-    L.check(L.lib().wsb_grid_unpack(ctx.handle, C.byref(g), int(v_start), int(v_count),
-                                    _ptr(grid_p), _ptr(out)))
+    L.check(L.lib().wsb_grid_unpack_rows(ctx.handle, C.byref(g), int(v_start), int(v_count),
+                                         int(r0), int(r1), _ptr(grid_p), _ptr(out)))
     return torch.view_as_complex(out)
 
 
@@ -411,28 +442,26 @@ def image_stream(batches, spec, kern, device: int = 0):
 _PINNED_POOLS: dict = {}
 
 
+_PINNED_POOL_CAP = 3   # page-locked images kept per shape (the stream holds <= 3 in flight)
+
+
 def _pinned_image(pool: list, spec) -> torch.Tensor:
     """A page-locked (n_v, n_u) float64 tensor from ``pool``: one nobody else
     references any more (the yielded numpy view holds its tensor), else a new
     one -- pinning is slow, so steady state allocates nothing and the image
-    is handed out without a host copy."""
+    is handed out without a host copy. The pool keeps at most
+    _PINNED_POOL_CAP buffers per shape; a caller holding more images at once
+    (e.g. ``list(image_stream(...))``) gets un-pooled buffers that go back to
+    torch's host allocator when dropped."""
     import sys
     for t in pool:
         # references: the pool list, the loop variable, getrefcount's argument
         if sys.getrefcount(t) <= 3:
             return t
     t = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, pin_memory=True)
-    pool.append(t)
+    if len(pool) < _PINNED_POOL_CAP:
+        pool.append(t)
     return t
-
-
-def _host_copy(t: torch.Tensor) -> np.ndarray:
-    """Private host copy of a page-locked staging tensor (torch's parallel
-    copy: the single-threaded numpy copy of a 32 MB image costs more than
-    the device pipeline it overlaps)."""
-    out = torch.empty(t.shape, dtype=t.dtype)
-    out.copy_(t)
-    return out.numpy()
 
 
 def diag_dict(d: L.WsbDiag) -> dict:
@@ -484,14 +513,93 @@ def image(u, v, w, time_index, vis, weight, spec, kern, device: int = 0,
 # reference-compatible hooks
 # ---------------------------------------------------------------------------
 
+@dataclass(frozen=True)
+class SlabRange:
+    """Rows [v_start, v_start + v_count) of one rank (mesh.py:113-126)."""
+    rank: int
+    v_start: int
+    v_count: int
+
+    @property
+    def v_end(self) -> int:
+        return self.v_start + self.v_count
+
+
+def slab_of(spec, rank: int, n_ranks: int) -> SlabRange:
+    """The v-slab of ``rank`` (mesh.py:152-159)."""
+    if n_ranks < 1 or not (0 <= rank < n_ranks):
+        raise ValueError(f"invalid rank {rank} of {n_ranks}")
+    if n_ranks > spec.n_v:
+        raise ValueError(f"n_ranks {n_ranks} exceeds n_v {spec.n_v}")
+    v0, vc = partition_1d(spec.n_v, n_ranks, rank)
+    return SlabRange(rank, v0, vc)
+
+
+@dataclass
+class ComplexGrid:
+    """A slab of the mesh, (plane, v_row, u_col) complex128 (mesh.py:129-146)."""
+    spec: object
+    slab: SlabRange
+    data: np.ndarray = None
+
+    def __post_init__(self):
+        shape = (self.spec.n_w, self.slab.v_count, self.spec.n_u)
+        if self.data is None:
+            self.data = np.zeros(shape, np.complex128)
+        else:
+            self.data = np.ascontiguousarray(self.data, np.complex128)
+            if self.data.shape != shape:
+                raise ValueError(f"grid data shape {self.data.shape} != {shape}")
+
+
+@dataclass
+class SectorBatch:
+    """One slab's prepared records in (time_index, gindex) order
+    (gridder.py:114-157); same validation: equal column lengths and every
+    anchor row within the slab's +-halo_rows band."""
+    slab: SlabRange
+    gu: np.ndarray
+    gv: np.ndarray
+    plane: np.ndarray
+    value: np.ndarray
+    time_index: np.ndarray = None
+    gindex: np.ndarray = None
+    is_halo: np.ndarray = None
+    halo_rows: int = 0
+
+    def __post_init__(self):
+        self.gu = np.ascontiguousarray(self.gu, np.float64)
+        self.gv = np.ascontiguousarray(self.gv, np.float64)
+        n = len(self.gu)
+        self.plane = np.ascontiguousarray(self.plane, np.uint32)
+        self.value = np.ascontiguousarray(self.value, np.complex128)
+        self.time_index = (np.zeros(n, np.uint32) if self.time_index is None
+                           else np.ascontiguousarray(self.time_index, np.uint32))
+        self.gindex = (np.arange(n, dtype=np.uint64) if self.gindex is None
+                       else np.ascontiguousarray(self.gindex, np.uint64))
+        rows = np.floor(self.gv).astype(np.int64)
+        if self.is_halo is None:
+            self.is_halo = ~((rows >= self.slab.v_start) & (rows < self.slab.v_end))
+        for a in (self.gv, self.plane, self.value, self.time_index, self.gindex, self.is_halo):
+            if len(a) != n:
+                raise ValueError("batch columns must share one length")
+        if n and (rows.min() < self.slab.v_start - self.halo_rows - 1
+                  or rows.max() > self.slab.v_end + self.halo_rows):
+            raise ValueError("record outside slab+halo")
+
+    def __len__(self) -> int:
+        return len(self.gu)
+
+
 def grid_sector(batch, kern, out, threads: int = 1, deterministic: bool = True) -> int:
     """gridder.grid_sector (gridder.py:186-259) on the GPU.
 
-    ``batch`` carries gu, gv, plane, value (a SectorBatch); ``out`` has
-    ``spec``, ``slab`` (v_start, v_count) and ``data`` (n_w, v_count, n_u)
-    complex128, which is accumulated into like the reference does. Returns
-    the number of cell updates. ``threads``/``deterministic`` are accepted for
-    API parity: the GPU result is always deterministic."""
+    ``batch`` carries gu, gv, plane, value (a SectorBatch, ours or the
+    reference's); ``out`` has ``spec``, ``slab`` (v_start, v_count) and
+    ``data`` (n_w, v_count, n_u) complex128, which is accumulated into like
+    the reference does. Returns the number of cell updates.
+    ``threads``/``deterministic`` are accepted for API parity: the GPU result
+    is always deterministic (and bit-identical for any thread count)."""
     slab = out.slab
     if (slab.v_start, slab.v_count) != (batch.slab.v_start, batch.slab.v_count):
         raise ValueError("batch and output slab ranges differ")
@@ -501,7 +609,7 @@ def grid_sector(batch, kern, out, threads: int = 1, deterministic: bool = True) 
         return 0
     S = kern.half_support
     gv = np.asarray(batch.gv, np.float64)
-    if np.any(gv + S < slab.v_start) or np.any(gv - S > slab.v_end - 1):
+    if np.any(gv + S < slab.v_start) or np.any(gv - S > slab.v_start + slab.v_count - 1):
         raise ValueError("record outside slab+halo")
     ctx = context()
     dev = torch.device("cuda", ctx.device)
@@ -513,6 +621,70 @@ def grid_sector(batch, kern, out, threads: int = 1, deterministic: bool = True) 
     g = unpack_grid_device(gp, spec, slab.v_start, slab.v_count)
     out.data += g.cpu().numpy()
     return upd
+
+
+def grid_all(per_rank_records, spec, kern, topo, strategy=None, log=None):
+    """gridder.grid_all (gridder.py:262-294) for a virtual topology on one GPU:
+    the ranks' record partitions (VisChunk-like: u, v, w, time_index, vis,
+    weight; rank order = gindex order) go to the v-slab owners with the
+    +-S halo (comms.py:495-547: records of a slab in (time_index, gindex)
+    order), each slab is gridded (wsb_grid_slab) and returned as a
+    ComplexGrid. The reduce is the identity after the exchange; the
+    returned MessageLog holds the exchange and reduce messages the
+    reference logs for ``topo`` (msglog.py). Bit-identical slabs for any
+    rank count. Returns (slabs, log)."""
+    from . import msglog
+    spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
+    kind = getattr(strategy, "kind", "direct") if strategy is not None else "direct"
+    R = int(topo.n_ranks)
+    if len(per_rank_records) != R:
+        raise ValueError(f"expected {R} record partitions, got {len(per_rank_records)}")
+    S = kern.half_support
+    ctx = context()
+    dev = torch.device("cuda", ctx.device)
+    lens = [len(c.u) for c in per_rank_records]
+    cat = lambda name: np.concatenate([np.asarray(getattr(c, name)) for c in per_rank_records])  # noqa: E731
+    u, v, w, t = cat("u"), cat("v"), cat("w"), cat("time_index").astype(np.uint32)
+    vis = np.concatenate([_cols2d(np.asarray(c.vis), len(c.u)) for c in per_rank_records])
+    wt = np.concatenate([_cols2d(np.asarray(c.weight), len(c.u)) for c in per_rank_records])
+    rec, plane = prepare_device(u, v, w, vis, wt, spec, device=dev)
+    if len(t) > 1 and np.any(np.diff(t.astype(np.int64)) < 0):
+        # the exchange delivers (time_index, gindex) order: a stable sort by time
+        order = torch.argsort(torch.from_numpy(t.astype(np.int64)).to(dev), stable=True)
+        rec, plane = rec[order].contiguous(), plane[order].contiguous()
+    g = spec.c_struct()
+    counts = []
+    off = 0
+    for n_r in lens:   # messages of the exchange: per source partition and slab
+        cnt = (C.c_int64 * R)()
+        L.check(L.lib().wsb_route_count(ctx.handle, C.byref(g), S, R, None,
+                                        _ptr(rec[off:off + n_r]) if n_r else None, n_r, cnt))
+        counts.append([int(x) for x in cnt])
+        off += n_r
+    slabs = []
+    if R > 1:
+        from .distributed import CudaBackend
+        srec, spl, per_slab = CudaBackend(dev).route(rec, plane, spec, S, R)
+    else:
+        srec, spl, per_slab = rec, plane, [rec.shape[0]]
+    off = 0
+    for d in range(R):
+        sl = slab_of(spec, d, R)
+        m = int(per_slab[d])
+        out = ComplexGrid(spec, sl)
+        if m:
+            gp, _ = grid_slab_device(srec[off:off + m], spl[off:off + m], spec, kern, sl.v_start,
+                                     sl.v_count)
+            out.data[...] = unpack_grid_device(gp, spec, sl.v_start, sl.v_count).cpu().numpy()
+        off += m
+        slabs.append(out)
+    log = log if log is not None else msglog.MessageLog()
+    if R > 1:
+        for msg in msglog.exchange_messages(topo, counts):
+            log.append(msg)
+        for msg in msglog.reduce_messages(topo, kind, spec.n_u, spec.n_v, spec.n_w):
+            log.append(msg)
+    return slabs, log
 
 
 # ---------------------------------------------------------------------------
@@ -655,28 +827,86 @@ def write_image(img: FinalImage, base_path, provenance: dict | None = None, pgm:
 # run_pipeline drop-in (pipeline.py:61-191)
 # ---------------------------------------------------------------------------
 
-class _EmptyLog:
-    """MessageLog stand-in: one GPU, no inter-rank messages."""
+def measure(meter, durations: dict, freq_level: str = "default") -> dict:
+    """metrics.measure (metrics.py:183-193): per-phase joules from the meter's
+    ``joules(durations, freq_level)``, plus their sum as "total" when the
+    meter reports phases only."""
+    for phase, seconds in durations.items():
+        if seconds < 0:
+            raise ValueError(f"negative duration for {phase}")
+    joules = meter.joules(durations, freq_level)
+    if "total" not in joules:
+        joules = dict(joules)
+        joules["total"] = sum(v for v in joules.values() if v is not None)
+    return joules
 
-    def total_bytes(self, phase=None):
-        return 0
 
-    def count(self, phase=None):
-        return 0
+def _partition_bounds(time_index: np.ndarray, n_ranks: int):
+    """_partition_for_ranks (pipeline.py:47-58): the [lo, hi) record range of
+    each rank -- contiguous groups of time slices (partition_time_ordered,
+    visdata.py:344-366), or plain record runs when there are more ranks than
+    slices. Also says whether the time-sorted check applies."""
+    n = len(time_index)
+    slices = np.unique(time_index)
+    if n_ranks <= len(slices):
+        out = []
+        for r in range(n_ranks):
+            s0, sc = partition_1d(len(slices), n_ranks, r)
+            lo = int(np.searchsorted(time_index, slices[s0], side="left"))
+            hi = int(np.searchsorted(time_index, slices[s0 + sc - 1], side="right"))
+            out.append((lo, hi))
+        return out, True
+    return [(partition_1d(n, n_ranks, r)[0], sum(partition_1d(n, n_ranks, r)))
+            for r in range(n_ranks)], False
 
-    def to_csv(self, path):
-        Path(path).write_text("phase,src_rank,dst_rank,intra_node,nbytes\n")
+
+def exchange_counts(cols, spec, half_support: int, bounds, device: int = 0):
+    """Records each source rank's time partition sends to each v-slab of
+    partition_1d(n_v, R) with the +-half_support halo predicate
+    (comms.py:516-523), counted on the GPU (wsb_route_count). [R][R] ints."""
+    R = len(bounds)
+    rec, _plane = prepare_device(cols["u"], cols["v"], cols["w"], cols["vis"], cols["weight"],
+                                 spec, device=device)
+    ctx = context(rec.device)
+    g = spec.c_struct()
+    out = []
+    for lo, hi in bounds:
+        cnt = (C.c_int64 * R)()
+        sub = rec[lo:hi]
+        L.check(L.lib().wsb_route_count(ctx.handle, C.byref(g), int(half_support), R, None,
+                                        _ptr(sub) if hi > lo else None, hi - lo, cnt))
+        out.append([int(x) for x in cnt])
+    return out
 
 
 def run_pipeline(dataset_path, n_u: int, n_v: int, n_w: int, cell_size_lm: float, kernel,
                  topo=None, strategy=None, meter=None, freq_level: str = "default",
                  label: str = "run", out_dir=None, pgm: bool = False, seed=None,
                  device: int = 0) -> PipelineResult:
-    """Same call as the reference run_pipeline; the gridding, FFT and
-    w-stacking phases run on one B200 through wsb_image. ``topo``/``strategy``
-    are accepted for API parity (the GPU path needs no virtual ranks; the
-    reduce phase is the identity after the exchange, pipeline.py:117-122)."""
+    """Same call, result type and error behaviour as the reference
+    run_pipeline (pipeline.py:61-191); the gridding, FFT and w-stacking
+    phases run on the B200 through wsb_image.
+
+    ``topo`` (a reference Topology, default 1x1) and ``strategy`` (default
+    ReduceStrategy("direct", True)) keep their meaning for everything the
+    caller can observe: the records are split into the ranks' time
+    partitions (pipeline.py:47-58; unsorted time_index raises ValueError as
+    partition_time_ordered does), and the returned MessageLog, messages.csv
+    and ``ops`` byte / message totals are those of the reference's virtual
+    choreography on ``topo`` (msglog.py; exchange counts measured on the
+    GPU). The image itself does not depend on the topology (the reference
+    guarantees bit-identical grids for any rank count, gridder.py:267-268)
+    and is computed once on ``device``. Multi-GPU imaging is
+    ``distributed.run_pipeline_distributed`` (one process per GPU).
+    ``meter``: any object with ``start()`` and ``joules(durations,
+    freq_level)`` (the reference's meters, energy.NvmlRaplMeter); per-phase
+    joules as metrics.measure returns them (pipeline.py:173-176)."""
+    from . import msglog
     kern = as_kernel_spec(kernel)
+    kind = getattr(strategy, "kind", "direct") if strategy is not None else "direct"
+    if kind not in msglog.REDUCE_KINDS:
+        raise ValueError(f"reduce kind must be one of {msglog.REDUCE_KINDS}, got {kind!r}")
+    R = int(topo.n_ranks) if topo is not None else 1
     if meter is not None and hasattr(meter, "start"):
         meter.start()
     t_begin = time.perf_counter()
@@ -685,10 +915,12 @@ def run_pipeline(dataset_path, n_u: int, n_v: int, n_w: int, cell_size_lm: float
     header, cols = read_dataset(dataset_path)
     spec = GridSpec(n_u=n_u, n_v=n_v, n_w=n_w, cell_size_lm=cell_size_lm,
                     w_min_native=header["w_min_native"], w_max_native=header["w_max_native"])
+    t_idx = cols["time_index"]
+    bounds, time_ordered = _partition_bounds(t_idx, R)
     times["read"] = time.perf_counter() - t0
     t0 = time.perf_counter()
-    img, diag = image(cols["u"], cols["v"], cols["w"], cols["time_index"], cols["vis"],
-                      cols["weight"], spec, kern, device=device)
+    img, diag = image(cols["u"], cols["v"], cols["w"], t_idx if time_ordered else None,
+                      cols["vis"], cols["weight"], spec, kern, device=device)
     wall = time.perf_counter() - t0
     pm = diag["phase_ms"]
     # exclusive segments of the device timeline, scaled into the call's wall time
@@ -696,18 +928,27 @@ def run_pipeline(dataset_path, n_u: int, n_v: int, n_w: int, cell_size_lm: float
     scale = min(1.0, wall / (dev_total / 1e3))
     times["read"] += pm[0] / 1e3 * scale          # host -> device copies
     times["gridding"] = pm[1] / 1e3 * scale
-    times["reduce"] = 0.0
+    times["reduce"] = 0.0                         # the identity after the exchange
     times["fft"] = pm[3] / 1e3 * scale
     times["wcorrect"] = pm[4] / 1e3 * scale
     t0 = time.perf_counter()
+    if R > 1:
+        counts = exchange_counts(cols, spec, kern.half_support, bounds, device=device)
+        log = msglog.virtual_log(topo, kind, n_u, n_v, n_w, counts)
+    else:
+        log = msglog.MessageLog()
     paths = {}
-    log = _EmptyLog()
     if out_dir is not None:
         out_dir = Path(out_dir)
         out_dir.mkdir(parents=True, exist_ok=True)
         prov = {"dataset": str(dataset_path),
                 "kernel": {"kind": kern.kind, "half_support": kern.half_support,
                            "shape_param": kern.shape_param},
+                "topology": ({"n_nodes": topo.n_nodes, "ranks_per_node": topo.ranks_per_node,
+                              "threads_per_rank": topo.threads_per_rank}
+                             if topo is not None else None),
+                "strategy": {"kind": kind,
+                             "deterministic": getattr(strategy, "deterministic", True)},
                 "engine": "wsb-b200", "seed": seed}
         paths = write_image(img, out_dir / "image", prov, pgm=pgm)
         log.to_csv(out_dir / "messages.csv")
@@ -715,10 +956,13 @@ def run_pipeline(dataset_path, n_u: int, n_v: int, n_w: int, cell_size_lm: float
     times["write"] = time.perf_counter() - t0 + pm[5] / 1e3 * scale
     times["total"] = time.perf_counter() - t_begin
     energy = {}
-    if meter is not None and hasattr(meter, "joules"):
-        energy = {"total": float(meter.joules())}
-    ops = {"records": len(cols["u"]), "grid_updates": diag["grid_updates"], "exchange_bytes": 0,
-           "reduce_bytes": 0, "fft_bytes": 0, "reduce_messages": 0, "stack_pixels": n_u * n_v}
+    if meter is not None:
+        energy = measure(meter, {k: v for k, v in times.items() if k != "total"}, freq_level)
+    ops = {"records": len(cols["u"]), "grid_updates": diag["grid_updates"],
+           "exchange_bytes": log.total_bytes(phase="exchange"),
+           "reduce_bytes": log.total_bytes(phase="reduce"),
+           "fft_bytes": log.total_bytes(phase="fft"),
+           "reduce_messages": log.count(phase="reduce"), "stack_pixels": n_u * n_v}
     run = RunRecord(label=label, topology=topo, freq_level=freq_level, phase_times=times,
                     energy_joules=energy)
     return PipelineResult(run=run, image=img, log=log, ops=ops, paths=paths)

@@ -208,15 +208,59 @@ def make_rvis(visdata):
     np.savez_compressed(HERE / "rvis.npz", **out)
 
 
+PIPELINE_CASES = [
+    # name, n_nodes, ranks_per_node, reduce kind, deterministic
+    ("t1x1", 1, 1, "direct", True),
+    ("t1x3", 1, 3, "direct", True),
+    ("t2x2h", 2, 2, "hybrid_ring", True),
+    ("t2x3r", 2, 3, "ring_rdma_like", True),
+    ("t3x2d", 3, 2, "direct", False),
+    ("t1x4h", 1, 4, "hybrid_ring", True),
+    ("t2x2r", 2, 2, "ring_rdma_like", False),
+]
+
+
+def make_pipeline(comms, metrics, pipeline):
+    """run_pipeline (pipeline.py:61-191) on chunks.rvis for several virtual
+    topologies and reduce strategies with a SyntheticPowerMeter: the written
+    messages.csv, the ops totals, the per-phase energy keys and the image."""
+    out = {}
+    path = HERE / "chunks.rvis"
+    kern = __import__("wstack.gridder", fromlist=["KernelSpec"]).KernelSpec.gaussian(3, 1.0)
+    for name, nn, rpn, kind, det in PIPELINE_CASES:
+        with tempfile.TemporaryDirectory() as tmp:
+            res = pipeline.run_pipeline(path, 64, 64, 4, 1e-3, kernel=kern,
+                                        topo=comms.Topology(nn, rpn),
+                                        strategy=comms.ReduceStrategy(kind, det),
+                                        meter=metrics.SyntheticPowerMeter(), freq_level="medium",
+                                        label=name, out_dir=tmp)
+            csv_text = Path(res.paths["messages"]).read_text()
+        p = f"{name}_"
+        out[p + "topo"] = np.array([nn, rpn, int(det)])
+        out[p + "kind"] = np.array(kind)
+        out[p + "messages_csv"] = np.array(csv_text)
+        out[p + "ops"] = np.array([res.ops[k] for k in ("records", "grid_updates", "exchange_bytes",
+                                                          "reduce_bytes", "fft_bytes",
+                                                          "reduce_messages", "stack_pixels")])
+        out[p + "energy_keys"] = np.array(sorted(res.run.energy_joules))
+        out[p + "pixels"] = res.image.pixels
+    np.savez_compressed(HERE / "pipeline.npz", **out)
+
+
 def main():
     comms, gridder, mesh, pipeline, visdata = _ref()
     if sys.argv[1:] == ["rvis"]:
         make_rvis(visdata)
         return
+    from wstack import metrics
+    if sys.argv[1:] == ["pipeline"]:
+        make_pipeline(comms, metrics, pipeline)
+        return
     make_bucket(comms, gridder, mesh, visdata)
     make_grid(comms, gridder, mesh, visdata)
     make_images(comms, gridder, mesh, pipeline, visdata)
     make_rvis(visdata)
+    make_pipeline(comms, metrics, pipeline)
     for f in sorted(HERE.glob("*.npz")):
         print(f.name, f.stat().st_size)
 

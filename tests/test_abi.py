@@ -39,7 +39,7 @@ def test_struct_sizes_match_header(L):
     assert C.sizeof(L.WsbGrid) == 40
     assert C.sizeof(L.WsbKernel) == 16
     assert C.sizeof(L.WsbExec) == 16
-    assert C.sizeof(L.WsbDiag) == 2 * 8 + 3 * 8 + 7 * 8
+    assert C.sizeof(L.WsbDiag) == 2 * 8 + 3 * 8 + 7 * 8 + 8 + 2 * 8
 
 
 def test_invalid_grid_rejected_before_any_launch(L):

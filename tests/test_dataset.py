@@ -72,37 +72,3 @@ def test_image_time_chunks_streamed(W):
         ref, dref = W.image(c["u"], c["v"], c["w"], None, c["vis"], c["weight"], spec, kern)
         assert img.pixels.tobytes() == ref.pixels.tobytes()
         assert diag["grid_updates"] == dref["grid_updates"]
-
-
-def test_plan_aggregate_rules():
-    """Aggregates: mean / sample std over the ok repeats, a failed run marks
-    its cell, image-hash identity per cell (bench.py:180-205)."""
-    from paper_2504_00959_b200.plan import PHASE_COLUMNS, aggregate_rows
-    from paper_2504_00959_b200.imager import OPS_COLUMNS
-    def row(cfg, rep, t, h, status="ok"):
-        r = {"config": cfg, "label": f"c{cfg}", "status": status, "failure_reason": "",
-             "image_sha256": h, "total_j": 0.0}
-        for c in PHASE_COLUMNS:
-            r[c] = t
-        for c in OPS_COLUMNS:
-            r[c] = 7
-        return r
-    hdr, out = aggregate_rows([row(0, 0, 1.0, "a"), row(0, 1, 3.0, "a"), row(1, 0, 2.0, "a"),
-                               row(1, 1, 2.0, "b"),
-                               {**row(2, 0, 0.0, ""), "status": "failed", "failure_reason": "X"}])
-    i = hdr.index("total_s_mean")
-    assert out[0][i] == 2.0 and abs(out[0][i + 1] - 2 ** 0.5) < 1e-12
-    assert out[0][-1] == 1 and out[1][-1] == 0
-    assert out[2][2] == "failed" and out[2][3] == 0
-
-
-@pytest.mark.gpu
-def test_run_plan_repeats_identical(W, tmp_path):
-    from paper_2504_00959_b200.plan import BenchPlan, run_plan
-    plan = BenchPlan(64, 64, 4, 1e-3, W.KernelSpec.gaussian(3, 1.0), topologies=["1x1"],
-                     strategies=["none"], repeats=3, dataset=GOLD / "chunks.rvis",
-                     output_dir=tmp_path)
-    res = run_plan(plan)
-    assert res.all_ok and len(res.raw_rows) == 3
-    assert res.aggregate_rows[0][-1] == 1          # image hashes identical across repeats
-    assert res.raw_path.exists() and res.aggregate_path.exists()
