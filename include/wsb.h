@@ -79,8 +79,13 @@ typedef struct {
     int32_t device;        /* CUDA ordinal */
     int32_t precision;     /* 64 (FP64 path) or 32 (FP32 path, see wsb_ctx_set_precision) */
     int32_t deterministic; /* accepted for API parity; results are always deterministic */
-    int32_t reserved;
+    int32_t flags;         /* WSB_EXEC_* bits */
 } wsb_exec;
+
+/* wsb_exec.flags / wsb_ctx_set_energy: read the NVML (GPU) and RAPL (host)
+ * energy counters around the call into wsb_diag.gpu_joules / host_joules.
+ * Off by default: an NVML energy query costs milliseconds. */
+#define WSB_EXEC_ENERGY 1
 
 /* Diagnostics: FinalImage norms (transform.py:72-83, 233-241) and the ops /
  * phase-time surrogates of run_pipeline (pipeline.py:178-186). */
@@ -91,8 +96,9 @@ typedef struct {
     int64_t tile_entries;     /* (record, 32-column strip) pairs bucketed */
     double phase_ms[7];       /* read, gridding, reduce, fft, wcorrect, write, total (exclusive) */
     int64_t exchanged_records;/* records sent to another GPU (ops["exchange_bytes"] / 36); 0 on one GPU */
-    double gpu_joules;        /* NVML energy of the call's GPU over the call; -1 if unreadable */
-    double host_joules;       /* RAPL package energy of the host over the call; -1 if unreadable */
+    double gpu_joules;        /* NVML energy of the call's GPU over the call; -1 if not measured
+                                 (WSB_EXEC_ENERGY off) or unreadable */
+    double host_joules;       /* RAPL package energy of the host over the call; -1 likewise */
 } wsb_diag;
 
 typedef struct wsb_ctx wsb_ctx;
@@ -110,6 +116,9 @@ int wsb_ctx_set_stream(wsb_ctx *ctx, void *stream);
  * weights, accumulation, phase screen and plane stack stay FP64; within 1e-5
  * relative L2 of the reference image). wsb_image takes it from exec. */
 int wsb_ctx_set_precision(wsb_ctx *ctx, int32_t precision);
+/* Energy counters around wsb_image_device calls on this context (see
+ * WSB_EXEC_ENERGY): on != 0 to enable. */
+int wsb_ctx_set_energy(wsb_ctx *ctx, int32_t on);
 /* Release cached device workspace. */
 int wsb_ctx_trim(wsb_ctx *ctx);
 

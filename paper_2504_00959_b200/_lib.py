@@ -20,6 +20,7 @@ WSB_ENCCL = -3
 WSB_ENOMEM = -4
 WSB_EUNSUPPORTED = -5
 P_GROUP = 1
+EXEC_ENERGY = 1
 KERNEL_GAUSSIAN = 0
 KERNEL_KAISER_BESSEL = 1
 
@@ -31,7 +32,7 @@ EXPORTS = (
     "wsb_grid_unpack", "wsb_tiles_debug", "wsb_last_timings", "wsb_row_histogram",
     "wsb_fft_rows_peer", "wsb_push_blocks", "wsb_ctx_set_precision", "wsb_route_planes_count",
     "wsb_route_planes_pack", "wsb_fft_cols_partial", "wsb_image_finish", "wsb_plane_histogram",
-    "wsb_grid_unpack_rows",
+    "wsb_grid_unpack_rows", "wsb_ctx_set_energy",
 )
 
 
@@ -47,7 +48,7 @@ class WsbKernel(C.Structure):
 
 class WsbExec(C.Structure):
     _fields_ = [("device", C.c_int32), ("precision", C.c_int32), ("deterministic", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("flags", C.c_int32)]
 
 
 class WsbDiag(C.Structure):
@@ -111,6 +112,7 @@ def lib() -> C.CDLL:
         "wsb_fft_rows_peer": (C.c_int, [p, G, i32, p, i32, i32, i32, p, p]),
         "wsb_push_blocks": (C.c_int, [p, i32, p, p, p]),
         "wsb_ctx_set_precision": (C.c_int, [p, i32]),
+        "wsb_ctx_set_energy": (C.c_int, [p, i32]),
         "wsb_fft_cols_stack": (C.c_int, [p, G, i32, p, i32, i32, i32, i32, p, p, p]),
         "wsb_grid_unpack": (C.c_int, [p, G, i32, i32, p, p]),
         "wsb_grid_unpack_rows": (C.c_int, [p, G, i32, i32, i32, i32, p, p]),

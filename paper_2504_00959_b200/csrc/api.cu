@@ -293,6 +293,12 @@ int wsb_ctx_set_precision(wsb_ctx *ctx, int32_t precision) {
     return WSB_OK;
 }
 
+int wsb_ctx_set_energy(wsb_ctx *ctx, int32_t on) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    ctx->energy = on ? 1 : 0;
+    return WSB_OK;
+}
+
 int wsb_ctx_set_stream(wsb_ctx *ctx, void *stream) {
     if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
     ctx->stream = (cudaStream_t)stream;
@@ -612,10 +618,14 @@ int wsb_image_device(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
                      const double *v, const double *w, const float *vis, const float *weight,
                      int64_t n, int32_t n_chan, double *image_out, wsb_diag *diag) {
     EnergyWindow en;
-    if (diag && ctx) en.start(ctx->device);
+    const bool metered = diag && ctx && ctx->energy;
+    if (metered) en.start(ctx->device);
     int rc = image_device_impl(ctx, grid, kern, u, v, w, vis, weight, nullptr, n, n_chan, image_out,
                                diag);
-    if (rc == WSB_OK && diag) en.stop(&diag->gpu_joules, &diag->host_joules);
+    if (rc == WSB_OK && diag) {
+        diag->gpu_joules = diag->host_joules = -1.0;
+        if (metered) en.stop(&diag->gpu_joules, &diag->host_joules);
+    }
     return rc;
 }
 
@@ -649,7 +659,8 @@ int wsb_image(const wsb_grid *grid, const wsb_kernel *kern, const wsb_exec *exec
     WSB_TRY(ensure(ctx, kSlotHostIn, 3 * b_uvw + b_vis + b_wt + b_img + b_t, (void **)&in));
     uint32_t *dt = time_index ? (uint32_t *)(in + 3 * b_uvw + b_vis + b_wt + b_img) : nullptr;
     EnergyWindow en;
-    if (diag) en.start(dev);
+    const bool metered = diag && exec && (exec->flags & WSB_EXEC_ENERGY);
+    if (metered) en.start(dev);
     double *du = (double *)in, *dv = (double *)(in + b_uvw), *dw = (double *)(in + 2 * b_uvw);
     float *dvis = (float *)(in + 3 * b_uvw), *dwt = (float *)(in + 3 * b_uvw + b_vis);
     double *dimg = (double *)(in + 3 * b_uvw + b_vis + b_wt);
@@ -686,7 +697,8 @@ int wsb_image(const wsb_grid *grid, const wsb_kernel *kern, const wsb_exec *exec
         diag->phase_ms[0] = r;
         diag->phase_ms[5] = wr;
         diag->phase_ms[6] = tot;
-        en.stop(&diag->gpu_joules, &diag->host_joules);
+        diag->gpu_joules = diag->host_joules = -1.0;
+        if (metered) en.stop(&diag->gpu_joules, &diag->host_joules);
     }
     cudaEventDestroy(a0);
     cudaEventDestroy(a1);

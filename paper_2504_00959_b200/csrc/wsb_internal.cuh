@@ -72,6 +72,7 @@ struct wsb_ctx {
         bool valid = false;
     } route;
     int precision = 64;               // wsb_ctx_set_precision: 64 or 32 (complex64 grids)
+    int energy = 0;                   // wsb_ctx_set_energy: NVML/RAPL counters around calls
     double last_ms[6] = {0, 0, 0, 0, 0, 0};
 };
 

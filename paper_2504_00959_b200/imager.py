@@ -467,7 +467,10 @@ def _pinned_image(pool: list, spec) -> torch.Tensor:
 def diag_dict(d: L.WsbDiag) -> dict:
     return {"imag_residual_norm": d.imag_residual_norm, "real_norm": d.real_norm,
             "grid_updates": int(d.grid_updates), "records": int(d.records),
-            "tile_entries": int(d.tile_entries), "phase_ms": list(d.phase_ms)}
+            "tile_entries": int(d.tile_entries), "phase_ms": list(d.phase_ms),
+            "exchanged_records": int(d.exchanged_records),
+            "gpu_joules": d.gpu_joules if d.gpu_joules >= 0 else None,
+            "host_joules": d.host_joules if d.host_joules >= 0 else None}
 
 
 def last_timings(device=None):
@@ -483,9 +486,11 @@ def last_timings(device=None):
 # ---------------------------------------------------------------------------
 
 def image(u, v, w, time_index, vis, weight, spec, kern, device: int = 0,
-          precision: int = 64) -> tuple[FinalImage, dict]:
+          precision: int = 64, energy: bool = False) -> tuple[FinalImage, dict]:
     """Dirty image from HOST arrays through wsb_image (copies in and out are
-    part of the call). Mirrors run_pipeline phases 2-5 (pipeline.py:95-152)."""
+    part of the call). Mirrors run_pipeline phases 2-5 (pipeline.py:95-152).
+    ``energy`` reads the NVML / RAPL counters around the call into
+    diag["gpu_joules"] / diag["host_joules"] (-1: unreadable)."""
     spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
     _require_cuda()
     u = np.ascontiguousarray(u, np.float64)
@@ -501,7 +506,7 @@ def image(u, v, w, time_index, vis, weight, spec, kern, device: int = 0,
     out = torch.empty((spec.n_v, spec.n_u), dtype=torch.float64, pin_memory=True).numpy()
     d = L.WsbDiag()
     g, k = spec.c_struct(), kern.c_struct()
-    ex = L.WsbExec(int(device), int(precision), 1, 0)
+    ex = L.WsbExec(int(device), int(precision), 1, L.EXEC_ENERGY if energy else 0)
     ti = None if time_index is None else np.ascontiguousarray(time_index, np.uint32)
     vp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)  # noqa: E731
     L.check(L.lib().wsb_image(C.byref(g), C.byref(k), C.byref(ex), vp(u), vp(v), vp(w), vp(ti),

@@ -262,3 +262,19 @@ def test_run_pipeline_unsorted_dataset_raises(W, tmp_path):
     with pytest.raises(ValueError, match="sorted by time_index"):
         W.run_pipeline(tmp_path / "bad.rvis", 64, 64, 4, 1e-3, W.KernelSpec.gaussian(3, 1.0),
                        topo=Topo(1, 2))
+
+
+def test_energy_counters_opt_in(W):
+    """wsb_diag.gpu_joules / host_joules (NVML / RAPL around the call) are
+    read only on request (WSB_EXEC_ENERGY); -1 / None otherwise."""
+    from paper_2504_00959_b200 import read_dataset
+    _, c = read_dataset(GOLDEN / "chunks.rvis")
+    spec = W.GridSpec(64, 64, 4, 1e-3, w_max_native=40.0)
+    k = W.KernelSpec.gaussian(3, 1.0)
+    _, d0 = W.image(c["u"], c["v"], c["w"], c["time_index"], c["vis"], c["weight"], spec, k)
+    assert d0["gpu_joules"] is None and d0["host_joules"] is None
+    _, d1 = W.image(c["u"], c["v"], c["w"], c["time_index"], c["vis"], c["weight"], spec, k,
+                    energy=True)
+    assert d1["gpu_joules"] is not None and d1["gpu_joules"] >= 0.0
+    assert d1["host_joules"] is None or d1["host_joules"] >= 0.0
+    assert d1["exchanged_records"] == 0
