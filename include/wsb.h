@@ -53,6 +53,12 @@ extern "C" {
  * transform.py:180-185 is already applied. */
 #define WSB_P_GROUP 1
 
+/* Column width of the gridder's output "strip layout":
+ *   grid_s[plane][col / WSB_STRIP][row][col % WSB_STRIP]   (complex128)
+ * every two rows of a strip are one 512-byte run; the checkerboard sign of
+ * transform.py:180-185 is applied. */
+#define WSB_STRIP 16
+
 /* Longest transform handled on chip (one CTA) and longest transform
  * supported: rows/columns of SP = N / WSB_ONCHIP_FFT_N > 1 blocks are split
  * by decimation in frequency into SP on-chip transforms (one CTA per output
@@ -93,7 +99,7 @@ typedef struct {
     double imag_residual_norm, real_norm;
     int64_t grid_updates;     /* == ops["grid_updates"] */
     int64_t records;          /* == ops["records"] */
-    int64_t tile_entries;     /* (record, 32-column strip) pairs bucketed */
+    int64_t tile_entries;     /* (record, gridder work item) pairs bucketed */
     double phase_ms[7];       /* read, gridding, reduce, fft, wcorrect, write, total (exclusive) */
     int64_t exchanged_records;/* records sent to another GPU (ops["exchange_bytes"] / 36); 0 on one GPU */
     double gpu_joules;        /* NVML energy of the call's GPU over the call; -1 if not measured
@@ -207,12 +213,13 @@ int wsb_row_histogram(wsb_ctx *ctx, const wsb_grid *grid, const double *rec, int
                       uint32_t *hist);
 
 /* grid_sector (gridder.py:186-259) for the slab rows [v_start, v_start+v_count):
- * buckets the m records by (plane, 32-column strip, anchor row) (counting
- * sort, record order inside a bucket), grids them with the convolution kernel
- * in a register-window sweep and writes the slab in the strip layout
- * (grid_s: complex128[n_w][ceil(n_u/32)][v_count][32], sign applied; every
- * row of a 32-column strip is one 512-byte run). grid_updates (host,
- * nullable) receives the number of cell updates; synchronises if given. */
+ * buckets the m records into work items (w plane, 64-column superstrip,
+ * 128-row block; stable radix sort, record order inside an item), grids them
+ * with the convolution kernel in a register-window sweep and writes the slab
+ * in the strip layout (grid_s: complex128[n_w][ceil(n_u/WSB_STRIP)][v_count]
+ * [WSB_STRIP], sign applied). grid_updates (host, nullable) receives the
+ * number of cell updates. Synchronises (entry count). Slabs that start on a
+ * multiple of 128 rows grid every cell bit-identically to a whole-mesh call. */
 int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern,
                   int32_t v_start, int32_t v_count,
                   const double *rec, const uint32_t *plane, int64_t m,
@@ -315,9 +322,10 @@ int wsb_grid_unpack_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, in
                          int32_t row_lo, int32_t row_hi, const double *grid_s, double *grid_out);
 
 /* Debug / parity: the bucketing of the last wsb_grid_slab / wsb_image_device
- * call: record indices in bucket order and the n_buckets+1 bucket offsets,
- * bucket = (plane * n_strips + strip) * (v_count + 2S) + floor(gv) - v_start + S
- * with 32-column strips. Sizes via wsb_tiles_debug(ctx, NULL, NULL, &n, &nb). */
+ * call: record indices in item order (record order inside an item) and the
+ * n_items+1 item offsets, item = (plane * ceil(n_u/64) + superstrip) *
+ * ceil(v_count/128) + row block. Sizes via wsb_tiles_debug(ctx, NULL, NULL,
+ * &n, &nb). */
 int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *idx_host, uint32_t *off_host,
                     int64_t *n_entries, int64_t *n_buckets);
 

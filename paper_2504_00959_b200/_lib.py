@@ -20,6 +20,7 @@ WSB_ENCCL = -3
 WSB_ENOMEM = -4
 WSB_EUNSUPPORTED = -5
 P_GROUP = 1
+STRIP = 16          # WSB_STRIP: column width of the gridder's strip layout
 EXEC_ENERGY = 1
 KERNEL_GAUSSIAN = 0
 KERNEL_KAISER_BESSEL = 1

@@ -112,8 +112,9 @@ __global__ void k_unpack(const double2 *p, double2 *out, int n_w, int n_u, int v
     const int64_t t = e / n_u;
     const int j = (int)(t % nr) + r0;
     const int k = (int)(t / nr);
-    // strip layout [plane][col/32][row][col%32]
-    double2 z = p[(((int64_t)k * ((n_u + 31) / 32) + i / 32) * v_count + j) * 32 + i % 32];
+    // strip layout [plane][col/WSB_STRIP][row][col%WSB_STRIP]
+    constexpr int SW = WSB_STRIP;
+    double2 z = p[(((int64_t)k * ((n_u + SW - 1) / SW) + i / SW) * v_count + j) * SW + i % SW];
     const double s = ((i + v_start + j) & 1) ? -1.0 : 1.0;
     out[e] = make_double2(z.x * s, z.y * s);
 }
@@ -380,11 +381,12 @@ static int grid_slab_impl(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *
                           const uint32_t *plane, int64_t m, double *grid_p,
                           unsigned long long *updates_dev, int64_t *n_entries_out,
                           const cudaEvent_t *mid = nullptr) {
-    RowBuckets bk;
-    WSB_TRY(bucket_rows(ctx, grid, kern->half_support, v_start, v_count, rec, plane, m, &bk));
+    ItemBuckets bk;
+    WSB_TRY(bucket_items(ctx, grid, kern->half_support, v_start, v_count, nullptr,
+                         const_cast<double *>(rec), const_cast<uint32_t *>(plane), m, &bk));
     if (n_entries_out) *n_entries_out = bk.n_entries;
     if (mid) WSB_CUDA_TRY(cudaEventRecord(*mid, ctx->stream));
-    return grid_sweep(ctx, grid, kern, v_start, v_count, rec, bk, grid_p, updates_dev);
+    return grid_items(ctx, grid, kern, v_start, v_count, rec, bk, grid_p, updates_dev);
 }
 
 int wsb_grid_slab(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kernel *kern, int32_t v_start,
@@ -555,7 +557,7 @@ static int image_device_impl(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kerne
     WSB_TRY(ensure(ctx, kSlotRec, 32 * (size_t)nn, (void **)&rec));
     WSB_TRY(ensure(ctx, kSlotPlane, 4 * (size_t)nn, (void **)&plane));
     // strip layout (gridder output) and P layout (row-pass output)
-    WSB_TRY(ensure(ctx, kSlotGrid, esz * n_w * ceil_div(n_u, 32) * 32 * n_v, &gs));
+    WSB_TRY(ensure(ctx, kSlotGrid, esz * n_w * ceil_div(n_u, WSB_STRIP) * WSB_STRIP * n_v, &gs));
     WSB_TRY(ensure(ctx, kSlotGridP, esz * n_w * n_u * n_v, &gp));
     // norm partials [residue][column][2] (residues: columns longer than 4096 are split)
     const int sp = std::max(1, n_v >> kMaxOnChipLog);
@@ -569,13 +571,20 @@ static int image_device_impl(wsb_ctx *ctx, const wsb_grid *grid, const wsb_kerne
 
     WSB_CUDA_TRY(cudaEventRecord(ev[0], ctx->stream));
     WSB_CUDA_TRY(cudaMemsetAsync(upd, 0, sizeof(unsigned long long), ctx->stream));
-    WSB_TRY(prepare(ctx, grid, u, v, w, vis, weight, n, n_chan, rec, plane, time_index));
-    WSB_CUDA_TRY(cudaEventRecord(ev[1], ctx->stream));
-    RowBuckets bk;
-    WSB_TRY(bucket_rows(ctx, grid, kern->half_support, 0, n_v, rec, plane, n, &bk));
+    ItemBuckets bk;
+    if (n_chan == 1) {
+        // prepare_chunk fused into the bucketing pass (one read of the columns)
+        WSB_CUDA_TRY(cudaEventRecord(ev[1], ctx->stream));
+        const VisColumns cols{u, v, w, vis, weight, time_index};
+        WSB_TRY(bucket_items(ctx, grid, kern->half_support, 0, n_v, &cols, rec, nullptr, n, &bk));
+    } else {
+        WSB_TRY(prepare(ctx, grid, u, v, w, vis, weight, n, n_chan, rec, plane, time_index));
+        WSB_CUDA_TRY(cudaEventRecord(ev[1], ctx->stream));
+        WSB_TRY(bucket_items(ctx, grid, kern->half_support, 0, n_v, nullptr, rec, plane, n, &bk));
+    }
     const int64_t n_entries = bk.n_entries;
     WSB_CUDA_TRY(cudaEventRecord(ev[2], ctx->stream));
-    WSB_TRY(grid_sweep(ctx, grid, kern, 0, n_v, rec, bk, gs, upd, prec));
+    WSB_TRY(grid_items(ctx, grid, kern, 0, n_v, rec, bk, gs, upd, prec));
     WSB_CUDA_TRY(cudaEventRecord(ev[3], ctx->stream));
     WSB_TRY(fft_rows(ctx, grid, n_v, gs, gp, 0, n_w, 1, nullptr, nullptr, prec));
     WSB_CUDA_TRY(cudaEventRecord(ev[4], ctx->stream));

@@ -1,29 +1,33 @@
-// K1b: bucketing of a slab's records by (w plane, 32-column strip, anchor row).
+// K1b: bucketing of a slab's records into the gridder's work items.
 //
 // The reference gives every slab the records of exchange_to_space_order in
 // (time_index, gindex) order (comms.py:534-545) and grids them tap-major
-// (gridder.py:160-183). The sweep gridder (grid.cu) instead walks each
-// 32-column strip of a plane down its rows, so it needs the strip's records
-// sorted by anchor row floor(gv). Every (record, strip) pair becomes one
-// entry with the dense key
-//     key = (plane * n_tc + tc) * RS + (floor(gv) - v_start + S),
-//     RS  = v_count + 2S (anchor rows that can touch the slab),
-// written in record order (block-stable compaction), then sorted by a
-// stable LSD radix sort (sort.cu). The final order is (key, record index):
-// deterministic, independent of how skewed the buckets are (LOFAR-like
-// tracks put millions of records into a few buckets), and -- the record
-// index following gindex -- independent of the GPU count. Bucket offsets
-// come from a key histogram.
+// (gridder.py:160-183). The GPU gridder (grid.cu) sweeps work items
+// item = (w plane, 64-column superstrip, 128-row block of the slab), so
+// every (record, item) pair the record's taps reach becomes one entry
+//     key = item | rowrel << item_bits,   rowrel = anchor row - (R0 - 2S)
+// (anchor row = floor(gv) - S, R0 = the block's first row), written in
+// record order by ONE pass over the records (k_keys: prepare_chunk fused in
+// when it starts from the visibility columns, entry compaction by a
+// decoupled look-back across blocks, item histogram), then stably
+// radix-sorted on the item bits only (sort.cu). Each item's entries are thus
+// a contiguous run in record (gindex) order -- independent of how skewed the
+// items are and of the GPU count; the gridder orders a run by window step
+// itself (a stable counting sort in shared memory).
 #include "wsb_internal.cuh"
 
 namespace wsb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kBlockItems = 2048;  // records per block
+constexpr int kPer = 8;                    // consecutive records per thread
+constexpr int kTile = kThreads * kPer;     // 2048 records per block
+
+enum : int { kErrUV = 1, kErrW = 2, kErrWeight = 4, kErrTime = 8 };
 
 struct KeyGeom {
-    int n_u, v_start, v_count, S, n_tc, rs;
+    int n_u, n_v, n_w, v_start, v_count, S;
+    int n_ss, n_rb, item_bits;
 };
 
 // Inclusive tap range of one axis: {i : |g - i| <= S} (gridder.py:171,177),
@@ -33,151 +37,274 @@ __device__ __forceinline__ bool tap_range(double g, int S, int lo, int hi, int *
     const double fl = floor(g);
     int i0 = (int)fl - S;
     if (__dsub_rn(g, (double)i0) > (double)S) ++i0;
-    int i1 = (int)fl + S;
+    const int i1 = (int)fl + S;
     *a = max(i0, lo);
     *b = min(i1, hi);
     return *a <= *b;
 }
 
-// Number of strips (0, 1 or 2) a record reaches and its first key.
-__device__ __forceinline__ int record_keys(const double4 &r, uint32_t plane, const KeyGeom &k,
-                                           uint32_t *key0) {
+// Entries of one record (at most 4: two superstrips x two row blocks).
+__device__ __forceinline__ int record_entries(double gu, double gv, uint32_t plane,
+                                              const KeyGeom &k, uint32_t *keys) {
+    // invalid coordinates (flagged by the validation) reach no item
+    if (!(gu >= 0.0 && gu < (double)k.n_u && gv >= 0.0 && gv < (double)k.n_v) || plane >= (uint32_t)k.n_w)
+        return 0;
     int i0, i1, j0, j1;
-    if (!tap_range(r.x, k.S, 0, k.n_u - 1, &i0, &i1)) return 0;
-    if (!tap_range(r.y, k.S, k.v_start, k.v_start + k.v_count - 1, &j0, &j1)) return 0;
-    const int rel = (int)floor(r.y) - k.v_start + k.S;
-    if (rel < 0 || rel >= k.rs) return 0;
-    const int tc0 = i0 >> 5, tc1 = i1 >> 5;
-    *key0 = ((uint32_t)plane * k.n_tc + tc0) * (uint32_t)k.rs + rel;
-    return tc1 - tc0 + 1;
+    if (!tap_range(gu, k.S, 0, k.n_u - 1, &i0, &i1)) return 0;
+    if (!tap_range(gv, k.S, k.v_start, k.v_start + k.v_count - 1, &j0, &j1)) return 0;
+    const int anchor = (int)floor(gv) - k.S;
+    const int ss0 = i0 / kSSCols, ss1 = i1 / kSSCols;
+    const int rb0 = (j0 - k.v_start) / kItemRows, rb1 = (j1 - k.v_start) / kItemRows;
+    int n = 0;
+    for (int rb = rb0; rb <= rb1; ++rb) {
+        const uint32_t rowrel = (uint32_t)(anchor - (k.v_start + rb * kItemRows - 2 * k.S));
+        for (int ss = ss0; ss <= ss1; ++ss) {
+            const uint32_t item = ((uint32_t)plane * k.n_ss + ss) * (uint32_t)k.n_rb + rb;
+            keys[n++] = item | (rowrel << k.item_bits);
+        }
+    }
+    return n;
 }
 
-__device__ __forceinline__ uint32_t block_excl_sum(uint32_t x, uint32_t *total, uint32_t *smem) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t incl = x;
+__device__ __forceinline__ int check_record(double uu, double vv, double ww, float wt) {
+    int e = 0;
+    // VisChunk.validate (visdata.py:178-184): u,v in [0,1), w in [0,1], finite weights >= 0
+    if (!(uu >= 0.0 && uu < 1.0 && vv >= 0.0 && vv < 1.0)) e |= kErrUV;
+    if (!(ww >= 0.0 && ww <= 1.0)) e |= kErrW;
+    if (!isfinite(wt) || wt < 0.0f) e |= kErrWeight;
+    return e;
+}
+
+__device__ __forceinline__ uint32_t plane_of_w(double ww, int n_w) {
+    if (n_w <= 1) return 0;
+    // floor(w*(n_w-1) + 0.5), two rounded FP64 ops, then clip (comms.py:484-488)
+    double k = floor(__dadd_rn(__dmul_rn(ww, (double)(n_w - 1)), 0.5));
+    k = fmin(fmax(k, 0.0), (double)(n_w - 1));
+    return (uint32_t)(k == k ? k : 0.0);
+}
+
+struct KeysArgs {
+    // FROM_INPUT: the visibility columns (one channel); else prepared records
+    const double *u, *v, *w;
+    const float2 *vis;
+    const float *wt;
+    const uint32_t *tidx;       // nullable: time order check
+    double4 *rec;               // FROM_INPUT: written; else read
+    uint32_t *plane;            // FROM_INPUT: written if non-null; else read
+    int64_t n;
+    KeyGeom g;
+    uint32_t *keys, *idx;       // entries in record order
+    uint32_t *item_cnt;         // [n_items] histogram
+    unsigned long long *state;  // [n_blocks] look-back: flag << 32 | value
+    uint32_t *ticket;           // dynamic block order
+    uint32_t *total;            // entries in all
+    int *err;
+};
+
+constexpr unsigned long long kAgg = 1ull << 32, kInc = 2ull << 32;
+
+// exclusive prefix of this block's entry count over all earlier blocks
+// (decoupled look-back; blocks take their index from a ticket, so every
+// earlier block is already running)
+__device__ uint32_t lookback(unsigned long long *state, uint32_t bid, uint32_t agg) {
+    volatile unsigned long long *st = state;
+    if (bid == 0) {
+        __threadfence();
+        st[0] = kInc | agg;
+        return 0;
+    }
+    st[bid] = kAgg | agg;
+    uint32_t prefix = 0;
+    int64_t j = (int64_t)bid - 1;
+    while (true) {
+        const unsigned long long s = st[j];
+        const unsigned long long f = s & ~0xFFFFFFFFull;
+        if (f == 0) continue;
+        prefix += (uint32_t)s;
+        if (f == kInc) break;
+        --j;
+    }
+    __threadfence();
+    st[bid] = kInc | (prefix + agg);
+    return prefix;
+}
+
+template <bool FROM_INPUT>
+__global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
+    __shared__ uint32_t s_bid, s_prefix, s_wsum[kThreads / 32];
+    __shared__ int s_err;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        s_bid = atomicAdd(a.ticket, 1u);
+        s_err = 0;
+    }
+    __syncthreads();
+    const uint32_t bid = s_bid;
+    const int64_t first = (int64_t)bid * kTile + (int64_t)tid * kPer;
+    uint32_t keys[kPer][4];
+    int cnt[kPer];
+    uint32_t mine = 0;
+    int e = 0;
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+        const int64_t i = first + r;
+        cnt[r] = 0;
+        if (i >= a.n) continue;
+        double gu, gv;
+        uint32_t pl;
+        if constexpr (FROM_INPUT) {
+            const double uu = a.u[i], vv = a.v[i], ww = a.w[i];
+            const float wt = a.wt[i];
+            const float2 vs = a.vis[i];
+            e |= check_record(uu, vv, ww, wt);
+            if (a.tidx && i + 1 < a.n && a.tidx[i] > a.tidx[i + 1]) e |= kErrTime;
+            gu = __dmul_rn(uu, (double)a.g.n_u);
+            gv = __dmul_rn(vv, (double)a.g.n_v);
+            pl = plane_of_w(ww, a.g.n_w);
+            // value = 0.0 + (-0.0 + vis*weight): NumPy's complex multiply with a
+            // zero imaginary weight and its pairwise-sum start, bit-exact
+            const double ar = vs.x, ai = vs.y, br = wt;
+            const double re = __dadd_rn(0.0, __dadd_rn(-0.0, __dsub_rn(__dmul_rn(ar, br), __dmul_rn(ai, 0.0))));
+            const double im = __dadd_rn(0.0, __dadd_rn(-0.0, __dadd_rn(__dmul_rn(ar, 0.0), __dmul_rn(ai, br))));
+            a.rec[i] = make_double4(gu, gv, re, im);
+            if (a.plane) a.plane[i] = pl;
+        } else {
+            const double4 rc = a.rec[i];
+            gu = rc.x;
+            gv = rc.y;
+            pl = a.plane[i];
+        }
+        cnt[r] = record_entries(gu, gv, pl, a.g, keys[r]);
+        mine += cnt[r];
+    }
+    if (FROM_INPUT && e) atomicOr(&s_err, e);
+    // block exclusive scan of the per-thread entry counts (record order)
+    uint32_t incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
     }
-    if (lane == 31) smem[warp] = incl;
+    if (lane == 31) s_wsum[warp] = incl;
     __syncthreads();
-    uint32_t base = 0, tot = 0;
+    uint32_t base = 0, agg = 0;
 #pragma unroll
-    for (int k = 0; k < kThreads / 32; ++k) {
-        const uint32_t s = smem[k];
-        if (k < warp) base += s;
-        tot += s;
+    for (int w = 0; w < kThreads / 32; ++w) {
+        const uint32_t s = s_wsum[w];
+        if (w < warp) base += s;
+        agg += s;
+    }
+    if (tid == 0) {
+        s_prefix = lookback(a.state, bid, agg);
+        if ((int64_t)(bid + 1) * kTile >= a.n) *a.total = s_prefix + agg;   // the last block
+        if (FROM_INPUT && s_err) atomicOr(a.err, s_err);
     }
     __syncthreads();
-    *total = tot;
-    return base + incl - x;
-}
-
-// entries per block (for the compaction) and the key histogram
-__global__ void __launch_bounds__(kThreads) k_keys_count(const double4 *__restrict__ rec,
-                                                         const uint32_t *__restrict__ plane,
-                                                         int64_t m, KeyGeom k,
-                                                         uint32_t *__restrict__ block_cnt,
-                                                         uint32_t *__restrict__ key_cnt) {
-    __shared__ uint32_t c;
-    if (threadIdx.x == 0) c = 0;
-    __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * kBlockItems;
-    uint32_t local = 0;
-    for (int it = 0; it < kBlockItems / kThreads; ++it) {
-        const int64_t i = base + it * kThreads + threadIdx.x;
-        if (i < m) {
-            uint32_t key;
-            const int n = record_keys(rec[i], plane[i], k, &key);
-            for (int t = 0; t < n; ++t) atomicAdd(&key_cnt[key + t * k.rs], 1u);
-            local += n;
-        }
-    }
+    uint32_t pos = s_prefix + base + incl - mine;
+    const uint32_t imask = (1u << a.g.item_bits) - 1u;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(&c, local);
-    __syncthreads();
-    if (threadIdx.x == 0) block_cnt[blockIdx.x] = c;
-}
-
-// (key, record) entries in record order
-__global__ void __launch_bounds__(kThreads) k_keys_write(const double4 *__restrict__ rec,
-                                                         const uint32_t *__restrict__ plane,
-                                                         int64_t m, KeyGeom k,
-                                                         const uint32_t *__restrict__ block_off,
-                                                         uint32_t *__restrict__ keys,
-                                                         uint32_t *__restrict__ idx) {
-    __shared__ uint32_t wsum[kThreads / 32];
-    uint32_t run = block_off[blockIdx.x];
-    const int64_t base = (int64_t)blockIdx.x * kBlockItems;
-    for (int it = 0; it < kBlockItems / kThreads; ++it) {
-        const int64_t i = base + it * kThreads + threadIdx.x;
-        uint32_t key = 0;
-        int n = 0;
-        if (i < m) n = record_keys(rec[i], plane[i], k, &key);
-        uint32_t tot;
-        uint32_t pos = run + block_excl_sum((uint32_t)n, &tot, wsum);
-        for (int t = 0; t < n; ++t) {
-            keys[pos + t] = key + t * k.rs;
-            idx[pos + t] = (uint32_t)i;
+    for (int r = 0; r < kPer; ++r)
+        for (int t = 0; t < cnt[r]; ++t) {
+            a.keys[pos] = keys[r][t];
+            a.idx[pos] = (uint32_t)(first + r);
+            atomicAdd(&a.item_cnt[keys[r][t] & imask], 1u);
+            ++pos;
         }
-        run += tot;
-    }
 }
 
 }  // namespace
 
-int bucket_rows(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_count,
-                const double *rec, const uint32_t *plane, int64_t m, RowBuckets *out) {
+int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_count,
+                 const VisColumns *in, double *rec, uint32_t *plane, int64_t m,
+                 ItemBuckets *out) {
     KeyGeom k;
     k.n_u = g->n_u;
+    k.n_v = g->n_v;
+    k.n_w = g->n_w;
     k.v_start = v_start;
     k.v_count = v_count;
     k.S = S;
-    k.n_tc = ceil_div(g->n_u, 32);
-    k.rs = v_count + 2 * S;
-    const int64_t n_keys = (int64_t)g->n_w * k.n_tc * k.rs;
-    if (n_keys >= 0xFFFFFFFFll) return fail(WSB_EUNSUPPORTED, "bucket key space exceeds 32 bits");
+    k.n_ss = ceil_div(g->n_u, kSSCols);
+    k.n_rb = ceil_div(v_count, kItemRows);
+    const int64_t n_items = (int64_t)g->n_w * k.n_ss * k.n_rb;
+    k.item_bits = std::max(1, ilog2(n_items));
+    // rowrel < kItemRows + 2S must fit above the item bits
+    if (k.item_bits + ilog2(kItemRows + 2 * kMaxS) > 32)
+        return fail(WSB_EUNSUPPORTED, "gridder item space exceeds 32-bit keys");
+    if (m > (int64_t)(0x7FFFFFFF / 4)) return fail(WSB_EUNSUPPORTED, "more than 2^29 records per GPU");
     uint32_t *cnt, *off;
-    WSB_TRY(ensure(ctx, kSlotTileCount, sizeof(uint32_t) * (n_keys + 1), (void **)&cnt));
-    WSB_TRY(ensure(ctx, kSlotTileOff, sizeof(uint32_t) * (n_keys + 1), (void **)&off));
-    WSB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (n_keys + 1), ctx->stream));
-    const int nb = std::max(1, ceil_div(m, kBlockItems));
-    uint32_t *bcnt, *boff;
-    WSB_TRY(ensure(ctx, kSlotBlockCounts, sizeof(uint32_t) * (nb + 1), (void **)&bcnt));
-    WSB_TRY(ensure(ctx, kSlotBlockOffsets, sizeof(uint32_t) * (nb + 1), (void **)&boff));
-    uint32_t total = 0;
-    if (m > 0) {
-        k_keys_count<<<nb, kThreads, 0, ctx->stream>>>((const double4 *)rec, plane, m, k, bcnt, cnt);
-        ctx->launches += 1;
-        WSB_CUDA_TRY(cudaGetLastError());
-        WSB_TRY(exclusive_scan_u32(ctx, bcnt, boff, nb, &total));
-    }
-    WSB_TRY(exclusive_scan_u32(ctx, cnt, off, n_keys + 1, nullptr));
-    const size_t eb = sizeof(uint32_t) * std::max<int64_t>(1, total);
+    WSB_TRY(ensure(ctx, kSlotTileCount, sizeof(uint32_t) * (n_items + 1), (void **)&cnt));
+    WSB_TRY(ensure(ctx, kSlotTileOff, sizeof(uint32_t) * (n_items + 1), (void **)&off));
+    WSB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (n_items + 1), ctx->stream));
+    const int nb = std::max(1, ceil_div(m, kTile));
+    // look-back state + ticket + total + error flag in one zeroed slot
+    unsigned long long *state;
+    WSB_TRY(ensure(ctx, kSlotBlockCounts, sizeof(unsigned long long) * (nb + 4), (void **)&state));
+    WSB_CUDA_TRY(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (nb + 4), ctx->stream));
+    uint32_t *ticket = reinterpret_cast<uint32_t *>(state + nb);
+    uint32_t *total = ticket + 2;
+    int *err = reinterpret_cast<int *>(ticket + 4);
+    // entry buffers: at most 4 entries per record
+    const size_t eb = sizeof(uint32_t) * std::max<int64_t>(1, 4 * m);
     uint32_t *ka, *kb, *ia, *ib;
     WSB_TRY(ensure(ctx, kSlotKeysA, eb, (void **)&ka));
     WSB_TRY(ensure(ctx, kSlotKeysB, eb, (void **)&kb));
     WSB_TRY(ensure(ctx, kSlotIdxA, eb, (void **)&ia));
     WSB_TRY(ensure(ctx, kSlotIdxB, eb, (void **)&ib));
-    if (total > 0) {
-        k_keys_write<<<nb, kThreads, 0, ctx->stream>>>((const double4 *)rec, plane, m, k, boff, ka, ia);
+    KeysArgs a;
+    a.u = in ? in->u : nullptr;
+    a.v = in ? in->v : nullptr;
+    a.w = in ? in->w : nullptr;
+    a.vis = in ? (const float2 *)in->vis : nullptr;
+    a.wt = in ? in->weight : nullptr;
+    a.tidx = in ? in->time_index : nullptr;
+    a.rec = (double4 *)rec;
+    a.plane = plane;
+    a.n = m;
+    a.g = k;
+    a.keys = ka;
+    a.idx = ia;
+    a.item_cnt = cnt;
+    a.state = state;
+    a.ticket = ticket;
+    a.total = total;
+    a.err = err;
+    if (m > 0) {
+        if (in)
+            k_keys<true><<<nb, kThreads, 0, ctx->stream>>>(a);
+        else
+            k_keys<false><<<nb, kThreads, 0, ctx->stream>>>(a);
         ctx->launches += 1;
         WSB_CUDA_TRY(cudaGetLastError());
     }
+    // entry count (and, from the columns, the validation flags) to the host
+    WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host, total, 2 * sizeof(int) + 2 * sizeof(int),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    const uint32_t n_entries = m > 0 ? (uint32_t)ctx->flag_host[0] : 0u;
+    const int e = ctx->flag_host[2];
+    if (e & kErrUV) return fail(WSB_EINVAL, "u and v must lie in [0, 1)");
+    if (e & kErrW) return fail(WSB_EINVAL, "w must lie in [0, 1]");
+    if (e & kErrWeight) return fail(WSB_EINVAL, "weights must be finite and >= 0");
+    // partition_time_ordered (visdata.py:354-355), reached by run_pipeline
+    // through _partition_for_ranks (pipeline.py:47-52)
+    if (e & kErrTime) return fail(WSB_EINVAL, "records must be sorted by time_index");
+    WSB_TRY(exclusive_scan_u32(ctx, cnt, off, n_items + 1, nullptr));
     uint32_t *ks, *is;
-    WSB_TRY(radix_sort_pairs(ctx, ka, kb, ia, ib, total, ilog2(n_keys), &ks, &is));
+    WSB_TRY(radix_sort_pairs(ctx, ka, kb, ia, ib, n_entries, k.item_bits, &ks, &is));
+    out->keys = ks;
     out->idx = is;
     out->off = off;
-    out->n_entries = total;
-    out->n_keys = n_keys;
-    out->n_tc = k.n_tc;
-    out->rs = k.rs;
+    out->n_entries = n_entries;
+    out->n_items = n_items;
+    out->n_ss = k.n_ss;
+    out->n_rb = k.n_rb;
+    out->item_bits = k.item_bits;
+    ctx->last_keys = ks;
     ctx->last_idx = is;
     ctx->last_off = off;
-    ctx->last_entries = total;
-    ctx->last_tiles = n_keys;
+    ctx->last_entries = n_entries;
+    ctx->last_tiles = n_items;
     return WSB_OK;
 }
 

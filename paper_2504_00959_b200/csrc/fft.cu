@@ -370,15 +370,16 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
     const int j0 = blockIdx.x * NSEQ;
     const int64_t plane = plane_lo + blockIdx.y;
     const int e = SPL ? (int)blockIdx.z : 0;
-    // in: strip layout [plane][col/32][row][col%32] (512-byte row runs)
+    // in: strip layout [plane][col/WSB_STRIP][row][col%WSB_STRIP]
+    constexpr int SW = WSB_STRIP;
     auto gld = [&](int seq, int col) {
         if (j0 + seq >= v_count) return cx<V>(0.0, 0.0);
-        const V *p = in + ((plane * n_strips + col / 32) * v_count + j0 + seq) * 32 + (col % 32);
+        const V *p = in + ((plane * n_strips + col / SW) * v_count + j0 + seq) * SW + (col % SW);
         if constexpr (SPL == 0) {
             return *p;
         } else {
-            // column col + s*N lies (N/32) strips further on
-            return dif_split<SPL>(p, (N / 32) * v_count * 32, e, col, N, twN);
+            // column col + s*N lies (N/SW) strips further on
+            return dif_split<SPL>(p, (N / SW) * v_count * SW, e, col, N, twN);
         }
     };
     // out: P[plane][col/G][row][col%G] per destination (RowDest); with a
@@ -831,7 +832,7 @@ int launch_cols(wsb_ctx *ctx, const ColArgs &a, const V *tw, int *nblocks, int s
 template <class V>
 int rows_dispatch(wsb_ctx *ctx, const wsb_grid *g, int v_count, const void *grid_a, int plo,
                   int phi, const RowDest &dst) {
-    const int ng = g->n_u / kG, ns = ceil_div(g->n_u, 32);
+    const int ng = g->n_u / kG, ns = ceil_div(g->n_u, WSB_STRIP);
     const int prec = sizeof(V) == 8 ? 32 : 64;
     // rows above the on-chip 4096 points: SP = n_u / 4096 residue CTAs per row
     const int logn = ilog2(g->n_u), logs = std::min(logn, kMaxOnChipLog), spl = logn - logs;

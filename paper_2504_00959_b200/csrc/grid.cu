@@ -1,21 +1,32 @@
-// K2: register-window sweep gridder (gridder.py:160-259, Eq. 3).
+// K2: register-window gridder over (plane, 64-column superstrip, 128-row
+// block) work items (gridder.py:160-259, Eq. 3).
 //
-// Work item = one warp = (w plane, 32-column strip, block of 128 slab rows).
-// Lane l owns column 32*strip + l. The item's records (bucket.cu) arrive
-// sorted by anchor row floor(gv); the warp keeps the 2S+1 rows a record can
-// touch as complex128 accumulators in registers and slides that window down
-// the block: before a record is applied, every row above its footprint is
-// final and is written straight to HBM (strip layout, checkerboard sign of
-// transform.py:180-185 applied). Each cell is therefore accumulated by one
-// lane in (anchor row, gindex) order -- deterministic and independent of
-// the number of GPUs -- and written exactly once: no shared-memory tile, no
-// atomics, no read-modify-write of HBM.
+// CTA = 4 warps = one item; warp w owns the 16 columns [16w, 16w+16) of the
+// superstrip. Inside a warp, lane = (row group q = lane / 16, column c =
+// lane % 16): lane (q, c) accumulates the rows B + q + 2t (t = 0..S) of its
+// column as complex128 registers, a window of 2S+2 rows that slides down the
+// block two rows at a time (a ring of S+1 slots, one code copy per ring
+// phase). A record with anchor row a = floor(gv) - S is applied while
+// a - B is 0 or 1: its 2S+1 footprint rows then lie inside the window. When
+// the next record starts lower, rows B and B+1 are final: the 32 lanes write
+// them as one 512-byte run (strip layout [plane][col/16][row][16], the
+// checkerboard sign of transform.py:180-185 applied) and the window moves on.
+// Each cell is accumulated by one lane, in (window step, record) order --
+// deterministic, and the same for any GPU count when slabs start on 128-row
+// boundaries (items then hold the same records) -- and written once: no
+// shared-memory tile, no atomics, no read-modify-write of HBM.
 //
-// Records are staged 32 at a time per warp: lane r loads record r through
-// the bucket index and computes its separable per-axis kernel weights once
-// (FP64; excluded taps get weight 0, so the per-record update below is
-// branch-free). The tap set is the reference's: |g - i| <= S with g - i
-// rounded as in gridder.py:170-177.
+// Versus one lane per column and a (2S+1)-row window (round 1: 7 of 32
+// lanes carried a record's taps at S=3), a record now occupies 2 x 16 lanes
+// x (S+1) rows: the FMA work per record falls from 14 to 8 double
+// instructions per touched 16-column strip at S=3.
+//
+// Records reach an item in record order (the stable bucketing of bucket.cu);
+// the CTA first sorts its item's entry list by window step in shared memory
+// (counting sort, stable, warp match/ballot ranks), then streams it in
+// chunks of 64 records gathered by cp.async two chunks ahead. Two threads
+// stage a record: one forms value * u-weight for the window columns, the
+// other the v weights in the parity-split order the lane groups read.
 #include <type_traits>
 
 #include "i0_coeffs.h"
@@ -23,25 +34,6 @@
 
 namespace wsb {
 namespace {
-
-#ifndef WSB_GRID_WARPS
-#define WSB_GRID_WARPS 4
-#endif
-#ifndef WSB_GRID_ROWS
-#define WSB_GRID_ROWS 128
-#endif
-#ifndef WSB_GRID_RUNROLL
-#define WSB_GRID_RUNROLL 1
-#endif
-#ifndef WSB_GRID_PREMUL
-#define WSB_GRID_PREMUL 1   // stage value * u weight per window column (vs value and weights)
-#endif
-#ifndef WSB_GRID_MINB
-#define WSB_GRID_MINB 0   // > 0: one occupancy target for every instantiation
-#endif
-constexpr int kWarpsPerCta = WSB_GRID_WARPS;  // independent warps per CTA
-constexpr int kRowBlock = WSB_GRID_ROWS;      // slab rows per work item
-constexpr int kRunUnroll = WSB_GRID_RUNROLL;  // records per iteration of the run loop
 
 __device__ __forceinline__ double chbevl(double x, const double *vals, int n) {
     // numpy _chbevl: b0 = x*b1 - b2 + vals[i] with separate roundings
@@ -163,276 +155,298 @@ __device__ __forceinline__ uint32_t axis_weights(double g, int i0, const KParams
     return mask;
 }
 
-// Calls f(std::integral_constant<int, phase>) for a runtime phase in [0, W).
-template <int I, int W, class F>
-__device__ __forceinline__ void dispatch_phase(int phase, F &f) {
-    if constexpr (I < W) {
+
+// Calls f(std::integral_constant<int, phase>) for a runtime phase in [0, N).
+template <int I, int N, class F>
+__device__ __forceinline__ void dispatch_phase(int phase, F &&f) {
+    if constexpr (I < N) {
         if (phase == I)
             f(std::integral_constant<int, I>{});
         else
-            dispatch_phase<I + 1, W>(phase, f);
+            dispatch_phase<I + 1, N>(phase, f);
     }
 }
+
+constexpr int kC = WSB_STRIP;          // columns per warp strip
+constexpr int kWarps = 4;              // strips (warps) per item
+constexpr int kSS = kC * kWarps;       // superstrip width (64)
+constexpr int kThreads = 32 * kWarps;
+constexpr int kChunk = 64;             // records staged per round (2 threads each)
+constexpr int kRaw = 3;                // gather ring: chunks in flight
 
 struct SweepArgs {
     const double4 *rec;
-    const uint32_t *idx;
-    const uint32_t *off;
-    void *out;                    // strip layout [n_w][ceil(n_u/32)][v_count][32]
-    int out_f32;                  // 1: complex64 grid (FP32 path; accumulation stays FP64)
+    const uint32_t *keys;      // sorted entries: item | rowrel << item_bits
+    const uint32_t *idx;       // record index per entry
+    const uint4 *parts;        // (item, first entry, end entry, slot | ~0 = direct)
+    void *out;                 // strip layout [n_w][n_u/16][v_count][16]
+    double2 *partial;          // [slot][kItemRows][kSS] partial tiles of split items
     unsigned long long *updates;
-    const double *i0beta;         // device scalar, np.i0(beta) (Kaiser-Bessel)
-    const uint4 *parts;           // (item, first entry, end entry, slot | ~0 = direct)
-    double2 *partial;             // [slot][kRowBlock][32] partial tiles of split items
-    int n_u, v_start, v_count, n_tc, rs, n_rb, n_groups;
-    int64_t n_items, n_parts;
+    const double *i0beta;      // device scalar, np.i0(beta) (Kaiser-Bessel)
+    int out_f32;               // 1: complex64 grid (FP32 path; accumulation stays FP64)
+    int n_u, v_start, v_count, n_ss, n_rb, item_bits, n_s16;
+    int64_t n_parts;
 };
 
-// Value * u-weight staging on/off per (kernel, half_support): measured on
-// cfg2 records (profiles/gridder_minb_r01.txt); above S = 5 the premultiplied
-// records exceed 48 KB of static shared memory per CTA.
 template <int KIND, int S>
-constexpr bool sweep_premul() {
-    constexpr bool gauss[8] = {false, false, true, true, false, true, false, false};
-    constexpr bool kb[8] = {false, true, true, true, false, true, false, false};
-    return WSB_GRID_PREMUL && (KIND == WSB_KERNEL_GAUSSIAN ? gauss[S] : kb[S]);
-}
-
-template <int KIND, int S>
-struct WarpStage {
+struct Shm {
     static constexpr int W = 2 * S + 1;
-    // one contiguous struct per staged record: the sweep addresses a record
-    // with a single base pointer (vs. separate wu/wv/val/ij arrays: -2% grid
-    // time at S=3, -20% at S=4 where the split arrays had bank conflicts)
-    static constexpr int WVS = (W + 1) & ~1;
-    // PRE: value * u weight staged per window column (the run loop loads one
-    // complex instead of the value and a weight, no multiplies)
-    static constexpr bool PRE = sweep_premul<KIND, S>();
-    struct RecPre {
-        double2 tu[W + 1];        // value * u weight per window column; slot W = 0 (off the footprint)
-        double wv[WVS];
-        int2 ij;                  // (first window column, first window row)
-    };
-    struct RecVal {
-        double2 val;
-        double wv[WVS];
-        double wu[W + 1];         // slot W is the zero weight for columns off the footprint
-        int2 ij;                  // (first window column, first window row)
-    };
-    using Rec = std::conditional_t<PRE, RecPre, RecVal>;
-    Rec rec[32];
-    double2 raw[2][32][2];        // records in flight (cp.async), one chunk ahead
+    static constexpr int T = S + 1;              // ring slots (row pairs) per lane
+    static constexpr int TP = (T + 1) & ~1;      // padded to 16 bytes
+    static constexpr int NSTEP = (kItemRows + 2 * S + 1) / 2;
+    double2 tu[kChunk][W + 1];      // value * u weight per window column; slot W = 0
+    double wv[kChunk][3][TP];       // v weights: [0] rows 2t-1, [1] rows 2t, [2] rows 2t+1
+    int4 meta[kChunk];              // (first window column - superstrip col0, step, d, strip mask)
+    double4 raw[kRaw][kChunk];      // gathered records (gu, gv, Re, Im)
+    uint32_t sorted[kPartCap];      // record indices of the part in (step, entry) order
+    uint32_t cnt[NSTEP + 1], run[NSTEP];
+    uint16_t wcnt[kWarps][NSTEP];
+    unsigned long long upd;
 };
-#define ST_TU(r, k) st.rec[r].tu[k]
-#define ST_WU(r, k) st.rec[r].wu[k]
-#define ST_WV(r, b) st.rec[r].wv[b]
-#define ST_VAL(r) st.rec[r].val
-#define ST_IJ(r) st.rec[r].ij
 
-// Resident CTAs per SM the sweep is compiled for (register budget), per
-// (kernel, half_support): measured on cfg2 records (profiles/gridder_minb_r01.txt);
-// the best point moves with each instantiation's register allocation.
 template <int KIND, int S>
 constexpr int sweep_min_blocks() {
-    if (WSB_GRID_MINB > 0) return WSB_GRID_MINB;
-    constexpr int gauss[8] = {4, 4, 5, 5, 4, 4, 3, 3};
-    constexpr int kb[8] = {4, 6, 2, 6, 5, 2, 2, 2};
-    return KIND == WSB_KERNEL_GAUSSIAN ? gauss[S] : kb[S];
+    return sizeof(Shm<KIND, S>) <= 24 * 1024 ? 8 : (sizeof(Shm<KIND, S>) <= 36 * 1024 ? 6 : 4);
 }
 
 template <int KIND, int S>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, sweep_min_blocks<KIND, S>()) k_grid_sweep(SweepArgs a, KParams<S> kp) {
+__global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
+    k_grid_items(SweepArgs a, KParams<S> kp) {
     constexpr int W = 2 * S + 1;
-    using St = WarpStage<KIND, S>;
-    __shared__ __align__(16) St stage_all[kWarpsPerCta];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    St &st = stage_all[warp];
-    const int64_t part = (int64_t)blockIdx.x * kWarpsPerCta + warp;
-    if (part >= a.n_parts) return;
-    // work part = (item, record sub-range, partial-tile slot or direct)
-    const uint4 pd = a.parts[part];
+    constexpr int T = S + 1;
+    using Sm = Shm<KIND, S>;
+    constexpr int NSTEP = Sm::NSTEP;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Sm &sm = *reinterpret_cast<Sm *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint4 pd = a.parts[blockIdx.x];
     const int64_t item = pd.x;
-    // item -> (plane, strip, row block); row block fastest
     const int rb = (int)(item % a.n_rb);
     const int64_t pt = item / a.n_rb;
-    const int tc = (int)(pt % a.n_tc);
-    const int plane = (int)(pt / a.n_tc);
-    const int col0 = tc * 32;
-    const int col = col0 + lane;
-    const bool col_ok = col < a.n_u;
-    const int ncols = min(32, a.n_u - col0);
-    const int R0 = a.v_start + rb * kRowBlock;
-    const int R1 = min(R0 + kRowBlock, a.v_start + a.v_count);
-    const uint32_t beg = pd.y, end = pd.z;
+    const int ss = (int)(pt % a.n_ss);
+    const int plane = (int)(pt / a.n_ss);
+    const int col0 = ss * kSS;
+    const int R0 = a.v_start + rb * kItemRows;
+    const int R1 = min(R0 + kItemRows, a.v_start + a.v_count);
+    const int Bfirst = R0 - 2 * S;      // window base of step 0
+    const uint32_t eb = pd.y, n = pd.z - pd.y;
     const bool direct = pd.w == 0xFFFFFFFFu;
+    const uint32_t imask = (1u << a.item_bits) - 1u;
+
+    // ---- phase A: stable counting sort of the part's entries by window step
+    for (int s = tid; s <= NSTEP; s += kThreads) sm.cnt[s] = 0;
+    for (int s = tid; s < NSTEP; s += kThreads) sm.run[s] = 0;
+    if (tid == 0) sm.upd = 0;
+    __syncthreads();
+    for (uint32_t e = tid; e < n; e += kThreads)
+        atomicAdd(&sm.cnt[(__ldg(&a.keys[eb + e]) >> a.item_bits) >> 1], 1u);
+    __syncthreads();
+    if (warp == 0) {   // exclusive scan of NSTEP counts, 32 at a time
+        uint32_t carry = 0;
+        for (int s0 = 0; s0 <= NSTEP; s0 += 32) {
+            const int s = s0 + lane;
+            const uint32_t x = s <= NSTEP ? sm.cnt[s] : 0u;
+            uint32_t incl = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (s <= NSTEP) sm.cnt[s] = carry + incl - x;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    __syncthreads();
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t r0 = 0; r0 < n; r0 += kThreads) {
+        const uint32_t e = r0 + tid;
+        const bool ok = e < n;
+        const uint32_t st = ok ? (__ldg(&a.keys[eb + e]) >> a.item_bits) >> 1 : 0xFFFFu;
+        const uint32_t id = ok ? __ldg(&a.idx[eb + e]) : 0u;
+        for (int s = tid; s < kWarps * NSTEP; s += kThreads) (&sm.wcnt[0][0])[s] = 0;
+        __syncthreads();
+        const uint32_t peers = __match_any_sync(0xffffffffu, st);
+        if (ok && lane == __ffs(peers) - 1) sm.wcnt[warp][st] = (uint16_t)__popc(peers);
+        __syncthreads();
+        if (ok) {
+            uint32_t pos = sm.cnt[st] + sm.run[st] + __popc(peers & lt);
+            for (int w = 0; w < warp; ++w) pos += sm.wcnt[w][st];
+            sm.sorted[pos] = id;
+        }
+        __syncthreads();
+        for (int s = tid; s < NSTEP; s += kThreads) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) t += sm.wcnt[w][s];
+            sm.run[s] += t;
+        }
+    }
+
+    // ---- phase B: the sweep -------------------------------------------------
+    const int q = lane >> 4, c = lane & 15;
+    const int wc = warp * kC + c;                  // lane column inside the superstrip
+    const int col = col0 + wc;
+    const bool col_ok = col < a.n_u;
     const double i0b = KIND == WSB_KERNEL_KAISER_BESSEL ? *a.i0beta : 0.0;
-    // strip layout [plane][strip][row][32]: an emitted row is one 512-byte run;
-    // a split item writes its unsigned partial tile [slot][row - R0][32]
-    const int64_t colbase = direct ? ((int64_t)plane * a.n_tc + tc) * a.v_count + (R0 - a.v_start)
-                                   : (int64_t)pd.w * kRowBlock;
-    double2 *const out = direct ? (double2 *)a.out : a.partial;
+    double2 *const outp = (double2 *)a.out;
     float2 *const out32 = (float2 *)a.out;
     const bool f32 = direct && a.out_f32;
-    if constexpr (St::PRE)
-        ST_TU(lane, W) = make_double2(0.0, 0.0);
-    else
-        ST_WU(lane, W) = 0.0;
+    const int64_t strip_base = ((int64_t)plane * a.n_s16 + col / kC) * a.v_count;
+    double2 *const ptile = direct ? nullptr : a.partial + (int64_t)pd.w * kItemRows * kSS;
 
-    // Window of W rows kept as a ring of W register slots: row `base` is in
-    // slot `phase`, row base+b in slot (phase+b) % W. Records with anchor
-    // row == base are applied with the slot mapping fixed at compile time
-    // (one code copy per phase, no register moves); when the next record
-    // starts lower, row `base` is final: it is written out, its slot
-    // zeroed, and the ring turns by one.
-    double2 acc[W];
+    double2 acc[T];
 #pragma unroll
-    for (int b = 0; b < W; ++b) acc[b] = make_double2(0.0, 0.0);
-    int base = R0 - 2 * S;
-    int phase = 0;
-    unsigned cnt = 0;           // cell updates of the records this lane staged
-    uint32_t cs = beg, ce = beg, r = beg;
+    for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
+    int step = 0, phase = 0;         // window base B = Bfirst + 2 * step, slot `phase` holds rows B, B+1
+    unsigned cnt_upd = 0;
 
-    auto emit_slot = [&](auto P) {
+    auto emit = [&](auto P) {
         constexpr int p = decltype(P)::value;
-        if (base >= R0 && base < R1 && col_ok) {
-            const double s = (direct && ((col + base) & 1)) ? -1.0 : 1.0;
-            const int64_t o = (colbase + (base - R0)) * 32 + lane;
-            if (f32)
-                out32[o] = make_float2((float)(acc[p].x * s), (float)(acc[p].y * s));
-            else
-                out[o] = make_double2(acc[p].x * s, acc[p].y * s);
+        const int row = Bfirst + 2 * step + q;
+        if (row >= R0 && row < R1 && col_ok) {
+            if (direct) {
+                const double sg = ((col + row) & 1) ? -1.0 : 1.0;
+                const int64_t o = (strip_base + (row - a.v_start)) * kC + c;
+                if (f32)
+                    out32[o] = make_float2((float)(acc[p].x * sg), (float)(acc[p].y * sg));
+                else
+                    outp[o] = make_double2(acc[p].x * sg, acc[p].y * sg);
+            } else {
+                ptile[(row - R0) * kSS + wc] = acc[p];
+            }
         }
         acc[p] = make_double2(0.0, 0.0);
-        ++base;
-        phase = (p + 1 == W) ? 0 : p + 1;
+        ++step;
+        phase = (p + 1 == T) ? 0 : p + 1;
     };
-    // lane l holds the anchor row of staged record cs+l (INT_MAX past the
-    // chunk end); records are sorted by anchor row, so the staged records
-    // with anchor row == base are the contiguous run starting at r
-    int my_jb = INT_MAX;
-    auto run = [&](auto P) {
+    auto apply = [&](auto P, int r) {
         constexpr int p = decltype(P)::value;
-        const int rr0 = (int)(r - cs);
-        const uint32_t m = __ballot_sync(0xffffffffu, my_jb == base) >> rr0;
-        const int n = __popc(m);
-#pragma unroll kRunUnroll
-        for (int rr = rr0; rr < rr0 + n; ++rr) {
-            int k = col - ST_IJ(rr).x;
-            k = (unsigned)k < (unsigned)W ? k : W;   // slot W holds weight 0
-            double tr, ti;
-            if constexpr (St::PRE) {
-                const double2 t = ST_TU(rr, k);
-                tr = t.x;
-                ti = t.y;
-            } else {
-                const double2 v = ST_VAL(rr);
-                const double wu = ST_WU(rr, k);
-                tr = __dmul_rn(v.x, wu);
-                ti = __dmul_rn(v.y, wu);
-            }
+        const int4 m = sm.meta[r];
+        int k = wc - m.x;
+        k = (unsigned)k < (unsigned)W ? k : W;
+        const double2 tv = sm.tu[r][k];
+        const double *wp = &sm.wv[r][q - m.z + 1][0];
 #pragma unroll
-            for (int b = 0; b < W; b += 2) {
-                const double2 wv2 = *reinterpret_cast<const double2 *>(&ST_WV(rr, b));
-                acc[(p + b) % W].x = fma(tr, wv2.x, acc[(p + b) % W].x);
-                acc[(p + b) % W].y = fma(ti, wv2.x, acc[(p + b) % W].y);
-                if (b + 1 < W) {
-                    acc[(p + b + 1) % W].x = fma(tr, wv2.y, acc[(p + b + 1) % W].x);
-                    acc[(p + b + 1) % W].y = fma(ti, wv2.y, acc[(p + b + 1) % W].y);
-                }
+        for (int t = 0; t < T; t += 2) {
+            const double2 w2 = *reinterpret_cast<const double2 *>(wp + t);
+            acc[(p + t) % T].x = fma(tv.x, w2.x, acc[(p + t) % T].x);
+            acc[(p + t) % T].y = fma(tv.y, w2.x, acc[(p + t) % T].y);
+            if (t + 1 < T) {
+                acc[(p + t + 1) % T].x = fma(tv.x, w2.y, acc[(p + t + 1) % T].x);
+                acc[(p + t + 1) % T].y = fma(tv.y, w2.y, acc[(p + t + 1) % T].y);
             }
         }
-        r += n;
-        if (r == ce) return true;   // chunk used up: stage the next one, same row
-        emit_slot(P);               // the next record starts lower: row base is final
-        return false;
     };
 
-    // the record a lane stages next is gathered one chunk ahead by cp.async
-    // into the warp's raw buffer (no registers held across the run, so the
-    // random 32-byte loads overlap the previous chunk's updates), and its
-    // bucket index one chunk before that
-    int buf = 0;
-    auto fetch = [&](uint32_t e, uint32_t id, int b) {
-        if (e < end) {
-            const double2 *src = reinterpret_cast<const double2 *>(a.rec + id);
-            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&st.raw[b][lane][0]);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16), "l"(src + 1)
-                         : "memory");
+    // gather: thread pair (2r, 2r+1) copies record r's two 16-byte halves
+    const int nchunks = (int)((n + kChunk - 1) / kChunk);
+    auto fetch = [&](int ch) {
+        if (ch < nchunks) {
+            const uint32_t r = ch * kChunk + (tid >> 1);
+            if (r < n) {
+                const double2 *src = reinterpret_cast<const double2 *>(a.rec + sm.sorted[r]) + (tid & 1);
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(
+                    reinterpret_cast<double2 *>(&sm.raw[ch % kRaw][tid >> 1]) + (tid & 1));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    auto index_at = [&](uint32_t e) { return e < end ? __ldg(&a.idx[e]) : 0u; };
-    fetch(beg + lane, index_at(beg + lane), 0);
-    uint32_t nid = index_at(beg + 32 + lane);
+    __syncthreads();   // sorted[] complete
+#pragma unroll
+    for (int ch = 0; ch < kRaw - 1; ++ch) fetch(ch);
 
-    while (true) {
-        if (r == ce) {
-            if (ce >= end) break;
-            // ---- stage the next 32 records: one per lane -------------------
-            __syncwarp();
-            cs = ce;
-            ce = min(cs + 32u, end);
-            const uint32_t e = cs + lane;
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-            const double2 lo = st.raw[buf][lane][0], hi = st.raw[buf][lane][1];
-            my_jb = INT_MAX;
-            fetch(e + 32, nid, buf ^ 1);
-            nid = index_at(e + 64);
-            buf ^= 1;
-            if (e < ce) {
-                const double gu = lo.x, gv = lo.y;
-                const int ib = (int)floor(gu) - S, jb = (int)floor(gv) - S;
-                double w[W];
-                const uint32_t um = axis_weights<KIND, S>(gu, ib, kp, i0b, w);
-                if constexpr (St::PRE) {
-                    // the run loop's value * u-weight products, formed once per record
+    for (int ch = 0; ch < nchunks; ++ch) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kRaw - 2) : "memory");
+        __syncthreads();   // raw[ch] landed for every thread; the previous sweep is done
+        fetch(ch + kRaw - 1);
+        const int nr = (int)min((uint32_t)kChunk, n - (uint32_t)ch * kChunk);
+        // ---- stage: thread pair per record -------------------------------
+        {
+            const int r = tid >> 1;
+            unsigned mine = 0;      // u-tap (even thread) / v-tap (odd thread) count in the item
+            if (r < nr) {
+                const double4 rc = sm.raw[ch % kRaw][r];
+                double wgt[W];
+                if ((tid & 1) == 0) {            // u axis: value * weight per window column
+                    const int ib = (int)floor(rc.x) - S;
+                    const uint32_t um = axis_weights<KIND, S>(rc.x, ib, kp, i0b, wgt);
 #pragma unroll
                     for (int k = 0; k < W; ++k)
-                        ST_TU(lane, k) = make_double2(__dmul_rn(hi.x, w[k]), __dmul_rn(hi.y, w[k]));
-                } else {
+                        sm.tu[r][k] = make_double2(__dmul_rn(rc.z, wgt[k]), __dmul_rn(rc.w, wgt[k]));
+                    sm.tu[r][W] = make_double2(0.0, 0.0);
+                    // tap columns inside the superstrip and the mesh, and the
+                    // warps (16-column strips) they fall into
+                    const int c_lo = max(col0, 0) - ib, c_hi = min(col0 + kSS, a.n_u) - 1 - ib;
+                    uint32_t in = um;
 #pragma unroll
-                    for (int k = 0; k < W; ++k) ST_WU(lane, k) = w[k];
-                    ST_VAL(lane) = hi;
+                    for (int k = 0; k < W; ++k)
+                        if (k < c_lo || k > c_hi) in &= ~(1u << k);
+                    int mask = 0;
+                    if (in) {
+                        const int k_lo = __ffs(in) - 1, k_hi = 31 - __clz(in);
+                        const int w_lo = (ib + k_lo - col0) / kC, w_hi = (ib + k_hi - col0) / kC;
+                        mask = ((2 << w_hi) - 1) & ~((1 << w_lo) - 1);
+                    }
+                    mine = __popc(in);
+                    sm.meta[r].x = ib - col0;
+                    sm.meta[r].w = mask;
+                } else {                          // v axis: parity-split row weights
+                    const int jb = (int)floor(rc.y) - S;
+                    const uint32_t vm = axis_weights<KIND, S>(rc.y, jb, kp, i0b, wgt);
+                    const int rel = jb - Bfirst;
+#pragma unroll
+                    for (int t = 0; t < Sm::TP; ++t) {
+                        sm.wv[r][0][t] = (2 * t - 1 >= 0 && 2 * t - 1 < W) ? wgt[max(2 * t - 1, 0)] : 0.0;
+                        sm.wv[r][1][t] = (2 * t < W) ? wgt[min(2 * t, W - 1)] : 0.0;
+                        sm.wv[r][2][t] = (2 * t + 1 < W) ? wgt[min(2 * t + 1, W - 1)] : 0.0;
+                    }
+                    sm.meta[r].y = rel >> 1;
+                    sm.meta[r].z = rel & 1;
+                    uint32_t in = vm;
+#pragma unroll
+                    for (int k = 0; k < W; ++k)
+                        if (jb + k < R0 || jb + k >= R1) in &= ~(1u << k);
+                    mine = __popc(in);
                 }
-                const uint32_t vm = axis_weights<KIND, S>(gv, jb, kp, i0b, w);
-#pragma unroll
-                for (int k = 0; k < W; ++k) ST_WV(lane, k) = w[k];
-                ST_IJ(lane) = make_int2(ib, jb);
-                my_jb = jb;
-                // cell updates inside this strip and row block (grid_sector's count)
-                const int c_lo = max(col0 - ib, 0), c_hi = min(col0 + ncols - ib, W);
-                const int r_lo = max(R0 - jb, 0), r_hi = min(R1 - jb, W);
-                const uint32_t cm = c_hi > c_lo ? ((1u << (c_hi - c_lo)) - 1u) << c_lo : 0u;
-                const uint32_t rm = r_hi > r_lo ? ((1u << (r_hi - r_lo)) - 1u) << r_lo : 0u;
-                cnt += __popc(um & cm) * __popc(vm & rm);
             }
-            __syncwarp();
+            const unsigned other = __shfl_xor_sync(0xffffffffu, mine, 1);
+            if ((tid & 1) == 0) cnt_upd += mine * other;
         }
-        // consecutive rows walk the ring statically: one jump-table dispatch
-        // per W rows (and per staged chunk) instead of one per row
-        for (;;) {
-            switch (phase) {
-#define WSB_STEP(q)                                                   \
-    case q:                                                           \
-        if constexpr (q < W) {                                        \
-            if (run(std::integral_constant<int, q>{})) goto next_chunk; \
-        }                                                             \
-        [[fallthrough]];
-                WSB_STEP(0) WSB_STEP(1) WSB_STEP(2) WSB_STEP(3) WSB_STEP(4)
-                WSB_STEP(5) WSB_STEP(6) WSB_STEP(7) WSB_STEP(8) WSB_STEP(9)
-                WSB_STEP(10) WSB_STEP(11) WSB_STEP(12) WSB_STEP(13) WSB_STEP(14)
-#undef WSB_STEP
-                default: break;
+        __syncthreads();   // stage complete
+        // ---- sweep: this warp's strip -----------------------------------
+#pragma unroll 1
+        for (int g = 0; g < kChunk / 32; ++g) {
+            const int r = g * 32 + lane;
+            const bool ok = r < nr;
+            const int4 mm = ok ? sm.meta[r] : make_int4(0, 0x7fffffff, 0, 0);
+            const bool touch = ok && ((mm.w >> warp) & 1);
+            uint32_t rem = __ballot_sync(0xffffffffu, ok);
+            const uint32_t tm = __ballot_sync(0xffffffffu, touch);
+            while (rem) {
+                const int s = __shfl_sync(0xffffffffu, mm.y, __ffs(rem) - 1);
+                while (step < s) dispatch_phase<0, T>(phase, emit);
+                const uint32_t runm = __ballot_sync(0xffffffffu, ok && mm.y == s) & rem;
+                rem &= ~runm;
+                uint32_t app = runm & tm;
+                dispatch_phase<0, T>(phase, [&](auto P) {
+                    while (app) {
+                        const int b = __ffs(app) - 1;
+                        app &= app - 1;
+                        apply(P, g * 32 + b);
+                    }
+                });
             }
         }
-    next_chunk:;
     }
-    while (base < R1) dispatch_phase<0, W>(phase, emit_slot);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    // flush the rest of the block
+    while (Bfirst + 2 * step < R1) dispatch_phase<0, T>(phase, emit);
 
+    // cell updates inside this item (grid_sector's count)
 #pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0 && cnt) atomicAdd(a.updates, (unsigned long long)cnt);
+    for (int o = 16; o; o >>= 1) cnt_upd += __shfl_xor_sync(0xffffffffu, cnt_upd, o);
+    if (lane == 0 && cnt_upd) atomicAdd(a.updates, (unsigned long long)cnt_upd);
 }
 
 __global__ void k_i0(double beta, double *out) { *out = bessel_i0(beta); }
@@ -478,8 +492,10 @@ int launch_s(wsb_ctx *ctx, const SweepArgs &a, double p0) {
             kp.cm[k] = std::exp(-(m * m) / p0);
         }
     }
-    const int64_t blocks = (a.n_parts + kWarpsPerCta - 1) / kWarpsPerCta;
-    k_grid_sweep<KIND, S><<<(unsigned)blocks, 32 * kWarpsPerCta, 0, ctx->stream>>>(a, kp);
+    const size_t smem = sizeof(Shm<KIND, S>);
+    auto kern = k_grid_items<KIND, S>;
+    WSB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)a.n_parts, kThreads, smem, ctx->stream>>>(a, kp);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
@@ -500,45 +516,30 @@ int launch_kind(wsb_ctx *ctx, int S, const SweepArgs &a, double p0) {
 }
 
 // ---------------------------------------------------------------------------
-// Load balancing. Earth-rotation tracks pile millions of records into a few
-// (plane, strip, row block) items. An item with more than kPartRecords
-// records is split into equal consecutive sub-ranges of its (sorted) list;
-// each part sweeps the item into its own partial tile, and k_combine adds
-// the parts in part order (fixed association: deterministic, and the same
-// split for any GPU count since items never straddle slabs).
+// Work parts. An item holding more than kPartCap entries (Earth-rotation
+// tracks pile millions of records into a few central items) is split into
+// equal consecutive ranges of its entry list (record order); each part
+// sweeps the item into its own partial tile, and k_combine adds the tiles in
+// part order: a fixed association, the same for any GPU count when slabs
+// start on item boundaries (the item then holds the same entries).
 // ---------------------------------------------------------------------------
-constexpr uint32_t kPartRecords = 4096;
-
-__device__ __forceinline__ void item_range(const SweepArgs &a, int S, int64_t item, uint32_t *b,
-                                           uint32_t *e) {
-    const int rb = (int)(item % a.n_rb);
-    const int64_t pt = item / a.n_rb;
-    const int tc = (int)(pt % a.n_tc), plane = (int)(pt / a.n_tc);
-    const int R0 = a.v_start + rb * kRowBlock;
-    const int R1 = min(R0 + kRowBlock, a.v_start + a.v_count);
-    const uint32_t kbase = ((uint32_t)plane * a.n_tc + tc) * (uint32_t)a.rs;
-    *b = a.off[kbase + (R0 - a.v_start)];
-    *e = a.off[kbase + (R1 - 1 - a.v_start + 2 * S) + 1];
-}
-
-__global__ void k_item_parts(SweepArgs a, int S, uint32_t *nparts, uint32_t *nslots,
-                             uint32_t *split) {
+__global__ void k_item_parts(const uint32_t *off, int64_t n_items, uint32_t *nparts,
+                             uint32_t *nslots, uint32_t *split) {
     const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (item >= a.n_items) return;
-    uint32_t b, e;
-    item_range(a, S, item, &b, &e);
-    const uint32_t np = e - b > kPartRecords ? (e - b + kPartRecords - 1) / kPartRecords : 1;
+    if (item >= n_items) return;
+    const uint32_t cnt = off[item + 1] - off[item];
+    const uint32_t np = cnt > kPartCap ? (cnt + kPartCap - 1) / kPartCap : 1;
     nparts[item] = np;
     nslots[item] = np > 1 ? np : 0;
     split[item] = np > 1 ? 1 : 0;
 }
 
-__global__ void k_build_parts(SweepArgs a, int S, const uint32_t *part_off, const uint32_t *slot_off,
-                              const uint32_t *split_off, uint4 *parts, uint2 *split_items) {
+__global__ void k_build_parts(const uint32_t *off, int64_t n_items, const uint32_t *part_off,
+                              const uint32_t *slot_off, const uint32_t *split_off, uint4 *parts,
+                              uint2 *split_items) {
     const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (item >= a.n_items) return;
-    uint32_t b, e;
-    item_range(a, S, item, &b, &e);
+    if (item >= n_items) return;
+    const uint32_t b = off[item], e = off[item + 1];
     const uint32_t np = part_off[item + 1] - part_off[item];
     if (np == 1) {
         parts[part_off[item]] = make_uint4((uint32_t)item, b, e, 0xFFFFFFFFu);
@@ -552,7 +553,8 @@ __global__ void k_build_parts(SweepArgs a, int S, const uint32_t *part_off, cons
     split_items[split_off[item]] = make_uint2((uint32_t)item, slot_off[item]);
 }
 
-// one warp per row of a split item: sum its parts' partial rows in part order
+// one warp per (row, half superstrip) of a split item: its parts' partial
+// tiles summed in part order, sign applied, written to the strip layout
 __global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split_items,
                                                   const uint32_t *part_off) {
     const uint2 si = split_items[blockIdx.x];
@@ -560,24 +562,26 @@ __global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split
     const int np = (int)(part_off[item + 1] - part_off[item]);
     const int rb = (int)(item % a.n_rb);
     const int64_t pt = item / a.n_rb;
-    const int tc = (int)(pt % a.n_tc), plane = (int)(pt / a.n_tc);
-    const int R0 = a.v_start + rb * kRowBlock;
-    const int R1 = min(R0 + kRowBlock, a.v_start + a.v_count);
+    const int ss = (int)(pt % a.n_ss), plane = (int)(pt / a.n_ss);
+    const int R0 = a.v_start + rb * kItemRows;
+    const int R1 = min(R0 + kItemRows, a.v_start + a.v_count);
     const int lane = threadIdx.x & 31;
-    const int col = tc * 32 + lane;
-    for (int r = blockIdx.y * 4 + (threadIdx.x >> 5); r < kRowBlock; r += gridDim.y * 4) {
+    const int wcol = (threadIdx.x >> 5) & 1;          // half superstrip
+    for (int r = blockIdx.y * 2 + (threadIdx.x >> 6); r < kItemRows; r += gridDim.y * 2) {
         const int row = R0 + r;
         if (row >= R1) break;
+        const int wc = wcol * 32 + lane;
+        const int col = ss * kSS + wc;
         double2 acc = make_double2(0.0, 0.0);
-        const double2 *src = a.partial + ((int64_t)si.y * kRowBlock + r) * 32 + lane;
+        const double2 *src = a.partial + ((int64_t)si.y * kItemRows + r) * kSS + wc;
         for (int p = 0; p < np; ++p) {
-            const double2 z = src[(int64_t)p * kRowBlock * 32];
+            const double2 z = src[(int64_t)p * kItemRows * kSS];
             acc.x += z.x;
             acc.y += z.y;
         }
         if (col < a.n_u) {
             const double s = ((col + row) & 1) ? -1.0 : 1.0;
-            const int64_t o = (((int64_t)plane * a.n_tc + tc) * a.v_count + (row - a.v_start)) * 32 + lane;
+            const int64_t o = (((int64_t)plane * a.n_s16 + col / kC) * a.v_count + (row - a.v_start)) * kC + col % kC;
             if (a.out_f32)
                 ((float2 *)a.out)[o] = make_float2((float)(acc.x * s), (float)(acc.y * s));
             else
@@ -588,29 +592,28 @@ __global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split
 
 }  // namespace
 
-int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start, int v_count,
-               const double *rec, const RowBuckets &bk, void *grid_p,
+int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start, int v_count,
+               const double *rec, const ItemBuckets &bk, void *grid_s,
                unsigned long long *updates_dev, int prec) {
     SweepArgs a;
     a.rec = (const double4 *)rec;
+    a.keys = bk.keys;
     a.idx = bk.idx;
-    a.off = bk.off;
-    a.out = grid_p;
+    a.out = grid_s;
     a.out_f32 = prec == 32 ? 1 : 0;
     a.updates = updates_dev;
     a.i0beta = nullptr;
     a.n_u = g->n_u;
     a.v_start = v_start;
     a.v_count = v_count;
-    a.n_tc = bk.n_tc;
-    a.rs = bk.rs;
-    a.n_rb = ceil_div(v_count, kRowBlock);
-    a.n_groups = g->n_u / kG;
-    a.n_items = (int64_t)g->n_w * a.n_tc * a.n_rb;
-    if (a.n_items <= 0) return WSB_OK;
+    a.n_ss = bk.n_ss;
+    a.n_rb = bk.n_rb;
+    a.item_bits = bk.item_bits;
+    a.n_s16 = ceil_div(g->n_u, kC);
+    const int64_t ni = bk.n_items;
+    if (ni <= 0) return WSB_OK;
     const int S = k->half_support;
     // ---- work parts (split heavy items) ------------------------------------
-    const int64_t ni = a.n_items;
     uint32_t *np, *ns, *sp, *np_off, *ns_off, *sp_off;
     WSB_TRY(ensure(ctx, kSlotPartCnt, sizeof(uint32_t) * 3 * (ni + 1), (void **)&np));
     WSB_TRY(ensure(ctx, kSlotPartOff, sizeof(uint32_t) * 3 * (ni + 1), (void **)&np_off));
@@ -619,7 +622,7 @@ int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
     ns_off = np_off + (ni + 1);
     sp_off = ns_off + (ni + 1);
     WSB_CUDA_TRY(cudaMemsetAsync(np, 0, sizeof(uint32_t) * 3 * (ni + 1), ctx->stream));
-    k_item_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(a, S, np, ns, sp);
+    k_item_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(bk.off, ni, np, ns, sp);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     uint32_t n_parts = 0, n_slots = 0, n_split = 0;
@@ -633,10 +636,10 @@ int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
                    (void **)&parts));
     split_items = reinterpret_cast<uint2 *>(parts + n_parts);
     if (n_slots)
-        WSB_TRY(ensure(ctx, kSlotPartial, sizeof(double2) * (size_t)n_slots * kRowBlock * 32,
+        WSB_TRY(ensure(ctx, kSlotPartial, sizeof(double2) * (size_t)n_slots * kItemRows * kSS,
                        (void **)&partial));
-    k_build_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(a, S, np_off, ns_off, sp_off, parts,
-                                                              split_items);
+    k_build_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(bk.off, ni, np_off, ns_off, sp_off,
+                                                              parts, split_items);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     a.parts = parts;
@@ -655,10 +658,11 @@ int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
         rc = launch_kind<WSB_KERNEL_KAISER_BESSEL>(ctx, S, a, k->shape_param);
     }
     if (rc != WSB_OK || n_split == 0) return rc;
-    k_combine<<<dim3(n_split, kRowBlock / 4 / 4), 128, 0, ctx->stream>>>(a, split_items, np_off);
+    k_combine<<<dim3(n_split, kItemRows / 2 / 8), 128, 0, ctx->stream>>>(a, split_items, np_off);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
 }
 
 }  // namespace wsb
+

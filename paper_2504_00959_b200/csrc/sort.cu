@@ -293,7 +293,7 @@ int exclusive_scan_u32(wsb_ctx *ctx, const uint32_t *in, uint32_t *out, int64_t 
 
 int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
                      uint32_t *vals_alt, int64_t n, int bits, uint32_t **keys_out,
-                     uint32_t **vals_out) {
+                     uint32_t **vals_out, bool keep_keys) {
     *keys_out = keys;
     *vals_out = vals;
     if (n <= 1 || bits <= 0) return WSB_OK;
@@ -308,7 +308,7 @@ int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t 
                    (void **)&hist));
     uint32_t *ka = keys, *kb = keys_alt, *va = vals, *vb = vals_alt;
     for (int shift = 0; shift < bits; shift += B) {
-        const bool last = shift + B >= bits;
+        const bool last = !keep_keys && shift + B >= bits;
         switch (B) {
             case 8: WSB_TRY(radix_pass<8>(ctx, ka, va, kb, vb, n, shift, hist, nb, last)); break;
             case 9: WSB_TRY(radix_pass<9>(ctx, ka, va, kb, vb, n, shift, hist, nb, last)); break;

@@ -122,7 +122,7 @@ int exclusive_scan_u32(wsb_ctx *ctx, const uint32_t *in, uint32_t *out, int64_t 
 // pass writes the values only (*keys_out then holds a previous pass's keys).
 int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
                      uint32_t *vals_alt, int64_t n, int bits, uint32_t **keys_out,
-                     uint32_t **vals_out);
+                     uint32_t **vals_out, bool keep_keys = true);
 
 // prepare.cu
 int prepare(wsb_ctx *ctx, const wsb_grid *g, const double *u, const double *v,
@@ -140,19 +140,37 @@ int row_histogram(wsb_ctx *ctx, const wsb_grid *g, const double *rec, int64_t n,
 int plane_histogram(wsb_ctx *ctx, const wsb_grid *g, const uint32_t *plane, int64_t n,
                     uint32_t *hist);
 
-// bucket.cu: records of a slab bucketed by (plane, 32-column strip, anchor row)
-struct RowBuckets {
-    uint32_t *idx = nullptr;   // record indices, bucket-major, ascending inside a bucket
-    uint32_t *off = nullptr;   // [n_keys + 1] exclusive offsets
-    int64_t n_entries = 0, n_keys = 0;
-    int n_tc = 0, rs = 0;      // strips, anchor rows per strip (v_count + 2S)
+// Gridder work items (bucket.cu, grid.cu): (w plane, kSSCols-column
+// superstrip, kItemRows-row block of the slab); one CTA of 4 warps per item,
+// warp = one WSB_STRIP-column strip.
+constexpr int kItemRows = 128;
+constexpr int kSSCols = 4 * WSB_STRIP;
+constexpr int kPartCap = 2048;     // entries per work part (the CTA's shared-memory sort)
+
+// the visibility columns of one channel (fused prepare + bucketing)
+struct VisColumns {
+    const double *u, *v, *w;
+    const float *vis, *weight;
+    const uint32_t *time_index;   // nullable
 };
-int bucket_rows(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_count,
-                const double *rec, const uint32_t *plane, int64_t m, RowBuckets *out);
+
+struct ItemBuckets {
+    uint32_t *keys = nullptr;  // item | rowrel << item_bits, item-major, record order inside an item
+    uint32_t *idx = nullptr;   // record index per entry
+    uint32_t *off = nullptr;   // [n_items + 1] exclusive offsets
+    int64_t n_entries = 0, n_items = 0;
+    int n_ss = 0, n_rb = 0, item_bits = 0;
+};
+// in != nullptr: records are prepared from the columns on the fly (rec
+// written, plane written if non-null; one channel); else rec/plane are read.
+// Synchronises once (entry count, validation flags).
+int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_count,
+                 const VisColumns *in, double *rec, uint32_t *plane, int64_t m,
+                 ItemBuckets *out);
 
 // grid.cu
-int grid_sweep(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start, int v_count,
-               const double *rec, const RowBuckets &bk, void *grid_p,
+int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start, int v_count,
+               const double *rec, const ItemBuckets &bk, void *grid_s,
                unsigned long long *updates_dev, int prec = 64);
 
 // peer.cu: copy n_dest contiguous blocks src[d] -> dst[d] (bytes[d] each; dst

@@ -10,6 +10,7 @@ import numpy as np
 import torch
 
 from oracle import wstack_oracle as O
+from paper_2504_00959_b200 import _lib as L
 
 G = 1
 
@@ -47,19 +48,21 @@ class NumpyBackend:
         kind = O.KIND_GAUSSIAN if kern.kind == "gaussian" else O.KIND_KAISER_BESSEL
         grid, upd = O.grid_slab(batch, spec.n_u, spec.n_w, kind, kern.half_support, kern.shape_param)
         grid = grid * O.checker_sign(spec.n_u, v0, vc)[None]
-        # (plane, row, col) -> strip layout (plane, col/32, row, col%32)
-        ns = (spec.n_u + 31) // 32
-        pad = np.zeros((spec.n_w, vc, ns * 32), np.complex128)
+        # (plane, row, col) -> strip layout (plane, col/SW, row, col%SW)
+        sw = L.STRIP
+        ns = (spec.n_u + sw - 1) // sw
+        pad = np.zeros((spec.n_w, vc, ns * sw), np.complex128)
         pad[:, :, : spec.n_u] = grid
-        s = np.ascontiguousarray(pad.reshape(spec.n_w, vc, ns, 32).transpose(0, 2, 1, 3))
-        return torch.from_numpy(s.view(np.float64).reshape(spec.n_w, ns, vc, 32, 2)), upd
+        s = np.ascontiguousarray(pad.reshape(spec.n_w, vc, ns, sw).transpose(0, 2, 1, 3))
+        return torch.from_numpy(s.view(np.float64).reshape(spec.n_w, ns, vc, sw, 2)), upd
 
     def fft_rows(self, grid_s, spec, vc, dest_pairs, plane_lo=0, plane_hi=None):
         plane_hi = spec.n_w if plane_hi is None else plane_hi
         nk = plane_hi - plane_lo
-        ns = (spec.n_u + 31) // 32
-        a = grid_s.numpy().view(np.complex128).reshape(spec.n_w, ns, vc, 32)[plane_lo:plane_hi]
-        nat = a.transpose(0, 2, 1, 3).reshape(nk, vc, ns * 32)[:, :, : spec.n_u]
+        sw = L.STRIP
+        ns = (spec.n_u + sw - 1) // sw
+        a = grid_s.numpy().view(np.complex128).reshape(spec.n_w, ns, vc, sw)[plane_lo:plane_hi]
+        nat = a.transpose(0, 2, 1, 3).reshape(nk, vc, ns * sw)[:, :, : spec.n_u]
         f = np.fft.ifft(nat, axis=-1) * spec.n_u               # unnormalised inverse
         # -> P layout (plane, col/G, row, col%G), then destination major
         p = f.reshape(nk, vc, spec.n_u // G, G).transpose(0, 2, 1, 3)
