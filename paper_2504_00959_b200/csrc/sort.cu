@@ -116,7 +116,7 @@ struct RsSmem {
 
 template <int B>
 __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const uint32_t *__restrict__ keys,
-                                                           int64_t n, int shift,
+                                                           int64_t n, int shift, uint32_t dmask,
                                                            uint32_t *hist, int nb) {
     // one sub-histogram per warp (shared-memory atomics, little contention),
     // all loads of a thread issued up front
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const uint32_t *__res
 #pragma unroll
     for (int r = 0; r < kRsIpt; ++r) {
         const int64_t i = base + (int64_t)r * kRsThreads + threadIdx.x;
-        d[r] = i < n ? (__ldg(&keys[i]) >> shift) & (D - 1) : (uint32_t)D;
+        d[r] = i < n ? (__ldg(&keys[i]) >> shift) & dmask : (uint32_t)D;
     }
 #pragma unroll
     for (int r = 0; r < kRsIpt; ++r)
@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const uint32_t *__res
 template <int B, bool LAST>
 __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
-    uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ offs, int nb) {
+    uint32_t *__restrict__ vout, int64_t n, int shift, uint32_t dmask,
+    const uint32_t *__restrict__ offs, int nb) {
     constexpr int D = 1 << B;
     constexpr int DPT = D / kRsThreads;  // digits per thread in the block scan (1..8)
     extern __shared__ __align__(16) unsigned char raw[];
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
 #pragma unroll
     for (int r = 0; r < kRsIpt; ++r) {
         const bool ok = base + r * 32 + lane < n;
-        const uint32_t d = ok ? (k[r] >> shift) & (D - 1) : (uint32_t)D;
+        const uint32_t d = ok ? (k[r] >> shift) & dmask : (uint32_t)D;
         pm[r] = __match_any_sync(0xffffffffu, d);
         if (d < (uint32_t)D && lane == __ffs(pm[r]) - 1) sm.wc[warp][d] += __popc(pm[r]);
         __syncwarp();
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
     for (int r = 0; r < kRsIpt; ++r) {
         int64_t i = base + r * 32 + lane;
         bool ok = i < n;
-        uint32_t d = ok ? (k[r] >> shift) & (D - 1) : (uint32_t)D;
+        uint32_t d = ok ? (k[r] >> shift) & dmask : (uint32_t)D;
         const uint32_t peers = pm[r];
         uint32_t pos = 0;
         if (ok) pos = sm.bstart[d] + sm.wc[warp][d] + __popc(peers & lt);
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
     }
     for (int p = threadIdx.x; p < nblk; p += kRsThreads) {
         const uint32_t key = sm.ks[p];
-        const uint32_t d = (key >> shift) & (D - 1);
+        const uint32_t d = (key >> shift) & dmask;
         const uint32_t gpos = sm.goff[d] + (p - sm.bstart[d]);
         kout[gpos] = key;
         vout[gpos] = sm.vs[p];
@@ -250,17 +251,20 @@ __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
 
 template <int B>
 int radix_pass(wsb_ctx *ctx, const uint32_t *ka, const uint32_t *va, uint32_t *kb, uint32_t *vb,
-               int64_t n, int shift, uint32_t *hist, int nb, bool last) {
+               int64_t n, int shift, int bits, uint32_t *hist, int nb, bool last) {
     constexpr int D = 1 << B;
+    // the digit covers key bits [shift, min(shift + B, bits)): key bits above
+    // `bits` (the payload the caller keeps in the key) are not sorted on
+    const uint32_t dmask = (bits - shift >= B) ? (uint32_t)(D - 1) : ((1u << (bits - shift)) - 1u);
     const size_t hsm = sizeof(uint32_t) * kRsWarps * D, ssm = sizeof(RsSmem<B>);
     auto scatter = last ? k_radix_scatter<B, true> : k_radix_scatter<B, false>;
     WSB_CUDA_TRY(cudaFuncSetAttribute(k_radix_hist<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)hsm));
     WSB_CUDA_TRY(cudaFuncSetAttribute(scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
-    k_radix_hist<B><<<nb, kRsThreads, hsm, ctx->stream>>>(ka, n, shift, hist, nb);
+    k_radix_hist<B><<<nb, kRsThreads, hsm, ctx->stream>>>(ka, n, shift, dmask, hist, nb);
     ctx->launches += 1;
     WSB_TRY(exclusive_scan_u32(ctx, hist, hist, (int64_t)D * nb, nullptr));
-    scatter<<<nb, kRsThreads, ssm, ctx->stream>>>(ka, va, kb, vb, n, shift, hist, nb);
+    scatter<<<nb, kRsThreads, ssm, ctx->stream>>>(ka, va, kb, vb, n, shift, dmask, hist, nb);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
@@ -310,10 +314,10 @@ int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t 
     for (int shift = 0; shift < bits; shift += B) {
         const bool last = !keep_keys && shift + B >= bits;
         switch (B) {
-            case 8: WSB_TRY(radix_pass<8>(ctx, ka, va, kb, vb, n, shift, hist, nb, last)); break;
-            case 9: WSB_TRY(radix_pass<9>(ctx, ka, va, kb, vb, n, shift, hist, nb, last)); break;
-            case 10: WSB_TRY(radix_pass<10>(ctx, ka, va, kb, vb, n, shift, hist, nb, last)); break;
-            case 11: WSB_TRY(radix_pass<11>(ctx, ka, va, kb, vb, n, shift, hist, nb, last)); break;
+            case 8: WSB_TRY(radix_pass<8>(ctx, ka, va, kb, vb, n, shift, bits, hist, nb, last)); break;
+            case 9: WSB_TRY(radix_pass<9>(ctx, ka, va, kb, vb, n, shift, bits, hist, nb, last)); break;
+            case 10: WSB_TRY(radix_pass<10>(ctx, ka, va, kb, vb, n, shift, bits, hist, nb, last)); break;
+            case 11: WSB_TRY(radix_pass<11>(ctx, ka, va, kb, vb, n, shift, bits, hist, nb, last)); break;
             default: return fail(WSB_EUNSUPPORTED, "radix digit width");
         }
         uint32_t *t = ka; ka = kb; kb = t;
