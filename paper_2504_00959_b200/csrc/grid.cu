@@ -193,14 +193,14 @@ struct Shm {
     static constexpr int W = 2 * S + 1;
     static constexpr int T = S + 1;              // ring slots (row pairs) per lane
     static constexpr int TP = (T + 1) & ~1;      // padded to 16 bytes
-    static constexpr int NSTEP = (kItemRows + 2 * S + 1) / 2;
+    static constexpr int NROW = kItemRows + 2 * S;   // anchor rows that reach the item
     double2 tu[kChunk][W + 1];      // value * u weight per window column; slot W = 0
     double wv[kChunk][3][TP];       // v weights: [0] rows 2t-1, [1] rows 2t, [2] rows 2t+1
     int4 meta[kChunk];              // (first window column - superstrip col0, step, d, strip mask)
     double4 raw[kRaw][kChunk];      // gathered records (gu, gv, Re, Im)
-    uint32_t sorted[kPartCap];      // record indices of the part in (step, entry) order
-    uint32_t cnt[NSTEP + 1], run[NSTEP];
-    uint16_t wcnt[kWarps][NSTEP];
+    uint32_t sorted[kPartCap];      // record indices of the part in (anchor row, entry) order
+    uint32_t cnt[NROW + 1], run[NROW];
+    uint16_t wcnt[kWarps][NROW];
     unsigned long long upd;
 };
 
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     constexpr int W = 2 * S + 1;
     constexpr int T = S + 1;
     using Sm = Shm<KIND, S>;
-    constexpr int NSTEP = Sm::NSTEP;
+    constexpr int NSTEP = Sm::NROW;   // sort bins: anchor rows (a window step holds two)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Sm &sm = *reinterpret_cast<Sm *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -231,15 +231,18 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     const int Bfirst = R0 - 2 * S;      // window base of step 0
     const uint32_t eb = pd.y, n = pd.z - pd.y;
     const bool direct = pd.w == 0xFFFFFFFFu;
-    const uint32_t imask = (1u << a.item_bits) - 1u;
 
-    // ---- phase A: stable counting sort of the part's entries by window step
+    // ---- phase A: stable counting sort of the part's entries by anchor row.
+    // Sorting by the row (not just the two-row window step) makes every
+    // cell's accumulation order (anchor row, record) whatever the slab
+    // boundaries' parity -- the v-slab result is then bit-identical for any
+    // slab split.
     for (int s = tid; s <= NSTEP; s += kThreads) sm.cnt[s] = 0;
     for (int s = tid; s < NSTEP; s += kThreads) sm.run[s] = 0;
     if (tid == 0) sm.upd = 0;
     __syncthreads();
     for (uint32_t e = tid; e < n; e += kThreads)
-        atomicAdd(&sm.cnt[(__ldg(&a.keys[eb + e]) >> a.item_bits) >> 1], 1u);
+        atomicAdd(&sm.cnt[__ldg(&a.keys[eb + e]) >> a.item_bits], 1u);
     __syncthreads();
     if (warp == 0) {   // exclusive scan of NSTEP counts, 32 at a time
         uint32_t carry = 0;
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     for (uint32_t r0 = 0; r0 < n; r0 += kThreads) {
         const uint32_t e = r0 + tid;
         const bool ok = e < n;
-        const uint32_t st = ok ? (__ldg(&a.keys[eb + e]) >> a.item_bits) >> 1 : 0xFFFFu;
+        const uint32_t st = ok ? __ldg(&a.keys[eb + e]) >> a.item_bits : 0xFFFFu;
         const uint32_t id = ok ? __ldg(&a.idx[eb + e]) : 0u;
         for (int s = tid; s < kWarps * NSTEP; s += kThreads) (&sm.wcnt[0][0])[s] = 0;
         __syncthreads();
