@@ -329,6 +329,19 @@ int wsb_grid_unpack_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, in
 int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *idx_host, uint32_t *off_host,
                     int64_t *n_entries, int64_t *n_buckets);
 
+/* Debug / parity: the gridder's bucketing (K1) of m prepared records for
+ * the slab rows [v_start, v_start+v_count): entries (record, work item)
+ * with key = item | rowrel << item_bits (item = (plane * ceil(n_u/64) +
+ * superstrip) * ceil(v_count/128) + row block, rowrel = floor(gv) - S - (first
+ * row of the block - 2S)), sorted by item, record order inside an item.
+ * Host buffers (nullable): keys/idx u32[n_entries] (at most 4 m), off
+ * u32[n_items + 1]. Sizes returned in *n_entries / *n_items / *item_bits.
+ * Synchronous. */
+int wsb_bucket_items(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int32_t v_start,
+                     int32_t v_count, const double *rec, const uint32_t *plane, int64_t m,
+                     uint32_t *keys_host, uint32_t *idx_host, uint32_t *off_host,
+                     int64_t *n_entries, int64_t *n_items, int32_t *item_bits);
+
 /* Timing of the kernels launched by the last wsb_image_device call, in ms,
  * measured with CUDA events on the context stream:
  * [0] prepare, [1] bucket+sort, [2] grid, [3] fft rows, [4] fft cols+stack,

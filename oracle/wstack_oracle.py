@@ -262,6 +262,57 @@ def count_updates(gu, gv, n_u: int, row_lo: int, row_hi: int, S: int) -> int:
     return total
 
 
+def tap_bounds(g, S: int, lo: int, hi: int):
+    """First / last tap index {i : |g - i| <= S} (gridder.py:164-177) clipped
+    to [lo, hi], per record (empty where first > last)."""
+    g = np.asarray(g, np.float64)
+    fl = np.floor(g).astype(np.int64)
+    i0 = fl - S
+    i0 = np.where(g - i0 > S, i0 + 1, i0)
+    return np.maximum(i0, lo), np.minimum(fl + S, hi)
+
+
+def item_entries(gu, gv, plane, n_u: int, n_w: int, S: int, v_start: int, v_count: int,
+                 ss_cols: int = 64, item_rows: int = 128):
+    """The GPU gridder's work-item bucketing restated (contract of
+    wsb_bucket_items, include/wsb.h): every (record, item) pair whose taps
+    reach item = (plane, ss_cols-column superstrip, item_rows-row block of
+    the slab), key = item | rowrel << item_bits with rowrel = floor(gv) - S -
+    (block row0 - 2S), stably sorted by item (record order inside an item).
+    Tap sets are the reference's (gridder.py:164-177). Returns
+    (keys u32, idx u32, off u32[n_items + 1], item_bits)."""
+    gu, gv = np.asarray(gu, np.float64), np.asarray(gv, np.float64)
+    plane = np.asarray(plane, np.int64)
+    n_ss = -(-n_u // ss_cols)
+    n_rb = -(-v_count // item_rows)
+    n_items = n_w * n_ss * n_rb
+    item_bits = max(1, int(np.ceil(np.log2(n_items))) if n_items > 1 else 0)
+    i0, i1 = tap_bounds(gu, S, 0, n_u - 1)
+    j0, j1 = tap_bounds(gv, S, v_start, v_start + v_count - 1)
+    ok = (i0 <= i1) & (j0 <= j1)
+    anchor = np.floor(gv).astype(np.int64) - S
+    keys, idx = [], []
+    rec = np.arange(len(gu), dtype=np.int64)
+    for drb in (0, 1):
+        for dss in (0, 1):
+            ss = i0 // ss_cols + dss
+            rb = (j0 - v_start) // item_rows + drb
+            m = ok & (ss <= i1 // ss_cols) & (rb <= (j1 - v_start) // item_rows)
+            item = (plane[m] * n_ss + ss[m]) * n_rb + rb[m]
+            rowrel = anchor[m] - (v_start + rb[m] * item_rows - 2 * S)
+            keys.append((item | (rowrel << item_bits)).astype(np.uint32))
+            idx.append(rec[m])
+    keys, idx = np.concatenate(keys), np.concatenate(idx)
+    # record order, then the per-record entry order (row block, superstrip)
+    order = np.lexsort((keys & ((1 << item_bits) - 1), idx))
+    keys, idx = keys[order], idx[order]
+    srt = np.argsort(keys & ((1 << item_bits) - 1), kind="stable")
+    keys, idx = keys[srt], idx[srt].astype(np.uint32)
+    cnt = np.bincount(keys & ((1 << item_bits) - 1), minlength=n_items)
+    off = np.concatenate([[0], np.cumsum(cnt)]).astype(np.uint32)
+    return keys, idx, off, item_bits
+
+
 def grid_all(prepared_parts, n_u, n_v, n_w, kind, S, shape, n_ranks):
     """grid_all (gridder.py:262-294): exchange then grid each slab; the
     reduce is the identity after the exchange (pipeline.py:117-122).

@@ -33,7 +33,7 @@ EXPORTS = (
     "wsb_grid_unpack", "wsb_tiles_debug", "wsb_last_timings", "wsb_row_histogram",
     "wsb_fft_rows_peer", "wsb_push_blocks", "wsb_ctx_set_precision", "wsb_route_planes_count",
     "wsb_route_planes_pack", "wsb_fft_cols_partial", "wsb_image_finish", "wsb_plane_histogram",
-    "wsb_grid_unpack_rows", "wsb_ctx_set_energy",
+    "wsb_grid_unpack_rows", "wsb_ctx_set_energy", "wsb_bucket_items",
 )
 
 
@@ -118,6 +118,7 @@ def lib() -> C.CDLL:
         "wsb_grid_unpack": (C.c_int, [p, G, i32, i32, p, p]),
         "wsb_grid_unpack_rows": (C.c_int, [p, G, i32, i32, i32, i32, p, p]),
         "wsb_tiles_debug": (C.c_int, [p, p, p, p, p]),
+        "wsb_bucket_items": (C.c_int, [p, G, i32, i32, i32, p, p, i64, p, p, p, p, p, p]),
         "wsb_last_timings": (C.c_int, [p, p, p]),
     }
     for name, (res, args) in sig.items():

@@ -526,6 +526,32 @@ int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *idx_host, uint32_t *off_host, int64_
     return WSB_OK;
 }
 
+int wsb_bucket_items(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, int32_t v_start,
+                     int32_t v_count, const double *rec, const uint32_t *plane, int64_t m,
+                     uint32_t *keys_host, uint32_t *idx_host, uint32_t *off_host,
+                     int64_t *n_entries, int64_t *n_items, int32_t *item_bits) {
+    if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
+    WSB_TRY(validate_grid(grid));
+    if (half_support < 1 || half_support > kMaxS) return fail(WSB_EINVAL, "half_support out of range");
+    if (v_start < 0 || v_count < 1 || v_start + v_count > grid->n_v)
+        return fail(WSB_EINVAL, "slab rows outside the mesh");
+    WSB_TRY(set_device(ctx));
+    ItemBuckets bk;
+    WSB_TRY(bucket_items(ctx, grid, half_support, v_start, v_count, nullptr, const_cast<double *>(rec),
+                         const_cast<uint32_t *>(plane), m, &bk));
+    if (n_entries) *n_entries = bk.n_entries;
+    if (n_items) *n_items = bk.n_items;
+    if (item_bits) *item_bits = bk.item_bits;
+    WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (keys_host && bk.n_entries)
+        WSB_CUDA_TRY(cudaMemcpy(keys_host, bk.keys, 4 * bk.n_entries, cudaMemcpyDeviceToHost));
+    if (idx_host && bk.n_entries)
+        WSB_CUDA_TRY(cudaMemcpy(idx_host, bk.idx, 4 * bk.n_entries, cudaMemcpyDeviceToHost));
+    if (off_host)
+        WSB_CUDA_TRY(cudaMemcpy(off_host, bk.off, 4 * (bk.n_items + 1), cudaMemcpyDeviceToHost));
+    return WSB_OK;
+}
+
 int wsb_last_timings(wsb_ctx *ctx, double *ms6, int32_t *launches) {
     if (!ctx) return fail(WSB_EINVAL, "ctx is NULL");
     if (ms6)

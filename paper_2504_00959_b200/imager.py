@@ -304,6 +304,32 @@ def grid_slab_device(rec: torch.Tensor, plane: torch.Tensor, spec: GridSpec, ker
     return out, int(upd.value)
 
 
+def bucket_items_device(rec: torch.Tensor, plane: torch.Tensor, spec, half_support: int,
+                        v_start: int, v_count: int):
+    """The gridder's bucketing (K1) of prepared records, copied to the host:
+    (keys u32, idx u32, off u32 [n_items + 1], item_bits) -- see
+    wsb_bucket_items in include/wsb.h."""
+    spec = as_grid_spec(spec)
+    ctx = context(rec.device)
+    m = rec.shape[0]
+    g = spec.c_struct()
+    ne, ni, ib = C.c_int64(), C.c_int64(), C.c_int32()
+    L.check(L.lib().wsb_bucket_items(ctx.handle, C.byref(g), int(half_support), int(v_start),
+                                     int(v_count), _ptr(rec.contiguous()),
+                                     _ptr(plane.contiguous()), m, None, None, None,
+                                     C.byref(ne), C.byref(ni), C.byref(ib)))
+    keys = np.empty(max(ne.value, 1), np.uint32)
+    idx = np.empty(max(ne.value, 1), np.uint32)
+    off = np.empty(ni.value + 1, np.uint32)
+    L.check(L.lib().wsb_bucket_items(ctx.handle, C.byref(g), int(half_support), int(v_start),
+                                     int(v_count), _ptr(rec.contiguous()),
+                                     _ptr(plane.contiguous()), m,
+                                     keys.ctypes.data_as(C.c_void_p), idx.ctypes.data_as(C.c_void_p),
+                                     off.ctypes.data_as(C.c_void_p), C.byref(ne), C.byref(ni),
+                                     C.byref(ib)))
+    return keys[:ne.value], idx[:ne.value], off, int(ib.value)
+
+
 def unpack_grid_device(grid_p: torch.Tensor, spec: GridSpec, v_start: int, v_count: int,
                        rows: tuple | None = None):
     """Strip layout -> (n_w, v_count, n_u) complex128 without the checkerboard

@@ -75,6 +75,30 @@ def cfg2(W):
     return spec, (u, v, w, t, vis, wt)
 
 
+@pytest.mark.parametrize("slabs", [1, 3])
+def test_cfg2_bucketing_bitexact(W, cfg2, slabs):
+    """K1 (wsb_bucket_items) at the benched size: every (record, work item)
+    entry, its key and the item order equal the restated contract
+    (oracle.item_entries, taps of gridder.py:164-177), for the whole mesh and
+    for a slab of an uneven 3-way split."""
+    spec, (u, v, w, t, vis, wt) = cfg2
+    dev = torch.device("cuda", 0)
+    rec, plane = W.prepare_device(*(torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+                                    for a in (u, v, w, vis, wt)), spec)
+    v0, vc = (0, spec.n_v) if slabs == 1 else (700, 650)
+    gv = rec[:, 1].cpu().numpy()
+    sel = np.nonzero(O.halo_mask(gv, 3, v0, vc))[0]
+    r = rec[torch.from_numpy(sel).to(dev)].contiguous()
+    pl = plane[torch.from_numpy(sel).to(dev)].contiguous()
+    keys, idx, off, ib = W.bucket_items_device(r, pl, spec, 3, v0, vc)
+    rk, ri, ro, rib = O.item_entries(u[sel] * spec.n_u, v[sel] * spec.n_v,
+                                     O.plane_of_w(w[sel], spec.n_w), spec.n_u, spec.n_w, 3, v0, vc)
+    assert ib == rib
+    assert np.array_equal(off, ro)
+    assert np.array_equal(keys, rk)
+    assert np.array_equal(idx, ri)
+
+
 def test_cfg2_update_count_and_grid_block(W, cfg2):
     spec, (u, v, w, t, vis, wt) = cfg2
     kern = W.KernelSpec.gaussian(3, 1.0)

@@ -96,3 +96,34 @@ def test_validation_errors():
         O.prepare([0.5], [0.5], [1.5], [0], [[1 + 0j]], [[1.0]], 8, 8, 2)
     with pytest.raises(ValueError):
         O.prepare([0.5], [0.5], [0.5], [0], [[1 + 0j]], [[-1.0]], 8, 8, 2)
+
+
+def test_item_entries_cover_every_update(golden_grid):
+    """The gridder's work-item bucketing restated (oracle.item_entries): the
+    per-entry tap products add up to the reference's grid_updates, every
+    record with taps in the slab appears, and items are in record order."""
+    g = golden_grid
+    for R in (1, 2, 3):
+        tot = 0
+        n_u, n_v = 64, 96
+        rng = np.random.default_rng(7)
+        gu, gv = rng.uniform(0, n_u, 3000), rng.uniform(0, n_v, 3000)
+        gu[:5] = [0.0, 63.5, 31.0, 64 - 1e-9, 2.999]          # edges, integers
+        plane = rng.integers(0, 3, 3000)
+        for d in range(R):
+            v0, vc = O.partition_1d(n_v, R, d)
+            m = O.halo_mask(gv, 3, v0, vc)
+            keys, idx, off, ib = O.item_entries(gu[m], gv[m], plane[m], n_u, 3, 3, v0, vc,
+                                                ss_cols=16, item_rows=8)
+            assert np.all(np.diff(keys & ((1 << ib) - 1)) >= 0)
+            for it in range(len(off) - 1):
+                assert np.all(np.diff(idx[off[it]:off[it + 1]].astype(np.int64)) > 0)
+            n_rb = -(-vc // 8)
+            for k, i in zip(keys, idx):
+                item = int(k) & ((1 << ib) - 1)
+                rb, ss = item % n_rb, (item // n_rb) % 4
+                c0, c1 = O.tap_bounds(gu[m][i:i + 1], 3, ss * 16, ss * 16 + 15)
+                r0, r1 = O.tap_bounds(gv[m][i:i + 1], 3, v0 + rb * 8, min(v0 + rb * 8 + 7, v0 + vc - 1))
+                assert c0[0] <= c1[0] and r0[0] <= r1[0]
+                tot += int((c1[0] - c0[0] + 1) * (r1[0] - r0[0] + 1))
+        assert tot == O.count_updates(gu, gv, n_u, 0, n_v, 3)
