@@ -21,6 +21,7 @@ from .imager import (  # noqa: F401
     grid_all,
     grid_sector,
     slab_of,
+    bucket_items_device,
     grid_slab_device,
     image,
     image_device,
