@@ -50,39 +50,44 @@ def stale_sources(lib: Path = LIB) -> list:
     return [d.name for d in deps if d.exists() and d.stat().st_mtime > t]
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> Path:
+    """debug: device bounds checks (WSB_DCHECK) into libwsb_dbg.so / build/dbg."""
     nvcc = _nvcc()
-    BUILD.mkdir(exist_ok=True)
+    build_dir = BUILD / "dbg" if debug else BUILD
+    lib = PKG / "libwsb_dbg.so" if debug else LIB
+    flags = FLAGS + (["-DWSB_DEBUG_CHECKS"] if debug else [])
+    build_dir.mkdir(parents=True, exist_ok=True)
     hdrs = [CSRC / h for h in HEADERS] + [ROOT / "include" / "wsb.h"]
     objs = []
     for src in SOURCES:
         s = CSRC / src
-        o = BUILD / (Path(src).stem + ".o")
+        o = build_dir / (Path(src).stem + ".o")
         objs.append(o)
         if force or _stale(o, [s, *hdrs]):
-            cmd = [nvcc, *ARCH, *FLAGS, "-I", str(ROOT / "include"), "-c", str(s), "-o", str(o)]
+            cmd = [nvcc, *ARCH, *flags, "-I", str(ROOT / "include"), "-c", str(s), "-o", str(o)]
             r = subprocess.run(cmd, capture_output=True, text=True)
-            log = (BUILD / (Path(src).stem + ".ptxas.log"))
+            log = (build_dir / (Path(src).stem + ".ptxas.log"))
             log.write_text(r.stdout + r.stderr)
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
                 raise RuntimeError(f"nvcc failed on {src}")
             if verbose:
                 sys.stdout.write(r.stderr)
-    if force or _stale(LIB, objs):
-        tmp = LIB.with_suffix(".so.tmp")
+    if force or _stale(lib, objs):
+        tmp = lib.with_suffix(".so.tmp")
         cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
-        tmp.replace(LIB)
-    return LIB
+        tmp.replace(lib)
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--debug", action="store_true")
     a = ap.parse_args()
-    print(build(a.force, a.verbose))
+    print(build(a.force, a.verbose, a.debug))

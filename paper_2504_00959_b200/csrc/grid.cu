@@ -186,6 +186,7 @@ struct SweepArgs {
     int out_f32;               // 1: complex64 grid (FP32 path; accumulation stays FP64)
     int n_u, v_start, v_count, n_ss, n_rb, item_bits, n_s16;
     int64_t n_parts;
+    int64_t n_rec, out_elems;  // bounds (debug checks)
 };
 
 template <int KIND, int S>
@@ -242,7 +243,11 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     if (tid == 0) sm.upd = 0;
     __syncthreads();
     for (uint32_t e = tid; e < n; e += kThreads)
-        atomicAdd(&sm.cnt[__ldg(&a.keys[eb + e]) >> a.item_bits], 1u);
+    {
+        const uint32_t st = __ldg(&a.keys[eb + e]) >> a.item_bits;
+        WSB_DCHECK(st < (uint32_t)NSTEP, "item %lld e %u st %u", (long long)item, e, st);
+        atomicAdd(&sm.cnt[st], 1u);
+    }
     __syncthreads();
     if (warp == 0) {   // exclusive scan of NSTEP counts, 32 at a time
         uint32_t carry = 0;
@@ -274,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         if (ok) {
             uint32_t pos = sm.cnt[st] + sm.run[st] + __popc(peers & lt);
             for (int w = 0; w < warp; ++w) pos += sm.wcnt[w][st];
+            WSB_DCHECK(pos < n && id < a.n_rec, "item %lld pos %u n %u id %u", (long long)item, pos, n, id);
             sm.sorted[pos] = id;
         }
         __syncthreads();
@@ -283,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             for (int w = 0; w < kWarps; ++w) t += sm.wcnt[w][s];
             sm.run[s] += t;
         }
+        __syncthreads();   // wcnt is cleared by the next round
     }
 
     // ---- phase B: the sweep -------------------------------------------------
@@ -310,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             if (direct) {
                 const double sg = ((col + row) & 1) ? -1.0 : 1.0;
                 const int64_t o = (strip_base + (row - a.v_start)) * kC + c;
+                WSB_DCHECK(o >= 0 && o < a.out_elems, "item %lld o %lld", (long long)item, (long long)o);
                 if (f32)
                     out32[o] = make_float2((float)(acc[p].x * sg), (float)(acc[p].y * sg));
                 else
@@ -404,6 +412,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                         sm.wv[r][1][t] = (2 * t < W) ? wgt[min(2 * t, W - 1)] : 0.0;
                         sm.wv[r][2][t] = (2 * t + 1 < W) ? wgt[min(2 * t + 1, W - 1)] : 0.0;
                     }
+                    WSB_DCHECK(rel >= 0 && rel < NSTEP, "item %lld rel %d gv %f", (long long)item, rel, rc.y);
                     sm.meta[r].y = rel >> 1;
                     sm.meta[r].z = rel & 1;
                     uint32_t in = vm;
@@ -648,6 +657,8 @@ int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
     a.parts = parts;
     a.partial = partial;
     a.n_parts = n_parts;
+    a.n_rec = 0x7FFFFFFF;
+    a.out_elems = (int64_t)g->n_w * a.n_s16 * kC * v_count;
     // ---- sweep ---------------------------------------------------------------
     int rc;
     if (k->kind == WSB_KERNEL_GAUSSIAN) {  // s2 = 2 sigma^2 (gridder.py:85)

@@ -2,12 +2,32 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stdio.h>
 #include <stdint.h>
 #include <algorithm>
 #include <string>
 #include <vector>
 
 #include "../../include/wsb.h"
+
+// Device-side bounds checks of the debug build (python -m
+// paper_2504_00959_b200.build --debug: libwsb_dbg.so, loaded with
+// WSB_LIB=.../libwsb_dbg.so): a failed check prints and traps.
+#ifdef WSB_DEBUG_CHECKS
+#define WSB_DCHECK(cond, ...)                                                   \
+    do {                                                                        \
+        if (!(cond)) {                                                          \
+            printf("WSB_DCHECK %s:%d: %s | ", __FILE__, __LINE__, #cond);       \
+            printf(__VA_ARGS__);                                                \
+            printf("\n");                                                       \
+            __trap();                                                           \
+        }                                                                       \
+    } while (0)
+#else
+#define WSB_DCHECK(cond, ...) \
+    do {                      \
+    } while (0)
+#endif
 
 namespace wsb {
 
