@@ -101,12 +101,11 @@ template <int KIND, int S>
 __device__ __forceinline__ uint32_t axis_weights(double g, int i0, const KParams<S> &kp,
                                                  double i0beta, double *w) {
     constexpr int W = 2 * S + 1;
-    uint32_t mask = 0;
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-        const double d = __dsub_rn(g, (double)(i0 + k));
-        mask |= (uint32_t)(fabs(d) <= (double)S) << k;
-    }
+    // with i0 = floor(g) - S, d_k = g - (i0 + k) lies in (S - k - 1, S - k]
+    // exactly for k >= 1 (Sterbenz): |d_k| <= S holds for k = 1..2S; only the
+    // first tap needs the reference's rounded test |g - i| <= S
+    uint32_t mask = (2u << (W - 1)) - 2u;
+    mask |= (uint32_t)(fabs(__dsub_rn(g, (double)i0)) <= (double)S);
     if (KIND == WSB_KERNEL_GAUSSIAN && kp.factorised) {
         const double f = __dsub_rn(g, (double)(i0 + S));
         // (multiplying by 1/s2 instead of dividing: a few ulp, no FP64 division)
@@ -171,7 +170,7 @@ constexpr int kC = WSB_STRIP;          // columns per warp strip
 constexpr int kWarps = 4;              // strips (warps) per item
 constexpr int kSS = kC * kWarps;       // superstrip width (64)
 constexpr int kThreads = 32 * kWarps;
-constexpr int kChunk = 64;             // records staged per round (2 threads each)
+constexpr int kChunk = 64;             // records staged per round (one per thread of warps 0-1)
 constexpr int kRaw = 3;                // gather ring: chunks in flight
 
 struct SweepArgs {
@@ -189,25 +188,31 @@ struct SweepArgs {
     int64_t n_rec, out_elems;  // bounds (debug checks)
 };
 
+// One staged record: everything a lane reads to apply it, at one base
+// address (the sweep addresses a record with a single IMAD).
+template <int S>
+struct StagedRec {
+    static constexpr int W = 2 * S + 1;
+    static constexpr int TP = (S + 2) & ~1;   // ring slots S+1, padded to 16 bytes
+    double2 tu[W + 1];     // value * u weight per window column; slot W = 0
+    double wv[3][TP];      // v weights: [0] rows 2t-1, [1] rows 2t, [2] rows 2t+1 of the window
+    int4 meta;             // (first window column - superstrip col0, window step, parity, strip mask)
+};
+
 template <int KIND, int S>
 struct Shm {
-    static constexpr int W = 2 * S + 1;
-    static constexpr int T = S + 1;              // ring slots (row pairs) per lane
-    static constexpr int TP = (T + 1) & ~1;      // padded to 16 bytes
     static constexpr int NROW = kItemRows + 2 * S;   // anchor rows that reach the item
-    double2 tu[kChunk][W + 1];      // value * u weight per window column; slot W = 0
-    double wv[kChunk][3][TP];       // v weights: [0] rows 2t-1, [1] rows 2t, [2] rows 2t+1
-    int4 meta[kChunk];              // (first window column - superstrip col0, step, d, strip mask)
+    StagedRec<S> rec[kChunk];
     double4 raw[kRaw][kChunk];      // gathered records (gu, gv, Re, Im)
     uint32_t sorted[kPartCap];      // record indices of the part in (anchor row, entry) order
     uint32_t cnt[NROW + 1], run[NROW];
     uint16_t wcnt[kWarps][NROW];
-    unsigned long long upd;
+    uint32_t touch[kChunk / 32][kWarps];   // per staging warp: ballot of records touching strip w
 };
 
 template <int KIND, int S>
 constexpr int sweep_min_blocks() {
-    return sizeof(Shm<KIND, S>) <= 24 * 1024 ? 8 : (sizeof(Shm<KIND, S>) <= 36 * 1024 ? 6 : 4);
+    return sizeof(Shm<KIND, S>) <= 28 * 1024 ? 7 : (sizeof(Shm<KIND, S>) <= 36 * 1024 ? 6 : 4);
 }
 
 template <int KIND, int S>
@@ -216,7 +221,8 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     constexpr int W = 2 * S + 1;
     constexpr int T = S + 1;
     using Sm = Shm<KIND, S>;
-    constexpr int NSTEP = Sm::NROW;   // sort bins: anchor rows (a window step holds two)
+    using Rec = StagedRec<S>;
+    constexpr int NROW = Sm::NROW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Sm &sm = *reinterpret_cast<Sm *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -238,29 +244,27 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     // cell's accumulation order (anchor row, record) whatever the slab
     // boundaries' parity -- the v-slab result is then bit-identical for any
     // slab split.
-    for (int s = tid; s <= NSTEP; s += kThreads) sm.cnt[s] = 0;
-    for (int s = tid; s < NSTEP; s += kThreads) sm.run[s] = 0;
-    if (tid == 0) sm.upd = 0;
+    for (int s = tid; s <= NROW; s += kThreads) sm.cnt[s] = 0;
+    for (int s = tid; s < NROW; s += kThreads) sm.run[s] = 0;
     __syncthreads();
-    for (uint32_t e = tid; e < n; e += kThreads)
-    {
+    for (uint32_t e = tid; e < n; e += kThreads) {
         const uint32_t st = __ldg(&a.keys[eb + e]) >> a.item_bits;
-        WSB_DCHECK(st < (uint32_t)NSTEP, "item %lld e %u st %u", (long long)item, e, st);
+        WSB_DCHECK(st < (uint32_t)NROW, "item %lld e %u st %u", (long long)item, e, st);
         atomicAdd(&sm.cnt[st], 1u);
     }
     __syncthreads();
-    if (warp == 0) {   // exclusive scan of NSTEP counts, 32 at a time
+    if (warp == 0) {   // exclusive scan of the row counts, 32 at a time
         uint32_t carry = 0;
-        for (int s0 = 0; s0 <= NSTEP; s0 += 32) {
+        for (int s0 = 0; s0 <= NROW; s0 += 32) {
             const int s = s0 + lane;
-            const uint32_t x = s <= NSTEP ? sm.cnt[s] : 0u;
+            const uint32_t x = s <= NROW ? sm.cnt[s] : 0u;
             uint32_t incl = x;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            if (s <= NSTEP) sm.cnt[s] = carry + incl - x;
+            if (s <= NROW) sm.cnt[s] = carry + incl - x;
             carry += __shfl_sync(0xffffffffu, incl, 31);
         }
     }
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         const bool ok = e < n;
         const uint32_t st = ok ? __ldg(&a.keys[eb + e]) >> a.item_bits : 0xFFFFu;
         const uint32_t id = ok ? __ldg(&a.idx[eb + e]) : 0u;
-        for (int s = tid; s < kWarps * NSTEP; s += kThreads) (&sm.wcnt[0][0])[s] = 0;
+        for (int s = tid; s < kWarps * NROW; s += kThreads) (&sm.wcnt[0][0])[s] = 0;
         __syncthreads();
         const uint32_t peers = __match_any_sync(0xffffffffu, st);
         if (ok && lane == __ffs(peers) - 1) sm.wcnt[warp][st] = (uint16_t)__popc(peers);
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             sm.sorted[pos] = id;
         }
         __syncthreads();
-        for (int s = tid; s < NSTEP; s += kThreads) {
+        for (int s = tid; s < NROW; s += kThreads) {
             uint32_t t = 0;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) t += sm.wcnt[w][s];
@@ -303,11 +307,14 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     const bool f32 = direct && a.out_f32;
     const int64_t strip_base = ((int64_t)plane * a.n_s16 + col / kC) * a.v_count;
     double2 *const ptile = direct ? nullptr : a.partial + (int64_t)pd.w * kItemRows * kSS;
+    // lane offsets inside a staged record: its tu column (clamped to the zero
+    // slot) and its parity row of v weights
+    const int lane_wv = 32 * (q + 1);               // + (-32 * parity) per record
 
     double2 acc[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
-    int step = 0, phase = 0;         // window base B = Bfirst + 2 * step, slot `phase` holds rows B, B+1
+    int step = 0, phase = 0;   // window base B = Bfirst + 2 step; slot `phase` holds rows B + q
     unsigned cnt_upd = 0;
 
     auto emit = [&](auto P) {
@@ -330,24 +337,6 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         ++step;
         phase = (p + 1 == T) ? 0 : p + 1;
     };
-    auto apply = [&](auto P, int r) {
-        constexpr int p = decltype(P)::value;
-        const int4 m = sm.meta[r];
-        int k = wc - m.x;
-        k = (unsigned)k < (unsigned)W ? k : W;
-        const double2 tv = sm.tu[r][k];
-        const double *wp = &sm.wv[r][q - m.z + 1][0];
-#pragma unroll
-        for (int t = 0; t < T; t += 2) {
-            const double2 w2 = *reinterpret_cast<const double2 *>(wp + t);
-            acc[(p + t) % T].x = fma(tv.x, w2.x, acc[(p + t) % T].x);
-            acc[(p + t) % T].y = fma(tv.y, w2.x, acc[(p + t) % T].y);
-            if (t + 1 < T) {
-                acc[(p + t + 1) % T].x = fma(tv.x, w2.y, acc[(p + t + 1) % T].x);
-                acc[(p + t + 1) % T].y = fma(tv.y, w2.y, acc[(p + t + 1) % T].y);
-            }
-        }
-    };
 
     // gather: thread pair (2r, 2r+1) copies record r's two 16-byte halves
     const int nchunks = (int)((n + kChunk - 1) / kChunk);
@@ -367,87 +356,96 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
 #pragma unroll
     for (int ch = 0; ch < kRaw - 1; ++ch) fetch(ch);
 
+    const unsigned char *const recbase = reinterpret_cast<const unsigned char *>(&sm.rec[0]);
     for (int ch = 0; ch < nchunks; ++ch) {
         asm volatile("cp.async.wait_group %0;\n" ::"n"(kRaw - 2) : "memory");
         __syncthreads();   // raw[ch] landed for every thread; the previous sweep is done
         fetch(ch + kRaw - 1);
         const int nr = (int)min((uint32_t)kChunk, n - (uint32_t)ch * kChunk);
-        // ---- stage: thread pair per record -------------------------------
-        {
-            const int r = tid >> 1;
-            unsigned mine = 0;      // u-tap (even thread) / v-tap (odd thread) count in the item
+        // ---- stage: warps 0-1, one record per thread (no divergence) --------
+        if (tid < kChunk) {
+            const int r = tid;
+            int mask = 0;
             if (r < nr) {
                 const double4 rc = sm.raw[ch % kRaw][r];
+                Rec &st = sm.rec[r];
                 double wgt[W];
-                if ((tid & 1) == 0) {            // u axis: value * weight per window column
-                    const int ib = (int)floor(rc.x) - S;
-                    const uint32_t um = axis_weights<KIND, S>(rc.x, ib, kp, i0b, wgt);
+                // u axis: value * weight per window column
+                const int ib = (int)floor(rc.x) - S;
+                const uint32_t um = axis_weights<KIND, S>(rc.x, ib, kp, i0b, wgt);
 #pragma unroll
-                    for (int k = 0; k < W; ++k)
-                        sm.tu[r][k] = make_double2(__dmul_rn(rc.z, wgt[k]), __dmul_rn(rc.w, wgt[k]));
-                    sm.tu[r][W] = make_double2(0.0, 0.0);
-                    // tap columns inside the superstrip and the mesh, and the
-                    // warps (16-column strips) they fall into
-                    const int c_lo = max(col0, 0) - ib, c_hi = min(col0 + kSS, a.n_u) - 1 - ib;
-                    uint32_t in = um;
-#pragma unroll
-                    for (int k = 0; k < W; ++k)
-                        if (k < c_lo || k > c_hi) in &= ~(1u << k);
-                    int mask = 0;
-                    if (in) {
-                        const int k_lo = __ffs(in) - 1, k_hi = 31 - __clz(in);
-                        const int w_lo = (ib + k_lo - col0) / kC, w_hi = (ib + k_hi - col0) / kC;
-                        mask = ((2 << w_hi) - 1) & ~((1 << w_lo) - 1);
-                    }
-                    mine = __popc(in);
-                    sm.meta[r].x = ib - col0;
-                    sm.meta[r].w = mask;
-                } else {                          // v axis: parity-split row weights
-                    const int jb = (int)floor(rc.y) - S;
-                    const uint32_t vm = axis_weights<KIND, S>(rc.y, jb, kp, i0b, wgt);
-                    const int rel = jb - Bfirst;
-#pragma unroll
-                    for (int t = 0; t < Sm::TP; ++t) {
-                        sm.wv[r][0][t] = (2 * t - 1 >= 0 && 2 * t - 1 < W) ? wgt[max(2 * t - 1, 0)] : 0.0;
-                        sm.wv[r][1][t] = (2 * t < W) ? wgt[min(2 * t, W - 1)] : 0.0;
-                        sm.wv[r][2][t] = (2 * t + 1 < W) ? wgt[min(2 * t + 1, W - 1)] : 0.0;
-                    }
-                    WSB_DCHECK(rel >= 0 && rel < NSTEP, "item %lld rel %d gv %f", (long long)item, rel, rc.y);
-                    sm.meta[r].y = rel >> 1;
-                    sm.meta[r].z = rel & 1;
-                    uint32_t in = vm;
-#pragma unroll
-                    for (int k = 0; k < W; ++k)
-                        if (jb + k < R0 || jb + k >= R1) in &= ~(1u << k);
-                    mine = __popc(in);
+                for (int k = 0; k < W; ++k)
+                    st.tu[k] = make_double2(__dmul_rn(rc.z, wgt[k]), __dmul_rn(rc.w, wgt[k]));
+                st.tu[W] = make_double2(0.0, 0.0);
+                // tap columns inside the superstrip (and the mesh); the strips they touch
+                const int k_lo = max(col0 - ib, 0), k_hi = min(min(col0 + kSS, a.n_u) - ib, W) - 1;
+                uint32_t uin = k_hi >= k_lo ? um & (((2u << k_hi) - 1u) & ~((1u << k_lo) - 1u)) : 0u;
+                if (uin) {
+                    const int w_lo = (ib + __ffs(uin) - 1 - col0) / kC;
+                    const int w_hi = (ib + 31 - __clz(uin) - col0) / kC;
+                    mask = ((2 << w_hi) - 1) & ~((1 << w_lo) - 1);
                 }
+                // v axis: parity-split row weights
+                const int jb = (int)floor(rc.y) - S;
+                const uint32_t vm = axis_weights<KIND, S>(rc.y, jb, kp, i0b, wgt);
+                const int rel = jb - Bfirst;
+                WSB_DCHECK(rel >= 0 && rel < NROW, "item %lld rel %d", (long long)item, rel);
+#pragma unroll
+                for (int t = 0; t < Rec::TP; ++t) {
+                    st.wv[0][t] = (2 * t - 1 >= 0 && 2 * t - 1 < W) ? wgt[max(2 * t - 1, 0)] : 0.0;
+                    st.wv[1][t] = (2 * t < W) ? wgt[min(2 * t, W - 1)] : 0.0;
+                    st.wv[2][t] = (2 * t + 1 < W) ? wgt[min(2 * t + 1, W - 1)] : 0.0;
+                }
+                st.meta = make_int4(ib - col0, rel >> 1, -32 * (rel & 1), mask);
+                // cell updates inside this item (grid_sector's count)
+                const int r_lo = max(R0 - jb, 0), r_hi = min(R1 - jb, W) - 1;
+                const uint32_t vin = r_hi >= r_lo ? vm & (((2u << r_hi) - 1u) & ~((1u << r_lo) - 1u)) : 0u;
+                cnt_upd += __popc(uin) * __popc(vin);
             }
-            const unsigned other = __shfl_xor_sync(0xffffffffu, mine, 1);
-            if ((tid & 1) == 0) cnt_upd += mine * other;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t b = __ballot_sync(0xffffffffu, (mask >> w) & 1);
+                if (lane == 0) sm.touch[warp][w] = b;
+            }
         }
         __syncthreads();   // stage complete
-        // ---- sweep: this warp's strip -----------------------------------
+        // ---- sweep: this warp's strip, records in order ---------------------
 #pragma unroll 1
         for (int g = 0; g < kChunk / 32; ++g) {
-            const int r = g * 32 + lane;
-            const bool ok = r < nr;
-            const int4 mm = ok ? sm.meta[r] : make_int4(0, 0x7fffffff, 0, 0);
-            const bool touch = ok && ((mm.w >> warp) & 1);
-            uint32_t rem = __ballot_sync(0xffffffffu, ok);
-            const uint32_t tm = __ballot_sync(0xffffffffu, touch);
-            while (rem) {
-                const int s = __shfl_sync(0xffffffffu, mm.y, __ffs(rem) - 1);
-                while (step < s) dispatch_phase<0, T>(phase, emit);
-                const uint32_t runm = __ballot_sync(0xffffffffu, ok && mm.y == s) & rem;
-                rem &= ~runm;
-                uint32_t app = runm & tm;
+            uint32_t m = sm.touch[g][warp];
+            const int gbase = g * 32;
+            while (m) {
                 dispatch_phase<0, T>(phase, [&](auto P) {
-                    while (app) {
-                        const int b = __ffs(app) - 1;
-                        app &= app - 1;
-                        apply(P, g * 32 + b);
+                    constexpr int p = decltype(P)::value;
+                    while (m) {
+                        const int r = gbase + __ffs(m) - 1;
+                        const unsigned char *rp = recbase + r * (int)sizeof(Rec);
+                        const int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
+                        if (mt.y != step) return;          // the window moves first
+                        m &= m - 1;
+                        int k = wc - mt.x;
+                        k = (unsigned)k < (unsigned)W ? k : W;
+                        const double2 tv = *reinterpret_cast<const double2 *>(rp + 16 * k);
+                        const double *wp = reinterpret_cast<const double *>(
+                            rp + offsetof(Rec, wv) + lane_wv + mt.z);
+#pragma unroll
+                        for (int t = 0; t < T; t += 2) {
+                            const double2 w2 = *reinterpret_cast<const double2 *>(wp + t);
+                            acc[(p + t) % T].x = fma(tv.x, w2.x, acc[(p + t) % T].x);
+                            acc[(p + t) % T].y = fma(tv.y, w2.x, acc[(p + t) % T].y);
+                            if (t + 1 < T) {
+                                acc[(p + t + 1) % T].x = fma(tv.x, w2.y, acc[(p + t + 1) % T].x);
+                                acc[(p + t + 1) % T].y = fma(tv.y, w2.y, acc[(p + t + 1) % T].y);
+                            }
+                        }
                     }
                 });
+                if (m) {   // next record starts a later window step: emit the rows passed
+                    const int r = gbase + __ffs(m) - 1;
+                    const int s = reinterpret_cast<const int4 *>(recbase + r * (int)sizeof(Rec) +
+                                                                 offsetof(Rec, meta))->y;
+                    while (step < s) dispatch_phase<0, T>(phase, emit);
+                }
             }
         }
     }
@@ -455,7 +453,6 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     // flush the rest of the block
     while (Bfirst + 2 * step < R1) dispatch_phase<0, T>(phase, emit);
 
-    // cell updates inside this item (grid_sector's count)
 #pragma unroll
     for (int o = 16; o; o >>= 1) cnt_upd += __shfl_xor_sync(0xffffffffu, cnt_upd, o);
     if (lane == 0 && cnt_upd) atomicAdd(a.updates, (unsigned long long)cnt_upd);
