@@ -309,16 +309,21 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     double2 *const ptile = direct ? nullptr : a.partial + (int64_t)pd.w * kItemRows * kSS;
     // lane offsets inside a staged record: its tu column (clamped to the zero
     // slot) and its parity row of v weights
-    const int lane_wv = 32 * (q + 1);               // + (-32 * parity) per record
+    constexpr int WVROW = Rec::TP * 8;             // bytes per parity row of v weights
+    const int lane_wv = WVROW * (q + 1);           // + (-WVROW * parity) per record
 
+    // window: acc[t] holds rows B + q + 2t, B = Bfirst + 2 step. Moving the
+    // window writes acc[0] (rows B, B+1: one 512-byte run for the warp) and
+    // shifts the slots down -- a few register moves per window step instead
+    // of a per-phase code copy and its dispatch (measured: the phase
+    // dispatch cost more than the moves)
     double2 acc[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
-    int step = 0, phase = 0;   // window base B = Bfirst + 2 step; slot `phase` holds rows B + q
+    int step = 0;
     unsigned cnt_upd = 0;
 
-    auto emit = [&](auto P) {
-        constexpr int p = decltype(P)::value;
+    auto advance = [&]() {
         const int row = Bfirst + 2 * step + q;
         if (row >= R0 && row < R1 && col_ok) {
             if (direct) {
@@ -326,16 +331,17 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                 const int64_t o = (strip_base + (row - a.v_start)) * kC + c;
                 WSB_DCHECK(o >= 0 && o < a.out_elems, "item %lld o %lld", (long long)item, (long long)o);
                 if (f32)
-                    out32[o] = make_float2((float)(acc[p].x * sg), (float)(acc[p].y * sg));
+                    out32[o] = make_float2((float)(acc[0].x * sg), (float)(acc[0].y * sg));
                 else
-                    outp[o] = make_double2(acc[p].x * sg, acc[p].y * sg);
+                    outp[o] = make_double2(acc[0].x * sg, acc[0].y * sg);
             } else {
-                ptile[(row - R0) * kSS + wc] = acc[p];
+                ptile[(row - R0) * kSS + wc] = acc[0];
             }
         }
-        acc[p] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t + 1 < T; ++t) acc[t] = acc[t + 1];
+        acc[T - 1] = make_double2(0.0, 0.0);
         ++step;
-        phase = (p + 1 == T) ? 0 : p + 1;
     };
 
     // gather: thread pair (2r, 2r+1) copies record r's two 16-byte halves
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                     st.wv[1][t] = (2 * t < W) ? wgt[min(2 * t, W - 1)] : 0.0;
                     st.wv[2][t] = (2 * t + 1 < W) ? wgt[min(2 * t + 1, W - 1)] : 0.0;
                 }
-                st.meta = make_int4(ib - col0, rel >> 1, -32 * (rel & 1), mask);
+                st.meta = make_int4(ib - col0, rel >> 1, -WVROW * (rel & 1), mask);
                 // cell updates inside this item (grid_sector's count)
                 const int r_lo = max(R0 - jb, 0), r_hi = min(R1 - jb, W) - 1;
                 const uint32_t vin = r_hi >= r_lo ? vm & (((2u << r_hi) - 1u) & ~((1u << r_lo) - 1u)) : 0u;
@@ -413,45 +419,33 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
 #pragma unroll 1
         for (int g = 0; g < kChunk / 32; ++g) {
             uint32_t m = sm.touch[g][warp];
-            const int gbase = g * 32;
+            const unsigned char *gb = recbase + g * 32 * (int)sizeof(Rec);
+#pragma unroll 1
             while (m) {
-                dispatch_phase<0, T>(phase, [&](auto P) {
-                    constexpr int p = decltype(P)::value;
-                    while (m) {
-                        const int r = gbase + __ffs(m) - 1;
-                        const unsigned char *rp = recbase + r * (int)sizeof(Rec);
-                        const int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
-                        if (mt.y != step) return;          // the window moves first
-                        m &= m - 1;
-                        int k = wc - mt.x;
-                        k = (unsigned)k < (unsigned)W ? k : W;
-                        const double2 tv = *reinterpret_cast<const double2 *>(rp + 16 * k);
-                        const double *wp = reinterpret_cast<const double *>(
-                            rp + offsetof(Rec, wv) + lane_wv + mt.z);
+                const unsigned char *rp = gb + (__ffs(m) - 1) * (int)sizeof(Rec);
+                m &= m - 1;
+                const int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
+                while (step < mt.y) advance();       // rows above the record are final
+                int k = wc - mt.x;
+                k = (unsigned)k < (unsigned)W ? k : W;
+                const double2 tv = *reinterpret_cast<const double2 *>(rp + 16 * k);
+                const double *wp = reinterpret_cast<const double *>(rp + offsetof(Rec, wv) + lane_wv + mt.z);
 #pragma unroll
-                        for (int t = 0; t < T; t += 2) {
-                            const double2 w2 = *reinterpret_cast<const double2 *>(wp + t);
-                            acc[(p + t) % T].x = fma(tv.x, w2.x, acc[(p + t) % T].x);
-                            acc[(p + t) % T].y = fma(tv.y, w2.x, acc[(p + t) % T].y);
-                            if (t + 1 < T) {
-                                acc[(p + t + 1) % T].x = fma(tv.x, w2.y, acc[(p + t + 1) % T].x);
-                                acc[(p + t + 1) % T].y = fma(tv.y, w2.y, acc[(p + t + 1) % T].y);
-                            }
-                        }
+                for (int t = 0; t < T; t += 2) {
+                    const double2 w2 = *reinterpret_cast<const double2 *>(wp + t);
+                    acc[t].x = fma(tv.x, w2.x, acc[t].x);
+                    acc[t].y = fma(tv.y, w2.x, acc[t].y);
+                    if (t + 1 < T) {
+                        acc[t + 1].x = fma(tv.x, w2.y, acc[t + 1].x);
+                        acc[t + 1].y = fma(tv.y, w2.y, acc[t + 1].y);
                     }
-                });
-                if (m) {   // next record starts a later window step: emit the rows passed
-                    const int r = gbase + __ffs(m) - 1;
-                    const int s = reinterpret_cast<const int4 *>(recbase + r * (int)sizeof(Rec) +
-                                                                 offsetof(Rec, meta))->y;
-                    while (step < s) dispatch_phase<0, T>(phase, emit);
                 }
             }
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     // flush the rest of the block
-    while (Bfirst + 2 * step < R1) dispatch_phase<0, T>(phase, emit);
+    while (Bfirst + 2 * step < R1) advance();
 
 #pragma unroll
     for (int o = 16; o; o >>= 1) cnt_upd += __shfl_xor_sync(0xffffffffu, cnt_upd, o);
