@@ -423,22 +423,36 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
 #pragma unroll 1
             while (m) {
                 const unsigned char *rp = gb + (__ffs(m) - 1) * (int)sizeof(Rec);
-                m &= m - 1;
-                const int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
-                while (step < mt.y) advance();       // rows above the record are final
-                int k = wc - mt.x;
-                k = (unsigned)k < (unsigned)W ? k : W;
-                const double2 tv = *reinterpret_cast<const double2 *>(rp + 16 * k);
-                const double *wp = reinterpret_cast<const double *>(rp + offsetof(Rec, wv) + lane_wv + mt.z);
+                int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
+                // rows above the record are final (the register shift stays out
+                // of the per-record loop below: no accumulator copies there)
+                if (step < mt.y) {
+                    do advance();
+                    while (step < mt.y);
+                }
+                // this record and the following ones of the same window step
+#pragma unroll 1
+                for (;;) {
+                    m &= m - 1;
+                    int k = wc - mt.x;
+                    k = (unsigned)k < (unsigned)W ? k : W;
+                    const double2 tv = *reinterpret_cast<const double2 *>(rp + 16 * k);
+                    const double *wp =
+                        reinterpret_cast<const double *>(rp + offsetof(Rec, wv) + lane_wv + mt.z);
 #pragma unroll
-                for (int t = 0; t < T; t += 2) {
-                    const double2 w2 = *reinterpret_cast<const double2 *>(wp + t);
-                    acc[t].x = fma(tv.x, w2.x, acc[t].x);
-                    acc[t].y = fma(tv.y, w2.x, acc[t].y);
-                    if (t + 1 < T) {
-                        acc[t + 1].x = fma(tv.x, w2.y, acc[t + 1].x);
-                        acc[t + 1].y = fma(tv.y, w2.y, acc[t + 1].y);
+                    for (int t = 0; t < T; t += 2) {
+                        const double2 w2 = *reinterpret_cast<const double2 *>(wp + t);
+                        acc[t].x = fma(tv.x, w2.x, acc[t].x);
+                        acc[t].y = fma(tv.y, w2.x, acc[t].y);
+                        if (t + 1 < T) {
+                            acc[t + 1].x = fma(tv.x, w2.y, acc[t + 1].x);
+                            acc[t + 1].y = fma(tv.y, w2.y, acc[t + 1].y);
+                        }
                     }
+                    if (!m) break;
+                    rp = gb + (__ffs(m) - 1) * (int)sizeof(Rec);
+                    mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
+                    if (mt.y != step) break;
                 }
             }
         }
