@@ -312,18 +312,21 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     constexpr int WVROW = Rec::TP * 8;             // bytes per parity row of v weights
     const int lane_wv = WVROW * (q + 1);           // + (-WVROW * parity) per record
 
-    // window: acc[t] holds rows B + q + 2t, B = Bfirst + 2 step. Moving the
-    // window writes acc[0] (rows B, B+1: one 512-byte run for the warp) and
-    // shifts the slots down -- a few register moves per window step instead
-    // of a per-phase code copy and its dispatch (measured: the phase
-    // dispatch cost more than the moves)
+    // window: a ring of T slots; with phase p = step mod T, slot (p + t) % T
+    // holds rows B + q + 2t, B = Bfirst + 2 step. The sweep code exists once
+    // per phase (the slot mapping is static: no register moves), and
+    // consecutive window steps fall through from one phase's copy to the
+    // next: one jump-table dispatch per T steps and per chunk, not per step.
     double2 acc[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
-    int step = 0;
+    int step = 0, phase = 0;
     unsigned cnt_upd = 0;
 
-    auto advance = [&]() {
+    // rows B, B+1 are final: write them (one 512-byte run for the warp),
+    // clear their slot, move the window down two rows
+    auto emit = [&](auto P) {
+        constexpr int p = decltype(P)::value;
         const int row = Bfirst + 2 * step + q;
         if (row >= R0 && row < R1 && col_ok) {
             if (direct) {
@@ -331,17 +334,16 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                 const int64_t o = (strip_base + (row - a.v_start)) * kC + c;
                 WSB_DCHECK(o >= 0 && o < a.out_elems, "item %lld o %lld", (long long)item, (long long)o);
                 if (f32)
-                    out32[o] = make_float2((float)(acc[0].x * sg), (float)(acc[0].y * sg));
+                    out32[o] = make_float2((float)(acc[p].x * sg), (float)(acc[p].y * sg));
                 else
-                    outp[o] = make_double2(acc[0].x * sg, acc[0].y * sg);
+                    outp[o] = make_double2(acc[p].x * sg, acc[p].y * sg);
             } else {
-                ptile[(row - R0) * kSS + wc] = acc[0];
+                ptile[(row - R0) * kSS + wc] = acc[p];
             }
         }
-#pragma unroll
-        for (int t = 0; t + 1 < T; ++t) acc[t] = acc[t + 1];
-        acc[T - 1] = make_double2(0.0, 0.0);
+        acc[p] = make_double2(0.0, 0.0);
         ++step;
+        phase = (p + 1 == T) ? 0 : p + 1;
     };
 
     // gather: thread pair (2r, 2r+1) copies record r's two 16-byte halves
@@ -416,24 +418,30 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         }
         __syncthreads();   // stage complete
         // ---- sweep: this warp's strip, records in order ---------------------
-#pragma unroll 1
-        for (int g = 0; g < kChunk / 32; ++g) {
-            uint32_t m = sm.touch[g][warp];
-            const unsigned char *gb = recbase + g * 32 * (int)sizeof(Rec);
-#pragma unroll 1
-            while (m) {
-                const unsigned char *rp = gb + (__ffs(m) - 1) * (int)sizeof(Rec);
-                int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
-                // rows above the record are final (the register shift stays out
-                // of the per-record loop below: no accumulator copies there)
-                if (step < mt.y) {
-                    do advance();
-                    while (step < mt.y);
+        {
+            // records of this chunk touching the strip: bit r of mk[r / 32]
+            uint32_t mk0 = sm.touch[0][warp], mk1 = sm.touch[1][warp];
+            // next record (or none); its staged data and window step
+            auto next_rec = [&](const unsigned char *&rp) -> int {
+                if (mk0) {
+                    rp = recbase + (__ffs(mk0) - 1) * (int)sizeof(Rec);
+                    mk0 &= mk0 - 1;
+                } else if (mk1) {
+                    rp = recbase + (31 + __ffs(mk1)) * (int)sizeof(Rec);
+                    mk1 &= mk1 - 1;
+                } else {
+                    return -1;
                 }
-                // this record and the following ones of the same window step
-#pragma unroll 1
-                for (;;) {
-                    m &= m - 1;
+                return reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta))->y;
+            };
+            const unsigned char *rp = nullptr;
+            int rs = next_rec(rp);   // window step of the pending record, -1: chunk done
+            // phase P: apply the pending records of the current step, then (if
+            // the chunk still has records) emit the step's rows. false: chunk done
+            auto run = [&](auto P) -> bool {
+                constexpr int p = decltype(P)::value;
+                while (rs == step) {
+                    const int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
                     int k = wc - mt.x;
                     k = (unsigned)k < (unsigned)W ? k : W;
                     const double2 tv = *reinterpret_cast<const double2 *>(rp + 16 * k);
@@ -442,24 +450,40 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
 #pragma unroll
                     for (int t = 0; t < T; t += 2) {
                         const double2 w2 = *reinterpret_cast<const double2 *>(wp + t);
-                        acc[t].x = fma(tv.x, w2.x, acc[t].x);
-                        acc[t].y = fma(tv.y, w2.x, acc[t].y);
+                        acc[(p + t) % T].x = fma(tv.x, w2.x, acc[(p + t) % T].x);
+                        acc[(p + t) % T].y = fma(tv.y, w2.x, acc[(p + t) % T].y);
                         if (t + 1 < T) {
-                            acc[t + 1].x = fma(tv.x, w2.y, acc[t + 1].x);
-                            acc[t + 1].y = fma(tv.y, w2.y, acc[t + 1].y);
+                            acc[(p + t + 1) % T].x = fma(tv.x, w2.y, acc[(p + t + 1) % T].x);
+                            acc[(p + t + 1) % T].y = fma(tv.y, w2.y, acc[(p + t + 1) % T].y);
                         }
                     }
-                    if (!m) break;
-                    rp = gb + (__ffs(m) - 1) * (int)sizeof(Rec);
-                    mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
-                    if (mt.y != step) break;
+                    rs = next_rec(rp);
                 }
+                if (rs < 0) return false;   // the next chunk may still add to this step
+                emit(P);                     // rows above the pending record are final
+                return true;
+            };
+            for (;;) {
+                bool more = true;
+                switch (phase) {
+#define WSB_PHASE(q)                                                        \
+    case q:                                                                 \
+        if constexpr (q < T) {                                              \
+            if (!(more = run(std::integral_constant<int, q>{}))) break;     \
+        }                                                                   \
+        [[fallthrough]];
+                    WSB_PHASE(0) WSB_PHASE(1) WSB_PHASE(2) WSB_PHASE(3)
+                    WSB_PHASE(4) WSB_PHASE(5) WSB_PHASE(6) WSB_PHASE(7)
+#undef WSB_PHASE
+                    default: break;
+                }
+                if (!more) break;
             }
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     // flush the rest of the block
-    while (Bfirst + 2 * step < R1) advance();
+    while (Bfirst + 2 * step < R1) dispatch_phase<0, T>(phase, emit);
 
 #pragma unroll
     for (int o = 16; o; o >>= 1) cnt_upd += __shfl_xor_sync(0xffffffffu, cnt_upd, o);
