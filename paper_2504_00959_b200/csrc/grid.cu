@@ -419,29 +419,26 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         __syncthreads();   // stage complete
         // ---- sweep: this warp's strip, records in order ---------------------
         {
-            // records of this chunk touching the strip: bit r of mk[r / 32]
-            uint32_t mk0 = sm.touch[0][warp], mk1 = sm.touch[1][warp];
-            // next record (or none); its staged data and window step
-            auto next_rec = [&](const unsigned char *&rp) -> int {
-                if (mk0) {
-                    rp = recbase + (__ffs(mk0) - 1) * (int)sizeof(Rec);
-                    mk0 &= mk0 - 1;
-                } else if (mk1) {
-                    rp = recbase + (31 + __ffs(mk1)) * (int)sizeof(Rec);
-                    mk1 &= mk1 - 1;
-                } else {
-                    return -1;
-                }
-                return reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta))->y;
+            // records of this chunk touching the strip, in order: bit r of mk.
+            // Fetching the next one is branch-free (an empty mask yields step
+            // -1 from a valid dummy address): the loops stay warp-uniform
+            // without reconvergence blocks.
+            uint64_t mk = (uint64_t)sm.touch[0][warp] | ((uint64_t)sm.touch[1][warp] << 32);
+            const unsigned char *rp;
+            int4 mt;
+            auto next_rec = [&]() {
+                const int b = __ffsll((long long)mk) - 1;
+                rp = recbase + max(b, 0) * (int)sizeof(Rec);
+                mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
+                mt.y = b >= 0 ? mt.y : -1;
+                mk &= mk - 1;
             };
-            const unsigned char *rp = nullptr;
-            int rs = next_rec(rp);   // window step of the pending record, -1: chunk done
+            next_rec();
             // phase P: apply the pending records of the current step, then (if
             // the chunk still has records) emit the step's rows. false: chunk done
             auto run = [&](auto P) -> bool {
                 constexpr int p = decltype(P)::value;
-                while (rs == step) {
-                    const int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
+                while (mt.y == step) {
                     int k = wc - mt.x;
                     k = (unsigned)k < (unsigned)W ? k : W;
                     const double2 tv = *reinterpret_cast<const double2 *>(rp + 16 * k);
@@ -457,10 +454,10 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                             acc[(p + t + 1) % T].y = fma(tv.y, w2.y, acc[(p + t + 1) % T].y);
                         }
                     }
-                    rs = next_rec(rp);
+                    next_rec();
                 }
-                if (rs < 0) return false;   // the next chunk may still add to this step
-                emit(P);                     // rows above the pending record are final
+                if (mt.y < 0) return false;  // the next chunk may still add to this step
+                emit(P);                      // rows above the pending record are final
                 return true;
             };
             for (;;) {
