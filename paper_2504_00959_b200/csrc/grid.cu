@@ -202,12 +202,13 @@ struct StagedRec {
 template <int KIND, int S>
 struct Shm {
     static constexpr int NROW = kItemRows + 2 * S;   // anchor rows that reach the item
-    StagedRec<S> rec[kChunk];
+    StagedRec<S> rec[kChunk + 1];   // + a sentinel (window step -1) ending every list
     double4 raw[kRaw][kChunk];      // gathered records (gu, gv, Re, Im)
     uint32_t sorted[kPartCap];      // record indices of the part in (anchor row, entry) order
     uint32_t cnt[NROW + 1], run[NROW];
     uint16_t wcnt[kWarps][NROW];
     uint32_t touch[kChunk / 32][kWarps];   // per staging warp: ballot of records touching strip w
+    uint8_t list[kWarps][kChunk + 4];      // per strip: the chunk's records touching it, in order
 };
 
 template <int KIND, int S>
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     for (int ch = 0; ch < kRaw - 1; ++ch) fetch(ch);
 
     const unsigned char *const recbase = reinterpret_cast<const unsigned char *>(&sm.rec[0]);
+    if (tid == 0) sm.rec[kChunk].meta = make_int4(0, -1, 0, 0);   // list sentinel
     for (int ch = 0; ch < nchunks; ++ch) {
         asm volatile("cp.async.wait_group %0;\n" ::"n"(kRaw - 2) : "memory");
         __syncthreads();   // raw[ch] landed for every thread; the previous sweep is done
@@ -419,19 +421,23 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         __syncthreads();   // stage complete
         // ---- sweep: this warp's strip, records in order ---------------------
         {
-            // records of this chunk touching the strip, in order: bit r of mk.
-            // Fetching the next one is branch-free (an empty mask yields step
-            // -1 from a valid dummy address): the loops stay warp-uniform
-            // without reconvergence blocks.
-            uint64_t mk = (uint64_t)sm.touch[0][warp] | ((uint64_t)sm.touch[1][warp] << 32);
+            // records of this chunk touching the strip, in order, as a byte list
+            // ending at the sentinel record (window step -1): fetching the next
+            // record is one shared load, no bit scans and no bounds test
+            {
+                const uint32_t m0 = sm.touch[0][warp], m1 = sm.touch[1][warp];
+                const uint32_t lt = (1u << lane) - 1u;
+                if ((m0 >> lane) & 1) sm.list[warp][__popc(m0 & lt)] = (uint8_t)lane;
+                if ((m1 >> lane) & 1) sm.list[warp][__popc(m0) + __popc(m1 & lt)] = (uint8_t)(32 + lane);
+                if (lane == 0) sm.list[warp][__popc(m0) + __popc(m1)] = (uint8_t)kChunk;
+                __syncwarp();
+            }
+            const uint8_t *lp = sm.list[warp];
             const unsigned char *rp;
             int4 mt;
             auto next_rec = [&]() {
-                const int b = __ffsll((long long)mk) - 1;
-                rp = recbase + max(b, 0) * (int)sizeof(Rec);
+                rp = recbase + (int)(*lp++) * (int)sizeof(Rec);
                 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
-                mt.y = b >= 0 ? mt.y : -1;
-                mk &= mk - 1;
             };
             next_rec();
             // phase P: apply the pending records of the current step, then (if
