@@ -20,8 +20,8 @@ namespace wsb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kPer = 8;                    // consecutive records per thread
-constexpr int kTile = kThreads * kPer;     // 2048 records per block
+constexpr int kPer = 4;                    // consecutive records per thread
+constexpr int kTile = kThreads * kPer;     // 1024 records per block
 
 enum : int { kErrUV = 1, kErrW = 2, kErrWeight = 4, kErrTime = 8 };
 
@@ -103,61 +103,146 @@ struct KeysArgs {
 
 constexpr unsigned long long kAgg = 1ull << 32, kInc = 2ull << 32;
 
-// exclusive prefix of this block's entry count over all earlier blocks
-// (decoupled look-back; blocks take their index from a ticket, so every
-// earlier block is already running)
+// Exclusive prefix of this block's entry count over all earlier blocks:
+// decoupled look-back, 32 predecessors per step (warp 0). Blocks take their
+// index from a ticket, so every earlier block is already running and will
+// publish.
 __device__ uint32_t lookback(unsigned long long *state, uint32_t bid, uint32_t agg) {
     volatile unsigned long long *st = state;
+    const int lane = threadIdx.x & 31;
     if (bid == 0) {
-        __threadfence();
-        st[0] = kInc | agg;
+        if (lane == 0) st[0] = kInc | agg;
         return 0;
     }
-    st[bid] = kAgg | agg;
+    if (lane == 0) st[bid] = kAgg | agg;
     uint32_t prefix = 0;
     int64_t j = (int64_t)bid - 1;
     while (true) {
-        const unsigned long long s = st[j];
+        const int64_t at = j - lane;
+        const unsigned long long s = at >= 0 ? st[at] : (unsigned long long)(2ull << 32);
         const unsigned long long f = s & ~0xFFFFFFFFull;
-        if (f == 0) continue;
-        prefix += (uint32_t)s;
-        if (f == kInc) break;
-        --j;
+        if (__any_sync(0xffffffffu, f == 0)) continue;          // a predecessor has not published
+        const uint32_t inc = __ballot_sync(0xffffffffu, f == kInc);
+        const int last = inc ? __ffs(inc) - 1 : 31;              // nearest inclusive prefix
+        uint32_t v = lane <= last ? (uint32_t)s : 0u;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        prefix += v;
+        if (inc) break;
+        j -= 32;
     }
-    __threadfence();
-    st[bid] = kInc | (prefix + agg);
+    if (lane == 0) {
+        __threadfence();
+        st[bid] = kInc | (prefix + agg);
+    }
     return prefix;
 }
 
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// 1D bulk copy global -> shared (TMA, completion on an mbarrier)
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+template <bool FROM_INPUT>
+struct KeysSmem {
+    static constexpr int N = kTile;
+    // FROM_INPUT: u, v, w, vis, weight in; rec out. Else: rec, plane in.
+    double4 rec[N];
+    double u[FROM_INPUT ? N : 1], v[FROM_INPUT ? N : 1], w[FROM_INPUT ? N : 1];
+    float2 vis[FROM_INPUT ? N : 1];
+    float wt[FROM_INPUT ? N : 1];
+    uint32_t plane[FROM_INPUT ? 1 : N];
+    uint64_t bar;
+    uint32_t bid, prefix, wsum[kThreads / 32];
+    int err;
+};
+
+// One pass over a tile of kTile records: TMA bulk loads of the columns (or
+// of the prepared records), prepare_chunk fused in, the tile's entries
+// compacted in record order at the offset the look-back gives, prepared
+// records written back by one bulk store.
 template <bool FROM_INPUT>
 __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
-    __shared__ uint32_t s_bid, s_prefix, s_wsum[kThreads / 32];
-    __shared__ int s_err;
+    using Sm = KeysSmem<FROM_INPUT>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Sm &sm = *reinterpret_cast<Sm *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
-        s_bid = atomicAdd(a.ticket, 1u);
-        s_err = 0;
+        sm.bid = atomicAdd(a.ticket, 1u);
+        sm.err = 0;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(&sm.bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    const uint32_t bid = s_bid;
-    const int64_t first = (int64_t)bid * kTile + (int64_t)tid * kPer;
+    const uint32_t bid = sm.bid;
+    const int64_t base = (int64_t)bid * kTile;
+    const int cnt_tile = (int)min((int64_t)kTile, a.n - base);
+    const bool full = cnt_tile == kTile;
+    // ---- tile in: bulk copies (full tiles) or plain loads (the last one) ----
+    if (full) {
+        if (tid == 0) {
+            const uint32_t bytes = FROM_INPUT ? kTile * (3 * 8 + 8 + 4) : kTile * (32 + 4);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(&sm.bar)),
+                         "r"(bytes)
+                         : "memory");
+            if constexpr (FROM_INPUT) {
+                bulk_load(sm.u, a.u + base, kTile * 8, &sm.bar);
+                bulk_load(sm.v, a.v + base, kTile * 8, &sm.bar);
+                bulk_load(sm.w, a.w + base, kTile * 8, &sm.bar);
+                bulk_load(sm.vis, a.vis + base, kTile * 8, &sm.bar);
+                bulk_load(sm.wt, a.wt + base, kTile * 4, &sm.bar);
+            } else {
+                bulk_load(sm.rec, a.rec + base, kTile * 32, &sm.bar);
+                bulk_load(sm.plane, a.plane + base, kTile * 4, &sm.bar);
+            }
+        }
+        asm volatile(
+            "{\n .reg .pred p;\n WAIT_%=:\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+            " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(&sm.bar))
+            : "memory");
+    } else {
+        for (int i = tid; i < cnt_tile; i += kThreads) {
+            if constexpr (FROM_INPUT) {
+                sm.u[i] = a.u[base + i];
+                sm.v[i] = a.v[base + i];
+                sm.w[i] = a.w[base + i];
+                sm.vis[i] = a.vis[base + i];
+                sm.wt[i] = a.wt[base + i];
+            } else {
+                sm.rec[i] = a.rec[base + i];
+                sm.plane[i] = a.plane[base + i];
+            }
+        }
+        __syncthreads();
+    }
+    // ---- per thread: kPer consecutive records --------------------------------
     uint32_t keys[kPer][4];
     int cnt[kPer];
     uint32_t mine = 0;
     int e = 0;
 #pragma unroll
     for (int r = 0; r < kPer; ++r) {
-        const int64_t i = first + r;
+        const int li = tid * kPer + r;
         cnt[r] = 0;
-        if (i >= a.n) continue;
+        if (li >= cnt_tile) continue;
         double gu, gv;
         uint32_t pl;
         if constexpr (FROM_INPUT) {
-            const double uu = a.u[i], vv = a.v[i], ww = a.w[i];
-            const float wt = a.wt[i];
-            const float2 vs = a.vis[i];
+            const int64_t i = base + li;
+            const double uu = sm.u[li], vv = sm.v[li], ww = sm.w[li];
+            const float wt = sm.wt[li];
+            const float2 vs = sm.vis[li];
             e |= check_record(uu, vv, ww, wt);
-            if (a.tidx && i + 1 < a.n && a.tidx[i] > a.tidx[i + 1]) e |= kErrTime;
+            if (a.tidx && i + 1 < a.n && __ldg(&a.tidx[i]) > __ldg(&a.tidx[i + 1])) e |= kErrTime;
             gu = __dmul_rn(uu, (double)a.g.n_u);
             gv = __dmul_rn(vv, (double)a.g.n_v);
             pl = plane_of_w(ww, a.g.n_w);
@@ -166,18 +251,23 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
             const double ar = vs.x, ai = vs.y, br = wt;
             const double re = __dadd_rn(0.0, __dadd_rn(-0.0, __dsub_rn(__dmul_rn(ar, br), __dmul_rn(ai, 0.0))));
             const double im = __dadd_rn(0.0, __dadd_rn(-0.0, __dadd_rn(__dmul_rn(ar, 0.0), __dmul_rn(ai, br))));
-            a.rec[i] = make_double4(gu, gv, re, im);
+            sm.rec[li] = make_double4(gu, gv, re, im);
             if (a.plane) a.plane[i] = pl;
         } else {
-            const double4 rc = a.rec[i];
+            const double4 rc = sm.rec[li];
             gu = rc.x;
             gv = rc.y;
-            pl = a.plane[i];
+            pl = sm.plane[li];
         }
         cnt[r] = record_entries(gu, gv, pl, a.g, keys[r]);
         mine += cnt[r];
     }
-    if (FROM_INPUT && e) atomicOr(&s_err, e);
+    if (FROM_INPUT && e) atomicOr(&sm.err, e);
+    // prepared records out: one bulk store of the tile (generic-proxy writes
+    // fenced for the async proxy first)
+    if constexpr (FROM_INPUT) {
+        if (full) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
     // block exclusive scan of the per-thread entry counts (record order)
     uint32_t incl = mine;
 #pragma unroll
@@ -185,31 +275,50 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
     }
-    if (lane == 31) s_wsum[warp] = incl;
+    if (lane == 31) sm.wsum[warp] = incl;
     __syncthreads();
-    uint32_t base = 0, agg = 0;
+    uint32_t wbase = 0, agg = 0;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) {
-        const uint32_t s = s_wsum[w];
-        if (w < warp) base += s;
+        const uint32_t s = sm.wsum[w];
+        if (w < warp) wbase += s;
         agg += s;
     }
-    if (tid == 0) {
-        s_prefix = lookback(a.state, bid, agg);
-        if ((int64_t)(bid + 1) * kTile >= a.n) *a.total = s_prefix + agg;   // the last block
-        if (FROM_INPUT && s_err) atomicOr(a.err, s_err);
+    if constexpr (FROM_INPUT) {
+        if (tid == 0) {
+            if (full) {
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(a.rec + base),
+                             "r"(smem_addr(sm.rec)), "r"(kTile * 32)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+            }
+        }
+        if (!full)
+            for (int i = tid; i < cnt_tile; i += kThreads) a.rec[base + i] = sm.rec[i];
+    }
+    if (warp == 0) {
+        const uint32_t pre = lookback(a.state, bid, agg);
+        if (lane == 0) {
+            sm.prefix = pre;
+            if (base + kTile >= a.n) *a.total = pre + agg;   // the last block
+            if (FROM_INPUT && sm.err) atomicOr(a.err, sm.err);
+        }
     }
     __syncthreads();
-    uint32_t pos = s_prefix + base + incl - mine;
+    uint32_t pos = sm.prefix + wbase + incl - mine;
     const uint32_t imask = (1u << a.g.item_bits) - 1u;
 #pragma unroll
     for (int r = 0; r < kPer; ++r)
         for (int t = 0; t < cnt[r]; ++t) {
             a.keys[pos] = keys[r][t];
-            a.idx[pos] = (uint32_t)(first + r);
+            a.idx[pos] = (uint32_t)(base + tid * kPer + r);
             atomicAdd(&a.item_cnt[keys[r][t] & imask], 1u);
             ++pos;
         }
+    if constexpr (FROM_INPUT) {
+        // the bulk store reads the tile from shared memory: keep it until then
+        if (tid == 0 && full) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
 }
 
 }  // namespace
@@ -270,10 +379,15 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     a.total = total;
     a.err = err;
     if (m > 0) {
-        if (in)
-            k_keys<true><<<nb, kThreads, 0, ctx->stream>>>(a);
-        else
-            k_keys<false><<<nb, kThreads, 0, ctx->stream>>>(a);
+        if (in) {
+            const int sm = (int)sizeof(KeysSmem<true>);
+            WSB_CUDA_TRY(cudaFuncSetAttribute(k_keys<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+            k_keys<true><<<nb, kThreads, sm, ctx->stream>>>(a);
+        } else {
+            const int sm = (int)sizeof(KeysSmem<false>);
+            WSB_CUDA_TRY(cudaFuncSetAttribute(k_keys<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+            k_keys<false><<<nb, kThreads, sm, ctx->stream>>>(a);
+        }
         ctx->launches += 1;
         WSB_CUDA_TRY(cudaGetLastError());
     }
