@@ -95,47 +95,45 @@ struct KeysArgs {
     KeyGeom g;
     uint32_t *keys, *idx;       // entries in record order
     uint32_t *item_cnt;         // [n_items] histogram
-    unsigned long long *state;  // [n_blocks] look-back: flag << 32 | value
-    uint32_t *ticket;           // dynamic block order
-    uint32_t *total;            // entries in all
+    const uint32_t *block_off;  // [n_blocks] first entry of each tile (k_count + scan)
     int *err;
 };
 
-constexpr unsigned long long kAgg = 1ull << 32, kInc = 2ull << 32;
-
-// Exclusive prefix of this block's entry count over all earlier blocks:
-// decoupled look-back, 32 predecessors per step (warp 0). Blocks take their
-// index from a ticket, so every earlier block is already running and will
-// publish.
-__device__ uint32_t lookback(unsigned long long *state, uint32_t bid, uint32_t agg) {
-    volatile unsigned long long *st = state;
-    const int lane = threadIdx.x & 31;
-    if (bid == 0) {
-        if (lane == 0) st[0] = kInc | agg;
-        return 0;
-    }
-    if (lane == 0) st[bid] = kAgg | agg;
-    uint32_t prefix = 0;
-    int64_t j = (int64_t)bid - 1;
-    while (true) {
-        const int64_t at = j - lane;
-        const unsigned long long s = at >= 0 ? st[at] : (unsigned long long)(2ull << 32);
-        const unsigned long long f = s & ~0xFFFFFFFFull;
-        if (__any_sync(0xffffffffu, f == 0)) continue;          // a predecessor has not published
-        const uint32_t inc = __ballot_sync(0xffffffffu, f == kInc);
-        const int last = inc ? __ffs(inc) - 1 : 31;              // nearest inclusive prefix
-        uint32_t v = lane <= last ? (uint32_t)s : 0u;
+// entries per tile (the compaction offsets of k_keys): taps depend on gu, gv
+// only, so the count pass reads 16 of the 36 bytes per record
+template <bool FROM_INPUT>
+__global__ void __launch_bounds__(kThreads) k_count(const double *__restrict__ u,
+                                                    const double *__restrict__ v,
+                                                    const double4 *__restrict__ rec, int64_t n,
+                                                    KeyGeom g, uint32_t *__restrict__ block_cnt) {
+    __shared__ uint32_t wsum[kThreads / 32];
+    const int64_t base = (int64_t)blockIdx.x * kTile;
+    uint32_t mine = 0;
 #pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        prefix += v;
-        if (inc) break;
-        j -= 32;
+    for (int r = 0; r < kPer; ++r) {
+        const int64_t i = base + r * kThreads + threadIdx.x;
+        if (i >= n) continue;
+        double gu, gv;
+        if constexpr (FROM_INPUT) {
+            gu = __dmul_rn(__ldg(&u[i]), (double)g.n_u);
+            gv = __dmul_rn(__ldg(&v[i]), (double)g.n_v);
+        } else {
+            const double2 c = __ldg(reinterpret_cast<const double2 *>(rec + i));
+            gu = c.x;
+            gv = c.y;
+        }
+        uint32_t k4[4];
+        mine += record_entries(gu, gv, 0u, g, k4);
     }
-    if (lane == 0) {
-        __threadfence();
-        st[bid] = kInc | (prefix + agg);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kThreads / 32; ++w) t += wsum[w];
+        block_cnt[blockIdx.x] = t;
     }
-    return prefix;
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
@@ -155,13 +153,16 @@ template <bool FROM_INPUT>
 struct KeysSmem {
     static constexpr int N = kTile;
     // FROM_INPUT: u, v, w, vis, weight in; rec out. Else: rec, plane in.
-    double4 rec[N];
-    double u[FROM_INPUT ? N : 1], v[FROM_INPUT ? N : 1], w[FROM_INPUT ? N : 1];
-    float2 vis[FROM_INPUT ? N : 1];
-    float wt[FROM_INPUT ? N : 1];
-    uint32_t plane[FROM_INPUT ? 1 : N];
+    // (bulk-copy destinations: 16-byte aligned)
+    alignas(16) double4 rec[N];
+    alignas(16) double u[FROM_INPUT ? N : 2];
+    alignas(16) double v[FROM_INPUT ? N : 2];
+    alignas(16) double w[FROM_INPUT ? N : 2];
+    alignas(16) float2 vis[FROM_INPUT ? N : 2];
+    alignas(16) float wt[FROM_INPUT ? N : 4];
+    alignas(16) uint32_t plane[FROM_INPUT ? 4 : N];
     uint64_t bar;
-    uint32_t bid, prefix, wsum[kThreads / 32];
+    uint32_t bid, wsum[kThreads / 32];
     int err;
 };
 
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
     Sm &sm = *reinterpret_cast<Sm *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
-        sm.bid = atomicAdd(a.ticket, 1u);
+        sm.bid = blockIdx.x;
         sm.err = 0;
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(&sm.bar)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -296,16 +297,9 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
         if (!full)
             for (int i = tid; i < cnt_tile; i += kThreads) a.rec[base + i] = sm.rec[i];
     }
-    if (warp == 0) {
-        const uint32_t pre = lookback(a.state, bid, agg);
-        if (lane == 0) {
-            sm.prefix = pre;
-            if (base + kTile >= a.n) *a.total = pre + agg;   // the last block
-            if (FROM_INPUT && sm.err) atomicOr(a.err, sm.err);
-        }
-    }
-    __syncthreads();
-    uint32_t pos = sm.prefix + wbase + incl - mine;
+    if (tid == 0 && FROM_INPUT && sm.err) atomicOr(a.err, sm.err);
+    (void)agg;
+    uint32_t pos = a.block_off[bid] + wbase + incl - mine;
     const uint32_t imask = (1u << a.g.item_bits) - 1u;
 #pragma unroll
     for (int r = 0; r < kPer; ++r)
@@ -346,13 +340,13 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     WSB_TRY(ensure(ctx, kSlotTileOff, sizeof(uint32_t) * (n_items + 1), (void **)&off));
     WSB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (n_items + 1), ctx->stream));
     const int nb = std::max(1, ceil_div(m, kTile));
-    // look-back state + ticket + total + error flag in one zeroed slot
-    unsigned long long *state;
-    WSB_TRY(ensure(ctx, kSlotBlockCounts, sizeof(unsigned long long) * (nb + 4), (void **)&state));
-    WSB_CUDA_TRY(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (nb + 4), ctx->stream));
-    uint32_t *ticket = reinterpret_cast<uint32_t *>(state + nb);
-    uint32_t *total = ticket + 2;
-    int *err = reinterpret_cast<int *>(ticket + 4);
+    // tile entry counts -> offsets (+ total), error flag
+    uint32_t *bcnt, *boff;
+    WSB_TRY(ensure(ctx, kSlotBlockCounts, sizeof(uint32_t) * (nb + 8), (void **)&bcnt));
+    WSB_TRY(ensure(ctx, kSlotBlockOffsets, sizeof(uint32_t) * (nb + 8), (void **)&boff));
+    WSB_CUDA_TRY(cudaMemsetAsync(bcnt, 0, sizeof(uint32_t) * (nb + 8), ctx->stream));
+    uint32_t *total = boff + nb;       // exclusive scan over nb + 1 counts: the total
+    int *err = reinterpret_cast<int *>(bcnt + nb + 4);
     // entry buffers: at most 4 entries per record
     const size_t eb = sizeof(uint32_t) * std::max<int64_t>(1, 4 * m);
     uint32_t *ka, *kb, *ia, *ib;
@@ -374,10 +368,18 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     a.keys = ka;
     a.idx = ia;
     a.item_cnt = cnt;
-    a.state = state;
-    a.ticket = ticket;
-    a.total = total;
+    a.block_off = boff;
     a.err = err;
+    if (m > 0) {
+        if (in)
+            k_count<true><<<nb, kThreads, 0, ctx->stream>>>(in->u, in->v, nullptr, m, k, bcnt);
+        else
+            k_count<false><<<nb, kThreads, 0, ctx->stream>>>(nullptr, nullptr, (const double4 *)rec, m,
+                                                              k, bcnt);
+        ctx->launches += 1;
+        WSB_CUDA_TRY(cudaGetLastError());
+    }
+    WSB_TRY(exclusive_scan_u32(ctx, bcnt, boff, nb + 1, nullptr));
     if (m > 0) {
         if (in) {
             const int sm = (int)sizeof(KeysSmem<true>);
@@ -392,8 +394,8 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
         WSB_CUDA_TRY(cudaGetLastError());
     }
     // entry count (and, from the columns, the validation flags) to the host
-    WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host, total, 2 * sizeof(int) + 2 * sizeof(int),
-                                 cudaMemcpyDeviceToHost, ctx->stream));
+    WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host, total, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host + 2, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     const uint32_t n_entries = m > 0 ? (uint32_t)ctx->flag_host[0] : 0u;
     const int e = ctx->flag_host[2];
