@@ -55,15 +55,18 @@ __device__ __forceinline__ int record_entries(double gu, double gv, uint32_t pla
     const int anchor = (int)floor(gv) - k.S;
     const int ss0 = i0 / kSSCols, ss1 = i1 / kSSCols;
     const int rb0 = (j0 - k.v_start) / kItemRows, rb1 = (j1 - k.v_start) / kItemRows;
-    int n = 0;
-    for (int rb = rb0; rb <= rb1; ++rb) {
-        const uint32_t rowrel = (uint32_t)(anchor - (k.v_start + rb * kItemRows - 2 * k.S));
-        for (int ss = ss0; ss <= ss1; ++ss) {
-            const uint32_t item = ((uint32_t)plane * k.n_ss + ss) * (uint32_t)k.n_rb + rb;
-            keys[n++] = item | (rowrel << k.item_bits);
-        }
-    }
-    return n;
+    // entries in (row block, superstrip) order; a record spans at most two of each
+    const uint32_t rr0 = (uint32_t)(anchor - (k.v_start + rb0 * kItemRows - 2 * k.S));
+    const uint32_t it0 = ((uint32_t)plane * k.n_ss + ss0) * (uint32_t)k.n_rb + rb0;
+    const uint32_t key00 = it0 | (rr0 << k.item_bits);
+    const uint32_t dss = (uint32_t)k.n_rb;                        // next superstrip
+    const uint32_t drb = 1u - ((uint32_t)kItemRows << k.item_bits); // next row block
+    const bool two_ss = ss1 > ss0, two_rb = rb1 > rb0;
+    keys[0] = key00;
+    keys[1] = two_ss ? key00 + dss : key00 + drb;
+    keys[2] = key00 + drb;
+    keys[3] = key00 + drb + dss;
+    return (two_ss ? 2 : 1) * (two_rb ? 2 : 1);
 }
 
 __device__ __forceinline__ int check_record(double uu, double vv, double ww, float wt) {
@@ -301,14 +304,17 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
     (void)agg;
     uint32_t pos = a.block_off[bid] + wbase + incl - mine;
     const uint32_t imask = (1u << a.g.item_bits) - 1u;
+    // (static indices: the entry arrays stay in registers)
 #pragma unroll
     for (int r = 0; r < kPer; ++r)
-        for (int t = 0; t < cnt[r]; ++t) {
-            a.keys[pos] = keys[r][t];
-            a.idx[pos] = (uint32_t)(base + tid * kPer + r);
-            atomicAdd(&a.item_cnt[keys[r][t] & imask], 1u);
-            ++pos;
-        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (t < cnt[r]) {
+                a.keys[pos] = keys[r][t];
+                a.idx[pos] = (uint32_t)(base + tid * kPer + r);
+                atomicAdd(&a.item_cnt[keys[r][t] & imask], 1u);
+                ++pos;
+            }
     if constexpr (FROM_INPUT) {
         // the bulk store reads the tile from shared memory: keep it until then
         if (tid == 0 && full) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
