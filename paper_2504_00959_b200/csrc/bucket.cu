@@ -157,7 +157,7 @@ struct KeysSmem {
     static constexpr int N = kTile;
     // FROM_INPUT: u, v, w, vis, weight in; rec out. Else: rec, plane in.
     // (bulk-copy destinations: 16-byte aligned)
-    alignas(16) double4 rec[N];
+    alignas(16) double4 rec[FROM_INPUT ? 1 : N];
     alignas(16) double u[FROM_INPUT ? N : 2];
     alignas(16) double v[FROM_INPUT ? N : 2];
     alignas(16) double w[FROM_INPUT ? N : 2];
@@ -170,9 +170,10 @@ struct KeysSmem {
 };
 
 // One pass over a tile of kTile records: TMA bulk loads of the columns (or
-// of the prepared records), prepare_chunk fused in, the tile's entries
-// compacted in record order at the offset the look-back gives, prepared
-// records written back by one bulk store.
+// of the prepared records) into shared memory, prepare_chunk fused in, the
+// tile's entries compacted in record order at the tile's offset (k_count +
+// scan). (A bulk store of the prepared tile measured no faster than each
+// thread writing its 4 consecutive records, and cost 32 KB of shared memory.)
 template <bool FROM_INPUT>
 __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
     using Sm = KeysSmem<FROM_INPUT>;
@@ -255,7 +256,8 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
             const double ar = vs.x, ai = vs.y, br = wt;
             const double re = __dadd_rn(0.0, __dadd_rn(-0.0, __dsub_rn(__dmul_rn(ar, br), __dmul_rn(ai, 0.0))));
             const double im = __dadd_rn(0.0, __dadd_rn(-0.0, __dadd_rn(__dmul_rn(ar, 0.0), __dmul_rn(ai, br))));
-            sm.rec[li] = make_double4(gu, gv, re, im);
+            // a thread's kPer consecutive records are one 128-byte line
+            a.rec[i] = make_double4(gu, gv, re, im);
             if (a.plane) a.plane[i] = pl;
         } else {
             const double4 rc = sm.rec[li];
@@ -267,11 +269,6 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
         mine += cnt[r];
     }
     if (FROM_INPUT && e) atomicOr(&sm.err, e);
-    // prepared records out: one bulk store of the tile (generic-proxy writes
-    // fenced for the async proxy first)
-    if constexpr (FROM_INPUT) {
-        if (full) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    }
     // block exclusive scan of the per-thread entry counts (record order)
     uint32_t incl = mine;
 #pragma unroll
@@ -288,18 +285,6 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
         if (w < warp) wbase += s;
         agg += s;
     }
-    if constexpr (FROM_INPUT) {
-        if (tid == 0) {
-            if (full) {
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(a.rec + base),
-                             "r"(smem_addr(sm.rec)), "r"(kTile * 32)
-                             : "memory");
-                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-            }
-        }
-        if (!full)
-            for (int i = tid; i < cnt_tile; i += kThreads) a.rec[base + i] = sm.rec[i];
-    }
     if (tid == 0 && FROM_INPUT && sm.err) atomicOr(a.err, sm.err);
     (void)agg;
     uint32_t pos = a.block_off[bid] + wbase + incl - mine;
@@ -315,10 +300,6 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
                 atomicAdd(&a.item_cnt[keys[r][t] & imask], 1u);
                 ++pos;
             }
-    if constexpr (FROM_INPUT) {
-        // the bulk store reads the tile from shared memory: keep it until then
-        if (tid == 0 && full) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-    }
 }
 
 }  // namespace
