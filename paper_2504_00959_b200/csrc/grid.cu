@@ -207,7 +207,6 @@ struct Shm {
     uint32_t sorted[kPartCap];      // record indices of the part in (anchor row, entry) order
     uint32_t cnt[NROW + 1], run[NROW];
     uint16_t wcnt[kWarps][NROW];
-    uint32_t touch[kChunk / 32][kWarps];   // per staging warp: ballot of records touching strip w
     uint8_t list[kWarps][kChunk + 4];      // per strip: the chunk's records touching it, in order
 };
 
@@ -372,51 +371,56 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         __syncthreads();   // raw[ch] landed for every thread; the previous sweep is done
         fetch(ch + kRaw - 1);
         const int nr = (int)min((uint32_t)kChunk, n - (uint32_t)ch * kChunk);
-        // ---- stage: warps 0-1, one record per thread (no divergence) --------
-        if (tid < kChunk) {
-            const int r = tid;
-            int mask = 0;
+        // ---- stage: thread pair per record, thread (2r + a) does axis a of
+        // record r. Both axes run the same weight code (one instruction stream
+        // for the warp), only the short tails differ; all 4 warps stage.
+        {
+            const int r = tid >> 1, ax = tid & 1;
+            unsigned mine = 0;      // taps of this axis inside the item
             if (r < nr) {
                 const double4 rc = sm.raw[ch % kRaw][r];
                 Rec &st = sm.rec[r];
                 double wgt[W];
-                // u axis: value * weight per window column
-                const int ib = (int)floor(rc.x) - S;
-                const uint32_t um = axis_weights<KIND, S>(rc.x, ib, kp, i0b, wgt);
+                const double g = ax ? rc.y : rc.x;
+                const int i0 = (int)floor(g) - S;
+                const uint32_t wm = axis_weights<KIND, S>(g, i0, kp, i0b, wgt);
+                if (ax == 0) {
+                    // u axis: value * weight per window column
 #pragma unroll
-                for (int k = 0; k < W; ++k)
-                    st.tu[k] = make_double2(__dmul_rn(rc.z, wgt[k]), __dmul_rn(rc.w, wgt[k]));
-                st.tu[W] = make_double2(0.0, 0.0);
-                // tap columns inside the superstrip (and the mesh); the strips they touch
-                const int k_lo = max(col0 - ib, 0), k_hi = min(min(col0 + kSS, a.n_u) - ib, W) - 1;
-                uint32_t uin = k_hi >= k_lo ? um & (((2u << k_hi) - 1u) & ~((1u << k_lo) - 1u)) : 0u;
-                if (uin) {
-                    const int w_lo = (ib + __ffs(uin) - 1 - col0) / kC;
-                    const int w_hi = (ib + 31 - __clz(uin) - col0) / kC;
-                    mask = ((2 << w_hi) - 1) & ~((1 << w_lo) - 1);
+                    for (int k = 0; k < W; ++k)
+                        st.tu[k] = make_double2(__dmul_rn(rc.z, wgt[k]), __dmul_rn(rc.w, wgt[k]));
+                    st.tu[W] = make_double2(0.0, 0.0);
+                    // tap columns inside the superstrip (and the mesh); the strips they touch
+                    const int k_lo = max(col0 - i0, 0), k_hi = min(min(col0 + kSS, a.n_u) - i0, W) - 1;
+                    const uint32_t uin = k_hi >= k_lo ? wm & (((2u << k_hi) - 1u) & ~((1u << k_lo) - 1u)) : 0u;
+                    int mask = 0;
+                    if (uin) {
+                        const int w_lo = (i0 + __ffs(uin) - 1 - col0) / kC;
+                        const int w_hi = (i0 + 31 - __clz(uin) - col0) / kC;
+                        mask = ((2 << w_hi) - 1) & ~((1 << w_lo) - 1);
+                    }
+                    st.meta.x = i0 - col0;
+                    st.meta.w = mask;
+                    mine = __popc(uin);
+                } else {
+                    // v axis: parity-split row weights
+                    const int rel = i0 - Bfirst;
+                    WSB_DCHECK(rel >= 0 && rel < NROW, "item %lld rel %d", (long long)item, rel);
+#pragma unroll
+                    for (int t = 0; t < Rec::TP; ++t) {
+                        st.wv[0][t] = (2 * t - 1 >= 0 && 2 * t - 1 < W) ? wgt[max(2 * t - 1, 0)] : 0.0;
+                        st.wv[1][t] = (2 * t < W) ? wgt[min(2 * t, W - 1)] : 0.0;
+                        st.wv[2][t] = (2 * t + 1 < W) ? wgt[min(2 * t + 1, W - 1)] : 0.0;
+                    }
+                    st.meta.y = rel >> 1;
+                    st.meta.z = -WVROW * (rel & 1);
+                    const int r_lo = max(R0 - i0, 0), r_hi = min(R1 - i0, W) - 1;
+                    mine = __popc(r_hi >= r_lo ? wm & (((2u << r_hi) - 1u) & ~((1u << r_lo) - 1u)) : 0u);
                 }
-                // v axis: parity-split row weights
-                const int jb = (int)floor(rc.y) - S;
-                const uint32_t vm = axis_weights<KIND, S>(rc.y, jb, kp, i0b, wgt);
-                const int rel = jb - Bfirst;
-                WSB_DCHECK(rel >= 0 && rel < NROW, "item %lld rel %d", (long long)item, rel);
-#pragma unroll
-                for (int t = 0; t < Rec::TP; ++t) {
-                    st.wv[0][t] = (2 * t - 1 >= 0 && 2 * t - 1 < W) ? wgt[max(2 * t - 1, 0)] : 0.0;
-                    st.wv[1][t] = (2 * t < W) ? wgt[min(2 * t, W - 1)] : 0.0;
-                    st.wv[2][t] = (2 * t + 1 < W) ? wgt[min(2 * t + 1, W - 1)] : 0.0;
-                }
-                st.meta = make_int4(ib - col0, rel >> 1, -WVROW * (rel & 1), mask);
-                // cell updates inside this item (grid_sector's count)
-                const int r_lo = max(R0 - jb, 0), r_hi = min(R1 - jb, W) - 1;
-                const uint32_t vin = r_hi >= r_lo ? vm & (((2u << r_hi) - 1u) & ~((1u << r_lo) - 1u)) : 0u;
-                cnt_upd += __popc(uin) * __popc(vin);
             }
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                const uint32_t b = __ballot_sync(0xffffffffu, (mask >> w) & 1);
-                if (lane == 0) sm.touch[warp][w] = b;
-            }
+            // cell updates inside this item (grid_sector's count): u taps x v taps
+            const unsigned other = __shfl_xor_sync(0xffffffffu, mine, 1);
+            if (ax == 0) cnt_upd += mine * other;
         }
         __syncthreads();   // stage complete
         // ---- sweep: this warp's strip, records in order ---------------------
@@ -425,7 +429,9 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             // ending at the sentinel record (window step -1): fetching the next
             // record is one shared load, no bit scans and no bounds test
             {
-                const uint32_t m0 = sm.touch[0][warp], m1 = sm.touch[1][warp];
+                const uint32_t m0 = __ballot_sync(0xffffffffu, lane < nr && ((sm.rec[lane].meta.w >> warp) & 1));
+                const uint32_t m1 =
+                    __ballot_sync(0xffffffffu, 32 + lane < nr && ((sm.rec[32 + lane].meta.w >> warp) & 1));
                 const uint32_t lt = (1u << lane) - 1u;
                 if ((m0 >> lane) & 1) sm.list[warp][__popc(m0 & lt)] = (uint8_t)lane;
                 if ((m1 >> lane) & 1) sm.list[warp][__popc(m0) + __popc(m1 & lt)] = (uint8_t)(32 + lane);
