@@ -17,10 +17,16 @@ exchange (pipeline.py:117-122) and has no counterpart here.
 
 Every numeric stage runs through a backend; the product backend is
 ``CudaBackend`` (libwsb.so). The collectives are torch.distributed calls,
-NCCL over NVLink on the GPU box. The result is bit-identical to the
-single-GPU image for any number of ranks: records reach each slab in gindex
-order, tiles never straddle slabs, and the norms are summed per column in
-global column order.
+NCCL over NVLink on the GPU box. In this v-slab mode (the default,
+deterministic=True) the image is bit-identical to the single-GPU image for
+any number of ranks whose slab starts lie on the gridder's 128-row item
+boundaries (partition_1d of a power-of-two mesh over 2/4/8 ranks; balanced
+starts are rounded to them): records reach each slab in gindex order, every
+cell is accumulated in (anchor row, record) order inside an item that holds
+the same records on any GPU count, and the norms are summed per column in
+global column order. The w-plane decomposition (decomposition="planes") is
+a faster mode whose image agrees to ~1e-16 relative (the plane sum
+associates differently).
 """
 
 from __future__ import annotations
@@ -208,14 +214,21 @@ class _Stages:
         return {b[0]: a[1].elapsed_time(b[1]) for a, b in zip(self.marks, self.marks[1:])}
 
 
+ITEM_ROWS = 128       # csrc/wsb_internal.cuh kItemRows: the gridder's row blocks
+
+
 def balanced_slab_starts(row_counts, n_ranks: int, row_weight: float = 10_000.0,
-                         max_rows: int | None = None):
+                         max_rows: int | None = None, align: int = ITEM_ROWS):
     """Slab rows with equal estimated work instead of partition_1d's equal
     rows. A slab's cost is modelled as records + row_weight * rows (the
     gridder scales with the records, the row pass and the sweep's row
     emission with the rows; row_weight ~ records-equivalent of one row,
     measured on cfg3). Returns starts[0..R] with starts[R] = n_v and every
-    slab at least one row. The image does not depend on the slab rows."""
+    slab at least one row. The image does not depend on the slab rows.
+    ``align``: slab starts are rounded to multiples of it when the mesh has
+    room (n_v >= align * n_ranks): slabs that start on the gridder's 128-row
+    item boundaries grid every cell exactly as one GPU does, so the image is
+    bit-identical for any rank count."""
     import numpy as np
     h = np.asarray(row_counts, dtype=np.float64)
     n_v = h.shape[0]
@@ -231,11 +244,17 @@ def balanced_slab_starts(row_counts, n_ranks: int, row_weight: float = 10_000.0,
         r = min(r, n_v - (n_ranks - d))
         starts.append(r)
     starts.append(n_v)
+    if align > 1 and n_v >= align * n_ranks and n_v % align == 0:
+        for d in range(1, n_ranks):
+            a_ = int(round(starts[d] / align)) * align
+            starts[d] = min(max(a_, starts[d - 1] + align), n_v - (n_ranks - d) * align)
     # memory bound: no slab taller than max_rows (default 1.5x the equal share;
     # the slab's grid and transforms scale with its rows)
     if max_rows is None:
         max_rows = -(-3 * n_v // (2 * n_ranks))
     max_rows = max(max_rows, -(-n_v // n_ranks))
+    step = align if (align > 1 and n_v >= align * n_ranks and n_v % align == 0) else 1
+    max_rows = max(step, max_rows // step * step)
     for d in range(1, n_ranks):
         starts[d] = min(starts[d], starts[d - 1] + max_rows)
     for d in range(n_ranks - 1, 0, -1):
@@ -350,7 +369,8 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
                       to_host: bool = True, n_ranges: int = 4, timings: dict | None = None,
                       balance: bool = True, row_weight: float = 10_000.0,
                       transpose: str = "auto", exchange: str = "auto",
-                      decomposition: str = "auto", plane_weight: float | None = None):
+                      decomposition: str = "auto", plane_weight: float | None = None,
+                      deterministic: bool = True):
     """Dirty image of the union of every rank's records. Each rank passes its
     own time partition (records in gindex order, rank r holding the r-th
     contiguous block, as visdata.partition_time_ordered produces).
@@ -372,11 +392,15 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     ``balance`` sizes the v-slabs for equal work from a global histogram of
     the anchor rows (one all-reduce of n_v counts) instead of partition_1d's
     equal rows: Earth-rotation tracks put most records in the central rows.
-    ``decomposition``: "auto" (planes when every rank gets a plane and the
-    backend supports it; measured faster on 2 and 4 GPUs: cfg2 4.30 vs 4.93
-    ms/step, cfg3 16.9 vs 21.8 ms/step at N=4), "slabs" (the reference's
-    v-slabs, above; the image is
-    bit-identical for any R) or "planes": rank d owns a contiguous range of w
+    ``decomposition``: "auto" (v-slabs when ``deterministic``, the
+    default -- the reference's ReduceStrategy default -- else w-plane ranges
+    when every rank gets a plane), "slabs" (the reference's v-slabs, above;
+    the image is bit-identical to the single-GPU one for any R when the slab
+    starts lie on the gridder's 128-row item boundaries: partition_1d of a
+    power-of-two mesh over 2/4/8 ranks, and the balanced starts, which are
+    rounded to them) or "planes" (a performance mode, measured faster on 2
+    and 4 GPUs: cfg2 4.30 vs 4.93 ms/step, cfg3 16.9 vs 21.8 ms/step at N=4
+    in round 1): rank d owns a contiguous range of w
     planes (balanced on records per plane + ``plane_weight`` records per
     plane's transforms), grids them over the whole mesh, transforms and
     stacks them locally, and the ranks' complex partial stacks are summed by
@@ -402,7 +426,10 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     rec, plane = be.prepare(u, v, w, vis, weight, spec)
     st.mark("prepare")
     if decomposition == "auto":
-        decomposition = "planes" if (R <= spec.n_w and hasattr(be, "route_planes")) else "slabs"
+        # deterministic (the reference's ReduceStrategy default): v-slabs,
+        # bit-identical for any R; else the faster w-plane ranges
+        decomposition = ("slabs" if deterministic or R > spec.n_w or not hasattr(be, "route_planes")
+                         else "planes")
     if decomposition == "planes":
         return _image_planes(be, rec, plane, spec, kern, group, root, to_host, timings, st,
                              balance, plane_weight, exchange)

@@ -117,3 +117,20 @@ def test_balanced_slab_starts():
     # the memory cap: no slab above 1.5x the equal share by default
     st = balanced_slab_starts(h, 4, row_weight=0.0)
     assert max(b - a for a, b in zip(st, st[1:])) <= 24 and st[-1] == 64
+
+
+def test_balanced_slab_starts_align_to_gridder_items():
+    """Balanced slabs start on the gridder's 128-row item boundaries (the
+    condition for a bit-identical image across GPU counts) when the mesh has
+    room for it; memory caps and the ordering still hold."""
+    from paper_2504_00959_b200.distributed import ITEM_ROWS, balanced_slab_starts
+    rng = np.random.default_rng(3)
+    h = rng.poisson(5, 2048)
+    h[900:1100] += 5000                    # dense central rows
+    for R in (2, 3, 4, 8):
+        st = balanced_slab_starts(h, R, row_weight=100.0)
+        assert st[0] == 0 and st[-1] == 2048 and all(b > a for a, b in zip(st, st[1:]))
+        assert all(s % ITEM_ROWS == 0 for s in st), (R, st)
+    # no room (fewer than 128 rows per rank): unaligned but valid
+    st = balanced_slab_starts(h[:512], 8, row_weight=1.0)
+    assert st[0] == 0 and st[-1] == 512 and all(b > a for a, b in zip(st, st[1:]))
