@@ -331,9 +331,9 @@ int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *idx_host, uint32_t *off_host,
 
 /* Debug / parity: the gridder's bucketing (K1) of m prepared records for
  * the slab rows [v_start, v_start+v_count): entries (record, work item)
- * with key = item | rowrel << item_bits (item = (plane * ceil(n_u/64) +
- * superstrip) * ceil(v_count/128) + row block, rowrel = floor(gv) - S - (first
- * row of the block - 2S)), sorted by item, record order inside an item.
+ * with key = item << 8 | rowrel (item = (plane * ceil(n_u/64) + superstrip)
+ * * ceil(v_count/128) + row block, rowrel = floor(gv) - S - (first row of the
+ * block - 2S)), sorted by key, record order for equal keys.
  * Host buffers (nullable): keys/idx u32[n_entries] (at most 4 m), off
  * u32[n_items + 1]. Sizes returned in *n_entries / *n_items / *item_bits.
  * Synchronous. */

@@ -273,12 +273,12 @@ def tap_bounds(g, S: int, lo: int, hi: int):
 
 
 def item_entries(gu, gv, plane, n_u: int, n_w: int, S: int, v_start: int, v_count: int,
-                 ss_cols: int = 64, item_rows: int = 128):
+                 ss_cols: int = 64, item_rows: int = 128, row_bits: int = 8):
     """The GPU gridder's work-item bucketing restated (contract of
     wsb_bucket_items, include/wsb.h): every (record, item) pair whose taps
     reach item = (plane, ss_cols-column superstrip, item_rows-row block of
-    the slab), key = item | rowrel << item_bits with rowrel = floor(gv) - S -
-    (block row0 - 2S), stably sorted by item (record order inside an item).
+    the slab), key = item << row_bits | rowrel with rowrel = floor(gv) - S -
+    (block row0 - 2S), stably sorted by key (record order for equal keys).
     Tap sets are the reference's (gridder.py:164-177). Returns
     (keys u32, idx u32, off u32[n_items + 1], item_bits)."""
     gu, gv = np.asarray(gu, np.float64), np.asarray(gv, np.float64)
@@ -300,15 +300,12 @@ def item_entries(gu, gv, plane, n_u: int, n_w: int, S: int, v_start: int, v_coun
             m = ok & (ss <= i1 // ss_cols) & (rb <= (j1 - v_start) // item_rows)
             item = (plane[m] * n_ss + ss[m]) * n_rb + rb[m]
             rowrel = anchor[m] - (v_start + rb[m] * item_rows - 2 * S)
-            keys.append((item | (rowrel << item_bits)).astype(np.uint32))
+            keys.append(((item << row_bits) | rowrel).astype(np.uint32))
             idx.append(rec[m])
     keys, idx = np.concatenate(keys), np.concatenate(idx)
-    # record order, then the per-record entry order (row block, superstrip)
-    order = np.lexsort((keys & ((1 << item_bits) - 1), idx))
-    keys, idx = keys[order], idx[order]
-    srt = np.argsort(keys & ((1 << item_bits) - 1), kind="stable")
-    keys, idx = keys[srt], idx[srt].astype(np.uint32)
-    cnt = np.bincount(keys & ((1 << item_bits) - 1), minlength=n_items)
+    order = np.lexsort((idx, keys))           # by key, then record
+    keys, idx = keys[order], idx[order].astype(np.uint32)
+    cnt = np.bincount(keys >> row_bits, minlength=n_items)
     off = np.concatenate([[0], np.cumsum(cnt)]).astype(np.uint32)
     return keys, idx, off, item_bits
 

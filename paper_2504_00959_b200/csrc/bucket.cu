@@ -5,15 +5,16 @@
 // (gridder.py:160-183). The GPU gridder (grid.cu) sweeps work items
 // item = (w plane, 64-column superstrip, 128-row block of the slab), so
 // every (record, item) pair the record's taps reach becomes one entry
-//     key = item | rowrel << item_bits,   rowrel = anchor row - (R0 - 2S)
+//     key = item << 8 | rowrel,   rowrel = anchor row - (R0 - 2S) < 128 + 2S
 // (anchor row = floor(gv) - S, R0 = the block's first row), written in
-// record order by ONE pass over the records (k_keys: prepare_chunk fused in
-// when it starts from the visibility columns, entry compaction by a
-// decoupled look-back across blocks, item histogram), then stably
-// radix-sorted on the item bits only (sort.cu). Each item's entries are thus
-// a contiguous run in record (gindex) order -- independent of how skewed the
-// items are and of the GPU count; the gridder orders a run by window step
-// itself (a stable counting sort in shared memory).
+// record order (k_count: entries per tile; k_keys: prepare_chunk fused in
+// when it starts from the visibility columns, the tile's entries compacted
+// at its offset), then stably radix-sorted on the whole key (sort.cu). Each
+// item's entries are thus a contiguous run in (anchor row, record) order --
+// the per-cell accumulation order of the gridder -- independent of how
+// skewed the items are and of the GPU count. Item offsets come from the
+// boundaries of the sorted keys (no histogram atomics: Earth-rotation tracks
+// send millions of entries to single items).
 #include "wsb_internal.cuh"
 
 namespace wsb {
@@ -58,9 +59,9 @@ __device__ __forceinline__ int record_entries(double gu, double gv, uint32_t pla
     // entries in (row block, superstrip) order; a record spans at most two of each
     const uint32_t rr0 = (uint32_t)(anchor - (k.v_start + rb0 * kItemRows - 2 * k.S));
     const uint32_t it0 = ((uint32_t)plane * k.n_ss + ss0) * (uint32_t)k.n_rb + rb0;
-    const uint32_t key00 = it0 | (rr0 << k.item_bits);
-    const uint32_t dss = (uint32_t)k.n_rb;                        // next superstrip
-    const uint32_t drb = 1u - ((uint32_t)kItemRows << k.item_bits); // next row block
+    const uint32_t key00 = it0 << kRowBits | rr0;
+    const uint32_t dss = (uint32_t)k.n_rb << kRowBits;                // next superstrip
+    const uint32_t drb = (1u << kRowBits) - (uint32_t)kItemRows;      // next row block
     const bool two_ss = ss1 > ss0, two_rb = rb1 > rb0;
     keys[0] = key00;
     keys[1] = two_ss ? key00 + dss : key00 + drb;
@@ -97,7 +98,6 @@ struct KeysArgs {
     int64_t n;
     KeyGeom g;
     uint32_t *keys, *idx;       // entries in record order
-    uint32_t *item_cnt;         // [n_items] histogram
     const uint32_t *block_off;  // [n_blocks] first entry of each tile (k_count + scan)
     int *err;
 };
@@ -288,7 +288,6 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
     if (tid == 0 && FROM_INPUT && sm.err) atomicOr(a.err, sm.err);
     (void)agg;
     uint32_t pos = a.block_off[bid] + wbase + incl - mine;
-    const uint32_t imask = (1u << a.g.item_bits) - 1u;
     // (static indices: the entry arrays stay in registers)
 #pragma unroll
     for (int r = 0; r < kPer; ++r)
@@ -297,9 +296,19 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
             if (t < cnt[r]) {
                 a.keys[pos] = keys[r][t];
                 a.idx[pos] = (uint32_t)(base + tid * kPer + r);
-                atomicAdd(&a.item_cnt[keys[r][t] & imask], 1u);
                 ++pos;
             }
+}
+
+// item offsets from the sorted keys: off[it] = first entry of item it (the
+// next non-empty item's first entry for an empty one), off[n_items] = n
+__global__ void k_item_offsets(const uint32_t *__restrict__ keys, int64_t n, int64_t n_items,
+                               uint32_t *__restrict__ off) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    const int64_t cur = i < n ? (int64_t)(keys[i] >> kRowBits) : n_items;
+    const int64_t prev = i > 0 ? (int64_t)(keys[i - 1] >> kRowBits) : -1;
+    for (int64_t it = prev + 1; it <= cur; ++it) off[it] = (uint32_t)i;
 }
 
 }  // namespace
@@ -318,14 +327,12 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     k.n_rb = ceil_div(v_count, kItemRows);
     const int64_t n_items = (int64_t)g->n_w * k.n_ss * k.n_rb;
     k.item_bits = std::max(1, ilog2(n_items));
-    // rowrel < kItemRows + 2S must fit above the item bits
-    if (k.item_bits + ilog2(kItemRows + 2 * kMaxS) > 32)
-        return fail(WSB_EUNSUPPORTED, "gridder item space exceeds 32-bit keys");
+    // item << kRowBits | rowrel (rowrel < kItemRows + 2S) in 32 bits
+    static_assert(kItemRows + 2 * kMaxS <= (1 << kRowBits), "row offset bits");
+    if (k.item_bits + kRowBits > 32) return fail(WSB_EUNSUPPORTED, "gridder item space exceeds 32-bit keys");
     if (m > (int64_t)(0x7FFFFFFF / 4)) return fail(WSB_EUNSUPPORTED, "more than 2^29 records per GPU");
-    uint32_t *cnt, *off;
-    WSB_TRY(ensure(ctx, kSlotTileCount, sizeof(uint32_t) * (n_items + 1), (void **)&cnt));
+    uint32_t *off;
     WSB_TRY(ensure(ctx, kSlotTileOff, sizeof(uint32_t) * (n_items + 1), (void **)&off));
-    WSB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (n_items + 1), ctx->stream));
     const int nb = std::max(1, ceil_div(m, kTile));
     // tile entry counts -> offsets (+ total), error flag
     uint32_t *bcnt, *boff;
@@ -354,7 +361,6 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     a.g = k;
     a.keys = ka;
     a.idx = ia;
-    a.item_cnt = cnt;
     a.block_off = boff;
     a.err = err;
     if (m > 0) {
@@ -392,9 +398,12 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     // partition_time_ordered (visdata.py:354-355), reached by run_pipeline
     // through _partition_for_ranks (pipeline.py:47-52)
     if (e & kErrTime) return fail(WSB_EINVAL, "records must be sorted by time_index");
-    WSB_TRY(exclusive_scan_u32(ctx, cnt, off, n_items + 1, nullptr));
     uint32_t *ks, *is;
-    WSB_TRY(radix_sort_pairs(ctx, ka, kb, ia, ib, n_entries, k.item_bits, &ks, &is));
+    WSB_TRY(radix_sort_pairs(ctx, ka, kb, ia, ib, n_entries, k.item_bits + kRowBits, &ks, &is));
+    k_item_offsets<<<ceil_div((int64_t)n_entries + 1, 256), 256, 0, ctx->stream>>>(ks, n_entries, n_items,
+                                                                                 off);
+    ctx->launches += 1;
+    WSB_CUDA_TRY(cudaGetLastError());
     out->keys = ks;
     out->idx = is;
     out->off = off;

@@ -178,6 +178,7 @@ struct SweepArgs {
     const uint32_t *keys;      // sorted entries: item | rowrel << item_bits
     const uint32_t *idx;       // record index per entry
     const uint4 *parts;        // (item, first entry, end entry, slot | ~0 = direct)
+    uint2 *part_rows;          // split parts: rows [lo, hi) (relative to the block) they wrote
     void *out;                 // strip layout [n_w][n_u/16][v_count][16]
     double2 *partial;          // [slot][kItemRows][kSS] partial tiles of split items
     unsigned long long *updates;
@@ -204,15 +205,12 @@ struct Shm {
     static constexpr int NROW = kItemRows + 2 * S;   // anchor rows that reach the item
     StagedRec<S> rec[kChunk + 1];   // + a sentinel (window step -1) ending every list
     double4 raw[kRaw][kChunk];      // gathered records (gu, gv, Re, Im)
-    uint32_t sorted[kPartCap];      // record indices of the part in (anchor row, entry) order
-    uint32_t cnt[NROW + 1], run[NROW];
-    uint16_t wcnt[kWarps][NROW];
     uint8_t list[kWarps][kChunk + 4];      // per strip: the chunk's records touching it, in order
 };
 
 template <int KIND, int S>
 constexpr int sweep_min_blocks() {
-    return sizeof(Shm<KIND, S>) <= 28 * 1024 ? 7 : (sizeof(Shm<KIND, S>) <= 36 * 1024 ? 6 : 4);
+    return sizeof(Shm<KIND, S>) <= 24 * 1024 ? 6 : 4;
 }
 
 template <int KIND, int S>
@@ -239,63 +237,17 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     const uint32_t eb = pd.y, n = pd.z - pd.y;
     const bool direct = pd.w == 0xFFFFFFFFu;
 
-    // ---- phase A: stable counting sort of the part's entries by anchor row.
-    // Sorting by the row (not just the two-row window step) makes every
-    // cell's accumulation order (anchor row, record) whatever the slab
-    // boundaries' parity -- the v-slab result is then bit-identical for any
-    // slab split.
-    for (int s = tid; s <= NROW; s += kThreads) sm.cnt[s] = 0;
-    for (int s = tid; s < NROW; s += kThreads) sm.run[s] = 0;
-    __syncthreads();
-    for (uint32_t e = tid; e < n; e += kThreads) {
-        const uint32_t st = __ldg(&a.keys[eb + e]) >> a.item_bits;
-        WSB_DCHECK(st < (uint32_t)NROW, "item %lld e %u st %u", (long long)item, e, st);
-        atomicAdd(&sm.cnt[st], 1u);
-    }
-    __syncthreads();
-    if (warp == 0) {   // exclusive scan of the row counts, 32 at a time
-        uint32_t carry = 0;
-        for (int s0 = 0; s0 <= NROW; s0 += 32) {
-            const int s = s0 + lane;
-            const uint32_t x = s <= NROW ? sm.cnt[s] : 0u;
-            uint32_t incl = x;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (s <= NROW) sm.cnt[s] = carry + incl - x;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-    }
-    __syncthreads();
-    const uint32_t lt = (1u << lane) - 1u;
-    for (uint32_t r0 = 0; r0 < n; r0 += kThreads) {
-        const uint32_t e = r0 + tid;
-        const bool ok = e < n;
-        const uint32_t st = ok ? __ldg(&a.keys[eb + e]) >> a.item_bits : 0xFFFFu;
-        const uint32_t id = ok ? __ldg(&a.idx[eb + e]) : 0u;
-        for (int s = tid; s < kWarps * NROW; s += kThreads) (&sm.wcnt[0][0])[s] = 0;
-        __syncthreads();
-        const uint32_t peers = __match_any_sync(0xffffffffu, st);
-        if (ok && lane == __ffs(peers) - 1) sm.wcnt[warp][st] = (uint16_t)__popc(peers);
-        __syncthreads();
-        if (ok) {
-            uint32_t pos = sm.cnt[st] + sm.run[st] + __popc(peers & lt);
-            for (int w = 0; w < warp; ++w) pos += sm.wcnt[w][st];
-            WSB_DCHECK(pos < n && id < a.n_rec, "item %lld pos %u n %u id %u", (long long)item, pos, n, id);
-            sm.sorted[pos] = id;
-        }
-        __syncthreads();
-        for (int s = tid; s < NROW; s += kThreads) {
-            uint32_t t = 0;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) t += sm.wcnt[w][s];
-            sm.run[s] += t;
-        }
-        __syncthreads();   // wcnt is cleared by the next round
-    }
-
+    // The part's entries arrive sorted by (anchor row, record) -- the order
+    // every cell accumulates in, whatever the slab split. A direct part
+    // sweeps (and writes) the whole block; a split part only the rows its
+    // records reach, recorded for k_combine.
+    const int rr_first = n ? (int)(__ldg(&a.keys[eb]) & 0xFFu) : 0;
+    const int rr_last = n ? (int)(__ldg(&a.keys[eb + n - 1]) & 0xFFu) : 0;
+    const int step0 = direct ? 0 : rr_first >> 1;
+    const int row_end = direct ? R1 : min(R1, Bfirst + rr_last + 2 * S + 1);
+    if (!direct && tid == 0)
+        a.part_rows[blockIdx.x] = make_uint2((uint32_t)max(Bfirst + 2 * step0 - R0, 0),
+                                             (uint32_t)max(row_end - R0, 0));
     // ---- phase B: the sweep -------------------------------------------------
     const int q = lane >> 4, c = lane & 15;
     const int wc = warp * kC + c;                  // lane column inside the superstrip
@@ -320,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     double2 acc[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
-    int step = 0, phase = 0;
+    int step = step0, phase = step0 % T;
     unsigned cnt_upd = 0;
 
     // rows B, B+1 are final: write them (one 512-byte run for the warp),
@@ -346,13 +298,19 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         phase = (p + 1 == T) ? 0 : p + 1;
     };
 
-    // gather: thread pair (2r, 2r+1) copies record r's two 16-byte halves
+    // gather: thread pair (2r, 2r+1) copies record r's two 16-byte halves;
+    // the entry's record index is loaded one chunk before its gather
     const int nchunks = (int)((n + kChunk - 1) / kChunk);
-    auto fetch = [&](int ch) {
+    auto index_of = [&](int ch) -> uint32_t {
+        const uint32_t r = ch * kChunk + (tid >> 1);
+        return (ch < nchunks && r < n) ? __ldg(&a.idx[eb + r]) : 0u;
+    };
+    auto fetch = [&](int ch, uint32_t id) {
         if (ch < nchunks) {
             const uint32_t r = ch * kChunk + (tid >> 1);
             if (r < n) {
-                const double2 *src = reinterpret_cast<const double2 *>(a.rec + sm.sorted[r]) + (tid & 1);
+                WSB_DCHECK(id < a.n_rec, "item %lld id %u", (long long)item, id);
+                const double2 *src = reinterpret_cast<const double2 *>(a.rec + id) + (tid & 1);
                 const uint32_t dst = (uint32_t)__cvta_generic_to_shared(
                     reinterpret_cast<double2 *>(&sm.raw[ch % kRaw][tid >> 1]) + (tid & 1));
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
@@ -360,16 +318,17 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    __syncthreads();   // sorted[] complete
 #pragma unroll
-    for (int ch = 0; ch < kRaw - 1; ++ch) fetch(ch);
+    for (int ch = 0; ch < kRaw - 1; ++ch) fetch(ch, index_of(ch));
+    uint32_t nid = index_of(kRaw - 1);
 
     const unsigned char *const recbase = reinterpret_cast<const unsigned char *>(&sm.rec[0]);
     if (tid == 0) sm.rec[kChunk].meta = make_int4(0, -1, 0, 0);   // list sentinel
     for (int ch = 0; ch < nchunks; ++ch) {
         asm volatile("cp.async.wait_group %0;\n" ::"n"(kRaw - 2) : "memory");
         __syncthreads();   // raw[ch] landed for every thread; the previous sweep is done
-        fetch(ch + kRaw - 1);
+        fetch(ch + kRaw - 1, nid);
+        nid = index_of(ch + kRaw);
         const int nr = (int)min((uint32_t)kChunk, n - (uint32_t)ch * kChunk);
         // ---- stage: thread pair per record, thread (2r + a) does axis a of
         // record r. Both axes run the same weight code (one instruction stream
@@ -491,8 +450,8 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    // flush the rest of the block
-    while (Bfirst + 2 * step < R1) dispatch_phase<0, T>(phase, emit);
+    // flush the rest of the block (split parts: of their rows)
+    while (Bfirst + 2 * step < row_end) dispatch_phase<0, T>(phase, emit);
 
 #pragma unroll
     for (int o = 16; o; o >>= 1) cnt_upd += __shfl_xor_sync(0xffffffffu, cnt_upd, o);
@@ -624,7 +583,11 @@ __global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split
         const int col = ss * kSS + wc;
         double2 acc = make_double2(0.0, 0.0);
         const double2 *src = a.partial + ((int64_t)si.y * kItemRows + r) * kSS + wc;
-        for (int p = 0; p < np; ++p) {
+        const uint2 *pr = a.part_rows + part_off[item];
+        for (int p = 0; p < np; ++p) {          // parts in order; rows ascend with p
+            const uint2 span = pr[p];
+            if ((uint32_t)r < span.x) break;
+            if ((uint32_t)r >= span.y) continue;
             const double2 z = src[(int64_t)p * kItemRows * kSS];
             acc.x += z.x;
             acc.y += z.y;
@@ -680,11 +643,12 @@ int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
     WSB_TRY(exclusive_scan_u32(ctx, ns, ns_off, ni + 1, &n_slots));
     WSB_TRY(exclusive_scan_u32(ctx, sp, sp_off, ni + 1, &n_split));
     uint4 *parts;
-    uint2 *split_items;
+    uint2 *split_items, *part_rows;
     double2 *partial = nullptr;
-    WSB_TRY(ensure(ctx, kSlotParts, sizeof(uint4) * n_parts + sizeof(uint2) * (n_split + 1),
+    WSB_TRY(ensure(ctx, kSlotParts, sizeof(uint4) * n_parts + sizeof(uint2) * (n_split + 1 + n_parts),
                    (void **)&parts));
     split_items = reinterpret_cast<uint2 *>(parts + n_parts);
+    part_rows = split_items + n_split + 1;
     if (n_slots)
         WSB_TRY(ensure(ctx, kSlotPartial, sizeof(double2) * (size_t)n_slots * kItemRows * kSS,
                        (void **)&partial));
@@ -693,6 +657,7 @@ int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     a.parts = parts;
+    a.part_rows = part_rows;
     a.partial = partial;
     a.n_parts = n_parts;
     a.n_rec = 0x7FFFFFFF;

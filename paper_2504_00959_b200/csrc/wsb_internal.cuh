@@ -165,7 +165,8 @@ int plane_histogram(wsb_ctx *ctx, const wsb_grid *g, const uint32_t *plane, int6
 // warp = one WSB_STRIP-column strip.
 constexpr int kItemRows = 128;
 constexpr int kSSCols = 4 * WSB_STRIP;
-constexpr int kPartCap = 2048;     // entries per work part (the CTA's shared-memory sort)
+constexpr int kPartCap = 2048;     // entries per work part (split heavy items)
+constexpr int kRowBits = 8;        // entry key = item << kRowBits | row offset
 
 // the visibility columns of one channel (fused prepare + bucketing)
 struct VisColumns {
@@ -175,7 +176,7 @@ struct VisColumns {
 };
 
 struct ItemBuckets {
-    uint32_t *keys = nullptr;  // item | rowrel << item_bits, item-major, record order inside an item
+    uint32_t *keys = nullptr;  // item << kRowBits | rowrel, sorted: (item, row, record) order
     uint32_t *idx = nullptr;   // record index per entry
     uint32_t *off = nullptr;   // [n_items + 1] exclusive offsets
     int64_t n_entries = 0, n_items = 0;
