@@ -189,37 +189,55 @@ struct SweepArgs {
     int64_t n_rec, out_elems;  // bounds (debug checks)
 };
 
+// Window of the tensor-core sweep: 8 * MT rows (MT = 1 for S <= 3, else 2),
+// a ring of 2-row bands; the two 16-column halves x (Re, Im) of each 8-row
+// band are four 8x8 FP64 MMA accumulators.
+template <int S>
+struct Win {
+    static constexpr int MT = (2 * S + 2 <= 8) ? 1 : 2;
+    static constexpr int ROWS = 8 * MT;
+    static constexpr int NB = ROWS / 2;            // 2-row bands in the ring
+};
+
 // One staged record: everything a lane reads to apply it, at one base
-// address (the sweep addresses a record with a single IMAD).
+// address (one IMAD per record).
 template <int S>
 struct StagedRec {
     static constexpr int W = 2 * S + 1;
-    static constexpr int TP = (S + 2) & ~1;   // ring slots S+1, padded to 16 bytes
+    static constexpr int NV = Win<S>::ROWS;
     double2 tu[W + 1];     // value * u weight per window column; slot W = 0
-    double wv[3][TP];      // v weights: [0] rows 2t-1, [1] rows 2t, [2] rows 2t+1 of the window
-    int4 meta;             // (first window column - superstrip col0, window step, parity, strip mask)
+    double wv[NV];         // v weight of window row b (0 .. ROWS-1 from the window base); 0 off the footprint
+    int4 meta;             // (first window column - superstrip col0, window step, row offset d, strip mask)
 };
 
 template <int KIND, int S>
 struct Shm {
     static constexpr int NROW = kItemRows + 2 * S;   // anchor rows that reach the item
-    StagedRec<S> rec[kChunk + 1];   // + a sentinel (window step -1) ending every list
+    StagedRec<S> rec[kChunk + 1];   // + a zero sentinel (window step -1) ending every list
     double4 raw[kRaw][kChunk];      // gathered records (gu, gv, Re, Im)
-    uint8_t list[kWarps][kChunk + 4];      // per strip: the chunk's records touching it, in order
+    uint8_t list[kWarps][kChunk + 8];      // per strip: the chunk's records touching it, in order
 };
 
 template <int KIND, int S>
 constexpr int sweep_min_blocks() {
-    return sizeof(Shm<KIND, S>) <= 24 * 1024 ? 6 : 4;
+    return 6;
+}
+
+// m8n8k4 FP64 MMA, D = A B + D: a(row lane/4, k lane%4), b(k lane%4, col lane/4),
+// d(row lane/4, cols 2(lane%4), 2(lane%4)+1)
+__device__ __forceinline__ void dmma(double2 &d, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d.x), "+d"(d.y)
+                 : "d"(a), "d"(b));
 }
 
 template <int KIND, int S>
 __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     k_grid_items(SweepArgs a, KParams<S> kp) {
     constexpr int W = 2 * S + 1;
-    constexpr int T = S + 1;
     using Sm = Shm<KIND, S>;
     using Rec = StagedRec<S>;
+    constexpr int MT = Win<S>::MT, ROWS = Win<S>::ROWS, NB = Win<S>::NB;
     constexpr int NROW = Sm::NROW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Sm &sm = *reinterpret_cast<Sm *>(smem_raw);
@@ -248,54 +266,76 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     if (!direct && tid == 0)
         a.part_rows[blockIdx.x] = make_uint2((uint32_t)max(Bfirst + 2 * step0 - R0, 0),
                                              (uint32_t)max(row_end - R0, 0));
-    // ---- phase B: the sweep -------------------------------------------------
-    const int q = lane >> 4, c = lane & 15;
-    const int wc = warp * kC + c;                  // lane column inside the superstrip
-    const int col = col0 + wc;
-    const bool col_ok = col < a.n_u;
+
+    // ---- the sweep --------------------------------------------------------
+    // Warp w owns columns [16w, 16w+16) of the superstrip. Its window holds
+    // rows B .. B+ROWS-1 (B = Bfirst + 2 step) in a ring of 2-row bands:
+    // band (phase + t) % NB holds rows B + 2t, B + 2t + 1. The records of a
+    // window step (anchor rows B, B+1) are applied four at a time as one
+    // rank-4 update per 8x8 accumulator tile: A = their v weights on the
+    // tile's rows, B = value x u weight on its columns (FP64 tensor cores:
+    // one MMA instruction per 256 multiply-adds instead of 8 DFMA per record
+    // and lane). When the next record starts lower, band `phase` (rows B,
+    // B+1) is final: its 8 lanes write it (512 bytes), clear it, and the
+    // window moves two rows down.
     const double i0b = KIND == WSB_KERNEL_KAISER_BESSEL ? *a.i0beta : 0.0;
     double2 *const outp = (double2 *)a.out;
     float2 *const out32 = (float2 *)a.out;
     const bool f32 = direct && a.out_f32;
-    const int64_t strip_base = ((int64_t)plane * a.n_s16 + col / kC) * a.v_count;
-    double2 *const ptile = direct ? nullptr : a.partial + (int64_t)pd.w * kItemRows * kSS;
-    // lane offsets inside a staged record: its tu column (clamped to the zero
-    // slot) and its parity row of v weights
-    constexpr int WVROW = Rec::TP * 8;             // bytes per parity row of v weights
-    const int lane_wv = WVROW * (q + 1);           // + (-WVROW * parity) per record
-
-    // window: a ring of T slots; with phase p = step mod T, slot (p + t) % T
-    // holds rows B + q + 2t, B = Bfirst + 2 step. The sweep code exists once
-    // per phase (the slot mapping is static: no register moves), and
-    // consecutive window steps fall through from one phase's copy to the
-    // next: one jump-table dispatch per T steps and per chunk, not per step.
-    double2 acc[T];
+    const int g4 = lane >> 2, k4 = lane & 3;       // MMA fragment coordinates
+    // accumulators: [m tile][n half][Re/Im], lane holds row g4 of the tile and
+    // columns 2 k4, 2 k4 + 1 of the half
+    double2 acc[MT][2][2];
 #pragma unroll
-    for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
-    int step = step0, phase = step0 % T;
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[m][h][0] = acc[m][h][1] = make_double2(0.0, 0.0);
+    int step = step0, phase = step0 % NB;
     unsigned cnt_upd = 0;
+    const int64_t strip_base = ((int64_t)plane * a.n_s16 + (col0 / kC + warp)) * a.v_count;
+    double2 *const ptile = direct ? nullptr : a.partial + (int64_t)pd.w * kItemRows * kSS;
 
-    // rows B, B+1 are final: write them (one 512-byte run for the warp),
-    // clear their slot, move the window down two rows
-    auto emit = [&](auto P) {
-        constexpr int p = decltype(P)::value;
-        const int row = Bfirst + 2 * step + q;
-        if (row >= R0 && row < R1 && col_ok) {
-            if (direct) {
-                const double sg = ((col + row) & 1) ? -1.0 : 1.0;
-                const int64_t o = (strip_base + (row - a.v_start)) * kC + c;
-                WSB_DCHECK(o >= 0 && o < a.out_elems, "item %lld o %lld", (long long)item, (long long)o);
-                if (f32)
-                    out32[o] = make_float2((float)(acc[p].x * sg), (float)(acc[p].y * sg));
-                else
-                    outp[o] = make_double2(acc[p].x * sg, acc[p].y * sg);
-            } else {
-                ptile[(row - R0) * kSS + wc] = acc[p];
+    // rows B, B+1 final: the lanes of band `phase` write them, clear it
+    auto emit = [&]() {
+        const int band = phase;            // band b lives in tile b / 4, lane rows 2(b % 4), +1
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            const bool mine = (band >> 2) == m && (g4 >> 1) == (band & 3);
+            if (mine) {
+                const int row = Bfirst + 2 * step + (g4 & 1);
+                if (row >= R0 && row < R1) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = h * 8 + 2 * k4;                 // column inside the strip
+                        const int col = col0 + warp * kC + c;
+                        if (col < a.n_u) {
+                            const double2 re = acc[m][h][0], im = acc[m][h][1];
+                            if (direct) {
+                                const double sg = ((col + row) & 1) ? -1.0 : 1.0;
+                                const int64_t o = (strip_base + (row - a.v_start)) * kC + c;
+                                WSB_DCHECK(o >= 0 && o + 1 < a.out_elems, "item %lld o %lld", (long long)item,
+                                           (long long)o);
+                                if (f32) {
+                                    out32[o] = make_float2((float)(re.x * sg), (float)(im.x * sg));
+                                    out32[o + 1] = make_float2((float)(-re.y * sg), (float)(-im.y * sg));
+                                } else {
+                                    outp[o] = make_double2(re.x * sg, im.x * sg);
+                                    outp[o + 1] = make_double2(-re.y * sg, -im.y * sg);
+                                }
+                            } else {
+                                double2 *pt_ = ptile + (row - R0) * kSS + warp * kC + c;
+                                pt_[0] = make_double2(re.x, im.x);
+                                pt_[1] = make_double2(re.y, im.y);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) acc[m][h][0] = acc[m][h][1] = make_double2(0.0, 0.0);
             }
         }
-        acc[p] = make_double2(0.0, 0.0);
         ++step;
-        phase = (p + 1 == T) ? 0 : p + 1;
+        phase = phase + 1 == NB ? 0 : phase + 1;
     };
 
     // gather: thread pair (2r, 2r+1) copies record r's two 16-byte halves;
@@ -323,16 +363,20 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     uint32_t nid = index_of(kRaw - 1);
 
     const unsigned char *const recbase = reinterpret_cast<const unsigned char *>(&sm.rec[0]);
-    if (tid == 0) sm.rec[kChunk].meta = make_int4(0, -1, 0, 0);   // list sentinel
+    // the sentinel: zero weights, window step -1
+    for (int e = tid; e < (int)(sizeof(Rec) / 8); e += kThreads)
+        reinterpret_cast<double *>(&sm.rec[kChunk])[e] = 0.0;
+    __syncthreads();
+    if (tid == 0) sm.rec[kChunk].meta = make_int4(0, -1, 0, 0);
     for (int ch = 0; ch < nchunks; ++ch) {
         asm volatile("cp.async.wait_group %0;\n" ::"n"(kRaw - 2) : "memory");
         __syncthreads();   // raw[ch] landed for every thread; the previous sweep is done
         fetch(ch + kRaw - 1, nid);
         nid = index_of(ch + kRaw);
         const int nr = (int)min((uint32_t)kChunk, n - (uint32_t)ch * kChunk);
-        // ---- stage: thread pair per record, thread (2r + a) does axis a of
+        // ---- stage: thread pair per record, thread (2r + ax) does axis ax of
         // record r. Both axes run the same weight code (one instruction stream
-        // for the warp), only the short tails differ; all 4 warps stage.
+        // for the warp); only the short tails differ.
         {
             const int r = tid >> 1, ax = tid & 1;
             unsigned mine = 0;      // taps of this axis inside the item
@@ -362,17 +406,20 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                     st.meta.w = mask;
                     mine = __popc(uin);
                 } else {
-                    // v axis: parity-split row weights
+                    // v axis: weight of window row b (from the window base; the
+                    // record's footprint starts at row d = anchor - base, 0 or 1)
                     const int rel = i0 - Bfirst;
                     WSB_DCHECK(rel >= 0 && rel < NROW, "item %lld rel %d", (long long)item, rel);
+                    const int d = rel & 1;
 #pragma unroll
-                    for (int t = 0; t < Rec::TP; ++t) {
-                        st.wv[0][t] = (2 * t - 1 >= 0 && 2 * t - 1 < W) ? wgt[max(2 * t - 1, 0)] : 0.0;
-                        st.wv[1][t] = (2 * t < W) ? wgt[min(2 * t, W - 1)] : 0.0;
-                        st.wv[2][t] = (2 * t + 1 < W) ? wgt[min(2 * t + 1, W - 1)] : 0.0;
+                    for (int b = 0; b < Rec::NV; ++b) {
+                        // b - d in [0, W): weight, else 0 (d is 0 or 1)
+                        const double x0 = b < W ? wgt[b < W ? b : 0] : 0.0;            // d = 0
+                        const double x1 = (b >= 1 && b - 1 < W) ? wgt[b >= 1 && b - 1 < W ? b - 1 : 0] : 0.0;
+                        st.wv[b] = d ? x1 : x0;
                     }
                     st.meta.y = rel >> 1;
-                    st.meta.z = -WVROW * (rel & 1);
+                    st.meta.z = d;
                     const int r_lo = max(R0 - i0, 0), r_hi = min(R1 - i0, W) - 1;
                     mine = __popc(r_hi >= r_lo ? wm & (((2u << r_hi) - 1u) & ~((1u << r_lo) - 1u)) : 0u);
                 }
@@ -382,76 +429,60 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             if (ax == 0) cnt_upd += mine * other;
         }
         __syncthreads();   // stage complete
-        // ---- sweep: this warp's strip, records in order ---------------------
+        // ---- sweep: this warp's strip ---------------------------------------
         {
             // records of this chunk touching the strip, in order, as a byte list
-            // ending at the sentinel record (window step -1): fetching the next
-            // record is one shared load, no bit scans and no bounds test
+            // padded with sentinels
             {
                 const uint32_t m0 = __ballot_sync(0xffffffffu, lane < nr && ((sm.rec[lane].meta.w >> warp) & 1));
                 const uint32_t m1 =
                     __ballot_sync(0xffffffffu, 32 + lane < nr && ((sm.rec[32 + lane].meta.w >> warp) & 1));
                 const uint32_t lt = (1u << lane) - 1u;
+                const int tot = __popc(m0) + __popc(m1);
                 if ((m0 >> lane) & 1) sm.list[warp][__popc(m0 & lt)] = (uint8_t)lane;
                 if ((m1 >> lane) & 1) sm.list[warp][__popc(m0) + __popc(m1 & lt)] = (uint8_t)(32 + lane);
-                if (lane == 0) sm.list[warp][__popc(m0) + __popc(m1)] = (uint8_t)kChunk;
+                if (lane < 8) sm.list[warp][tot + lane] = (uint8_t)kChunk;
                 __syncwarp();
             }
             const uint8_t *lp = sm.list[warp];
-            const unsigned char *rp;
-            int4 mt;
-            auto next_rec = [&]() {
-                rp = recbase + (int)(*lp++) * (int)sizeof(Rec);
-                mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
-            };
-            next_rec();
-            // phase P: apply the pending records of the current step, then (if
-            // the chunk still has records) emit the step's rows. false: chunk done
-            auto run = [&](auto P) -> bool {
-                constexpr int p = decltype(P)::value;
-                while (mt.y == step) {
-                    int k = wc - mt.x;
-                    k = (unsigned)k < (unsigned)W ? k : W;
-                    const double2 tv = *reinterpret_cast<const double2 *>(rp + 16 * k);
-                    const double *wp =
-                        reinterpret_cast<const double *>(rp + offsetof(Rec, wv) + lane_wv + mt.z);
-#pragma unroll
-                    for (int t = 0; t < T; t += 2) {
-                        const double2 w2 = *reinterpret_cast<const double2 *>(wp + t);
-                        acc[(p + t) % T].x = fma(tv.x, w2.x, acc[(p + t) % T].x);
-                        acc[(p + t) % T].y = fma(tv.y, w2.x, acc[(p + t) % T].y);
-                        if (t + 1 < T) {
-                            acc[(p + t + 1) % T].x = fma(tv.x, w2.y, acc[(p + t + 1) % T].x);
-                            acc[(p + t + 1) % T].y = fma(tv.y, w2.y, acc[(p + t + 1) % T].y);
-                        }
-                    }
-                    next_rec();
-                }
-                if (mt.y < 0) return false;  // the next chunk may still add to this step
-                emit(P);                      // rows above the pending record are final
-                return true;
-            };
+            const int wc8 = warp * kC + g4;        // this lane's B column (half 0) in the superstrip
+#pragma unroll 1
             for (;;) {
-                bool more = true;
-                switch (phase) {
-#define WSB_PHASE(q)                                                        \
-    case q:                                                                 \
-        if constexpr (q < T) {                                              \
-            if (!(more = run(std::integral_constant<int, q>{}))) break;     \
-        }                                                                   \
-        [[fallthrough]];
-                    WSB_PHASE(0) WSB_PHASE(1) WSB_PHASE(2) WSB_PHASE(3)
-                    WSB_PHASE(4) WSB_PHASE(5) WSB_PHASE(6) WSB_PHASE(7)
-#undef WSB_PHASE
-                    default: break;
+                // the next four records of the list, one per k slot
+                const unsigned char *rp = recbase + (int)lp[k4] * (int)sizeof(Rec);
+                const int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
+                const bool match = mt.y == step;
+                const uint32_t m4 = __ballot_sync(0xffffffffu, match) & 0xFu;
+                if (!m4) {
+                    if (lp[0] == (uint8_t)kChunk) break;            // chunk done
+                    emit();                                         // rows above the next record are final
+                    continue;
                 }
-                if (!more) break;
+                if (!match) rp = recbase + kChunk * (int)sizeof(Rec);   // zero slot
+                const int ibr = match ? mt.x : 0;
+                // B: value x u weight at this lane's column of each 8-column half
+                const int c0 = wc8 - ibr;
+                const int i0 = (unsigned)c0 < (unsigned)W ? c0 : W;
+                const int i1 = (unsigned)(c0 + 8) < (unsigned)W ? c0 + 8 : W;
+                const double2 b0 = *reinterpret_cast<const double2 *>(rp + 16 * i0);
+                const double2 b1 = *reinterpret_cast<const double2 *>(rp + 16 * i1);
+#pragma unroll
+                for (int m = 0; m < MT; ++m) {
+                    // A: this record's v weight on tile row g4 of tile m
+                    const int band = (4 * m + (g4 >> 1) - phase + NB) % NB;   // ring band -> window band
+                    const double av = reinterpret_cast<const double *>(rp + offsetof(Rec, wv))[2 * band + (g4 & 1)];
+                    dmma(acc[m][0][0], av, b0.x);
+                    dmma(acc[m][0][1], av, b0.y);
+                    dmma(acc[m][1][0], av, b1.x);
+                    dmma(acc[m][1][1], av, b1.y);
+                }
+                lp += __popc(m4);
             }
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     // flush the rest of the block (split parts: of their rows)
-    while (Bfirst + 2 * step < row_end) dispatch_phase<0, T>(phase, emit);
+    while (Bfirst + 2 * step < row_end) emit();
 
 #pragma unroll
     for (int o = 16; o; o >>= 1) cnt_upd += __shfl_xor_sync(0xffffffffu, cnt_upd, o);
