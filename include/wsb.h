@@ -54,9 +54,10 @@ extern "C" {
 #define WSB_P_GROUP 1
 
 /* Column width of the gridder's output "strip layout":
- *   grid_s[plane][col / WSB_STRIP][row][col % WSB_STRIP]   (complex128)
- * every two rows of a strip are one 512-byte run; the checkerboard sign of
- * transform.py:180-185 is applied. */
+ *   grid_s[plane][col / WSB_STRIP][row][re | im][col % WSB_STRIP]
+ * (each strip row stores its WSB_STRIP real parts, then its imaginary parts,
+ * f64 -- f32 on the FP32 path; every two rows of a strip are one 512-byte
+ * run); the checkerboard sign of transform.py:180-185 is applied. */
 #define WSB_STRIP 16
 
 /* Longest transform handled on chip (one CTA) and longest transform

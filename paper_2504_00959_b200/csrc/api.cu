@@ -112,9 +112,11 @@ __global__ void k_unpack(const double2 *p, double2 *out, int n_w, int n_u, int v
     const int64_t t = e / n_u;
     const int j = (int)(t % nr) + r0;
     const int k = (int)(t / nr);
-    // strip layout [plane][col/WSB_STRIP][row][col%WSB_STRIP]
+    // strip layout [plane][col/WSB_STRIP][row][re | im][col%WSB_STRIP]
     constexpr int SW = WSB_STRIP;
-    double2 z = p[(((int64_t)k * ((n_u + SW - 1) / SW) + i / SW) * v_count + j) * SW + i % SW];
+    const double *q = reinterpret_cast<const double *>(p) +
+                      (((int64_t)k * ((n_u + SW - 1) / SW) + i / SW) * v_count + j) * (2 * SW) + i % SW;
+    double2 z = make_double2(q[0], q[SW]);
     const double s = ((i + v_start + j) & 1) ? -1.0 : 1.0;
     out[e] = make_double2(z.x * s, z.y * s);
 }

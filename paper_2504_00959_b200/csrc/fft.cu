@@ -350,6 +350,16 @@ __device__ __forceinline__ V dif_split(const V *x, int stride, int e, int n, int
     return e ? cmul(u, __ldg(&twN[n * e])) : u;
 }
 
+// the same for a loader ld(s) of the s-th column of the split
+template <int SPL, class V, class LD>
+__device__ __forceinline__ V dif_split_ld(LD ld, int e, int n, const V *__restrict__ twN) {
+    constexpr int SP = 1 << SPL;
+    V u = ld(0);
+#pragma unroll
+    for (int s = 1; s < SP; ++s) u = cadd(u, rot_quarter(ld(s), (4 / SP) * s * e));
+    return e ? cmul(u, __ldg(&twN[n * e])) : u;
+}
+
 // 4096/N rows per CTA. The first pass reads its inputs straight from HBM
 // (32-byte sectors, 16 loads in flight per thread) and the last pass writes
 // its outputs straight back: shared memory only carries the inner exchanges.
@@ -370,16 +380,30 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
     const int j0 = blockIdx.x * NSEQ;
     const int64_t plane = plane_lo + blockIdx.y;
     const int e = SPL ? (int)blockIdx.z : 0;
-    // in: strip layout [plane][col/WSB_STRIP][row][col%WSB_STRIP]
+    // in: strip layout [plane][col/WSB_STRIP][row][re | im][col%WSB_STRIP]
+    // (a strip row holds its WSB_STRIP real parts, then the imaginary parts)
     constexpr int SW = WSB_STRIP;
+    using Sc = decltype(V{}.x);
+    const Sc *ins = reinterpret_cast<const Sc *>(in);
     auto gld = [&](int seq, int col) {
         if (j0 + seq >= v_count) return cx<V>(0.0, 0.0);
-        const V *p = in + ((plane * n_strips + col / SW) * v_count + j0 + seq) * SW + (col % SW);
+        const Sc *p = ins + ((plane * n_strips + col / SW) * v_count + j0 + seq) * (2 * SW) + (col % SW);
         if constexpr (SPL == 0) {
-            return *p;
+            V z;
+            z.x = p[0];
+            z.y = p[SW];
+            return z;
         } else {
             // column col + s*N lies (N/SW) strips further on
-            return dif_split<SPL>(p, (N / SW) * v_count * SW, e, col, N, twN);
+            const int64_t stride = (int64_t)(N / SW) * v_count * (2 * SW);
+            return dif_split_ld<SPL, V>(
+                [&](int s_) {
+                    V z;
+                    z.x = p[s_ * stride];
+                    z.y = p[s_ * stride + SW];
+                    return z;
+                },
+                e, col, twN);
         }
     };
     // out: P[plane][col/G][row][col%G] per destination (RowDest); with a

@@ -295,38 +295,53 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     const int64_t strip_base = ((int64_t)plane * a.n_s16 + (col0 / kC + warp)) * a.v_count;
     double2 *const ptile = direct ? nullptr : a.partial + (int64_t)pd.w * kItemRows * kSS;
 
-    // rows B, B+1 final: the lanes of band `phase` write them, clear it
+    // rows B, B+1 final: the lanes of band `phase` write them (already
+    // signed), clear them. Output strip rows hold 16 real parts, then 16
+    // imaginary parts: a lane's two columns of a half are one 16-byte store
+    // straight from its accumulator fragment. The lane's destination for
+    // window step `step` is ob + 64 * step doubles (two strip rows per step).
+    const int c_lane = 2 * k4;                                  // + 8 h: column in the strip
+    const int64_t row_lane0 = (int64_t)Bfirst + (g4 & 1);       // mesh row at step 0
+    double *const ob = direct ? reinterpret_cast<double *>(a.out) +
+                                    (strip_base + (row_lane0 - a.v_start)) * (2 * kC) + c_lane
+                              : nullptr;
+    float *const ob32 = direct ? reinterpret_cast<float *>(a.out) +
+                                     (strip_base + (row_lane0 - a.v_start)) * (2 * kC) + c_lane
+                               : nullptr;
+    const bool col_ok = col0 + warp * kC + c_lane < a.n_u;      // (n_u >= 2: both columns or none)
     auto emit = [&]() {
         const int band = phase;            // band b lives in tile b / 4, lane rows 2(b % 4), +1
+        const int row = Bfirst + 2 * step + (g4 & 1);
+        const bool in_rows = row >= R0 && row < R1 && col_ok;
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
-            const bool mine = (band >> 2) == m && (g4 >> 1) == (band & 3);
-            if (mine) {
-                const int row = Bfirst + 2 * step + (g4 & 1);
-                if (row >= R0 && row < R1) {
+            if ((band >> 2) == m && (g4 >> 1) == (band & 3)) {
+                if (in_rows) {
+                    if (direct) {
+                        const int64_t o = (int64_t)step * (4 * kC);
+                        if (f32) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int c = h * 8 + 2 * k4;                 // column inside the strip
-                        const int col = col0 + warp * kC + c;
-                        if (col < a.n_u) {
-                            const double2 re = acc[m][h][0], im = acc[m][h][1];
-                            if (direct) {
-                                const double sg = ((col + row) & 1) ? -1.0 : 1.0;
-                                const int64_t o = (strip_base + (row - a.v_start)) * kC + c;
-                                WSB_DCHECK(o >= 0 && o + 1 < a.out_elems, "item %lld o %lld", (long long)item,
-                                           (long long)o);
-                                if (f32) {
-                                    out32[o] = make_float2((float)(re.x * sg), (float)(im.x * sg));
-                                    out32[o + 1] = make_float2((float)(-re.y * sg), (float)(-im.y * sg));
-                                } else {
-                                    outp[o] = make_double2(re.x * sg, im.x * sg);
-                                    outp[o + 1] = make_double2(-re.y * sg, -im.y * sg);
-                                }
-                            } else {
-                                double2 *pt_ = ptile + (row - R0) * kSS + warp * kC + c;
-                                pt_[0] = make_double2(re.x, im.x);
-                                pt_[1] = make_double2(re.y, im.y);
+                            for (int h = 0; h < 2; ++h) {
+                                *reinterpret_cast<float2 *>(ob32 + o + 8 * h) =
+                                    make_float2((float)acc[m][h][0].x, (float)acc[m][h][0].y);
+                                *reinterpret_cast<float2 *>(ob32 + o + kC + 8 * h) =
+                                    make_float2((float)acc[m][h][1].x, (float)acc[m][h][1].y);
                             }
+                        } else {
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                *reinterpret_cast<double2 *>(ob + o + 8 * h) = acc[m][h][0];
+                                *reinterpret_cast<double2 *>(ob + o + kC + 8 * h) = acc[m][h][1];
+                            }
+                        }
+                    } else {
+                        // partial tile [row][re | im][64 columns] of the item
+                        double *pt_ = reinterpret_cast<double *>(ptile) + (int64_t)(row - R0) * (2 * kSS) +
+                                      warp * kC + c_lane;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            *reinterpret_cast<double2 *>(pt_ + 8 * h) = acc[m][h][0];
+                            *reinterpret_cast<double2 *>(pt_ + kSS + 8 * h) = acc[m][h][1];
                         }
                     }
                 }
@@ -389,9 +404,14 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                 const uint32_t wm = axis_weights<KIND, S>(g, i0, kp, i0b, wgt);
                 if (ax == 0) {
                     // u axis: value * weight per window column
+                    // with the column factor (-1)^i of the checkerboard sign
+                    // (transform.py:180-185; a sign flip commutes with rounding)
+                    const double cs = (i0 & 1) ? -1.0 : 1.0;
 #pragma unroll
-                    for (int k = 0; k < W; ++k)
-                        st.tu[k] = make_double2(__dmul_rn(rc.z, wgt[k]), __dmul_rn(rc.w, wgt[k]));
+                    for (int k = 0; k < W; ++k) {
+                        const double wk = (k & 1) ? -cs * wgt[k] : cs * wgt[k];
+                        st.tu[k] = make_double2(__dmul_rn(rc.z, wk), __dmul_rn(rc.w, wk));
+                    }
                     st.tu[W] = make_double2(0.0, 0.0);
                     // tap columns inside the superstrip (and the mesh); the strips they touch
                     const int k_lo = max(col0 - i0, 0), k_hi = min(min(col0 + kSS, a.n_u) - i0, W) - 1;
@@ -411,12 +431,14 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                     const int rel = i0 - Bfirst;
                     WSB_DCHECK(rel >= 0 && rel < NROW, "item %lld rel %d", (long long)item, rel);
                     const int d = rel & 1;
+                    // with the row factor (-1)^j: window row b is mesh row Bfirst + 2k + b
+                    const double rs = (Bfirst & 1) ? -1.0 : 1.0;
 #pragma unroll
                     for (int b = 0; b < Rec::NV; ++b) {
                         // b - d in [0, W): weight, else 0 (d is 0 or 1)
                         const double x0 = b < W ? wgt[b < W ? b : 0] : 0.0;            // d = 0
                         const double x1 = (b >= 1 && b - 1 < W) ? wgt[b >= 1 && b - 1 < W ? b - 1 : 0] : 0.0;
-                        st.wv[b] = d ? x1 : x0;
+                        st.wv[b] = ((b & 1) ? -rs : rs) * (d ? x1 : x0);
                     }
                     st.meta.y = rel >> 1;
                     st.meta.z = d;
@@ -593,8 +615,9 @@ __global__ void k_build_parts(const uint32_t *off, int64_t n_items, const uint32
     split_items[split_off[item]] = make_uint2((uint32_t)item, slot_off[item]);
 }
 
-// one warp per (row, half superstrip) of a split item: its parts' partial
-// tiles summed in part order, sign applied, written to the strip layout
+// one thread per (row, column) of a split item: its parts' partial tiles
+// (signed, [row][re | im][64]) summed in part order, written to the strip
+// layout
 __global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split_items,
                                                   const uint32_t *part_off) {
     const uint2 si = split_items[blockIdx.x];
@@ -605,31 +628,33 @@ __global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split
     const int ss = (int)(pt % a.n_ss), plane = (int)(pt / a.n_ss);
     const int R0 = a.v_start + rb * kItemRows;
     const int R1 = min(R0 + kItemRows, a.v_start + a.v_count);
-    const int lane = threadIdx.x & 31;
-    const int wcol = (threadIdx.x >> 5) & 1;          // half superstrip
+    const int wc = threadIdx.x & 63;                   // column inside the superstrip
+    const int col = ss * kSS + wc;
+    const uint2 *pr = a.part_rows + part_off[item];
     for (int r = blockIdx.y * 2 + (threadIdx.x >> 6); r < kItemRows; r += gridDim.y * 2) {
         const int row = R0 + r;
         if (row >= R1) break;
-        const int wc = wcol * 32 + lane;
-        const int col = ss * kSS + wc;
-        double2 acc = make_double2(0.0, 0.0);
-        const double2 *src = a.partial + ((int64_t)si.y * kItemRows + r) * kSS + wc;
-        const uint2 *pr = a.part_rows + part_off[item];
+        double re = 0.0, im = 0.0;
+        const double *src = reinterpret_cast<const double *>(a.partial) +
+                            ((int64_t)si.y * kItemRows + r) * (2 * kSS) + wc;
         for (int p = 0; p < np; ++p) {          // parts in order; rows ascend with p
             const uint2 span = pr[p];
             if ((uint32_t)r < span.x) break;
             if ((uint32_t)r >= span.y) continue;
-            const double2 z = src[(int64_t)p * kItemRows * kSS];
-            acc.x += z.x;
-            acc.y += z.y;
+            const double *z = src + (int64_t)p * kItemRows * (2 * kSS);
+            re += z[0];
+            im += z[kSS];
         }
         if (col < a.n_u) {
-            const double s = ((col + row) & 1) ? -1.0 : 1.0;
-            const int64_t o = (((int64_t)plane * a.n_s16 + col / kC) * a.v_count + (row - a.v_start)) * kC + col % kC;
-            if (a.out_f32)
-                ((float2 *)a.out)[o] = make_float2((float)(acc.x * s), (float)(acc.y * s));
-            else
-                ((double2 *)a.out)[o] = make_double2(acc.x * s, acc.y * s);
+            const int64_t o = (((int64_t)plane * a.n_s16 + col / kC) * a.v_count + (row - a.v_start)) * (2 * kC) +
+                              col % kC;
+            if (a.out_f32) {
+                ((float *)a.out)[o] = (float)re;
+                ((float *)a.out)[o + kC] = (float)im;
+            } else {
+                ((double *)a.out)[o] = re;
+                ((double *)a.out)[o + kC] = im;
+            }
         }
     }
 }

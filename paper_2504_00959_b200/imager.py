@@ -287,14 +287,14 @@ def prepare_device(u, v, w, vis, weight, spec: GridSpec, device=None):
 def grid_slab_device(rec: torch.Tensor, plane: torch.Tensor, spec: GridSpec, kern: KernelSpec,
                      v_start: int, v_count: int, out: torch.Tensor | None = None):
     """grid_sector (gridder.py:186-259) for one slab on the GPU. Returns
-    (strip-layout grid, complex128 [n_w, ceil(n_u/S), v_count, S] as float64
-    [..., 2] with S = WSB_STRIP, grid_updates)."""
+    (strip-layout grid, float64 [n_w, ceil(n_u/S), v_count, 2 (re, im), S]
+    with S = WSB_STRIP, grid_updates)."""
     spec, kern = as_grid_spec(spec), as_kernel_spec(kern)
     ctx = context(rec.device)
     m = rec.shape[0]
     if out is None:
         sw = L.STRIP
-        out = torch.empty((spec.n_w, (spec.n_u + sw - 1) // sw, v_count, sw, 2),
+        out = torch.empty((spec.n_w, (spec.n_u + sw - 1) // sw, v_count, 2, sw),
                           dtype=torch.float64, device=rec.device)
     upd = C.c_int64()
     g, k = spec.c_struct(), kern.c_struct()

@@ -54,14 +54,17 @@ class NumpyBackend:
         pad = np.zeros((spec.n_w, vc, ns * sw), np.complex128)
         pad[:, :, : spec.n_u] = grid
         s = np.ascontiguousarray(pad.reshape(spec.n_w, vc, ns, sw).transpose(0, 2, 1, 3))
-        return torch.from_numpy(s.view(np.float64).reshape(spec.n_w, ns, vc, sw, 2)), upd
+        # each strip row: its sw real parts, then its sw imaginary parts
+        split = np.stack([s.real, s.imag], axis=3)             # (n_w, ns, vc, 2, sw)
+        return torch.from_numpy(np.ascontiguousarray(split)), upd
 
     def fft_rows(self, grid_s, spec, vc, dest_pairs, plane_lo=0, plane_hi=None):
         plane_hi = spec.n_w if plane_hi is None else plane_hi
         nk = plane_hi - plane_lo
         sw = L.STRIP
         ns = (spec.n_u + sw - 1) // sw
-        a = grid_s.numpy().view(np.complex128).reshape(spec.n_w, ns, vc, sw)[plane_lo:plane_hi]
+        g = grid_s.numpy().reshape(spec.n_w, ns, vc, 2, sw)
+        a = (g[:, :, :, 0, :] + 1j * g[:, :, :, 1, :])[plane_lo:plane_hi]
         nat = a.transpose(0, 2, 1, 3).reshape(nk, vc, ns * sw)[:, :, : spec.n_u]
         f = np.fft.ifft(nat, axis=-1) * spec.n_u               # unnormalised inverse
         # -> P layout (plane, col/G, row, col%G), then destination major
