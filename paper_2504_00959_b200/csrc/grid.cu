@@ -309,45 +309,54 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                                      (strip_base + (row_lane0 - a.v_start)) * (2 * kC) + c_lane
                                : nullptr;
     const bool col_ok = col0 + warp * kC + c_lane < a.n_u;      // (n_u >= 2: both columns or none)
+    // (branch-light: the stores are predicated, the band is cleared by a
+    // multiply with 0 / 1 -- a data-dependent branch around the accumulators
+    // made the compiler copy all of them at every window step)
     auto emit = [&]() {
         const int band = phase;            // band b lives in tile b / 4, lane rows 2(b % 4), +1
         const int row = Bfirst + 2 * step + (g4 & 1);
         const bool in_rows = row >= R0 && row < R1 && col_ok;
+        const bool mine_row = (g4 >> 1) == (band & 3);
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
-            if ((band >> 2) == m && (g4 >> 1) == (band & 3)) {
-                if (in_rows) {
-                    if (direct) {
-                        const int64_t o = (int64_t)step * (4 * kC);
-                        if (f32) {
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                *reinterpret_cast<float2 *>(ob32 + o + 8 * h) =
-                                    make_float2((float)acc[m][h][0].x, (float)acc[m][h][0].y);
-                                *reinterpret_cast<float2 *>(ob32 + o + kC + 8 * h) =
-                                    make_float2((float)acc[m][h][1].x, (float)acc[m][h][1].y);
-                            }
-                        } else {
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                *reinterpret_cast<double2 *>(ob + o + 8 * h) = acc[m][h][0];
-                                *reinterpret_cast<double2 *>(ob + o + kC + 8 * h) = acc[m][h][1];
-                            }
-                        }
-                    } else {
-                        // partial tile [row][re | im][64 columns] of the item
-                        double *pt_ = reinterpret_cast<double *>(ptile) + (int64_t)(row - R0) * (2 * kSS) +
-                                      warp * kC + c_lane;
+            const bool mine = mine_row && (band >> 2) == m;
+            if (mine && in_rows) {
+                if (direct) {
+                    const int64_t o = (int64_t)step * (4 * kC);
+                    if (f32) {
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            *reinterpret_cast<double2 *>(pt_ + 8 * h) = acc[m][h][0];
-                            *reinterpret_cast<double2 *>(pt_ + kSS + 8 * h) = acc[m][h][1];
+                            *reinterpret_cast<float2 *>(ob32 + o + 8 * h) =
+                                make_float2((float)acc[m][h][0].x, (float)acc[m][h][0].y);
+                            *reinterpret_cast<float2 *>(ob32 + o + kC + 8 * h) =
+                                make_float2((float)acc[m][h][1].x, (float)acc[m][h][1].y);
+                        }
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            *reinterpret_cast<double2 *>(ob + o + 8 * h) = acc[m][h][0];
+                            *reinterpret_cast<double2 *>(ob + o + kC + 8 * h) = acc[m][h][1];
                         }
                     }
-                }
+                } else {
+                    // partial tile [row][re | im][64 columns] of the item
+                    double *pt_ = reinterpret_cast<double *>(ptile) + (int64_t)(row - R0) * (2 * kSS) +
+                                  warp * kC + c_lane;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) acc[m][h][0] = acc[m][h][1] = make_double2(0.0, 0.0);
+                    for (int h = 0; h < 2; ++h) {
+                        *reinterpret_cast<double2 *>(pt_ + 8 * h) = acc[m][h][0];
+                        *reinterpret_cast<double2 *>(pt_ + kSS + 8 * h) = acc[m][h][1];
+                    }
+                }
             }
+            const double keep = mine ? 0.0 : 1.0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int ri = 0; ri < 2; ++ri) {
+                    acc[m][h][ri].x *= keep;
+                    acc[m][h][ri].y *= keep;
+                }
         }
         ++step;
         phase = phase + 1 == NB ? 0 : phase + 1;
@@ -468,37 +477,42 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             }
             const uint8_t *lp = sm.list[warp];
             const int wc8 = warp * kC + g4;        // this lane's B column (half 0) in the superstrip
+            // window steps: apply the step's records four at a time, then (if
+            // the chunk has more records) emit the step's rows. The emit stays
+            // out of the MMA loop: no accumulator copies around it.
 #pragma unroll 1
             for (;;) {
-                // the next four records of the list, one per k slot
-                const unsigned char *rp = recbase + (int)lp[k4] * (int)sizeof(Rec);
-                const int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
-                const bool match = mt.y == step;
-                const uint32_t m4 = __ballot_sync(0xffffffffu, match) & 0xFu;
-                if (!m4) {
-                    if (lp[0] == (uint8_t)kChunk) break;            // chunk done
-                    emit();                                         // rows above the next record are final
-                    continue;
-                }
-                if (!match) rp = recbase + kChunk * (int)sizeof(Rec);   // zero slot
-                const int ibr = match ? mt.x : 0;
-                // B: value x u weight at this lane's column of each 8-column half
-                const int c0 = wc8 - ibr;
-                const int i0 = (unsigned)c0 < (unsigned)W ? c0 : W;
-                const int i1 = (unsigned)(c0 + 8) < (unsigned)W ? c0 + 8 : W;
-                const double2 b0 = *reinterpret_cast<const double2 *>(rp + 16 * i0);
-                const double2 b1 = *reinterpret_cast<const double2 *>(rp + 16 * i1);
+#pragma unroll 1
+                for (;;) {
+                    // the next four records of the list, one per k slot
+                    const unsigned char *rp = recbase + (int)lp[k4] * (int)sizeof(Rec);
+                    const int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
+                    const bool match = mt.y == step;
+                    const uint32_t m4 = __ballot_sync(0xffffffffu, match) & 0xFu;
+                    if (!m4) break;
+                    if (!match) rp = recbase + kChunk * (int)sizeof(Rec);   // zero slot
+                    const int ibr = match ? mt.x : 0;
+                    // B: value x u weight at this lane's column of each 8-column half
+                    const int c0 = wc8 - ibr;
+                    const int i0 = (unsigned)c0 < (unsigned)W ? c0 : W;
+                    const int i1 = (unsigned)(c0 + 8) < (unsigned)W ? c0 + 8 : W;
+                    const double2 b0 = *reinterpret_cast<const double2 *>(rp + 16 * i0);
+                    const double2 b1 = *reinterpret_cast<const double2 *>(rp + 16 * i1);
 #pragma unroll
-                for (int m = 0; m < MT; ++m) {
-                    // A: this record's v weight on tile row g4 of tile m
-                    const int band = (4 * m + (g4 >> 1) - phase + NB) % NB;   // ring band -> window band
-                    const double av = reinterpret_cast<const double *>(rp + offsetof(Rec, wv))[2 * band + (g4 & 1)];
-                    dmma(acc[m][0][0], av, b0.x);
-                    dmma(acc[m][0][1], av, b0.y);
-                    dmma(acc[m][1][0], av, b1.x);
-                    dmma(acc[m][1][1], av, b1.y);
+                    for (int m = 0; m < MT; ++m) {
+                        // A: this record's v weight on tile row g4 of tile m
+                        const int band = (4 * m + (g4 >> 1) - phase + NB) % NB;   // ring -> window band
+                        const double av =
+                            reinterpret_cast<const double *>(rp + offsetof(Rec, wv))[2 * band + (g4 & 1)];
+                        dmma(acc[m][0][0], av, b0.x);
+                        dmma(acc[m][0][1], av, b0.y);
+                        dmma(acc[m][1][0], av, b1.x);
+                        dmma(acc[m][1][1], av, b1.y);
+                    }
+                    lp += __popc(m4);
                 }
-                lp += __popc(m4);
+                if (lp[0] == (uint8_t)kChunk) break;   // chunk done: the next one may continue this step
+                emit();                                  // rows above the next record are final
             }
         }
     }
