@@ -310,8 +310,8 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                                : nullptr;
     const bool col_ok = col0 + warp * kC + c_lane < a.n_u;      // (n_u >= 2: both columns or none)
     // (branch-light: the stores are predicated, the band is cleared by a
-    // multiply with 0 / 1 -- a data-dependent branch around the accumulators
-    // made the compiler copy all of them at every window step)
+    // multiply-add with 0 / 1 -- a data-dependent branch around the
+    // accumulators made the compiler copy all of them at every window step)
     auto emit = [&]() {
         const int band = phase;            // band b lives in tile b / 4, lane rows 2(b % 4), +1
         const int row = Bfirst + 2 * step + (g4 & 1);
@@ -354,8 +354,11 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             for (int h = 0; h < 2; ++h)
 #pragma unroll
                 for (int ri = 0; ri < 2; ++ri) {
-                    acc[m][h][ri].x *= keep;
-                    acc[m][h][ri].y *= keep;
+                    // x * keep + 0: a cleared band starts at +0 whatever its old
+                    // value (a product with 0 keeps the sign of zero), so no
+                    // cell's sign of zero depends on the sweep's history
+                    acc[m][h][ri].x = fma(acc[m][h][ri].x, keep, 0.0);
+                    acc[m][h][ri].y = fma(acc[m][h][ri].y, keep, 0.0);
                 }
         }
         ++step;
