@@ -545,17 +545,64 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
             pst[i] = __double2loint(t[i].x);
         }
     }
-    // The next plane's inputs are prefetched with asynchronous global->shared
-    // copies (LDGSTS) into thread-private slots of the otherwise idle second
-    // buffer: no registers held across the plane's transform.
+    // The next plane's inputs are prefetched into the otherwise idle second
+    // buffer while this plane is transformed: no registers held across it.
+    // FP64: TMA bulk copies (cp.async.bulk, one elected thread, completion on
+    // an mbarrier) of each column's contiguous runs -- one per source slab --
+    // into [column][row]; each thread then reads its first-pass inputs from
+    // shared memory. FP32 (8-byte elements, runs not always 16-byte
+    // multiples): per-thread asynchronous copies (LDGSTS) into private slots.
     V *pbuf = reinterpret_cast<V *>(sbuf + C * STRIDE);
-    auto prefetch = [&](int k) {
+    constexpr bool BULK = sizeof(V) == 16 && SPL == 0;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(zbuf + C * N);
+    const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bar);
+    int lidx[kColE];   // BULK: this thread's first-pass inputs at pbuf[lidx[i]]
+    if constexpr (BULK) {
+        double2 t[kColE];
+        pass_load<LOGN, P0::RL, kColE, CT>(
+            t, [&](int seq, int j) { return make_double2(__hiloint2double(seq * N + j, 0), 0.0); });
 #pragma unroll
-        for (int i = 0; i < kColE; ++i)
-            if (off[i] >= 0)
-                __pipeline_memcpy_async(&pbuf[i * CT + threadIdx.x], &tg[off[i] + k * pst[i]],
-                                        sizeof(V));
-        __pipeline_commit();
+        for (int i = 0; i < kColE; ++i) lidx[i] = __double2hiint(t[i].x);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+    }
+    uint32_t bar_phase = 0;
+    auto prefetch = [&](int k) {
+        if constexpr (BULK) {
+            if (threadIdx.x == 0) {
+                // the buffer was read through the generic proxy: order that
+                // before the async-proxy writes
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                uint32_t bytes = 0;
+                for (int cc = 0; cc < C && c0 + cc < a.ncols; ++cc)
+                    for (int sidx = 0; sidx < a.n_src; ++sidx)
+                        bytes += (uint32_t)(a.src_start[sidx + 1] - a.src_start[sidx]) * (uint32_t)sizeof(V);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s), "r"(bytes)
+                             : "memory");
+                for (int cc = 0; cc < C && c0 + cc < a.ncols; ++cc)
+                    for (int sidx = 0; sidx < a.n_src; ++sidx) {
+                        const int r0 = a.src_start[sidx], r1 = a.src_start[sidx + 1];
+                        const V *src = tg + (int64_t)nk * a.ncols * r0 +
+                                       ((int64_t)k * a.ncols + c0 + cc) * (r1 - r0);
+                        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pbuf + cc * N + r0);
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                                dst),
+                            "l"(src), "r"((uint32_t)((r1 - r0) * sizeof(V))), "r"(bar_s)
+                            : "memory");
+                    }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < kColE; ++i)
+                if (off[i] >= 0)
+                    __pipeline_memcpy_async(&pbuf[i * CT + threadIdx.x], &tg[off[i] + k * pst[i]],
+                                            sizeof(V));
+            __pipeline_commit();
+        }
     };
     // split columns: input k of the on-chip transform combines rows k + s N
     auto ld_split = [&](int kpl, int seq, int j) -> V {
@@ -600,7 +647,20 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
 
     for (int kl = nk - 1; kl >= 0; --kl) {
         V v[kColE];
-        if constexpr (SPL == 0) {
+        if constexpr (BULK) {
+            asm volatile(
+                "{\n .reg .pred p;\n WAIT_%=:\n"
+                " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                " @!p bra WAIT_%=;\n}\n" ::"r"(bar_s),
+                "r"(bar_phase)
+                : "memory");
+            bar_phase ^= 1;
+#pragma unroll
+            for (int i = 0; i < kColE; ++i) v[i] = off[i] >= 0 ? pbuf[lidx[i]] : cx<V>(0.0, 0.0);
+            __syncthreads();   // every thread has its inputs: the buffer takes the next plane
+            if (kl > 0) prefetch(kl - 1);
+            pass_compute<LOGN, P0::RL, kColE, CT>(1, tw, v);
+        } else if constexpr (SPL == 0) {
             __pipeline_wait_prior(0);
 #pragma unroll
             for (int i = 0; i < kColE; ++i)
@@ -826,7 +886,7 @@ int launch_cols(wsb_ctx *ctx, const ColArgs &a, const V *tw, int *nblocks, int s
     constexpr int CT = ColCfg<LOGN>::T;
     constexpr int C = CT * kColE / N;
     // the finish stages complex128 pixels whatever the transform precision
-    const size_t smem = sizeof(double2) * (2 * C * Seq<LOGN>::STRIDE + C * N);
+    const size_t smem = sizeof(double2) * (2 * C * Seq<LOGN>::STRIDE + C * N) + 16;   // + mbarrier
     *nblocks = ceil_div(a.ncols, C);
     const dim3 grd(*nblocks, 1 << spl);
     if (spl == 0) {
