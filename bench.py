@@ -395,6 +395,11 @@ def run_ours(args):
         "e2e": e2e,
         "energy": energy,
     }
+    if ws == 1 and not args.no_cfg3:
+        try:
+            out["cfg3"] = bench_cfg3(W, peak)
+        except Exception as exc:   # report, do not fail the headline line
+            out["cfg3"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
     if ws == 1 and not args.no_cpu_baseline:
         cb = out["cpu_baseline"] = cpu_baseline(cfg)
         # green productivity, Eq. 4 (metrics.py:200-207): reference run = the
@@ -417,6 +422,61 @@ def run_ours(args):
     if ws > 1:
         dist.destroy_process_group()
     print(json.dumps(out), flush=True)
+
+
+def bench_cfg3(W, peak, steps=5):
+    """The north-star configuration on this GPU (BASELINE config 3): 100M
+    LOFAR-like track records (tools/lofar.py, generated on the device),
+    4096^2 x 64, Gaussian support 7, FP64. Device-resident inputs, CUDA
+    events, per-kernel fractions of the HBM roofline against the SURVEY 8(d)
+    algorithmic bytes, and the size-independent parity property the full
+    size allows (linearity over complementary record halves; the
+    slab-restricted oracle check of the densest rows is
+    tests/test_gpu_scale.py::test_cfg3_densest_rows_vs_slab_restricted_oracle)."""
+    import torch
+    sys.path.insert(0, str(ROOT / "tools"))
+    from lofar import tracks
+    n, nu, nw, cell = 100_000_000, 4096, 64, 1e-4
+    dev = torch.device("cuda", 0)
+    u, v, w, t, vis, wt = tracks(n, cell, device=dev)
+    spec = W.GridSpec(nu, nu, nw, cell, w_max_native=1000.0)
+    kern = W.KernelSpec.gaussian(3, 1.0)
+    for _ in range(2):
+        W.image_device(u, v, w, vis, wt, spec, kern)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms_k = np.zeros(6)
+    e0.record(stream)
+    for _ in range(steps):
+        W.image_device(u, v, w, vis, wt, spec, kern)
+        ms_k += np.array(W.last_timings(dev)[0])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    ms_k /= steps
+    cfg = dict(n_vis=n, n_u=nu, n_v=nu, n_w=nw)
+    kernels = {}
+    for name, (b, t_ms) in kernel_table(cfg, ms_k).items():
+        ach = b / (t_ms / 1e3) / 1e9 if t_ms > 0 else 0.0
+        kernels[name] = {"ms": round(t_ms, 3), "algorithmic_bytes": int(b),
+                         "floor_ms": round(b / (peak * 1e9) * 1e3, 3),
+                         "achieved_gbs": round(ach, 1), "frac": round(ach / peak, 3)}
+    # linearity: image(all) = image(A) + image(B), complementary weight halves
+    g = torch.Generator(device=dev).manual_seed(7)
+    mask = torch.rand(wt.shape, generator=g, device=dev) < 0.5
+    pall, _ = W.image_device(u, v, w, vis, wt, spec, kern)
+    pall = pall.clone()
+    pa, _ = W.image_device(u, v, w, vis, torch.where(mask, wt, torch.zeros_like(wt)), spec, kern)
+    pa = pa.clone()
+    pb, d = W.image_device(u, v, w, vis, torch.where(mask, torch.zeros_like(wt), wt), spec, kern)
+    lin = float((pall - pa - pb).norm() / pall.norm())
+    return {"workload": "cfg3: 100M LOFAR-like track records (62 stations, tools/lofar.py), "
+                        "4096x4096 grid, 64 w-planes, Gaussian support 7, FP64, 1 GPU",
+            "value": round(n / (ms / 1e3) / 1e6, 1), "unit": "Mvis/s", "ms_per_step": round(ms, 3),
+            "steps": steps, "grid_updates": int(d["grid_updates"]), "kernels": kernels,
+            "parity": {"linearity_rel_l2": lin, "ok": lin <= 1e-10,
+                       "oracle": "tests/test_gpu_scale.py::test_cfg3_densest_rows_vs_slab_restricted_oracle"}}
 
 
 def cpu_cores():
@@ -561,6 +621,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cfg3", action="store_true", help="skip the cfg3 (north-star) object")
     ap.add_argument("--decomp", choices=["auto", "slabs", "planes"], default="auto",
                     help="multi-GPU decomposition: v-slabs (grid transpose) or w-plane ranges "
                          "(partial-stack reduce)")

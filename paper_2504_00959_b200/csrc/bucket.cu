@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
     if (tid == 0 && FROM_INPUT && sm.err) atomicOr(a.err, sm.err);
     (void)agg;
     uint32_t pos = a.block_off[bid] + wbase + incl - mine;
+    WSB_DCHECK((int64_t)pos + mine <= 4 * a.n, "tile %u pos %u", bid, pos);
     // (static indices: the entry arrays stay in registers)
 #pragma unroll
     for (int r = 0; r < kPer; ++r)
@@ -409,6 +410,7 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     out->off = off;
     out->n_entries = n_entries;
     out->n_items = n_items;
+    out->n_rec = m;
     out->n_ss = k.n_ss;
     out->n_rb = k.n_rb;
     out->item_bits = k.item_bits;

@@ -733,7 +733,7 @@ int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
     a.part_rows = part_rows;
     a.partial = partial;
     a.n_parts = n_parts;
-    a.n_rec = 0x7FFFFFFF;
+    a.n_rec = bk.n_rec;
     a.out_elems = (int64_t)g->n_w * a.n_s16 * kC * v_count;
     // ---- sweep ---------------------------------------------------------------
     int rc;

@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
         const uint32_t key = sm.ks[p];
         const uint32_t d = (key >> shift) & dmask;
         const uint32_t gpos = sm.goff[d] + (p - sm.bstart[d]);
+        WSB_DCHECK(gpos < n, "radix gpos %u n %lld", gpos, (long long)n);
         kout[gpos] = key;
         vout[gpos] = sm.vs[p];
     }

@@ -179,7 +179,7 @@ struct ItemBuckets {
     uint32_t *keys = nullptr;  // item << kRowBits | rowrel, sorted: (item, row, record) order
     uint32_t *idx = nullptr;   // record index per entry
     uint32_t *off = nullptr;   // [n_items + 1] exclusive offsets
-    int64_t n_entries = 0, n_items = 0;
+    int64_t n_entries = 0, n_items = 0, n_rec = 0;
     int n_ss = 0, n_rb = 0, item_bits = 0;
 };
 // in != nullptr: records are prepared from the columns on the fly (rec
