@@ -292,16 +292,6 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         for (int h = 0; h < 2; ++h) acc[m][h][0] = acc[m][h][1] = make_double2(0.0, 0.0);
     int step = step0, phase = step0 % NB;
     unsigned cnt_upd = 0;
-    // byte offset of this lane's A operand (tile row g4 of tile 0) inside a
-    // staged record: window row 2((g4/2 - phase) mod NB) + g4%2 (tile m adds 8 rows)
-    // (tile m: window row + 8m, wrapped: the ring spans ROWS rows)
-    int a_off[MT];
-    auto a_offset = [&]() {
-        const int row0 = 2 * (((g4 >> 1) - phase + NB) % NB) + (g4 & 1);
-#pragma unroll
-        for (int m = 0; m < MT; ++m) a_off[m] = (int)offsetof(Rec, wv) + 8 * ((row0 + 8 * m) % ROWS);
-    };
-    a_offset();
     const int64_t strip_base = ((int64_t)plane * a.n_s16 + (col0 / kC + warp)) * a.v_count;
     double2 *const ptile = direct ? nullptr : a.partial + (int64_t)pd.w * kItemRows * kSS;
 
@@ -373,7 +363,6 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         }
         ++step;
         phase = phase + 1 == NB ? 0 : phase + 1;
-        a_offset();
     };
 
     // gather: thread pair (2r, 2r+1) copies record r's two 16-byte halves;
@@ -491,12 +480,11 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             }
             const uint8_t *lp = sm.list[warp];
             const int wc8 = warp * kC + g4;        // this lane's B column (half 0) in the superstrip
-            // window steps: apply the step's records four at a time, then emit
-            // rows up to the next record's step (no re-probe per empty step).
-            // The emit stays out of the MMA loop: no accumulator copies around it.
+            // window steps: apply the step's records four at a time, then (if
+            // the chunk has more records) emit the step's rows. The emit stays
+            // out of the MMA loop: no accumulator copies around it.
 #pragma unroll 1
             for (;;) {
-                int snext;
 #pragma unroll 1
                 for (;;) {
                     // the next four records of the list, one per k slot
@@ -504,10 +492,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                     const int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
                     const bool match = mt.y == step;
                     const uint32_t m4 = __ballot_sync(0xffffffffu, match) & 0xFu;
-                    if (!m4) {
-                        snext = __shfl_sync(0xffffffffu, mt.y, 0);   // slot 0: the next record
-                        break;
-                    }
+                    if (!m4) break;
                     if (!match) rp = recbase + kChunk * (int)sizeof(Rec);   // zero slot
                     const int ibr = match ? mt.x : 0;
                     // B: value x u weight at this lane's column of each 8-column half
@@ -519,7 +504,9 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
 #pragma unroll
                     for (int m = 0; m < MT; ++m) {
                         // A: this record's v weight on tile row g4 of tile m
-                        const double av = *reinterpret_cast<const double *>(rp + a_off[m]);
+                        const int band = (4 * m + (g4 >> 1) - phase + NB) % NB;   // ring -> window band
+                        const double av =
+                            reinterpret_cast<const double *>(rp + offsetof(Rec, wv))[2 * band + (g4 & 1)];
                         dmma(acc[m][0][0], av, b0.x);
                         dmma(acc[m][0][1], av, b0.y);
                         dmma(acc[m][1][0], av, b1.x);
@@ -527,9 +514,8 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                     }
                     lp += __popc(m4);
                 }
-                if (snext < 0) break;                   // chunk done: the next one may continue this step
-                do emit();                              // rows above the next record are final
-                while (step < snext);
+                if (lp[0] == (uint8_t)kChunk) break;   // chunk done: the next one may continue this step
+                emit();                                  // rows above the next record are final
             }
         }
     }
