@@ -27,7 +27,7 @@ def main():
         unit = r.get("Metric Unit", "ns")
         us = v / 1e3 if unit == "nsecond" or unit == "ns" else (v if unit in ("usecond", "us") else v * 1e3)
         rows.append((int(r["ID"]), short(r["Kernel Name"]), us))
-    starts = [i for i, (_, k, _) in enumerate(rows) if k == "k_prepare"]
+    starts = [i for i, (_, k, _) in enumerate(rows) if k in ("k_prepare", "k_count<true>", "k_count<1>")]
     if len(starts) >= 2:
         a, b = starts[-2], starts[-1]
     else:
