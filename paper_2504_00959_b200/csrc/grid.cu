@@ -215,7 +215,9 @@ struct Shm {
     static constexpr int NROW = kItemRows + 2 * S;   // anchor rows that reach the item
     StagedRec<S> rec[kChunk + 1];   // + a zero sentinel (window step -1) ending every list
     double4 raw[kRaw][kChunk];      // gathered records (gu, gv, Re, Im)
-    uint8_t list[kWarps][kChunk + 8];      // per strip: the chunk's records touching it, in order
+    int pstep[kWarps][kChunk];             // per strip: window steps of its records, list order
+    uint8_t prec[kWarps][kChunk];          //   and their records
+    uint2 kst[kWarps][kChunk + 1];         // per strip: MMA steps (4 record bytes, window step); -1 ends
 };
 
 template <int KIND, int S>
@@ -465,57 +467,79 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         __syncthreads();   // stage complete
         // ---- sweep: this warp's strip ---------------------------------------
         {
-            // records of this chunk touching the strip, in order, as a byte list
-            // padded with sentinels
+            // The chunk's records touching the strip, in order, cut into MMA
+            // steps: runs of records with the same window step, four at a time.
+            // Each MMA step is one (record bytes, window step) entry; empty
+            // slots name the zero sentinel record. The sweep then needs no
+            // probing or voting per record.
+            const uint32_t lt = (1u << lane) - 1u, le = (2u << lane) - 1u;
             {
-                const uint32_t m0 = __ballot_sync(0xffffffffu, lane < nr && ((sm.rec[lane].meta.w >> warp) & 1));
-                const uint32_t m1 =
-                    __ballot_sync(0xffffffffu, 32 + lane < nr && ((sm.rec[32 + lane].meta.w >> warp) & 1));
-                const uint32_t lt = (1u << lane) - 1u;
+                const bool t0 = lane < nr && ((sm.rec[lane].meta.w >> warp) & 1);
+                const bool t1 = 32 + lane < nr && ((sm.rec[32 + lane].meta.w >> warp) & 1);
+                const uint32_t m0 = __ballot_sync(0xffffffffu, t0);
+                const uint32_t m1 = __ballot_sync(0xffffffffu, t1);
+                if (t0) {
+                    const int p_ = __popc(m0 & lt);
+                    sm.pstep[warp][p_] = sm.rec[lane].meta.y;
+                    sm.prec[warp][p_] = (uint8_t)lane;
+                }
+                if (t1) {
+                    const int p_ = __popc(m0) + __popc(m1 & lt);
+                    sm.pstep[warp][p_] = sm.rec[32 + lane].meta.y;
+                    sm.prec[warp][p_] = (uint8_t)(32 + lane);
+                }
                 const int tot = __popc(m0) + __popc(m1);
-                if ((m0 >> lane) & 1) sm.list[warp][__popc(m0 & lt)] = (uint8_t)lane;
-                if ((m1 >> lane) & 1) sm.list[warp][__popc(m0) + __popc(m1 & lt)] = (uint8_t)(32 + lane);
-                if (lane < 8) sm.list[warp][tot + lane] = (uint8_t)kChunk;
+                __syncwarp();
+                // positions p = lane (round a) and 32 + lane (round b)
+                const bool va = lane < tot, vb = 32 + lane < tot;
+                const int sa = va ? sm.pstep[warp][lane] : 0;
+                const int sb = vb ? sm.pstep[warp][32 + lane] : 0;
+                const int pa = lane > 0 ? sm.pstep[warp][lane - 1] : -2;
+                const int pb = sm.pstep[warp][31 + lane];
+                const uint32_t fa = __ballot_sync(0xffffffffu, va && sa != pa);   // run starts
+                const uint32_t fb = __ballot_sync(0xffffffffu, vb && sb != pb);
+                const int ra = 31 - __clz(fa & le);
+                const int rb = (fb & le) ? 32 + 31 - __clz(fb & le) : 31 - __clz(fa);
+                const int slot_a = (lane - ra) & 3, slot_b = (32 + lane - rb) & 3;
+                const uint32_t ka = __ballot_sync(0xffffffffu, va && slot_a == 0);   // MMA step starts
+                const uint32_t kb = __ballot_sync(0xffffffffu, vb && slot_b == 0);
+                const int kia = __popc(ka & le) - 1, kib = __popc(ka) + __popc(kb & le) - 1;
+                const uint32_t empty = (uint32_t)kChunk * 0x01010101u;
+                if (va && slot_a == 0) sm.kst[warp][kia] = make_uint2(empty, (uint32_t)sa);
+                if (vb && slot_b == 0) sm.kst[warp][kib] = make_uint2(empty, (uint32_t)sb);
+                if (lane == 0) sm.kst[warp][__popc(ka) + __popc(kb)] = make_uint2(empty, 0xFFFFFFFFu);
+                __syncwarp();
+                if (va) reinterpret_cast<uint8_t *>(&sm.kst[warp][kia].x)[slot_a] = sm.prec[warp][lane];
+                if (vb) reinterpret_cast<uint8_t *>(&sm.kst[warp][kib].x)[slot_b] = sm.prec[warp][32 + lane];
                 __syncwarp();
             }
-            const uint8_t *lp = sm.list[warp];
+            const uint2 *ke = sm.kst[warp];
             const int wc8 = warp * kC + g4;        // this lane's B column (half 0) in the superstrip
-            // window steps: apply the step's records four at a time, then (if
-            // the chunk has more records) emit the step's rows. The emit stays
-            // out of the MMA loop: no accumulator copies around it.
 #pragma unroll 1
             for (;;) {
-#pragma unroll 1
-                for (;;) {
-                    // the next four records of the list, one per k slot
-                    const unsigned char *rp = recbase + (int)lp[k4] * (int)sizeof(Rec);
-                    const int4 mt = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
-                    const bool match = mt.y == step;
-                    const uint32_t m4 = __ballot_sync(0xffffffffu, match) & 0xFu;
-                    if (!m4) break;
-                    if (!match) rp = recbase + kChunk * (int)sizeof(Rec);   // zero slot
-                    const int ibr = match ? mt.x : 0;
-                    // B: value x u weight at this lane's column of each 8-column half
-                    const int c0 = wc8 - ibr;
-                    const int i0 = (unsigned)c0 < (unsigned)W ? c0 : W;
-                    const int i1 = (unsigned)(c0 + 8) < (unsigned)W ? c0 + 8 : W;
-                    const double2 b0 = *reinterpret_cast<const double2 *>(rp + 16 * i0);
-                    const double2 b1 = *reinterpret_cast<const double2 *>(rp + 16 * i1);
+                const uint2 en = *ke++;
+                const int est = (int)en.y;
+                if (est < 0) break;                        // chunk done: the next one may continue this step
+                while (step < est) emit();                 // rows above the step are final
+                const unsigned char *rp = recbase + (int)((en.x >> (8 * k4)) & 0xFFu) * (int)sizeof(Rec);
+                const int ibr = reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta))->x;
+                // B: value x u weight at this lane's column of each 8-column half
+                const int c0 = wc8 - ibr;
+                const int i0 = (unsigned)c0 < (unsigned)W ? c0 : W;
+                const int i1 = (unsigned)(c0 + 8) < (unsigned)W ? c0 + 8 : W;
+                const double2 b0 = *reinterpret_cast<const double2 *>(rp + 16 * i0);
+                const double2 b1 = *reinterpret_cast<const double2 *>(rp + 16 * i1);
 #pragma unroll
-                    for (int m = 0; m < MT; ++m) {
-                        // A: this record's v weight on tile row g4 of tile m
-                        const int band = (4 * m + (g4 >> 1) - phase + NB) % NB;   // ring -> window band
-                        const double av =
-                            reinterpret_cast<const double *>(rp + offsetof(Rec, wv))[2 * band + (g4 & 1)];
-                        dmma(acc[m][0][0], av, b0.x);
-                        dmma(acc[m][0][1], av, b0.y);
-                        dmma(acc[m][1][0], av, b1.x);
-                        dmma(acc[m][1][1], av, b1.y);
-                    }
-                    lp += __popc(m4);
+                for (int m = 0; m < MT; ++m) {
+                    // A: this record's v weight on tile row g4 of tile m
+                    const int band = (4 * m + (g4 >> 1) - phase) & (NB - 1);   // ring -> window band
+                    const double av =
+                        reinterpret_cast<const double *>(rp + offsetof(Rec, wv))[2 * band + (g4 & 1)];
+                    dmma(acc[m][0][0], av, b0.x);
+                    dmma(acc[m][0][1], av, b0.y);
+                    dmma(acc[m][1][0], av, b1.x);
+                    dmma(acc[m][1][1], av, b1.y);
                 }
-                if (lp[0] == (uint8_t)kChunk) break;   // chunk done: the next one may continue this step
-                emit();                                  // rows above the next record are final
             }
         }
     }
