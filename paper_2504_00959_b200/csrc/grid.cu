@@ -1,32 +1,28 @@
-// K2: register-window gridder over (plane, 64-column superstrip, 128-row
+// K2: tensor-core window gridder over (plane, 64-column superstrip, 128-row
 // block) work items (gridder.py:160-259, Eq. 3).
 //
-// CTA = 4 warps = one item; warp w owns the 16 columns [16w, 16w+16) of the
-// superstrip. Inside a warp, lane = (row group q = lane / 16, column c =
-// lane % 16): lane (q, c) accumulates the rows B + q + 2t (t = 0..S) of its
-// column as complex128 registers, a window of 2S+2 rows that slides down the
-// block two rows at a time (a ring of S+1 slots, one code copy per ring
-// phase). A record with anchor row a = floor(gv) - S is applied while
-// a - B is 0 or 1: its 2S+1 footprint rows then lie inside the window. When
-// the next record starts lower, rows B and B+1 are final: the 32 lanes write
-// them as one 512-byte run (strip layout [plane][col/16][row][16], the
-// checkerboard sign of transform.py:180-185 applied) and the window moves on.
-// Each cell is accumulated by one lane, in (window step, record) order --
+// CTA = 4 warps = one item (or one part of a large item); warp w owns the 16
+// columns [16w, 16w+16) of the superstrip. Its accumulator is a window of
+// 8-row tiles held as FP64 MMA fragments (m8n8k4: lane = row lane/4, columns
+// 2(lane%4), +1 of an 8x8 tile; two column halves x Re/Im per tile). The
+// item's records arrive sorted by anchor row (K1); four records at a time are
+// applied as rank-4 updates D += A B of every tile they reach, A = their v
+// weights on the tile rows (row sign folded), B = value x u weight on the
+// columns (column sign folded) -- one DMMA instruction per 256 multiply-adds
+// on the FP64 tensor cores. When the records move past a tile it is final:
+// the 32 lanes store it (8 rows x 16 columns, re | im) straight from the
+// fragments, clear it and the window moves 8 rows down (a ring of tiles,
+// one code copy per ring phase).
+//
+// Each cell accumulates in (anchor row, record) order in groups of four --
 // deterministic, and the same for any GPU count when slabs start on 128-row
-// boundaries (items then hold the same records) -- and written once: no
+// boundaries (items then hold the same records) -- and is written once: no
 // shared-memory tile, no atomics, no read-modify-write of HBM.
 //
-// Versus one lane per column and a (2S+1)-row window (round 1: 7 of 32
-// lanes carried a record's taps at S=3), a record now occupies 2 x 16 lanes
-// x (S+1) rows: the FMA work per record falls from 14 to 8 double
-// instructions per touched 16-column strip at S=3.
-//
-// Records reach an item in record order (the stable bucketing of bucket.cu);
-// the CTA first sorts its item's entry list by window step in shared memory
-// (counting sort, stable, warp match/ballot ranks), then streams it in
-// chunks of 64 records gathered by cp.async two chunks ahead. Two threads
-// stage a record: one forms value * u-weight for the window columns, the
-// other the v weights in the parity-split order the lane groups read.
+// Records stream through the CTA in chunks of 64 gathered by cp.async two
+// chunks ahead (record index prefetched a chunk before its gather). Two
+// threads stage a record: one forms value x u weight per window column, the
+// other the v weights at the record's row offset in its 8-row step.
 #include <type_traits>
 
 #include "i0_coeffs.h"
@@ -189,14 +185,18 @@ struct SweepArgs {
     int64_t n_rec, out_elems;  // bounds (debug checks)
 };
 
-// Window of the tensor-core sweep: 8 * MT rows (MT = 1 for S <= 3, else 2),
-// a ring of 2-row bands; the two 16-column halves x (Re, Im) of each 8-row
-// band are four 8x8 FP64 MMA accumulators.
+// Window of the tensor-core sweep: a ring of NT tiles of 8 rows; a window
+// step is 8 rows. A record anchored at offset d (0..7) in its step's first
+// tile covers rows d .. d+2S: NTR = ceil((2S+8)/8) tiles from its step.
+// WSB_WIN_EXTRA extra tiles let a group of records span that many steps.
+#ifndef WSB_WIN_EXTRA
+#define WSB_WIN_EXTRA 0
+#endif
 template <int S>
 struct Win {
-    static constexpr int MT = (2 * S + 2 <= 8) ? 1 : 2;
-    static constexpr int ROWS = 8 * MT;
-    static constexpr int NB = ROWS / 2;            // 2-row bands in the ring
+    static constexpr int W = 2 * S + 1;
+    static constexpr int NTR = (W + 7 + 7) / 8;     // 2 for S <= 4, 3 for S <= 8
+    static constexpr int NT = NTR + WSB_WIN_EXTRA;
 };
 
 // One staged record: everything a lane reads to apply it, at one base
@@ -204,25 +204,23 @@ struct Win {
 template <int S>
 struct StagedRec {
     static constexpr int W = 2 * S + 1;
-    static constexpr int NV = Win<S>::ROWS;
-    double2 tu[W + 1];     // value * u weight per window column; slot W = 0
-    double wv[NV];         // v weight of window row b (0 .. ROWS-1 from the window base); 0 off the footprint
+    static constexpr int NV = 8 * Win<S>::NTR;
+    double2 tu[W + 1];     // value * u weight per window column; slot W = 0 (signs folded)
+    double wv[NV];         // v weight of row b = d .. d+W-1 of the record's step; 0 elsewhere
     int4 meta;             // (first window column - superstrip col0, window step, row offset d, strip mask)
 };
 
 template <int KIND, int S>
 struct Shm {
     static constexpr int NROW = kItemRows + 2 * S;   // anchor rows that reach the item
-    StagedRec<S> rec[kChunk + 1];   // + a zero sentinel (window step -1) ending every list
+    StagedRec<S> rec[kChunk + 1];   // + a zero sentinel filling the last group
     double4 raw[kRaw][kChunk];      // gathered records (gu, gv, Re, Im)
-    int pstep[kWarps][kChunk];             // per strip: window steps of its records, list order
-    uint8_t prec[kWarps][kChunk];          //   and their records
-    uint2 kst[kWarps][kChunk + 1];         // per strip: MMA steps (4 record bytes, window step); -1 ends
+    uint8_t prec[kWarps][kChunk];   // per strip: the chunk's records touching it, in order
 };
 
 template <int KIND, int S>
 constexpr int sweep_min_blocks() {
-    return 6;
+    return S <= 4 ? 6 : 4;
 }
 
 // m8n8k4 FP64 MMA, D = A B + D: a(row lane/4, k lane%4), b(k lane%4, col lane/4),
@@ -239,8 +237,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     constexpr int W = 2 * S + 1;
     using Sm = Shm<KIND, S>;
     using Rec = StagedRec<S>;
-    constexpr int MT = Win<S>::MT, ROWS = Win<S>::ROWS, NB = Win<S>::NB;
-    constexpr int NROW = Sm::NROW;
+    constexpr int NT = Win<S>::NT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Sm &sm = *reinterpret_cast<Sm *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -253,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     const int col0 = ss * kSS;
     const int R0 = a.v_start + rb * kItemRows;
     const int R1 = min(R0 + kItemRows, a.v_start + a.v_count);
-    const int Bfirst = R0 - 2 * S;      // window base of step 0
+    const int Bfirst = R0 - 2 * S;      // first anchor row that reaches the block: window base of step 0
     const uint32_t eb = pd.y, n = pd.z - pd.y;
     const bool direct = pd.w == 0xFFFFFFFFu;
 
@@ -263,108 +260,85 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     // records reach, recorded for k_combine.
     const int rr_first = n ? (int)(__ldg(&a.keys[eb]) & 0xFFu) : 0;
     const int rr_last = n ? (int)(__ldg(&a.keys[eb + n - 1]) & 0xFFu) : 0;
-    const int step0 = direct ? 0 : rr_first >> 1;
+    const int step0 = direct ? 0 : rr_first >> 3;
     const int row_end = direct ? R1 : min(R1, Bfirst + rr_last + 2 * S + 1);
     if (!direct && tid == 0)
-        a.part_rows[blockIdx.x] = make_uint2((uint32_t)max(Bfirst + 2 * step0 - R0, 0),
+        a.part_rows[blockIdx.x] = make_uint2((uint32_t)max(Bfirst + 8 * step0 - R0, 0),
                                              (uint32_t)max(row_end - R0, 0));
 
     // ---- the sweep --------------------------------------------------------
     // Warp w owns columns [16w, 16w+16) of the superstrip. Its window holds
-    // rows B .. B+ROWS-1 (B = Bfirst + 2 step) in a ring of 2-row bands:
-    // band (phase + t) % NB holds rows B + 2t, B + 2t + 1. The records of a
-    // window step (anchor rows B, B+1) are applied four at a time as one
-    // rank-4 update per 8x8 accumulator tile: A = their v weights on the
-    // tile's rows, B = value x u weight on its columns (FP64 tensor cores:
-    // one MMA instruction per 256 multiply-adds instead of 8 DFMA per record
-    // and lane). When the next record starts lower, band `phase` (rows B,
-    // B+1) is final: its 8 lanes write it (512 bytes), clear it, and the
-    // window moves two rows down.
+    // rows B .. B + 8 NT - 1 (B = Bfirst + 8 step) as a ring of NT tiles of 8
+    // rows: tile (phase + t) % NT holds rows B + 8t .. B + 8t + 7, as four 8x8
+    // FP64 MMA accumulators (two 8-column halves x Re/Im; lane holds row
+    // lane/4, columns 2(lane%4), +1). The records of a window step (anchor
+    // rows B .. B+7) are applied four at a time as one rank-4 update per tile
+    // they reach: A = their v weights on the tile's rows, B = value x u weight
+    // on its columns (FP64 tensor cores: one MMA instruction per 256
+    // multiply-adds). When the records move on to a later step, tile `phase`
+    // (rows B .. B+7) is final: the 32 lanes write it (8 rows x 16 columns,
+    // re | im, 2 KB), clear it, and the window moves 8 rows down.
     const double i0b = KIND == WSB_KERNEL_KAISER_BESSEL ? *a.i0beta : 0.0;
-    double2 *const outp = (double2 *)a.out;
-    float2 *const out32 = (float2 *)a.out;
     const bool f32 = direct && a.out_f32;
     const int g4 = lane >> 2, k4 = lane & 3;       // MMA fragment coordinates
-    // accumulators: [m tile][n half][Re/Im], lane holds row g4 of the tile and
-    // columns 2 k4, 2 k4 + 1 of the half
-    double2 acc[MT][2][2];
+    double2 acc[NT][2][2];                         // [ring tile][column half][Re, Im]
 #pragma unroll
-    for (int m = 0; m < MT; ++m)
+    for (int t = 0; t < NT; ++t)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) acc[m][h][0] = acc[m][h][1] = make_double2(0.0, 0.0);
-    int step = step0, phase = step0 % NB;
+        for (int h = 0; h < 2; ++h) acc[t][h][0] = acc[t][h][1] = make_double2(0.0, 0.0);
+    int step = step0, phase = step0 % NT;
     unsigned cnt_upd = 0;
     const int64_t strip_base = ((int64_t)plane * a.n_s16 + (col0 / kC + warp)) * a.v_count;
     double2 *const ptile = direct ? nullptr : a.partial + (int64_t)pd.w * kItemRows * kSS;
-
-    // rows B, B+1 final: the lanes of band `phase` write them (already
-    // signed), clear them. Output strip rows hold 16 real parts, then 16
-    // imaginary parts: a lane's two columns of a half are one 16-byte store
-    // straight from its accumulator fragment. The lane's destination for
-    // window step `step` is ob + 64 * step doubles (two strip rows per step).
-    const int c_lane = 2 * k4;                                  // + 8 h: column in the strip
-    const int64_t row_lane0 = (int64_t)Bfirst + (g4 & 1);       // mesh row at step 0
+    // Output strip rows hold 16 real parts, then 16 imaginary parts: a lane's
+    // two columns of a half are one 16-byte store straight from its
+    // accumulator fragment. Lane row at step s: Bfirst + 8 s + g4.
+    const int c_lane = 2 * k4;
     double *const ob = direct ? reinterpret_cast<double *>(a.out) +
-                                    (strip_base + (row_lane0 - a.v_start)) * (2 * kC) + c_lane
+                                    (strip_base + ((int64_t)Bfirst + g4 - a.v_start)) * (2 * kC) + c_lane
                               : nullptr;
     float *const ob32 = direct ? reinterpret_cast<float *>(a.out) +
-                                     (strip_base + (row_lane0 - a.v_start)) * (2 * kC) + c_lane
+                                     (strip_base + ((int64_t)Bfirst + g4 - a.v_start)) * (2 * kC) + c_lane
                                : nullptr;
-    const bool col_ok = col0 + warp * kC + c_lane < a.n_u;      // (n_u >= 2: both columns or none)
-    // (branch-light: the stores are predicated, the band is cleared by a
-    // multiply-add with 0 / 1 -- a data-dependent branch around the
-    // accumulators made the compiler copy all of them at every window step)
-    auto emit = [&]() {
-        const int band = phase;            // band b lives in tile b / 4, lane rows 2(b % 4), +1
-        const int row = Bfirst + 2 * step + (g4 & 1);
-        const bool in_rows = row >= R0 && row < R1 && col_ok;
-        const bool mine_row = (g4 >> 1) == (band & 3);
-#pragma unroll
-        for (int m = 0; m < MT; ++m) {
-            const bool mine = mine_row && (band >> 2) == m;
-            if (mine && in_rows) {
-                if (direct) {
-                    const int64_t o = (int64_t)step * (4 * kC);
-                    if (f32) {
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            *reinterpret_cast<float2 *>(ob32 + o + 8 * h) =
-                                make_float2((float)acc[m][h][0].x, (float)acc[m][h][0].y);
-                            *reinterpret_cast<float2 *>(ob32 + o + kC + 8 * h) =
-                                make_float2((float)acc[m][h][1].x, (float)acc[m][h][1].y);
-                        }
-                    } else {
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            *reinterpret_cast<double2 *>(ob + o + 8 * h) = acc[m][h][0];
-                            *reinterpret_cast<double2 *>(ob + o + kC + 8 * h) = acc[m][h][1];
-                        }
-                    }
-                } else {
-                    // partial tile [row][re | im][64 columns] of the item
-                    double *pt_ = reinterpret_cast<double *>(ptile) + (int64_t)(row - R0) * (2 * kSS) +
-                                  warp * kC + c_lane;
+    const bool col_ok = col0 + warp * kC + c_lane < a.n_u;
+
+    // tile `P` (rows B .. B+7) final: write, clear, move the window
+    auto emit = [&](auto P) {
+        constexpr int p = decltype(P)::value;
+        const int row = Bfirst + 8 * step + g4;
+        if (row >= R0 && row < R1 && col_ok) {
+            if (direct) {
+                const int64_t o = (int64_t)step * (16 * kC);        // 8 rows x (16 re + 16 im)
+                if (f32) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        *reinterpret_cast<double2 *>(pt_ + 8 * h) = acc[m][h][0];
-                        *reinterpret_cast<double2 *>(pt_ + kSS + 8 * h) = acc[m][h][1];
+                        *reinterpret_cast<float2 *>(ob32 + o + 8 * h) =
+                            make_float2((float)acc[p][h][0].x, (float)acc[p][h][0].y);
+                        *reinterpret_cast<float2 *>(ob32 + o + kC + 8 * h) =
+                            make_float2((float)acc[p][h][1].x, (float)acc[p][h][1].y);
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        *reinterpret_cast<double2 *>(ob + o + 8 * h) = acc[p][h][0];
+                        *reinterpret_cast<double2 *>(ob + o + kC + 8 * h) = acc[p][h][1];
                     }
                 }
-            }
-            const double keep = mine ? 0.0 : 1.0;
+            } else {
+                // partial tile [row][re | im][64 columns] of the item
+                double *pt_ = reinterpret_cast<double *>(ptile) + (int64_t)(row - R0) * (2 * kSS) +
+                              warp * kC + c_lane;
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int ri = 0; ri < 2; ++ri) {
-                    // x * keep + 0: a cleared band starts at +0 whatever its old
-                    // value (a product with 0 keeps the sign of zero), so no
-                    // cell's sign of zero depends on the sweep's history
-                    acc[m][h][ri].x = fma(acc[m][h][ri].x, keep, 0.0);
-                    acc[m][h][ri].y = fma(acc[m][h][ri].y, keep, 0.0);
+                for (int h = 0; h < 2; ++h) {
+                    *reinterpret_cast<double2 *>(pt_ + 8 * h) = acc[p][h][0];
+                    *reinterpret_cast<double2 *>(pt_ + kSS + 8 * h) = acc[p][h][1];
                 }
+            }
         }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[p][h][0] = acc[p][h][1] = make_double2(0.0, 0.0);
         ++step;
-        phase = phase + 1 == NB ? 0 : phase + 1;
+        phase = (p + 1 == NT) ? 0 : p + 1;
     };
 
     // gather: thread pair (2r, 2r+1) copies record r's two 16-byte halves;
@@ -392,11 +366,10 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     uint32_t nid = index_of(kRaw - 1);
 
     const unsigned char *const recbase = reinterpret_cast<const unsigned char *>(&sm.rec[0]);
-    // the sentinel: zero weights, window step -1
+    // the sentinel: zero weights
     for (int e = tid; e < (int)(sizeof(Rec) / 8); e += kThreads)
         reinterpret_cast<double *>(&sm.rec[kChunk])[e] = 0.0;
-    __syncthreads();
-    if (tid == 0) sm.rec[kChunk].meta = make_int4(0, -1, 0, 0);
+    const double rs = (Bfirst & 1) ? -1.0 : 1.0;    // (-1)^row of window row 0 (8 step is even)
     for (int ch = 0; ch < nchunks; ++ch) {
         asm volatile("cp.async.wait_group %0;\n" ::"n"(kRaw - 2) : "memory");
         __syncthreads();   // raw[ch] landed for every thread; the previous sweep is done
@@ -417,9 +390,9 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                 const int i0 = (int)floor(g) - S;
                 const uint32_t wm = axis_weights<KIND, S>(g, i0, kp, i0b, wgt);
                 if (ax == 0) {
-                    // u axis: value * weight per window column
-                    // with the column factor (-1)^i of the checkerboard sign
-                    // (transform.py:180-185; a sign flip commutes with rounding)
+                    // u axis: value * weight per window column, with the column
+                    // factor (-1)^i of the checkerboard sign (transform.py:180-185;
+                    // a sign flip commutes with rounding)
                     const double cs = (i0 & 1) ? -1.0 : 1.0;
 #pragma unroll
                     for (int k = 0; k < W; ++k) {
@@ -440,21 +413,20 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                     st.meta.w = mask;
                     mine = __popc(uin);
                 } else {
-                    // v axis: weight of window row b (from the window base; the
-                    // record's footprint starts at row d = anchor - base, 0 or 1)
+                    // v axis: weight of row b of the record's window step; the
+                    // footprint starts at row d = anchor - step base, 0..7; with
+                    // the row factor (-1)^row
                     const int rel = i0 - Bfirst;
-                    WSB_DCHECK(rel >= 0 && rel < NROW, "item %lld rel %d", (long long)item, rel);
-                    const int d = rel & 1;
-                    // with the row factor (-1)^j: window row b is mesh row Bfirst + 2k + b
-                    const double rs = (Bfirst & 1) ? -1.0 : 1.0;
+                    WSB_DCHECK(rel >= 0 && rel < Sm::NROW, "item %lld rel %d", (long long)item, rel);
+                    const int d = rel & 7;
 #pragma unroll
-                    for (int b = 0; b < Rec::NV; ++b) {
-                        // b - d in [0, W): weight, else 0 (d is 0 or 1)
-                        const double x0 = b < W ? wgt[b < W ? b : 0] : 0.0;            // d = 0
-                        const double x1 = (b >= 1 && b - 1 < W) ? wgt[b >= 1 && b - 1 < W ? b - 1 : 0] : 0.0;
-                        st.wv[b] = ((b & 1) ? -rs : rs) * (d ? x1 : x0);
-                    }
-                    st.meta.y = rel >> 1;
+                    for (int b = 0; b < Rec::NV; b += 2)
+                        *reinterpret_cast<double2 *>(&st.wv[b]) = make_double2(0.0, 0.0);
+                    const double sd = (d & 1) ? -rs : rs;
+                    double *const wr = st.wv + d;
+#pragma unroll
+                    for (int k = 0; k < W; ++k) wr[k] = (k & 1) ? -sd * wgt[k] : sd * wgt[k];
+                    st.meta.y = rel >> 3;
                     st.meta.z = d;
                     const int r_lo = max(R0 - i0, 0), r_hi = min(R1 - i0, W) - 1;
                     mine = __popc(r_hi >= r_lo ? wm & (((2u << r_hi) - 1u) & ~((1u << r_lo) - 1u)) : 0u);
@@ -467,85 +439,99 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         __syncthreads();   // stage complete
         // ---- sweep: this warp's strip ---------------------------------------
         {
-            // The chunk's records touching the strip, in order, cut into MMA
-            // steps: runs of records with the same window step, four at a time.
-            // Each MMA step is one (record bytes, window step) entry; empty
-            // slots name the zero sentinel record. The sweep then needs no
-            // probing or voting per record.
-            const uint32_t lt = (1u << lane) - 1u, le = (2u << lane) - 1u;
+            // The chunk's records touching the strip, in order, taken four at a
+            // time: lane (g4, k4) holds record k4 of the group. A record is
+            // applied once the window's first tile is its step's (or, with
+            // WSB_WIN_EXTRA, up to that many steps earlier); a group whose
+            // records lie further apart is applied in several passes, the
+            // window moving on in between.
+            const uint32_t lt = (1u << lane) - 1u;
+            int tot;
             {
                 const bool t0 = lane < nr && ((sm.rec[lane].meta.w >> warp) & 1);
                 const bool t1 = 32 + lane < nr && ((sm.rec[32 + lane].meta.w >> warp) & 1);
                 const uint32_t m0 = __ballot_sync(0xffffffffu, t0);
                 const uint32_t m1 = __ballot_sync(0xffffffffu, t1);
-                if (t0) {
-                    const int p_ = __popc(m0 & lt);
-                    sm.pstep[warp][p_] = sm.rec[lane].meta.y;
-                    sm.prec[warp][p_] = (uint8_t)lane;
-                }
-                if (t1) {
-                    const int p_ = __popc(m0) + __popc(m1 & lt);
-                    sm.pstep[warp][p_] = sm.rec[32 + lane].meta.y;
-                    sm.prec[warp][p_] = (uint8_t)(32 + lane);
-                }
-                const int tot = __popc(m0) + __popc(m1);
-                __syncwarp();
-                // positions p = lane (round a) and 32 + lane (round b)
-                const bool va = lane < tot, vb = 32 + lane < tot;
-                const int sa = va ? sm.pstep[warp][lane] : 0;
-                const int sb = vb ? sm.pstep[warp][32 + lane] : 0;
-                const int pa = lane > 0 ? sm.pstep[warp][lane - 1] : -2;
-                const int pb = sm.pstep[warp][31 + lane];
-                const uint32_t fa = __ballot_sync(0xffffffffu, va && sa != pa);   // run starts
-                const uint32_t fb = __ballot_sync(0xffffffffu, vb && sb != pb);
-                const int ra = 31 - __clz(fa & le);
-                const int rb = (fb & le) ? 32 + 31 - __clz(fb & le) : 31 - __clz(fa);
-                const int slot_a = (lane - ra) & 3, slot_b = (32 + lane - rb) & 3;
-                const uint32_t ka = __ballot_sync(0xffffffffu, va && slot_a == 0);   // MMA step starts
-                const uint32_t kb = __ballot_sync(0xffffffffu, vb && slot_b == 0);
-                const int kia = __popc(ka & le) - 1, kib = __popc(ka) + __popc(kb & le) - 1;
-                const uint32_t empty = (uint32_t)kChunk * 0x01010101u;
-                if (va && slot_a == 0) sm.kst[warp][kia] = make_uint2(empty, (uint32_t)sa);
-                if (vb && slot_b == 0) sm.kst[warp][kib] = make_uint2(empty, (uint32_t)sb);
-                if (lane == 0) sm.kst[warp][__popc(ka) + __popc(kb)] = make_uint2(empty, 0xFFFFFFFFu);
-                __syncwarp();
-                if (va) reinterpret_cast<uint8_t *>(&sm.kst[warp][kia].x)[slot_a] = sm.prec[warp][lane];
-                if (vb) reinterpret_cast<uint8_t *>(&sm.kst[warp][kib].x)[slot_b] = sm.prec[warp][32 + lane];
+                if (t0) sm.prec[warp][__popc(m0 & lt)] = (uint8_t)lane;
+                if (t1) sm.prec[warp][__popc(m0) + __popc(m1 & lt)] = (uint8_t)(32 + lane);
+                tot = __popc(m0) + __popc(m1);
                 __syncwarp();
             }
-            const uint2 *ke = sm.kst[warp];
+            constexpr int NTR = Win<S>::NTR;
             const int wc8 = warp * kC + g4;        // this lane's B column (half 0) in the superstrip
-#pragma unroll 1
-            for (;;) {
-                const uint2 en = *ke++;
-                const int est = (int)en.y;
-                if (est < 0) break;                        // chunk done: the next one may continue this step
-                while (step < est) emit();                 // rows above the step are final
-                const unsigned char *rp = recbase + (int)((en.x >> (8 * k4)) & 0xFFu) * (int)sizeof(Rec);
-                const int ibr = reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta))->x;
-                // B: value x u weight at this lane's column of each 8-column half
-                const int c0 = wc8 - ibr;
+            int pos = k4;                          // this lane's record position in the list
+            bool pend;                             // its record still to apply
+            int srec, span;                        // its window step; tiles it reaches from there
+            double2 b0, b1;                        // B: value x u weight at the lane's columns
+            const double *wvp;                     // A: v weights of its rows
+            auto load = [&]() {
+                pend = pos < tot;
+                const unsigned char *rp =
+                    recbase + (int)(pend ? sm.prec[warp][pos] : kChunk) * (int)sizeof(Rec);
+                const int4 m = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
+                const int c0 = wc8 - m.x;
                 const int i0 = (unsigned)c0 < (unsigned)W ? c0 : W;
                 const int i1 = (unsigned)(c0 + 8) < (unsigned)W ? c0 + 8 : W;
-                const double2 b0 = *reinterpret_cast<const double2 *>(rp + 16 * i0);
-                const double2 b1 = *reinterpret_cast<const double2 *>(rp + 16 * i1);
+                b0 = *reinterpret_cast<const double2 *>(rp + 16 * i0);
+                b1 = *reinterpret_cast<const double2 *>(rp + 16 * i1);
+                wvp = reinterpret_cast<const double *>(rp + offsetof(Rec, wv)) + g4;
+                srec = m.y;
+                span = (m.z + W + 7) >> 3;
+            };
+            load();
+            // phase P: apply groups while their first pending record is in the
+            // current step, then emit tile P. false: chunk done
+            auto run = [&](auto P) -> bool {
+                constexpr int p = decltype(P)::value;
+                for (;;) {
+                    if (!__any_sync(0xffffffffu, pend)) return false;   // (the list is used up)
+                    const int smin = __reduce_min_sync(0xffffffffu, pend ? srec : 0x7FFFFFFF);
+                    if (smin != step) break;
+                    const int delta = srec - step;
+                    const bool act = pend && delta <= NT - NTR;
+                    const int ntile = __reduce_max_sync(0xffffffffu, act ? delta + span : 0);
 #pragma unroll
-                for (int m = 0; m < MT; ++m) {
-                    // A: this record's v weight on tile row g4 of tile m
-                    const int band = (4 * m + (g4 >> 1) - phase) & (NB - 1);   // ring -> window band
-                    const double av =
-                        reinterpret_cast<const double *>(rp + offsetof(Rec, wv))[2 * band + (g4 & 1)];
-                    dmma(acc[m][0][0], av, b0.x);
-                    dmma(acc[m][0][1], av, b0.y);
-                    dmma(acc[m][1][0], av, b1.x);
-                    dmma(acc[m][1][1], av, b1.y);
+                    for (int t = 0; t < NT; ++t) {
+                        if (t < ntile) {   // (uniform) tiles the pass reaches
+                            // A: v weight of the records on tile row g4 (window row 8t + g4)
+                            const int tt = t - delta;
+                            const double av = (act && (unsigned)tt < (unsigned)NTR) ? wvp[8 * tt] : 0.0;
+                            const int tr = (p + t) % NT;          // ring tile holding window tile t (folds)
+                            dmma(acc[tr][0][0], av, b0.x);
+                            dmma(acc[tr][0][1], av, b0.y);
+                            dmma(acc[tr][1][0], av, b1.x);
+                            dmma(acc[tr][1][1], av, b1.y);
+                        }
+                    }
+                    pend = pend && !act;
+                    if (!__any_sync(0xffffffffu, pend)) {
+                        pos += 4;
+                        load();
+                    }
                 }
+                emit(P);   // rows above the next pending record's step are final
+                return true;
+            };
+            for (;;) {
+                bool more = true;
+                switch (phase) {
+#define WSB_PHASE(q)                                                        \
+    case q:                                                                 \
+        if constexpr (q < NT) {                                             \
+            if (!(more = run(std::integral_constant<int, q>{}))) break;     \
+        }                                                                   \
+        [[fallthrough]];
+                    WSB_PHASE(0) WSB_PHASE(1) WSB_PHASE(2) WSB_PHASE(3)
+#undef WSB_PHASE
+                    default: break;
+                }
+                if (!more) break;
             }
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     // flush the rest of the block (split parts: of their rows)
-    while (Bfirst + 2 * step < row_end) emit();
+    while (Bfirst + 8 * step < row_end) dispatch_phase<0, NT>(phase, emit);
 
 #pragma unroll
     for (int o = 16; o; o >>= 1) cnt_upd += __shfl_xor_sync(0xffffffffu, cnt_upd, o);

@@ -1,0 +1,15 @@
+# bench each variant library build/var*/libwsb.so (WSB_LIB) on one GPU: K2 / step times
+cd $GRAFT_REPO_ROOT
+for L in build/var*/libwsb.so; do
+  v=$(basename $(dirname $L))
+  WSB_LIB=$PWD/$L timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-cfg3 > gpurun_out/var_$v.json 2> gpurun_out/var_$v.err
+  python - "$v" <<'PY'
+import json, sys
+v = sys.argv[1]
+try:
+    d = json.loads(open(f"gpurun_out/var_{v}.json").readline())
+    print(v, d["ms_per_step"], {k: x["ms"] for k, x in d["kernels"].items()})
+except Exception as e:
+    print(v, "FAIL", e)
+PY
+done > gpurun_out/variants.txt 2>&1
