@@ -303,13 +303,30 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
 
 // item offsets from the sorted keys: off[it] = first entry of item it (the
 // next non-empty item's first entry for an empty one), off[n_items] = n
+// (four entries per thread: one 16-byte load and the previous key)
 __global__ void k_item_offsets(const uint32_t *__restrict__ keys, int64_t n, int64_t n_items,
                                uint32_t *__restrict__ off) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i > n) return;
-    const int64_t cur = i < n ? (int64_t)(keys[i] >> kRowBits) : n_items;
-    const int64_t prev = i > 0 ? (int64_t)(keys[i - 1] >> kRowBits) : -1;
-    for (int64_t it = prev + 1; it <= cur; ++it) off[it] = (uint32_t)i;
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i0 > n) return;
+    int64_t cur[4];
+    if (i0 + 4 <= n) {
+        const uint4 k4 = __ldg(reinterpret_cast<const uint4 *>(keys + i0));
+        cur[0] = k4.x >> kRowBits;
+        cur[1] = k4.y >> kRowBits;
+        cur[2] = k4.z >> kRowBits;
+        cur[3] = k4.w >> kRowBits;
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            cur[q] = i0 + q < n ? (int64_t)(__ldg(&keys[i0 + q]) >> kRowBits) : n_items;
+    }
+    int64_t prev = i0 > 0 ? (int64_t)(__ldg(&keys[i0 - 1]) >> kRowBits) : -1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (i0 + q > n) break;
+        for (int64_t it = prev + 1; it <= cur[q]; ++it) off[it] = (uint32_t)(i0 + q);
+        prev = cur[q];
+    }
 }
 
 }  // namespace
@@ -401,8 +418,8 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     if (e & kErrTime) return fail(WSB_EINVAL, "records must be sorted by time_index");
     uint32_t *ks, *is;
     WSB_TRY(radix_sort_pairs(ctx, ka, kb, ia, ib, n_entries, k.item_bits + kRowBits, &ks, &is));
-    k_item_offsets<<<ceil_div((int64_t)n_entries + 1, 256), 256, 0, ctx->stream>>>(ks, n_entries, n_items,
-                                                                                 off);
+    k_item_offsets<<<ceil_div(((int64_t)n_entries + 4) / 4, 256), 256, 0, ctx->stream>>>(ks, n_entries,
+                                                                                       n_items, off);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     out->keys = ks;

@@ -623,9 +623,10 @@ __global__ void k_item_parts(const uint32_t *off, int64_t n_items, uint32_t *npa
     split[item] = np > 1 ? 1 : 0;
 }
 
+// slot_off / split_off: segments of one concatenated scan, minus their bases
 __global__ void k_build_parts(const uint32_t *off, int64_t n_items, const uint32_t *part_off,
-                              const uint32_t *slot_off, const uint32_t *split_off, uint4 *parts,
-                              uint2 *split_items) {
+                              const uint32_t *slot_off, uint32_t slot_base, const uint32_t *split_off,
+                              uint32_t split_base, uint4 *parts, uint2 *split_items) {
     const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (item >= n_items) return;
     const uint32_t b = off[item], e = off[item + 1];
@@ -635,11 +636,12 @@ __global__ void k_build_parts(const uint32_t *off, int64_t n_items, const uint32
         return;
     }
     const uint32_t chunk = (e - b + np - 1) / np;
+    const uint32_t slot = slot_off[item] - slot_base;
     for (uint32_t p = 0; p < np; ++p) {
         const uint32_t pb = min(e, b + p * chunk), pe = min(e, pb + chunk);
-        parts[part_off[item] + p] = make_uint4((uint32_t)item, pb, pe, slot_off[item] + p);
+        parts[part_off[item] + p] = make_uint4((uint32_t)item, pb, pe, slot + p);
     }
-    split_items[split_off[item]] = make_uint2((uint32_t)item, slot_off[item]);
+    split_items[split_off[item] - split_base] = make_uint2((uint32_t)item, slot);
 }
 
 // one thread per (row, column) of a split item: its parts' partial tiles
@@ -710,21 +712,25 @@ int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
     if (ni <= 0) return WSB_OK;
     const int S = k->half_support;
     // ---- work parts (split heavy items) ------------------------------------
-    uint32_t *np, *ns, *sp, *np_off, *ns_off, *sp_off;
-    WSB_TRY(ensure(ctx, kSlotPartCnt, sizeof(uint32_t) * 3 * (ni + 1), (void **)&np));
-    WSB_TRY(ensure(ctx, kSlotPartOff, sizeof(uint32_t) * 3 * (ni + 1), (void **)&np_off));
-    ns = np + (ni + 1);
-    sp = ns + (ni + 1);
-    ns_off = np_off + (ni + 1);
-    sp_off = ns_off + (ni + 1);
-    WSB_CUDA_TRY(cudaMemsetAsync(np, 0, sizeof(uint32_t) * 3 * (ni + 1), ctx->stream));
-    k_item_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(bk.off, ni, np, ns, sp);
+    // per item: parts, partial-tile slots, split flag -- three count arrays
+    // scanned as one concatenation (one scan, one host round trip)
+    const int64_t seg = ni + 1, len = 3 * seg + 1;
+    uint32_t *cnt, *pre;
+    WSB_TRY(ensure(ctx, kSlotPartCnt, sizeof(uint32_t) * len, (void **)&cnt));
+    WSB_TRY(ensure(ctx, kSlotPartOff, sizeof(uint32_t) * len, (void **)&pre));
+    WSB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * len, ctx->stream));
+    k_item_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(bk.off, ni, cnt, cnt + seg, cnt + 2 * seg);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
-    uint32_t n_parts = 0, n_slots = 0, n_split = 0;
-    WSB_TRY(exclusive_scan_u32(ctx, np, np_off, ni + 1, &n_parts));
-    WSB_TRY(exclusive_scan_u32(ctx, ns, ns_off, ni + 1, &n_slots));
-    WSB_TRY(exclusive_scan_u32(ctx, sp, sp_off, ni + 1, &n_split));
+    WSB_TRY(exclusive_scan_u32(ctx, cnt, pre, len, nullptr));
+    for (int q = 0; q < 3; ++q)
+        WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host + q, pre + (q + 1) * seg, sizeof(uint32_t),
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+    WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    const uint32_t b1 = (uint32_t)ctx->flag_host[0], b2 = (uint32_t)ctx->flag_host[1],
+                   b3 = (uint32_t)ctx->flag_host[2];
+    const uint32_t n_parts = b1, n_slots = b2 - b1, n_split = b3 - b2;
+    const uint32_t *np_off = pre;
     uint4 *parts;
     uint2 *split_items, *part_rows;
     double2 *partial = nullptr;
@@ -735,8 +741,8 @@ int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
     if (n_slots)
         WSB_TRY(ensure(ctx, kSlotPartial, sizeof(double2) * (size_t)n_slots * kItemRows * kSS,
                        (void **)&partial));
-    k_build_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(bk.off, ni, np_off, ns_off, sp_off,
-                                                              parts, split_items);
+    k_build_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(bk.off, ni, np_off, pre + seg, b1,
+                                                              pre + 2 * seg, b2, parts, split_items);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     a.parts = parts;
