@@ -1,4 +1,5 @@
-# bench each variant library build/var*/libwsb.so (WSB_LIB) on one GPU: K2 / step times
+# bench each variant library build/var*/libwsb.so (WSB_LIB) on one GPU: step and kernel
+# times, plus an ncu launch list per variant (per-kernel durations)
 cd $GRAFT_REPO_ROOT
 for L in build/var*/libwsb.so; do
   v=$(basename $(dirname $L))
@@ -12,4 +13,8 @@ try:
 except Exception as e:
     print(v, "FAIL", e)
 PY
+  if [ -n "$LAUNCHES" ]; then
+    WSB_LIB=$PWD/$L ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/var_$v.csv python tools/repro_grid.py 10000000 2048 32 > /dev/null 2>&1
+    python tools/launch_summary.py gpurun_out/var_$v.csv | head -12
+  fi
 done > gpurun_out/variants.txt 2>&1
