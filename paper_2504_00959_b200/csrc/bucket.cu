@@ -165,7 +165,8 @@ struct KeysSmem {
     alignas(16) float wt[FROM_INPUT ? N : 4];
     alignas(16) uint32_t plane[FROM_INPUT ? 4 : N];
     uint64_t bar;
-    uint32_t bid, wsum[kThreads / 32];
+    uint64_t wsum[kThreads / 32];
+    uint32_t bid;
     int err;
 };
 
@@ -229,14 +230,14 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
         }
         __syncthreads();
     }
-    // ---- per thread: kPer consecutive records --------------------------------
+    // ---- per thread: records tid, tid + 256, ... (conflict-free shared-memory
+    // reads; each warp writes 32 consecutive prepared records per round) ----
     uint32_t keys[kPer][4];
     int cnt[kPer];
-    uint32_t mine = 0;
     int e = 0;
 #pragma unroll
     for (int r = 0; r < kPer; ++r) {
-        const int li = tid * kPer + r;
+        const int li = r * kThreads + tid;
         cnt[r] = 0;
         if (li >= cnt_tile) continue;
         double gu, gv;
@@ -256,7 +257,6 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
             const double ar = vs.x, ai = vs.y, br = wt;
             const double re = __dadd_rn(0.0, __dadd_rn(-0.0, __dsub_rn(__dmul_rn(ar, br), __dmul_rn(ai, 0.0))));
             const double im = __dadd_rn(0.0, __dadd_rn(-0.0, __dadd_rn(__dmul_rn(ar, 0.0), __dmul_rn(ai, br))));
-            // a thread's kPer consecutive records are one 128-byte line
             a.rec[i] = make_double4(gu, gv, re, im);
             if (a.plane) a.plane[i] = pl;
         } else {
@@ -266,39 +266,54 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
             pl = sm.plane[li];
         }
         cnt[r] = record_entries(gu, gv, pl, a.g, keys[r]);
-        mine += cnt[r];
     }
     if (FROM_INPUT && e) atomicOr(&sm.err, e);
-    // block exclusive scan of the per-thread entry counts (record order)
-    uint32_t incl = mine;
+    // entry positions in record order (r, tid): one block scan of the four
+    // per-round counts packed in 16-bit fields
+    uint64_t mine = 0;
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) mine |= (uint64_t)cnt[r] << (16 * r);
+    uint64_t incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
     }
     if (lane == 31) sm.wsum[warp] = incl;
-    __syncthreads();
-    uint32_t wbase = 0, agg = 0;
+    __syncthreads();   // (also: every thread has read its inputs -- the staging below reuses them)
+    uint64_t wbase = 0, agg = 0;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) {
-        const uint32_t s = sm.wsum[w];
-        if (w < warp) wbase += s;
-        agg += s;
+        const uint64_t s_ = sm.wsum[w];
+        if (w < warp) wbase += s_;
+        agg += s_;
     }
     if (tid == 0 && FROM_INPUT && sm.err) atomicOr(a.err, sm.err);
-    (void)agg;
-    uint32_t pos = a.block_off[bid] + wbase + incl - mine;
-    WSB_DCHECK((int64_t)pos + mine <= 4 * a.n, "tile %u pos %u", bid, pos);
-    // (static indices: the entry arrays stay in registers)
+    const uint64_t ex = wbase + incl - mine;
+    // stage the tile's entries compacted in shared memory, then write them
+    // with consecutive threads on consecutive entries
+    uint32_t *sk = reinterpret_cast<uint32_t *>(smem_raw);
+    uint32_t *si = sk + 4 * kTile;
+    uint32_t rbase = 0;
 #pragma unroll
-    for (int r = 0; r < kPer; ++r)
+    for (int r = 0; r < kPer; ++r) {
+        uint32_t q = rbase + (uint32_t)((ex >> (16 * r)) & 0xFFFFu);
 #pragma unroll
         for (int t = 0; t < 4; ++t)
             if (t < cnt[r]) {
-                a.keys[pos] = keys[r][t];
-                a.idx[pos] = (uint32_t)(base + tid * kPer + r);
-                ++pos;
+                sk[q] = keys[r][t];
+                si[q] = (uint32_t)(base + r * kThreads + tid);
+                ++q;
             }
+        rbase += (uint32_t)((agg >> (16 * r)) & 0xFFFFu);
+    }
+    __syncthreads();
+    const uint32_t pos0 = a.block_off[bid];
+    WSB_DCHECK((int64_t)pos0 + rbase <= 4 * a.n, "tile %u pos %u", bid, pos0);
+    for (uint32_t q = tid; q < rbase; q += kThreads) {
+        a.keys[pos0 + q] = sk[q];
+        a.idx[pos0 + q] = si[q];
+    }
 }
 
 // item offsets from the sorted keys: off[it] = first entry of item it (the
