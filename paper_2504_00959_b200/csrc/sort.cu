@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
     for (int i = lane; i < D; i += 32) sm.wc[warp][i] = 0;
     __syncwarp();
     const int64_t base = (int64_t)blockIdx.x * kRsItems + warp * kRsPerWarp;
-    uint32_t k[kRsIpt], v[kRsIpt], pm[kRsIpt];
+    uint32_t k[kRsIpt], v[kRsIpt], pm[kRsIpt];   // pm: rank among the warp's items of the digit
 #pragma unroll
     for (int r = 0; r < kRsIpt; ++r) {
         int64_t i = base + r * 32 + lane;
@@ -183,9 +183,12 @@ __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
                 const uint32_t bb = __ballot_sync(0xffffffffu, on);
                 peers &= on ? bb : ~bb;
             }
-            pm[r] = peers;
+            // rank of this item among the warp's items of its digit so far
+            const uint32_t before = d < (uint32_t)D ? sm.wc[warp][d] : 0u;
+            pm[r] = before + __popc(peers & ((1u << lane) - 1u));
+            __syncwarp();
+            if (d < (uint32_t)D && lane == __ffs(peers) - 1) sm.wc[warp][d] = before + __popc(peers);
         }
-        if (d < (uint32_t)D && lane == __ffs(pm[r]) - 1) sm.wc[warp][d] += __popc(pm[r]);
         __syncwarp();
     }
     __syncthreads();
@@ -227,18 +230,13 @@ __global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
     }
     __syncthreads();
     // stable rank inside the block -> shared-memory staging in digit order
-    const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int r = 0; r < kRsIpt; ++r) {
         int64_t i = base + r * 32 + lane;
         bool ok = i < n;
         uint32_t d = ok ? (k[r] >> shift) & dmask : (uint32_t)D;
-        const uint32_t peers = pm[r];
-        uint32_t pos = 0;
-        if (ok) pos = sm.bstart[d] + sm.wc[warp][d] + __popc(peers & lt);
-        __syncwarp();
-        if (ok && lane == __ffs(peers) - 1) sm.wc[warp][d] += __popc(peers);
-        __syncwarp();
+        // block start of the digit + this warp's start in it + the item's rank
+        const uint32_t pos = ok ? sm.bstart[d] + sm.wc[warp][d] + pm[r] : 0u;
         if (ok) {
             sm.ks[pos] = LAST ? sm.goff[d] + (pos - sm.bstart[d]) : k[r];
             sm.vs[pos] = v[r];
