@@ -77,21 +77,34 @@ static int set_device(wsb_ctx *ctx) {
     return WSB_OK;
 }
 
-// Device-side final sum of the per-column-block norm partials, in block order.
-// Chunks are staged in shared memory by the whole block (coalesced); one
-// thread adds them left to right, the association the multi-GPU root uses.
+// Device-side final sum of the per-column norm partials in a fixed
+// two-level association: chunks of kNormChunk consecutive partials summed left
+// to right (one thread per chunk), then the chunk sums left to right -- the
+// association the multi-GPU root applies to the gathered partials
+// (distributed.norm_sum), so the norms do not depend on the GPU count.
+constexpr int kNormChunk = 64;
 __global__ void __launch_bounds__(256) k_sum_partials(const double *p, int nb, double *out) {
-    __shared__ double2 buf[1024];
+    __shared__ double2 cs[1024];
+    const int nc = (nb + kNormChunk - 1) / kNormChunk;
     double si = 0.0, sr = 0.0;
-    for (int base = 0; base < nb; base += 1024) {
-        const int n = min(1024, nb - base);
-        for (int i = threadIdx.x; i < n; i += blockDim.x)
-            buf[i] = make_double2(p[2 * (base + i)], p[2 * (base + i) + 1]);
+    for (int base = 0; base < nc; base += 1024) {
+        const int n = min(1024, nc - base);
+        for (int c = threadIdx.x; c < n; c += blockDim.x) {
+            const int lo = (base + c) * kNormChunk, hi = min(lo + kNormChunk, nb);
+            double a = 0.0, b = 0.0;
+#pragma unroll 8
+            for (int i = lo; i < hi; ++i) {
+                const double2 x = *reinterpret_cast<const double2 *>(p + 2 * i);
+                a += x.x;
+                b += x.y;
+            }
+            cs[c] = make_double2(a, b);
+        }
         __syncthreads();
         if (threadIdx.x == 0)
-            for (int i = 0; i < n; ++i) {
-                si += buf[i].x;
-                sr += buf[i].y;
+            for (int c = 0; c < n; ++c) {
+                si += cs[c].x;
+                sr += cs[c].y;
             }
         __syncthreads();
     }

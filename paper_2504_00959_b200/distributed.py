@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -588,14 +589,29 @@ def image_distributed(u, v, w, vis, weight, spec, kern, group=None, backend=None
     return _final(spec, pix, torch.cat(col_parts, dim=1), to_host, diag)
 
 
+NORM_CHUNK = 64   # k_sum_partials' chunk (csrc/api.cu)
+
+
+def norm_sum(p) -> tuple:
+    """(sum of column 0, sum of column 1) of the norm partials p [n][2] in
+    k_sum_partials' association: chunks of NORM_CHUNK consecutive rows summed
+    left to right, then the chunk sums left to right (cumsum is left to
+    right; padding with +0.0 leaves a sum of squares unchanged)."""
+    p = np.asarray(p, dtype=np.float64).reshape(-1, 2)
+    nc = -(-len(p) // NORM_CHUNK)
+    q = np.zeros((nc * NORM_CHUNK, 2))
+    q[: len(p)] = p
+    chunks = q.reshape(nc, NORM_CHUNK, 2).cumsum(axis=1)[:, -1, :]
+    tot = chunks.cumsum(axis=0)[-1]
+    return float(tot[0]), float(tot[1])
+
+
 def _final(spec, pix, partials, to_host, diag):
     """FinalImage on the root from the device image and the norm partials
     [residue][column][2]."""
     p = partials.reshape(-1, 2).cpu().numpy()
-    # sequential sum residue-major, in global column order (cumsum is left to
-    # right): the same association as the single-GPU path, for any R
-    im_sq = float(p[:, 0].cumsum()[-1])
-    re_sq = float(p[:, 1].cumsum()[-1])
+    # residue-major, global column order, the single-GPU association (any R)
+    im_sq, re_sq = norm_sum(p)
     if to_host and pix.is_cuda:
         # page-locked destination: the image leaves at DMA speed (a pageable
         # destination costs ~10x). The returned pixels are that buffer itself

@@ -38,7 +38,7 @@ def _parts(t, R):
 
 
 def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges=1, starts=None):
-    from paper_2504_00959_b200.distributed import CudaBackend, plane_ranges
+    from paper_2504_00959_b200.distributed import CudaBackend, norm_sum, plane_ranges
     be = CudaBackend(0)
     G = 1
     S = kern.half_support
@@ -78,7 +78,7 @@ def _virtual_ranks(W, u, v, w, t, vis, wt, spec, kern, R, n_ranges=1, starts=Non
         pix[:, g0 * G:(g0 + ng) * G] = strip.cpu().numpy()
         parts.append(partials.cpu().numpy().reshape(-1, ng * G, 2))
     p = np.concatenate(parts, axis=1).reshape(-1, 2)   # residue-major, global column order
-    return pix, np.sqrt([p[:, 0].cumsum()[-1], p[:, 1].cumsum()[-1]]), upd
+    return pix, np.sqrt(norm_sum(p)), upd
 
 
 @pytest.mark.parametrize("R,n_ranges,uneven", [(2, 1, False), (4, 1, False), (8, 1, False),
@@ -108,7 +108,7 @@ def _virtual_plane_ranks(W, u, v, w, t, vis, wt, spec, kern, starts, n_ranges=1)
     route by plane, grid + transform + partial stack per rank, the reduce as
     a sum of the partial images, then the finish kernel."""
     import dataclasses
-    from paper_2504_00959_b200.distributed import CudaBackend, plane_ranges
+    from paper_2504_00959_b200.distributed import CudaBackend, norm_sum, plane_ranges
     be = CudaBackend(0)
     R = len(starts) - 1
     sends = []
@@ -136,7 +136,7 @@ def _virtual_plane_ranks(W, u, v, w, t, vis, wt, spec, kern, starts, n_ranges=1)
         total = pimg if total is None else total + pimg
     pix, parts = be.image_finish(total, spec)
     p = parts.reshape(-1, 2).cpu().numpy()
-    return pix.cpu().numpy(), np.sqrt([p[:, 0].cumsum()[-1], p[:, 1].cumsum()[-1]]), upd
+    return pix.cpu().numpy(), np.sqrt(norm_sum(p)), upd
 
 
 @pytest.mark.parametrize("starts,n_ranges", [([0, 8, 16], 1), ([0, 3, 9, 10, 16], 1),
