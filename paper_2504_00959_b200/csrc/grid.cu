@@ -166,8 +166,15 @@ constexpr int kC = WSB_STRIP;          // columns per warp strip
 constexpr int kWarps = 4;              // strips (warps) per item
 constexpr int kSS = kC * kWarps;       // superstrip width (64)
 constexpr int kThreads = 32 * kWarps;
-constexpr int kChunk = 64;             // records staged per round (one per thread of warps 0-1)
-constexpr int kRaw = 3;                // gather ring: chunks in flight
+#ifndef WSB_CHUNK_MUL
+#define WSB_CHUNK_MUL 1
+#endif
+constexpr int kCM = WSB_CHUNK_MUL;     // records per thread pair per chunk
+constexpr int kChunk = 64 * kCM;       // records staged per round
+#ifndef WSB_RAW
+#define WSB_RAW 3
+#endif
+constexpr int kRaw = WSB_RAW;          // gather ring: chunks in flight
 
 struct SweepArgs {
     const double4 *rec;
@@ -341,29 +348,40 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         phase = (p + 1 == NT) ? 0 : p + 1;
     };
 
-    // gather: thread pair (2r, 2r+1) copies record r's two 16-byte halves;
-    // the entry's record index is loaded one chunk before its gather
+    // gather: thread pair (2r, 2r+1) copies the two 16-byte halves of
+    // records r, r + 64, ...; an entry's record index is loaded one chunk
+    // before its gather
     const int nchunks = (int)((n + kChunk - 1) / kChunk);
-    auto index_of = [&](int ch) -> uint32_t {
-        const uint32_t r = ch * kChunk + (tid >> 1);
-        return (ch < nchunks && r < n) ? __ldg(&a.idx[eb + r]) : 0u;
+    struct Ids { uint32_t v[kCM]; };
+    auto index_of = [&](int ch) -> Ids {
+        Ids ids;
+#pragma unroll
+        for (int q = 0; q < kCM; ++q) {
+            const uint32_t r = ch * kChunk + q * 64 + (tid >> 1);
+            ids.v[q] = (ch < nchunks && r < n) ? __ldg(&a.idx[eb + r]) : 0u;
+        }
+        return ids;
     };
-    auto fetch = [&](int ch, uint32_t id) {
+    auto fetch = [&](int ch, const Ids &ids) {
         if (ch < nchunks) {
-            const uint32_t r = ch * kChunk + (tid >> 1);
-            if (r < n) {
-                WSB_DCHECK(id < a.n_rec, "item %lld id %u", (long long)item, id);
-                const double2 *src = reinterpret_cast<const double2 *>(a.rec + id) + (tid & 1);
-                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(
-                    reinterpret_cast<double2 *>(&sm.raw[ch % kRaw][tid >> 1]) + (tid & 1));
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+#pragma unroll
+            for (int q = 0; q < kCM; ++q) {
+                const uint32_t r = ch * kChunk + q * 64 + (tid >> 1);
+                if (r < n) {
+                    const uint32_t id = ids.v[q];
+                    WSB_DCHECK(id < a.n_rec, "item %lld id %u", (long long)item, id);
+                    const double2 *src = reinterpret_cast<const double2 *>(a.rec + id) + (tid & 1);
+                    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(
+                        reinterpret_cast<double2 *>(&sm.raw[ch % kRaw][q * 64 + (tid >> 1)]) + (tid & 1));
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+                }
             }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
 #pragma unroll
     for (int ch = 0; ch < kRaw - 1; ++ch) fetch(ch, index_of(ch));
-    uint32_t nid = index_of(kRaw - 1);
+    Ids nid = index_of(kRaw - 1);
 
     const unsigned char *const recbase = reinterpret_cast<const unsigned char *>(&sm.rec[0]);
     // the sentinel: zero weights
@@ -379,8 +397,9 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         // ---- stage: thread pair per record, thread (2r + ax) does axis ax of
         // record r. Both axes run the same weight code (one instruction stream
         // for the warp); only the short tails differ.
-        {
-            const int r = tid >> 1, ax = tid & 1;
+#pragma unroll 1
+        for (int q = 0; q < kCM; ++q) {
+            const int r = q * 64 + (tid >> 1), ax = tid & 1;
             unsigned mine = 0;      // taps of this axis inside the item
             if (r < nr) {
                 const double4 rc = sm.raw[ch % kRaw][r];
@@ -448,13 +467,15 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             const uint32_t lt = (1u << lane) - 1u;
             int tot;
             {
-                const bool t0 = lane < nr && ((sm.rec[lane].meta.w >> warp) & 1);
-                const bool t1 = 32 + lane < nr && ((sm.rec[32 + lane].meta.w >> warp) & 1);
-                const uint32_t m0 = __ballot_sync(0xffffffffu, t0);
-                const uint32_t m1 = __ballot_sync(0xffffffffu, t1);
-                if (t0) sm.prec[warp][__popc(m0 & lt)] = (uint8_t)lane;
-                if (t1) sm.prec[warp][__popc(m0) + __popc(m1 & lt)] = (uint8_t)(32 + lane);
-                tot = __popc(m0) + __popc(m1);
+                tot = 0;
+#pragma unroll
+                for (int q = 0; q < kChunk / 32; ++q) {
+                    const int r = 32 * q + lane;
+                    const bool t = r < nr && ((sm.rec[r].meta.w >> warp) & 1);
+                    const uint32_t m = __ballot_sync(0xffffffffu, t);
+                    if (t) sm.prec[warp][tot + __popc(m & lt)] = (uint8_t)r;
+                    tot += __popc(m);
+                }
                 __syncwarp();
             }
             constexpr int NTR = Win<S>::NTR;
