@@ -59,6 +59,10 @@ extern "C" {
  * f64 -- f32 on the FP32 path; every two rows of a strip are one 512-byte
  * run); the checkerboard sign of transform.py:180-185 is applied. */
 #define WSB_STRIP 16
+/* Columns of one gridder work item (one K2 CTA): a multiple of WSB_STRIP. */
+#ifndef WSB_ITEM_COLS
+#define WSB_ITEM_COLS 16
+#endif
 
 /* Longest transform handled on chip (one CTA) and longest transform
  * supported: rows/columns of SP = N / WSB_ONCHIP_FFT_N > 1 blocks are split
@@ -332,8 +336,8 @@ int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *idx_host, uint32_t *off_host,
 
 /* Debug / parity: the gridder's bucketing (K1) of m prepared records for
  * the slab rows [v_start, v_start+v_count): entries (record, work item)
- * with key = item << 8 | rowrel (item = (plane * ceil(n_u/64) + superstrip)
- * * ceil(v_count/128) + row block, rowrel = floor(gv) - S - (first row of the
+ * with key = item << 8 | rowrel (item = (plane * ceil(n_u/WSB_ITEM_COLS) +
+ * column block) * ceil(v_count/128) + row block, rowrel = floor(gv) - S - (first row of the
  * block - 2S)), sorted by key, record order for equal keys.
  * Host buffers (nullable): keys/idx u32[n_entries] (at most 4 m), off
  * u32[n_items + 1]. Sizes returned in *n_entries / *n_items / *item_bits.

@@ -273,7 +273,7 @@ def tap_bounds(g, S: int, lo: int, hi: int):
 
 
 def item_entries(gu, gv, plane, n_u: int, n_w: int, S: int, v_start: int, v_count: int,
-                 ss_cols: int = 64, item_rows: int = 128, row_bits: int = 8):
+                 ss_cols: int = 16, item_rows: int = 128, row_bits: int = 8):
     """The GPU gridder's work-item bucketing restated (contract of
     wsb_bucket_items, include/wsb.h): every (record, item) pair whose taps
     reach item = (plane, ss_cols-column superstrip, item_rows-row block of

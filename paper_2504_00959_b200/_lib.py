@@ -21,6 +21,7 @@ WSB_ENOMEM = -4
 WSB_EUNSUPPORTED = -5
 P_GROUP = 1
 STRIP = 16          # WSB_STRIP: column width of the gridder's strip layout
+ITEM_COLS = 16      # WSB_ITEM_COLS: columns of one gridder work item (K1 keys)
 EXEC_ENERGY = 1
 KERNEL_GAUSSIAN = 0
 KERNEL_KAISER_BESSEL = 1

@@ -1,28 +1,34 @@
-// K2: tensor-core window gridder over (plane, 64-column superstrip, 128-row
+// K2: tensor-core window gridder over (plane, 16-column strip, 128-row
 // block) work items (gridder.py:160-259, Eq. 3).
 //
-// CTA = 4 warps = one item (or one part of a large item); warp w owns the 16
-// columns [16w, 16w+16) of the superstrip. Its accumulator is a window of
-// 8-row tiles held as FP64 MMA fragments (m8n8k4: lane = row lane/4, columns
-// 2(lane%4), +1 of an 8x8 tile; two column halves x Re/Im per tile). The
-// item's records arrive sorted by anchor row (K1); four records at a time are
-// applied as rank-4 updates D += A B of every tile they reach, A = their v
-// weights on the tile rows (row sign folded), B = value x u weight on the
-// columns (column sign folded) -- one DMMA instruction per 256 multiply-adds
-// on the FP64 tensor cores. When the records move past a tile it is final:
-// the 32 lanes store it (8 rows x 16 columns, re | im) straight from the
-// fragments, clear it and the window moves 8 rows down (a ring of tiles,
-// one code copy per ring phase).
+// CTA = one warp = one item (or one part of a heavy item): the warp owns the
+// item's 16 columns (WSB_ITEM_COLS; a build can widen items to 2-4 strips,
+// one warp each). Its accumulator is a window of 8-row tiles held as FP64 MMA
+// fragments (m8n8k4: lane = row lane/4, columns 2(lane%4), +1 of an 8x8 tile;
+// two column halves x Re/Im per tile). The item's records arrive sorted by
+// anchor row (K1); four records at a time are applied as rank-4 updates
+// D += A B of every tile they reach, A = their v weights on the tile rows
+// (row sign folded), B = value x u weight on the columns (column sign folded)
+// -- one DMMA instruction per 256 multiply-adds on the FP64 tensor cores.
+// When the records move past a tile it is final: the 32 lanes store it (8
+// rows x 16 columns, re | im) straight from the fragments, clear it and the
+// window moves 8 rows down (a ring of tiles, one code copy per ring phase).
 //
 // Each cell accumulates in (anchor row, record) order in groups of four --
 // deterministic, and the same for any GPU count when slabs start on 128-row
 // boundaries (items then hold the same records) -- and is written once: no
 // shared-memory tile, no atomics, no read-modify-write of HBM.
 //
-// Records stream through the CTA in chunks of 64 gathered by cp.async two
-// chunks ahead (record index prefetched a chunk before its gather). Two
-// threads stage a record: one forms value x u weight per window column, the
-// other the v weights at the record's row offset in its 8-row step.
+// One warp per item keeps skewed data cheap: with four strips per CTA the
+// strips of an Earth-rotation track item carry very different record counts
+// and three warps waited at every chunk barrier (cfg3: 16.0 -> 10.6 ms). The
+// price is K1 entries for each 16-column strip a record reaches (1.23 per
+// record at cfg2 instead of 1.17 per 64-column block).
+//
+// Records stream through the warp in chunks of 16 gathered by cp.async one
+// chunk ahead (record index prefetched a chunk before its gather). Two lanes
+// stage a record: one forms value x u weight per window column, the other
+// the v weights at the record's row offset in its 8-row step.
 #include <type_traits>
 
 #include "i0_coeffs.h"
@@ -163,16 +169,18 @@ __device__ __forceinline__ void dispatch_phase(int phase, F &&f) {
 }
 
 constexpr int kC = WSB_STRIP;          // columns per warp strip
-constexpr int kWarps = 4;              // strips (warps) per item
-constexpr int kSS = kC * kWarps;       // superstrip width (64)
+constexpr int kSS = kSSCols;           // item width (WSB_ITEM_COLS)
+constexpr int kWarps = kSS / kC;       // strips (warps) per item
 constexpr int kThreads = 32 * kWarps;
-#ifndef WSB_CHUNK_MUL
-#define WSB_CHUNK_MUL 1
+constexpr int kRPR = kThreads / 2;     // records per gather / staging round (a thread pair each)
+#ifndef WSB_CHUNK
+#define WSB_CHUNK 16
 #endif
-constexpr int kCM = WSB_CHUNK_MUL;     // records per thread pair per chunk
-constexpr int kChunk = 64 * kCM;       // records staged per round
+constexpr int kChunk = WSB_CHUNK;      // records staged per round (<= 255: byte indices)
+constexpr int kCM = kChunk / kRPR;     // gather / staging rounds per chunk
+static_assert(kChunk % kRPR == 0 && (kWarps == 1 || kChunk % 32 == 0) && kChunk < 256, "chunk");
 #ifndef WSB_RAW
-#define WSB_RAW 3
+#define WSB_RAW 2
 #endif
 constexpr int kRaw = WSB_RAW;          // gather ring: chunks in flight
 
@@ -227,7 +235,7 @@ struct Shm {
 
 template <int KIND, int S>
 constexpr int sweep_min_blocks() {
-    return S <= 4 ? 6 : 4;
+    return (S <= 4 ? 24 : 16) / kWarps;
 }
 
 // m8n8k4 FP64 MMA, D = A B + D: a(row lane/4, k lane%4), b(k lane%4, col lane/4),
@@ -332,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                     }
                 }
             } else {
-                // partial tile [row][re | im][64 columns] of the item
+                // partial tile [row][re | im][kSS columns] of the item
                 double *pt_ = reinterpret_cast<double *>(ptile) + (int64_t)(row - R0) * (2 * kSS) +
                               warp * kC + c_lane;
 #pragma unroll
@@ -349,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     };
 
     // gather: thread pair (2r, 2r+1) copies the two 16-byte halves of
-    // records r, r + 64, ...; an entry's record index is loaded one chunk
+    // records r, r + kRPR, ...; an entry's record index is loaded one chunk
     // before its gather
     const int nchunks = (int)((n + kChunk - 1) / kChunk);
     struct Ids { uint32_t v[kCM]; };
@@ -357,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         Ids ids;
 #pragma unroll
         for (int q = 0; q < kCM; ++q) {
-            const uint32_t r = ch * kChunk + q * 64 + (tid >> 1);
+            const uint32_t r = ch * kChunk + q * kRPR + (tid >> 1);
             ids.v[q] = (ch < nchunks && r < n) ? __ldg(&a.idx[eb + r]) : 0u;
         }
         return ids;
@@ -366,13 +374,13 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         if (ch < nchunks) {
 #pragma unroll
             for (int q = 0; q < kCM; ++q) {
-                const uint32_t r = ch * kChunk + q * 64 + (tid >> 1);
+                const uint32_t r = ch * kChunk + q * kRPR + (tid >> 1);
                 if (r < n) {
                     const uint32_t id = ids.v[q];
                     WSB_DCHECK(id < a.n_rec, "item %lld id %u", (long long)item, id);
                     const double2 *src = reinterpret_cast<const double2 *>(a.rec + id) + (tid & 1);
                     const uint32_t dst = (uint32_t)__cvta_generic_to_shared(
-                        reinterpret_cast<double2 *>(&sm.raw[ch % kRaw][q * 64 + (tid >> 1)]) + (tid & 1));
+                        reinterpret_cast<double2 *>(&sm.raw[ch % kRaw][q * kRPR + (tid >> 1)]) + (tid & 1));
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
                 }
             }
@@ -399,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         // for the warp); only the short tails differ.
 #pragma unroll 1
         for (int q = 0; q < kCM; ++q) {
-            const int r = q * 64 + (tid >> 1), ax = tid & 1;
+            const int r = q * kRPR + (tid >> 1), ax = tid & 1;
             unsigned mine = 0;      // taps of this axis inside the item
             if (r < nr) {
                 const double4 rc = sm.raw[ch % kRaw][r];
@@ -466,7 +474,9 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             // window moving on in between.
             const uint32_t lt = (1u << lane) - 1u;
             int tot;
-            {
+            if constexpr (kWarps == 1) {
+                tot = nr;   // (K1 gives a one-strip item only records whose taps reach it)
+            } else {
                 tot = 0;
 #pragma unroll
                 for (int q = 0; q < kChunk / 32; ++q) {
@@ -487,8 +497,8 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             const double *wvp;                     // A: v weights of its rows
             auto load = [&]() {
                 pend = pos < tot;
-                const unsigned char *rp =
-                    recbase + (int)(pend ? sm.prec[warp][pos] : kChunk) * (int)sizeof(Rec);
+                const int slot = kWarps == 1 ? pos : (int)sm.prec[warp][pos];
+                const unsigned char *rp = recbase + (pend ? slot : kChunk) * (int)sizeof(Rec);
                 const int4 m = *reinterpret_cast<const int4 *>(rp + offsetof(Rec, meta));
                 const int c0 = wc8 - m.x;
                 const int i0 = (unsigned)c0 < (unsigned)W ? c0 : W;
@@ -666,7 +676,7 @@ __global__ void k_build_parts(const uint32_t *off, int64_t n_items, const uint32
 }
 
 // one thread per (row, column) of a split item: its parts' partial tiles
-// (signed, [row][re | im][64]) summed in part order, written to the strip
+// (signed, [row][re | im][kSS]) summed in part order, written to the strip
 // layout
 __global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split_items,
                                                   const uint32_t *part_off) {
@@ -678,10 +688,11 @@ __global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split
     const int ss = (int)(pt % a.n_ss), plane = (int)(pt / a.n_ss);
     const int R0 = a.v_start + rb * kItemRows;
     const int R1 = min(R0 + kItemRows, a.v_start + a.v_count);
-    const int wc = threadIdx.x & 63;                   // column inside the superstrip
+    constexpr int RPI = 128 / kSS;                     // rows per iteration of the block
+    const int wc = threadIdx.x % kSS;                  // column inside the item
     const int col = ss * kSS + wc;
     const uint2 *pr = a.part_rows + part_off[item];
-    for (int r = blockIdx.y * 2 + (threadIdx.x >> 6); r < kItemRows; r += gridDim.y * 2) {
+    for (int r = blockIdx.y * RPI + threadIdx.x / kSS; r < kItemRows; r += gridDim.y * RPI) {
         const int row = R0 + r;
         if (row >= R1) break;
         double re = 0.0, im = 0.0;

@@ -160,11 +160,12 @@ int row_histogram(wsb_ctx *ctx, const wsb_grid *g, const double *rec, int64_t n,
 int plane_histogram(wsb_ctx *ctx, const wsb_grid *g, const uint32_t *plane, int64_t n,
                     uint32_t *hist);
 
-// Gridder work items (bucket.cu, grid.cu): (w plane, kSSCols-column
-// superstrip, kItemRows-row block of the slab); one CTA of 4 warps per item,
-// warp = one WSB_STRIP-column strip.
+// Gridder work items (bucket.cu, grid.cu): (w plane, kSSCols-column block,
+// kItemRows-row block of the slab); one CTA per item, one warp per
+// WSB_STRIP-column strip of it.
 constexpr int kItemRows = 128;
-constexpr int kSSCols = 4 * WSB_STRIP;
+constexpr int kSSCols = WSB_ITEM_COLS;
+static_assert(kSSCols % WSB_STRIP == 0 && kSSCols <= 4 * WSB_STRIP, "item columns");
 constexpr int kPartCap = 2048;     // entries per work part (split heavy items)
 constexpr int kRowBits = 8;        // entry key = item << kRowBits | row offset
 

@@ -91,8 +91,10 @@ def test_cfg2_bucketing_bitexact(W, cfg2, slabs):
     r = rec[torch.from_numpy(sel).to(dev)].contiguous()
     pl = plane[torch.from_numpy(sel).to(dev)].contiguous()
     keys, idx, off, ib = W.bucket_items_device(r, pl, spec, 3, v0, vc)
+    from paper_2504_00959_b200 import _lib as L
     rk, ri, ro, rib = O.item_entries(u[sel] * spec.n_u, v[sel] * spec.n_v,
-                                     O.plane_of_w(w[sel], spec.n_w), spec.n_u, spec.n_w, 3, v0, vc)
+                                     O.plane_of_w(w[sel], spec.n_w), spec.n_u, spec.n_w, 3, v0, vc,
+                                     ss_cols=L.ITEM_COLS)
     assert ib == rib
     assert np.array_equal(off, ro)
     assert np.array_equal(keys, rk)

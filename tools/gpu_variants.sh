@@ -13,6 +13,9 @@ try:
 except Exception as e:
     print(v, "FAIL", e)
 PY
+  if [ -n "$CFG3" ]; then
+    WSB_LIB=$PWD/$L timeout 300 python tools/run_cfg3.py --steps 3 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('  cfg3', d['ms_per_step'], d['kernel_ms'])"
+  fi
   if [ -n "$LAUNCHES" ]; then
     WSB_LIB=$PWD/$L ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/var_$v.csv python tools/repro_grid.py 10000000 2048 32 > /dev/null 2>&1
     python tools/launch_summary.py gpurun_out/var_$v.csv | head -12
