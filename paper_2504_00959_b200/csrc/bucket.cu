@@ -317,31 +317,26 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
 }
 
 // item offsets from the sorted keys: off[it] = first entry of item it (the
-// next non-empty item's first entry for an empty one), off[n_items] = n
-// (four entries per thread: one 16-byte load and the previous key)
+// next non-empty item's first entry for an empty one), off[n_items] = n --
+// one binary search per item (Earth-rotation tracks leave long runs of empty
+// items between two entries: a fill loop per boundary serialised them)
 __global__ void k_item_offsets(const uint32_t *__restrict__ keys, int64_t n, int64_t n_items,
                                uint32_t *__restrict__ off) {
-    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-    if (i0 > n) return;
-    int64_t cur[4];
-    if (i0 + 4 <= n) {
-        const uint4 k4 = __ldg(reinterpret_cast<const uint4 *>(keys + i0));
-        cur[0] = k4.x >> kRowBits;
-        cur[1] = k4.y >> kRowBits;
-        cur[2] = k4.z >> kRowBits;
-        cur[3] = k4.w >> kRowBits;
+    const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (it > n_items) return;
+    int64_t lo = 0, hi = n;
+    if (it == n_items) {
+        lo = n;
     } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            cur[q] = i0 + q < n ? (int64_t)(__ldg(&keys[i0 + q]) >> kRowBits) : n_items;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)(__ldg(&keys[mid]) >> kRowBits) < it)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
     }
-    int64_t prev = i0 > 0 ? (int64_t)(__ldg(&keys[i0 - 1]) >> kRowBits) : -1;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        if (i0 + q > n) break;
-        for (int64_t it = prev + 1; it <= cur[q]; ++it) off[it] = (uint32_t)(i0 + q);
-        prev = cur[q];
-    }
+    off[it] = (uint32_t)lo;
 }
 
 }  // namespace
@@ -433,8 +428,7 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     if (e & kErrTime) return fail(WSB_EINVAL, "records must be sorted by time_index");
     uint32_t *ks, *is;
     WSB_TRY(radix_sort_pairs(ctx, ka, kb, ia, ib, n_entries, k.item_bits + kRowBits, &ks, &is));
-    k_item_offsets<<<ceil_div(((int64_t)n_entries + 4) / 4, 256), 256, 0, ctx->stream>>>(ks, n_entries,
-                                                                                       n_items, off);
+    k_item_offsets<<<ceil_div(n_items + 1, 256), 256, 0, ctx->stream>>>(ks, n_entries, n_items, off);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     out->keys = ks;
