@@ -79,6 +79,71 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+class NvmlClockSampler:
+    """SM clock and throttle reasons sampled through NVML every 5 ms during
+    the timed region (nvidia-smi's 100 ms period gives one sample of a
+    0.1 s region). Same interface as ClockSampler."""
+
+    PERIOD = 0.005
+    BITS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+            ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
+
+    def __init__(self, dev):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        props = torch.cuda.get_device_properties(dev)
+        bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+        self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)    # (raise here, not in the thread)
+        pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.samples = []
+        self.stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), float(sm), int(rs)))
+            except Exception:
+                pass
+            time.sleep(self.PERIOD)
+
+    def __enter__(self):
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+        return self
+
+    def mark(self, which: str):
+        setattr(self, "t_" + which, time.perf_counter())
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        self.thread.join(timeout=2)
+
+    def summary(self):
+        t0, t1 = getattr(self, "t_start", -1e18), getattr(self, "t_end", 1e18)
+        inside = [x for x in self.samples if t0 <= x[0] <= t1]
+        if not inside and self.samples:
+            inside = [min(self.samples, key=lambda x: abs(x[0] - t1))]
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": self.mx, "reasons": [], "samples": 0, "source": "nvml"}
+        reasons = sorted({nm for _, _, rs in inside for nm, bit in self.BITS if rs & bit})
+        return {"sm_mhz": float(np.median([x[1] for x in inside])), "sm_max_mhz": self.mx,
+                "reasons": reasons, "samples": len(inside), "source": "nvml, 5 ms period"}
+
+
+def clock_sampler(dev):
+    """NVML sampler when pynvml can see the device, else nvidia-smi."""
+    try:
+        return NvmlClockSampler(dev)
+    except Exception:
+        return ClockSampler(dev.index if hasattr(dev, "index") else int(dev))
+
+
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons during the timed region."""
 
@@ -195,7 +260,7 @@ def run_ours(args):
                                         decomposition=decomp)
         return W.image_device(du, dv, dw, dvis, dwt, spec, kern, image_out=img)
 
-    clk = ClockSampler(dev.index).__enter__()   # sampling runs through warm-up and timing
+    clk = clock_sampler(dev).__enter__()   # sampling runs through warm-up and timing
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()

@@ -13,6 +13,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 python tools/profile_step.py --steps 1 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_(grid_sweep|fft_rows|fft_cols|prepare|radix_scatter|radix_hist|keys_count|keys_write)" \
+    -k regex:"k_(grid_items|fft_rows|fft_cols|keys|count|radix_scatter|radix_hist|item_offsets)" \
     -c 12 -o gpurun_out/full python tools/profile_step.py --steps 1 > gpurun_out/ncu_full.log 2>&1
+# cfg3 (north-star mesh): launch list of one step
+python tools/run_cfg3.py --steps 1 > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_cfg3_raw.csv python tools/run_cfg3.py --steps 1 > /dev/null 2>&1
 echo done

@@ -15,8 +15,8 @@ OUT = ROOT / "gpurun_out"
 PROF = ROOT / "profiles"
 
 GROUPS = {  # bench.py kernel-table names
-    "k_prepare": "prepare(K1a)", "k_radix_scatter": "bucket_scatter(K1c)",
-    "k_grid_sweep": "grid(K2)", "k_fft_rows": "fft_rows(K3a)",
+    "k_keys": "bucket_keys(K1a)", "k_radix_scatter": "bucket_scatter(K1c)",
+    "k_grid_items": "grid(K2)", "k_fft_rows": "fft_rows(K3a)",
     "k_fft_cols": "fft_cols_stack(K3b+K4)",
 }
 
@@ -27,6 +27,10 @@ def main():
     subprocess.run([sys.executable, str(ROOT / "tools/launch_summary.py"),
                     str(OUT / "launches_raw.csv"), str(PROF / f"launches_{rnd}.csv")], check=True,
                    capture_output=True)
+    if (OUT / "launches_cfg3_raw.csv").exists():
+        subprocess.run([sys.executable, str(ROOT / "tools/launch_summary.py"),
+                        str(OUT / "launches_cfg3_raw.csv"), str(PROF / f"launches_cfg3_{rnd}.csv")],
+                       check=True, capture_output=True)
     rep = OUT / "full.ncu-rep"
     txt = subprocess.run([sys.executable, str(ROOT / "tools/ncu_summary.py"), str(rep)],
                          capture_output=True, text=True).stdout
@@ -52,9 +56,9 @@ def main():
 
 
 # hot kernels whose SASS is kept: (file stem, regex on the mangled name)
-SASS = (("k_grid_sweep_0_3", r"k_grid_sweepILi0ELi3E"), ("k_fft_rows_11", r"k_fft_rowsILi11ELi0E7double2"),
+SASS = (("k_grid_items_0_3", r"k_grid_itemsILi0ELi3E"), ("k_fft_rows_11", r"k_fft_rowsILi11ELi0E7double2"),
         ("k_fft_cols_11", r"k_fft_colsILi11ELi0E7double2"), ("k_fft_cols_11_fp32", r"k_fft_colsILi11ELi0E6float2"),
-        ("k_radix_scatter_8", r"k_radix_scatterILi8ELb0E"), ("k_keys_write", r"k_keys_write"),
+        ("k_radix_scatter_8", r"k_radix_scatterILi8ELb0E"), ("k_keys", r"k_keysILb1E"),
         ("k_prepare", r"k_prepareEPK"), ("k_push", r"k_push[^4]"), ("k_image_finish", r"k_image_finish"),
         ("k_route_pack", r"k_route_pack"))
 
