@@ -22,8 +22,8 @@
 // One warp per item keeps skewed data cheap: with four strips per CTA the
 // strips of an Earth-rotation track item carry very different record counts
 // and three warps waited at every chunk barrier (cfg3: 16.0 -> 10.6 ms). The
-// price is K1 entries for each 16-column strip a record reaches (1.23 per
-// record at cfg2 instead of 1.17 per 64-column block).
+// price is K1 entries for each 16-column strip a record reaches (1.36 per
+// record at cfg2 instead of 1.12 per 64-column block).
 //
 // Records stream through the warp in chunks of 16 gathered by cp.async one
 // chunk ahead (record index prefetched a chunk before its gather). Two lanes
