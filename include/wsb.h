@@ -218,9 +218,10 @@ int wsb_row_histogram(wsb_ctx *ctx, const wsb_grid *grid, const double *rec, int
                       uint32_t *hist);
 
 /* grid_sector (gridder.py:186-259) for the slab rows [v_start, v_start+v_count):
- * buckets the m records into work items (w plane, 64-column superstrip,
- * 128-row block; stable radix sort, record order inside an item), grids them
- * with the convolution kernel in a register-window sweep and writes the slab
+ * buckets the m records into work items (w plane, WSB_ITEM_COLS-column
+ * block, 128-row block; stable radix sort, (anchor row, record) order inside
+ * an item), grids them with the convolution kernel as rank-4 FP64 tensor-core
+ * updates of a register window of 8-row tiles and writes the slab
  * in the strip layout (grid_s: complex128[n_w][ceil(n_u/WSB_STRIP)][v_count]
  * [WSB_STRIP], sign applied). grid_updates (host, nullable) receives the
  * number of cell updates. Synchronises (entry count). Slabs that start on a
@@ -328,8 +329,8 @@ int wsb_grid_unpack_rows(wsb_ctx *ctx, const wsb_grid *grid, int32_t v_start, in
 
 /* Debug / parity: the bucketing of the last wsb_grid_slab / wsb_image_device
  * call: record indices in item order (record order inside an item) and the
- * n_items+1 item offsets, item = (plane * ceil(n_u/64) + superstrip) *
- * ceil(v_count/128) + row block. Sizes via wsb_tiles_debug(ctx, NULL, NULL,
+ * n_items+1 item offsets, item = (plane * ceil(n_u/WSB_ITEM_COLS) + column
+ * block) * ceil(v_count/128) + row block. Sizes via wsb_tiles_debug(ctx, NULL, NULL,
  * &n, &nb). */
 int wsb_tiles_debug(wsb_ctx *ctx, uint32_t *idx_host, uint32_t *off_host,
                     int64_t *n_entries, int64_t *n_buckets);
