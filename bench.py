@@ -92,12 +92,18 @@ class NvmlClockSampler:
         import pynvml
         self.nv = pynvml
         pynvml.nvmlInit()
-        props = torch.cuda.get_device_properties(dev)
-        bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
-        self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        idx = dev.index if hasattr(dev, "index") and dev.index is not None else int(dev)
+        try:   # the CUDA device's PCI address (CUDA_VISIBLE_DEVICES may renumber)
+            props = torch.cuda.get_device_properties(idx)
+            bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+        self.reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(pynvml, "nvmlDeviceGetCurrentClocksThrottleReasons")
         self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
         pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)    # (raise here, not in the thread)
-        pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.reasons_fn(self.h)
         self.samples = []
         self.stop = threading.Event()
 
@@ -106,7 +112,7 @@ class NvmlClockSampler:
         while not self.stop.is_set():
             try:
                 sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                rs = self.reasons_fn(self.h)
                 self.samples.append((time.perf_counter(), float(sm), int(rs)))
             except Exception:
                 pass
@@ -140,7 +146,8 @@ def clock_sampler(dev):
     """NVML sampler when pynvml can see the device, else nvidia-smi."""
     try:
         return NvmlClockSampler(dev)
-    except Exception:
+    except Exception as e:
+        log(f"NVML clock sampler unavailable ({type(e).__name__}: {e}); nvidia-smi at 100 ms")
         return ClockSampler(dev.index if hasattr(dev, "index") else int(dev))
 
 
