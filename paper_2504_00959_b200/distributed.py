@@ -763,3 +763,129 @@ def image_distributed_stream(batches, spec, kern, group=None, root: int = 0, **k
         done[slot].record(compute)
         yield img, diag
         i += 1
+
+
+def _route_counts_local(rec, spec, half_support: int, R: int):
+    """Records of this rank's prepared partition that each v-slab of
+    partition_1d(n_v, R) receives under the +-half_support halo predicate
+    (comms.py:516-523), counted on the GPU (wsb_route_count): [R] ints."""
+    ctx = context(rec.device)
+    g = spec.c_struct()
+    cnt = (C.c_int64 * R)()
+    n = rec.shape[0]
+    L.check(L.lib().wsb_route_count(ctx.handle, C.byref(g), int(half_support), R, None,
+                                    _ptr(rec) if n else None, n, cnt))
+    return [int(x) for x in cnt]
+
+
+def run_pipeline_distributed(dataset_path, n_u: int, n_v: int, n_w: int, cell_size_lm: float,
+                             kernel, group=None, root: int = 0, strategy=None, meter=None,
+                             freq_level: str = "default", label: str = "run", out_dir=None,
+                             pgm: bool = False, seed=None, **image_kwargs):
+    """run_pipeline (pipeline.py:61-191) over a process group, one GPU per
+    rank (torchrun). Ingest as the reference's read phase: rank r takes the
+    r-th time partition of the RVIS dataset (_partition_for_ranks,
+    pipeline.py:47-58 -> partition_time_ordered, visdata.py:344-366:
+    contiguous groups of time slices; an unsorted time_index raises its
+    ValueError on every rank) and reads only those records of the
+    memory-mapped file; image_distributed then exchanges them to their
+    v-slabs, grids, transforms and stacks (``image_kwargs`` go to it; the
+    default deterministic v-slab decomposition gives run_pipeline's image bit
+    for bit). The topology is 1 node x R ranks; the MessageLog / ``ops`` are
+    the reference's virtual choreography for it (msglog.py), from exchange
+    counts each rank measures on its own records. Returns the PipelineResult
+    on ``root`` and None on the other ranks."""
+    import time as _time
+
+    from . import msglog
+    from .imager import (PipelineResult, RunRecord, GridSpec, _partition_bounds, measure,
+                         read_dataset, write_image)
+
+    kern = as_kernel_spec(kernel)
+    kind = getattr(strategy, "kind", "direct") if strategy is not None else "direct"
+    if kind not in msglog.REDUCE_KINDS:
+        raise ValueError(f"reduce kind must be one of {msglog.REDUCE_KINDS}, got {kind!r}")
+    R, r = dist.get_world_size(group), dist.get_rank(group)
+    if meter is not None and hasattr(meter, "start") and r == root:
+        meter.start()
+    t_begin = _time.perf_counter()
+    times = {}
+    # 1. read: this rank's contiguous run of observing time
+    t0 = _time.perf_counter()
+    header, _ = read_dataset(dataset_path, rows=(0, 0))
+    from .imager import _HEADER, _record_dtype
+    rec_dt = _record_dtype(header["n_freq"] * header["n_corr"])
+    t_idx = (np.asarray(np.memmap(dataset_path, dtype=rec_dt, mode="r", offset=_HEADER.size,
+                                  shape=(header["n_records"],))["time_index"])
+             if header["n_records"] else np.zeros(0, np.uint32))
+    bounds, time_ordered = _partition_bounds(t_idx, R)
+    if time_ordered and len(t_idx) > 1 and np.any(np.diff(t_idx.astype(np.int64)) < 0):
+        raise ValueError("records must be sorted by time_index")
+    lo, hi = bounds[r]
+    _, cols = read_dataset(dataset_path, rows=(lo, hi))
+    spec = GridSpec(n_u=n_u, n_v=n_v, n_w=n_w, cell_size_lm=cell_size_lm,
+                    w_min_native=header["w_min_native"], w_max_native=header["w_max_native"])
+    times["read"] = _time.perf_counter() - t0
+    # 2-5. exchange, gridding, transforms, w correction, stack
+    t0 = _time.perf_counter()
+    stage_ms = {}
+    img, diag = image_distributed(cols["u"], cols["v"], cols["w"], cols["vis"], cols["weight"],
+                                  spec, kern, group=group, root=root, to_host=True,
+                                  timings=stage_ms, **image_kwargs)
+    wall = _time.perf_counter() - t0
+    grid_ms = sum(stage_ms.get(k, 0.0) for k in ("prepare", "route", "exchange", "grid"))
+    fft_ms = sum(stage_ms.get(k, 0.0) for k in ("rows", "cols", "fft"))
+    fin_ms = sum(stage_ms.get(k, 0.0) for k in ("gather", "reduce"))
+    dev_total = max(grid_ms + fft_ms + fin_ms, 1e-9)
+    scale = wall / (dev_total / 1e3) if dev_total > 0 else 0.0
+    times["gridding"] = grid_ms / 1e3 * scale
+    times["reduce"] = 0.0          # the identity after the exchange (pipeline.py:117-122)
+    times["fft"] = fft_ms / 1e3 * scale
+    times["wcorrect"] = fin_ms / 1e3 * scale
+    # the reference's message log for 1 x R ranks: exchange counts per source
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rec, _pl = prepare_device(cols["u"], cols["v"], cols["w"], cols["vis"], cols["weight"], spec,
+                              device=dev)
+    mine = torch.tensor(_route_counts_local(rec, spec, kern.half_support, R), dtype=torch.int64,
+                        device=dev)
+    del rec, _pl
+    allc = [torch.empty_like(mine) for _ in range(R)]
+    dist.all_gather(allc, mine, group=group)
+    if r != root:
+        return None
+    counts = [c.cpu().tolist() for c in allc]
+
+    class _Topo:   # Topology(n_nodes=1, ranks_per_node=R, threads_per_rank=1)
+        n_nodes, ranks_per_node, threads_per_rank, n_ranks = 1, R, 1, R
+
+    topo = _Topo()
+    log = msglog.virtual_log(topo, kind, n_u, n_v, n_w, counts) if R > 1 else msglog.MessageLog()
+    t0 = _time.perf_counter()
+    paths = {}
+    if out_dir is not None:
+        from pathlib import Path as _Path
+        out_dir = _Path(out_dir)
+        out_dir.mkdir(parents=True, exist_ok=True)
+        prov = {"dataset": str(dataset_path),
+                "kernel": {"kind": kern.kind, "half_support": kern.half_support,
+                           "shape_param": kern.shape_param},
+                "topology": {"n_nodes": 1, "ranks_per_node": R, "threads_per_rank": 1},
+                "strategy": {"kind": kind,
+                             "deterministic": getattr(strategy, "deterministic", True)},
+                "engine": "wsb-b200", "gpus": R, "seed": seed}
+        paths = write_image(img, out_dir / "image", prov, pgm=pgm)
+        log.to_csv(out_dir / "messages.csv")
+        paths["messages"] = out_dir / "messages.csv"
+    times["write"] = _time.perf_counter() - t0
+    times["total"] = _time.perf_counter() - t_begin
+    energy = {}
+    if meter is not None:
+        energy = measure(meter, {k: v for k, v in times.items() if k != "total"}, freq_level)
+    ops = {"records": int(header["n_records"]), "grid_updates": int(diag["grid_updates"]),
+           "exchange_bytes": log.total_bytes(phase="exchange"),
+           "reduce_bytes": log.total_bytes(phase="reduce"),
+           "fft_bytes": log.total_bytes(phase="fft"),
+           "reduce_messages": log.count(phase="reduce"), "stack_pixels": n_u * n_v}
+    run = RunRecord(label=label, topology=topo, freq_level=freq_level, phase_times=times,
+                    energy_joules=energy)
+    return PipelineResult(run=run, image=img, log=log, ops=ops, paths=paths)

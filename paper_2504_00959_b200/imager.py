@@ -757,10 +757,11 @@ class ChunkSpec:
             raise ValueError(f"chunk_index {self.chunk_index} outside range(0, {self.n_chunks})")
 
 
-def read_dataset(path, chunk: ChunkSpec | None = None):
+def read_dataset(path, chunk: ChunkSpec | None = None, rows: tuple | None = None):
     """Read an RVIS file (visdata.py:312-341): 64-byte header + records of
-    28 + 12*n_chan bytes, optionally one ChunkSpec of it. The file is memory
-    mapped, so a chunk reads only what it selects. Returns (header dict,
+    28 + 12*n_chan bytes, optionally one ChunkSpec of it, or only the records
+    [rows[0], rows[1]) (a rank's time partition). The file is memory mapped,
+    so a chunk or row range reads only what it selects. Returns (header dict,
     dict of column arrays)."""
     path = Path(path)
     with open(path, "rb") as fh:
@@ -779,6 +780,8 @@ def read_dataset(path, chunk: ChunkSpec | None = None):
         raise FormatError(f"truncated file: {body} payload bytes, expected {n_rec * rec_dt.itemsize}")
     packed = (np.memmap(path, dtype=rec_dt, mode="r", offset=_HEADER.size, shape=(n_rec,))
               if n_rec else np.zeros(0, dtype=rec_dt))
+    if rows is not None:
+        packed = packed[int(rows[0]):int(rows[1])]
     c0, c1 = 0, n_chan
     if chunk is not None and chunk.axis == "frequency":
         f0, fc = partition_1d(n_freq, chunk.n_chunks, chunk.chunk_index)   # visdata.py:297-300
@@ -928,8 +931,9 @@ def run_pipeline(dataset_path, n_u: int, n_v: int, n_w: int, cell_size_lm: float
     choreography on ``topo`` (msglog.py; exchange counts measured on the
     GPU). The image itself does not depend on the topology (the reference
     guarantees bit-identical grids for any rank count, gridder.py:267-268)
-    and is computed once on ``device``. Multi-GPU imaging is
-    ``distributed.run_pipeline_distributed`` (one process per GPU).
+    and is computed once on ``device``. Multi-GPU imaging of a dataset is
+    ``distributed.run_pipeline_distributed`` (one process per GPU, each
+    reading its own time partition).
     ``meter``: any object with ``start()`` and ``joules(durations,
     freq_level)`` (the reference's meters, energy.NvmlRaplMeter); per-phase
     joules as metrics.measure returns them (pipeline.py:173-176)."""

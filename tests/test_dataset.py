@@ -72,3 +72,22 @@ def test_image_time_chunks_streamed(W):
         ref, dref = W.image(c["u"], c["v"], c["w"], None, c["vis"], c["weight"], spec, kern)
         assert img.pixels.tobytes() == ref.pixels.tobytes()
         assert diag["grid_updates"] == dref["grid_updates"]
+
+
+@pytest.mark.parametrize("R", [1, 2, 3, 4, 8])
+def test_rank_partitions_read_only_their_rows(W, R):
+    """Multi-GPU ingest (run_pipeline_distributed): rank r reads records
+    [lo, hi) of the r-th time partition (_partition_for_ranks,
+    pipeline.py:47-58); the partitions tile the file in order."""
+    from paper_2504_00959_b200.imager import _partition_bounds
+    _, cols = W.read_dataset(GOLD / "chunks.rvis")
+    bounds, ordered = _partition_bounds(cols["time_index"], R)
+    assert ordered and bounds[0][0] == 0 and bounds[-1][1] == len(cols["u"])
+    assert all(a[1] == b[0] for a, b in zip(bounds, bounds[1:]))
+    for lo, hi in bounds:
+        _, part = W.read_dataset(GOLD / "chunks.rvis", rows=(lo, hi))
+        for k in ("u", "v", "w", "time_index", "vis", "weight"):
+            assert part[k].tobytes() == cols[k][lo:hi].tobytes(), k
+        # a partition holds whole time slices
+        if hi < len(cols["u"]):
+            assert cols["time_index"][hi - 1] != cols["time_index"][hi]

@@ -11,7 +11,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from conftest import chunk_from, rel_l2
+from conftest import GOLDEN, chunk_from, rel_l2
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -255,10 +255,31 @@ def _nccl_worker(rank, world, port, outdir):
         for bi, (img, diag) in enumerate(image_distributed_stream(batches, spec, kern)):  # auto
             if rank == 0:
                 outs[f"pstream{bi}"] = img.pixels
+        # multi-GPU ingest: every rank reads its own time partition of an RVIS
+        # dataset (run_pipeline over the process group)
+        from paper_2504_00959_b200.distributed import run_pipeline_distributed
+        res = run_pipeline_distributed(TESTS / "golden" / "chunks.rvis", 64, 64, 4, 1e-3,
+                                       W.KernelSpec.gaussian(3, 1.0), out_dir=Path(outdir) / "rpd")
+        if rank == 0:
+            outs["rpd_pixels"] = res.image.pixels
+            outs["rpd_ops"] = np.array([res.ops[k] for k in _OPS])
+            outs["rpd_phases"] = np.array(sorted(res.run.phase_times))
+        else:
+            assert res is None
         if rank == 0:
             np.savez(Path(outdir) / "out.npz", **outs)
     finally:
         dist.destroy_process_group()
+
+
+_OPS = ("records", "grid_updates", "exchange_bytes", "reduce_bytes", "fft_bytes",
+        "reduce_messages", "stack_pixels")
+
+
+class _Topo:
+    def __init__(self, n_nodes, ranks_per_node):
+        self.n_nodes, self.ranks_per_node, self.threads_per_rank = n_nodes, ranks_per_node, 1
+        self.n_ranks = n_nodes * ranks_per_node
 
 
 def test_nccl_multi_gpu_matches_single(W, golden_image, tmp_path):
@@ -297,3 +318,11 @@ def test_nccl_multi_gpu_matches_single(W, golden_image, tmp_path):
         assert out[f"stream{bi}"].tobytes() == ref_b.pixels.tobytes(), bi
         err = np.linalg.norm(out[f"pstream{bi}"] - ref_b.pixels) / np.linalg.norm(ref_b.pixels)
         assert err <= 1e-13, (bi, err)
+    # run_pipeline_distributed vs the single-GPU run_pipeline on topology 1 x world
+    one = W.run_pipeline(GOLDEN / "chunks.rvis", 64, 64, 4, 1e-3, W.KernelSpec.gaussian(3, 1.0),
+                         topo=_Topo(1, world), out_dir=tmp_path / "one")
+    err = np.linalg.norm(out["rpd_pixels"] - one.image.pixels) / np.linalg.norm(one.image.pixels)
+    assert err <= 1e-13, err
+    assert [int(x) for x in out["rpd_ops"]] == [one.ops[k] for k in _OPS]
+    assert (tmp_path / "rpd" / "messages.csv").read_text() == (tmp_path / "one" / "messages.csv").read_text()
+    assert list(out["rpd_phases"]) == ["fft", "gridding", "read", "reduce", "total", "wcorrect", "write"]
