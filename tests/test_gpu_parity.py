@@ -115,6 +115,36 @@ def test_grid_kaiser_bessel_any_beta(W, golden_grid, S, beta):
     assert np.max(np.abs(grid - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
 
 
+@pytest.mark.parametrize("kind,S", [("gaussian", 2), ("gaussian", 4), ("gaussian", 5),
+                                    ("gaussian", 6), ("gaussian", 7), ("kaiser_bessel", 4),
+                                    ("kaiser_bessel", 7)])
+def test_grid_every_support_vs_oracle(W, kind, S):
+    """Every K2 instantiation (half supports 1..7: two- and three-tile
+    windows) against the oracle's grid_slab, on dense random records that
+    fill single items beyond one work part (split items) and reach the mesh
+    edges; grid_updates equal."""
+    rng = np.random.default_rng(100 + S)
+    n = 40000
+    u = np.concatenate([rng.random(n // 2), 0.30 + 0.02 * rng.random(n // 2)])   # a dense patch
+    v = np.concatenate([rng.random(n // 2), 0.60 + 0.02 * rng.random(n // 2)])
+    w = rng.random(n)
+    t = np.zeros(n, np.uint32)
+    vis = (rng.standard_normal((n, 1)) + 1j * rng.standard_normal((n, 1))).astype(np.complex64)
+    wt = rng.uniform(0.5, 1.5, (n, 1)).astype(np.float32)
+    spec = W.GridSpec(128, 128, 3, 1e-3, w_max_native=10.0)
+    shape = 1.0 if kind == "gaussian" else 2.34 * S
+    kern = W.KernelSpec(kind, S, shape)
+    rec, plane = W.prepare_device(u, v, w, vis, wt, spec)
+    gp, upd = W.grid_slab_device(rec, plane, spec, kern, 0, 128)
+    grid = W.unpack_grid_device(gp, spec, 0, 128).cpu().numpy()
+    prep = O.prepare(u, v, w, t, vis, wt, 128, 128, 3)
+    batch = O.exchange([prep], 128, 1, S)[0]
+    ref, upd_ref = O.grid_slab(batch, 128, 3, O.KIND_GAUSSIAN if kind == "gaussian" else O.KIND_KAISER_BESSEL,
+                               S, shape, 0, 128)
+    assert upd == upd_ref
+    assert np.max(np.abs(grid - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+
 @pytest.mark.parametrize("R", [2, 4])
 def test_grid_slabs_bitwise_across_slab_counts(W, golden_grid, R):
     """Per-slab gridding after the exchange reproduces the 1-slab grid
