@@ -558,6 +558,7 @@ int wsb_bucket_items(wsb_ctx *ctx, const wsb_grid *grid, int32_t half_support, i
     if (n_items) *n_items = bk.n_items;
     if (item_bits) *item_bits = bk.item_bits;
     WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    WSB_TRY(bucket_errors(ctx));
     if (keys_host && bk.n_entries)
         WSB_CUDA_TRY(cudaMemcpy(keys_host, bk.keys, 4 * bk.n_entries, cudaMemcpyDeviceToHost));
     if (idx_host && bk.n_entries)

@@ -99,6 +99,7 @@ struct KeysArgs {
     KeyGeom g;
     uint32_t *keys, *idx;       // entries in record order
     const uint32_t *block_off;  // [n_blocks] first entry of each tile (k_count + scan)
+    uint32_t cap;               // entries the key / index buffers hold (more are dropped: re-run)
     int *err;
 };
 
@@ -311,8 +312,10 @@ __global__ void __launch_bounds__(kThreads) k_keys(KeysArgs a) {
     const uint32_t pos0 = a.block_off[bid];
     WSB_DCHECK((int64_t)pos0 + rbase <= 4 * a.n, "tile %u pos %u", bid, pos0);
     for (uint32_t q = tid; q < rbase; q += kThreads) {
-        a.keys[pos0 + q] = sk[q];
-        a.idx[pos0 + q] = si[q];
+        if (pos0 + q < a.cap) {
+            a.keys[pos0 + q] = sk[q];
+            a.idx[pos0 + q] = si[q];
+        }
     }
 }
 
@@ -358,7 +361,8 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     // item << kRowBits | rowrel (rowrel < kItemRows + 2S) in 32 bits
     static_assert(kItemRows + 2 * kMaxS <= (1 << kRowBits), "row offset bits");
     if (k.item_bits + kRowBits > 32) return fail(WSB_EUNSUPPORTED, "gridder item space exceeds 32-bit keys");
-    if (m > (int64_t)(0x7FFFFFFF / 4)) return fail(WSB_EUNSUPPORTED, "more than 2^29 records per GPU");
+    // (at most 4 entries per record: the u32 entry count cannot wrap)
+    if (m > (int64_t)1 << 30) return fail(WSB_EUNSUPPORTED, "more than 2^30 records per GPU");
     uint32_t *off;
     WSB_TRY(ensure(ctx, kSlotTileOff, sizeof(uint32_t) * (n_items + 1), (void **)&off));
     const int nb = std::max(1, ceil_div(m, kTile));
@@ -369,13 +373,24 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     WSB_CUDA_TRY(cudaMemsetAsync(bcnt, 0, sizeof(uint32_t) * (nb + 8), ctx->stream));
     uint32_t *total = boff + nb;       // exclusive scan over nb + 1 counts: the total
     int *err = reinterpret_cast<int *>(bcnt + nb + 4);
-    // entry buffers: at most 4 entries per record
-    const size_t eb = sizeof(uint32_t) * std::max<int64_t>(1, 4 * m);
-    uint32_t *ka, *kb, *ia, *ib;
-    WSB_TRY(ensure(ctx, kSlotKeysA, eb, (void **)&ka));
-    WSB_TRY(ensure(ctx, kSlotKeysB, eb, (void **)&kb));
-    WSB_TRY(ensure(ctx, kSlotIdxA, eb, (void **)&ia));
-    WSB_TRY(ensure(ctx, kSlotIdxB, eb, (void **)&ib));
+    if (m > 0) {
+        if (in)
+            k_count<true><<<nb, kThreads, 0, ctx->stream>>>(in->u, in->v, nullptr, m, k, bcnt);
+        else
+            k_count<false><<<nb, kThreads, 0, ctx->stream>>>(nullptr, nullptr, (const double4 *)rec, m,
+                                                              k, bcnt);
+        ctx->launches += 1;
+        WSB_CUDA_TRY(cudaGetLastError());
+    }
+    WSB_TRY(exclusive_scan_u32(ctx, bcnt, boff, nb + 1, nullptr));
+    // k_keys writes into buffers of the capacity they have (at least 2 entries
+    // per record: 1.1-1.4 typical, 4 the worst case); the entry count comes
+    // back with the validation flags, and an overflow re-runs k_keys once
+    // with exact buffers
+    auto cap_of = [&](int slot) { return ctx->bufs[slot].bytes / sizeof(uint32_t); };
+    uint32_t *ka, *ia;
+    WSB_TRY(ensure(ctx, kSlotKeysA, sizeof(uint32_t) * std::max<int64_t>(1024, 2 * m + 1024), (void **)&ka));
+    WSB_TRY(ensure(ctx, kSlotIdxA, sizeof(uint32_t) * std::max<int64_t>(1024, 2 * m + 1024), (void **)&ia));
     KeysArgs a;
     a.u = in ? in->u : nullptr;
     a.v = in ? in->v : nullptr;
@@ -387,45 +402,46 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     a.plane = plane;
     a.n = m;
     a.g = k;
-    a.keys = ka;
-    a.idx = ia;
     a.block_off = boff;
     a.err = err;
-    if (m > 0) {
-        if (in)
-            k_count<true><<<nb, kThreads, 0, ctx->stream>>>(in->u, in->v, nullptr, m, k, bcnt);
-        else
-            k_count<false><<<nb, kThreads, 0, ctx->stream>>>(nullptr, nullptr, (const double4 *)rec, m,
-                                                              k, bcnt);
-        ctx->launches += 1;
-        WSB_CUDA_TRY(cudaGetLastError());
-    }
-    WSB_TRY(exclusive_scan_u32(ctx, bcnt, boff, nb + 1, nullptr));
-    if (m > 0) {
-        if (in) {
-            const int sm = (int)sizeof(KeysSmem<true>);
-            WSB_CUDA_TRY(cudaFuncSetAttribute(k_keys<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-            k_keys<true><<<nb, kThreads, sm, ctx->stream>>>(a);
-        } else {
-            const int sm = (int)sizeof(KeysSmem<false>);
-            WSB_CUDA_TRY(cudaFuncSetAttribute(k_keys<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-            k_keys<false><<<nb, kThreads, sm, ctx->stream>>>(a);
+    auto run_keys = [&]() -> int {
+        a.keys = ka;
+        a.idx = ia;
+        a.cap = (uint32_t)std::min<size_t>(std::min(cap_of(kSlotKeysA), cap_of(kSlotIdxA)), 0xFFFFFFFFu);
+        if (m > 0) {
+            if (in) {
+                const int sm = (int)sizeof(KeysSmem<true>);
+                WSB_CUDA_TRY(cudaFuncSetAttribute(k_keys<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+                k_keys<true><<<nb, kThreads, sm, ctx->stream>>>(a);
+            } else {
+                const int sm = (int)sizeof(KeysSmem<false>);
+                WSB_CUDA_TRY(cudaFuncSetAttribute(k_keys<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+                k_keys<false><<<nb, kThreads, sm, ctx->stream>>>(a);
+            }
+            ctx->launches += 1;
+            WSB_CUDA_TRY(cudaGetLastError());
         }
-        ctx->launches += 1;
-        WSB_CUDA_TRY(cudaGetLastError());
-    }
-    // entry count (and, from the columns, the validation flags) to the host
-    WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host, total, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host + 2, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        // entry count (and, from the columns, the validation flags) to the host
+        WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host, total, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host + kFlagBucketErr, err, sizeof(int), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+        WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        return WSB_OK;
+    };
+    WSB_TRY(run_keys());
     const uint32_t n_entries = m > 0 ? (uint32_t)ctx->flag_host[0] : 0u;
-    const int e = ctx->flag_host[2];
-    if (e & kErrUV) return fail(WSB_EINVAL, "u and v must lie in [0, 1)");
-    if (e & kErrW) return fail(WSB_EINVAL, "w must lie in [0, 1]");
-    if (e & kErrWeight) return fail(WSB_EINVAL, "weights must be finite and >= 0");
-    // partition_time_ordered (visdata.py:354-355), reached by run_pipeline
-    // through _partition_for_ranks (pipeline.py:47-52)
-    if (e & kErrTime) return fail(WSB_EINVAL, "records must be sorted by time_index");
+    if (n_entries > a.cap) {   // more than 2 entries per record on average: exact buffers, again
+        WSB_TRY(ensure(ctx, kSlotKeysA, sizeof(uint32_t) * (size_t)n_entries, (void **)&ka));
+        WSB_TRY(ensure(ctx, kSlotIdxA, sizeof(uint32_t) * (size_t)n_entries, (void **)&ia));
+        WSB_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+        WSB_TRY(run_keys());
+    }
+    ctx->pending_bucket_err = in != nullptr;
+    WSB_TRY(bucket_errors(ctx));
+    uint32_t *kb, *ib;
+    const size_t eb = sizeof(uint32_t) * std::max<size_t>(4, n_entries);
+    WSB_TRY(ensure(ctx, kSlotKeysB, eb, (void **)&kb));
+    WSB_TRY(ensure(ctx, kSlotIdxB, eb, (void **)&ib));
     uint32_t *ks, *is;
     WSB_TRY(radix_sort_pairs(ctx, ka, kb, ia, ib, n_entries, k.item_bits + kRowBits, &ks, &is));
     k_item_offsets<<<ceil_div(n_items + 1, 256), 256, 0, ctx->stream>>>(ks, n_entries, n_items, off);
@@ -445,6 +461,19 @@ int bucket_items(wsb_ctx *ctx, const wsb_grid *g, int S, int v_start, int v_coun
     ctx->last_off = off;
     ctx->last_entries = n_entries;
     ctx->last_tiles = n_items;
+    return WSB_OK;
+}
+
+int bucket_errors(wsb_ctx *ctx) {
+    if (!ctx->pending_bucket_err) return WSB_OK;
+    ctx->pending_bucket_err = false;
+    const int e = ctx->flag_host[kFlagBucketErr];
+    if (e & kErrUV) return fail(WSB_EINVAL, "u and v must lie in [0, 1)");
+    if (e & kErrW) return fail(WSB_EINVAL, "w must lie in [0, 1]");
+    if (e & kErrWeight) return fail(WSB_EINVAL, "weights must be finite and >= 0");
+    // partition_time_ordered (visdata.py:354-355), reached by run_pipeline
+    // through _partition_for_ranks (pipeline.py:47-52)
+    if (e & kErrTime) return fail(WSB_EINVAL, "records must be sorted by time_index");
     return WSB_OK;
 }
 

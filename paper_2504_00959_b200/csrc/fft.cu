@@ -301,7 +301,10 @@ struct RowCfg {
 #endif
     // N = 4096 takes 2 rows (512 threads) so the interleaved last pass can
     // write whole 32-byte sectors of the column-major P layout
-    static constexpr int T = LOGN >= 12 ? (1 << LOGN) / 8
+#ifndef WSB_ROW12_DIV
+#define WSB_ROW12_DIV 8
+#endif
+    static constexpr int T = LOGN >= 12 ? (1 << LOGN) / WSB_ROW12_DIV
                              : ((1 << LOGN) / 16 > WSB_ROW_MIN_T) ? (1 << LOGN) / 16 : WSB_ROW_MIN_T;
     static constexpr int MINB = T <= 128 ? 4 : (T <= 256 ? 2 : 1);
 };

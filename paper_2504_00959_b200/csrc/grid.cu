@@ -741,7 +741,10 @@ int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
     a.item_bits = bk.item_bits;
     a.n_s16 = ceil_div(g->n_u, kC);
     const int64_t ni = bk.n_items;
-    if (ni <= 0) return WSB_OK;
+    if (ni <= 0) {
+        WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        return bucket_errors(ctx);
+    }
     const int S = k->half_support;
     // ---- work parts (split heavy items) ------------------------------------
     // per item: parts, partial-tile slots, split flag -- three count arrays
@@ -759,6 +762,7 @@ int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
         WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host + q, pre + (q + 1) * seg, sizeof(uint32_t),
                                      cudaMemcpyDeviceToHost, ctx->stream));
     WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    WSB_TRY(bucket_errors(ctx));   // (the records' validation flags rode along)
     const uint32_t b1 = (uint32_t)ctx->flag_host[0], b2 = (uint32_t)ctx->flag_host[1],
                    b3 = (uint32_t)ctx->flag_host[2];
     const uint32_t n_parts = b1, n_slots = b2 - b1, n_split = b3 - b2;

@@ -80,6 +80,7 @@ struct wsb_ctx {
     int64_t last_entries = 0, last_tiles = 0;
     uint32_t *last_keys = nullptr, *last_idx = nullptr, *last_off = nullptr;
     int launches = 0;
+    bool pending_bucket_err = false;   // bucket_items' validation flags await a host round trip
     // route_count -> route_pack hand-over: the pack reuses the counts of the
     // immediately preceding count on the same records and slabs
     struct {
@@ -140,6 +141,9 @@ int exclusive_scan_u32(wsb_ctx *ctx, const uint32_t *in, uint32_t *out, int64_t 
 // sort.cu: stable LSD radix sort of (key, val) pairs by the low `bits` of key.
 // Returns the buffers holding the result in *keys_out/*vals_out; the final
 // pass writes the values only (*keys_out then holds a previous pass's keys).
+// Report bucket_items' validation flags (call after a stream synchronisation).
+int bucket_errors(wsb_ctx *ctx);
+
 int radix_sort_pairs(wsb_ctx *ctx, uint32_t *keys, uint32_t *keys_alt, uint32_t *vals,
                      uint32_t *vals_alt, int64_t n, int bits, uint32_t **keys_out,
                      uint32_t **vals_out, bool keep_keys = true);
@@ -167,6 +171,7 @@ constexpr int kItemRows = 128;
 constexpr int kSSCols = WSB_ITEM_COLS;
 static_assert(kSSCols % WSB_STRIP == 0 && kSSCols <= 4 * WSB_STRIP, "item columns");
 constexpr int kPartCap = 2048;     // entries per work part (split heavy items)
+constexpr int kFlagBucketErr = 8;  // flag_host slot of bucket_items' validation flags
 constexpr int kRowBits = 8;        // entry key = item << kRowBits | row offset
 
 // the visibility columns of one channel (fused prepare + bucketing)
