@@ -456,6 +456,9 @@ struct ColCfg {
     static constexpr int T = ((1 << LOGN) / 8 > 256) ? (1 << LOGN) / 8 : 256;
     static constexpr int MINB = T <= 256 ? 2 : 1;
 };
+#ifndef WSB_COLS_ZREG
+#define WSB_COLS_ZREG 1
+#endif
 constexpr int kColE = 8;
 constexpr int kColRL = 3;
 
@@ -637,7 +640,9 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
     };
 
     const double dw = a.n_w > 1 ? (a.w_max - a.w_min) / (double)(a.n_w - 1) : 0.0;
-    // (z in registers instead: 104 B of spills, measured 0.90 vs 0.79 ms)
+    // z per pixel, staged once; with the TMA prefetch holding no registers the
+    // thread's eight z then live in registers for every plane (WSB_COLS_ZREG:
+    // cfg3 6.92 -> 6.47 ms; round 1, with register prefetch, they spilled)
     for (int e = threadIdx.x; e < C * N; e += CT)
         zbuf[e] = cis_pi(2.0 * dw * (n_of(e / N, prow(e % N)) - 1.0));
 
@@ -647,6 +652,18 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
 #pragma unroll
     for (int i = 0; i < kColE; ++i) acc[i] = a.k1 < a.k_top ? run[i * CT] : make_double2(0.0, 0.0);
     if constexpr (SPL == 0) prefetch(nk - 1);
+#if WSB_COLS_ZREG
+    // z of this thread's output pixels, in registers for every plane
+    __syncthreads();
+    double2 zr[kColE];
+#pragma unroll
+    for (int kb = 0; kb < NB; ++kb) {
+        const int b = threadIdx.x + kb * CT;
+        const int seq = b / M, j = b % M;
+#pragma unroll
+        for (int r = 0; r < R; ++r) zr[kb * R + r] = zbuf[seq * N + j + r * M];
+    }
+#endif
 
     for (int kl = nk - 1; kl >= 0; --kl) {
         V v[kColE];
@@ -658,8 +675,13 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
                 "r"(bar_phase)
                 : "memory");
             bar_phase ^= 1;
+#if WSB_COLS_ZREG
+            pass_load<LOGN, P0::RL, kColE, CT>(
+                v, [&](int seq, int j) { return c0 + seq < a.ncols ? pbuf[seq * N + j] : cx<V>(0.0, 0.0); });
+#else
 #pragma unroll
             for (int i = 0; i < kColE; ++i) v[i] = off[i] >= 0 ? pbuf[lidx[i]] : cx<V>(0.0, 0.0);
+#endif
             __syncthreads();   // every thread has its inputs: the buffer takes the next plane
             if (kl > 0) prefetch(kl - 1);
             pass_compute<LOGN, P0::RL, kColE, CT>(1, tw, v);
@@ -690,7 +712,13 @@ __global__ void __launch_bounds__(ColCfg<LOGN>::T, ColCfg<LOGN>::MINB)
             const int seq = b / M, j = b % M;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
+#if WSB_COLS_ZREG
+                const double2 z = zr[kb * R + r];
+                (void)seq;
+                (void)j;
+#else
                 const double2 z = zbuf[seq * N + j + r * M];
+#endif
                 const double2 p = to_d2(v[kb * R + r]);
                 double2 &q = acc[kb * R + r];
                 const double qx = fma(q.x, z.x, fma(-q.y, z.y, p.x));
