@@ -25,10 +25,11 @@
 // price is K1 entries for each 16-column strip a record reaches (1.36 per
 // record at cfg2 instead of 1.12 per 64-column block).
 //
-// Records stream through the warp in chunks of 16 gathered by cp.async one
-// chunk ahead (record index prefetched a chunk before its gather). Two lanes
-// stage a record: one forms value x u weight per window column, the other
-// the v weights at the record's row offset in its 8-row step.
+// Records stream through the warp in chunks of 32 gathered by cp.async one
+// chunk ahead (record index prefetched a chunk before its gather). One lane
+// stages a record: value x u weight per window column and the v weights of
+// its footprint rows (the sweep offsets them by the record's first row in
+// its 8-row step) -- no divergent per-axis tails (K2 1.06 -> 0.95 ms at cfg2).
 #include <type_traits>
 
 #include "i0_coeffs.h"
@@ -172,9 +173,17 @@ constexpr int kC = WSB_STRIP;          // columns per warp strip
 constexpr int kSS = kSSCols;           // item width (WSB_ITEM_COLS)
 constexpr int kWarps = kSS / kC;       // strips (warps) per item
 constexpr int kThreads = 32 * kWarps;
-constexpr int kRPR = kThreads / 2;     // records per gather / staging round (a thread pair each)
+// WSB_STAGE_ONE: one lane stages a whole record (both axes; the v weights
+// stored compactly, 8-row offset applied when the sweep reads them) instead
+// of a lane pair splitting the axes (the warp then runs both axes' tails)
+#ifndef WSB_STAGE_ONE
+#define WSB_STAGE_ONE 1
+#endif
+constexpr bool kOne = WSB_STAGE_ONE && kWarps == 1;
+constexpr int kLPR = kOne ? 1 : 2;       // lanes per record (gather and staging)
+constexpr int kRPR = kThreads / kLPR;    // records per gather / staging round
 #ifndef WSB_CHUNK
-#define WSB_CHUNK 16
+#define WSB_CHUNK 32
 #endif
 constexpr int kChunk = WSB_CHUNK;      // records staged per round (<= 255: byte indices)
 constexpr int kCM = kChunk / kRPR;     // gather / staging rounds per chunk
@@ -219,9 +228,10 @@ struct Win {
 template <int S>
 struct StagedRec {
     static constexpr int W = 2 * S + 1;
-    static constexpr int NV = 8 * Win<S>::NTR;
+    static constexpr int NV = kOne ? (W + 1) & ~1 : 8 * Win<S>::NTR;
     double2 tu[W + 1];     // value * u weight per window column; slot W = 0 (signs folded)
     double wv[NV];         // v weight of row b = d .. d+W-1 of the record's step; 0 elsewhere
+                           // (kOne: of footprint row k = 0 .. W-1, signs folded)
     int4 meta;             // (first window column - superstrip col0, window step, row offset d, strip mask)
 };
 
@@ -365,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         Ids ids;
 #pragma unroll
         for (int q = 0; q < kCM; ++q) {
-            const uint32_t r = ch * kChunk + q * kRPR + (tid >> 1);
+            const uint32_t r = ch * kChunk + q * kRPR + tid / kLPR;
             ids.v[q] = (ch < nchunks && r < n) ? __ldg(&a.idx[eb + r]) : 0u;
         }
         return ids;
@@ -374,14 +384,17 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         if (ch < nchunks) {
 #pragma unroll
             for (int q = 0; q < kCM; ++q) {
-                const uint32_t r = ch * kChunk + q * kRPR + (tid >> 1);
+                const uint32_t r = ch * kChunk + q * kRPR + tid / kLPR;
                 if (r < n) {
                     const uint32_t id = ids.v[q];
                     WSB_DCHECK(id < a.n_rec, "item %lld id %u", (long long)item, id);
-                    const double2 *src = reinterpret_cast<const double2 *>(a.rec + id) + (tid & 1);
-                    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(
-                        reinterpret_cast<double2 *>(&sm.raw[ch % kRaw][q * kRPR + (tid >> 1)]) + (tid & 1));
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+#pragma unroll
+                    for (int h = (kLPR == 2 ? (tid & 1) : 0); h < 2; h += kLPR) {
+                        const double2 *src = reinterpret_cast<const double2 *>(a.rec + id) + h;
+                        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(
+                            reinterpret_cast<double2 *>(&sm.raw[ch % kRaw][q * kRPR + tid / kLPR]) + h);
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+                    }
                 }
             }
         }
@@ -405,6 +418,43 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
         // ---- stage: thread pair per record, thread (2r + ax) does axis ax of
         // record r. Both axes run the same weight code (one instruction stream
         // for the warp); only the short tails differ.
+        if constexpr (kOne) {
+#pragma unroll 1
+            for (int q = 0; q < kCM; ++q) {
+                const int r = q * kRPR + tid;
+                if (r < nr) {
+                    const double4 rc = sm.raw[ch % kRaw][r];
+                    Rec &st = sm.rec[r];
+                    double wgt[W];
+                    // u axis: value * weight per window column, column sign folded
+                    // (transform.py:180-185; a sign flip commutes with rounding)
+                    const int i0 = (int)floor(rc.x) - S;
+                    const uint32_t wmu = axis_weights<KIND, S>(rc.x, i0, kp, i0b, wgt);
+                    const double cs = (i0 & 1) ? -1.0 : 1.0;
+#pragma unroll
+                    for (int k = 0; k < W; ++k) {
+                        const double wk = (k & 1) ? -cs * wgt[k] : cs * wgt[k];
+                        st.tu[k] = make_double2(__dmul_rn(rc.z, wk), __dmul_rn(rc.w, wk));
+                    }
+                    st.tu[W] = make_double2(0.0, 0.0);
+                    const int k_lo = max(col0 - i0, 0), k_hi = min(min(col0 + kSS, a.n_u) - i0, W) - 1;
+                    const uint32_t uin = k_hi >= k_lo ? wmu & (((2u << k_hi) - 1u) & ~((1u << k_lo) - 1u)) : 0u;
+                    // v axis: weight of footprint row k, row sign (-1)^row folded
+                    const int j0 = (int)floor(rc.y) - S;
+                    const uint32_t wmv = axis_weights<KIND, S>(rc.y, j0, kp, i0b, wgt);
+                    const int rel = j0 - Bfirst;
+                    WSB_DCHECK(rel >= 0 && rel < Sm::NROW, "item %lld rel %d", (long long)item, rel);
+                    const double sj = (rel & 1) ? -rs : rs;
+#pragma unroll
+                    for (int k = 0; k < W; ++k) st.wv[k] = (k & 1) ? -sj * wgt[k] : sj * wgt[k];
+                    st.meta = make_int4(i0 - col0, rel >> 3, rel & 7, uin ? 1 : 0);
+                    // cell updates inside this item (grid_sector's count): u taps x v taps
+                    const int r_lo = max(R0 - j0, 0), r_hi = min(R1 - j0, W) - 1;
+                    cnt_upd += __popc(uin) *
+                               __popc(r_hi >= r_lo ? wmv & (((2u << r_hi) - 1u) & ~((1u << r_lo) - 1u)) : 0u);
+                }
+            }
+        } else
 #pragma unroll 1
         for (int q = 0; q < kCM; ++q) {
             const int r = q * kRPR + (tid >> 1), ax = tid & 1;
@@ -493,6 +543,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
             int pos = k4;                          // this lane's record position in the list
             bool pend;                             // its record still to apply
             int srec, span;                        // its window step; tiles it reaches from there
+            int dl;                                // its first footprint row in the step (0..7)
             double2 b0, b1;                        // B: value x u weight at the lane's columns
             const double *wvp;                     // A: v weights of its rows
             auto load = [&]() {
@@ -505,7 +556,8 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                 const int i1 = (unsigned)(c0 + 8) < (unsigned)W ? c0 + 8 : W;
                 b0 = *reinterpret_cast<const double2 *>(rp + 16 * i0);
                 b1 = *reinterpret_cast<const double2 *>(rp + 16 * i1);
-                wvp = reinterpret_cast<const double *>(rp + offsetof(Rec, wv)) + g4;
+                wvp = reinterpret_cast<const double *>(rp + offsetof(Rec, wv)) + (kOne ? 0 : g4);
+                dl = m.z;
                 srec = m.y;
                 span = (m.z + W + 7) >> 3;
             };
@@ -526,7 +578,13 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                         if (t < ntile) {   // (uniform) tiles the pass reaches
                             // A: v weight of the records on tile row g4 (window row 8t + g4)
                             const int tt = t - delta;
-                            const double av = (act && (unsigned)tt < (unsigned)NTR) ? wvp[8 * tt] : 0.0;
+                            double av;
+                            if constexpr (kOne) {   // footprint row of tile row g4
+                                const int kr = 8 * tt + g4 - dl;
+                                av = (act && (unsigned)kr < (unsigned)W) ? wvp[kr] : 0.0;
+                            } else {
+                                av = (act && (unsigned)tt < (unsigned)NTR) ? wvp[8 * tt] : 0.0;
+                            }
                             const int tr = (p + t) % NT;          // ring tile holding window tile t (folds)
                             dmma(acc[tr][0][0], av, b0.x);
                             dmma(acc[tr][0][1], av, b0.y);
