@@ -149,7 +149,10 @@ __global__ void __launch_bounds__(kRsThreads) k_radix_hist(const uint32_t *__res
 // values and the key histogram only), so each item's global position is
 // staged in place of its key and only the values are written
 template <int B, bool LAST>
-__global__ void __launch_bounds__(kRsThreads, 16 / kRsIpt * 2) k_radix_scatter(
+#ifndef WSB_RS_MINB
+#define WSB_RS_MINB (16 / kRsIpt * 2)
+#endif
+__global__ void __launch_bounds__(kRsThreads, WSB_RS_MINB) k_radix_scatter(
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
     uint32_t *__restrict__ vout, int64_t n, int shift, uint32_t dmask,
     const uint32_t *__restrict__ offs, int nb) {
