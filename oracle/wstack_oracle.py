@@ -276,7 +276,7 @@ def item_entries(gu, gv, plane, n_u: int, n_w: int, S: int, v_start: int, v_coun
                  ss_cols: int = 16, item_rows: int = 128, row_bits: int = 8):
     """The GPU gridder's work-item bucketing restated (contract of
     wsb_bucket_items, include/wsb.h): every (record, item) pair whose taps
-    reach item = (plane, ss_cols-column superstrip, item_rows-row block of
+    reach item = (plane, ss_cols-column block, item_rows-row block of
     the slab), key = item << row_bits | rowrel with rowrel = floor(gv) - S -
     (block row0 - 2S), stably sorted by key (record order for equal keys).
     Tap sets are the reference's (gridder.py:164-177). Returns

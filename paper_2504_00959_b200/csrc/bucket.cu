@@ -3,7 +3,7 @@
 // The reference gives every slab the records of exchange_to_space_order in
 // (time_index, gindex) order (comms.py:534-545) and grids them tap-major
 // (gridder.py:160-183). The GPU gridder (grid.cu) sweeps work items
-// item = (w plane, 64-column superstrip, 128-row block of the slab), so
+// item = (w plane, 16-column strip (WSB_ITEM_COLS), 128-row block of the slab), so
 // every (record, item) pair the record's taps reach becomes one entry
 //     key = item << 8 | rowrel,   rowrel = anchor row - (R0 - 2S) < 128 + 2S
 // (anchor row = floor(gv) - S, R0 = the block's first row), written in
@@ -44,7 +44,7 @@ __device__ __forceinline__ bool tap_range(double g, int S, int lo, int hi, int *
     return *a <= *b;
 }
 
-// Entries of one record (at most 4: two superstrips x two row blocks).
+// Entries of one record (at most 4: two column blocks x two row blocks).
 __device__ __forceinline__ int record_entries(double gu, double gv, uint32_t plane,
                                               const KeyGeom &k, uint32_t *keys) {
     // invalid coordinates (flagged by the validation) reach no item
@@ -56,11 +56,11 @@ __device__ __forceinline__ int record_entries(double gu, double gv, uint32_t pla
     const int anchor = (int)floor(gv) - k.S;
     const int ss0 = i0 / kSSCols, ss1 = i1 / kSSCols;
     const int rb0 = (j0 - k.v_start) / kItemRows, rb1 = (j1 - k.v_start) / kItemRows;
-    // entries in (row block, superstrip) order; a record spans at most two of each
+    // entries in (row block, column block) order; a record spans at most two of each
     const uint32_t rr0 = (uint32_t)(anchor - (k.v_start + rb0 * kItemRows - 2 * k.S));
     const uint32_t it0 = ((uint32_t)plane * k.n_ss + ss0) * (uint32_t)k.n_rb + rb0;
     const uint32_t key00 = it0 << kRowBits | rr0;
-    const uint32_t dss = (uint32_t)k.n_rb << kRowBits;                // next superstrip
+    const uint32_t dss = (uint32_t)k.n_rb << kRowBits;                // next column block
     const uint32_t drb = (1u << kRowBits) - (uint32_t)kItemRows;      // next row block
     const bool two_ss = ss1 > ss0, two_rb = rb1 > rb0;
     keys[0] = key00;

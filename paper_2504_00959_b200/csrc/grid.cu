@@ -232,7 +232,7 @@ struct StagedRec {
     double2 tu[W + 1];     // value * u weight per window column; slot W = 0 (signs folded)
     double wv[NV];         // v weight of row b = d .. d+W-1 of the record's step; 0 elsewhere
                            // (kOne: of footprint row k = 0 .. W-1, signs folded)
-    int4 meta;             // (first window column - superstrip col0, window step, row offset d, strip mask)
+    int4 meta;             // (first window column - item col0, window step, row offset d, strip mask)
 };
 
 template <int KIND, int S>
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                                              (uint32_t)max(row_end - R0, 0));
 
     // ---- the sweep --------------------------------------------------------
-    // Warp w owns columns [16w, 16w+16) of the superstrip. Its window holds
+    // Warp w owns columns [16w, 16w+16) of the item. Its window holds
     // rows B .. B + 8 NT - 1 (B = Bfirst + 8 step) as a ring of NT tiles of 8
     // rows: tile (phase + t) % NT holds rows B + 8t .. B + 8t + 7, as four 8x8
     // FP64 MMA accumulators (two 8-column halves x Re/Im; lane holds row
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                         st.tu[k] = make_double2(__dmul_rn(rc.z, wk), __dmul_rn(rc.w, wk));
                     }
                     st.tu[W] = make_double2(0.0, 0.0);
-                    // tap columns inside the superstrip (and the mesh); the strips they touch
+                    // tap columns inside the item (and the mesh); the strips they touch
                     const int k_lo = max(col0 - i0, 0), k_hi = min(min(col0 + kSS, a.n_u) - i0, W) - 1;
                     const uint32_t uin = k_hi >= k_lo ? wm & (((2u << k_hi) - 1u) & ~((1u << k_lo) - 1u)) : 0u;
                     int mask = 0;
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
                 __syncwarp();
             }
             constexpr int NTR = Win<S>::NTR;
-            const int wc8 = warp * kC + g4;        // this lane's B column (half 0) in the superstrip
+            const int wc8 = warp * kC + g4;        // this lane's B column (half 0) in the item
             int pos = k4;                          // this lane's record position in the list
             bool pend;                             // its record still to apply
             int srec, span;                        // its window step; tiles it reaches from there
