@@ -205,7 +205,8 @@ struct SweepArgs {
     const double *i0beta;      // device scalar, np.i0(beta) (Kaiser-Bessel)
     int out_f32;               // 1: complex64 grid (FP32 path; accumulation stays FP64)
     int n_u, v_start, v_count, n_ss, n_rb, item_bits, n_s16;
-    int64_t n_parts;
+    int64_t n_parts;           // launched CTAs (the count or an upper bound of it)
+    const uint32_t *n_parts_dev, *n_split_dev;   // the actual counts (device)
     int64_t n_rec, out_elems;  // bounds (debug checks)
 };
 
@@ -266,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, sweep_min_blocks<KIND, S>())
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Sm &sm = *reinterpret_cast<Sm *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (blockIdx.x >= *a.n_parts_dev) return;   // (grids sized by an upper bound)
     const uint4 pd = a.parts[blockIdx.x];
     const int64_t item = pd.x;
     const int rb = (int)(item % a.n_rb);
@@ -712,12 +714,17 @@ __global__ void k_item_parts(const uint32_t *off, int64_t n_items, uint32_t *npa
     split[item] = np > 1 ? 1 : 0;
 }
 
+__global__ void k_split_count(const uint32_t *pre, int64_t seg, uint32_t *n_split) {
+    if (threadIdx.x == 0) *n_split = pre[3 * seg] - pre[2 * seg];
+}
+
 // slot_off / split_off: segments of one concatenated scan, minus their bases
 __global__ void k_build_parts(const uint32_t *off, int64_t n_items, const uint32_t *part_off,
-                              const uint32_t *slot_off, uint32_t slot_base, const uint32_t *split_off,
-                              uint32_t split_base, uint4 *parts, uint2 *split_items) {
+                              const uint32_t *slot_off, const uint32_t *slot_base_p, const uint32_t *split_off,
+                              const uint32_t *split_base_p, uint4 *parts, uint2 *split_items) {
     const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (item >= n_items) return;
+    const uint32_t slot_base = *slot_base_p, split_base = *split_base_p;
     const uint32_t b = off[item], e = off[item + 1];
     const uint32_t np = part_off[item + 1] - part_off[item];
     if (np == 1) {
@@ -736,9 +743,7 @@ __global__ void k_build_parts(const uint32_t *off, int64_t n_items, const uint32
 // one thread per (row, column) of a split item: its parts' partial tiles
 // (signed, [row][re | im][kSS]) summed in part order, written to the strip
 // layout
-__global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split_items,
-                                                  const uint32_t *part_off) {
-    const uint2 si = split_items[blockIdx.x];
+__device__ __forceinline__ void combine_item(const SweepArgs &a, uint2 si, const uint32_t *part_off) {
     const int64_t item = si.x;
     const int np = (int)(part_off[item + 1] - part_off[item]);
     const int rb = (int)(item % a.n_rb);
@@ -776,6 +781,14 @@ __global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(128) k_combine(SweepArgs a, const uint2 *split_items,
+                                                  const uint32_t *part_off) {
+    // (the grid is sized by a bound: blocks stride over the device count)
+    const uint32_t n_split = *a.n_split_dev;
+    for (uint32_t sidx = blockIdx.x; sidx < n_split; sidx += gridDim.x)
+        combine_item(a, split_items[sidx], part_off);
 }
 
 }  // namespace
@@ -816,15 +829,30 @@ int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     WSB_TRY(exclusive_scan_u32(ctx, cnt, pre, len, nullptr));
-    for (int q = 0; q < 3; ++q)
-        WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host + q, pre + (q + 1) * seg, sizeof(uint32_t),
-                                     cudaMemcpyDeviceToHost, ctx->stream));
-    WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    WSB_TRY(bucket_errors(ctx));   // (the records' validation flags rode along)
-    const uint32_t b1 = (uint32_t)ctx->flag_host[0], b2 = (uint32_t)ctx->flag_host[1],
-                   b3 = (uint32_t)ctx->flag_host[2];
-    const uint32_t n_parts = b1, n_slots = b2 - b1, n_split = b3 - b2;
+    // The launch sizes need the part / slot / split counts. Without a host
+    // round trip they are bounded from the entry count: parts <= items +
+    // entries / cap, slots <= 2 entries / cap, split items <= entries / (cap+1);
+    // CTAs beyond the device counts exit at once. Above 1 GiB of bounded
+    // partial tiles the exact counts are read back instead.
+    const uint64_t ne = (uint64_t)bk.n_entries;
+    uint64_t n_parts = (uint64_t)ni + ne / kPartCap + 1, n_slots = 2 * (ne / kPartCap) + 2,
+             n_split = ne / (kPartCap + 1) + 1;
+    if (sizeof(double2) * n_slots * kItemRows * kSS > ((size_t)1 << 30)) {
+        for (int q = 0; q < 3; ++q)
+            WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host + q, pre + (q + 1) * seg, sizeof(uint32_t),
+                                         cudaMemcpyDeviceToHost, ctx->stream));
+        WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        WSB_TRY(bucket_errors(ctx));
+        const uint32_t b1 = (uint32_t)ctx->flag_host[0], b2 = (uint32_t)ctx->flag_host[1],
+                       b3 = (uint32_t)ctx->flag_host[2];
+        n_parts = b1;
+        n_slots = b2 - b1;
+        n_split = b3 - b2;
+    }
     const uint32_t *np_off = pre;
+    // device counts: parts = pre[seg]; splits = pre[3 seg] - pre[2 seg] (one word)
+    uint32_t *n_split_dev;
+    WSB_TRY(ensure(ctx, kSlotFlag, 64, (void **)&n_split_dev));
     uint4 *parts;
     uint2 *split_items, *part_rows;
     double2 *partial = nullptr;
@@ -835,10 +863,15 @@ int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
     if (n_slots)
         WSB_TRY(ensure(ctx, kSlotPartial, sizeof(double2) * (size_t)n_slots * kItemRows * kSS,
                        (void **)&partial));
-    k_build_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(bk.off, ni, np_off, pre + seg, b1,
-                                                              pre + 2 * seg, b2, parts, split_items);
+    k_build_parts<<<ceil_div(ni, 256), 256, 0, ctx->stream>>>(bk.off, ni, np_off, pre + seg, pre + seg,
+                                                              pre + 2 * seg, pre + 2 * seg, parts, split_items);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
+    k_split_count<<<1, 32, 0, ctx->stream>>>(pre, seg, n_split_dev + 12);
+    ctx->launches += 1;
+    WSB_CUDA_TRY(cudaGetLastError());
+    a.n_parts_dev = pre + seg;
+    a.n_split_dev = n_split_dev + 12;
     a.parts = parts;
     a.part_rows = part_rows;
     a.partial = partial;
@@ -858,7 +891,8 @@ int grid_items(wsb_ctx *ctx, const wsb_grid *g, const wsb_kernel *k, int v_start
         rc = launch_kind<WSB_KERNEL_KAISER_BESSEL>(ctx, S, a, k->shape_param);
     }
     if (rc != WSB_OK || n_split == 0) return rc;
-    k_combine<<<dim3(n_split, kItemRows / 2 / 8), 128, 0, ctx->stream>>>(a, split_items, np_off);
+    k_combine<<<dim3((unsigned)std::min<uint64_t>(n_split, 1184), kItemRows / 2 / 8), 128, 0, ctx->stream>>>(
+        a, split_items, np_off);
     ctx->launches += 1;
     WSB_CUDA_TRY(cudaGetLastError());
     return WSB_OK;
