@@ -90,6 +90,77 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_final(const uint32_t *__r
     }
 }
 
+// Single-pass exclusive scan: tiles taken in launch order (atomic ticket);
+// each publishes its total, warp 0 then looks back over the 32 preceding
+// tiles at a time until one with an inclusive prefix, and publishes its own.
+// Status word: (epoch << 2 | flag) << 32 | value; words of earlier scans
+// (older epochs) read as unpublished, so the array is never cleared.
+constexpr uint32_t kScAgg = 1u, kScInc = 2u;
+constexpr int kScanOnePassMaxTiles = 1024;   // (cfg2's scans: <= 210 tiles; cfg3's radix scans: 3900)
+
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_onepass(const uint32_t *__restrict__ in,
+                                                               uint32_t *out, int64_t n, int nb,
+                                                               uint64_t *status, uint32_t *ticket,
+                                                               uint32_t epoch, uint32_t *total) {
+    __shared__ uint32_t s_tile, s_excl, s_tot;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t base = (int64_t)tile * kScanTile + threadIdx.x * kScanItems;
+    uint32_t v[kScanItems], sum = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        v[i] = base + i < n ? in[base + i] : 0u;
+        sum += v[i];
+    }
+    uint32_t ex = block_excl_scan(sum, &s_tot);
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const uint32_t tot = s_tot;
+        const uint64_t hi = (uint64_t)epoch << 34;
+        if (lane == 0) st_relaxed(&status[tile], hi | (uint64_t)(tile == 0 ? kScInc : kScAgg) << 32 | tot);
+        uint32_t excl = 0;
+        if (tile > 0) {
+            for (int64_t j = (int64_t)tile - 1 - lane;; j -= 32) {
+                uint64_t st = hi | (uint64_t)kScInc << 32;    // before tile 0: an inclusive 0
+                if (j >= 0) {
+                    do {
+                        st = ld_relaxed(&status[j]);
+                    } while ((uint32_t)(st >> 34) != epoch);
+                }
+                const uint32_t inc = __ballot_sync(0xffffffffu, ((uint32_t)(st >> 32) & 3u) == kScInc);
+                const int first = inc ? __ffs(inc) - 1 : 32;   // nearest tile with an inclusive prefix
+                uint32_t val = lane <= first ? (uint32_t)st : 0u;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                excl += val;
+                if (inc) break;
+            }
+            if (lane == 0) st_relaxed(&status[tile], hi | (uint64_t)kScInc << 32 | (excl + tot));
+        }
+        if (lane == 0) {
+            s_excl = excl;
+            if (total && tile == (uint32_t)nb - 1) *total = excl + tot;
+        }
+    }
+    __syncthreads();
+    ex += s_excl;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        if (base + i < n) out[base + i] = ex;
+        ex += v[i];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // radix sort: B-bit digits (B = 8..9, chosen so the key needs as few passes
 // as possible: cfg3's 26-bit keys take 3 passes of 9 bits instead of 4 of 8;
@@ -293,14 +364,37 @@ int exclusive_scan_u32(wsb_ctx *ctx, const uint32_t *in, uint32_t *out, int64_t 
     }
     const int nb = ceil_div(n, kScanTile);
     uint32_t *sums;
-    WSB_TRY(ensure(ctx, kSlotScanTmp, sizeof(uint32_t) * (nb + 1), (void **)&sums));
-    k_scan_reduce<<<nb, kScanThreads, 0, ctx->stream>>>(in, n, sums);
-    k_scan_sums<<<1, kScanThreads, 0, ctx->stream>>>(sums, nb, sums + nb);
-    k_scan_final<<<nb, kScanThreads, 0, ctx->stream>>>(in, out, n, sums);
-    ctx->launches += 3;
-    WSB_CUDA_TRY(cudaGetLastError());
+    if (nb > kScanOnePassMaxTiles) {
+        // many tiles: reduce / scan of the tile sums / final (the single pass's
+        // look-back chains grow with the resident tiles)
+        WSB_TRY(ensure(ctx, kSlotScanTmp2, sizeof(uint32_t) * (nb + 1), (void **)&sums));
+        k_scan_reduce<<<nb, kScanThreads, 0, ctx->stream>>>(in, n, sums);
+        k_scan_sums<<<1, kScanThreads, 0, ctx->stream>>>(sums, nb, sums + nb);
+        k_scan_final<<<nb, kScanThreads, 0, ctx->stream>>>(in, out, n, sums);
+        ctx->launches += 3;
+        WSB_CUDA_TRY(cudaGetLastError());
+        sums += nb;
+    } else {
+        // [nb] status words, then the ticket and the total
+        const size_t bytes = sizeof(uint64_t) * ((size_t)nb + 2);
+        unsigned char *work;
+        const void *before = (int)ctx->bufs.size() > kSlotScanTmp ? ctx->bufs[kSlotScanTmp].ptr : nullptr;
+        WSB_TRY(ensure(ctx, kSlotScanTmp, bytes, (void **)&work));
+        uint64_t *status = reinterpret_cast<uint64_t *>(work);
+        uint32_t *ticket = reinterpret_cast<uint32_t *>(status + nb);
+        sums = ticket + 1;   // the total
+        uint32_t epoch = ++ctx->scan_epoch;
+        if (work != before || epoch >= (1u << 29)) {   // fresh memory (or epochs used up)
+            WSB_CUDA_TRY(cudaMemsetAsync(work, 0, bytes, ctx->stream));
+            epoch = ctx->scan_epoch = 1;
+        }
+        WSB_CUDA_TRY(cudaMemsetAsync(ticket, 0, sizeof(uint32_t), ctx->stream));
+        k_scan_onepass<<<nb, kScanThreads, 0, ctx->stream>>>(in, out, n, nb, status, ticket, epoch, sums);
+        ctx->launches += 1;
+        WSB_CUDA_TRY(cudaGetLastError());
+    }
     if (total_host) {
-        WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host, sums + nb, sizeof(uint32_t),
+        WSB_CUDA_TRY(cudaMemcpyAsync(ctx->flag_host, sums, sizeof(uint32_t),
                                      cudaMemcpyDeviceToHost, ctx->stream));
         WSB_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         *total_host = (uint32_t)ctx->flag_host[0];

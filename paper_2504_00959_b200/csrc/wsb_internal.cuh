@@ -80,7 +80,8 @@ struct wsb_ctx {
     int64_t last_entries = 0, last_tiles = 0;
     uint32_t *last_keys = nullptr, *last_idx = nullptr, *last_off = nullptr;
     int launches = 0;
-    bool pending_bucket_err = false;   // bucket_items' validation flags await a host round trip
+    bool pending_bucket_err = false;
+    uint32_t scan_epoch = 0;          // single-pass scan: status words of earlier scans are stale   // bucket_items' validation flags await a host round trip
     // route_count -> route_pack hand-over: the pack reuses the counts of the
     // immediately preceding count on the same records and slabs
     struct {
@@ -104,6 +105,7 @@ enum Slot {
     kSlotBlockCounts,
     kSlotBlockOffsets,
     kSlotScanTmp,
+    kSlotScanTmp2,
     kSlotKeysA,
     kSlotKeysB,
     kSlotIdxA,
