@@ -21,6 +21,8 @@
 //                 of the reference is never materialised.
 #include <cuda_pipeline_primitives.h>
 
+#include <cstdlib>
+
 #include "wsb_internal.cuh"
 
 
@@ -368,10 +370,10 @@ __device__ __forceinline__ V dif_split_ld(LD ld, int e, int n, const V *__restri
 // its outputs straight back: shared memory only carries the inner exchanges.
 // SPL > 0: rows of N = 2^(LOGN+SPL) points, residue e = blockIdx.z (above).
 template <int LOGN, int SPL, class V>
-__global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
-    k_fft_rows(const V *__restrict__ in, int n_strips, int n_groups, int v_count,
-               int plane_lo, const V *__restrict__ tw, const V *__restrict__ twN,
-               RowDest dst) {
+__device__ __forceinline__ void rows_body(const V *__restrict__ in, int n_strips, int v_count,
+                                          const V *__restrict__ tw, const V *__restrict__ twN,
+                                          const RowDest &dst, const int j0, const int64_t plane,
+                                          const int e) {
     constexpr int N = 1 << LOGN;          // on-chip transform length M
     constexpr int SP = 1 << SPL;
     constexpr int RT = RowCfg<LOGN>::T;
@@ -380,9 +382,6 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
     using P0 = Plan<LOGN, kRowRL, 0>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     V *s = reinterpret_cast<V *>(smem_raw);
-    const int j0 = blockIdx.x * NSEQ;
-    const int64_t plane = plane_lo + blockIdx.y;
-    const int e = SPL ? (int)blockIdx.z : 0;
     // in: strip layout [plane][col/WSB_STRIP][row][re | im][col%WSB_STRIP]
     // (a strip row holds its WSB_STRIP real parts, then the imaginary parts)
     constexpr int SW = WSB_STRIP;
@@ -444,6 +443,42 @@ __global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
         constexpr int RLL = kRowRL;  // the last pass is always a full-radix pass here
         pass_store<LOGN, RLL, kRowE, RT, ILL>(N >> RLL, v, gst);
     }
+}
+
+// persist_nbx > 0 (rows of <= 4096 points): CTAs stride over the linear
+// (plane, row pair) index (persist_nbx row pairs per plane); l2pf: each
+// also prefetches its next pair into L2 (TMA bulk prefetch, one per strip)
+// while the current one is transformed (measured slower: off by default)
+template <int LOGN, int SPL, class V>
+__global__ void __launch_bounds__(RowCfg<LOGN>::T, RowCfg<LOGN>::MINB)
+    k_fft_rows(const V *__restrict__ in, int n_strips, int n_groups, int v_count,
+               int plane_lo, const V *__restrict__ tw, const V *__restrict__ twN,
+               RowDest dst, int persist_nbx, int64_t n_pairs, int l2pf) {
+    constexpr int N = 1 << LOGN;
+    constexpr int NSEQ = RowCfg<LOGN>::T * kRowE / N;
+    if (SPL == 0 && persist_nbx > 0) {
+        using Sc = decltype(V{}.x);
+        constexpr int SW = WSB_STRIP;
+        const Sc *ins = reinterpret_cast<const Sc *>(in);
+        for (int64_t L = blockIdx.x; L < n_pairs; L += gridDim.x) {
+            const int64_t Ln = L + gridDim.x;
+            if (l2pf && Ln < n_pairs) {
+                const int jn = (int)(Ln % persist_nbx) * NSEQ;
+                const int64_t pn = plane_lo + Ln / persist_nbx;
+                const uint32_t bytes = (uint32_t)(min(NSEQ, v_count - jn) * 2 * SW * sizeof(Sc));
+                for (int st = threadIdx.x; st < n_strips; st += blockDim.x) {
+                    const Sc *q = ins + ((pn * n_strips + st) * v_count + jn) * (2 * SW);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(q), "r"(bytes) : "memory");
+                }
+            }
+            rows_body<LOGN, SPL, V>(in, n_strips, v_count, tw, twN, dst, (int)(L % persist_nbx) * NSEQ,
+                                    plane_lo + L / persist_nbx, 0);
+            __syncthreads();   // shared memory is reused by the next pair
+        }
+        return;
+    }
+    rows_body<LOGN, SPL, V>(in, n_strips, v_count, tw, twN, dst, blockIdx.x * NSEQ, plane_lo + blockIdx.y,
+                            SPL ? (int)blockIdx.z : 0);
 }
 
 
@@ -886,19 +921,41 @@ int launch_rows(wsb_ctx *ctx, const V *in, int n_strips, int n_groups, int v_cou
     if (spl == 0) {
         WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 0, V>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_fft_rows<LOGN, 0, V><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo,
-                                                               tw, twN, dst);
+        // persistent CTAs: 16 x the resident count (measured: rows 1.08 ->
+        // 0.99 ms at cfg2, 10.8 -> 9.5 ms at cfg3; 1-4 x is slower, and so is
+        // an L2 prefetch of the next pair); WSB_ROW_PERSIST=0 launches one
+        // CTA per row pair
+        static int persist = -1, l2pf = 0;
+        if (persist < 0) {
+            const char *e = std::getenv("WSB_ROW_PERSIST");
+            persist = e ? std::atoi(e) : 16;
+            const char *f = std::getenv("WSB_ROW_L2PF");
+            l2pf = f ? std::atoi(f) : 0;
+        }
+        if (persist > 0) {
+            int per_sm = 0, dev = 0, n_sm = 0;
+            WSB_CUDA_TRY(cudaGetDevice(&dev));
+            WSB_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+            WSB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fft_rows<LOGN, 0, V>, RT, smem));
+            const int64_t n_pairs = (int64_t)grd.x * grd.y;
+            const int ctas = (int)std::min<int64_t>(n_pairs, (int64_t)per_sm * n_sm * persist);
+            k_fft_rows<LOGN, 0, V><<<ctas, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo, tw,
+                                                                     twN, dst, (int)grd.x, n_pairs, l2pf);
+        } else {
+            k_fft_rows<LOGN, 0, V><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count, plo,
+                                                                   tw, twN, dst, 0, 0, 0);
+        }
     } else if constexpr (LOGN == 12) {
         if (spl == 1) {
             WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 1, V>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             k_fft_rows<LOGN, 1, V><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count,
-                                                                   plo, tw, twN, dst);
+                                                                   plo, tw, twN, dst, 0, 0, 0);
         } else if (spl == 2) {
             WSB_CUDA_TRY(cudaFuncSetAttribute(k_fft_rows<LOGN, 2, V>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             k_fft_rows<LOGN, 2, V><<<grd, RT, smem, ctx->stream>>>(in, n_strips, n_groups, v_count,
-                                                                   plo, tw, twN, dst);
+                                                                   plo, tw, twN, dst, 0, 0, 0);
         } else {
             return fail(WSB_EUNSUPPORTED, "row length above 16384");
         }
