@@ -33,6 +33,9 @@ OPS_COLUMNS = ("records", "grid_updates", "exchange_bytes", "reduce_bytes", "fft
 # specs (mesh.py:59-112, gridder.py:47-72)
 # ---------------------------------------------------------------------------
 
+_C_STRUCTS: dict = {}   # GridSpec / KernelSpec -> their ctypes struct (the C side only reads it)
+
+
 def _is_pow2(n: int) -> bool:
     return n >= 1 and (n & (n - 1)) == 0
 
@@ -72,8 +75,11 @@ class GridSpec:
         return self.w_min_native + (k / (self.n_w - 1)) * (self.w_max_native - self.w_min_native)
 
     def c_struct(self) -> L.WsbGrid:
-        return L.grid_struct(self.n_u, self.n_v, self.n_w, self.cell_size_lm,
-                             self.w_min_native, self.w_max_native)
+        c = _C_STRUCTS.get(self)
+        if c is None:   # (one ctypes struct per distinct spec)
+            c = _C_STRUCTS[self] = L.grid_struct(self.n_u, self.n_v, self.n_w, self.cell_size_lm,
+                                                 self.w_min_native, self.w_max_native)
+        return c
 
 
 @dataclass(frozen=True)
@@ -101,7 +107,11 @@ class KernelSpec:
         return cls(kind="kaiser_bessel", half_support=half_support, shape_param=beta)
 
     def c_struct(self) -> L.WsbKernel:
-        return L.kernel_struct(KERNEL_KINDS.index(self.kind), self.half_support, self.shape_param)
+        c = _C_STRUCTS.get(self)
+        if c is None:
+            c = _C_STRUCTS[self] = L.kernel_struct(KERNEL_KINDS.index(self.kind), self.half_support,
+                                                   self.shape_param)
+        return c
 
 
 def as_grid_spec(spec) -> GridSpec:
@@ -222,8 +232,11 @@ def context(device=None) -> L.Context:
     _require_cuda()
     dev = _device_index(device)
     ctx = L.Context.get(dev)
-    with torch.cuda.device(dev):
-        ctx.bind_stream(torch.cuda.current_stream(dev).cuda_stream)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    if getattr(ctx, "_bound", None) != stream:     # (rebinding costs a C call per image)
+        with torch.cuda.device(dev):
+            ctx.bind_stream(stream)
+        ctx._bound = stream
     return ctx
 
 
@@ -233,6 +246,8 @@ def _ptr(t: torch.Tensor | None):
 
 def _to_dev(a, dtype, dev) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
+        if a.dtype == dtype and a.device == dev and a.is_contiguous():
+            return a                                  # (already in place: no dispatch)
         return a.to(device=dev, dtype=dtype).contiguous()
     return torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dtype)
 
@@ -247,6 +262,9 @@ def _cols2d(a, n: int):
 def _vis_f32(vis, n: int, dev) -> tuple[torch.Tensor, int]:
     """complex64 (n, n_chan) -> float32 (n, n_chan, 2) interleaved, on device."""
     if isinstance(vis, torch.Tensor):
+        if (vis.dtype == torch.float32 and vis.device == dev and vis.dim() == 3 and vis.shape[0] == n
+                and vis.shape[2] == 2 and vis.is_contiguous()):
+            return vis, vis.shape[1]                  # (already interleaved f32 on the device)
         t = vis.to(dev)
         if t.is_complex():
             t = torch.view_as_real(_cols2d(t.to(torch.complex64), n).contiguous())
@@ -366,6 +384,10 @@ def image_device(u, v, w, vis, weight, spec, kern, image_out: torch.Tensor | Non
     d = L.WsbDiag()
     g, k = spec.c_struct(), kern.c_struct()
     lib = L.lib()
+    if int(precision) == 64:   # (the context's default: no precision round trip)
+        L.check(lib.wsb_image_device(ctx.handle, C.byref(g), C.byref(k), _ptr(u), _ptr(v), _ptr(w),
+                                     _ptr(visf), _ptr(wt), n, n_chan, _ptr(image_out), C.byref(d)))
+        return image_out, diag_dict(d)
     L.check(lib.wsb_ctx_set_precision(ctx.handle, int(precision)))
     try:
         L.check(lib.wsb_image_device(ctx.handle, C.byref(g), C.byref(k), _ptr(u), _ptr(v), _ptr(w),
