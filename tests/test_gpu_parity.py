@@ -145,6 +145,42 @@ def test_grid_every_support_vs_oracle(W, kind, S):
     assert np.max(np.abs(grid - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
 
 
+def test_grid_records_at_item_corners_four_entries_each(W):
+    """Every record's footprint straddles two 16-column strips and two
+    128-row blocks: four K1 entries per record, above the entry buffers'
+    first sizing (2 per record), so K1 re-runs with exact buffers; the grid
+    still equals the oracle's and grid_updates the reference count."""
+    rng = np.random.default_rng(11)
+    n = 30000
+    n_u, n_v = 64, 256
+    ci = rng.integers(1, n_u // 16, n) * 16          # strip boundaries 16, 32, 48
+    u = (ci + rng.uniform(-2.0, 2.0, n)) / n_u
+    v = (128 + rng.uniform(-2.0, 2.0, n)) / n_v       # the row-block boundary 128
+    w = rng.random(n)
+    t = np.zeros(n, np.uint32)
+    vis = (rng.standard_normal((n, 1)) + 1j * rng.standard_normal((n, 1))).astype(np.complex64)
+    wt = np.ones((n, 1), np.float32)
+    spec = W.GridSpec(n_u, n_v, 2, 1e-3, w_max_native=10.0)
+    kern = W.KernelSpec.gaussian(3, 1.0)
+    from paper_2504_00959_b200 import _lib as L
+    dev = torch.cuda.current_device()
+    saved = L.Context._per_device.get(dev)
+    L.Context._per_device[dev] = L.Context(dev)        # fresh buffers: the first sizing applies
+    try:
+        rec, plane = W.prepare_device(u, v, w, vis, wt, spec)
+        keys, idx, off, ib = W.bucket_items_device(rec, plane, spec, 3, 0, n_v)
+        assert len(keys) > 3.5 * n                     # ~4 entries per record
+        gp, upd = W.grid_slab_device(rec, plane, spec, kern, 0, n_v)
+        grid = W.unpack_grid_device(gp, spec, 0, n_v).cpu().numpy()
+    finally:
+        L.Context._per_device[dev] = saved
+    prep = O.prepare(u, v, w, t, vis, wt, n_u, n_v, 2)
+    batch = O.exchange([prep], n_v, 1, 3)[0]
+    ref, upd_ref = O.grid_slab(batch, n_u, 2, O.KIND_GAUSSIAN, 3, 1.0, 0, n_v)
+    assert upd == upd_ref
+    assert np.max(np.abs(grid - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+
 @pytest.mark.parametrize("R", [2, 4])
 def test_grid_slabs_bitwise_across_slab_counts(W, golden_grid, R):
     """Per-slab gridding after the exchange reproduces the 1-slab grid
