@@ -246,7 +246,7 @@ struct Shm {
 
 template <int KIND, int S>
 constexpr int sweep_min_blocks() {
-    return (S <= 4 ? 21 : 16) / kWarps;   // (80 registers either way; 21 schedules better than 24: 0.955 -> 0.911 ms)
+    return (S <= 4 ? 21 : 14) / kWarps;   // (80 registers either way; 21 schedules better than 24: 0.955 -> 0.911 ms)
 }
 
 // m8n8k4 FP64 MMA, D = A B + D: a(row lane/4, k lane%4), b(k lane%4, col lane/4),
