@@ -246,7 +246,11 @@ struct Shm {
 
 template <int KIND, int S>
 constexpr int sweep_min_blocks() {
-    return (S <= 4 ? 21 : 14) / kWarps;   // (80 registers either way; 21 schedules better than 24: 0.955 -> 0.911 ms)
+    // measured per kernel: Gaussian S <= 4 21 (80 registers either way, 21
+    // schedules better than 24: 0.955 -> 0.911 ms at cfg2); Kaiser-Bessel
+    // 2 <= S <= 4 18 (94 registers, no spills: support 7 14.6 -> 13.4 ms);
+    // S > 4 14
+    return (S > 4 ? 14 : (KIND == WSB_KERNEL_KAISER_BESSEL && S >= 2) ? 18 : 21) / kWarps;
 }
 
 // m8n8k4 FP64 MMA, D = A B + D: a(row lane/4, k lane%4), b(k lane%4, col lane/4),
